@@ -1,0 +1,152 @@
+// rq_plan.hpp -- host-side plan object and error plumbing.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "rigidq_b200.h"
+#include "rq_internal.cuh"
+
+namespace rq {
+
+// thread-local error message (rq_last_error)
+void set_error(const std::string &msg);
+const char *last_error();
+
+struct Status {
+  int code = RQ_OK;
+  std::string msg;
+  bool ok() const { return code == RQ_OK; }
+};
+
+#define RQ_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      throw ::rq::Error(RQ_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    }                                                                              \
+  } while (0)
+
+struct Error {
+  int code;
+  std::string msg;
+  Error(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+// owning device buffer
+struct DBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf &) = delete;
+  DBuf &operator=(const DBuf &) = delete;
+  DBuf(DBuf &&o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf &operator=(DBuf &&o) noexcept {
+    reset();
+    p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0;
+    return *this;
+  }
+  ~DBuf() { reset(); }
+  void alloc(size_t b) {
+    reset();
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw Error(RQ_ERR_NOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr; bytes = 0;
+  }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+struct Plan {
+  int device = 0;
+  int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
+  int max_depth = 96;
+  int tile_leaves = 128;           // S
+  int64_t max_blob = 0;            // largest chunk blob (bytes)
+  int max_chunk_nodes = 0, max_chunk_beads = 0, max_chunk_levels = 0, max_chunk_res = 0;
+  std::vector<int64_t> bead_off;   // host copy, m+1
+  int64_t n_case[4] = {0, 0, 0, 0};
+  int64_t rec_doubles = 0;
+  int64_t blob_bytes = 0;
+  int64_t n_chunks = 0, n_tiles = 0, n_top = 0, n_slots = 0, n_topbodies = 0, n_toplevels = 0;
+  int64_t n_small = 0;             // bodies with n == 1
+  int64_t min_n = 0;
+
+  // per body
+  DBuf bead_off_d, node_off_d;     // int64 [m+1]
+  DBuf body_centroid;              // double [3m] (model centroid)
+  DBuf root_box;                   // double [6m]
+  // per bead (tree order)
+  DBuf perm;                       // int32 body-local original index
+  DBuf pos_tree;                   // double [3N]
+  DBuf pos_orig;                   // double [3N] (original order, for Z ops)
+  DBuf body_of;                    // int32 [N] (original/tree order share bodies)
+  // per node (global postorder id)
+  DBuf start, stop, left, right, parent;  // int32 body-local
+  DBuf depth;                      // int16
+  DBuf axis;                       // int8
+  DBuf flags;                      // uint8
+  DBuf height;                     // int32
+  DBuf centroid;                   // double [3NN]
+  DBuf t22;                        // double [6NN] lower triangle
+  DBuf rec_off;                    // int64 [NN]
+  DBuf res_off;                    // int32 [NN] body-relative spectral offsets
+  DBuf rec;                        // double [rec_doubles] compact records (postorder)
+  // apply layout
+  DBuf chunks;                     // ChunkDesc [n_chunks]
+  DBuf tiles;                      // TileDesc [n_tiles]
+  DBuf blob;                       // bytes
+  DBuf top;                        // TopNode [n_top], sorted by (body, height)
+  DBuf topbody;                    // int32 [n_topbodies]: body ids needing the top kernels
+  DBuf topbody_lvl;                // int32 [n_topbodies+1]: level CSR into toplvl
+  DBuf toplvl;                     // int32 [n_toplevels+1]: top index ranges per level
+  DBuf small_bodies;               // int32 [n_small]
+  mutable DBuf scratch;            // double [6 * n_slots * kcap]
+  mutable int64_t scratch_k = 0;
+  DBuf err;                        // int64 [8] device error flags
+  // deterministic per-body reductions (centroid, Zf): fixed segments
+  int64_t n_seg = 0;
+  DBuf seg_body;                   // int32 [n_seg]
+  DBuf seg_begin;                  // int64 [n_seg + 1] bead ranges
+  DBuf body_seg;                   // int64 [m + 1] segment CSR
+  mutable DBuf zpart;              // double [6 * n_seg]
+
+  int64_t device_bytes() const;
+};
+
+void build_plan(Plan &p, const double *pos, const int64_t *offsets, int64_t m, int max_depth,
+                bool host_input, cudaStream_t s);
+void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s);
+void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, const double *origin_d,
+           cudaStream_t s);
+int check_duplicates(const double *pos, const int64_t *offsets, int64_t m, bool host_input,
+                     cudaStream_t s, int64_t *body, int64_t *i, int64_t *j, double *tol);
+void export_tree(const Plan &p, int64_t body, int64_t *perm, int64_t *start, int64_t *stop,
+                 int64_t *left, int64_t *right, int32_t *split_axis, int32_t *depth,
+                 double *centroid, double *box);
+void export_factors(const Plan &p, int64_t body, int32_t *ncase, int64_t *n, int64_t *nx,
+                    int64_t *ny, uint8_t *swapped, double *t22, double *omega,
+                    int64_t *res_offsets, int64_t *total_rows);
+int64_t omega_size(const Plan &p, int64_t body);
+void explicit_q_size(const Plan &p, int64_t body, int64_t *n_blocks, int64_t *n_doubles);
+void explicit_q(const Plan &p, int64_t body, double *root_rows, int64_t *block_node,
+                int64_t *block_col, int64_t *block_rows, double *block_data);
+
+void node_small_lq(const double *a, int k, int64_t batch, double *t, double *om);
+void node_factor_bb(const double *d, int64_t batch, double *t, double *g);
+void node_merge(int cs, const double *om, double a, double b, const double *mx, const double *my, int64_t K,
+                double *mp, double *res);
+void node_split(int cs, const double *om, double a, double b, const double *lp, const double *res, int64_t K,
+                double *lx, double *ly);
+
+}  // namespace rq

@@ -1,0 +1,1465 @@
+// rq_setup.cu -- batched per-body setup on the GPU: tree (tree.py:73-134),
+// factors (factor.py:213-244) and the chunked apply layout.
+//
+// Pipeline (all bodies at once, no per-body host loop):
+//   1. per-body bounding cube (tree.py:78-81)
+//   2. per-bead ghost key: the bead's own midpoint-bisection walk z,y,x
+//      (tree.py:96-114); bit d = (pos > mid_d).  The reference tree is the
+//      binary radix tree of these keys (empty halves pruned = levels where a
+//      node's keys agree).
+//   3. radix sort of (body, key) -> perm (tree.py:368)
+//   4. Karras radix-tree topology; reference postorder ids from
+//        id(X) = start + C(start) + 2L - 2,  C(s) = #internal nodes with stop <= s
+//   5. bottom-up factor pass (last-arriver): centroids (tree.py:126), the
+//      three node cases (factor.py:224-243), compact LQ records
+//   6. apply layout: tiles (maximal subtrees with <= S beads), chunks (greedy
+//      byte-budget packing of consecutive tiles), level-major SoA blobs, and
+//      the top tree above the tiles.
+// Compiled with --fmad=false (see rq_lq.cuh).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rq_lq.cuh"
+#include "rq_plan.hpp"
+
+namespace rq {
+namespace {
+
+constexpr int NT = 256;
+__constant__ int c_axis_cycle[3] = {2, 1, 0};  // tree.py:27
+
+inline int nblk(int64_t n, int t = NT) { return (int)std::max<int64_t>(1, (n + t - 1) / t); }
+
+__device__ __forceinline__ int find_body(const int64_t *off, int64_t m, int64_t i) {
+  int64_t lo = 0, hi = m;  // off[lo] <= i < off[hi]
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= i) lo = mid; else hi = mid;
+  }
+  return (int)lo;
+}
+
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord_key(unsigned long long u) {
+  return __longlong_as_double((long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u));
+}
+
+struct Key128 {
+  uint64_t hi, lo;
+};
+struct KeyDec {
+  __host__ __device__ ::cuda::std::tuple<uint64_t &, uint64_t &> operator()(Key128 &k) const {
+    return {k.hi, k.lo};
+  }
+};
+
+// ---- 1. bodies, bounding cube ------------------------------------------------
+
+__global__ void k_body_of(const int64_t *off, int64_t m, int64_t N, int32_t *body_of) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < N) body_of[i] = find_body(off, m, i);
+}
+
+__global__ void k_bbox(const double *pos, const int32_t *body_of, int64_t N,
+                       unsigned long long *bmin, unsigned long long *bmax, long long *err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  bool valid = i < N;
+  int j = valid ? body_of[i] : -1;
+  unsigned long long kmin[3], kmax[3];
+  for (int a = 0; a < 3; a++) {
+    double x = valid ? pos[i * 3 + a] : 0.0;
+    if (valid && !isfinite(x)) atomicExch((unsigned long long *)&err[1], 1ull);
+    kmin[a] = valid ? ord_key(x) : ~0ull;
+    kmax[a] = valid ? ord_key(x) : 0ull;
+  }
+  unsigned full = 0xffffffffu;
+  int j0 = __shfl_sync(full, j, 0);
+  bool uniform = __all_sync(full, j == j0) && j0 >= 0;
+  if (uniform) {
+    for (int a = 0; a < 3; a++)
+      for (int o = 16; o; o >>= 1) {
+        unsigned long long vmin = __shfl_xor_sync(full, kmin[a], o);
+        unsigned long long vmax = __shfl_xor_sync(full, kmax[a], o);
+        kmin[a] = vmin < kmin[a] ? vmin : kmin[a];
+        kmax[a] = vmax > kmax[a] ? vmax : kmax[a];
+      }
+    if ((threadIdx.x & 31) == 0)
+      for (int a = 0; a < 3; a++) {
+        atomicMin(&bmin[j0 * 3 + a], kmin[a]);
+        atomicMax(&bmax[j0 * 3 + a], kmax[a]);
+      }
+  } else if (valid) {
+    for (int a = 0; a < 3; a++) {
+      atomicMin(&bmin[j * 3 + a], kmin[a]);
+      atomicMax(&bmax[j * 3 + a], kmax[a]);
+    }
+  }
+}
+
+// tree.py:78-81: center = (lo+hi)/2; half = max(hi-lo) * (1+1e-9) / 2
+__global__ void k_root_box(const unsigned long long *bmin, const unsigned long long *bmax,
+                           int64_t m, double *box) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; a++) { lo[a] = unord_key(bmin[j * 3 + a]); hi[a] = unord_key(bmax[j * 3 + a]); }
+  double ext = hi[0] - lo[0];
+  for (int a = 1; a < 3; a++) { double e = hi[a] - lo[a]; if (e > ext) ext = e; }
+  double half = ext * (1.0 + 1e-9) / 2.0;
+  for (int a = 0; a < 3; a++) {
+    double c = (lo[a] + hi[a]) / 2.0;
+    box[j * 6 + a] = c - half;
+    box[j * 6 + 3 + a] = c + half;
+  }
+}
+
+// ---- 2. ghost keys -------------------------------------------------------------
+
+__global__ void k_keys(const double *pos, const int32_t *body_of, const double *box, int64_t N,
+                       int max_depth, int body_shift, Key128 *keys, int32_t *vals) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int j = body_of[i];
+  double p[3], cl[3], ch[3];
+  for (int a = 0; a < 3; a++) {
+    p[a] = pos[i * 3 + a];
+    cl[a] = box[j * 6 + a];
+    ch[a] = box[j * 6 + 3 + a];
+  }
+  uint64_t hi = 0, lo = 0;
+  for (int d = 0; d < max_depth; d++) {
+    int a = c_axis_cycle[d % 3];
+    double mid = 0.5 * (cl[a] + ch[a]);
+    unsigned bit = p[a] > mid;  // ties go to the lower half (tree.py:106)
+    if (bit) cl[a] = mid; else ch[a] = mid;
+    hi = (hi << 1) | (lo >> 63);
+    lo = (lo << 1) | bit;
+  }
+  // body id above the key bits (bits [max_depth, max_depth + body_bits))
+  if (body_shift >= 64) hi |= (uint64_t)j << (body_shift - 64);
+  else {
+    hi |= body_shift > 0 ? ((uint64_t)j >> (64 - body_shift)) : 0;
+    lo |= (uint64_t)j << body_shift;
+  }
+  keys[i] = {hi, lo};
+  vals[i] = (int32_t)i;
+}
+
+__device__ __forceinline__ int prefix_len(const Key128 &a, const Key128 &b, int max_depth) {
+  uint64_t xh = a.hi ^ b.hi, xl = a.lo ^ b.lo;
+  int clz = xh ? __clzll((long long)xh) : 64 + (xl ? __clzll((long long)xl) : 64);
+  return clz - (128 - max_depth);
+}
+
+// ---- 3. after the sort: perm, tree-order positions, gaps -----------------------
+
+__global__ void k_post_sort(const Key128 *keys, const int32_t *vals, const double *pos,
+                            const int64_t *bead_off, const int32_t *body_of, int64_t N,
+                            int max_depth, int32_t *perm, double *pos_tree, int16_t *gap,
+                            long long *err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int j = body_of[i];
+  int64_t src = vals[i];
+  perm[i] = (int32_t)(src - bead_off[j]);
+  for (int a = 0; a < 3; a++) pos_tree[i * 3 + a] = pos[src * 3 + a];
+  int16_t g = -1;
+  if (i + 1 < bead_off[j + 1]) {
+    Key128 a = keys[i], b = keys[i + 1];
+    if (a.hi == b.hi && a.lo == b.lo) {
+      // tree.py:99-103: split depth exceeded without separating beads
+      atomicMin((unsigned long long *)&err[0], (unsigned long long)j);
+      g = 0;
+    } else {
+      g = (int16_t)prefix_len(a, b, max_depth);
+    }
+  }
+  gap[i] = g;
+}
+
+// ---- 4. Karras radix tree ------------------------------------------------------
+
+struct KarrasCtx {
+  const Key128 *k;  // body base
+  int n, max_depth;
+  __device__ int delta(int i, int j) const {
+    if (j < 0 || j >= n) return -1;
+    return prefix_len(k[i], k[j], max_depth);
+  }
+};
+
+__global__ void k_karras(const Key128 *keys, const int64_t *bead_off, int64_t m, int max_depth,
+                         int64_t n_internal, int32_t *kfirst, int32_t *klast, int32_t *kgamma,
+                         int32_t *cnt_stop) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_internal) return;
+  // body: largest j with bead_off[j] - j <= q
+  int64_t lo = 0, hi = m;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (bead_off[mid] - mid <= q) lo = mid; else hi = mid;
+  }
+  int j = (int)lo;
+  int64_t base = bead_off[j];
+  int n = (int)(bead_off[j + 1] - base);
+  int i = (int)(q - (base - j));
+  KarrasCtx c{keys + base, n, max_depth};
+  int d = (c.delta(i, i + 1) - c.delta(i, i - 1)) > 0 ? 1 : -1;
+  int dmin = c.delta(i, i - d);
+  int lmax = 2;
+  while (c.delta(i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (c.delta(i, i + (l + t) * d) > dmin) l += t;
+  int jj = i + l * d;
+  int dnode = c.delta(i, jj);
+  int s = 0;
+  for (int div = 2;; div <<= 1) {
+    int t = (l + div - 1) / div;
+    if (c.delta(i, i + (s + t) * d) > dnode) s += t;
+    if (t <= 1) break;
+  }
+  int gamma = i + s * d + (d < 0 ? -1 : 0);
+  int first = min(i, jj), last = max(i, jj);
+  kfirst[q] = first;
+  klast[q] = last;
+  kgamma[q] = gamma;
+  atomicAdd(&cnt_stop[base + last], 1);  // internal node with stop = last + 1
+}
+
+struct TopoCtx {
+  const int64_t *bead_off;
+  const int32_t *cscan;  // inclusive scan of cnt_stop over all beads
+  const int16_t *gap;
+  __device__ int C(int j, int64_t base, int s) const {  // #internal nodes with stop <= s
+    return s == 0 ? 0 : (int)(cscan[base + s - 1] - (base - j));
+  }
+  __device__ int g(int64_t base, int n, int k) const { return (k < 0 || k >= n - 1) ? -1 : gap[base + k]; }
+};
+
+__device__ __forceinline__ int16_t node_depth(const TopoCtx &t, int64_t base, int n, int s, int e) {
+  int gl = t.g(base, n, s - 1), gr = t.g(base, n, e - 1);
+  if (gl < 0 && gr < 0) return 0;  // root
+  bool right = s > 0 && gl > gr;
+  return (int16_t)((right ? gl : gr) + 1);
+}
+
+__global__ void k_topo_internal(TopoCtx t, const int64_t *node_off, int64_t m, const int32_t *kfirst,
+                                const int32_t *klast, const int32_t *kgamma, int64_t n_internal,
+                                int32_t *start, int32_t *stop, int32_t *left, int32_t *right,
+                                int32_t *parent, int16_t *depth, int8_t *axis, uint8_t *flags) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_internal) return;
+  int64_t lo = 0, hi = m;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (t.bead_off[mid] - mid <= q) lo = mid; else hi = mid;
+  }
+  int j = (int)lo;
+  int64_t base = t.bead_off[j];
+  int n = (int)(t.bead_off[j + 1] - base);
+  int first = kfirst[q], last = klast[q], gm = kgamma[q];
+  int s = first, e = last + 1, L = e - s;
+  int id = s + t.C(j, base, s) + 2 * L - 2;
+  int Ll = gm - first + 1, Lr = last - gm;
+  int idl = first + t.C(j, base, first) + 2 * Ll - 2;
+  int idr = (gm + 1) + t.C(j, base, gm + 1) + 2 * Lr - 2;
+  int64_t nb = node_off[j];
+  start[nb + id] = s;
+  stop[nb + id] = e;
+  left[nb + id] = idl;
+  right[nb + id] = idr;
+  parent[nb + idl] = id;
+  parent[nb + idr] = id;
+  int lvl = t.g(base, n, gm);
+  axis[nb + id] = (int8_t)c_axis_cycle[lvl % 3];
+  depth[nb + id] = node_depth(t, base, n, s, e);
+  int c = (Ll == 1 && Lr == 1) ? BEAD_BEAD : ((Ll == 1 || Lr == 1) ? RIGID_BEAD : GENERAL);
+  flags[nb + id] = (uint8_t)(c | ((c == RIGID_BEAD && Ll == 1) ? 4 : 0));
+}
+
+__global__ void k_topo_leaf(TopoCtx t, const int64_t *node_off, const int32_t *body_of, int64_t N,
+                            const double *pos_tree, int32_t *start, int32_t *stop, int32_t *left,
+                            int32_t *right, int16_t *depth, int8_t *axis, uint8_t *flags,
+                            double *centroid, int32_t *leaf_id) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int j = body_of[i];
+  int64_t base = t.bead_off[j];
+  int n = (int)(t.bead_off[j + 1] - base);
+  int li = (int)(i - base);
+  int id = li + t.C(j, base, li);
+  int64_t g = node_off[j] + id;
+  start[g] = li;
+  stop[g] = li + 1;
+  left[g] = -1;
+  right[g] = -1;
+  axis[g] = -1;
+  flags[g] = LEAF;
+  depth[g] = n == 1 ? 0 : node_depth(t, base, n, li, li + 1);
+  for (int a = 0; a < 3; a++) centroid[g * 3 + a] = pos_tree[i * 3 + a];
+  leaf_id[i] = id;
+}
+
+// node -> body (binary search on node_off)
+__global__ void k_node_sizes(const int64_t *node_off, int64_t m, int64_t NN, const uint8_t *flags,
+                             int64_t *recsz, int32_t *rr, int32_t *node_body) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN) return;
+  int c = flag_case(flags[g]);
+  recsz[g] = rec_size(c);
+  rr[g] = res_rows(c);
+  node_body[g] = find_body(node_off, m, g);
+}
+
+__global__ void k_res_off(const int64_t *node_off, const int64_t *bead_off, const int32_t *node_body,
+                          const int32_t *rr_scan, int64_t NN, int32_t *res_off) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN) return;
+  int j = node_body[g];
+  int64_t n = bead_off[j + 1] - bead_off[j];
+  res_off[g] = rr_scan[g] - rr_scan[node_off[j]] + (n >= 2 ? 6 : 3);  // factor.py:198-204
+}
+
+// ---- 5. bottom-up factor pass (last arriver) --------------------------------------
+
+struct FactorCtx {
+  const int64_t *bead_off, *node_off;
+  const int32_t *body_of, *leaf_id, *start, *stop, *left, *right, *parent;
+  const double *pos_tree;
+  const int64_t *rec_off;
+  int32_t *counter, *height;
+  uint8_t *flags;
+  double *centroid, *t22, *rec;
+};
+
+__device__ inline void load_child(const FactorCtx &c, int64_t nb, int64_t base, int id, double cen[3],
+                                  double t[9], int &L, int &h) {
+  int64_t g = nb + id;
+  L = c.stop[g] - c.start[g];
+  if (L == 1) {
+    for (int a = 0; a < 3; a++) cen[a] = c.pos_tree[(base + c.start[g]) * 3 + a];
+    for (int a = 0; a < 9; a++) t[a] = 0.0;
+    h = 0;
+    return;
+  }
+  for (int a = 0; a < 3; a++) cen[a] = __ldcg(&c.centroid[g * 3 + a]);
+  double p[6];
+  for (int a = 0; a < 6; a++) p[a] = __ldcg(&c.t22[g * 6 + a]);
+  t[0] = p[0]; t[1] = 0.0;  t[2] = 0.0;
+  t[3] = p[1]; t[4] = p[2]; t[5] = 0.0;
+  t[6] = p[3]; t[7] = p[4]; t[8] = p[5];
+  h = __ldcg(&c.height[g]);
+}
+
+__global__ void k_factor(FactorCtx c, int64_t N) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int j = c.body_of[i];
+  int64_t base = c.bead_off[j], nb = c.node_off[j];
+  int x = c.parent[nb + c.leaf_id[i]];
+  while (x >= 0) {
+    int64_t g = nb + x;
+    __threadfence();
+    if (atomicAdd(&c.counter[g], 1) == 0) return;
+    __threadfence();
+    int l = c.left[g], r = c.right[g];
+    double cl[3], cr[3], tl[9], tr[9];
+    int nl, nr, hl, hr;
+    load_child(c, nb, base, l, cl, tl, nl, hl);
+    load_child(c, nb, base, r, cr, tr, nr, hr);
+    int n = nl + nr;
+    double cp[3];
+    for (int a = 0; a < 3; a++)  // tree.py:126
+      cp[a] = ((double)nl * cl[a] + (double)nr * cr[a]) / (double)n;
+    double t6[6];
+    unsigned signs = 0;
+    int cs = flag_case(c.flags[g]);
+    double *rec = c.rec + c.rec_off[g];
+    if (cs == BEAD_BEAD) {  // factor.py:224-225
+      double d[3];
+      for (int a = 0; a < 3; a++) d[a] = c.pos_tree[(base + c.start[nb + l]) * 3 + a] - cp[a];
+      double gm[9];
+      factor_bead_bead(d, t6, gm);
+      for (int a = 0; a < 9; a++) rec[a] = gm[a];
+    } else if (cs == RIGID_BEAD) {  // factor.py:226-236, 171-178
+      bool sw = nl == 1;
+      const double *cg = sw ? cr : cl;
+      const double *tg = sw ? tr : tl;
+      int nx = sw ? nr : nl;
+      double dr[3], R[9];
+      for (int a = 0; a < 3; a++) dr[a] = cg[a] - cp[a];
+      skew3(dr, R);
+      double sc = sqrt((double)((int64_t)nx * n));
+      double cpl[18];
+      for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) {
+          cpl[a * 6 + b] = tg[a * 3 + b];
+          cpl[a * 6 + 3 + b] = sc * R[a * 3 + b];
+        }
+      double hh[HH<6>::SIZE];
+      lq_factor<6>(cpl, t6, hh, signs);
+      for (int a = 0; a < HH<6>::SIZE; a++) rec[a] = hh[a];
+    } else {  // factor.py:237-243, 181-188
+      double dr[3], R[9];
+      for (int a = 0; a < 3; a++) dr[a] = cl[a] - cp[a];
+      skew3(dr, R);
+      double sc = sqrt((double)((int64_t)nl * n) / (double)nr);
+      double cpl[27];
+      for (int a = 0; a < 3; a++)
+        for (int b = 0; b < 3; b++) {
+          cpl[a * 9 + b] = tl[a * 3 + b];
+          cpl[a * 9 + 3 + b] = tr[a * 3 + b];
+          cpl[a * 9 + 6 + b] = sc * R[a * 3 + b];
+        }
+      double hh[HH<9>::SIZE];
+      lq_factor<9>(cpl, t6, hh, signs);
+      for (int a = 0; a < HH<9>::SIZE; a++) rec[a] = hh[a];
+    }
+    for (int a = 0; a < 3; a++) c.centroid[g * 3 + a] = cp[a];
+    for (int a = 0; a < 6; a++) c.t22[g * 6 + a] = t6[a];
+    c.height[g] = max(hl, hr) + 1;
+    c.flags[g] = (uint8_t)((c.flags[g] & 7u) | (signs << 3));
+    __threadfence();
+    x = c.parent[g];
+  }
+}
+
+// ---- 6. apply layout ------------------------------------------------------------
+
+struct LayoutCtx {
+  int S;
+  const int64_t *bead_off, *node_off;
+  const int32_t *node_body, *start, *stop, *parent, *height, *res_off;
+  const int64_t *rec_off;
+  const uint8_t *flags;
+};
+
+__device__ __forceinline__ int nodeL(const LayoutCtx &c, int64_t g) { return c.stop[g] - c.start[g]; }
+
+// tile roots / top nodes / exchange slots
+__global__ void k_classify(LayoutCtx c, int64_t NN, int32_t *is_tile, int32_t *is_slot, int32_t *is_top) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN) return;
+  int j = c.node_body[g];
+  int64_t nb = c.node_off[j];
+  int L = nodeL(c, g);
+  int p = c.parent[g];
+  bool top = L > c.S;
+  bool tile = !top && (p < 0 || nodeL(c, nb + p) > c.S);
+  is_top[g] = top;
+  is_tile[g] = tile;
+  is_slot[g] = top || (tile && L >= 2);
+}
+
+struct TileTmp {
+  int64_t root;      // global node id
+  int32_t body, L, start, height;
+  int64_t rec_doubles;
+  int32_t res_q;     // body-relative Q~ offset of the first residue
+  int32_t big;       // L >= 2
+};
+
+__global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const int32_t *tile_scan,
+                        TileTmp *tiles, int32_t *marker) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN || !is_tile[g]) return;
+  int t = tile_scan[g];  // exclusive
+  int L = nodeL(c, g);
+  int64_t first = g - 2 * L + 2;
+  TileTmp T;
+  T.root = g;
+  T.body = c.node_body[g];
+  T.L = L;
+  T.start = c.start[g];
+  T.height = c.height[g];
+  T.rec_doubles = c.rec_off[g] + rec_size(flag_case(c.flags[g])) - c.rec_off[first];
+  T.res_q = c.res_off[first] - 6;
+  T.big = L >= 2;
+  tiles[t] = T;
+  marker[first] = t;
+}
+
+struct ChunkLimits {
+  int64_t max_bytes;
+  int max_nodes, max_beads, max_res;
+};
+
+__host__ __device__ inline int64_t blob_bytes_of(int H, int nodes, int beads, int64_t rec) {
+  int64_t perm = ((int64_t)beads * 4 + 15) / 16 * 16;
+  int64_t b = (int64_t)H * 32 + (int64_t)nodes * 16 + perm + rec * 8;
+  return (b + 15) / 16 * 16;
+}
+
+// Greedy packing of a body's consecutive tiles into chunks (one thread per body).
+// pass 0: count chunks per body; pass 1: write descriptors.
+__global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, const int64_t *bead_off,
+                       int64_t m, ChunkLimits lim, int pass, const int64_t *chunk_base,
+                       const int32_t *big_scan, int64_t *n_chunks_body, ChunkDesc *chunks,
+                       int64_t *chunk_of_tile, int32_t *res_local_of_tile) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  int64_t tb = body_tile_begin[j], te = body_tile_begin[j + 1];
+  int64_t nch = 0;
+  bool open = false;
+  int bead0 = 0, nodes = 0, H = 0, res = 0, ntiles = 0;
+  int64_t rec = 0, tile0 = 0;
+  auto flush = [&]() {
+    if (!open) return;
+    if (pass == 1) {
+      ChunkDesc &d = chunks[chunk_base[j] + nch];
+      d.blob_off = 0;
+      d.n_nodes = nodes;
+      d.n_levels = H;
+      d.n_tiles = ntiles;
+      d.body = (int32_t)j;
+      d.bead_begin = bead_off[j] + bead0;
+      d.tile_begin = big_scan[tile0];
+      d.n_res = res;
+      d.off_meta = H * 32;
+      d.off_perm = d.off_meta + nodes * 16;
+      // n_beads, off_rec and blob_bytes set by the caller below
+    }
+    nch++;
+    open = false;
+  };
+  int last_stop = 0;
+  for (int64_t t = tb; t < te; t++) {
+    const TileTmp &T = tiles[t];
+    if (!T.big) continue;
+    int Tn = T.L - 1, Tres = 3 * T.L - 6;
+    if (open) {
+      int beads2 = T.start + T.L - bead0;
+      int nodes2 = nodes + Tn, H2 = max(H, T.height), res2 = res + Tres;
+      int64_t rec2 = rec + T.rec_doubles;
+      if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res ||
+          blob_bytes_of(H2, nodes2, beads2, rec2) > lim.max_bytes) {
+        if (pass == 1) {
+          ChunkDesc &d = chunks[chunk_base[j] + nch];
+          d.n_beads = last_stop - bead0;
+          int64_t pb = ((int64_t)d.n_beads * 4 + 15) / 16 * 16;
+          d.off_rec = (int32_t)(H * 32 + nodes * 16 + pb);
+          d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec);
+        }
+        flush();
+      }
+    }
+    if (!open) {
+      open = true;
+      bead0 = T.start; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; tile0 = t;
+    }
+    if (pass == 1) {
+      chunk_of_tile[t] = chunk_base[j] + nch;
+      res_local_of_tile[t] = res;
+    }
+    nodes += Tn;
+    H = max(H, T.height);
+    res += Tres;
+    rec += T.rec_doubles;
+    ntiles++;
+    last_stop = T.start + T.L;
+  }
+  if (open && pass == 1) {
+    ChunkDesc &d = chunks[chunk_base[j] + nch];
+    d.n_beads = last_stop - bead0;
+    int64_t pb = ((int64_t)d.n_beads * 4 + 15) / 16 * 16;
+    d.off_rec = (int32_t)(H * 32 + nodes * 16 + pb);
+    d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec);
+  }
+  flush();
+  if (pass == 0) n_chunks_body[j] = nch;
+}
+
+__global__ void k_chunk_sizes(const ChunkDesc *chunks, int64_t nc, int64_t *bytes, int64_t *nodes,
+                              int64_t *levels) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  bytes[c] = chunks[c].blob_bytes;
+  nodes[c] = chunks[c].n_nodes;
+  levels[c] = chunks[c].n_levels;
+}
+
+__global__ void k_chunk_offsets(ChunkDesc *chunks, int64_t nc, const int64_t *bytes_scan) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < nc) chunks[c].blob_off = bytes_scan[c];
+}
+
+// key for the level-major node order inside chunks
+__global__ void k_node_keys(LayoutCtx c, int64_t NN, const int32_t *is_top, const int32_t *tile_of,
+                            const int64_t *chunk_of_tile, uint64_t *keys, int32_t *vals) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN) return;
+  int cs = flag_case(c.flags[g]);
+  uint64_t key = ~0ull;
+  if (cs != LEAF && !is_top[g]) {
+    int64_t ch = chunk_of_tile[tile_of[g]];
+    int rank = cs == GENERAL ? 0 : (cs == RIGID_BEAD ? 1 : 2);
+    key = ((uint64_t)ch << 24) | ((uint64_t)c.height[g] << 2) | (uint64_t)rank;
+  }
+  keys[g] = key;
+  vals[g] = (int32_t)g;
+}
+
+__global__ void k_slots(const uint64_t *keys, const int32_t *vals, int64_t n_part,
+                        const int64_t *chunk_node_scan, int32_t *slot_of, const int64_t *lvl_base,
+                        LevelDesc *lvl, const uint8_t *flags) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n_part) return;
+  uint64_t key = keys[p];
+  int64_t ch = (int64_t)(key >> 24);
+  int h = (int)((key >> 2) & 0x3fffff);
+  int g = vals[p];
+  slot_of[g] = (int32_t)(p - chunk_node_scan[ch]);
+  int cs = flag_case(flags[g]);
+  LevelDesc *L = &lvl[lvl_base[ch] + h - 1];
+  atomicAdd(cs == GENERAL ? &L->nG : (cs == RIGID_BEAD ? &L->nR : &L->nB), 1);
+}
+
+__global__ void k_levels_finalize(const ChunkDesc *chunks, int64_t nc, const int64_t *lvl_base,
+                                  LevelDesc *lvl, uint8_t *blob) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const ChunkDesc &d = chunks[c];
+  int slot = 0, recd = 0;
+  LevelDesc *dst = reinterpret_cast<LevelDesc *>(blob + d.blob_off);
+  for (int h = 0; h < d.n_levels; h++) {
+    LevelDesc &L = lvl[lvl_base[c] + h];
+    L.slot_begin = slot;
+    L.recG = recd; recd += 24 * L.nG;
+    L.recR = recd; recd += 15 * L.nR;
+    L.recB = recd; recd += 9 * L.nB;
+    L.pad = 0;
+    slot += L.nG + L.nR + L.nB;
+    dst[h] = L;
+  }
+}
+
+struct WriteCtx {
+  LayoutCtx c;
+  const uint64_t *keys;
+  const int32_t *vals;
+  const int32_t *slot_of, *tile_of, *left, *right;
+  const TileTmp *tiles;
+  const int32_t *res_local_of_tile;
+  const ChunkDesc *chunks;
+  const int64_t *lvl_base;
+  const LevelDesc *lvl;
+  const double *rec;
+  uint8_t *blob;
+};
+
+__global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n_part) return;
+  uint64_t key = w.keys[p];
+  int64_t ch = (int64_t)(key >> 24);
+  int h = (int)((key >> 2) & 0x3fffff);
+  int64_t g = w.vals[p];
+  const ChunkDesc &d = w.chunks[ch];
+  const LevelDesc &L = w.lvl[w.lvl_base[ch] + h - 1];
+  int slot = w.slot_of[g];
+  unsigned f = w.c.flags[g];
+  int cs = flag_case(f);
+  int j = d.body;
+  int64_t nb = w.c.node_off[j];
+  int local0 = (int)(d.bead_begin - w.c.bead_off[j]);  // body-local bead index of chunk bead 0
+  int l = w.left[g], r = w.right[g];
+  int xi = l, yi = r;
+  if (flag_swapped(f)) { xi = r; yi = l; }
+  auto enc = [&](int id) -> uint16_t {
+    int64_t cg = nb + id;
+    if (w.c.stop[cg] - w.c.start[cg] == 1) return (uint16_t)(SRC_BEAD | (w.c.start[cg] - local0));
+    return (uint16_t)w.slot_of[cg];
+  };
+  NodeMeta md;
+  md.x = enc(xi);
+  md.y = enc(yi);
+  const TileTmp &T = w.tiles[w.tile_of[g]];
+  int tile_idx = w.tile_of[g];
+  md.res = (uint16_t)(w.res_local_of_tile[tile_idx] + (w.c.res_off[g] - 6 - T.res_q));
+  md.flags = (uint16_t)f;
+  md.nx = (uint16_t)(w.c.stop[nb + xi] - w.c.start[nb + xi]);
+  md.ny = (uint16_t)(w.c.stop[nb + yi] - w.c.start[nb + yi]);
+  md.spare = 0;
+  uint8_t *base = w.blob + d.blob_off;
+  reinterpret_cast<NodeMeta *>(base + d.off_meta)[slot] = md;
+  double *R = reinterpret_cast<double *>(base + d.off_rec);
+  int q = slot - L.slot_begin;
+  const double *src = w.rec + w.c.rec_off[g];
+  if (cs == GENERAL) {
+    for (int e = 0; e < 24; e++) R[L.recG + e * L.nG + q] = src[e];
+  } else if (cs == RIGID_BEAD) {
+    q -= L.nG;
+    for (int e = 0; e < 15; e++) R[L.recR + e * L.nR + q] = src[e];
+  } else {
+    q -= L.nG + L.nR;
+    for (int e = 0; e < 9; e++) R[L.recB + e * L.nB + q] = src[e];
+  }
+}
+
+// perm section of each blob; beads of singleton tiles are marked foreign
+__global__ void k_write_perm(const ChunkDesc *chunks, int64_t nc, const int32_t *perm,
+                             const int32_t *leaf_id, const int64_t *node_off, const int32_t *parent,
+                             const int32_t *start, const int32_t *stop, int S, uint8_t *blob) {
+  int64_t c = blockIdx.x;
+  if (c >= nc) return;
+  const ChunkDesc &d = chunks[c];
+  int64_t nb = node_off[d.body];
+  uint32_t *P = reinterpret_cast<uint32_t *>(blob + d.blob_off + d.off_perm);
+  for (int i = threadIdx.x; i < d.n_beads; i += blockDim.x) {
+    int64_t gb = d.bead_begin + i;
+    int lf = leaf_id[gb];
+    int p = parent[nb + lf];
+    bool foreign = p >= 0 && (stop[nb + p] - start[nb + p]) > S;
+    P[i] = (uint32_t)perm[gb] | (foreign ? PERM_FOREIGN : 0u);
+  }
+}
+
+__global__ void k_tile_desc(const TileTmp *tiles, int64_t n_tiles_all, const int32_t *big_scan,
+                            const int32_t *slot_of, const int32_t *slot_scan,
+                            const int32_t *res_local_of_tile, const int32_t *parent, TileDesc *out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_tiles_all) return;
+  const TileTmp &T = tiles[t];
+  if (!T.big) return;
+  TileDesc d;
+  d.root_slot = slot_of[T.root];
+  d.scratch = parent[T.root] < 0 ? -1 : slot_scan[T.root];
+  d.res_q = T.res_q;
+  d.res_count = 3 * T.L - 6;
+  d.res_local = res_local_of_tile[t];
+  d.pad = 0;
+  out[big_scan[t]] = d;
+}
+
+__global__ void k_top_fill(LayoutCtx c, int64_t NN, const int32_t *is_top, const int32_t *top_scan,
+                           const int32_t *slot_scan, const int32_t *left, const int32_t *right,
+                           TopNode *top, uint64_t *keys, int32_t *vals) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN || !is_top[g]) return;
+  int t = top_scan[g];
+  int j = c.node_body[g];
+  int64_t nb = c.node_off[j];
+  unsigned f = c.flags[g];
+  int l = left[g], r = right[g];
+  int xi = l, yi = r;
+  if (flag_swapped(f)) { xi = r; yi = l; }
+  auto ref = [&](int id) -> int32_t {
+    int64_t cg = nb + id;
+    int L = c.stop[cg] - c.start[cg];
+    if (L == 1) return ~(int32_t)(c.bead_off[j] + c.start[cg]);
+    return slot_scan[cg];
+  };
+  TopNode T;
+  T.x = ref(xi);
+  T.y = ref(yi);
+  T.self_slot = slot_scan[g];
+  int cs = flag_case(f);
+  T.res_q = res_rows(cs) ? c.res_off[g] - 6 : -1;
+  T.nx = c.stop[nb + xi] - c.start[nb + xi];
+  T.ny = c.stop[nb + yi] - c.start[nb + yi];
+  T.body = j;
+  T.flags = (uint16_t)f;
+  T.is_root = c.parent[g] < 0;
+  T.rec_off = c.rec_off[g];
+  top[t] = T;
+  keys[t] = ((uint64_t)j << 32) | (uint64_t)c.height[g];
+  vals[t] = t;
+}
+
+__global__ void k_top_gather(const TopNode *src, const int32_t *order, const uint64_t *keys_sorted,
+                             int64_t n, TopNode *dst, int32_t *lvl_start_flag) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  dst[p] = src[order[p]];
+  lvl_start_flag[p] = (p == 0 || keys_sorted[p] != keys_sorted[p - 1]) ? 1 : 0;
+}
+
+__global__ void k_top_levels(const uint64_t *keys_sorted, const int32_t *flag, const int32_t *lvl_scan,
+                             int64_t n, int32_t *toplvl, const int32_t *topbody_idx,
+                             int32_t *topbody_lvl) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n || !flag[p]) return;
+  int lv = lvl_scan[p];
+  toplvl[lv] = (int32_t)p;
+  int j = (int)(keys_sorted[p] >> 32);
+  if (p == 0 || (keys_sorted[p - 1] >> 32) != (uint64_t)j) topbody_lvl[topbody_idx[j]] = lv;
+}
+
+// ---- helpers ------------------------------------------------------------------------
+
+template <class T>
+void d2h(T *dst, const void *src, size_t count, cudaStream_t s) {
+  RQ_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  RQ_CUDA(cudaStreamSynchronize(s));
+}
+
+template <class T>
+T d2h1(const void *src, cudaStream_t s) {
+  T v;
+  d2h(&v, src, 1, s);
+  return v;
+}
+
+template <class In, class Out>
+void exclusive_scan(const In *in, Out *out, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s));
+  DBuf tmp;
+  tmp.alloc(tb);
+  RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, s));
+}
+
+template <class In, class Out>
+void inclusive_scan(const In *in, Out *out, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  RQ_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out, n, s));
+  DBuf tmp;
+  tmp.alloc(tb);
+  RQ_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, in, out, n, s));
+}
+
+struct MaxOp {
+  __device__ int32_t operator()(int32_t a, int32_t b) const { return a > b ? a : b; }
+};
+
+
+// ---- duplicate-bead check (model.py:65-78) ----------------------------------------
+// Hash grid with cell h = 64 * tol: a pair within tol lies in cells that the
+// probe box [p - tol, p + tol] touches (<= 2 per axis, usually 1).
+
+struct DupCtx {
+  const double *pos;
+  const int32_t *body_of;
+  const int64_t *bead_off;
+  const unsigned long long *bmin, *bmax;
+  int32_t *table;
+  uint64_t mask;
+  unsigned long long *hit;  // per body: (i << 32) | j, min
+  long long *err;
+};
+
+__device__ __forceinline__ void dup_params(const DupCtx &c, int j, double &tol, double lo[3]) {
+  double d2 = 0.0;
+  for (int a = 0; a < 3; a++) {
+    lo[a] = unord_key(c.bmin[j * 3 + a]);
+    double e = unord_key(c.bmax[j * 3 + a]) - lo[a];
+    d2 += e * e;
+  }
+  tol = 1e-12 * sqrt(d2);
+}
+
+__device__ __forceinline__ uint64_t cell_hash(int j, long long x, long long y, long long z) {
+  uint64_t h = (uint64_t)j * 0x9E3779B97F4A7C15ull;
+  h ^= (uint64_t)x * 0xC2B2AE3D27D4EB4Full; h = (h << 31) | (h >> 33);
+  h ^= (uint64_t)y * 0x165667B19E3779F9ull; h = (h << 29) | (h >> 35);
+  h ^= (uint64_t)z * 0x27D4EB2F165667C5ull;
+  h ^= h >> 33; h *= 0xff51afd7ed558ccdull; h ^= h >> 33;
+  return h;
+}
+
+__device__ __forceinline__ long long cell_of(double x, double lo, double h) { return (long long)floor((x - lo) / h); }
+
+__global__ void k_dup_insert(DupCtx c, int64_t N) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int j = c.body_of[i];
+  int64_t n = c.bead_off[j + 1] - c.bead_off[j];
+  if (n < 2) return;
+  double tol, lo[3];
+  dup_params(c, j, tol, lo);
+  if (tol == 0.0) { atomicMin((unsigned long long *)&c.err[2], (unsigned long long)j); return; }
+  double h = 64.0 * tol;
+  long long q[3];
+  for (int a = 0; a < 3; a++) q[a] = cell_of(c.pos[i * 3 + a], lo[a], h);
+  uint64_t s = cell_hash(j, q[0], q[1], q[2]) & c.mask;
+  while (atomicCAS(&c.table[s], -1, (int32_t)i) != -1) s = (s + 1) & c.mask;
+}
+
+__global__ void k_dup_query(DupCtx c, int64_t N) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int j = c.body_of[i];
+  int64_t base = c.bead_off[j];
+  int64_t n = c.bead_off[j + 1] - base;
+  if (n < 2) return;
+  double tol, lo[3];
+  dup_params(c, j, tol, lo);
+  if (tol == 0.0) return;
+  double h = 64.0 * tol;
+  double p[3];
+  long long qlo[3], qhi[3];
+  for (int a = 0; a < 3; a++) {
+    p[a] = c.pos[i * 3 + a];
+    qlo[a] = cell_of(p[a] - tol, lo[a], h);
+    qhi[a] = cell_of(p[a] + tol, lo[a], h);
+  }
+  for (long long x = qlo[0]; x <= qhi[0]; x++)
+    for (long long y = qlo[1]; y <= qhi[1]; y++)
+      for (long long z = qlo[2]; z <= qhi[2]; z++) {
+        uint64_t s = cell_hash(j, x, y, z) & c.mask;
+        for (;;) {
+          int32_t e = c.table[s];
+          if (e < 0) break;
+          if (e != i && c.body_of[e] == j) {
+            double d2 = 0.0, q[3];
+            bool same = true;
+            for (int a = 0; a < 3; a++) {
+              q[a] = c.pos[(int64_t)e * 3 + a];
+              double dd = q[a] - p[a];
+              d2 += dd * dd;
+            }
+            same = cell_of(q[0], lo[0], h) == x && cell_of(q[1], lo[1], h) == y && cell_of(q[2], lo[2], h) == z;
+            if (same && sqrt(d2) <= tol) {
+              unsigned long long a0 = (unsigned long long)(min((int64_t)e, i) - base);
+              unsigned long long b0 = (unsigned long long)(max((int64_t)e, i) - base);
+              atomicMin(&c.hit[j], (a0 << 32) | b0);
+            }
+          }
+          s = (s + 1) & c.mask;
+        }
+      }
+}
+
+}  // namespace
+
+int64_t Plan::device_bytes() const {
+  const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
+                        &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
+                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart};
+  int64_t s = 0;
+  for (auto b : bufs) s += (int64_t)b->bytes;
+  return s;
+}
+
+void compute_body_centroids(Plan &p, cudaStream_t s);  // rq_z.cu
+
+void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m, int max_depth,
+                bool host_input, cudaStream_t s) {
+  if (m < 1) throw Error(RQ_ERR_VALUE, "need at least one body");
+  if (offsets[0] != 0) throw Error(RQ_ERR_VALUE, "offsets[0] must be 0");
+  for (int64_t j = 0; j < m; j++)
+    if (offsets[j + 1] <= offsets[j])
+      throw Error(RQ_ERR_VALUE, "positions must be (n, 3) with n >= 1 for every body");
+  const int64_t N = offsets[m];
+  if (N >= (int64_t(1) << 30)) throw Error(RQ_ERR_VALUE, "too many beads for one plan (>= 2^30)");
+  int body_bits = 0;
+  while ((int64_t(1) << body_bits) < m) body_bits++;
+  if (max_depth < 1 || max_depth + body_bits > 128)
+    throw Error(RQ_ERR_VALUE, "max_depth must be in [1, 128 - ceil(log2 m)]");
+  if (const char *e = getenv("RQ_TILE_LEAVES")) p.tile_leaves = std::min(1024, std::max(2, atoi(e)));
+  p.m = m;
+  p.N = N;
+  p.NN = 2 * N - m;
+  p.max_depth = max_depth;
+  p.bead_off.assign(offsets, offsets + m + 1);
+  const int64_t NN = p.NN;
+  std::vector<int64_t> node_off(m + 1);
+  p.min_n = N;
+  for (int64_t j = 0; j <= m; j++) node_off[j] = 2 * offsets[j] - j;
+  for (int64_t j = 0; j < m; j++) p.min_n = std::min<int64_t>(p.min_n, offsets[j + 1] - offsets[j]);
+
+  p.bead_off_d.alloc((m + 1) * 8);
+  p.node_off_d.alloc((m + 1) * 8);
+  RQ_CUDA(cudaMemcpyAsync(p.bead_off_d.p, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, s));
+  RQ_CUDA(cudaMemcpyAsync(p.node_off_d.p, node_off.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
+  p.pos_orig.alloc(N * 24);
+  RQ_CUDA(cudaMemcpyAsync(p.pos_orig.p, pos_in, N * 24,
+                          host_input ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  p.err.alloc(8 * 8);
+  {
+    long long init[8] = {0x7fffffffffffffffLL, 0, 0, 0, 0, 0, 0, 0};
+    RQ_CUDA(cudaMemcpyAsync(p.err.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  }
+  const int64_t *boff = p.bead_off_d.as<int64_t>();
+  const int64_t *noff = p.node_off_d.as<int64_t>();
+  long long *err = p.err.as<long long>();
+  const double *pos = p.pos_orig.as<double>();
+
+  // 1. bodies + bounding cube
+  p.body_of.alloc(N * 4);
+  k_body_of<<<nblk(N), NT, 0, s>>>(boff, m, N, p.body_of.as<int32_t>());
+  DBuf bmin, bmax;
+  bmin.alloc(m * 24);
+  bmax.alloc(m * 24);
+  RQ_CUDA(cudaMemsetAsync(bmin.p, 0xff, m * 24, s));
+  RQ_CUDA(cudaMemsetAsync(bmax.p, 0x00, m * 24, s));
+  k_bbox<<<nblk(N), NT, 0, s>>>(pos, p.body_of.as<int32_t>(), N, bmin.as<unsigned long long>(),
+                                 bmax.as<unsigned long long>(), err);
+  p.root_box.alloc(m * 48);
+  k_root_box<<<nblk(m), NT, 0, s>>>(bmin.as<unsigned long long>(), bmax.as<unsigned long long>(), m,
+                                     p.root_box.as<double>());
+  {
+    long long e[2];
+    d2h(e, err, 2, s);
+    if (e[1]) throw Error(RQ_ERR_VALUE, "positions must be finite");
+  }
+  compute_body_centroids(p, s);
+
+  // 2-3. keys + sort
+  {
+    DBuf keys, vals, keys2, vals2;
+    keys.alloc(N * 16);
+    vals.alloc(N * 4);
+    keys2.alloc(N * 16);
+    vals2.alloc(N * 4);
+    k_keys<<<nblk(N), NT, 0, s>>>(pos, p.body_of.as<int32_t>(), p.root_box.as<double>(), N, max_depth,
+                                   max_depth, keys.as<Key128>(), vals.as<int32_t>());
+    int end_bit = max_depth + body_bits;
+    size_t tb = 0;
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<Key128>(), keys2.as<Key128>(),
+                                            vals.as<int32_t>(), vals2.as<int32_t>(), (int)N, KeyDec{},
+                                            0, end_bit, s));
+    DBuf tmp;
+    tmp.alloc(tb);
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<Key128>(), keys2.as<Key128>(),
+                                            vals.as<int32_t>(), vals2.as<int32_t>(), (int)N, KeyDec{},
+                                            0, end_bit, s));
+    tmp.reset();
+    keys.reset();
+    vals.reset();
+    p.perm.alloc(N * 4);
+    p.pos_tree.alloc(N * 24);
+    DBuf gap;
+    gap.alloc(N * 2);
+    k_post_sort<<<nblk(N), NT, 0, s>>>(keys2.as<Key128>(), vals2.as<int32_t>(), pos, boff,
+                                        p.body_of.as<int32_t>(), N, max_depth, p.perm.as<int32_t>(),
+                                        p.pos_tree.as<double>(), gap.as<int16_t>(), err);
+    long long dup = d2h1<long long>(err, s);
+    if (dup != 0x7fffffffffffffffLL)
+      throw Error(RQ_ERR_DUPLICATE, "body " + std::to_string(dup) +
+                                        ": split depth " + std::to_string(max_depth) +
+                                        " exceeded without separating beads (near-coincident input)");
+
+    // 4. topology
+    const int64_t n_internal = N - m;
+    p.start.alloc(NN * 4);
+    p.stop.alloc(NN * 4);
+    p.left.alloc(NN * 4);
+    p.right.alloc(NN * 4);
+    p.parent.alloc(NN * 4);
+    p.depth.alloc(NN * 2);
+    p.axis.alloc(NN);
+    p.flags.alloc(NN);
+    p.centroid.alloc(NN * 24);
+    RQ_CUDA(cudaMemsetAsync(p.parent.p, 0xff, NN * 4, s));
+    DBuf cnt, cscan, leaf_id;
+    cnt.alloc(N * 4);
+    cscan.alloc(N * 4);
+    leaf_id.alloc(N * 4);
+    RQ_CUDA(cudaMemsetAsync(cnt.p, 0, N * 4, s));
+    DBuf kfirst, klast, kgamma;
+    kfirst.alloc(std::max<int64_t>(n_internal, 1) * 4);
+    klast.alloc(std::max<int64_t>(n_internal, 1) * 4);
+    kgamma.alloc(std::max<int64_t>(n_internal, 1) * 4);
+    if (n_internal > 0)
+      k_karras<<<nblk(n_internal), NT, 0, s>>>(keys2.as<Key128>(), boff, m, max_depth, n_internal,
+                                                kfirst.as<int32_t>(), klast.as<int32_t>(),
+                                                kgamma.as<int32_t>(), cnt.as<int32_t>());
+    inclusive_scan(cnt.as<int32_t>(), cscan.as<int32_t>(), N, s);
+    TopoCtx tc{boff, cscan.as<int32_t>(), gap.as<int16_t>()};
+    if (n_internal > 0)
+      k_topo_internal<<<nblk(n_internal), NT, 0, s>>>(
+          tc, noff, m, kfirst.as<int32_t>(), klast.as<int32_t>(), kgamma.as<int32_t>(), n_internal,
+          p.start.as<int32_t>(), p.stop.as<int32_t>(), p.left.as<int32_t>(), p.right.as<int32_t>(),
+          p.parent.as<int32_t>(), p.depth.as<int16_t>(), p.axis.as<int8_t>(), p.flags.as<uint8_t>());
+    k_topo_leaf<<<nblk(N), NT, 0, s>>>(tc, noff, p.body_of.as<int32_t>(), N, p.pos_tree.as<double>(),
+                                        p.start.as<int32_t>(), p.stop.as<int32_t>(), p.left.as<int32_t>(),
+                                        p.right.as<int32_t>(), p.depth.as<int16_t>(), p.axis.as<int8_t>(),
+                                        p.flags.as<uint8_t>(), p.centroid.as<double>(),
+                                        leaf_id.as<int32_t>());
+    keys2.reset();
+    vals2.reset();
+
+    // sizes, residue and record offsets
+    DBuf recsz, rr, rr_scan, node_body;
+    recsz.alloc(NN * 8);
+    rr.alloc(NN * 4);
+    rr_scan.alloc(NN * 4);
+    node_body.alloc(NN * 4);
+    k_node_sizes<<<nblk(NN), NT, 0, s>>>(noff, m, NN, p.flags.as<uint8_t>(), recsz.as<int64_t>(),
+                                          rr.as<int32_t>(), node_body.as<int32_t>());
+    p.rec_off.alloc((NN + 1) * 8);
+    exclusive_scan(recsz.as<int64_t>(), p.rec_off.as<int64_t>(), NN, s);
+    exclusive_scan(rr.as<int32_t>(), rr_scan.as<int32_t>(), NN, s);
+    p.res_off.alloc(NN * 4);
+    k_res_off<<<nblk(NN), NT, 0, s>>>(noff, boff, node_body.as<int32_t>(), rr_scan.as<int32_t>(), NN,
+                                       p.res_off.as<int32_t>());
+    {
+      int64_t last_off = d2h1<int64_t>(p.rec_off.as<int64_t>() + NN - 1, s);
+      int64_t last_sz = d2h1<int64_t>(recsz.as<int64_t>() + NN - 1, s);
+      p.rec_doubles = last_off + last_sz;
+    }
+    RQ_CUDA(cudaMemcpyAsync(p.rec_off.as<int64_t>() + NN, &p.rec_doubles, 8, cudaMemcpyHostToDevice, s));
+    recsz.reset();
+    rr.reset();
+    rr_scan.reset();
+
+    // 5. factors
+    p.t22.alloc(NN * 48);
+    p.rec.alloc(std::max<int64_t>(p.rec_doubles, 1) * 8);
+    p.height.alloc(NN * 4);
+    RQ_CUDA(cudaMemsetAsync(p.height.p, 0, NN * 4, s));
+    RQ_CUDA(cudaMemsetAsync(p.t22.p, 0, NN * 48, s));
+    {
+      DBuf counter;
+      counter.alloc(NN * 4);
+      RQ_CUDA(cudaMemsetAsync(counter.p, 0, NN * 4, s));
+      FactorCtx fc{boff,
+                   noff,
+                   p.body_of.as<int32_t>(),
+                   leaf_id.as<int32_t>(),
+                   p.start.as<int32_t>(),
+                   p.stop.as<int32_t>(),
+                   p.left.as<int32_t>(),
+                   p.right.as<int32_t>(),
+                   p.parent.as<int32_t>(),
+                   p.pos_tree.as<double>(),
+                   p.rec_off.as<int64_t>(),
+                   counter.as<int32_t>(),
+                   p.height.as<int32_t>(),
+                   p.flags.as<uint8_t>(),
+                   p.centroid.as<double>(),
+                   p.t22.as<double>(),
+                   p.rec.as<double>()};
+      k_factor<<<nblk(N, 128), 128, 0, s>>>(fc, N);
+      RQ_CUDA(cudaGetLastError());
+      RQ_CUDA(cudaStreamSynchronize(s));
+    }
+
+    // 6. apply layout
+    const int S = p.tile_leaves;
+    LayoutCtx lc{S,
+                 boff,
+                 noff,
+                 node_body.as<int32_t>(),
+                 p.start.as<int32_t>(),
+                 p.stop.as<int32_t>(),
+                 p.parent.as<int32_t>(),
+                 p.height.as<int32_t>(),
+                 p.res_off.as<int32_t>(),
+                 p.rec_off.as<int64_t>(),
+                 p.flags.as<uint8_t>()};
+    DBuf is_tile, is_slot, is_top, tile_scan, slot_scan, top_scan;
+    is_tile.alloc(NN * 4);
+    is_slot.alloc(NN * 4);
+    is_top.alloc(NN * 4);
+    tile_scan.alloc(NN * 4);
+    slot_scan.alloc(NN * 4);
+    top_scan.alloc(NN * 4);
+    k_classify<<<nblk(NN), NT, 0, s>>>(lc, NN, is_tile.as<int32_t>(), is_slot.as<int32_t>(),
+                                        is_top.as<int32_t>());
+    exclusive_scan(is_tile.as<int32_t>(), tile_scan.as<int32_t>(), NN, s);
+    exclusive_scan(is_slot.as<int32_t>(), slot_scan.as<int32_t>(), NN, s);
+    exclusive_scan(is_top.as<int32_t>(), top_scan.as<int32_t>(), NN, s);
+    auto count_of = [&](DBuf &flag, DBuf &scan) {
+      return (int64_t)d2h1<int32_t>(scan.as<int32_t>() + NN - 1, s) +
+             d2h1<int32_t>(flag.as<int32_t>() + NN - 1, s);
+    };
+    const int64_t n_tiles_all = count_of(is_tile, tile_scan);
+    p.n_slots = count_of(is_slot, slot_scan);
+    p.n_top = count_of(is_top, top_scan);
+
+    DBuf tiles_tmp, marker, tile_of;
+    tiles_tmp.alloc(n_tiles_all * sizeof(TileTmp));
+    marker.alloc(NN * 4);
+    tile_of.alloc(NN * 4);
+    RQ_CUDA(cudaMemsetAsync(marker.p, 0xff, NN * 4, s));
+    k_tiles<<<nblk(NN), NT, 0, s>>>(lc, NN, is_tile.as<int32_t>(), tile_scan.as<int32_t>(),
+                                     tiles_tmp.as<TileTmp>(), marker.as<int32_t>());
+    {
+      size_t tb = 0;
+      RQ_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, marker.as<int32_t>(), tile_of.as<int32_t>(),
+                                             MaxOp{}, NN, s));
+      DBuf tmp;
+      tmp.alloc(tb);
+      RQ_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, tb, marker.as<int32_t>(), tile_of.as<int32_t>(),
+                                             MaxOp{}, NN, s));
+    }
+    // per-body tile ranges (tiles are in global postorder = body order)
+    std::vector<TileTmp> htiles(n_tiles_all);
+    d2h(htiles.data(), tiles_tmp.p, n_tiles_all, s);
+    std::vector<int64_t> body_tile_begin(m + 1, 0);
+    std::vector<int32_t> big_scan(n_tiles_all + 1, 0);
+    {
+      int64_t t = 0;
+      for (int64_t j = 0; j < m; j++) {
+        body_tile_begin[j] = t;
+        while (t < n_tiles_all && htiles[t].body == j) t++;
+      }
+      body_tile_begin[m] = n_tiles_all;
+      for (int64_t i = 0; i < n_tiles_all; i++) big_scan[i + 1] = big_scan[i] + htiles[i].big;
+    }
+    p.n_tiles = big_scan[n_tiles_all];
+    DBuf d_body_tile_begin, d_big_scan;
+    d_body_tile_begin.alloc((m + 1) * 8);
+    d_big_scan.alloc((n_tiles_all + 1) * 4);
+    RQ_CUDA(cudaMemcpyAsync(d_body_tile_begin.p, body_tile_begin.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
+    RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
+
+    ChunkLimits lim;
+    lim.max_bytes = 32 * 1024;
+    if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
+    // a single worst-case tile (all GENERAL nodes) must fit a chunk
+    lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, 24 * (S - 1)));
+    lim.max_nodes = 1024;
+    lim.max_beads = 1024;
+    lim.max_res = 3 * 1024;
+    DBuf nch_body, chunk_base;
+    nch_body.alloc(m * 8);
+    chunk_base.alloc((m + 1) * 8);
+    DBuf chunk_of_tile, res_local_of_tile;
+    chunk_of_tile.alloc(n_tiles_all * 8);
+    res_local_of_tile.alloc(n_tiles_all * 4);
+    k_pack<<<nblk(m, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_body_tile_begin.as<int64_t>(), boff, m,
+                                         lim, 0, nullptr, d_big_scan.as<int32_t>(), nch_body.as<int64_t>(),
+                                         nullptr, nullptr, nullptr);
+    exclusive_scan(nch_body.as<int64_t>(), chunk_base.as<int64_t>(), m, s);
+    p.n_chunks = d2h1<int64_t>(chunk_base.as<int64_t>() + m - 1, s) + d2h1<int64_t>(nch_body.as<int64_t>() + m - 1, s);
+    RQ_CUDA(cudaMemcpyAsync(chunk_base.as<int64_t>() + m, &p.n_chunks, 8, cudaMemcpyHostToDevice, s));
+    p.chunks.alloc(std::max<int64_t>(p.n_chunks, 1) * sizeof(ChunkDesc));
+    k_pack<<<nblk(m, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_body_tile_begin.as<int64_t>(), boff, m,
+                                         lim, 1, chunk_base.as<int64_t>(), d_big_scan.as<int32_t>(),
+                                         nch_body.as<int64_t>(), p.chunks.as<ChunkDesc>(),
+                                         chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>());
+    const int64_t nc = p.n_chunks;
+    DBuf cbytes, cnodes, clevels, bytes_scan, node_scan, lvl_base;
+    cbytes.alloc(nc * 8);
+    cnodes.alloc(nc * 8);
+    clevels.alloc(nc * 8);
+    bytes_scan.alloc((nc + 1) * 8);
+    node_scan.alloc((nc + 1) * 8);
+    lvl_base.alloc((nc + 1) * 8);
+    k_chunk_sizes<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, cbytes.as<int64_t>(),
+                                           cnodes.as<int64_t>(), clevels.as<int64_t>());
+    exclusive_scan(cbytes.as<int64_t>(), bytes_scan.as<int64_t>(), nc, s);
+    exclusive_scan(cnodes.as<int64_t>(), node_scan.as<int64_t>(), nc, s);
+    exclusive_scan(clevels.as<int64_t>(), lvl_base.as<int64_t>(), nc, s);
+    k_chunk_offsets<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, bytes_scan.as<int64_t>());
+    {
+      std::vector<ChunkDesc> hc(nc);
+      d2h(hc.data(), p.chunks.p, nc, s);
+      p.blob_bytes = hc[nc - 1].blob_off + hc[nc - 1].blob_bytes;
+      int64_t n_part = 0, n_lvl = 0;
+      p.max_blob = p.max_chunk_nodes = p.max_chunk_beads = p.max_chunk_levels = p.max_chunk_res = 0;
+      for (auto &d : hc) {
+        n_part += d.n_nodes;
+        n_lvl += d.n_levels;
+        p.max_blob = std::max<int64_t>(p.max_blob, d.blob_bytes);
+        p.max_chunk_nodes = std::max(p.max_chunk_nodes, d.n_nodes);
+        p.max_chunk_beads = std::max(p.max_chunk_beads, d.n_beads);
+        p.max_chunk_levels = std::max(p.max_chunk_levels, d.n_levels);
+        p.max_chunk_res = std::max(p.max_chunk_res, d.n_res);
+      }
+      p.blob.alloc(p.blob_bytes);
+      RQ_CUDA(cudaMemsetAsync(p.blob.p, 0, p.blob_bytes, s));
+      DBuf lvl;
+      lvl.alloc(std::max<int64_t>(n_lvl, 1) * sizeof(LevelDesc));
+      RQ_CUDA(cudaMemsetAsync(lvl.p, 0, std::max<int64_t>(n_lvl, 1) * sizeof(LevelDesc), s));
+
+      // level-major node order inside chunks
+      DBuf nkeys, nvals, nkeys2, nvals2, slot_of;
+      nkeys.alloc(NN * 8);
+      nvals.alloc(NN * 4);
+      nkeys2.alloc(NN * 8);
+      nvals2.alloc(NN * 4);
+      slot_of.alloc(NN * 4);
+      RQ_CUDA(cudaMemsetAsync(slot_of.p, 0xff, NN * 4, s));
+      k_node_keys<<<nblk(NN), NT, 0, s>>>(lc, NN, is_top.as<int32_t>(), tile_of.as<int32_t>(),
+                                           chunk_of_tile.as<int64_t>(), nkeys.as<uint64_t>(),
+                                           nvals.as<int32_t>());
+      size_t tb = 0;
+      RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, nkeys.as<uint64_t>(), nkeys2.as<uint64_t>(),
+                                              nvals.as<int32_t>(), nvals2.as<int32_t>(), (int)NN, 0, 64, s));
+      DBuf tmp;
+      tmp.alloc(tb);
+      RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, nkeys.as<uint64_t>(), nkeys2.as<uint64_t>(),
+                                              nvals.as<int32_t>(), nvals2.as<int32_t>(), (int)NN, 0, 64, s));
+      tmp.reset();
+      if (n_part > 0)
+        k_slots<<<nblk(n_part), NT, 0, s>>>(nkeys2.as<uint64_t>(), nvals2.as<int32_t>(), n_part,
+                                             node_scan.as<int64_t>(), slot_of.as<int32_t>(),
+                                             lvl_base.as<int64_t>(), lvl.as<LevelDesc>(), p.flags.as<uint8_t>());
+      k_levels_finalize<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, lvl_base.as<int64_t>(),
+                                                 lvl.as<LevelDesc>(), p.blob.as<uint8_t>());
+      WriteCtx wc{lc,
+                  nkeys2.as<uint64_t>(),
+                  nvals2.as<int32_t>(),
+                  slot_of.as<int32_t>(),
+                  tile_of.as<int32_t>(),
+                  p.left.as<int32_t>(),
+                  p.right.as<int32_t>(),
+                  tiles_tmp.as<TileTmp>(),
+                  res_local_of_tile.as<int32_t>(),
+                  p.chunks.as<ChunkDesc>(),
+                  lvl_base.as<int64_t>(),
+                  lvl.as<LevelDesc>(),
+                  p.rec.as<double>(),
+                  p.blob.as<uint8_t>()};
+      if (n_part > 0) k_write_nodes<<<nblk(n_part), NT, 0, s>>>(wc, n_part);
+      k_write_perm<<<(unsigned)nc, 128, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, p.perm.as<int32_t>(),
+                                                  leaf_id.as<int32_t>(), noff, p.parent.as<int32_t>(),
+                                                  p.start.as<int32_t>(), p.stop.as<int32_t>(), S,
+                                                  p.blob.as<uint8_t>());
+      p.tiles.alloc(std::max<int64_t>(p.n_tiles, 1) * sizeof(TileDesc));
+      k_tile_desc<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
+                                                    d_big_scan.as<int32_t>(), slot_of.as<int32_t>(),
+                                                    slot_scan.as<int32_t>(), res_local_of_tile.as<int32_t>(),
+                                                    p.parent.as<int32_t>(), p.tiles.as<TileDesc>());
+    }
+
+    // top tree
+    {
+      std::vector<int64_t> topbodies;
+      std::vector<int32_t> smalls;
+      std::vector<int32_t> topbody_idx(m, -1);
+      for (int64_t j = 0; j < m; j++) {
+        int64_t n = offsets[j + 1] - offsets[j];
+        if (n > S) { topbody_idx[j] = (int32_t)topbodies.size(); topbodies.push_back(j); }
+        if (n == 1) smalls.push_back((int32_t)j);
+      }
+      p.n_topbodies = (int64_t)topbodies.size();
+      p.n_small = (int64_t)smalls.size();
+      p.small_bodies.alloc(std::max<int64_t>(p.n_small, 1) * 4);
+      if (p.n_small)
+        RQ_CUDA(cudaMemcpyAsync(p.small_bodies.p, smalls.data(), p.n_small * 4, cudaMemcpyHostToDevice, s));
+      const int64_t nt = p.n_top;
+      p.top.alloc(std::max<int64_t>(nt, 1) * sizeof(TopNode));
+      std::vector<int32_t> hb(topbodies.begin(), topbodies.end());
+      p.topbody.alloc(std::max<int64_t>(p.n_topbodies, 1) * 4);
+      p.topbody_lvl.alloc((p.n_topbodies + 1) * 4);
+      if (p.n_topbodies)
+        RQ_CUDA(cudaMemcpyAsync(p.topbody.p, hb.data(), p.n_topbodies * 4, cudaMemcpyHostToDevice, s));
+      if (nt > 0) {
+        DBuf tmp_top, tkeys, tvals, tkeys2, tvals2, lflag, lscan, d_tbi;
+        tmp_top.alloc(nt * sizeof(TopNode));
+        tkeys.alloc(nt * 8);
+        tvals.alloc(nt * 4);
+        tkeys2.alloc(nt * 8);
+        tvals2.alloc(nt * 4);
+        lflag.alloc(nt * 4);
+        lscan.alloc(nt * 4);
+        d_tbi.alloc(m * 4);
+        RQ_CUDA(cudaMemcpyAsync(d_tbi.p, topbody_idx.data(), m * 4, cudaMemcpyHostToDevice, s));
+        k_top_fill<<<nblk(NN), NT, 0, s>>>(lc, NN, is_top.as<int32_t>(), top_scan.as<int32_t>(),
+                                            slot_scan.as<int32_t>(), p.left.as<int32_t>(), p.right.as<int32_t>(),
+                                            tmp_top.as<TopNode>(), tkeys.as<uint64_t>(), tvals.as<int32_t>());
+        size_t tb = 0;
+        RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkeys.as<uint64_t>(), tkeys2.as<uint64_t>(),
+                                                tvals.as<int32_t>(), tvals2.as<int32_t>(), (int)nt, 0, 64, s));
+        DBuf tmp;
+        tmp.alloc(tb);
+        RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkeys.as<uint64_t>(), tkeys2.as<uint64_t>(),
+                                                tvals.as<int32_t>(), tvals2.as<int32_t>(), (int)nt, 0, 64, s));
+        k_top_gather<<<nblk(nt), NT, 0, s>>>(tmp_top.as<TopNode>(), tvals2.as<int32_t>(), tkeys2.as<uint64_t>(),
+                                              nt, p.top.as<TopNode>(), lflag.as<int32_t>());
+        exclusive_scan(lflag.as<int32_t>(), lscan.as<int32_t>(), nt, s);
+        p.n_toplevels = d2h1<int32_t>(lscan.as<int32_t>() + nt - 1, s) + d2h1<int32_t>(lflag.as<int32_t>() + nt - 1, s);
+        p.toplvl.alloc((p.n_toplevels + 1) * 4);
+        k_top_levels<<<nblk(nt), NT, 0, s>>>(tkeys2.as<uint64_t>(), lflag.as<int32_t>(), lscan.as<int32_t>(), nt,
+                                              p.toplvl.as<int32_t>(), d_tbi.as<int32_t>(),
+                                              p.topbody_lvl.as<int32_t>());
+        int32_t endv[2] = {(int32_t)nt, (int32_t)p.n_toplevels};
+        RQ_CUDA(cudaMemcpyAsync(p.toplvl.as<int32_t>() + p.n_toplevels, &endv[0], 4, cudaMemcpyHostToDevice, s));
+        RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.as<int32_t>() + p.n_topbodies, &endv[1], 4, cudaMemcpyHostToDevice, s));
+        RQ_CUDA(cudaStreamSynchronize(s));
+      } else {
+        p.toplvl.alloc(4);
+        int32_t z = 0;
+        RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.p, &z, 4, cudaMemcpyHostToDevice, s));
+        RQ_CUDA(cudaStreamSynchronize(s));
+      }
+    }
+    // case counts
+    {
+      std::vector<uint8_t> hf(NN);
+      d2h(hf.data(), p.flags.p, NN, s);
+      for (auto f : hf) p.n_case[f & 3]++;
+    }
+    RQ_CUDA(cudaGetLastError());
+    RQ_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+int check_duplicates(const double *pos_in, const int64_t *offsets, int64_t m, bool host_input, cudaStream_t s,
+                     int64_t *body, int64_t *bi, int64_t *bj, double *tol_out) {
+  if (m < 1) throw Error(RQ_ERR_VALUE, "need at least one body");
+  for (int64_t j = 0; j < m; j++)
+    if (offsets[j + 1] <= offsets[j]) throw Error(RQ_ERR_VALUE, "every body needs n >= 1");
+  const int64_t N = offsets[m];
+  DBuf pos, off, body_of, bmin, bmax, table, hit, err;
+  pos.alloc(N * 24);
+  RQ_CUDA(cudaMemcpyAsync(pos.p, pos_in, N * 24, host_input ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  off.alloc((m + 1) * 8);
+  RQ_CUDA(cudaMemcpyAsync(off.p, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, s));
+  body_of.alloc(N * 4);
+  k_body_of<<<nblk(N), NT, 0, s>>>(off.as<int64_t>(), m, N, body_of.as<int32_t>());
+  bmin.alloc(m * 24);
+  bmax.alloc(m * 24);
+  err.alloc(64);
+  RQ_CUDA(cudaMemsetAsync(bmin.p, 0xff, m * 24, s));
+  RQ_CUDA(cudaMemsetAsync(bmax.p, 0x00, m * 24, s));
+  {
+    long long init[8] = {0, 0, 0x7fffffffffffffffLL, 0, 0, 0, 0, 0};
+    RQ_CUDA(cudaMemcpyAsync(err.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  }
+  k_bbox<<<nblk(N), NT, 0, s>>>(pos.as<double>(), body_of.as<int32_t>(), N, bmin.as<unsigned long long>(),
+                                 bmax.as<unsigned long long>(), err.as<long long>());
+  uint64_t cap = 1;
+  while (cap < (uint64_t)(2 * N)) cap <<= 1;
+  table.alloc(cap * 4);
+  RQ_CUDA(cudaMemsetAsync(table.p, 0xff, cap * 4, s));
+  hit.alloc(m * 8);
+  RQ_CUDA(cudaMemsetAsync(hit.p, 0xff, m * 8, s));
+  DupCtx c{pos.as<double>(), body_of.as<int32_t>(), off.as<int64_t>(), bmin.as<unsigned long long>(),
+           bmax.as<unsigned long long>(), table.as<int32_t>(), cap - 1, hit.as<unsigned long long>(),
+           err.as<long long>()};
+  k_dup_insert<<<nblk(N), NT, 0, s>>>(c, N);
+  k_dup_query<<<nblk(N), NT, 0, s>>>(c, N);
+  RQ_CUDA(cudaGetLastError());
+  long long e[3];
+  d2h(e, err.p, 3, s);
+  if (e[1]) throw Error(RQ_ERR_VALUE, "positions must be finite");
+  std::vector<unsigned long long> h(m);
+  d2h(h.data(), hit.p, m, s);
+  int64_t coincide = e[2];
+  for (int64_t j = 0; j < m; j++) {
+    if (j == coincide) {
+      *body = j; *bi = -1; *bj = -1; *tol_out = 0.0;
+      return RQ_ERR_DUPLICATE;
+    }
+    if (h[j] != ~0ull) {
+      *body = j;
+      *bi = (int64_t)(h[j] >> 32);
+      *bj = (int64_t)(h[j] & 0xffffffffull);
+      std::vector<unsigned long long> bb(6);
+      d2h(bb.data(), bmin.as<unsigned long long>() + 3 * j, 3, s);
+      d2h(bb.data() + 3, bmax.as<unsigned long long>() + 3 * j, 3, s);
+      double d2 = 0.0;
+      for (int a = 0; a < 3; a++) {
+        auto un = [](unsigned long long u) {
+          long long v = (long long)((u >> 63) ? (u & 0x7fffffffffffffffull) : ~u);
+          double d;
+          memcpy(&d, &v, 8);
+          return d;
+        };
+        double ext = un(bb[3 + a]) - un(bb[a]);
+        d2 += ext * ext;
+      }
+      *tol_out = 1e-12 * sqrt(d2);
+      return RQ_ERR_DUPLICATE;
+    }
+  }
+  return RQ_OK;
+}
+
+}  // namespace rq

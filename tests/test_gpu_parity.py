@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path vs the reference's own outputs (tests/golden) and
+vs the pinned C oracle on seeded inputs, plus size-independent properties at
+larger sizes.  Tolerances: 1e-12 relative (2-norm, per body) for vectors as
+BASELINE.json north_star states; exact for tree structure and index layout.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_cases
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def rq():
+    import paper_1708_08427_b200 as rq
+    from paper_1708_08427_b200 import _lib
+
+    if _lib.device_count() < 1:
+        pytest.fail("no GPU visible: the gpu tests must run on a B200 (no CPU fallback)")
+    return rq
+
+
+def load(name):
+    return dict(np.load(f"{GOLDEN}/{name}.npz"))
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - b) / (nb if nb > 0 else 1.0)
+
+
+def per_body_rel(out, ref, lens):
+    worst = 0.0
+    o = 0
+    for ln in lens:
+        if ln:
+            worst = max(worst, rel(out[o:o + ln], ref[o:o + ln]))
+        o += ln
+    return worst
+
+
+NONDEGEN = [c for c in golden_cases() if not c.startswith("line")]
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_tree_layout_exact(rq, name):
+    """Tree structure and index layout equal the reference exactly (tree.py, factor.py:195-204)."""
+    g = load(name)
+    off = g["offsets"]
+    for j in range(len(off) - 1):
+        model = rq.BeadModel(g["positions"][off[j]:off[j + 1]])
+        tree = rq.build_tree(model)
+        fac = rq.factor_all(tree)
+        a = tree._plan.export_tree(0)
+        for key in ("perm", "start", "stop", "left", "right", "split_axis", "depth"):
+            np.testing.assert_array_equal(a[key], g[f"b{j}_{key}"], err_msg=f"{name} body {j} {key}")
+        np.testing.assert_array_equal(a["box"], g[f"b{j}_box"])
+        # centroid recursion (tree.py:126) is reproduced bit for bit
+        np.testing.assert_array_equal(a["centroid"], g[f"b{j}_centroid"])
+        f = tree._plan.export_factors(0)
+        for key, gk in (("case", "case"), ("n", "fn"), ("nx", "fnx"), ("ny", "fny"), ("res_offsets", "res_offsets")):
+            np.testing.assert_array_equal(f[key], g[f"b{j}_{gk}"], err_msg=f"{name} {key}")
+        np.testing.assert_array_equal(f["swapped"].astype(bool), g[f"b{j}_swapped"])
+        assert f["total_rows"] == int(g[f"b{j}_total_rows"])
+        assert fac.total_rows == int(g[f"b{j}_total_rows"])
+        if not name.startswith("line"):
+            np.testing.assert_allclose(f["t22"], g[f"b{j}_t22"], rtol=0, atol=1e-12)
+            if model.n > 1:
+                np.testing.assert_allclose(f["omega_flat"], g[f"b{j}_omega"], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", NONDEGEN)
+def test_apply_vs_reference(rq, name):
+    g = load(name)
+    off = g["offsets"]
+    n = np.diff(off)
+    model = rq.MultiBodyModel.from_arrays(g["positions"], off)
+    op = rq.MultiBodyOperator(model)
+    full = list(3 * n)
+    comp = list(3 * n - 6)
+    for opn, src, lens in (("qv", "v", full), ("qtv", "w", full), ("qtilde_v", "v", comp),
+                           ("qtilde_tv", "g", full)):
+        if opn not in g:
+            continue
+        out = op.apply(opn, g[src])
+        assert out.shape == g[opn].shape
+        assert per_body_rel(out, g[opn], lens) < TOL, opn
+        big = {"v": "V", "w": "W", "g": "G"}[src]
+        outk = op.apply(opn, g[big])
+        assert outk.shape == g[opn + "_k"].shape
+        assert per_body_rel(outk, g[opn + "_k"], lens) < TOL, opn + "_k"
+
+
+@pytest.mark.parametrize("name", [c for c in NONDEGEN if "zf" in np.load(f"{GOLDEN}/{c}.npz")])
+def test_z_vs_reference(rq, name):
+    g = load(name)
+    off = g["offsets"]
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(g["positions"], off))
+    zf = op.zf(g["f"])
+    for j in range(len(off) - 1):
+        p = g["positions"][off[j]:off[j + 1]]
+        zfro = np.sqrt(3 * len(p) + 2 * np.sum((p - p.mean(0)) ** 2))
+        fn = np.linalg.norm(g["f"][3 * off[j]:3 * off[j + 1]])
+        assert np.abs(zf[6 * j:6 * j + 6] - g["zf"][6 * j:6 * j + 6]).max() <= 1e-13 * zfro * fn
+    assert rel(op.ztu(g["u"]), g["ztu"]) < 1e-13
+    np.testing.assert_allclose(op.plan.centroids(), g["model_centroid"], rtol=0, atol=1e-15)
+
+
+def test_explicit_q_vs_reference(rq):
+    for name in ("explicit_q", "uniform300", "kat_pm", "kat_two"):
+        g = load(name)
+        off = g["offsets"]
+        for j in range(len(off) - 1):
+            if f"q{j}_root_rows" not in g:
+                continue
+            tree = rq.build_tree(rq.BeadModel(g["positions"][off[j]:off[j + 1]]))
+            hq = rq.generate_explicit_q(tree)
+            np.testing.assert_allclose(hq.root_rows, g[f"q{j}_root_rows"], rtol=0, atol=1e-12)
+            assert [b[0] for b in hq.blocks] == list(g[f"q{j}_block_node"])
+            assert [b[1] for b in hq.blocks] == list(g[f"q{j}_block_col"])
+            assert [b[2].shape[0] for b in hq.blocks] == list(g[f"q{j}_block_rows"])
+            data = np.concatenate([b[2].ravel() for b in hq.blocks]) if hq.blocks else np.zeros(0)
+            np.testing.assert_allclose(data, g[f"q{j}_block_data"], rtol=0, atol=1e-12)
+            q = rq.materialize_dense(hq)
+            assert np.abs(q @ q.T - np.eye(q.shape[0])).max() < 1e-13
+
+
+def test_kat_pm(rq):
+    """SPEC.md:265/345/355/376/385 known answers."""
+    op = rq.BodyOperator(rq.BeadModel([[0, 0, 1.0], [0, 0, -1.0]]))
+    out = op.qv(np.array([1.0, 0, 0, 1.0, 0, 0]))
+    np.testing.assert_allclose(out, [np.sqrt(2), 0, 0, 0, 0, 0], atol=1e-15)
+    np.testing.assert_allclose(op.qtv(out), [1, 0, 0, 1, 0, 0], atol=1e-15)
+    assert op.qtilde_v(np.ones(6)).shape == (0,)
+    f = op.factors[2]
+    np.testing.assert_allclose(f.t22, [[np.sqrt(2), 0, 0], [0, np.sqrt(2), 0], [0, 0, 0]], atol=1e-15)
+
+
+def test_degenerate_line_by_span(rq):
+    """Collinear input: compare spans (projector distance), never vectors."""
+    g = load("line64")
+    pos = g["positions"]
+    n = pos.shape[0]
+    op = rq.BodyOperator(rq.BeadModel(pos))
+    qt = op.qtilde_v(np.eye(3 * n))  # Q~ itself, (3n-6) x 3n
+    assert np.abs(qt @ qt.T - np.eye(3 * n - 6)).max() < 1e-10
+    z = rq.assemble_z(rq.BeadModel(pos)).entries
+    _, s, vt = np.linalg.svd(z, full_matrices=True)
+    rank = int((s > max(z.shape) * np.finfo(float).eps * s[0]).sum())
+    assert rank == 5
+    # Q~ is orthogonal to the row space of Z
+    assert np.abs(qt @ z.T).max() < 1e-10 * np.abs(z).max()
+
+
+def test_oracle_config_sizes(rq, oracle_mod):
+    """Config-2/4 style bodies (ellipsoid shells, mixed sizes incl. > 1 chunk and top trees)."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch, sphere_shell
+
+    counts = [4096] * 12 + [2, 3, 129, 130, 500, 50000, 1000, 257]
+    pos, off = ellipsoid_batch(counts, seed=11)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    ref = oracle_mod.OracleBatch(pos, off, threads=8)
+    rng = np.random.default_rng(5)
+    n = np.diff(off)
+    v = rng.normal(size=3 * off[-1])
+    for opn, lens in (("qv", 3 * n), ("qtv", 3 * n), ("qtilde_v", 3 * n - 6)):
+        assert per_body_rel(op.apply(opn, v), ref.apply(opn, v), lens) < TOL, opn
+    V = rng.normal(size=(3 * off[-1], 4))
+    assert per_body_rel(op.apply("qv", V), ref.apply("qv", V), 3 * n) < TOL
+    # single large sphere body (config-3 generator, reduced n)
+    p3 = sphere_shell(1 << 16, 0)
+    o3 = np.array([0, 1 << 16])
+    op3 = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(p3, o3))
+    ref3 = oracle_mod.OracleBatch(p3, o3, threads=1)
+    v3 = rng.normal(size=3 << 16)
+    g3 = rng.normal(size=(3 << 16) - 6)
+    assert rel(op3.apply("qtilde_v", v3), ref3.apply("qtilde_v", v3)) < TOL
+    assert rel(op3.apply("qtilde_tv", g3), ref3.apply("qtilde_tv", g3)) < TOL
+
+
+def test_properties_large(rq):
+    """Size-independent properties at config-2 body size: round trip, isometry,
+    adjointness, complement property."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([4096] * 64, seed=2)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    rng = np.random.default_rng(1)
+    N, m = int(off[-1]), len(off) - 1
+    v = rng.normal(size=3 * N)
+    g = rng.normal(size=3 * N - 6 * m)
+    w = op.apply("qtilde_tv", g)
+    assert np.abs(op.apply("qtilde_v", w) - g).max() < 1e-12 * np.abs(g).max()
+    qv = op.apply("qv", v)
+    assert abs(np.linalg.norm(qv) - np.linalg.norm(v)) < 1e-12 * np.linalg.norm(v)
+    assert np.abs(op.apply("qtv", qv) - v).max() < 1e-12 * np.abs(v).max()
+    assert abs(op.apply("qtilde_v", v) @ g - v @ w) < 1e-12 * np.linalg.norm(v) * np.linalg.norm(g)
+    # Z Q~^T g = 0  and  Q~ Z^T u = 0
+    zf = op.zf(w)
+    assert np.abs(zf).max() < 1e-12 * np.linalg.norm(g) * 10
+    u = rng.normal(size=6 * m)
+    assert np.abs(op.apply("qtilde_v", op.ztu(u))).max() < 1e-12 * np.abs(op.ztu(u)).max() * 10
+
+
+def test_batch_bitwise_equals_per_body(rq):
+    """multi-body blocks equal independent per-body runs bit-exactly."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([700, 40, 3000], seed=9)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    rng = np.random.default_rng(2)
+    v = rng.normal(size=3 * off[-1])
+    out = op.apply("qtilde_v", v)
+    o = 0
+    for j in range(3):
+        body = rq.BodyOperator(rq.BeadModel(pos[off[j]:off[j + 1]]))
+        blk = body.qtilde_v(v[3 * off[j]:3 * off[j + 1]])
+        assert np.array_equal(blk, out[o:o + len(blk)])
+        o += len(blk)
+    again = op.apply("qtilde_v", v)
+    assert np.array_equal(out, again)
+
+
+def test_torch_device_path(rq):
+    import torch
+
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([1000, 2000], seed=3)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    v = np.random.default_rng(0).normal(size=3 * off[-1])
+    host = op.apply("qv", v)
+    dev = op.apply("qv", torch.from_numpy(v).cuda())
+    assert dev.is_cuda
+    np.testing.assert_array_equal(dev.cpu().numpy(), host)
+
+
+def test_errors(rq):
+    with pytest.raises(rq.DuplicateBeadsError):
+        rq.BeadModel([[0, 0, 0], [1, 1, 1], [0, 0, 1e-14]])
+    with pytest.raises(rq.DuplicateBeadsError):
+        rq.BeadModel([[1, 1, 1], [1, 1, 1]])
+    with pytest.raises(ValueError):
+        rq.BeadModel([[0, 0, np.nan]])
+    with pytest.raises(ValueError):
+        rq.BeadModel(np.zeros((3, 2)))
+    # tree-level guard (tree.py:99-103) with a tiny max_depth
+    with pytest.raises(rq.DuplicateBeadsError):
+        rq.build_tree(rq.BeadModel([[0, 0, 0], [1e-6, 0, 0], [1, 1, 1]]), max_depth=6)
+    one = rq.BodyOperator(rq.BeadModel([[0.5, 0.5, 0.5]]))
+    np.testing.assert_array_equal(one.qv([1.0, 2.0, 3.0]), [1.0, 2.0, 3.0])
+    with pytest.raises(rq.BodyTooSmallError):
+        one.qtilde_v([1.0, 2.0, 3.0])
+    two = rq.BodyOperator(rq.BeadModel([[0, 0, 1.0], [0, 0, -1.0], [1, 0, 0]]))
+    with pytest.raises(rq.LengthMismatchError):
+        two.qv(np.zeros(8))
+    with pytest.raises(rq.LengthMismatchError):
+        two.qv(np.zeros((9, 2, 2)))
+    mm = rq.MultiBodyModel([rq.BeadModel([[0, 0, 0.0]]), rq.BeadModel([[0, 0, 1.0], [1, 0, 0]])])
+    mop = rq.MultiBodyOperator(mm)
+    with pytest.raises(ValueError):
+        mop.apply("bogus", np.zeros(9))
+    with pytest.raises(rq.BodyTooSmallError):
+        mop.apply("qtilde_v", np.zeros(9))
+    np.testing.assert_allclose(mop.apply("qtv", mop.apply("qv", np.arange(9.0))), np.arange(9.0), atol=1e-14)
+    with pytest.raises(rq.TooSmallError):
+        rq.generate_explicit_q(one.tree)
+
+
+def test_node_primitives(rq, oracle_mod):
+    """small_lq / factor_bead_bead / merge / split single-node entry points."""
+    rng = np.random.default_rng(4)
+    for k in (3, 6, 9):
+        a = rng.normal(size=(3, k))
+        t, om = rq.small_lq(a)
+        t0, om0 = oracle_mod.small_lq(a)
+        np.testing.assert_allclose(t, t0, atol=1e-14)
+        np.testing.assert_allclose(om, om0, atol=1e-14)
+    t, om = rq.small_lq(np.zeros((3, 9)))
+    assert not t.any() and np.array_equal(om, np.eye(9))
+    f = rq.factor_bead_bead([0, 0, 1.0])
+    np.testing.assert_allclose(f.t22, [[np.sqrt(2), 0, 0], [0, np.sqrt(2), 0], [0, 0, 0]], atol=1e-15)
+    op = rq.BodyOperator(rq.BeadModel(rng.normal(size=(40, 3))))
+    for node in op.tree.nodes:
+        if node.is_leaf:
+            continue
+        fac = op.factors[node.id]
+        mx, my = rng.normal(size=(6, 2)), rng.normal(size=(6, 2))
+        if fac.case is rq.NodeCase.BEAD_BEAD:
+            mx[3:] = my[3:] = 0
+        mp, res = rq.merge_infosets(fac, mx, my)
+        lx, ly = rq.split_rvset(fac, mp, res)
+        if fac.case is rq.NodeCase.GENERAL:
+            np.testing.assert_allclose(lx, mx, atol=1e-13)
+            np.testing.assert_allclose(ly, my, atol=1e-13)
