@@ -94,7 +94,7 @@ constexpr uint16_t SRC_BEAD = 0x8000u;
 
 // Apply H_i = I - tau v v^T (v[i] = 1 implicit, v[j<i] = 0) to y (length K).
 template <int K>
-__device__ __forceinline__ void householder(double (&y)[K], const double* vi, double tau, int i) {
+__host__ __device__ __forceinline__ void householder(double (&y)[K], const double* vi, double tau, int i) {
   double d = y[i];
 #pragma unroll
   for (int j = i + 1; j < K; j++) d += vi[j - i - 1] * y[j];

@@ -14,13 +14,13 @@
 
 namespace rq {
 
-__device__ inline double lq_dnrm2(int n, const double *x) {
+__host__ __device__ inline double lq_dnrm2(int n, const double *x) {
   double s = 0.0;
   for (int i = 0; i < n; i++) s += x[i] * x[i];
   return sqrt(s);
 }
 
-__device__ inline double lq_dlapy2(double x, double y) {
+__host__ __device__ inline double lq_dlapy2(double x, double y) {
   double xa = fabs(x), ya = fabs(y);
   double w = fmax(xa, ya), z = fmin(xa, ya);
   if (z == 0.0 || w > 1.7976931348623157e308) return w;
@@ -29,7 +29,7 @@ __device__ inline double lq_dlapy2(double x, double y) {
 }
 
 // dlarfg(n, alpha, x, 1, tau)
-__device__ inline void lq_dlarfg(int n, double &alpha, double *x, double &tau) {
+__host__ __device__ inline void lq_dlarfg(int n, double &alpha, double *x, double &tau) {
   if (n <= 1) { tau = 0.0; return; }
   double xnorm = lq_dnrm2(n - 1, x);
   if (xnorm == 0.0) { tau = 0.0; return; }
@@ -55,7 +55,7 @@ __device__ inline void lq_dlarfg(int n, double &alpha, double *x, double &tau) {
 }
 
 // dlarf('Left') on the column-major m x n block C (ldc) with v (v[0] == 1).
-__device__ inline void lq_dlarf_left(int m, int n, const double *v, double tau, double *C, int ldc) {
+__host__ __device__ inline void lq_dlarf_left(int m, int n, const double *v, double tau, double *C, int ldc) {
   int lastv = 0, lastc = 0;
   if (tau != 0.0) {
     lastv = m;
@@ -88,7 +88,7 @@ __device__ inline void lq_dlarf_left(int m, int n, const double *v, double tau, 
 // Outputs t (lower-triangular, packed t00,t10,t11,t20,t21,t22), the
 // Householder record (HH<K> layout) and the sign bits s_i = -1.
 template <int K>
-__device__ inline void lq_factor(const double *a, double t6[6], double *rec, unsigned &signs) {
+__host__ __device__ inline void lq_factor(const double *a, double t6[6], double *rec, unsigned &signs) {
   bool any = false;
   for (int i = 0; i < 3 * K; i++) any |= (a[i] != 0.0);
   for (int i = 0; i < HH<K>::SIZE; i++) rec[i] = 0.0;
@@ -135,7 +135,7 @@ __device__ inline void lq_factor(const double *a, double t6[6], double *rec, uns
 
 // y <- omega y  = S H2 H1 H0 y   (record with unit stride)
 template <int K>
-__device__ inline void omega_apply(const double *rec, unsigned signs, double (&y)[K]) {
+__host__ __device__ inline void omega_apply(const double *rec, unsigned signs, double (&y)[K]) {
   householder<K>(y, rec + HH<K>::O0, rec[HH<K>::OT + 0], 0);
   householder<K>(y, rec + HH<K>::O1, rec[HH<K>::OT + 1], 1);
   householder<K>(y, rec + HH<K>::O2, rec[HH<K>::OT + 2], 2);
@@ -146,7 +146,7 @@ __device__ inline void omega_apply(const double *rec, unsigned signs, double (&y
 
 // y <- omega^T y = H0 H1 H2 S y
 template <int K>
-__device__ inline void omega_apply_t(const double *rec, unsigned signs, double (&y)[K]) {
+__host__ __device__ inline void omega_apply_t(const double *rec, unsigned signs, double (&y)[K]) {
 #pragma unroll
   for (int i = 0; i < 3; i++)
     if (signs & (1u << i)) y[i] = -y[i];
@@ -155,58 +155,69 @@ __device__ inline void omega_apply_t(const double *rec, unsigned signs, double (
   householder<K>(y, rec + HH<K>::O0, rec[HH<K>::OT + 0], 0);
 }
 
-__device__ inline void skew3(const double r[3], double A[9]) { // model.py:25-30
+__host__ __device__ inline void skew3(const double r[3], double A[9]) { // model.py:25-30
   A[0] = 0.0;   A[1] = -r[2]; A[2] = r[1];
   A[3] = r[2];  A[4] = 0.0;   A[5] = -r[0];
   A[6] = -r[1]; A[7] = r[0];  A[8] = 0.0;
 }
 
-// factor_bead_bead (factor.py:130-168): offset d -> t22 (packed), g (3x3 row-major)
-__device__ inline void factor_bead_bead(const double d[3], double t6[6], double g[9]) {
-  int am = 0;
-  if (fabs(d[1]) > fabs(d[am])) am = 1;
-  if (fabs(d[2]) > fabs(d[am])) am = 2;
-  // _CYCLIC = {2: (0,1,2), 0: (1,2,0), 1: (2,0,1)}
-  int ax0 = am == 2 ? 0 : (am == 0 ? 1 : 2);
-  int ax1 = am == 2 ? 1 : (am == 0 ? 2 : 0);
-  int ax2 = am;
-  int axes[3] = {ax0, ax1, ax2};
-  double a = d[ax0], b = d[ax1], c = d[ax2];
-  double bc2 = b * b + c * c;
-  double ell = a * a + bc2;
-  double sq2 = sqrt(2.0);
-  double sbc2 = sqrt(bc2);
-  double r2l = sqrt(2.0 * ell / bc2);
-  double tp[9] = {sqrt(2.0 * bc2), 0.0, 0.0,
-                  -sq2 * a * b / sbc2, c * r2l, 0.0,
-                  -sq2 * a * c / sbc2, -b * r2l, 0.0};
-  double den0 = sqrt(2.0 * bc2), den1 = sqrt(2.0 * ell * bc2), den2 = sqrt(2.0 * ell);
-  double uh[9] = {0.0 / den0, -c / den0, b / den0,
-                  bc2 / den1, -a * b / den1, -a * c / den1,
-                  -a / den2, -b / den2, -c / den2};
+// factor_bead_bead (factor.py:130-168) in the cyclic frame axes = (A0, A1, A2)
+// (compile-time, so every array index below is static).
+template <int A0, int A1, int A2>
+__host__ __device__ inline void factor_bead_bead_frame(const double d[3], double t6[6], double g[9]) {
+  const double a = d[A0], b = d[A1], c = d[A2];
+  const double bc2 = b * b + c * c;
+  const double ell = a * a + bc2;
+  const double sq2 = sqrt(2.0);
+  const double sbc2 = sqrt(bc2);
+  const double r2l = sqrt(2.0 * ell / bc2);
+  const double tp[9] = {sqrt(2.0 * bc2), 0.0, 0.0,
+                        -sq2 * a * b / sbc2, c * r2l, 0.0,
+                        -sq2 * a * c / sbc2, -b * r2l, 0.0};
+  const double den0 = sqrt(2.0 * bc2), den1 = sqrt(2.0 * ell * bc2), den2 = sqrt(2.0 * ell);
+  const double uh[9] = {0.0 / den0, -c / den0, b / den0,
+                        bc2 / den1, -a * b / den1, -a * c / den1,
+                        -a / den2, -b / den2, -c / den2};
+  constexpr int ax[3] = {A0, A1, A2};
   double m[9], gh[9];
+#pragma unroll
   for (int i = 0; i < 3; i++)
+#pragma unroll
     for (int j = 0; j < 3; j++) {
-      m[axes[i] * 3 + j] = tp[i * 3 + j];
-      gh[i * 3 + axes[j]] = uh[i * 3 + j];
+      m[ax[i] * 3 + j] = tp[i * 3 + j];   // m[perm, :] = t_prime
+      gh[i * 3 + ax[j]] = uh[i * 3 + j];  // g_half[:, perm] = u_half
     }
   double rec3[HH<3>::SIZE];
   unsigned sg;
   lq_factor<3>(m, t6, rec3, sg);
-  // om3 columns: om3 e_j
   double om3[9];
-  for (int j = 0; j < 3; j++) {
+#pragma unroll
+  for (int j = 0; j < 3; j++) {  // om3 e_j
     double y[3] = {0.0, 0.0, 0.0};
     y[j] = 1.0;
     omega_apply<3>(rec3, sg, y);
+#pragma unroll
     for (int i = 0; i < 3; i++) om3[i * 3 + j] = y[i];
   }
+#pragma unroll
   for (int i = 0; i < 3; i++)
+#pragma unroll
     for (int j = 0; j < 3; j++) {
       double s = 0.0;
+#pragma unroll
       for (int l = 0; l < 3; l++) s += om3[i * 3 + l] * gh[l * 3 + j];
-      g[i * 3 + j] = sq2 * s;
+      g[i * 3 + j] = sq2 * s;  // g = sqrt(2) * (om3 @ g_half)
     }
+}
+
+// _CYCLIC = {2: (0,1,2), 0: (1,2,0), 1: (2,0,1)} keyed by argmax|d| (first maximum)
+__host__ __device__ inline void factor_bead_bead(const double d[3], double t6[6], double g[9]) {
+  int am = 0;
+  if (fabs(d[1]) > fabs(d[am])) am = 1;
+  if (fabs(d[2]) > fabs(d[am])) am = 2;
+  if (am == 2) factor_bead_bead_frame<0, 1, 2>(d, t6, g);
+  else if (am == 0) factor_bead_bead_frame<1, 2, 0>(d, t6, g);
+  else factor_bead_bead_frame<2, 0, 1>(d, t6, g);
 }
 
 }  // namespace rq

@@ -1247,8 +1247,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     k_chunk_offsets<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, bytes_scan.as<int64_t>());
     {
       std::vector<ChunkDesc> hc(nc);
-      d2h(hc.data(), p.chunks.p, nc, s);
-      p.blob_bytes = hc[nc - 1].blob_off + hc[nc - 1].blob_bytes;
+      if (nc) d2h(hc.data(), p.chunks.p, nc, s);
+      p.blob_bytes = nc ? hc[nc - 1].blob_off + hc[nc - 1].blob_bytes : 0;
       int64_t n_part = 0, n_lvl = 0;
       p.max_blob = p.max_chunk_nodes = p.max_chunk_beads = p.max_chunk_levels = p.max_chunk_res = 0;
       for (auto &d : hc) {
@@ -1306,7 +1306,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                   p.rec.as<double>(),
                   p.blob.as<uint8_t>()};
       if (n_part > 0) k_write_nodes<<<nblk(n_part), NT, 0, s>>>(wc, n_part);
-      k_write_perm<<<(unsigned)nc, 128, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, p.perm.as<int32_t>(),
+      if (nc) k_write_perm<<<(unsigned)nc, 128, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, p.perm.as<int32_t>(),
                                                   leaf_id.as<int32_t>(), noff, p.parent.as<int32_t>(),
                                                   p.start.as<int32_t>(), p.stop.as<int32_t>(), S,
                                                   p.blob.as<uint8_t>());
