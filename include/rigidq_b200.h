@@ -110,6 +110,15 @@ int rq_plan_device(const rq_plan *plan);
  */
 int rq_apply(const rq_plan *plan, int op, const double *in, double *out, int64_t k,
              void *stream);
+/* Phase-selective variant for profiling (bench.py times the chunk sweep
+ * alone): phases is a mask of RQ_PHASE_*; rq_apply == all phases. */
+#define RQ_PHASE_CHUNKS 1u
+#define RQ_PHASE_TOP 2u
+#define RQ_PHASE_SMALL 4u
+int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int64_t k,
+                void *stream, uint32_t phases);
+/* Number of kernel launches one rq_apply issues. */
+int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k);
 /* Same on HOST buffers: H2D copy, apply, D2H copy (synchronous). */
 int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, int64_t k);
 

@@ -490,10 +490,16 @@ static void matvec_kT(const double *om, int k, const double *x, double *y, int64
     }
 }
 
+static void upward_ws(const rqo_body *b, const double *v, double *out, int64_t K, double *m);
 void rqo_upward(const rqo_body *b, const double *v, double *out, int64_t K) {
+  double *m = (double *)malloc((size_t)(b->nn * 6 * K + 1) * sizeof(double));
+  upward_ws(b, v, out, K, m);
+  free(m);
+}
+/* m: caller-provided workspace of nn*6*K doubles (reused across bodies). */
+static void upward_ws(const rqo_body *b, const double *v, double *out, int64_t K, double *m) {
   int64_t n = b->n;
   if (n == 1) { memcpy(out, v, 3 * K * sizeof(double)); return; } /* matfree.py:99-100 */
-  double *m = (double *)xcalloc(b->nn * 6 * K, sizeof(double));
   double x[9 * 64], y[9 * 64];
   double *xb = K <= 64 ? x : (double *)malloc(9 * K * sizeof(double));
   double *yb = K <= 64 ? y : (double *)malloc(9 * K * sizeof(double));
@@ -535,13 +541,17 @@ void rqo_upward(const rqo_body *b, const double *v, double *out, int64_t K) {
   memcpy(out, &m[b->root * 6 * K], 6 * K * sizeof(double));
   if (xb != x) free(xb);
   if (yb != y) free(yb);
-  free(m);
 }
 
+static void downward_ws(const rqo_body *b, const double *w, double *out, int64_t K, double *l);
 void rqo_downward(const rqo_body *b, const double *w, double *out, int64_t K) {
+  double *l = (double *)malloc((size_t)(b->nn * 6 * K + 1) * sizeof(double));
+  downward_ws(b, w, out, K, l);
+  free(l);
+}
+static void downward_ws(const rqo_body *b, const double *w, double *out, int64_t K, double *l) {
   int64_t n = b->n;
   if (n == 1) { memcpy(out, w, 3 * K * sizeof(double)); return; } /* matfree.py:127-128 */
-  double *l = (double *)xcalloc(b->nn * 6 * K, sizeof(double));
   double x[9 * 64], u[9 * 64];
   double *xb = K <= 64 ? x : (double *)malloc(9 * K * sizeof(double));
   double *ub = K <= 64 ? u : (double *)malloc(9 * K * sizeof(double));
@@ -578,7 +588,6 @@ void rqo_downward(const rqo_body *b, const double *w, double *out, int64_t K) {
   }
   if (xb != x) free(xb);
   if (ub != u) free(ub);
-  free(l);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -614,26 +623,35 @@ int rqo_batch_apply(const rqo_batch *b, int op, const double *in, double *out,
   if (op >= 2)
     for (int64_t j = 0; j < b->m; j++)
       if (b->bodies[j].n < 2) return RQO_ERR_TOO_SMALL;
+  int64_t nmax = 1;
+  for (int64_t j = 0; j < b->m; j++) if (b->bodies[j].n > nmax) nmax = b->bodies[j].n;
 #ifdef _OPENMP
-#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+#pragma omp parallel num_threads(nthreads)
 #endif
-  for (int64_t j = 0; j < b->m; j++) {
-    const rqo_body *bd = &b->bodies[j];
-    int64_t n = bd->n, o = b->offsets[j];
-    int64_t full = 3 * o, comp = 3 * o - 6 * j;
-    if (op == 0) rqo_upward(bd, in + full * K, out + full * K, K);
-    else if (op == 1) rqo_downward(bd, in + full * K, out + full * K, K);
-    else if (op == 2) {
-      double *tmp = (double *)malloc(3 * n * K * sizeof(double));
-      rqo_upward(bd, in + full * K, tmp, K);
-      memcpy(out + comp * K, tmp + 6 * K, (3 * n - 6) * K * sizeof(double));
-      free(tmp);
-    } else {
-      double *tmp = (double *)calloc(3 * n * K, sizeof(double));
-      memcpy(tmp + 6 * K, in + comp * K, (3 * n - 6) * K * sizeof(double));
-      rqo_downward(bd, tmp, out + full * K, K);
-      free(tmp);
+  {
+    /* per-thread workspaces reused across bodies (no per-body page faults) */
+    double *ws = (double *)malloc((size_t)(2 * nmax * 6 * K + 1) * sizeof(double));
+    double *tmp = (double *)malloc((size_t)(3 * nmax * K + 1) * sizeof(double));
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 1)
+#endif
+    for (int64_t j = 0; j < b->m; j++) {
+      const rqo_body *bd = &b->bodies[j];
+      int64_t n = bd->n, o = b->offsets[j];
+      int64_t full = 3 * o, comp = 3 * o - 6 * j;
+      if (op == 0) upward_ws(bd, in + full * K, out + full * K, K, ws);
+      else if (op == 1) downward_ws(bd, in + full * K, out + full * K, K, ws);
+      else if (op == 2) {
+        upward_ws(bd, in + full * K, tmp, K, ws);
+        memcpy(out + comp * K, tmp + 6 * K, (3 * n - 6) * K * sizeof(double));
+      } else {
+        memset(tmp, 0, 6 * K * sizeof(double));
+        memcpy(tmp + 6 * K, in + comp * K, (3 * n - 6) * K * sizeof(double));
+        downward_ws(bd, tmp, out + full * K, K, ws);
+      }
     }
+    free(ws);
+    free(tmp);
   }
   (void)nthreads;
   return RQO_OK;

@@ -2,6 +2,7 @@
 // catches rq::Error / std::exception, records the message in a thread-local
 // slot (rq_last_error) and returns the matching RQ_ERR_* code.
 #include <cstring>
+#include <mutex>
 #include <exception>
 #include <new>
 #include <string>
@@ -142,6 +143,22 @@ int rq_apply(const rq_plan *plan, int op, const double *in, double *out, int64_t
   })
 }
 
+int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int64_t k, void *stream,
+                uint32_t phases) {
+  RQ_GUARD({
+    need_plan(plan);
+    if (!in || !out) throw rq::Error(RQ_ERR_VALUE, "null vector");
+    rq::run_apply(plan->p, op, in, out, k, static_cast<cudaStream_t>(stream), phases);
+  })
+}
+
+int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
+  if (!plan) return -1;
+  const rq::Plan &p = plan->p;
+  int per_col = (p.n_chunks ? 1 : 0) + (p.n_topbodies ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
+  return (int)(per_col * k);
+}
+
 int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, int64_t k) {
   RQ_GUARD({
     need_plan(plan);
@@ -149,13 +166,16 @@ int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, in
     if (op < 0 || op > 3) throw rq::Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
     if (k < 1) throw rq::Error(RQ_ERR_LENGTH, "k must be >= 1");
     RQ_CUDA(cudaSetDevice(p.device));
+    std::lock_guard<std::mutex> lock(p.host_mu);
+    if (!p.host_stream) RQ_CUDA(cudaStreamCreateWithFlags(&p.host_stream, cudaStreamNonBlocking));
     const size_t bi = (size_t)in_len(p, op) * k * 8, bo = (size_t)out_len(p, op) * k * 8;
-    rq::DBuf din, dout;
-    din.alloc(bi);
-    dout.alloc(bo);
-    RQ_CUDA(cudaMemcpy(din.p, in, bi, cudaMemcpyHostToDevice));
-    rq::run_apply(p, op, din.as<double>(), dout.as<double>(), k, 0);
-    RQ_CUDA(cudaMemcpy(out, dout.p, bo, cudaMemcpyDeviceToHost));
+    if (p.stage_in.bytes < bi) p.stage_in.alloc(bi);
+    if (p.stage_out.bytes < bo) p.stage_out.alloc(bo);
+    cudaStream_t s = p.host_stream;
+    RQ_CUDA(cudaMemcpyAsync(p.stage_in.p, in, bi, cudaMemcpyHostToDevice, s));
+    rq::run_apply(p, op, p.stage_in.as<double>(), p.stage_out.as<double>(), k, s);
+    RQ_CUDA(cudaMemcpyAsync(out, p.stage_out.p, bo, cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
   })
 }
 

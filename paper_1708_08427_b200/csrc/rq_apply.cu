@@ -383,7 +383,7 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
 
 }  // namespace
 
-void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s) {
+void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases) {
   if (op < 0 || op > 3) throw Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
   if (op >= 2 && p.min_n < 2)
     throw Error(RQ_ERR_BODY_TOO_SMALL, "complement operators need every body to have >= 2 beads");
@@ -422,14 +422,15 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   for (int64_t col = 0; col < k; col++) {
     a.col = col;
     t.col = col;
+    const bool do_chunks = (phases & 1u) && p.n_chunks, do_top = (phases & 2u) && p.n_topbodies;
     if (up) {
-      if (p.n_chunks) k_chunk<true><<<cfg.grid, NT_CHUNK, cfg.smem, s>>>(a);
-      if (p.n_topbodies) k_top<true><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
+      if (do_chunks) k_chunk<true><<<cfg.grid, NT_CHUNK, cfg.smem, s>>>(a);
+      if (do_top) k_top<true><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
     } else {
-      if (p.n_topbodies) k_top<false><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
-      if (p.n_chunks) k_chunk<false><<<cfg.grid, NT_CHUNK, cfg.smem, s>>>(a);
+      if (do_top) k_top<false><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
+      if (do_chunks) k_chunk<false><<<cfg.grid, NT_CHUNK, cfg.smem, s>>>(a);
     }
-    if (p.n_small && op <= 1)
+    if ((phases & 4u) && p.n_small && op <= 1)
       k_small<<<(unsigned)((3 * p.n_small + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>(), p.n_small,
                                                                       p.bead_off_d.as<int64_t>(), in, out, k, col);
   }

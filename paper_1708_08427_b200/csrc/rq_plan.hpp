@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -120,13 +121,21 @@ struct Plan {
   DBuf seg_begin;                  // int64 [n_seg + 1] bead ranges
   DBuf body_seg;                   // int64 [m + 1] segment CSR
   mutable DBuf zpart;              // double [6 * n_seg]
+  // host-buffer entry points: persistent device staging (grown on demand)
+  mutable DBuf stage_in, stage_out;
+  mutable cudaStream_t host_stream = nullptr;
 
+  mutable std::mutex host_mu;
   int64_t device_bytes() const;
+  ~Plan() {
+    if (host_stream) cudaStreamDestroy(host_stream);
+  }
 };
 
 void build_plan(Plan &p, const double *pos, const int64_t *offsets, int64_t m, int max_depth,
                 bool host_input, cudaStream_t s);
-void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s);
+void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
+               unsigned phases = 7u);
 void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, const double *origin_d,
            cudaStream_t s);
 int check_duplicates(const double *pos, const int64_t *offsets, int64_t m, bool host_input,

@@ -935,7 +935,7 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
