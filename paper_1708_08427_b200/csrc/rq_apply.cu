@@ -24,7 +24,6 @@
 namespace rq {
 namespace {
 
-constexpr int NT_CHUNK = 256;
 constexpr int NT_TOP = 128;
 
 // ---- PTX helpers: mbarrier + bulk copy ------------------------------------------
@@ -92,7 +91,65 @@ __device__ __forceinline__ void issue_chunk(const ApplyCtx &a, int64_t c, void *
   bulk_g2s(dst, a.blob + d->blob_off, bytes, bar);
 }
 
-template <bool UP>
+// one node of the upward sweep (merge_infosets, matfree.py:41-62)
+template <int CS>
+__device__ __forceinline__ void up_node(int slot, const double *rec, int st, const NodeMeta *ME, double *M,
+                                        const double *F, double *RES) {
+  const NodeMeta md = ME[slot];
+  double mx[6], my[6];
+  if (md.x & SRC_BEAD) {
+    const double *f = F + 3 * (md.x & 0x7fff);
+    mx[0] = f[0]; mx[1] = f[1]; mx[2] = f[2]; mx[3] = 0.0; mx[4] = 0.0; mx[5] = 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < 6; r++) mx[r] = M[6 * md.x + r];
+  }
+  if (CS != GENERAL && (md.y & SRC_BEAD)) {  // formula-y of BB / RB is always a bead
+    const double *f = F + 3 * (md.y & 0x7fff);
+    my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
+  } else {
+#pragma unroll
+    for (int r = 0; r < 6; r++) my[r] = M[6 * md.y + r];
+  }
+  double aa, bb, mp[6], res[6];
+  rec_ratios(CS, rec, st, aa, bb);
+  merge(CS, rec, st, flag_signs(md.flags), aa, bb, mx, my, mp, res);
+#pragma unroll
+  for (int r = 0; r < res_rows(CS); r++) RES[md.res + r] = res[r];
+#pragma unroll
+  for (int r = 0; r < 6; r++) M[6 * slot + r] = mp[r];
+}
+
+// one node of the downward sweep (split_rvset, matfree.py:65-83)
+template <int CS>
+__device__ __forceinline__ void down_node(int slot, const double *rec, int st, const NodeMeta *ME, double *M,
+                                          double *F, const double *RES) {
+  const NodeMeta md = ME[slot];
+  double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
+#pragma unroll
+  for (int r = 0; r < 6; r++) lp[r] = M[6 * slot + r];
+#pragma unroll
+  for (int r = 0; r < res_rows(CS); r++) res[r] = RES[md.res + r];
+  double aa, bb;
+  rec_ratios(CS, rec, st, aa, bb);
+  split(CS, rec, st, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
+  if (md.x & SRC_BEAD) {
+    double *f = F + 3 * (md.x & 0x7fff);
+    f[0] = lx[0]; f[1] = lx[1]; f[2] = lx[2];
+  } else {
+#pragma unroll
+    for (int r = 0; r < 6; r++) M[6 * md.x + r] = lx[r];
+  }
+  if (md.y & SRC_BEAD) {
+    double *f = F + 3 * (md.y & 0x7fff);
+    f[0] = ly[0]; f[1] = ly[1]; f[2] = ly[2];
+  } else {
+#pragma unroll
+    for (int r = 0; r < 6; r++) M[6 * md.y + r] = ly[r];
+  }
+}
+
+template <bool UP, int NT_CHUNK>
 __global__ void __launch_bounds__(NT_CHUNK) k_chunk(ApplyCtx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[2];
@@ -143,43 +200,19 @@ __global__ void __launch_bounds__(NT_CHUNK) k_chunk(ApplyCtx a) {
       __syncthreads();
       for (int h = 0; h < d.n_levels; h++) {
         const LevelDesc L = LV[h];
-        const int tot = L.nG + L.nR + L.nB;
+        // case-uniform warps: each case group is padded to whole warps
+        const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
+        const int tot = gG + gR + L.nB;
         for (int q = tid; q < tot; q += NT_CHUNK) {
-          const int slot = L.slot_begin + q;
-          const NodeMeta md = ME[slot];
-          double mx[6], my[6];
-          if (md.x & SRC_BEAD) {
-            const double *f = F + 3 * (md.x & 0x7fff);
-            mx[0] = f[0]; mx[1] = f[1]; mx[2] = f[2]; mx[3] = 0.0; mx[4] = 0.0; mx[5] = 0.0;
+          if (q < gG) {
+            if (q < L.nG) up_node<GENERAL>(L.slot_begin + q, REC + L.recG + q, L.nG, ME, M, F, RES);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < L.nR) up_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, REC + L.recR + qq, L.nR, ME, M, F, RES);
           } else {
-#pragma unroll
-            for (int r = 0; r < 6; r++) mx[r] = M[6 * md.x + r];
+            const int qq = q - gG - gR;
+            up_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, REC + L.recB + qq, L.nB, ME, M, F, RES);
           }
-          if (md.y & SRC_BEAD) {
-            const double *f = F + 3 * (md.y & 0x7fff);
-            my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
-          } else {
-#pragma unroll
-            for (int r = 0; r < 6; r++) my[r] = M[6 * md.y + r];
-          }
-          double aa, bb;
-          ratios(md.nx, md.ny, aa, bb);
-          const unsigned signs = flag_signs(md.flags);
-          double mp[6], res[6];
-          if (q < L.nG) {
-            merge(GENERAL, REC + L.recG + q, L.nG, signs, aa, bb, mx, my, mp, res);
-#pragma unroll
-            for (int r = 0; r < 6; r++) RES[md.res + r] = res[r];
-          } else if (q < L.nG + L.nR) {
-            const int qq = q - L.nG;
-            merge(RIGID_BEAD, REC + L.recR + qq, L.nR, signs, aa, bb, mx, my, mp, res);
-            RES[md.res + 0] = res[0]; RES[md.res + 1] = res[1]; RES[md.res + 2] = res[2];
-          } else {
-            const int qq = q - L.nG - L.nR;
-            merge(BEAD_BEAD, REC + L.recB + qq, L.nB, signs, aa, bb, mx, my, mp, res);
-          }
-#pragma unroll
-          for (int r = 0; r < 6; r++) M[6 * slot + r] = mp[r];
         }
         __syncthreads();
       }
@@ -209,41 +242,17 @@ __global__ void __launch_bounds__(NT_CHUNK) k_chunk(ApplyCtx a) {
       __syncthreads();
       for (int h = d.n_levels - 1; h >= 0; h--) {
         const LevelDesc L = LV[h];
-        const int tot = L.nG + L.nR + L.nB;
+        const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
+        const int tot = gG + gR + L.nB;
         for (int q = tid; q < tot; q += NT_CHUNK) {
-          const int slot = L.slot_begin + q;
-          const NodeMeta md = ME[slot];
-          double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
-#pragma unroll
-          for (int r = 0; r < 6; r++) lp[r] = M[6 * slot + r];
-          double aa, bb;
-          ratios(md.nx, md.ny, aa, bb);
-          const unsigned signs = flag_signs(md.flags);
-          if (q < L.nG) {
-#pragma unroll
-            for (int r = 0; r < 6; r++) res[r] = RES[md.res + r];
-            split(GENERAL, REC + L.recG + q, L.nG, signs, aa, bb, lp, res, lx, ly);
-          } else if (q < L.nG + L.nR) {
-            const int qq = q - L.nG;
-            res[0] = RES[md.res + 0]; res[1] = RES[md.res + 1]; res[2] = RES[md.res + 2];
-            split(RIGID_BEAD, REC + L.recR + qq, L.nR, signs, aa, bb, lp, res, lx, ly);
+          if (q < gG) {
+            if (q < L.nG) down_node<GENERAL>(L.slot_begin + q, REC + L.recG + q, L.nG, ME, M, F, RES);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < L.nR) down_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, REC + L.recR + qq, L.nR, ME, M, F, RES);
           } else {
-            const int qq = q - L.nG - L.nR;
-            split(BEAD_BEAD, REC + L.recB + qq, L.nB, signs, aa, bb, lp, res, lx, ly);
-          }
-          if (md.x & SRC_BEAD) {
-            double *f = F + 3 * (md.x & 0x7fff);
-            f[0] = lx[0]; f[1] = lx[1]; f[2] = lx[2];
-          } else {
-#pragma unroll
-            for (int r = 0; r < 6; r++) M[6 * md.x + r] = lx[r];
-          }
-          if (md.y & SRC_BEAD) {
-            double *f = F + 3 * (md.y & 0x7fff);
-            f[0] = ly[0]; f[1] = ly[1]; f[2] = ly[2];
-          } else {
-#pragma unroll
-            for (int r = 0; r < 6; r++) M[6 * md.y + r] = ly[r];
+            const int qq = q - gG - gR;
+            down_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, REC + L.recB + qq, L.nB, ME, M, F, RES);
           }
         }
         __syncthreads();
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top(TopCtx a) {
       const unsigned signs = flag_signs(T.flags);
       const double *rec = a.rec + T.rec_off;
       double aa, bb;
-      ratios(T.nx, T.ny, aa, bb);
+      rec_ratios(cs, rec, 1, aa, bb);
       const int rr = res_rows(cs);
       if (UP) {
         double mx[6], my[6], mp[6], res[6];
@@ -358,9 +367,20 @@ __global__ void k_small(const int32_t *bodies, int64_t n, const int64_t *bead_of
 }
 
 struct KernelCfg {
-  int grid = 0;
+  int grid = 0, threads = 128;
   size_t smem = 0;
+  void (*fn)(ApplyCtx) = nullptr;
 };
+
+template <bool UP>
+void (*chunk_fn(int nt))(ApplyCtx) {
+  switch (nt) {
+    case 32: return k_chunk<UP, 32>;
+    case 64: return k_chunk<UP, 64>;
+    case 256: return k_chunk<UP, 256>;
+    default: return k_chunk<UP, 128>;
+  }
+}
 
 KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   int dev = p.device;
@@ -371,11 +391,12 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   a.max_beads = std::max(1, p.max_chunk_beads);
   a.max_res = std::max(1, p.max_chunk_res);
   KernelCfg cfg;
+  cfg.threads = p.chunk_threads;
   cfg.smem = 2 * (size_t)a.buf_bytes + 8 * (6 * (size_t)a.max_nodes + 3 * (size_t)a.max_beads + (size_t)a.max_res);
-  const void *fn = up ? (const void *)k_chunk<true> : (const void *)k_chunk<false>;
-  RQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
+  cfg.fn = up ? chunk_fn<true>(cfg.threads) : chunk_fn<false>(cfg.threads);
+  RQ_CUDA(cudaFuncSetAttribute((const void *)cfg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   int occ = 0;
-  RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, NT_CHUNK, cfg.smem));
+  RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)cfg.fn, cfg.threads, cfg.smem));
   if (occ < 1) throw Error(RQ_ERR_CUDA, "chunk kernel does not fit on an SM (smem " + std::to_string(cfg.smem) + ")");
   cfg.grid = (int)std::min<int64_t>(p.n_chunks, (int64_t)sms * occ);
   return cfg;
@@ -424,11 +445,11 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     t.col = col;
     const bool do_chunks = (phases & 1u) && p.n_chunks, do_top = (phases & 2u) && p.n_topbodies;
     if (up) {
-      if (do_chunks) k_chunk<true><<<cfg.grid, NT_CHUNK, cfg.smem, s>>>(a);
+      if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
       if (do_top) k_top<true><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
     } else {
       if (do_top) k_top<false><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
-      if (do_chunks) k_chunk<false><<<cfg.grid, NT_CHUNK, cfg.smem, s>>>(a);
+      if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
     }
     if ((phases & 4u) && p.n_small && op <= 1)
       k_small<<<(unsigned)((3 * p.n_small + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>(), p.n_small,

@@ -25,10 +25,12 @@ __host__ __device__ inline int flag_case(unsigned f) { return f & 3u; }
 __host__ __device__ inline bool flag_swapped(unsigned f) { return (f >> 2) & 1u; }
 __host__ __device__ inline unsigned flag_signs(unsigned f) { return (f >> 3) & 7u; }
 
-__host__ __device__ inline int rec_size(int c) {
-  return c == BEAD_BEAD ? 9 : (c == RIGID_BEAD ? 15 : (c == GENERAL ? 24 : 0));
+// compact record sizes (doubles): BEAD_BEAD explicit 3x3 g; RIGID_BEAD /
+// GENERAL Householder record (HH<6> / HH<9>) followed by the ratios a, b.
+__host__ __device__ constexpr int rec_size(int c) {
+  return c == BEAD_BEAD ? 9 : (c == RIGID_BEAD ? 17 : (c == GENERAL ? 26 : 0));
 }
-__host__ __device__ inline int res_rows(int c) {
+__host__ __device__ constexpr int res_rows(int c) {
   return c == RIGID_BEAD ? 3 : (c == GENERAL ? 6 : 0);
 }
 
@@ -41,12 +43,10 @@ struct LevelDesc {       // one height level of a chunk, 32 bytes
   int32_t pad;
 };
 
-struct NodeMeta {        // 16 bytes, one per in-chunk internal node (slot order)
+struct NodeMeta {        // 8 bytes, one per in-chunk internal node (slot order)
   uint16_t x, y;         // formula-x/-y child: bit 15 set -> bead (local index), else slot
   uint16_t res;          // residue offset in the chunk staging buffer
   uint16_t flags;        // case | swapped | signs
-  uint16_t nx, ny;       // formula bead counts (ratios, NodeFactor.ratios)
-  uint32_t spare;
 };
 
 struct ChunkDesc {
@@ -108,6 +108,9 @@ __host__ __device__ __forceinline__ void householder(double (&y)[K], const doubl
 template <int K>
 struct HH {
   static constexpr int O0 = 0, O1 = K - 1, O2 = 2 * K - 3, OT = 3 * K - 6, SIZE = 3 * K - 3;
+  static constexpr int RA = SIZE, RB = SIZE + 1;  // ratios a = sqrt(n_x/n), b = sqrt(n_y/n)
 };
+// NodeFactor.ratios of a BEAD_BEAD node: sqrt(1/2) (factor.py:85-87)
+constexpr double BB_RATIO = 0.70710678118654757;
 
 }  // namespace rq

@@ -11,10 +11,14 @@ namespace rq {
 // Apply H_i (reflector stored at rec[(o + e) * st], e = 0 .. K-i-2) to y.
 template <int K>
 __device__ __forceinline__ void hh_s(double (&y)[K], const double *rec, int st, int o, double tau, int i) {
-  double d = y[i];
+  // two interleaved partial dot products: halves the dependent FMA chain
+  double d0 = y[i], d1 = 0.0;
 #pragma unroll
-  for (int j = i + 1; j < K; j++) d = fma(rec[(o + j - i - 1) * st], y[j], d);
-  double td = tau * d;
+  for (int j = i + 1; j < K; j++) {
+    if ((j - i) & 1) d1 = fma(rec[(o + j - i - 1) * st], y[j], d1);
+    else d0 = fma(rec[(o + j - i - 1) * st], y[j], d0);
+  }
+  const double td = tau * (d0 + d1);
   y[i] -= td;
 #pragma unroll
   for (int j = i + 1; j < K; j++) y[j] = fma(-td, rec[(o + j - i - 1) * st], y[j]);
@@ -42,6 +46,13 @@ __device__ __forceinline__ void omega_t_s(const double *rec, int st, unsigned si
   hh_s<K>(y, rec, st, HH<K>::O2, t2, 2);
   hh_s<K>(y, rec, st, HH<K>::O1, t1, 1);
   hh_s<K>(y, rec, st, HH<K>::O0, t0, 0);
+}
+
+// ratios stored in the record (RIGID_BEAD / GENERAL) or the BEAD_BEAD constant
+__device__ __forceinline__ void rec_ratios(int cs, const double *rec, int st, double &a, double &b) {
+  if (cs == GENERAL) { a = rec[HH<9>::RA * st]; b = rec[HH<9>::RB * st]; }
+  else if (cs == RIGID_BEAD) { a = rec[HH<6>::RA * st]; b = rec[HH<6>::RB * st]; }
+  else { a = BB_RATIO; b = BB_RATIO; }
 }
 
 __device__ __forceinline__ void ratios(int nx, int ny, double &a, double &b) {

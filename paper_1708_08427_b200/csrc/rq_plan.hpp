@@ -73,6 +73,7 @@ struct Plan {
   int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
   int max_depth = 96;
   int tile_leaves = 128;           // S
+  int chunk_threads = 128;         // threads per chunk CTA
   int64_t max_blob = 0;            // largest chunk blob (bytes)
   int max_chunk_nodes = 0, max_chunk_beads = 0, max_chunk_levels = 0, max_chunk_res = 0;
   std::vector<int64_t> bead_off;   // host copy, m+1

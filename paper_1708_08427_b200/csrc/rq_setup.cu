@@ -408,6 +408,8 @@ __global__ void k_factor(FactorCtx c, int64_t N) {
       double hh[HH<6>::SIZE];
       lq_factor<6>(cpl, t6, hh, signs);
       for (int a = 0; a < HH<6>::SIZE; a++) rec[a] = hh[a];
+      rec[HH<6>::RA] = sqrt((double)nx / (double)n);  // NodeFactor.ratios (factor.py:85-87)
+      rec[HH<6>::RB] = sqrt(1.0 / (double)n);
     } else {  // factor.py:237-243, 181-188
       double dr[3], R[9];
       for (int a = 0; a < 3; a++) dr[a] = cl[a] - cp[a];
@@ -423,6 +425,8 @@ __global__ void k_factor(FactorCtx c, int64_t N) {
       double hh[HH<9>::SIZE];
       lq_factor<9>(cpl, t6, hh, signs);
       for (int a = 0; a < HH<9>::SIZE; a++) rec[a] = hh[a];
+      rec[HH<9>::RA] = sqrt((double)nl / (double)n);
+      rec[HH<9>::RB] = sqrt((double)nr / (double)n);
     }
     for (int a = 0; a < 3; a++) c.centroid[g * 3 + a] = cp[a];
     for (int a = 0; a < 6; a++) c.t22[g * 6 + a] = t6[a];
@@ -495,7 +499,8 @@ struct ChunkLimits {
 
 __host__ __device__ inline int64_t blob_bytes_of(int H, int nodes, int beads, int64_t rec) {
   int64_t perm = ((int64_t)beads * 4 + 15) / 16 * 16;
-  int64_t b = (int64_t)H * 32 + (int64_t)nodes * 16 + perm + rec * 8;
+  nodes = (nodes + 1) / 2 * 2;  // meta section padded to 16 bytes
+  int64_t b = (int64_t)H * 32 + (int64_t)nodes * 8 + perm + rec * 8;
   return (b + 15) / 16 * 16;
 }
 
@@ -525,7 +530,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
       d.tile_begin = big_scan[tile0];
       d.n_res = res;
       d.off_meta = H * 32;
-      d.off_perm = d.off_meta + nodes * 16;
+      d.off_perm = d.off_meta + (nodes * 8 + 15) / 16 * 16;
       // n_beads, off_rec and blob_bytes set by the caller below
     }
     nch++;
@@ -546,7 +551,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
           ChunkDesc &d = chunks[chunk_base[j] + nch];
           d.n_beads = last_stop - bead0;
           int64_t pb = ((int64_t)d.n_beads * 4 + 15) / 16 * 16;
-          d.off_rec = (int32_t)(H * 32 + nodes * 16 + pb);
+          d.off_rec = (int32_t)(H * 32 + (nodes * 8 + 15) / 16 * 16 + pb);
           d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec);
         }
         flush();
@@ -571,7 +576,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
     ChunkDesc &d = chunks[chunk_base[j] + nch];
     d.n_beads = last_stop - bead0;
     int64_t pb = ((int64_t)d.n_beads * 4 + 15) / 16 * 16;
-    d.off_rec = (int32_t)(H * 32 + nodes * 16 + pb);
+    d.off_rec = (int32_t)(H * 32 + (nodes * 8 + 15) / 16 * 16 + pb);
     d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec);
   }
   flush();
@@ -633,8 +638,8 @@ __global__ void k_levels_finalize(const ChunkDesc *chunks, int64_t nc, const int
   for (int h = 0; h < d.n_levels; h++) {
     LevelDesc &L = lvl[lvl_base[c] + h];
     L.slot_begin = slot;
-    L.recG = recd; recd += 24 * L.nG;
-    L.recR = recd; recd += 15 * L.nR;
+    L.recG = recd; recd += 26 * L.nG;
+    L.recR = recd; recd += 17 * L.nR;
     L.recB = recd; recd += 9 * L.nB;
     L.pad = 0;
     slot += L.nG + L.nR + L.nB;
@@ -686,19 +691,16 @@ __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
   int tile_idx = w.tile_of[g];
   md.res = (uint16_t)(w.res_local_of_tile[tile_idx] + (w.c.res_off[g] - 6 - T.res_q));
   md.flags = (uint16_t)f;
-  md.nx = (uint16_t)(w.c.stop[nb + xi] - w.c.start[nb + xi]);
-  md.ny = (uint16_t)(w.c.stop[nb + yi] - w.c.start[nb + yi]);
-  md.spare = 0;
   uint8_t *base = w.blob + d.blob_off;
   reinterpret_cast<NodeMeta *>(base + d.off_meta)[slot] = md;
   double *R = reinterpret_cast<double *>(base + d.off_rec);
   int q = slot - L.slot_begin;
   const double *src = w.rec + w.c.rec_off[g];
   if (cs == GENERAL) {
-    for (int e = 0; e < 24; e++) R[L.recG + e * L.nG + q] = src[e];
+    for (int e = 0; e < 26; e++) R[L.recG + e * L.nG + q] = src[e];
   } else if (cs == RIGID_BEAD) {
     q -= L.nG;
-    for (int e = 0; e < 15; e++) R[L.recR + e * L.nR + q] = src[e];
+    for (int e = 0; e < 17; e++) R[L.recR + e * L.nR + q] = src[e];
   } else {
     q -= L.nG + L.nR;
     for (int e = 0; e < 9; e++) R[L.recB + e * L.nB + q] = src[e];
@@ -957,6 +959,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
   if (max_depth < 1 || max_depth + body_bits > 128)
     throw Error(RQ_ERR_VALUE, "max_depth must be in [1, 128 - ceil(log2 m)]");
   if (const char *e = getenv("RQ_TILE_LEAVES")) p.tile_leaves = std::min(1024, std::max(2, atoi(e)));
+  if (const char *e = getenv("RQ_CHUNK_THREADS")) p.chunk_threads = atoi(e);
   p.m = m;
   p.N = N;
   p.NN = 2 * N - m;
@@ -1210,7 +1213,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     lim.max_bytes = 32 * 1024;
     if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
     // a single worst-case tile (all GENERAL nodes) must fit a chunk
-    lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, 24 * (S - 1)));
+    lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, 26 * (S - 1)));
     lim.max_nodes = 1024;
     lim.max_beads = 1024;
     lim.max_res = 3 * 1024;
