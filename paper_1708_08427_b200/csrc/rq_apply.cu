@@ -17,6 +17,8 @@
 // orthogonal transforms (~0.3-0.6 flop/B).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "rq_nodeops.cuh"
 #include "rq_plan.hpp"
@@ -76,151 +78,367 @@ struct ApplyCtx {
   int64_t k, col;
   double *scratch;
   int op;
-  int buf_bytes, max_nodes, max_beads, max_res;
+  int head_bytes, lrec_bytes, max_nodes, max_beads, max_res, max_tiles;
+  long long *dbg;  // phase timers, only with -DRQ_TIMING (8 per CTA)
 };
+
+#ifndef RQ_TIMING
+#define RQ_TIMING 0
+#endif
 
 __device__ __forceinline__ int64_t spec_base(int op, const int64_t *bead_off, int j) {
   // first residue row of body j in the op's spectral layout
   return (op == RQ_OP_QV || op == RQ_OP_QTV) ? 3 * bead_off[j] + 6 : 3 * bead_off[j] - 6 * (int64_t)j;
 }
 
-__device__ __forceinline__ void issue_chunk(const ApplyCtx &a, int64_t c, void *dst, uint64_t *bar) {
-  const ChunkDesc *d = &a.chunks[c];
-  unsigned bytes = (unsigned)d->blob_bytes;
-  mbar_expect_tx(bar, bytes);
-  bulk_g2s(dst, a.blob + d->blob_off, bytes, bar);
+// record -> registers with 16-byte loads (records are 16-byte aligned, AoS)
+template <int CS>
+__device__ __forceinline__ void load_rec(const double *rec, double (&R)[rec_size(CS)]) {
+  const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+#pragma unroll
+  for (int i = 0; i < rec_size(CS) / 2; i++) {
+    const double2 v = r2[i];
+    R[2 * i] = v.x;
+    R[2 * i + 1] = v.y;
+  }
+}
+
+__device__ __forceinline__ void load6(const double *p, double (&v)[6]) {
+  const double2 *p2 = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    const double2 w = p2[i];
+    v[2 * i] = w.x;
+    v[2 * i + 1] = w.y;
+  }
+}
+
+__device__ __forceinline__ void store6(double *p, const double (&v)[6]) {
+  double2 *p2 = reinterpret_cast<double2 *>(p);
+#pragma unroll
+  for (int i = 0; i < 3; i++) p2[i] = make_double2(v[2 * i], v[2 * i + 1]);
 }
 
 // one node of the upward sweep (merge_infosets, matfree.py:41-62)
 template <int CS>
-__device__ __forceinline__ void up_node(int slot, const double *rec, int st, const NodeMeta *ME, double *M,
-                                        const double *F, double *RES) {
+__device__ __forceinline__ void up_node(int slot, const double *rec, const NodeMeta *ME, double *M, const double *F,
+                                        double *RES) {
+  double R[rec_size(CS)];
+  load_rec<CS>(rec, R);
   const NodeMeta md = ME[slot];
   double mx[6], my[6];
-  if (md.x & SRC_BEAD) {
+  if (CS == BEAD_BEAD) {  // both children are beads
     const double *f = F + 3 * (md.x & 0x7fff);
     mx[0] = f[0]; mx[1] = f[1]; mx[2] = f[2]; mx[3] = 0.0; mx[4] = 0.0; mx[5] = 0.0;
   } else {
-#pragma unroll
-    for (int r = 0; r < 6; r++) mx[r] = M[6 * md.x + r];
+    load6(M + 6 * md.x, mx);
   }
-  if (CS != GENERAL && (md.y & SRC_BEAD)) {  // formula-y of BB / RB is always a bead
+  if (CS != GENERAL) {  // formula-y of BB / RB is a bead
     const double *f = F + 3 * (md.y & 0x7fff);
     my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
   } else {
-#pragma unroll
-    for (int r = 0; r < 6; r++) my[r] = M[6 * md.y + r];
+    load6(M + 6 * md.y, my);
   }
   double aa, bb, mp[6], res[6];
-  rec_ratios(CS, rec, st, aa, bb);
-  merge(CS, rec, st, flag_signs(md.flags), aa, bb, mx, my, mp, res);
+  rec_ratios(CS, R, 1, aa, bb);
+  merge(CS, R, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
+  if (CS == GENERAL) {
 #pragma unroll
-  for (int r = 0; r < res_rows(CS); r++) RES[md.res + r] = res[r];
-#pragma unroll
-  for (int r = 0; r < 6; r++) M[6 * slot + r] = mp[r];
+    for (int r = 0; r < 6; r++) RES[md.res + r] = res[r];  // residue offsets are 8-byte aligned only
+  } else if (CS == RIGID_BEAD) {
+    RES[md.res + 0] = res[0]; RES[md.res + 1] = res[1]; RES[md.res + 2] = res[2];
+  }
+  store6(M + 6 * slot, mp);
 }
 
 // one node of the downward sweep (split_rvset, matfree.py:65-83)
 template <int CS>
-__device__ __forceinline__ void down_node(int slot, const double *rec, int st, const NodeMeta *ME, double *M,
-                                          double *F, const double *RES) {
+__device__ __forceinline__ void down_node(int slot, const double *rec, const NodeMeta *ME, double *M, double *F,
+                                          const double *RES) {
+  double R[rec_size(CS)];
+  load_rec<CS>(rec, R);
   const NodeMeta md = ME[slot];
   double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
+  load6(M + 6 * slot, lp);
+  if (CS == GENERAL) {
 #pragma unroll
-  for (int r = 0; r < 6; r++) lp[r] = M[6 * slot + r];
-#pragma unroll
-  for (int r = 0; r < res_rows(CS); r++) res[r] = RES[md.res + r];
+    for (int r = 0; r < 6; r++) res[r] = RES[md.res + r];
+  }
+  else if (CS == RIGID_BEAD) { res[0] = RES[md.res]; res[1] = RES[md.res + 1]; res[2] = RES[md.res + 2]; }
   double aa, bb;
-  rec_ratios(CS, rec, st, aa, bb);
-  split(CS, rec, st, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
-  if (md.x & SRC_BEAD) {
+  rec_ratios(CS, R, 1, aa, bb);
+  split(CS, R, 1, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
+  if (CS == BEAD_BEAD) {
     double *f = F + 3 * (md.x & 0x7fff);
     f[0] = lx[0]; f[1] = lx[1]; f[2] = lx[2];
   } else {
-#pragma unroll
-    for (int r = 0; r < 6; r++) M[6 * md.x + r] = lx[r];
+    store6(M + 6 * md.x, lx);
   }
-  if (md.y & SRC_BEAD) {
+  if (CS != GENERAL) {
     double *f = F + 3 * (md.y & 0x7fff);
     f[0] = ly[0]; f[1] = ly[1]; f[2] = ly[2];
   } else {
-#pragma unroll
-    for (int r = 0; r < 6; r++) M[6 * md.y + r] = ly[r];
+    store6(M + 6 * md.y, ly);
   }
 }
 
-template <bool UP, int NT_CHUNK>
-__global__ void __launch_bounds__(NT_CHUNK) k_chunk(ApplyCtx a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[2];
-  const int tid = threadIdx.x;
-  unsigned char *buf0 = smem, *buf1 = smem + a.buf_bytes;
-  double *M = reinterpret_cast<double *>(smem + 2 * a.buf_bytes);
-  double *F = M + 6 * a.max_nodes;
-  double *RES = F + 3 * a.max_beads;
+__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Shared-memory map of the chunk kernels (all offsets 128-byte aligned):
+//   3 head stages (ChunkDesc | TileDesc[] | LevelDesc[] | NodeMeta[] | perm[])
+//   2 level-record stages (one height level's records at a time)
+//   2 vector stages (UP: gathered forces; DOWN: gathered residues)
+//   M (6 per node) | X (UP: residues; DOWN: velocities) | 2 tile-root stages
+// Pointers are derived arithmetically from the extern __shared__ base inside
+// the kernel (never stored in arrays) so every access compiles to LDS/STS.
+struct SmemMap {
+  uint32_t head, lrec, v, x, root;  // section sizes (bytes)
+  uint32_t o_lrec, o_v, o_m, o_x, o_root;
+};
+
+__host__ __device__ __forceinline__ size_t al128(size_t x) { return (x + 127) / 128 * 128; }
+
+__host__ __device__ __forceinline__ SmemMap smem_map(int head_bytes, int lrec_bytes, int max_beads, int max_res,
+                                                     int max_nodes, int max_tiles, bool up) {
+  SmemMap m;
+  m.head = (uint32_t)al128(head_bytes);
+  m.lrec = (uint32_t)al128(lrec_bytes);
+  m.v = (uint32_t)al128(8 * (size_t)(up ? 3 * max_beads : max_res));
+  m.x = (uint32_t)al128(8 * (size_t)(up ? max_res : 3 * max_beads));
+  m.root = (uint32_t)al128(48 * (size_t)max_tiles);
+  m.o_lrec = 3 * m.head;
+  m.o_v = m.o_lrec + 2 * m.lrec;
+  m.o_m = m.o_v + 2 * m.v;
+  m.o_x = m.o_m + (uint32_t)al128(48 * (size_t)max_nodes);
+  m.o_root = m.o_x + m.x;
+  return m;
+}
+
+__host__ __device__ inline size_t smem_total(const SmemMap &m) { return m.o_root + 2 * (size_t)m.root; }
+
+struct ChunkView {
+  const ChunkDesc *hdr;
+  const TileDesc *tiles;
+  const LevelDesc *LV;
+  const NodeMeta *ME;
+  const uint32_t *PERM;
+};
+
+__device__ __forceinline__ ChunkView view(const unsigned char *B) {
+  ChunkView v;
+  v.hdr = reinterpret_cast<const ChunkDesc *>(B);
+  v.tiles = reinterpret_cast<const TileDesc *>(B + sizeof(ChunkDesc));
+  v.LV = reinterpret_cast<const LevelDesc *>(B + sizeof(ChunkDesc) + sizeof(TileDesc) * v.hdr->n_tiles);
+  v.ME = reinterpret_cast<const NodeMeta *>(B + v.hdr->off_meta);
+  v.PERM = reinterpret_cast<const uint32_t *>(B + v.hdr->off_perm);
+  return v;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Stage the vector data a chunk needs, asynchronously (cp.async, one group):
+//   UP  : the chunk's bead forces, gathered through perm
+//   DOWN: the chunk's residue coefficients (contiguous per tile) + tile-root RV-sets
+template <bool UP, int NT>
+__device__ __forceinline__ void prefetch_vectors(const ApplyCtx &a, const unsigned char *B, double *V, double *ROOT) {
+  const ChunkView cv = view(B);
+  const ChunkDesc &d = *cv.hdr;
+  const int64_t bead0 = a.bead_off[d.body];
   const int64_t K = a.k, col = a.col;
+  if (UP) {
+    for (int i = threadIdx.x; i < d.n_beads; i += NT) {
+      const uint32_t pp = cv.PERM[i];
+      if (!(pp & PERM_FOREIGN)) {
+        const int64_t row = (bead0 + pp) * 3;
+        cp_async8(V + 3 * i + 0, a.in + (row + 0) * K + col);
+        cp_async8(V + 3 * i + 1, a.in + (row + 1) * K + col);
+        cp_async8(V + 3 * i + 2, a.in + (row + 2) * K + col);
+      }
+    }
+  } else {
+    const int64_t sbase = spec_base(a.op, a.bead_off, d.body);
+    for (int t = 0; t < d.n_tiles; t++) {
+      const TileDesc T = cv.tiles[t];
+      for (int r = threadIdx.x; r < T.res_count; r += NT)
+        cp_async8(V + T.res_local + r, a.in + (sbase + T.res_q + r) * K + col);
+      if (threadIdx.x < 6) {
+        if (T.scratch >= 0) cp_async8(ROOT + 6 * t + threadIdx.x, a.scratch + 6 * (int64_t)T.scratch + threadIdx.x);
+        else if (a.op == RQ_OP_QTV) cp_async8(ROOT + 6 * t + threadIdx.x, a.in + (3 * bead0 + threadIdx.x) * K + col);
+        else ROOT[6 * t + threadIdx.x] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+__device__ __forceinline__ int level_rec_doubles(const LevelDesc &L) {
+  return rec_size(GENERAL) * L.nG + rec_size(RIGID_BEAD) * L.nR + rec_size(BEAD_BEAD) * L.nB;
+}
+
+// Persistent chunk sweep.  Pipeline per CTA:
+//   * chunk k+2: head (desc | tiles | levels | meta | perm) TMA-copied to smem,
+//                records prefetched into L2 (cp.async.bulk.prefetch.L2)
+//   * chunk k+1: vectors staged with cp.async
+//   * chunk k  : swept level by level; the records of level h+1 are TMA-copied
+//                (from L2) into the second record stage while level h runs.
+template <bool UP, int NT>
+__global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[5];  // 0-2 heads, 3-4 level records
+  const int tid = threadIdx.x;
+  const SmemMap SM = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, UP);
+#define HEAD(i) (smem + (size_t)(i) * SM.head)
+#define LREC(i) reinterpret_cast<double *>(smem + SM.o_lrec + (size_t)(i) * SM.lrec)
+#define VBUF(i) reinterpret_cast<double *>(smem + SM.o_v + (size_t)(i) * SM.v)
+#define ROOTBUF(i) reinterpret_cast<double *>(smem + SM.o_root + (size_t)(i) * SM.root)
+  const int64_t K = a.k, col = a.col;
+  const int64_t G = gridDim.x;
+  const int64_t cnt = a.n_chunks > blockIdx.x ? (a.n_chunks - blockIdx.x + G - 1) / G : 0;
+  if (cnt == 0) return;
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < 5; i++) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  int64_t c = blockIdx.x;
-  if (c < a.n_chunks && tid == 0) issue_chunk(a, c, buf0, &bar[0]);
-  unsigned phase0 = 0, phase1 = 0;
-  for (int it = 0; c < a.n_chunks; c += gridDim.x, it++) {
-    const int b = it & 1;
-    const int64_t cn = c + gridDim.x;
-    if (cn < a.n_chunks && tid == 0) {
-      fence_proxy_async();
-      issue_chunk(a, cn, b ? buf0 : buf1, b ? &bar[0] : &bar[1]);
+  if (tid == 0) {
+    for (int64_t k = 0; k < 3 && k < cnt; k++) {
+      const ChunkDesc *d = &a.chunks[blockIdx.x + k * G];
+      const int64_t off = d->blob_off;
+      const unsigned hb = (unsigned)d->off_rec, rb = (unsigned)d->blob_bytes - hb;
+      if (rb) prefetch_l2(a.blob + off + hb, rb);
+      if (k < 2) {
+        mbar_expect_tx(&bar[k], hb);
+        bulk_g2s(HEAD(k), a.blob + off, hb, &bar[k]);
+      }
     }
-    const ChunkDesc d = a.chunks[c];
-    const int j = d.body;
-    const int64_t bead0 = a.bead_off[j];
-    const int64_t sbase = spec_base(a.op, a.bead_off, j);
-    if (b) { mbar_wait(&bar[1], phase1); phase1 ^= 1u; }
-    else { mbar_wait(&bar[0], phase0); phase0 ^= 1u; }
-    const unsigned char *B = b ? buf1 : buf0;
-    const LevelDesc *LV = reinterpret_cast<const LevelDesc *>(B);
-    const NodeMeta *ME = reinterpret_cast<const NodeMeta *>(B + d.off_meta);
-    const uint32_t *PERM = reinterpret_cast<const uint32_t *>(B + d.off_perm);
-    const double *REC = reinterpret_cast<const double *>(B + d.off_rec);
-
-    if (UP) {
-      for (int i = tid; i < d.n_beads; i += NT_CHUNK) {
-        uint32_t pp = PERM[i];
-        if (!(pp & PERM_FOREIGN)) {
-          const int64_t row = (bead0 + pp) * 3;
-          F[i * 3 + 0] = a.in[(row + 0) * K + col];
-          F[i * 3 + 1] = a.in[(row + 1) * K + col];
-          F[i * 3 + 2] = a.in[(row + 2) * K + col];
+  }
+  unsigned phase = 0;  // parity bit per barrier
+  int64_t lctr = 0;    // level steps so far (selects the record stage)
+  mbar_wait(&bar[0], 0);
+  phase ^= 1u;
+  prefetch_vectors<UP, NT>(a, HEAD(0), VBUF(0), ROOTBUF(0));
+  if (tid == 0) {  // first level of chunk 0
+    const ChunkView cv0 = view(HEAD(0));
+    const ChunkDesc &d0 = *cv0.hdr;
+    const LevelDesc L0 = cv0.LV[UP ? 0 : d0.n_levels - 1];
+    const unsigned bytes = 8u * (unsigned)level_rec_doubles(L0);
+    mbar_expect_tx(&bar[3], bytes);
+    bulk_g2s(LREC(0), reinterpret_cast<const double *>(a.blob + d0.blob_off + d0.off_rec) + L0.recG, bytes, &bar[3]);
+  }
+  for (int64_t k = 0; k < cnt; k++) {
+    const int st = (int)(k % 3), fb = (int)(k & 1);
+    if (tid == 0) {
+      if (k + 2 < cnt) {  // head of chunk k+2 (stage of chunk k-1, released at the end of k-1)
+        const ChunkDesc *d = &a.chunks[blockIdx.x + (k + 2) * G];
+        const int s2 = (int)((k + 2) % 3);
+        fence_proxy_async();
+        mbar_expect_tx(&bar[s2], (unsigned)d->off_rec);
+        bulk_g2s(HEAD(s2), a.blob + d->blob_off, (unsigned)d->off_rec, &bar[s2]);
+      }
+      if (k + 3 < cnt) {
+        const ChunkDesc *d = &a.chunks[blockIdx.x + (k + 3) * G];
+        const unsigned rb = (unsigned)(d->blob_bytes - d->off_rec);
+        if (rb) prefetch_l2(a.blob + d->blob_off + d->off_rec, rb);
+      }
+    }
+    if (k + 1 < cnt) {
+      const int s1 = (int)((k + 1) % 3);
+      mbar_wait(&bar[s1], (phase >> s1) & 1u);
+      phase ^= 1u << s1;
+      prefetch_vectors<UP, NT>(a, HEAD(s1), VBUF(fb ^ 1), ROOTBUF(fb ^ 1));
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const ChunkView cv = view(HEAD(st));
+    const ChunkDesc &d = *cv.hdr;
+    const int64_t bead0 = a.bead_off[d.body];
+    const int64_t sbase = spec_base(a.op, a.bead_off, d.body);
+    const double *grec = reinterpret_cast<const double *>(a.blob + d.blob_off + d.off_rec);
+    double *M = reinterpret_cast<double *>(smem + SM.o_m);
+    const int H = d.n_levels;
+    if (!UP) {
+      for (int i = tid; i < 6 * d.n_tiles; i += NT) M[6 * cv.tiles[i / 6].root_slot + i % 6] = ROOTBUF(fb)[i];
+      __syncthreads();
+    }
+    for (int s = 0; s < H; s++, lctr++) {
+      const int h = UP ? s : H - 1 - s;
+      const int ls = (int)(lctr & 1);
+      const LevelDesc L = cv.LV[h];
+      if (tid == 0) {  // records of the next level step (this chunk's next level, or chunk k+1's first)
+        const double *g2 = nullptr;
+        unsigned bytes = 0;
+        if (s + 1 < H) {
+          const LevelDesc L2 = cv.LV[UP ? h + 1 : h - 1];
+          g2 = grec + L2.recG;
+          bytes = 8u * (unsigned)level_rec_doubles(L2);
+        } else if (k + 1 < cnt) {
+          const ChunkView nv = view(HEAD((k + 1) % 3));
+          const ChunkDesc &nd = *nv.hdr;
+          const LevelDesc L2 = nv.LV[UP ? 0 : nd.n_levels - 1];
+          g2 = reinterpret_cast<const double *>(a.blob + nd.blob_off + nd.off_rec) + L2.recG;
+          bytes = 8u * (unsigned)level_rec_doubles(L2);
+        }
+        if (g2) {
+          fence_proxy_async();
+          mbar_expect_tx(&bar[3 + (ls ^ 1)], bytes);
+          bulk_g2s(LREC(ls ^ 1), g2, bytes, &bar[3 + (ls ^ 1)]);
+        }
+      }
+      mbar_wait(&bar[3 + ls], (phase >> (3 + ls)) & 1u);
+      phase ^= 1u << (3 + ls);
+      const double *R = LREC(ls);
+      const int oR = rec_size(GENERAL) * L.nG, oB = oR + rec_size(RIGID_BEAD) * L.nR;
+      // case-uniform warps: each case group is padded to whole warps
+      const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
+      const int tot = gG + gR + L.nB;
+      if (UP) {
+        const double *F = VBUF(fb);
+        double *RES = reinterpret_cast<double *>(smem + SM.o_x);
+        for (int q = tid; q < tot; q += NT) {
+          if (q < gG) {
+            if (q < L.nG) up_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < L.nR)
+              up_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
+          } else {
+            const int qq = q - gG - gR;
+            up_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
+          }
+        }
+      } else {
+        const double *RES = VBUF(fb);
+        double *F = reinterpret_cast<double *>(smem + SM.o_x);
+        for (int q = tid; q < tot; q += NT) {
+          if (q < gG) {
+            if (q < L.nG) down_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < L.nR)
+              down_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
+          } else {
+            const int qq = q - gG - gR;
+            down_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F,
+                                 RES);
+          }
         }
       }
       __syncthreads();
-      for (int h = 0; h < d.n_levels; h++) {
-        const LevelDesc L = LV[h];
-        // case-uniform warps: each case group is padded to whole warps
-        const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
-        const int tot = gG + gR + L.nB;
-        for (int q = tid; q < tot; q += NT_CHUNK) {
-          if (q < gG) {
-            if (q < L.nG) up_node<GENERAL>(L.slot_begin + q, REC + L.recG + q, L.nG, ME, M, F, RES);
-          } else if (q < gG + gR) {
-            const int qq = q - gG;
-            if (qq < L.nR) up_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, REC + L.recR + qq, L.nR, ME, M, F, RES);
-          } else {
-            const int qq = q - gG - gR;
-            up_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, REC + L.recB + qq, L.nB, ME, M, F, RES);
-          }
-        }
-        __syncthreads();
-      }
-      // residues (contiguous per tile) and tile-root info vectors
-      for (int t = 0; t < d.n_tiles; t++) {
-        const TileDesc T = a.tiles[d.tile_begin + t];
-        for (int r = tid; r < T.res_count; r += NT_CHUNK)
-          a.out[(sbase + T.res_q + r) * K + col] = RES[T.res_local + r];
+    }
+    if (UP) {
+      const double *RES = reinterpret_cast<const double *>(smem + SM.o_x);
+      for (int t = 0; t < d.n_tiles; t++) {  // residues (contiguous per tile) and tile-root info vectors
+        const TileDesc T = cv.tiles[t];
+        for (int r = tid; r < T.res_count; r += NT) a.out[(sbase + T.res_q + r) * K + col] = RES[T.res_local + r];
         if (tid < 6) {
           const double v = M[6 * T.root_slot + tid];
           if (T.scratch >= 0) a.scratch[6 * (int64_t)T.scratch + tid] = v;
@@ -228,37 +446,9 @@ __global__ void __launch_bounds__(NT_CHUNK) k_chunk(ApplyCtx a) {
         }
       }
     } else {
-      for (int t = 0; t < d.n_tiles; t++) {
-        const TileDesc T = a.tiles[d.tile_begin + t];
-        for (int r = tid; r < T.res_count; r += NT_CHUNK)
-          RES[T.res_local + r] = a.in[(sbase + T.res_q + r) * K + col];
-        if (tid < 6) {
-          double v;
-          if (T.scratch >= 0) v = a.scratch[6 * (int64_t)T.scratch + tid];
-          else v = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + tid) * K + col] : 0.0;
-          M[6 * T.root_slot + tid] = v;
-        }
-      }
-      __syncthreads();
-      for (int h = d.n_levels - 1; h >= 0; h--) {
-        const LevelDesc L = LV[h];
-        const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
-        const int tot = gG + gR + L.nB;
-        for (int q = tid; q < tot; q += NT_CHUNK) {
-          if (q < gG) {
-            if (q < L.nG) down_node<GENERAL>(L.slot_begin + q, REC + L.recG + q, L.nG, ME, M, F, RES);
-          } else if (q < gG + gR) {
-            const int qq = q - gG;
-            if (qq < L.nR) down_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, REC + L.recR + qq, L.nR, ME, M, F, RES);
-          } else {
-            const int qq = q - gG - gR;
-            down_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, REC + L.recB + qq, L.nB, ME, M, F, RES);
-          }
-        }
-        __syncthreads();
-      }
-      for (int i = tid; i < d.n_beads; i += NT_CHUNK) {
-        uint32_t pp = PERM[i];
+      const double *F = reinterpret_cast<const double *>(smem + SM.o_x);
+      for (int i = tid; i < d.n_beads; i += NT) {
+        const uint32_t pp = cv.PERM[i];
         if (!(pp & PERM_FOREIGN)) {
           const int64_t row = (bead0 + pp) * 3;
           a.out[(row + 0) * K + col] = F[i * 3 + 0];
@@ -269,6 +459,10 @@ __global__ void __launch_bounds__(NT_CHUNK) k_chunk(ApplyCtx a) {
     }
     __syncthreads();
   }
+#undef HEAD
+#undef LREC
+#undef VBUF
+#undef ROOTBUF
 }
 
 // ---- top tree (nodes with more than tile_leaves beads) ---------------------------------
@@ -386,13 +580,15 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   int dev = p.device;
   int sms = 0;
   RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  a.buf_bytes = (int)((p.max_blob + 127) / 128 * 128);
+  a.head_bytes = (int)p.max_head_bytes;
+  a.lrec_bytes = (int)p.max_level_rec_bytes;
   a.max_nodes = std::max(1, p.max_chunk_nodes);
   a.max_beads = std::max(1, p.max_chunk_beads);
   a.max_res = std::max(1, p.max_chunk_res);
+  a.max_tiles = std::max(1, p.max_chunk_tiles);
   KernelCfg cfg;
   cfg.threads = p.chunk_threads;
-  cfg.smem = 2 * (size_t)a.buf_bytes + 8 * (6 * (size_t)a.max_nodes + 3 * (size_t)a.max_beads + (size_t)a.max_res);
+  cfg.smem = smem_total(smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, up));
   cfg.fn = up ? chunk_fn<true>(cfg.threads) : chunk_fn<false>(cfg.threads);
   RQ_CUDA(cudaFuncSetAttribute((const void *)cfg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   int occ = 0;
@@ -427,6 +623,13 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   a.scratch = p.scratch.as<double>();
   a.op = op;
   KernelCfg cfg = chunk_cfg(p, up, a);
+  static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
+  DBuf dbg;
+  if (timing) {
+    dbg.alloc((size_t)cfg.grid * 64);
+    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
+    a.dbg = dbg.as<long long>();
+  }
   TopCtx t{};
   t.top = p.top.as<TopNode>();
   t.topbody = p.topbody.as<int32_t>();
@@ -450,6 +653,19 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     } else {
       if (do_top) k_top<false><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
+    }
+    if (timing && do_chunks) {
+      std::vector<long long> h((size_t)cfg.grid * 8);
+      RQ_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+      RQ_CUDA(cudaStreamSynchronize(s));
+      double acc[8] = {0};
+      for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) acc[i] += (double)h[8 * g + i];
+      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per chunk cycles wait_blob %.0f wait_vec %.0f levels %.0f out %.0f | levels/chunk %.1f beads/chunk %.1f chunks/CTA %.1f\n",
+              op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[6], acc[1] / acc[6], acc[2] / acc[6], acc[3] / acc[6],
+              acc[4] / acc[6], acc[5] / acc[6], acc[6] / cfg.grid);
+      { double lv = 0, bw = 0; for (int g = 0; g < cfg.grid; g++) { lv += (double)(h[8 * g + 4] & ((1ll << 20) - 1)); bw += (double)(h[8 * g + 4] >> 20); }
+        fprintf(stderr, "[rq timing]   tid0 node work per level %.0f cyc, barrier wait per level %.0f cyc\n", acc[7] / lv, bw / lv); }
+      RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
     }
     if ((phases & 4u) && p.n_small && op <= 1)
       k_small<<<(unsigned)((3 * p.n_small + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>(), p.n_small,

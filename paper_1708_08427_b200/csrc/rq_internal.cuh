@@ -27,8 +27,9 @@ __host__ __device__ inline unsigned flag_signs(unsigned f) { return (f >> 3) & 7
 
 // compact record sizes (doubles): BEAD_BEAD explicit 3x3 g; RIGID_BEAD /
 // GENERAL Householder record (HH<6> / HH<9>) followed by the ratios a, b.
+// Padded to an even count so records stay 16-byte aligned (LDS.128 / double2).
 __host__ __device__ constexpr int rec_size(int c) {
-  return c == BEAD_BEAD ? 9 : (c == RIGID_BEAD ? 17 : (c == GENERAL ? 26 : 0));
+  return c == BEAD_BEAD ? 10 : (c == RIGID_BEAD ? 18 : (c == GENERAL ? 26 : 0));
 }
 __host__ __device__ constexpr int res_rows(int c) {
   return c == RIGID_BEAD ? 3 : (c == GENERAL ? 6 : 0);
@@ -39,7 +40,7 @@ __host__ __device__ constexpr int res_rows(int c) {
 struct LevelDesc {       // one height level of a chunk, 32 bytes
   int32_t slot_begin;    // first chunk-local slot of the level
   int32_t nG, nR, nB;    // nodes per case (slots ordered GEN, RB, BB)
-  int32_t recG, recR, recB;  // double offsets of the SoA groups in the record area
+  int32_t recG, recR, recB;  // double offsets of the per-case record groups (AoS, rec_size stride)
   int32_t pad;
 };
 
@@ -49,6 +50,8 @@ struct NodeMeta {        // 8 bytes, one per in-chunk internal node (slot order)
   uint16_t flags;        // case | swapped | signs
 };
 
+// Chunk blob layout (16-byte aligned sections):
+//   ChunkDesc (64 B) | TileDesc[n_tiles] | LevelDesc[n_levels] | NodeMeta[n_nodes] | perm[n_beads] | records
 struct ChunkDesc {
   int64_t blob_off;      // byte offset of the blob (16-byte aligned)
   int32_t blob_bytes;    // multiple of 16
@@ -65,13 +68,13 @@ struct ChunkDesc {
   int32_t n_res;         // residue doubles staged
 };
 
-struct TileDesc {
+struct TileDesc {        // 32 bytes; copies live in the chunk blob after the ChunkDesc header
   int32_t root_slot;     // chunk-local slot of the tile root
   int32_t scratch;       // exchange slot with the top tree, -1 if the tile root is the body root
   int32_t res_q;         // body-relative complement (Q~) offset of the tile's first residue
   int32_t res_count;     // 3L - 6
   int32_t res_local;     // offset in the chunk staging buffer
-  int32_t pad;
+  int32_t pad[3];
 };
 
 struct TopNode {         // node with more than tile_leaves beads

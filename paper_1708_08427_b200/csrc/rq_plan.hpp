@@ -75,7 +75,9 @@ struct Plan {
   int tile_leaves = 128;           // S
   int chunk_threads = 128;         // threads per chunk CTA
   int64_t max_blob = 0;            // largest chunk blob (bytes)
-  int max_chunk_nodes = 0, max_chunk_beads = 0, max_chunk_levels = 0, max_chunk_res = 0;
+  int64_t max_head_bytes = 0;      // largest chunk head (everything before the records)
+  int64_t max_level_rec_bytes = 0; // largest record block of one level of one chunk
+  int max_chunk_nodes = 0, max_chunk_beads = 0, max_chunk_levels = 0, max_chunk_res = 0, max_chunk_tiles = 0;
   std::vector<int64_t> bead_off;   // host copy, m+1
   int64_t n_case[4] = {0, 0, 0, 0};
   int64_t rec_doubles = 0;

@@ -494,14 +494,16 @@ __global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const i
 
 struct ChunkLimits {
   int64_t max_bytes;
-  int max_nodes, max_beads, max_res;
+  int max_nodes, max_beads, max_res, max_tiles;
 };
 
-__host__ __device__ inline int64_t blob_bytes_of(int H, int nodes, int beads, int64_t rec) {
-  int64_t perm = ((int64_t)beads * 4 + 15) / 16 * 16;
-  nodes = (nodes + 1) / 2 * 2;  // meta section padded to 16 bytes
-  int64_t b = (int64_t)H * 32 + (int64_t)nodes * 8 + perm + rec * 8;
-  return (b + 15) / 16 * 16;
+__host__ __device__ inline int64_t meta_bytes(int nodes) { return ((int64_t)nodes * 8 + 15) / 16 * 16; }
+__host__ __device__ inline int64_t perm_bytes(int beads) { return ((int64_t)beads * 4 + 15) / 16 * 16; }
+__host__ __device__ inline int64_t head_bytes(int tiles, int H) {
+  return (int64_t)sizeof(ChunkDesc) + (int64_t)sizeof(TileDesc) * tiles + (int64_t)sizeof(LevelDesc) * H;
+}
+__host__ __device__ inline int64_t blob_bytes_of(int H, int nodes, int beads, int64_t rec, int tiles) {
+  return head_bytes(tiles, H) + meta_bytes(nodes) + perm_bytes(beads) + rec * 8;  // rec is even: 16-byte multiple
 }
 
 // Greedy packing of a body's consecutive tiles into chunks (one thread per body).
@@ -529,8 +531,8 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
       d.bead_begin = bead_off[j] + bead0;
       d.tile_begin = big_scan[tile0];
       d.n_res = res;
-      d.off_meta = H * 32;
-      d.off_perm = d.off_meta + (nodes * 8 + 15) / 16 * 16;
+      d.off_meta = (int32_t)head_bytes(ntiles, H);
+      d.off_perm = (int32_t)(d.off_meta + meta_bytes(nodes));
       // n_beads, off_rec and blob_bytes set by the caller below
     }
     nch++;
@@ -545,14 +547,13 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
       int beads2 = T.start + T.L - bead0;
       int nodes2 = nodes + Tn, H2 = max(H, T.height), res2 = res + Tres;
       int64_t rec2 = rec + T.rec_doubles;
-      if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res ||
-          blob_bytes_of(H2, nodes2, beads2, rec2) > lim.max_bytes) {
+      if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res || ntiles + 1 > lim.max_tiles ||
+          blob_bytes_of(H2, nodes2, beads2, rec2, ntiles + 1) > lim.max_bytes) {
         if (pass == 1) {
           ChunkDesc &d = chunks[chunk_base[j] + nch];
           d.n_beads = last_stop - bead0;
-          int64_t pb = ((int64_t)d.n_beads * 4 + 15) / 16 * 16;
-          d.off_rec = (int32_t)(H * 32 + (nodes * 8 + 15) / 16 * 16 + pb);
-          d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec);
+          d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(d.n_beads));
+          d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec, ntiles);
         }
         flush();
       }
@@ -575,9 +576,8 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
   if (open && pass == 1) {
     ChunkDesc &d = chunks[chunk_base[j] + nch];
     d.n_beads = last_stop - bead0;
-    int64_t pb = ((int64_t)d.n_beads * 4 + 15) / 16 * 16;
-    d.off_rec = (int32_t)(H * 32 + (nodes * 8 + 15) / 16 * 16 + pb);
-    d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec);
+    d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(d.n_beads));
+    d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec, ntiles);
   }
   flush();
   if (pass == 0) n_chunks_body[j] = nch;
@@ -629,21 +629,24 @@ __global__ void k_slots(const uint64_t *keys, const int32_t *vals, int64_t n_par
 }
 
 __global__ void k_levels_finalize(const ChunkDesc *chunks, int64_t nc, const int64_t *lvl_base,
-                                  LevelDesc *lvl, uint8_t *blob) {
+                                  LevelDesc *lvl, uint8_t *blob, unsigned long long *max_lrec) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= nc) return;
   const ChunkDesc &d = chunks[c];
   int slot = 0, recd = 0;
-  LevelDesc *dst = reinterpret_cast<LevelDesc *>(blob + d.blob_off);
+  LevelDesc *dst = reinterpret_cast<LevelDesc *>(blob + d.blob_off + sizeof(ChunkDesc) + sizeof(TileDesc) * d.n_tiles);
+  *reinterpret_cast<ChunkDesc *>(blob + d.blob_off) = d;  // header copy for the kernels
   for (int h = 0; h < d.n_levels; h++) {
     LevelDesc &L = lvl[lvl_base[c] + h];
     L.slot_begin = slot;
-    L.recG = recd; recd += 26 * L.nG;
-    L.recR = recd; recd += 17 * L.nR;
-    L.recB = recd; recd += 9 * L.nB;
+    L.recG = recd; recd += rec_size(GENERAL) * L.nG;
+    L.recR = recd; recd += rec_size(RIGID_BEAD) * L.nR;
+    L.recB = recd; recd += rec_size(BEAD_BEAD) * L.nB;
     L.pad = 0;
     slot += L.nG + L.nR + L.nB;
     dst[h] = L;
+    atomicMax(max_lrec, (unsigned long long)8 * (rec_size(GENERAL) * L.nG + rec_size(RIGID_BEAD) * L.nR +
+                                                 rec_size(BEAD_BEAD) * L.nB));
   }
 }
 
@@ -697,13 +700,13 @@ __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
   int q = slot - L.slot_begin;
   const double *src = w.rec + w.c.rec_off[g];
   if (cs == GENERAL) {
-    for (int e = 0; e < 26; e++) R[L.recG + e * L.nG + q] = src[e];
+    for (int e = 0; e < rec_size(GENERAL); e++) R[L.recG + q * rec_size(GENERAL) + e] = src[e];
   } else if (cs == RIGID_BEAD) {
     q -= L.nG;
-    for (int e = 0; e < 17; e++) R[L.recR + e * L.nR + q] = src[e];
+    for (int e = 0; e < rec_size(RIGID_BEAD); e++) R[L.recR + q * rec_size(RIGID_BEAD) + e] = src[e];
   } else {
     q -= L.nG + L.nR;
-    for (int e = 0; e < 9; e++) R[L.recB + e * L.nB + q] = src[e];
+    for (int e = 0; e < rec_size(BEAD_BEAD); e++) R[L.recB + q * rec_size(BEAD_BEAD) + e] = src[e];
   }
 }
 
@@ -727,7 +730,8 @@ __global__ void k_write_perm(const ChunkDesc *chunks, int64_t nc, const int32_t 
 
 __global__ void k_tile_desc(const TileTmp *tiles, int64_t n_tiles_all, const int32_t *big_scan,
                             const int32_t *slot_of, const int32_t *slot_scan,
-                            const int32_t *res_local_of_tile, const int32_t *parent, TileDesc *out) {
+                            const int32_t *res_local_of_tile, const int32_t *parent, TileDesc *out,
+                            const int64_t *chunk_of_tile, const ChunkDesc *chunks, uint8_t *blob) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n_tiles_all) return;
   const TileTmp &T = tiles[t];
@@ -738,8 +742,10 @@ __global__ void k_tile_desc(const TileTmp *tiles, int64_t n_tiles_all, const int
   d.res_q = T.res_q;
   d.res_count = 3 * T.L - 6;
   d.res_local = res_local_of_tile[t];
-  d.pad = 0;
+  d.pad[0] = d.pad[1] = d.pad[2] = 0;
   out[big_scan[t]] = d;
+  const ChunkDesc &c = chunks[chunk_of_tile[t]];
+  reinterpret_cast<TileDesc *>(blob + c.blob_off + sizeof(ChunkDesc))[big_scan[t] - c.tile_begin] = d;
 }
 
 __global__ void k_top_fill(LayoutCtx c, int64_t NN, const int32_t *is_top, const int32_t *top_scan,
@@ -1110,6 +1116,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     // 5. factors
     p.t22.alloc(NN * 48);
     p.rec.alloc(std::max<int64_t>(p.rec_doubles, 1) * 8);
+    RQ_CUDA(cudaMemsetAsync(p.rec.p, 0, std::max<int64_t>(p.rec_doubles, 1) * 8, s));
     p.height.alloc(NN * 4);
     RQ_CUDA(cudaMemsetAsync(p.height.p, 0, NN * 4, s));
     RQ_CUDA(cudaMemsetAsync(p.t22.p, 0, NN * 48, s));
@@ -1210,13 +1217,14 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
 
     ChunkLimits lim;
-    lim.max_bytes = 32 * 1024;
+    lim.max_bytes = 64 * 1024;
     if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
     // a single worst-case tile (all GENERAL nodes) must fit a chunk
-    lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, 26 * (S - 1)));
+    lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
     lim.max_nodes = 1024;
     lim.max_beads = 1024;
     lim.max_res = 3 * 1024;
+    lim.max_tiles = 64;
     DBuf nch_body, chunk_base;
     nch_body.alloc(m * 8);
     chunk_base.alloc((m + 1) * 8);
@@ -1253,7 +1261,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       if (nc) d2h(hc.data(), p.chunks.p, nc, s);
       p.blob_bytes = nc ? hc[nc - 1].blob_off + hc[nc - 1].blob_bytes : 0;
       int64_t n_part = 0, n_lvl = 0;
-      p.max_blob = p.max_chunk_nodes = p.max_chunk_beads = p.max_chunk_levels = p.max_chunk_res = 0;
+      p.max_blob = p.max_chunk_nodes = p.max_chunk_beads = p.max_chunk_levels = p.max_chunk_res = p.max_chunk_tiles = 0;
+      p.max_head_bytes = 0;
       for (auto &d : hc) {
         n_part += d.n_nodes;
         n_lvl += d.n_levels;
@@ -1262,6 +1271,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.max_chunk_beads = std::max(p.max_chunk_beads, d.n_beads);
         p.max_chunk_levels = std::max(p.max_chunk_levels, d.n_levels);
         p.max_chunk_res = std::max(p.max_chunk_res, d.n_res);
+        p.max_chunk_tiles = std::max(p.max_chunk_tiles, d.n_tiles);
+        p.max_head_bytes = std::max<int64_t>(p.max_head_bytes, d.off_rec);
       }
       p.blob.alloc(p.blob_bytes);
       RQ_CUDA(cudaMemsetAsync(p.blob.p, 0, p.blob_bytes, s));
@@ -1292,8 +1303,13 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         k_slots<<<nblk(n_part), NT, 0, s>>>(nkeys2.as<uint64_t>(), nvals2.as<int32_t>(), n_part,
                                              node_scan.as<int64_t>(), slot_of.as<int32_t>(),
                                              lvl_base.as<int64_t>(), lvl.as<LevelDesc>(), p.flags.as<uint8_t>());
+      DBuf d_max_lrec;
+      d_max_lrec.alloc(8);
+      RQ_CUDA(cudaMemsetAsync(d_max_lrec.p, 0, 8, s));
       k_levels_finalize<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, lvl_base.as<int64_t>(),
-                                                 lvl.as<LevelDesc>(), p.blob.as<uint8_t>());
+                                                 lvl.as<LevelDesc>(), p.blob.as<uint8_t>(),
+                                                 d_max_lrec.as<unsigned long long>());
+      p.max_level_rec_bytes = (int64_t)d2h1<unsigned long long>(d_max_lrec.p, s);
       WriteCtx wc{lc,
                   nkeys2.as<uint64_t>(),
                   nvals2.as<int32_t>(),
@@ -1317,7 +1333,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       k_tile_desc<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
                                                     d_big_scan.as<int32_t>(), slot_of.as<int32_t>(),
                                                     slot_scan.as<int32_t>(), res_local_of_tile.as<int32_t>(),
-                                                    p.parent.as<int32_t>(), p.tiles.as<TileDesc>());
+                                                    p.parent.as<int32_t>(), p.tiles.as<TileDesc>(),
+                                                    chunk_of_tile.as<int64_t>(), p.chunks.as<ChunkDesc>(),
+                                                    p.blob.as<uint8_t>());
     }
 
     // top tree
