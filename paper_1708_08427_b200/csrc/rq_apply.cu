@@ -189,6 +189,84 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// GENERAL and RIGID_BEAD share one 9-slot code path (so a level is one
+// case-uniform group): an RB node is a GENERAL node whose formula-y child
+// carries a zero rotational part; its 6-dim Householder record (HH<6>) is
+// scattered into the 9-slot layout (HH<9>) on load, with zero rows 3..5, which
+// leaves those slots untouched by every reflector.
+__device__ __forceinline__ void load_rec9(const double *rec, bool rb, double (&R)[26]) {
+  if (!rb) {
+    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+#pragma unroll
+    for (int i = 0; i < 13; i++) {
+      const double2 v = r2[i];
+      R[2 * i] = v.x;
+      R[2 * i + 1] = v.y;
+    }
+  } else {
+    double r[18];
+    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+#pragma unroll
+    for (int i = 0; i < 9; i++) {
+      const double2 v = r2[i];
+      r[2 * i] = v.x;
+      r[2 * i + 1] = v.y;
+    }
+    R[0] = r[0]; R[1] = r[1]; R[2] = 0.0; R[3] = 0.0; R[4] = 0.0; R[5] = r[2]; R[6] = r[3]; R[7] = r[4];  // v0
+    R[8] = r[5]; R[9] = 0.0; R[10] = 0.0; R[11] = 0.0; R[12] = r[6]; R[13] = r[7]; R[14] = r[8];         // v1
+    R[15] = 0.0; R[16] = 0.0; R[17] = 0.0; R[18] = r[9]; R[19] = r[10]; R[20] = r[11];                    // v2
+    R[21] = r[12]; R[22] = r[13]; R[23] = r[14];                                                          // taus
+    R[24] = r[15]; R[25] = r[16];                                                                         // a, b
+  }
+}
+
+// upward merge of a GENERAL or RIGID_BEAD node (merge_infosets, matfree.py:41-62)
+__device__ __forceinline__ void up_node9(int slot, const double *rec, const NodeMeta *ME, double *M, const double *F,
+                                         double *RES) {
+  const NodeMeta md = ME[slot];
+  const bool rb = flag_case(md.flags) == RIGID_BEAD;
+  double R[26];
+  load_rec9(rec, rb, R);
+  double mx[6], my[6];
+  load6(M + 6 * md.x, mx);
+  if (rb) {  // formula-y is a bead: [f; 0]
+    const double *f = F + 3 * (md.y & 0x7fff);
+    my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
+  } else {
+    load6(M + 6 * md.y, my);
+  }
+  double mp[6], res[6];
+  merge(GENERAL, R, 1, flag_signs(md.flags), R[HH<9>::RA], R[HH<9>::RB], mx, my, mp, res);
+  // GENERAL: residues = out[3:9]; RIGID_BEAD: out[6:9] (out[3:6] stays 0)
+  const int o = rb ? 3 : 0;
+#pragma unroll
+  for (int r = 0; r < 6; r++)
+    if (r >= o) RES[md.res + r - o] = res[r];
+  store6(M + 6 * slot, mp);
+}
+
+// downward split of a GENERAL or RIGID_BEAD node (split_rvset, matfree.py:65-83)
+__device__ __forceinline__ void down_node9(int slot, const double *rec, const NodeMeta *ME, double *M, double *F,
+                                           const double *RES) {
+  const NodeMeta md = ME[slot];
+  const bool rb = flag_case(md.flags) == RIGID_BEAD;
+  double R[26];
+  load_rec9(rec, rb, R);
+  double lp[6], res[6], lx[6], ly[6];
+  load6(M + 6 * slot, lp);
+  const int o = rb ? 3 : 0;
+#pragma unroll
+  for (int r = 0; r < 6; r++) res[r] = (r >= o) ? RES[md.res + r - o] : 0.0;
+  split(GENERAL, R, 1, flag_signs(md.flags), R[HH<9>::RA], R[HH<9>::RB], lp, res, lx, ly);
+  store6(M + 6 * md.x, lx);
+  if (rb) {
+    double *f = F + 3 * (md.y & 0x7fff);
+    f[0] = ly[0]; f[1] = ly[1]; f[2] = ly[2];
+  } else {
+    store6(M + 6 * md.y, ly);
+  }
+}
+
 // Shared-memory map of the chunk kernels (all offsets 128-byte aligned):
 //   3 head stages (ChunkDesc | TileDesc[] | LevelDesc[] | NodeMeta[] | perm[])
 //   2 level-record stages (one height level's records at a time)
@@ -348,6 +426,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
         if (rb) prefetch_l2(a.blob + d->blob_off + d->off_rec, rb);
       }
     }
+    long long tc0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (k + 1 < cnt) {
       const int s1 = (int)((k + 1) % 3);
       mbar_wait(&bar[s1], (phase >> s1) & 1u);
@@ -358,6 +437,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       cp_async_wait<0>();
     }
     __syncthreads();
+    if (RQ_TIMING && a.dbg && tid == 0) { a.dbg[8 * blockIdx.x + 3] += clock64() - tc0; a.dbg[8 * blockIdx.x + 6] += 1; }
     const ChunkView cv = view(HEAD(st));
     const ChunkDesc &d = *cv.hdr;
     const int64_t bead0 = a.bead_off[d.body];
@@ -393,47 +473,54 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
           bulk_g2s(LREC(ls ^ 1), g2, bytes, &bar[3 + (ls ^ 1)]);
         }
       }
+      long long tw0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       mbar_wait(&bar[3 + ls], (phase >> (3 + ls)) & 1u);
       phase ^= 1u << (3 + ls);
+      long long tw1 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       const double *R = LREC(ls);
       const int oR = rec_size(GENERAL) * L.nG, oB = oR + rec_size(RIGID_BEAD) * L.nR;
-      // case-uniform warps: each case group is padded to whole warps
-      const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
-      const int tot = gG + gR + L.nB;
+      const int nGR = L.nG + L.nR;
+      const int gGR = (nGR + 31) & ~31;  // case-uniform warps: GEN+RB group padded to whole warps
+      const int tot = gGR + L.nB;
       if (UP) {
         const double *F = VBUF(fb);
         double *RES = reinterpret_cast<double *>(smem + SM.o_x);
         for (int q = tid; q < tot; q += NT) {
-          if (q < gG) {
-            if (q < L.nG) up_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
-          } else if (q < gG + gR) {
-            const int qq = q - gG;
-            if (qq < L.nR)
-              up_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
+          if (q < gGR) {
+            if (q < nGR)
+              up_node9(L.slot_begin + q, R + (q < L.nG ? q * rec_size(GENERAL) : oR + (q - L.nG) * rec_size(RIGID_BEAD)),
+                       cv.ME, M, F, RES);
           } else {
-            const int qq = q - gG - gR;
-            up_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
+            const int qq = q - gGR;
+            up_node<BEAD_BEAD>(L.slot_begin + nGR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
           }
         }
       } else {
         const double *RES = VBUF(fb);
         double *F = reinterpret_cast<double *>(smem + SM.o_x);
         for (int q = tid; q < tot; q += NT) {
-          if (q < gG) {
-            if (q < L.nG) down_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
-          } else if (q < gG + gR) {
-            const int qq = q - gG;
-            if (qq < L.nR)
-              down_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
+          if (q < gGR) {
+            if (q < nGR)
+              down_node9(L.slot_begin + q,
+                         R + (q < L.nG ? q * rec_size(GENERAL) : oR + (q - L.nG) * rec_size(RIGID_BEAD)), cv.ME, M, F,
+                         RES);
           } else {
-            const int qq = q - gG - gR;
-            down_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F,
-                                 RES);
+            const int qq = q - gGR;
+            down_node<BEAD_BEAD>(L.slot_begin + nGR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
           }
         }
       }
+      long long tw2 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       __syncthreads();
+      if (RQ_TIMING && a.dbg && tid == 0) {
+        long long tw3 = clock64();
+        a.dbg[8 * blockIdx.x + 0] += tw1 - tw0;  // level record wait
+        a.dbg[8 * blockIdx.x + 1] += tw2 - tw1;  // tid0 node work
+        a.dbg[8 * blockIdx.x + 2] += tw3 - tw2;  // barrier
+        a.dbg[8 * blockIdx.x + 4] += 1;          // level steps
+      }
     }
+    long long to0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (UP) {
       const double *RES = reinterpret_cast<const double *>(smem + SM.o_x);
       for (int t = 0; t < d.n_tiles; t++) {  // residues (contiguous per tile) and tile-root info vectors
@@ -458,6 +545,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       }
     }
     __syncthreads();
+    if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 5] += clock64() - to0;
   }
 #undef HEAD
 #undef LREC
@@ -660,11 +748,9 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       RQ_CUDA(cudaStreamSynchronize(s));
       double acc[8] = {0};
       for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) acc[i] += (double)h[8 * g + i];
-      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per chunk cycles wait_blob %.0f wait_vec %.0f levels %.0f out %.0f | levels/chunk %.1f beads/chunk %.1f chunks/CTA %.1f\n",
-              op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[6], acc[1] / acc[6], acc[2] / acc[6], acc[3] / acc[6],
-              acc[4] / acc[6], acc[5] / acc[6], acc[6] / cfg.grid);
-      { double lv = 0, bw = 0; for (int g = 0; g < cfg.grid; g++) { lv += (double)(h[8 * g + 4] & ((1ll << 20) - 1)); bw += (double)(h[8 * g + 4] >> 20); }
-        fprintf(stderr, "[rq timing]   tid0 node work per level %.0f cyc, barrier wait per level %.0f cyc\n", acc[7] / lv, bw / lv); }
+      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f barrier %.0f | per chunk: head+vec wait %.0f, out %.0f, level steps %.1f, chunks/CTA %.1f\n",
+              op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[4], acc[1] / acc[4], acc[2] / acc[4], acc[3] / acc[6],
+              acc[5] / acc[6], acc[4] / acc[6], acc[6] / cfg.grid);
       RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
     }
     if ((phases & 4u) && p.n_small && op <= 1)

@@ -72,7 +72,7 @@ struct Plan {
   int device = 0;
   int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
   int max_depth = 96;
-  int tile_leaves = 128;           // S
+  int tile_leaves = 64;            // S
   int chunk_threads = 128;         // threads per chunk CTA
   int64_t max_blob = 0;            // largest chunk blob (bytes)
   int64_t max_head_bytes = 0;      // largest chunk head (everything before the records)

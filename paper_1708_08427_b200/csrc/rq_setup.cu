@@ -1217,7 +1217,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
 
     ChunkLimits lim;
-    lim.max_bytes = 64 * 1024;
+    lim.max_bytes = 32 * 1024;
     if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
     // a single worst-case tile (all GENERAL nodes) must fit a chunk
     lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
