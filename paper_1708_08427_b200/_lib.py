@@ -14,7 +14,7 @@ import threading
 from . import errors as E
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librigidq_b200.so")
+LIB_PATH = os.environ.get("RQ_LIB_PATH") or os.path.join(HERE, "librigidq_b200.so")
 
 OP_QV, OP_QTV, OP_QTILDE_V, OP_QTILDE_TV = 0, 1, 2, 3
 OPS = {"qv": OP_QV, "qtv": OP_QTV, "qtilde_v": OP_QTILDE_V, "qtilde_tv": OP_QTILDE_TV}

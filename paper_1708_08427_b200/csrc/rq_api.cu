@@ -155,7 +155,7 @@ int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int6
 int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
   if (!plan) return -1;
   const rq::Plan &p = plan->p;
-  int per_col = (p.n_chunks ? 1 : 0) + (p.n_topbodies ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
+  int per_col = (p.n_chunks ? 1 : 0) + (p.n_topblob ? 1 : 0) + (p.n_topbig ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
   return (int)(per_col * k);
 }
 

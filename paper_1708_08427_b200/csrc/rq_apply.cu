@@ -189,84 +189,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// GENERAL and RIGID_BEAD share one 9-slot code path (so a level is one
-// case-uniform group): an RB node is a GENERAL node whose formula-y child
-// carries a zero rotational part; its 6-dim Householder record (HH<6>) is
-// scattered into the 9-slot layout (HH<9>) on load, with zero rows 3..5, which
-// leaves those slots untouched by every reflector.
-__device__ __forceinline__ void load_rec9(const double *rec, bool rb, double (&R)[26]) {
-  if (!rb) {
-    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
-#pragma unroll
-    for (int i = 0; i < 13; i++) {
-      const double2 v = r2[i];
-      R[2 * i] = v.x;
-      R[2 * i + 1] = v.y;
-    }
-  } else {
-    double r[18];
-    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
-#pragma unroll
-    for (int i = 0; i < 9; i++) {
-      const double2 v = r2[i];
-      r[2 * i] = v.x;
-      r[2 * i + 1] = v.y;
-    }
-    R[0] = r[0]; R[1] = r[1]; R[2] = 0.0; R[3] = 0.0; R[4] = 0.0; R[5] = r[2]; R[6] = r[3]; R[7] = r[4];  // v0
-    R[8] = r[5]; R[9] = 0.0; R[10] = 0.0; R[11] = 0.0; R[12] = r[6]; R[13] = r[7]; R[14] = r[8];         // v1
-    R[15] = 0.0; R[16] = 0.0; R[17] = 0.0; R[18] = r[9]; R[19] = r[10]; R[20] = r[11];                    // v2
-    R[21] = r[12]; R[22] = r[13]; R[23] = r[14];                                                          // taus
-    R[24] = r[15]; R[25] = r[16];                                                                         // a, b
-  }
-}
-
-// upward merge of a GENERAL or RIGID_BEAD node (merge_infosets, matfree.py:41-62)
-__device__ __forceinline__ void up_node9(int slot, const double *rec, const NodeMeta *ME, double *M, const double *F,
-                                         double *RES) {
-  const NodeMeta md = ME[slot];
-  const bool rb = flag_case(md.flags) == RIGID_BEAD;
-  double R[26];
-  load_rec9(rec, rb, R);
-  double mx[6], my[6];
-  load6(M + 6 * md.x, mx);
-  if (rb) {  // formula-y is a bead: [f; 0]
-    const double *f = F + 3 * (md.y & 0x7fff);
-    my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
-  } else {
-    load6(M + 6 * md.y, my);
-  }
-  double mp[6], res[6];
-  merge(GENERAL, R, 1, flag_signs(md.flags), R[HH<9>::RA], R[HH<9>::RB], mx, my, mp, res);
-  // GENERAL: residues = out[3:9]; RIGID_BEAD: out[6:9] (out[3:6] stays 0)
-  const int o = rb ? 3 : 0;
-#pragma unroll
-  for (int r = 0; r < 6; r++)
-    if (r >= o) RES[md.res + r - o] = res[r];
-  store6(M + 6 * slot, mp);
-}
-
-// downward split of a GENERAL or RIGID_BEAD node (split_rvset, matfree.py:65-83)
-__device__ __forceinline__ void down_node9(int slot, const double *rec, const NodeMeta *ME, double *M, double *F,
-                                           const double *RES) {
-  const NodeMeta md = ME[slot];
-  const bool rb = flag_case(md.flags) == RIGID_BEAD;
-  double R[26];
-  load_rec9(rec, rb, R);
-  double lp[6], res[6], lx[6], ly[6];
-  load6(M + 6 * slot, lp);
-  const int o = rb ? 3 : 0;
-#pragma unroll
-  for (int r = 0; r < 6; r++) res[r] = (r >= o) ? RES[md.res + r - o] : 0.0;
-  split(GENERAL, R, 1, flag_signs(md.flags), R[HH<9>::RA], R[HH<9>::RB], lp, res, lx, ly);
-  store6(M + 6 * md.x, lx);
-  if (rb) {
-    double *f = F + 3 * (md.y & 0x7fff);
-    f[0] = ly[0]; f[1] = ly[1]; f[2] = ly[2];
-  } else {
-    store6(M + 6 * md.y, ly);
-  }
-}
-
 // Shared-memory map of the chunk kernels (all offsets 128-byte aligned):
 //   3 head stages (ChunkDesc | TileDesc[] | LevelDesc[] | NodeMeta[] | perm[])
 //   2 level-record stages (one height level's records at a time)
@@ -328,7 +250,7 @@ template <bool UP, int NT>
 __device__ __forceinline__ void prefetch_vectors(const ApplyCtx &a, const unsigned char *B, double *V, double *ROOT) {
   const ChunkView cv = view(B);
   const ChunkDesc &d = *cv.hdr;
-  const int64_t bead0 = a.bead_off[d.body];
+  const int64_t bead0 = d.body_bead0;
   const int64_t K = a.k, col = a.col;
   if (UP) {
     for (int i = threadIdx.x; i < d.n_beads; i += NT) {
@@ -341,15 +263,16 @@ __device__ __forceinline__ void prefetch_vectors(const ApplyCtx &a, const unsign
       }
     }
   } else {
-    const int64_t sbase = spec_base(a.op, a.bead_off, d.body);
-    for (int t = 0; t < d.n_tiles; t++) {
+    const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? d.spec_full : d.spec_comp;
+    // one warp per tile (tiles are independent contiguous residue runs)
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int t = wid; t < d.n_tiles; t += NT / 32) {
       const TileDesc T = cv.tiles[t];
-      for (int r = threadIdx.x; r < T.res_count; r += NT)
-        cp_async8(V + T.res_local + r, a.in + (sbase + T.res_q + r) * K + col);
-      if (threadIdx.x < 6) {
-        if (T.scratch >= 0) cp_async8(ROOT + 6 * t + threadIdx.x, a.scratch + 6 * (int64_t)T.scratch + threadIdx.x);
-        else if (a.op == RQ_OP_QTV) cp_async8(ROOT + 6 * t + threadIdx.x, a.in + (3 * bead0 + threadIdx.x) * K + col);
-        else ROOT[6 * t + threadIdx.x] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
+      for (int r = lane; r < T.res_count; r += 32) cp_async8(V + T.res_local + r, a.in + (sbase + T.res_q + r) * K + col);
+      if (lane < 6) {
+        if (T.scratch >= 0) cp_async8(ROOT + 6 * t + lane, a.scratch + 6 * (int64_t)T.scratch + lane);
+        else if (a.op == RQ_OP_QTV) cp_async8(ROOT + 6 * t + lane, a.in + (3 * bead0 + lane) * K + col);
+        else ROOT[6 * t + lane] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
       }
     }
   }
@@ -371,6 +294,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[5];  // 0-2 heads, 3-4 level records
   const int tid = threadIdx.x;
+  const long long t_kernel0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
   const SmemMap SM = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, UP);
 #define HEAD(i) (smem + (size_t)(i) * SM.head)
 #define LREC(i) reinterpret_cast<double *>(smem + SM.o_lrec + (size_t)(i) * SM.lrec)
@@ -385,17 +309,26 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     fence_mbar_init();
   }
   __syncthreads();
+  // thread 0 keeps the descriptors of chunks k+2 and k+3 in registers (loaded
+  // one iteration before use, so no global latency sits on the critical path)
+  longlong2 dk2 = make_longlong2(0, 0), dk3 = make_longlong2(0, 0);  // {blob_off, off_rec | blob_bytes << 32}
+  auto ldesc = [&](int64_t k) -> longlong2 {
+    if (k >= cnt) return make_longlong2(0, 0);
+    const ChunkDesc *d = &a.chunks[blockIdx.x + k * G];
+    return make_longlong2(d->blob_off, (long long)(uint32_t)d->off_rec | ((long long)(uint32_t)d->blob_bytes << 32));
+  };
   if (tid == 0) {
     for (int64_t k = 0; k < 3 && k < cnt; k++) {
-      const ChunkDesc *d = &a.chunks[blockIdx.x + k * G];
-      const int64_t off = d->blob_off;
-      const unsigned hb = (unsigned)d->off_rec, rb = (unsigned)d->blob_bytes - hb;
-      if (rb) prefetch_l2(a.blob + off + hb, rb);
+      const longlong2 dd = ldesc(k);
+      const unsigned hb = (unsigned)(dd.y & 0xffffffffll), rb = (unsigned)(dd.y >> 32) - hb;
+      if (rb) prefetch_l2(a.blob + dd.x + hb, rb);
       if (k < 2) {
         mbar_expect_tx(&bar[k], hb);
-        bulk_g2s(HEAD(k), a.blob + off, hb, &bar[k]);
+        bulk_g2s(HEAD(k), a.blob + dd.x, hb, &bar[k]);
       }
     }
+    dk2 = ldesc(2);
+    dk3 = ldesc(3);
   }
   unsigned phase = 0;  // parity bit per barrier
   int64_t lctr = 0;    // level steps so far (selects the record stage)
@@ -414,17 +347,18 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     const int st = (int)(k % 3), fb = (int)(k & 1);
     if (tid == 0) {
       if (k + 2 < cnt) {  // head of chunk k+2 (stage of chunk k-1, released at the end of k-1)
-        const ChunkDesc *d = &a.chunks[blockIdx.x + (k + 2) * G];
         const int s2 = (int)((k + 2) % 3);
-        fence_proxy_async();
-        mbar_expect_tx(&bar[s2], (unsigned)d->off_rec);
-        bulk_g2s(HEAD(s2), a.blob + d->blob_off, (unsigned)d->off_rec, &bar[s2]);
+        const unsigned hb = (unsigned)(dk2.y & 0xffffffffll);
+        // WAR on smem (generic reads -> TMA write) is ordered by the barrier; no proxy fence needed
+        mbar_expect_tx(&bar[s2], hb);
+        bulk_g2s(HEAD(s2), a.blob + dk2.x, hb, &bar[s2]);
       }
-      if (k + 3 < cnt) {
-        const ChunkDesc *d = &a.chunks[blockIdx.x + (k + 3) * G];
-        const unsigned rb = (unsigned)(d->blob_bytes - d->off_rec);
-        if (rb) prefetch_l2(a.blob + d->blob_off + d->off_rec, rb);
+      if (k + 3 < cnt) {  // records of chunk k+3 into L2
+        const unsigned hb = (unsigned)(dk3.y & 0xffffffffll), rb = (unsigned)(dk3.y >> 32) - hb;
+        if (rb) prefetch_l2(a.blob + dk3.x + hb, rb);
       }
+      dk2 = dk3;
+      dk3 = ldesc(k + 4);
     }
     long long tc0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (k + 1 < cnt) {
@@ -440,11 +374,12 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     if (RQ_TIMING && a.dbg && tid == 0) { a.dbg[8 * blockIdx.x + 3] += clock64() - tc0; a.dbg[8 * blockIdx.x + 6] += 1; }
     const ChunkView cv = view(HEAD(st));
     const ChunkDesc &d = *cv.hdr;
-    const int64_t bead0 = a.bead_off[d.body];
-    const int64_t sbase = spec_base(a.op, a.bead_off, d.body);
+    const int64_t bead0 = d.body_bead0;
+    const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? d.spec_full : d.spec_comp;
     const double *grec = reinterpret_cast<const double *>(a.blob + d.blob_off + d.off_rec);
     double *M = reinterpret_cast<double *>(smem + SM.o_m);
     const int H = d.n_levels;
+    const long long t_lv0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (!UP) {
       for (int i = tid; i < 6 * d.n_tiles; i += NT) M[6 * cv.tiles[i / 6].root_slot + i % 6] = ROOTBUF(fb)[i];
       __syncthreads();
@@ -468,7 +403,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
           bytes = 8u * (unsigned)level_rec_doubles(L2);
         }
         if (g2) {
-          fence_proxy_async();
+          // WAR on smem (generic reads -> TMA write) is ordered by the barrier; no proxy fence needed
           mbar_expect_tx(&bar[3 + (ls ^ 1)], bytes);
           bulk_g2s(LREC(ls ^ 1), g2, bytes, &bar[3 + (ls ^ 1)]);
         }
@@ -479,34 +414,38 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       long long tw1 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       const double *R = LREC(ls);
       const int oR = rec_size(GENERAL) * L.nG, oB = oR + rec_size(RIGID_BEAD) * L.nR;
-      const int nGR = L.nG + L.nR;
-      const int gGR = (nGR + 31) & ~31;  // case-uniform warps: GEN+RB group padded to whole warps
-      const int tot = gGR + L.nB;
+      // case-uniform warps: GEN and RB groups each padded to whole warps
+      const int gG = (L.nG + 31) & ~31, gR = (L.nR + 31) & ~31;
+      const int tot = gG + gR + L.nB;
       if (UP) {
         const double *F = VBUF(fb);
         double *RES = reinterpret_cast<double *>(smem + SM.o_x);
         for (int q = tid; q < tot; q += NT) {
-          if (q < gGR) {
-            if (q < nGR)
-              up_node9(L.slot_begin + q, R + (q < L.nG ? q * rec_size(GENERAL) : oR + (q - L.nG) * rec_size(RIGID_BEAD)),
-                       cv.ME, M, F, RES);
+          if (q < gG) {
+            if (q < L.nG) up_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < L.nR)
+              up_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
           } else {
-            const int qq = q - gGR;
-            up_node<BEAD_BEAD>(L.slot_begin + nGR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
+            const int qq = q - gG - gR;
+            up_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
           }
         }
       } else {
         const double *RES = VBUF(fb);
         double *F = reinterpret_cast<double *>(smem + SM.o_x);
         for (int q = tid; q < tot; q += NT) {
-          if (q < gGR) {
-            if (q < nGR)
-              down_node9(L.slot_begin + q,
-                         R + (q < L.nG ? q * rec_size(GENERAL) : oR + (q - L.nG) * rec_size(RIGID_BEAD)), cv.ME, M, F,
-                         RES);
+          if (q < gG) {
+            if (q < L.nG) down_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < L.nR)
+              down_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
           } else {
-            const int qq = q - gGR;
-            down_node<BEAD_BEAD>(L.slot_begin + nGR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
+            const int qq = q - gG - gR;
+            down_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F,
+                                 RES);
           }
         }
       }
@@ -516,20 +455,22 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
         long long tw3 = clock64();
         a.dbg[8 * blockIdx.x + 0] += tw1 - tw0;  // level record wait
         a.dbg[8 * blockIdx.x + 1] += tw2 - tw1;  // tid0 node work
-        a.dbg[8 * blockIdx.x + 2] += tw3 - tw2;  // barrier
+        (void)tw3;
         a.dbg[8 * blockIdx.x + 4] += 1;          // level steps
       }
     }
     long long to0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
+    if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 2] += to0 - t_lv0;  // whole level loop
     if (UP) {
       const double *RES = reinterpret_cast<const double *>(smem + SM.o_x);
-      for (int t = 0; t < d.n_tiles; t++) {  // residues (contiguous per tile) and tile-root info vectors
+      const int wid = tid >> 5, lane = tid & 31;
+      for (int t = wid; t < d.n_tiles; t += NT / 32) {  // residues (contiguous per tile) and tile-root info vectors
         const TileDesc T = cv.tiles[t];
-        for (int r = tid; r < T.res_count; r += NT) a.out[(sbase + T.res_q + r) * K + col] = RES[T.res_local + r];
-        if (tid < 6) {
-          const double v = M[6 * T.root_slot + tid];
-          if (T.scratch >= 0) a.scratch[6 * (int64_t)T.scratch + tid] = v;
-          else if (a.op == RQ_OP_QV) a.out[(3 * bead0 + tid) * K + col] = v;
+        for (int r = lane; r < T.res_count; r += 32) a.out[(sbase + T.res_q + r) * K + col] = RES[T.res_local + r];
+        if (lane < 6) {
+          const double v = M[6 * T.root_slot + lane];
+          if (T.scratch >= 0) a.scratch[6 * (int64_t)T.scratch + lane] = v;
+          else if (a.op == RQ_OP_QV) a.out[(3 * bead0 + lane) * K + col] = v;
         }
       }
     } else {
@@ -547,6 +488,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     __syncthreads();
     if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 5] += clock64() - to0;
   }
+  if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 7] = clock64() - t_kernel0;
 #undef HEAD
 #undef LREC
 #undef VBUF
@@ -556,6 +498,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
 // ---- top tree (nodes with more than tile_leaves beads) ---------------------------------
 
 struct TopCtx {
+  const int32_t *tb_list;  // top-body indices processed by this launch
   const TopNode *top;
   const int32_t *topbody, *topbody_lvl, *toplvl, *perm;
   const int64_t *bead_off;
@@ -569,7 +512,7 @@ struct TopCtx {
 
 template <bool UP>
 __global__ void __launch_bounds__(NT_TOP) k_top(TopCtx a) {
-  const int bi = blockIdx.x;
+  const int bi = a.tb_list[blockIdx.x];
   const int j = a.topbody[bi];
   const int64_t bead0 = a.bead_off[j];
   const int64_t sbase = spec_base(a.op, a.bead_off, j);
@@ -639,6 +582,120 @@ __global__ void __launch_bounds__(NT_TOP) k_top(TopCtx a) {
   }
 }
 
+
+// ---- staged top tree: one CTA per body, whole top tree in shared memory --------------
+
+struct Top2Ctx {
+  const uint8_t *blob;
+  const int64_t *blob_off;
+  const int64_t *bead_off;
+  const double *in;
+  double *out;
+  int64_t k, col;
+  double *scratch;
+  int op;
+};
+
+template <bool UP>
+__global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
+  if (tid == 0) {
+    const unsigned bytes = (unsigned)reinterpret_cast<const TopHdr *>(gB)->bytes;
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(smem, gB, bytes, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const TopHdr h = *reinterpret_cast<const TopHdr *>(smem);
+  const int32_t *LB = reinterpret_cast<const int32_t *>(smem + sizeof(TopHdr));
+  const TopMeta *MD = reinterpret_cast<const TopMeta *>(smem + h.off_meta);
+  const int32_t *INREF = reinterpret_cast<const int32_t *>(smem + h.off_in);
+  const double *REC = reinterpret_cast<const double *>(smem + h.off_rec);
+  double *IN = reinterpret_cast<double *>(smem + (h.bytes + 127) / 128 * 128);
+  double *MT = IN + 6 * h.n_inputs;
+  double *RT = MT + 6 * h.n_nodes;
+  const int64_t K = a.k, col = a.col;
+  const int64_t bead0 = a.bead_off[h.body];
+  const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)h.body;
+  if (UP) {
+    for (int i = tid; i < 6 * h.n_inputs; i += NT_TOP) {
+      const int q = i / 6, r = i % 6;
+      const int32_t ref = INREF[q];
+      double v;
+      if (ref >= 0) v = __ldcg(&a.scratch[6 * (int64_t)ref + r]);
+      else v = r < 3 ? a.in[((bead0 + ~(int64_t)ref) * 3 + r) * K + col] : 0.0;
+      IN[i] = v;
+    }
+    __syncthreads();
+    for (int lv = 0; lv < h.n_levels; lv++) {
+      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NT_TOP) {
+        const TopMeta md = MD[q];
+        const int cs = flag_case(md.flags);
+        const double *rec = REC + md.rec;
+        double mx[6], my[6], mp[6], res[6], aa, bb;
+        const double *px = md.x >= 0 ? MT + 6 * md.x : IN + 6 * ~(int)md.x;
+        const double *py = md.y >= 0 ? MT + 6 * md.y : IN + 6 * ~(int)md.y;
+#pragma unroll
+        for (int r = 0; r < 6; r++) { mx[r] = px[r]; my[r] = py[r]; }
+        rec_ratios(cs, rec, 1, aa, bb);
+        merge(cs, rec, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
+        const int rr = res_rows(cs);
+        for (int r = 0; r < rr; r++) a.out[(sbase + md.res_q + r) * K + col] = res[r];
+        if (md.is_root && a.op == RQ_OP_QV)
+          for (int r = 0; r < 6; r++) a.out[(3 * bead0 + r) * K + col] = mp[r];
+#pragma unroll
+        for (int r = 0; r < 6; r++) MT[6 * q + r] = mp[r];
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int q = tid; q < h.n_nodes; q += NT_TOP) {
+      const TopMeta md = MD[q];
+      const int rr = res_rows(flag_case(md.flags));
+      for (int r = 0; r < rr; r++) RT[6 * q + r] = a.in[(sbase + md.res_q + r) * K + col];
+      if (md.is_root)
+        for (int r = 0; r < 6; r++) MT[6 * q + r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * K + col] : 0.0;
+    }
+    __syncthreads();
+    for (int lv = h.n_levels - 1; lv >= 0; lv--) {
+      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NT_TOP) {
+        const TopMeta md = MD[q];
+        const int cs = flag_case(md.flags);
+        const double *rec = REC + md.rec;
+        double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6], aa, bb;
+#pragma unroll
+        for (int r = 0; r < 6; r++) lp[r] = MT[6 * q + r];
+        const int rr = res_rows(cs);
+        for (int r = 0; r < rr; r++) res[r] = RT[6 * q + r];
+        rec_ratios(cs, rec, 1, aa, bb);
+        split(cs, rec, 1, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
+        auto put = [&](int16_t ref, const double (&l)[6]) {
+          if (ref >= 0) {
+#pragma unroll
+            for (int r = 0; r < 6; r++) MT[6 * ref + r] = l[r];
+          } else {
+            const int32_t in = INREF[~(int)ref];
+            if (in >= 0) {
+              for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)in + r] = l[r];
+            } else {
+              const int64_t row = (bead0 + ~(int64_t)in) * 3;
+              for (int r = 0; r < 3; r++) a.out[(row + r) * K + col] = l[r];
+            }
+          }
+        };
+        put(md.x, lx);
+        put(md.y, ly);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // single-bead bodies: Qv and Q^T w are the identity (matfree.py:99-100, 127-128)
 __global__ void k_small(const int32_t *bodies, int64_t n, const int64_t *bead_off, const double *in,
                         double *out, int64_t K, int64_t col) {
@@ -682,6 +739,7 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   int occ = 0;
   RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)cfg.fn, cfg.threads, cfg.smem));
   if (occ < 1) throw Error(RQ_ERR_CUDA, "chunk kernel does not fit on an SM (smem " + std::to_string(cfg.smem) + ")");
+  if (const char *e = getenv("RQ_CTAS_PER_SM")) occ = std::max(1, std::min(occ, atoi(e)));
   cfg.grid = (int)std::min<int64_t>(p.n_chunks, (int64_t)sms * occ);
   return cfg;
 }
@@ -719,6 +777,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     a.dbg = dbg.as<long long>();
   }
   TopCtx t{};
+  t.tb_list = p.topbig.as<int32_t>();
   t.top = p.top.as<TopNode>();
   t.topbody = p.topbody.as<int32_t>();
   t.topbody_lvl = p.topbody_lvl.as<int32_t>();
@@ -731,15 +790,40 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.k = k;
   t.scratch = p.scratch.as<double>();
   t.op = op;
+  Top2Ctx t2{};
+  t2.blob = p.topblob.as<uint8_t>();
+  t2.blob_off = p.topblob_off.as<int64_t>();
+  t2.bead_off = p.bead_off_d.as<int64_t>();
+  t2.in = in;
+  t2.out = out;
+  t2.k = k;
+  t2.scratch = p.scratch.as<double>();
+  t2.op = op;
+  const size_t top_smem = (size_t)p.max_topblob_smem;
+  if (p.n_topblob) {
+    const void *f2 = up ? (const void *)k_top2<true> : (const void *)k_top2<false>;
+    RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)top_smem));
+  }
   for (int64_t col = 0; col < k; col++) {
     a.col = col;
     t.col = col;
+    t2.col = col;
     const bool do_chunks = (phases & 1u) && p.n_chunks, do_top = (phases & 2u) && p.n_topbodies;
+    auto top_pass = [&]() {
+      if (p.n_topblob) {
+        if (up) k_top2<true><<<(unsigned)p.n_topblob, NT_TOP, top_smem, s>>>(t2);
+        else k_top2<false><<<(unsigned)p.n_topblob, NT_TOP, top_smem, s>>>(t2);
+      }
+      if (p.n_topbig) {
+        if (up) k_top<true><<<(unsigned)p.n_topbig, NT_TOP, 0, s>>>(t);
+        else k_top<false><<<(unsigned)p.n_topbig, NT_TOP, 0, s>>>(t);
+      }
+    };
     if (up) {
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
-      if (do_top) k_top<true><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
+      if (do_top) top_pass();
     } else {
-      if (do_top) k_top<false><<<(unsigned)p.n_topbodies, NT_TOP, 0, s>>>(t);
+      if (do_top) top_pass();
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
     }
     if (timing && do_chunks) {
@@ -748,9 +832,9 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       RQ_CUDA(cudaStreamSynchronize(s));
       double acc[8] = {0};
       for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) acc[i] += (double)h[8 * g + i];
-      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f barrier %.0f | per chunk: head+vec wait %.0f, out %.0f, level steps %.1f, chunks/CTA %.1f\n",
+      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f level-total %.0f | per chunk: head+vec wait %.0f, out %.0f, level steps %.1f, chunks/CTA %.1f, CTA total %.0f (max %.0f)\n",
               op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[4], acc[1] / acc[4], acc[2] / acc[4], acc[3] / acc[6],
-              acc[5] / acc[6], acc[4] / acc[6], acc[6] / cfg.grid);
+              acc[5] / acc[6], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
       RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
     }
     if ((phases & 4u) && p.n_small && op <= 1)

@@ -26,10 +26,10 @@ __host__ __device__ inline bool flag_swapped(unsigned f) { return (f >> 2) & 1u;
 __host__ __device__ inline unsigned flag_signs(unsigned f) { return (f >> 3) & 7u; }
 
 // compact record sizes (doubles): BEAD_BEAD explicit 3x3 g; RIGID_BEAD /
-// GENERAL Householder record (HH<6> / HH<9>) followed by the ratios a, b.
+// GENERAL compact-WY record (WY<6> / WY<9>) followed by the ratios a, b.
 // Padded to an even count so records stay 16-byte aligned (LDS.128 / double2).
 __host__ __device__ constexpr int rec_size(int c) {
-  return c == BEAD_BEAD ? 10 : (c == RIGID_BEAD ? 18 : (c == GENERAL ? 26 : 0));
+  return c == BEAD_BEAD ? 10 : (c == RIGID_BEAD ? 20 : (c == GENERAL ? 30 : 0));
 }
 __host__ __device__ constexpr int res_rows(int c) {
   return c == RIGID_BEAD ? 3 : (c == GENERAL ? 6 : 0);
@@ -66,7 +66,11 @@ struct ChunkDesc {
   int32_t off_perm;
   int32_t off_rec;
   int32_t n_res;         // residue doubles staged
-};
+  int64_t body_bead0;    // first (global) bead of the body
+  int64_t spec_full;     // first residue row of the body in the Q layout (3 bead0 + 6)
+  int64_t spec_comp;     // first residue row of the body in the Q~ layout (3 bead0 - 6 body)
+  int64_t pad;
+};  // 96 bytes
 
 struct TileDesc {        // 32 bytes; copies live in the chunk blob after the ChunkDesc header
   int32_t root_slot;     // chunk-local slot of the tile root
@@ -88,32 +92,106 @@ struct TopNode {         // node with more than tile_leaves beads
   int64_t rec_off;       // offset of its record in the compact record table
 };
 
+// Per-body top-tree blob (one TMA bulk copy per body, swept in shared memory):
+//   TopHdr | int32 level_begin[n_levels+1] | TopMeta[n_nodes] | int32 inputs[n_inputs] | records
+struct TopHdr {          // 32 bytes
+  int32_t n_nodes, n_levels, n_inputs, body;
+  int32_t off_meta, off_in, off_rec, bytes;
+};
+struct TopMeta {         // 16 bytes, nodes sorted by height
+  int16_t x, y;          // >= 0: local top node; < 0: ~input index
+  uint16_t flags;
+  uint16_t is_root;
+  int32_t res_q;         // body-relative Q~ offset of its residue rows (-1 if none)
+  int32_t rec;           // double offset of its record in the record area
+};
+// top-blob inputs: >= 0 exchange slot (a tile root), < 0 ~(body-local original bead index)
+
 // perm entries in a chunk blob: body-local original bead index, or
 // (PERM_FOREIGN | idx) for beads handled by the top tree (singleton tiles).
 constexpr uint32_t PERM_FOREIGN = 0x80000000u;
 constexpr uint16_t SRC_BEAD = 0x8000u;
 
-// ---- device math --------------------------------------------------------
-
-// Apply H_i = I - tau v v^T (v[i] = 1 implicit, v[j<i] = 0) to y (length K).
-template <int K>
-__host__ __device__ __forceinline__ void householder(double (&y)[K], const double* vi, double tau, int i) {
-  double d = y[i];
-#pragma unroll
-  for (int j = i + 1; j < K; j++) d += vi[j - i - 1] * y[j];
-  double td = tau * d;
-  y[i] -= td;
-#pragma unroll
-  for (int j = i + 1; j < K; j++) y[j] -= td * vi[j - i - 1];
-}
-
-// Record layout for K in {6, 9}: v0 (K-1), v1 (K-2), v2 (K-3), tau0, tau1, tau2.
+// Householder work layout for K in {3, 6, 9}: v0 (K-1), v1 (K-2), v2 (K-3), tau0, tau1, tau2.
 template <int K>
 struct HH {
   static constexpr int O0 = 0, O1 = K - 1, O2 = 2 * K - 3, OT = 3 * K - 6, SIZE = 3 * K - 3;
-  static constexpr int RA = SIZE, RB = SIZE + 1;  // ratios a = sqrt(n_x/n), b = sqrt(n_y/n)
+};
+
+// Compact-WY record: Q = H0 H1 H2 = I - V T V^T (V unit lower trapezoidal, T
+// upper triangular 3x3, LAPACK dlarft 'F','C').  omega = S Q^T.
+//   V0 (K-1: rows 1..K-1) | V1 (K-2: rows 2..) | V2 (K-3: rows 3..) |
+//   T00 T01 T02 T11 T12 T22 | a = sqrt(n_x/n) | b = sqrt(n_y/n)
+template <int K>
+struct WY {
+  static constexpr int V0 = 0, V1 = K - 1, V2 = 2 * K - 3, T = 3 * K - 6;
+  static constexpr int RA = 3 * K, RB = 3 * K + 1, SIZE = 3 * K + 2;
 };
 // NodeFactor.ratios of a BEAD_BEAD node: sqrt(1/2) (factor.py:85-87)
 constexpr double BB_RATIO = 0.70710678118654757;
+
+
+// ---- device math --------------------------------------------------------
+
+// y <- (I - V T' V^T) y with T' = T (trans = false) or T^T (trans = true);
+// record in the WY<K> layout, element e at rec[e * st].
+template <int K, bool TRANS>
+__host__ __device__ __forceinline__ void wy_apply(const double *rec, int st, double (&y)[K]) {
+  using W = WY<K>;
+  // w = V^T y (implicit unit diagonal), two accumulators per dot
+  double w0a = y[0], w0b = 0.0, w1a = y[1], w1b = 0.0, w2a = y[2], w2b = 0.0;
+#pragma unroll
+  for (int j = 1; j < K; j++) {
+    const double v = rec[(W::V0 + j - 1) * st];
+    if (j & 1) w0b = fma(v, y[j], w0b); else w0a = fma(v, y[j], w0a);
+  }
+#pragma unroll
+  for (int j = 2; j < K; j++) {
+    const double v = rec[(W::V1 + j - 2) * st];
+    if (j & 1) w1b = fma(v, y[j], w1b); else w1a = fma(v, y[j], w1a);
+  }
+#pragma unroll
+  for (int j = 3; j < K; j++) {
+    const double v = rec[(W::V2 + j - 3) * st];
+    if (j & 1) w2b = fma(v, y[j], w2b); else w2a = fma(v, y[j], w2a);
+  }
+  const double w0 = w0a + w0b, w1 = w1a + w1b, w2 = w2a + w2b;
+  const double T00 = rec[(W::T + 0) * st], T01 = rec[(W::T + 1) * st], T02 = rec[(W::T + 2) * st];
+  const double T11 = rec[(W::T + 3) * st], T12 = rec[(W::T + 4) * st], T22 = rec[(W::T + 5) * st];
+  double z0, z1, z2;
+  if (TRANS) {  // T^T (lower)
+    z0 = T00 * w0;
+    z1 = fma(T01, w0, T11 * w1);
+    z2 = fma(T02, w0, fma(T12, w1, T22 * w2));
+  } else {      // T (upper)
+    z0 = fma(T00, w0, fma(T01, w1, T02 * w2));
+    z1 = fma(T11, w1, T12 * w2);
+    z2 = T22 * w2;
+  }
+  y[0] -= z0;
+  y[1] -= fma(rec[(W::V0 + 0) * st], z0, z1);
+  y[2] -= fma(rec[(W::V0 + 1) * st], z0, fma(rec[(W::V1 + 0) * st], z1, z2));
+#pragma unroll
+  for (int j = 3; j < K; j++)
+    y[j] -= fma(rec[(W::V0 + j - 1) * st], z0, fma(rec[(W::V1 + j - 2) * st], z1, rec[(W::V2 + j - 3) * st] * z2));
+}
+
+// y <- omega y = S Q^T y
+template <int K>
+__host__ __device__ __forceinline__ void omega_wy(const double *rec, int st, unsigned signs, double (&y)[K]) {
+  wy_apply<K, true>(rec, st, y);
+  if (signs & 1u) y[0] = -y[0];
+  if (signs & 2u) y[1] = -y[1];
+  if (signs & 4u) y[2] = -y[2];
+}
+
+// y <- omega^T y = Q S y
+template <int K>
+__host__ __device__ __forceinline__ void omega_t_wy(const double *rec, int st, unsigned signs, double (&y)[K]) {
+  if (signs & 1u) y[0] = -y[0];
+  if (signs & 2u) y[1] = -y[1];
+  if (signs & 4u) y[2] = -y[2];
+  wy_apply<K, false>(rec, st, y);
+}
 
 }  // namespace rq

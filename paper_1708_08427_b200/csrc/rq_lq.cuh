@@ -85,15 +85,15 @@ __host__ __device__ inline void lq_dlarf_left(int m, int n, const double *v, dou
 }
 
 // small_lq in compact form.  a: row-major 3 x K (== column-major K x 3 A = a^T).
-// Outputs t (lower-triangular, packed t00,t10,t11,t20,t21,t22), the
-// Householder record (HH<K> layout) and the sign bits s_i = -1.
+// Outputs t (lower-triangular, packed t00,t10,t11,t20,t21,t22), the compact-WY
+// record (WY<K> layout, without the ratios) and the sign bits s_i = -1.
 template <int K>
 __host__ __device__ inline void lq_factor(const double *a, double t6[6], double *rec, unsigned &signs) {
   bool any = false;
   for (int i = 0; i < 3 * K; i++) any |= (a[i] != 0.0);
-  for (int i = 0; i < HH<K>::SIZE; i++) rec[i] = 0.0;
+  for (int i = 0; i < WY<K>::RA; i++) rec[i] = 0.0;
   signs = 0;
-  if (!any) { // factor.py:100-101: t = 0, omega = I_k
+  if (!any) { // factor.py:100-101: t = 0, omega = I_k  (V = 0, T = 0)
     for (int i = 0; i < 6; i++) t6[i] = 0.0;
     return;
   }
@@ -124,35 +124,38 @@ __host__ __device__ inline void lq_factor(const double *a, double t6[6], double 
   t6[3] = A[2 * K + 0] * s[0];
   t6[4] = A[2 * K + 1] * s[1];
   t6[5] = A[2 * K + 2] * s[2];
-  // reflector vectors (rows below the diagonal) + taus
+  // V (rows below the diagonal) and T (dlarft forward/columnwise)
   int o = 0;
   for (int i = 0; i < 3; i++)
     for (int r = i + 1; r < K; r++) rec[o++] = A[i * K + r];
-  rec[HH<K>::OT + 0] = tau[0];
-  rec[HH<K>::OT + 1] = tau[1];
-  rec[HH<K>::OT + 2] = tau[2];
+  auto vdot = [&](int i, int j) {  // v_i^T v_j for i < j (v_i[i] = 1, v_j[j] = 1, v_j[r < j] = 0)
+    double d = (j < K) ? A[i * K + j] : 0.0;
+    for (int r = j + 1; r < K; r++) d += A[i * K + r] * A[j * K + r];
+    return d;
+  };
+  const double T00 = tau[0], T11 = tau[1], T22 = tau[2];
+  const double T01 = -tau[1] * T00 * vdot(0, 1);
+  const double t0 = vdot(0, 2), t1 = vdot(1, 2);
+  const double T02 = -tau[2] * (T00 * t0 + T01 * t1);
+  const double T12 = -tau[2] * (T11 * t1);
+  rec[WY<K>::T + 0] = T00;
+  rec[WY<K>::T + 1] = T01;
+  rec[WY<K>::T + 2] = T02;
+  rec[WY<K>::T + 3] = T11;
+  rec[WY<K>::T + 4] = T12;
+  rec[WY<K>::T + 5] = T22;
 }
 
-// y <- omega y  = S H2 H1 H0 y   (record with unit stride)
+// y <- omega y  = S Q^T y   (record with unit stride)
 template <int K>
 __host__ __device__ inline void omega_apply(const double *rec, unsigned signs, double (&y)[K]) {
-  householder<K>(y, rec + HH<K>::O0, rec[HH<K>::OT + 0], 0);
-  householder<K>(y, rec + HH<K>::O1, rec[HH<K>::OT + 1], 1);
-  householder<K>(y, rec + HH<K>::O2, rec[HH<K>::OT + 2], 2);
-#pragma unroll
-  for (int i = 0; i < 3; i++)
-    if (signs & (1u << i)) y[i] = -y[i];
+  omega_wy<K>(rec, 1, signs, y);
 }
 
-// y <- omega^T y = H0 H1 H2 S y
+// y <- omega^T y = Q S y
 template <int K>
 __host__ __device__ inline void omega_apply_t(const double *rec, unsigned signs, double (&y)[K]) {
-#pragma unroll
-  for (int i = 0; i < 3; i++)
-    if (signs & (1u << i)) y[i] = -y[i];
-  householder<K>(y, rec + HH<K>::O2, rec[HH<K>::OT + 2], 2);
-  householder<K>(y, rec + HH<K>::O1, rec[HH<K>::OT + 1], 1);
-  householder<K>(y, rec + HH<K>::O0, rec[HH<K>::OT + 0], 0);
+  omega_t_wy<K>(rec, 1, signs, y);
 }
 
 __host__ __device__ inline void skew3(const double r[3], double A[9]) { // model.py:25-30
@@ -187,7 +190,7 @@ __host__ __device__ inline void factor_bead_bead_frame(const double d[3], double
       m[ax[i] * 3 + j] = tp[i * 3 + j];   // m[perm, :] = t_prime
       gh[i * 3 + ax[j]] = uh[i * 3 + j];  // g_half[:, perm] = u_half
     }
-  double rec3[HH<3>::SIZE];
+  double rec3[WY<3>::SIZE];
   unsigned sg;
   lq_factor<3>(m, t6, rec3, sg);
   double om3[9];

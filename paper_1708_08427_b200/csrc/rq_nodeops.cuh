@@ -8,50 +8,20 @@
 
 namespace rq {
 
-// Apply H_i (reflector stored at rec[(o + e) * st], e = 0 .. K-i-2) to y.
-template <int K>
-__device__ __forceinline__ void hh_s(double (&y)[K], const double *rec, int st, int o, double tau, int i) {
-  // two interleaved partial dot products: halves the dependent FMA chain
-  double d0 = y[i], d1 = 0.0;
-#pragma unroll
-  for (int j = i + 1; j < K; j++) {
-    if ((j - i) & 1) d1 = fma(rec[(o + j - i - 1) * st], y[j], d1);
-    else d0 = fma(rec[(o + j - i - 1) * st], y[j], d0);
-  }
-  const double td = tau * (d0 + d1);
-  y[i] -= td;
-#pragma unroll
-  for (int j = i + 1; j < K; j++) y[j] = fma(-td, rec[(o + j - i - 1) * st], y[j]);
-}
-
-// y <- omega y = S H2 H1 H0 y
+// y <- omega y (S Q^T y) and y <- omega^T y (Q S y) from a compact-WY record
 template <int K>
 __device__ __forceinline__ void omega_s(const double *rec, int st, unsigned signs, double (&y)[K]) {
-  const double t0 = rec[(HH<K>::OT + 0) * st], t1 = rec[(HH<K>::OT + 1) * st], t2 = rec[(HH<K>::OT + 2) * st];
-  hh_s<K>(y, rec, st, HH<K>::O0, t0, 0);
-  hh_s<K>(y, rec, st, HH<K>::O1, t1, 1);
-  hh_s<K>(y, rec, st, HH<K>::O2, t2, 2);
-  if (signs & 1u) y[0] = -y[0];
-  if (signs & 2u) y[1] = -y[1];
-  if (signs & 4u) y[2] = -y[2];
+  omega_wy<K>(rec, st, signs, y);
 }
-
-// y <- omega^T y = H0 H1 H2 S y
 template <int K>
 __device__ __forceinline__ void omega_t_s(const double *rec, int st, unsigned signs, double (&y)[K]) {
-  if (signs & 1u) y[0] = -y[0];
-  if (signs & 2u) y[1] = -y[1];
-  if (signs & 4u) y[2] = -y[2];
-  const double t0 = rec[(HH<K>::OT + 0) * st], t1 = rec[(HH<K>::OT + 1) * st], t2 = rec[(HH<K>::OT + 2) * st];
-  hh_s<K>(y, rec, st, HH<K>::O2, t2, 2);
-  hh_s<K>(y, rec, st, HH<K>::O1, t1, 1);
-  hh_s<K>(y, rec, st, HH<K>::O0, t0, 0);
+  omega_t_wy<K>(rec, st, signs, y);
 }
 
 // ratios stored in the record (RIGID_BEAD / GENERAL) or the BEAD_BEAD constant
 __device__ __forceinline__ void rec_ratios(int cs, const double *rec, int st, double &a, double &b) {
-  if (cs == GENERAL) { a = rec[HH<9>::RA * st]; b = rec[HH<9>::RB * st]; }
-  else if (cs == RIGID_BEAD) { a = rec[HH<6>::RA * st]; b = rec[HH<6>::RB * st]; }
+  if (cs == GENERAL) { a = rec[WY<9>::RA * st]; b = rec[WY<9>::RB * st]; }
+  else if (cs == RIGID_BEAD) { a = rec[WY<6>::RA * st]; b = rec[WY<6>::RB * st]; }
   else { a = BB_RATIO; b = BB_RATIO; }
 }
 

@@ -14,7 +14,7 @@ namespace {
 
 template <int K>
 __device__ void small_lq_one(const double *a, double *t, double *om) {
-  double t6[6], rec[HH<K>::SIZE];
+  double t6[6], rec[WY<K>::SIZE];
   unsigned sg;
   lq_factor<K>(a, t6, rec, sg);
   t[0] = t6[0]; t[1] = 0.0;   t[2] = 0.0;

@@ -115,6 +115,13 @@ struct Plan {
   DBuf topbody_lvl;                // int32 [n_topbodies+1]: level CSR into toplvl
   DBuf toplvl;                     // int32 [n_toplevels+1]: top index ranges per level
   DBuf small_bodies;               // int32 [n_small]
+  // staged top tree (bodies whose top blob fits shared memory)
+  int64_t n_topblob = 0, max_topblob_smem = 0;
+  DBuf topblob;                    // bytes
+  DBuf topblob_off;                // int64 [n_topblob]: blob byte offsets
+  DBuf topblob_body;               // int32 [n_topblob]: top-body index (into topbody)
+  DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
+  int64_t n_topbig = 0;
   mutable DBuf scratch;            // double [6 * n_slots * kcap]
   mutable int64_t scratch_k = 0;
   DBuf err;                        // int64 [8] device error flags

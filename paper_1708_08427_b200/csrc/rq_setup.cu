@@ -405,11 +405,11 @@ __global__ void k_factor(FactorCtx c, int64_t N) {
           cpl[a * 6 + b] = tg[a * 3 + b];
           cpl[a * 6 + 3 + b] = sc * R[a * 3 + b];
         }
-      double hh[HH<6>::SIZE];
-      lq_factor<6>(cpl, t6, hh, signs);
-      for (int a = 0; a < HH<6>::SIZE; a++) rec[a] = hh[a];
-      rec[HH<6>::RA] = sqrt((double)nx / (double)n);  // NodeFactor.ratios (factor.py:85-87)
-      rec[HH<6>::RB] = sqrt(1.0 / (double)n);
+      double wy[WY<6>::SIZE];
+      lq_factor<6>(cpl, t6, wy, signs);
+      for (int a = 0; a < WY<6>::RA; a++) rec[a] = wy[a];
+      rec[WY<6>::RA] = sqrt((double)nx / (double)n);  // NodeFactor.ratios (factor.py:85-87)
+      rec[WY<6>::RB] = sqrt(1.0 / (double)n);
     } else {  // factor.py:237-243, 181-188
       double dr[3], R[9];
       for (int a = 0; a < 3; a++) dr[a] = cl[a] - cp[a];
@@ -422,11 +422,11 @@ __global__ void k_factor(FactorCtx c, int64_t N) {
           cpl[a * 9 + 3 + b] = tr[a * 3 + b];
           cpl[a * 9 + 6 + b] = sc * R[a * 3 + b];
         }
-      double hh[HH<9>::SIZE];
-      lq_factor<9>(cpl, t6, hh, signs);
-      for (int a = 0; a < HH<9>::SIZE; a++) rec[a] = hh[a];
-      rec[HH<9>::RA] = sqrt((double)nl / (double)n);
-      rec[HH<9>::RB] = sqrt((double)nr / (double)n);
+      double wy[WY<9>::SIZE];
+      lq_factor<9>(cpl, t6, wy, signs);
+      for (int a = 0; a < WY<9>::RA; a++) rec[a] = wy[a];
+      rec[WY<9>::RA] = sqrt((double)nl / (double)n);
+      rec[WY<9>::RB] = sqrt((double)nr / (double)n);
     }
     for (int a = 0; a < 3; a++) c.centroid[g * 3 + a] = cp[a];
     for (int a = 0; a < 6; a++) c.t22[g * 6 + a] = t6[a];
@@ -529,6 +529,10 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
       d.n_tiles = ntiles;
       d.body = (int32_t)j;
       d.bead_begin = bead_off[j] + bead0;
+      d.body_bead0 = bead_off[j];
+      d.spec_full = 3 * bead_off[j] + 6;
+      d.spec_comp = 3 * bead_off[j] - 6 * j;
+      d.pad = 0;
       d.tile_begin = big_scan[tile0];
       d.n_res = res;
       d.off_meta = (int32_t)head_bytes(ntiles, H);
@@ -802,6 +806,92 @@ __global__ void k_top_levels(const uint64_t *keys_sorted, const int32_t *flag, c
   if (p == 0 || (keys_sorted[p - 1] >> 32) != (uint64_t)j) topbody_lvl[topbody_idx[j]] = lv;
 }
 
+
+// ---- staged top-tree blobs ------------------------------------------------------------
+
+__global__ void k_top_slotmap(const TopNode *top, int64_t nt, const int32_t *topbody_idx, const int32_t *topbody_lvl,
+                              const int32_t *toplvl, int32_t *slot_to_local, int32_t *nin, int64_t *recsz) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nt) return;
+  const TopNode T = top[p];
+  const int bi = topbody_idx[T.body];
+  const int first = toplvl[topbody_lvl[bi]];
+  slot_to_local[T.self_slot] = (int32_t)(p - first);
+  recsz[p] = rec_size(flag_case(T.flags));
+  (void)nin;
+}
+
+__global__ void k_top_inputs(const TopNode *top, int64_t nt, const int32_t *slot_to_local, int32_t *nin) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nt) return;
+  const TopNode T = top[p];
+  int c = 0;
+  if (T.x < 0 || slot_to_local[T.x] < 0) c++;
+  if (T.y < 0 || slot_to_local[T.y] < 0) c++;
+  nin[p] = c;
+}
+
+__host__ __device__ inline int64_t topblob_bytes(int n_nodes, int n_levels, int n_inputs, int64_t rec) {
+  int64_t b = sizeof(TopHdr);
+  b += ((int64_t)(n_levels + 1) * 4 + 15) / 16 * 16;
+  b += (int64_t)n_nodes * sizeof(TopMeta);
+  b += ((int64_t)n_inputs * 4 + 15) / 16 * 16;
+  b += rec * 8;
+  return (b + 15) / 16 * 16;
+}
+
+// one thread per top node: writes its meta, inputs and record; the body's first
+// node also writes the header and level table
+__global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *topbody_idx, const int32_t *topbody_lvl,
+                           const int32_t *toplvl, const int32_t *slot_to_local, const int32_t *in_scan,
+                           const int64_t *rec_scan, const int64_t *blob_off_of_tb, const double *rec,
+                           const int32_t *perm, const int64_t *bead_off, uint8_t *blob) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= nt) return;
+  const TopNode T = top[p];
+  const int bi = topbody_idx[T.body];
+  const int lv0 = topbody_lvl[bi], lv1 = topbody_lvl[bi + 1];
+  const int first = toplvl[lv0], last = toplvl[lv1];
+  const int n_nodes = last - first, n_levels = lv1 - lv0;
+  const int n_inputs = in_scan[last] - in_scan[first];
+  const int64_t n_rec = rec_scan[last] - rec_scan[first];
+  uint8_t *B = blob + blob_off_of_tb[bi];
+  TopHdr h;
+  h.n_nodes = n_nodes;
+  h.n_levels = n_levels;
+  h.n_inputs = n_inputs;
+  h.body = T.body;
+  h.off_meta = (int32_t)(sizeof(TopHdr) + ((int64_t)(n_levels + 1) * 4 + 15) / 16 * 16);
+  h.off_in = h.off_meta + n_nodes * (int32_t)sizeof(TopMeta);
+  h.off_rec = h.off_in + (int32_t)(((int64_t)n_inputs * 4 + 15) / 16 * 16);
+  h.bytes = (int32_t)topblob_bytes(n_nodes, n_levels, n_inputs, n_rec);
+  const int local = (int)(p - first);
+  if (local == 0) {
+    *reinterpret_cast<TopHdr *>(B) = h;
+    int32_t *lv = reinterpret_cast<int32_t *>(B + sizeof(TopHdr));
+    for (int l = 0; l <= n_levels; l++) lv[l] = toplvl[lv0 + l] - first;
+  }
+  int32_t *IN = reinterpret_cast<int32_t *>(B + h.off_in);
+  int in_i = in_scan[p] - in_scan[first];
+  auto ref = [&](int32_t c) -> int16_t {
+    if (c >= 0 && slot_to_local[c] >= 0) return (int16_t)slot_to_local[c];
+    IN[in_i] = c >= 0 ? c : ~perm[~(int64_t)c];  // slot, or ~(body-local original bead index)
+    return (int16_t)~in_i++;
+  };
+  TopMeta md;
+  md.x = ref(T.x);
+  md.y = ref(T.y);
+  md.flags = T.flags;
+  md.is_root = T.is_root;
+  md.res_q = T.res_q;
+  md.rec = (int32_t)(rec_scan[p] - rec_scan[first]);
+  reinterpret_cast<TopMeta *>(B + h.off_meta)[local] = md;
+  double *R = reinterpret_cast<double *>(B + h.off_rec) + md.rec;
+  const int rs = rec_size(flag_case(T.flags));
+  for (int e = 0; e < rs; e++) R[e] = rec[T.rec_off + e];
+  (void)bead_off;
+}
+
 // ---- helpers ------------------------------------------------------------------------
 
 template <class T>
@@ -943,7 +1033,7 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topbig};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
@@ -1393,6 +1483,88 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         RQ_CUDA(cudaMemcpyAsync(p.toplvl.as<int32_t>() + p.n_toplevels, &endv[0], 4, cudaMemcpyHostToDevice, s));
         RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.as<int32_t>() + p.n_topbodies, &endv[1], 4, cudaMemcpyHostToDevice, s));
         RQ_CUDA(cudaStreamSynchronize(s));
+        // staged per-body top blobs
+        DBuf slot2loc, nin, in_scan, recsz, rec_scan;
+        slot2loc.alloc(std::max<int64_t>(p.n_slots, 1) * 4);
+        RQ_CUDA(cudaMemsetAsync(slot2loc.p, 0xff, std::max<int64_t>(p.n_slots, 1) * 4, s));
+        nin.alloc((nt + 1) * 4);
+        in_scan.alloc((nt + 1) * 4);
+        recsz.alloc((nt + 1) * 8);
+        rec_scan.alloc((nt + 1) * 8);
+        RQ_CUDA(cudaMemsetAsync(nin.p, 0, (nt + 1) * 4, s));
+        RQ_CUDA(cudaMemsetAsync(recsz.p, 0, (nt + 1) * 8, s));
+        k_top_slotmap<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, d_tbi.as<int32_t>(), p.topbody_lvl.as<int32_t>(),
+                                               p.toplvl.as<int32_t>(), slot2loc.as<int32_t>(), nin.as<int32_t>(),
+                                               recsz.as<int64_t>());
+        k_top_inputs<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, slot2loc.as<int32_t>(), nin.as<int32_t>());
+        exclusive_scan(nin.as<int32_t>(), in_scan.as<int32_t>(), nt + 1, s);
+        exclusive_scan(recsz.as<int64_t>(), rec_scan.as<int64_t>(), nt + 1, s);
+        std::vector<int32_t> h_lvl(p.n_topbodies + 1), h_toplvl(p.n_toplevels + 1), h_in(nt + 1);
+        std::vector<int64_t> h_rec(nt + 1);
+        d2h(h_lvl.data(), p.topbody_lvl.p, p.n_topbodies + 1, s);
+        d2h(h_toplvl.data(), p.toplvl.p, p.n_toplevels + 1, s);
+        d2h(h_in.data(), in_scan.p, nt + 1, s);
+        d2h(h_rec.data(), rec_scan.p, nt + 1, s);
+        const int64_t smem_cap = 180 * 1024;
+        std::vector<int64_t> blob_off(p.n_topbodies, -1), small_off;
+        std::vector<int32_t> small_tb, big_tb;
+        int64_t total = 0;
+        p.max_topblob_smem = 0;
+        for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
+          const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
+          const int nn = last - first, nl = h_lvl[bi + 1] - h_lvl[bi], ni = h_in[last] - h_in[first];
+          const int64_t bytes = topblob_bytes(nn, nl, ni, h_rec[last] - h_rec[first]);
+          const int64_t smem = (bytes + 127) / 128 * 128 + 48 * (int64_t)(ni + 2 * nn) + 128;
+          if (smem <= smem_cap && nn < 32000 && ni < 32000) {
+            blob_off[bi] = total;
+            small_tb.push_back((int32_t)bi);
+            small_off.push_back(total);
+            total += bytes;
+            p.max_topblob_smem = std::max(p.max_topblob_smem, smem);
+          } else {
+            blob_off[bi] = 0;  // unused
+            big_tb.push_back((int32_t)bi);
+          }
+        }
+        p.n_topblob = (int64_t)small_tb.size();
+        p.n_topbig = (int64_t)big_tb.size();
+        p.topblob.alloc(std::max<int64_t>(total, 16));
+        p.topblob_off.alloc(std::max<int64_t>(p.n_topblob, 1) * 8);
+        p.topblob_body.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
+        p.topbig.alloc(std::max<int64_t>(p.n_topbig, 1) * 4);
+        if (p.n_topblob) {
+          RQ_CUDA(cudaMemcpyAsync(p.topblob_off.p, small_off.data(), p.n_topblob * 8, cudaMemcpyHostToDevice, s));
+          RQ_CUDA(cudaMemcpyAsync(p.topblob_body.p, small_tb.data(), p.n_topblob * 4, cudaMemcpyHostToDevice, s));
+        }
+        if (p.n_topbig) RQ_CUDA(cudaMemcpyAsync(p.topbig.p, big_tb.data(), p.n_topbig * 4, cudaMemcpyHostToDevice, s));
+        DBuf d_blob_off;
+        d_blob_off.alloc(p.n_topbodies * 8);
+        RQ_CUDA(cudaMemcpyAsync(d_blob_off.p, blob_off.data(), p.n_topbodies * 8, cudaMemcpyHostToDevice, s));
+        // only bodies with a staged blob are written
+        DBuf is_small;
+        std::vector<uint8_t> hs(p.n_topbodies, 0);
+        for (auto bi : small_tb) hs[bi] = 1;
+        if (p.n_topblob) {
+          // write every node; nodes of "big" bodies write into a scratch blob that is dropped
+          DBuf dummy;
+          int64_t big_bytes = 0;
+          std::vector<int64_t> off2(blob_off);
+          for (auto bi : big_tb) {
+            const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
+            off2[bi] = total + big_bytes;
+            big_bytes += topblob_bytes(last - first, h_lvl[bi + 1] - h_lvl[bi], h_in[last] - h_in[first],
+                                       h_rec[last] - h_rec[first]);
+          }
+          DBuf all_blob;
+          all_blob.alloc(total + big_bytes + 16);
+          RQ_CUDA(cudaMemcpyAsync(d_blob_off.p, off2.data(), p.n_topbodies * 8, cudaMemcpyHostToDevice, s));
+          k_top_blob<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, d_tbi.as<int32_t>(), p.topbody_lvl.as<int32_t>(),
+                                              p.toplvl.as<int32_t>(), slot2loc.as<int32_t>(), in_scan.as<int32_t>(),
+                                              rec_scan.as<int64_t>(), d_blob_off.as<int64_t>(), p.rec.as<double>(),
+                                              p.perm.as<int32_t>(), boff, all_blob.as<uint8_t>());
+          RQ_CUDA(cudaMemcpyAsync(p.topblob.p, all_blob.p, total, cudaMemcpyDeviceToDevice, s));
+          RQ_CUDA(cudaStreamSynchronize(s));
+        }
       } else {
         p.toplvl.alloc(4);
         int32_t z = 0;

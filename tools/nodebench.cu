@@ -50,7 +50,7 @@ int main() {
   double *g, *s; long long *c; cudaMalloc(&g, 26 * 8); cudaMalloc(&s, 8192); cudaMalloc(&c, 8);
   cudaMemcpy(g, h, 26 * 8, cudaMemcpyHostToDevice);
   int it = 2000; long long cy;
-  kb<GENERAL><<<1, 32>>>(g, c, s, it); kb<GENERAL><<<1, 32>>>(g, c, s, it); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
+  kb<GENERAL><<<1, 32>>>(g, c, s, it); cudaDeviceSynchronize(); kb<GENERAL><<<1, 32>>>(g, c, s, it); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
   printf("GENERAL   %.1f cycles/node-step\n", cy / (double)it);
   kb<RIGID_BEAD><<<1, 32>>>(g, c, s, it); cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
   printf("RIGID     %.1f cycles/node-step\n", cy / (double)it);
