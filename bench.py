@@ -330,7 +330,8 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "clocks": ck, "gpu_launches": int(launches),
             "setup": {"seconds": setup_s, "beads_per_s": N / setup_s},
             "plan": {kk: info[kk] for kk in ("n_chunks", "n_top", "blob_bytes", "max_chunk_bytes", "n_case",
-                                             "device_bytes", "tile_leaves")},
+                                             "device_bytes", "tile_leaves", "chunk_smem", "top_staged",
+                                             "top_global")},
             "bytes_per_bead_per_op": chunk_bytes / N,
         }
         print(json.dumps(line), flush=True)

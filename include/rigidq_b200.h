@@ -69,6 +69,9 @@ typedef struct rq_plan_info {
   int64_t max_chunk_bytes; /* largest blob */
   int64_t n_case[4];       /* node counts per case (leaf, BB, RB, GEN) */
   int64_t device_bytes;    /* device memory held by the plan */
+  int64_t chunk_smem[6];   /* max head bytes, max level-record bytes, max beads, max nodes, max residues, max tiles */
+  int64_t top_staged;      /* bodies whose top tree is staged in shared memory */
+  int64_t top_global;      /* bodies whose top tree is swept from global memory */
 } rq_plan_info;
 
 /* Last error message of the calling thread ("" if none). */

@@ -132,6 +132,14 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
     info->max_chunk_bytes = p.max_blob;
     for (int c = 0; c < 4; c++) info->n_case[c] = p.n_case[c];
     info->device_bytes = p.device_bytes();
+    info->chunk_smem[0] = p.max_head_bytes;
+    info->chunk_smem[1] = p.max_level_rec_bytes;
+    info->chunk_smem[2] = p.max_chunk_beads;
+    info->chunk_smem[3] = p.max_chunk_nodes;
+    info->chunk_smem[4] = p.max_chunk_res;
+    info->chunk_smem[5] = p.max_chunk_tiles;
+    info->top_staged = p.n_topblob;
+    info->top_global = p.n_topbig;
   })
 }
 
