@@ -79,6 +79,7 @@ struct ApplyCtx {
   double *scratch;
   int op;
   int head_bytes, lrec_bytes, max_nodes, max_beads, max_res, max_tiles;
+  int pf_dist;     // L2 prefetch distance of chunk records (chunks ahead)
   long long *dbg;  // phase timers, only with -DRQ_TIMING (8 per CTA)
 };
 
@@ -321,14 +322,14 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     for (int64_t k = 0; k < 3 && k < cnt; k++) {
       const longlong2 dd = ldesc(k);
       const unsigned hb = (unsigned)(dd.y & 0xffffffffll), rb = (unsigned)(dd.y >> 32) - hb;
-      if (rb) prefetch_l2(a.blob + dd.x + hb, rb);
+      if (rb && k < a.pf_dist) prefetch_l2(a.blob + dd.x + hb, rb);
       if (k < 2) {
         mbar_expect_tx(&bar[k], hb);
         bulk_g2s(HEAD(k), a.blob + dd.x, hb, &bar[k]);
       }
     }
     dk2 = ldesc(2);
-    dk3 = ldesc(3);
+    dk3 = ldesc(a.pf_dist);
   }
   unsigned phase = 0;  // parity bit per barrier
   int64_t lctr = 0;    // level steps so far (selects the record stage)
@@ -353,12 +354,12 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
         mbar_expect_tx(&bar[s2], hb);
         bulk_g2s(HEAD(s2), a.blob + dk2.x, hb, &bar[s2]);
       }
-      if (k + 3 < cnt) {  // records of chunk k+3 into L2
+      if (k + a.pf_dist < cnt) {  // records of chunk k+pf_dist into L2
         const unsigned hb = (unsigned)(dk3.y & 0xffffffffll), rb = (unsigned)(dk3.y >> 32) - hb;
         if (rb) prefetch_l2(a.blob + dk3.x + hb, rb);
       }
-      dk2 = dk3;
-      dk3 = ldesc(k + 4);
+      dk2 = ldesc(k + 3);
+      dk3 = ldesc(k + 1 + a.pf_dist);
     }
     long long tc0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (k + 1 < cnt) {
@@ -769,6 +770,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   a.scratch = p.scratch.as<double>();
   a.op = op;
   KernelCfg cfg = chunk_cfg(p, up, a);
+  a.pf_dist = 1;
+  if (const char *e = getenv("RQ_PF_DIST")) a.pf_dist = std::max(1, std::min(8, atoi(e)));
   static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
   DBuf dbg;
   if (timing) {

@@ -32,9 +32,17 @@ __device__ __forceinline__ void ratios(int nx, int ny, double &a, double &b) {
 }
 
 // merge_infosets (matfree.py:41-62). res gets residue_rows entries.
+#ifndef RQ_SKIP_MATH
+#define RQ_SKIP_MATH 0
+#endif
 __device__ __forceinline__ void merge(int cs, const double *rec, int st, unsigned signs, double a, double b,
                                       const double (&mx)[6], const double (&my)[6], double (&mp)[6],
                                       double (&res)[6]) {
+  if (RQ_SKIP_MATH) {  // profiling experiment only: data movement without the transform
+#pragma unroll
+    for (int r = 0; r < 6; r++) { mp[r] = mx[r] + my[r] + rec[r * st]; res[r] = mx[r] * a + b; }
+    return;
+  }
   double t[3];
 #pragma unroll
   for (int r = 0; r < 3; r++) {
