@@ -27,6 +27,7 @@ namespace rq {
 namespace {
 
 constexpr int NT_TOP = 128;
+constexpr int NLS = 2;  // level-record stages in shared memory (records issued NLS-1 steps ahead)
 
 // ---- PTX helpers: mbarrier + bulk copy ------------------------------------------
 
@@ -213,7 +214,7 @@ __host__ __device__ __forceinline__ SmemMap smem_map(int head_bytes, int lrec_by
   m.x = (uint32_t)al128(8 * (size_t)(up ? max_res : 3 * max_beads));
   m.root = (uint32_t)al128(48 * (size_t)max_tiles);
   m.o_lrec = 3 * m.head;
-  m.o_v = m.o_lrec + 2 * m.lrec;
+  m.o_v = m.o_lrec + NLS * m.lrec;
   m.o_m = m.o_v + 2 * m.v;
   m.o_x = m.o_m + (uint32_t)al128(48 * (size_t)max_nodes);
   m.o_root = m.o_x + m.x;
@@ -293,7 +294,7 @@ __device__ __forceinline__ int level_rec_doubles(const LevelDesc &L) {
 template <bool UP, int NT>
 __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bar[5];  // 0-2 heads, 3-4 level records
+  __shared__ __align__(8) uint64_t bar[3 + NLS];  // 0-2 heads, 3.. level-record stages
   const int tid = threadIdx.x;
   const long long t_kernel0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
   const SmemMap SM = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, UP);
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   const int64_t cnt = a.n_chunks > blockIdx.x ? (a.n_chunks - blockIdx.x + G - 1) / G : 0;
   if (cnt == 0) return;
   if (tid == 0) {
-    for (int i = 0; i < 5; i++) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 3 + NLS; i++) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -336,14 +337,28 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   mbar_wait(&bar[0], 0);
   phase ^= 1u;
   prefetch_vectors<UP, NT>(a, HEAD(0), VBUF(0), ROOTBUF(0));
-  if (tid == 0) {  // first level of chunk 0
-    const ChunkView cv0 = view(HEAD(0));
-    const ChunkDesc &d0 = *cv0.hdr;
-    const LevelDesc L0 = cv0.LV[UP ? 0 : d0.n_levels - 1];
-    const unsigned bytes = 8u * (unsigned)level_rec_doubles(L0);
-    mbar_expect_tx(&bar[3], bytes);
-    bulk_g2s(LREC(0), reinterpret_cast<const double *>(a.blob + d0.blob_off + d0.off_rec) + L0.recG, bytes, &bar[3]);
-  }
+  // Level-record pipeline (thread 0): level steps are issued NLS-1 steps ahead of
+  // the step being swept, across chunk boundaries as far as heads are resident.
+  int64_t pf_k = 0;  // chunk iteration of the next level step to issue
+  int pf_s = 0;      // its level step within that chunk
+  int64_t pf_n = 0;  // level steps issued so far
+  auto issue_levels = [&](int64_t g, int64_t k_avail) {
+    // issue while fewer than NLS steps are in flight beyond the current one
+    while (pf_n < g + NLS && pf_k < cnt && pf_k <= k_avail) {
+      const ChunkView nv = view(HEAD(pf_k % 3));
+      const ChunkDesc &nd = *nv.hdr;
+      const int nH = nd.n_levels;
+      const LevelDesc L2 = nv.LV[UP ? pf_s : nH - 1 - pf_s];
+      const double *g2 = reinterpret_cast<const double *>(a.blob + nd.blob_off + nd.off_rec) + L2.recG;
+      const unsigned bytes = 8u * (unsigned)level_rec_doubles(L2);
+      const int st = (int)(pf_n % NLS);
+      mbar_expect_tx(&bar[3 + st], bytes);
+      bulk_g2s(LREC(st), g2, bytes, &bar[3 + st]);
+      pf_n++;
+      if (++pf_s == nH) { pf_s = 0; pf_k++; }
+    }
+  };
+  if (tid == 0) issue_levels(0, 0);
   for (int64_t k = 0; k < cnt; k++) {
     const int st = (int)(k % 3), fb = (int)(k & 1);
     if (tid == 0) {
@@ -387,28 +402,9 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     }
     for (int s = 0; s < H; s++, lctr++) {
       const int h = UP ? s : H - 1 - s;
-      const int ls = (int)(lctr & 1);
+      const int ls = (int)(lctr % NLS);
       const LevelDesc L = cv.LV[h];
-      if (tid == 0) {  // records of the next level step (this chunk's next level, or chunk k+1's first)
-        const double *g2 = nullptr;
-        unsigned bytes = 0;
-        if (s + 1 < H) {
-          const LevelDesc L2 = cv.LV[UP ? h + 1 : h - 1];
-          g2 = grec + L2.recG;
-          bytes = 8u * (unsigned)level_rec_doubles(L2);
-        } else if (k + 1 < cnt) {
-          const ChunkView nv = view(HEAD((k + 1) % 3));
-          const ChunkDesc &nd = *nv.hdr;
-          const LevelDesc L2 = nv.LV[UP ? 0 : nd.n_levels - 1];
-          g2 = reinterpret_cast<const double *>(a.blob + nd.blob_off + nd.off_rec) + L2.recG;
-          bytes = 8u * (unsigned)level_rec_doubles(L2);
-        }
-        if (g2) {
-          // WAR on smem (generic reads -> TMA write) is ordered by the barrier; no proxy fence needed
-          mbar_expect_tx(&bar[3 + (ls ^ 1)], bytes);
-          bulk_g2s(LREC(ls ^ 1), g2, bytes, &bar[3 + (ls ^ 1)]);
-        }
-      }
+      if (tid == 0) issue_levels(lctr, k + 1 < cnt ? k + 1 : k);
       long long tw0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       mbar_wait(&bar[3 + ls], (phase >> (3 + ls)) & 1u);
       phase ^= 1u << (3 + ls);
