@@ -170,20 +170,7 @@ int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
 int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, int64_t k) {
   RQ_GUARD({
     need_plan(plan);
-    const rq::Plan &p = plan->p;
-    if (op < 0 || op > 3) throw rq::Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
-    if (k < 1) throw rq::Error(RQ_ERR_LENGTH, "k must be >= 1");
-    RQ_CUDA(cudaSetDevice(p.device));
-    std::lock_guard<std::mutex> lock(p.host_mu);
-    if (!p.host_stream) RQ_CUDA(cudaStreamCreateWithFlags(&p.host_stream, cudaStreamNonBlocking));
-    const size_t bi = (size_t)in_len(p, op) * k * 8, bo = (size_t)out_len(p, op) * k * 8;
-    if (p.stage_in.bytes < bi) p.stage_in.alloc(bi);
-    if (p.stage_out.bytes < bo) p.stage_out.alloc(bo);
-    cudaStream_t s = p.host_stream;
-    RQ_CUDA(cudaMemcpyAsync(p.stage_in.p, in, bi, cudaMemcpyHostToDevice, s));
-    rq::run_apply(p, op, p.stage_in.as<double>(), p.stage_out.as<double>(), k, s);
-    RQ_CUDA(cudaMemcpyAsync(out, p.stage_out.p, bo, cudaMemcpyDeviceToHost, s));
-    RQ_CUDA(cudaStreamSynchronize(s));
+    rq::run_apply_host(plan->p, op, in, out, k);
   })
 }
 

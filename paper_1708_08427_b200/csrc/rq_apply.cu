@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "rq_nodeops.cuh"
@@ -292,7 +293,10 @@ __device__ __forceinline__ int level_rec_doubles(const LevelDesc &L) {
 //   * chunk k  : swept level by level; the records of level h+1 are TMA-copied
 //                (from L2) into the second record stage while level h runs.
 template <bool UP, int NT>
-__global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
+#ifndef RQ_MIN_BLOCKS
+#define RQ_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[3 + NLS];  // 0-2 heads, 3.. level-record stages
   const int tid = threadIdx.x;
@@ -737,13 +741,14 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)cfg.fn, cfg.threads, cfg.smem));
   if (occ < 1) throw Error(RQ_ERR_CUDA, "chunk kernel does not fit on an SM (smem " + std::to_string(cfg.smem) + ")");
   if (const char *e = getenv("RQ_CTAS_PER_SM")) occ = std::max(1, std::min(occ, atoi(e)));
-  cfg.grid = (int)std::min<int64_t>(p.n_chunks, (int64_t)sms * occ);
+  cfg.grid = (int)std::min<int64_t>(std::max<int64_t>(a.n_chunks, 1), (int64_t)sms * occ);
   return cfg;
 }
 
 }  // namespace
 
-void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases) {
+void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases,
+               BodyRange range) {
   if (op < 0 || op > 3) throw Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
   if (op >= 2 && p.min_n < 2)
     throw Error(RQ_ERR_BODY_TOO_SMALL, "complement operators need every body to have >= 2 beads");
@@ -754,11 +759,17 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     p.scratch_k = 1;
   }
   const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);
+  const bool all = range.j1 < 0;
+  const int64_t j0 = all ? 0 : range.j0, j1 = all ? p.m : range.j1;
+  const int64_t c0 = all ? 0 : p.h_chunk_first[j0], c1 = all ? p.n_chunks : p.h_chunk_first[j1];
+  const int64_t tb0 = all ? 0 : p.h_topblob_first[j0], tb1 = all ? p.n_topblob : p.h_topblob_first[j1];
+  const int64_t tg0 = all ? 0 : p.h_topbig_first[j0], tg1 = all ? p.n_topbig : p.h_topbig_first[j1];
+  const int64_t sm0 = all ? 0 : p.h_small_first[j0], sm1 = all ? p.n_small : p.h_small_first[j1];
   ApplyCtx a{};
-  a.chunks = p.chunks.as<ChunkDesc>();
+  a.chunks = p.chunks.as<ChunkDesc>() + c0;
   a.tiles = p.tiles.as<TileDesc>();
   a.blob = p.blob.as<uint8_t>();
-  a.n_chunks = p.n_chunks;
+  a.n_chunks = c1 - c0;
   a.bead_off = p.bead_off_d.as<int64_t>();
   a.in = in;
   a.out = out;
@@ -776,7 +787,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     a.dbg = dbg.as<long long>();
   }
   TopCtx t{};
-  t.tb_list = p.topbig.as<int32_t>();
+  t.tb_list = p.topbig.as<int32_t>() + tg0;
   t.top = p.top.as<TopNode>();
   t.topbody = p.topbody.as<int32_t>();
   t.topbody_lvl = p.topbody_lvl.as<int32_t>();
@@ -791,7 +802,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.op = op;
   Top2Ctx t2{};
   t2.blob = p.topblob.as<uint8_t>();
-  t2.blob_off = p.topblob_off.as<int64_t>();
+  t2.blob_off = p.topblob_off.as<int64_t>() + tb0;
   t2.bead_off = p.bead_off_d.as<int64_t>();
   t2.in = in;
   t2.out = out;
@@ -807,15 +818,15 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     a.col = col;
     t.col = col;
     t2.col = col;
-    const bool do_chunks = (phases & 1u) && p.n_chunks, do_top = (phases & 2u) && p.n_topbodies;
+    const bool do_chunks = (phases & 1u) && a.n_chunks > 0, do_top = (phases & 2u) && (tb1 > tb0 || tg1 > tg0);
     auto top_pass = [&]() {
-      if (p.n_topblob) {
-        if (up) k_top2<true><<<(unsigned)p.n_topblob, NT_TOP, top_smem, s>>>(t2);
-        else k_top2<false><<<(unsigned)p.n_topblob, NT_TOP, top_smem, s>>>(t2);
+      if (tb1 > tb0) {
+        if (up) k_top2<true><<<(unsigned)(tb1 - tb0), NT_TOP, top_smem, s>>>(t2);
+        else k_top2<false><<<(unsigned)(tb1 - tb0), NT_TOP, top_smem, s>>>(t2);
       }
-      if (p.n_topbig) {
-        if (up) k_top<true><<<(unsigned)p.n_topbig, NT_TOP, 0, s>>>(t);
-        else k_top<false><<<(unsigned)p.n_topbig, NT_TOP, 0, s>>>(t);
+      if (tg1 > tg0) {
+        if (up) k_top<true><<<(unsigned)(tg1 - tg0), NT_TOP, 0, s>>>(t);
+        else k_top<false><<<(unsigned)(tg1 - tg0), NT_TOP, 0, s>>>(t);
       }
     };
     if (up) {
@@ -836,11 +847,68 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
               acc[5] / acc[6], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
       RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
     }
-    if ((phases & 4u) && p.n_small && op <= 1)
-      k_small<<<(unsigned)((3 * p.n_small + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>(), p.n_small,
-                                                                      p.bead_off_d.as<int64_t>(), in, out, k, col);
+    if ((phases & 4u) && sm1 > sm0 && op <= 1)
+      k_small<<<(unsigned)((3 * (sm1 - sm0) + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>() + sm0, sm1 - sm0,
+                                                                        p.bead_off_d.as<int64_t>(), in, out, k, col);
   }
   RQ_CUDA(cudaGetLastError());
+}
+
+
+void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k) {
+  if (op < 0 || op > 3) throw Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
+  if (k < 1) throw Error(RQ_ERR_LENGTH, "k must be >= 1");
+  if (op >= 2 && p.min_n < 2)
+    throw Error(RQ_ERR_BODY_TOO_SMALL, "complement operators need every body to have >= 2 beads");
+  RQ_CUDA(cudaSetDevice(p.device));
+  std::lock_guard<std::mutex> lock(p.host_mu);
+  if (!p.host_stream) {
+    for (auto *st : {&p.host_stream, &p.host_stream2, &p.host_stream3})
+      RQ_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+  }
+  const bool in_comp = op == RQ_OP_QTILDE_TV, out_comp = op == RQ_OP_QTILDE_V;
+  auto rows = [&](bool comp, int64_t j) { return 3 * p.bead_off[j] - (comp ? 6 * j : 0); };
+  const size_t bi = (size_t)rows(in_comp, p.m) * k * 8, bo = (size_t)rows(out_comp, p.m) * k * 8;
+  if (p.stage_in.bytes < bi) p.stage_in.alloc(bi);
+  if (p.stage_out.bytes < bo) p.stage_out.alloc(bo);
+  // segments of roughly equal bead count (at least ~2 MB of vector data each)
+  const int64_t seg_target = std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(bi / (2u << 20))));
+  std::vector<int64_t> cuts{0};
+  for (int64_t s = 1; s < seg_target; s++) {
+    const int64_t target = p.bead_off[p.m] * s / seg_target;
+    int64_t j = (int64_t)(std::lower_bound(p.bead_off.begin(), p.bead_off.end(), target) - p.bead_off.begin());
+    j = std::min<int64_t>(std::max<int64_t>(j, cuts.back()), p.m);
+    if (j > cuts.back() && j < p.m) cuts.push_back(j);
+  }
+  cuts.push_back(p.m);
+  const int nseg = (int)cuts.size() - 1;
+  std::vector<cudaEvent_t> ev_in(nseg), ev_k(nseg);
+  for (int i = 0; i < nseg; i++) {
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming));
+  }
+  cudaStream_t s_in = p.host_stream, s_k = p.host_stream2, s_out = p.host_stream3;
+  double *din = p.stage_in.as<double>(), *dout = p.stage_out.as<double>();
+  for (int i = 0; i < nseg; i++) {
+    const int64_t j0 = cuts[i], j1 = cuts[i + 1];
+    const int64_t r0 = rows(in_comp, j0), r1 = rows(in_comp, j1);
+    RQ_CUDA(cudaMemcpyAsync(din + r0 * k, in + r0 * k, (size_t)(r1 - r0) * k * 8, cudaMemcpyHostToDevice, s_in));
+    RQ_CUDA(cudaEventRecord(ev_in[i], s_in));
+    RQ_CUDA(cudaStreamWaitEvent(s_k, ev_in[i], 0));
+    BodyRange br;
+    br.j0 = j0;
+    br.j1 = j1;
+    run_apply(p, op, din, dout, k, s_k, 7u, br);
+    RQ_CUDA(cudaEventRecord(ev_k[i], s_k));
+    RQ_CUDA(cudaStreamWaitEvent(s_out, ev_k[i], 0));
+    const int64_t o0 = rows(out_comp, j0), o1 = rows(out_comp, j1);
+    RQ_CUDA(cudaMemcpyAsync(out + o0 * k, dout + o0 * k, (size_t)(o1 - o0) * k * 8, cudaMemcpyDeviceToHost, s_out));
+  }
+  RQ_CUDA(cudaStreamSynchronize(s_out));
+  for (int i = 0; i < nseg; i++) {
+    cudaEventDestroy(ev_in[i]);
+    cudaEventDestroy(ev_k[i]);
+  }
 }
 
 }  // namespace rq

@@ -122,6 +122,8 @@ struct Plan {
   DBuf topblob_body;               // int32 [n_topblob]: top-body index (into topbody)
   DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
   int64_t n_topbig = 0;
+  // host-side body -> work-list ranges (segmented / pipelined applications)
+  std::vector<int64_t> h_chunk_first, h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each
   mutable DBuf scratch;            // double [6 * n_slots * kcap]
   mutable int64_t scratch_k = 0;
   DBuf err;                        // int64 [8] device error flags
@@ -133,19 +135,27 @@ struct Plan {
   mutable DBuf zpart;              // double [6 * n_seg]
   // host-buffer entry points: persistent device staging (grown on demand)
   mutable DBuf stage_in, stage_out;
-  mutable cudaStream_t host_stream = nullptr;
+  mutable cudaStream_t host_stream = nullptr, host_stream2 = nullptr, host_stream3 = nullptr;
 
   mutable std::mutex host_mu;
   int64_t device_bytes() const;
   ~Plan() {
-    if (host_stream) cudaStreamDestroy(host_stream);
+    for (cudaStream_t st : {host_stream, host_stream2, host_stream3})
+      if (st) cudaStreamDestroy(st);
   }
 };
 
 void build_plan(Plan &p, const double *pos, const int64_t *offsets, int64_t m, int max_depth,
                 bool host_input, cudaStream_t s);
+// bodies [j0, j1) of a plan (all work lists are in body order)
+struct BodyRange {
+  int64_t j0 = 0, j1 = -1;  // j1 < 0: all bodies
+};
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
-               unsigned phases = 7u);
+               unsigned phases = 7u, BodyRange range = BodyRange());
+// Host-buffer application pipelined over body segments: H2D of segment i+1,
+// kernels of segment i and D2H of segment i-1 overlap (three streams).
+void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k);
 void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, const double *origin_d,
            cudaStream_t s);
 int check_duplicates(const double *pos, const int64_t *offsets, int64_t m, bool host_input,

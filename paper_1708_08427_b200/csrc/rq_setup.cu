@@ -1364,6 +1364,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.max_chunk_tiles = std::max(p.max_chunk_tiles, d.n_tiles);
         p.max_head_bytes = std::max<int64_t>(p.max_head_bytes, d.off_rec);
       }
+      p.h_chunk_first.assign(m + 1, nc);
+      for (int64_t c = nc - 1; c >= 0; c--) p.h_chunk_first[hc[c].body] = c;
+      for (int64_t j = m - 1; j >= 0; j--) p.h_chunk_first[j] = std::min(p.h_chunk_first[j], p.h_chunk_first[j + 1]);
       p.blob.alloc(p.blob_bytes);
       RQ_CUDA(cudaMemsetAsync(p.blob.p, 0, p.blob_bytes, s));
       DBuf lvl;
@@ -1440,6 +1443,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       }
       p.n_topbodies = (int64_t)topbodies.size();
       p.n_small = (int64_t)smalls.size();
+      p.h_small_first.assign(m + 1, p.n_small);
+      for (int64_t i = p.n_small - 1; i >= 0; i--) p.h_small_first[smalls[i]] = i;
+      for (int64_t j = m - 1; j >= 0; j--) p.h_small_first[j] = std::min(p.h_small_first[j], p.h_small_first[j + 1]);
       p.small_bodies.alloc(std::max<int64_t>(p.n_small, 1) * 4);
       if (p.n_small)
         RQ_CUDA(cudaMemcpyAsync(p.small_bodies.p, smalls.data(), p.n_small * 4, cudaMemcpyHostToDevice, s));
@@ -1528,6 +1534,13 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         }
         p.n_topblob = (int64_t)small_tb.size();
         p.n_topbig = (int64_t)big_tb.size();
+        auto firsts = [&](const std::vector<int32_t> &list, std::vector<int64_t> &out) {
+          out.assign(m + 1, (int64_t)list.size());
+          for (int64_t i = (int64_t)list.size() - 1; i >= 0; i--) out[topbodies[list[i]]] = i;
+          for (int64_t j = m - 1; j >= 0; j--) out[j] = std::min(out[j], out[j + 1]);
+        };
+        firsts(small_tb, p.h_topblob_first);
+        firsts(big_tb, p.h_topbig_first);
         p.topblob.alloc(std::max<int64_t>(total, 16));
         p.topblob_off.alloc(std::max<int64_t>(p.n_topblob, 1) * 8);
         p.topblob_body.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
@@ -1566,6 +1579,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           RQ_CUDA(cudaStreamSynchronize(s));
         }
       } else {
+        p.h_topblob_first.assign(m + 1, 0);
+        p.h_topbig_first.assign(m + 1, 0);
         p.toplvl.alloc(4);
         int32_t z = 0;
         RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.p, &z, 4, cudaMemcpyHostToDevice, s));
