@@ -409,10 +409,13 @@ __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
       const int ls = (int)(lctr % NLS);
       const LevelDesc L = cv.LV[h];
       if (tid == 0) issue_levels(lctr, k + 1 < cnt ? k + 1 : k);
+      __shared__ unsigned long long t_max_node, t_step0;
+      if (RQ_TIMING && a.dbg && tid == 0) { t_max_node = 0; t_step0 = clock64(); }
       long long tw0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       mbar_wait(&bar[3 + ls], (phase >> (3 + ls)) & 1u);
       phase ^= 1u << (3 + ls);
       long long tw1 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
+      const long long tn0 = (RQ_TIMING && a.dbg) ? clock64() : 0;
       const double *R = LREC(ls);
       const int oR = rec_size(GENERAL) * L.nG, oB = oR + rec_size(RIGID_BEAD) * L.nR;
       // case-uniform warps: GEN and RB groups each padded to whole warps
@@ -451,11 +454,22 @@ __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
         }
       }
       long long tw2 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
+      if (RQ_TIMING && a.dbg && (tid & 31) == 0) {
+        const unsigned long long dt = (unsigned long long)(clock64() - (long long)t_step0);
+        atomicMax(&t_max_node, dt);
+        // per-group slowest: 0 GEN, 1 RB, 2 BB, 3 idle
+        const int q = tid;
+        const int grp = q < gG ? (q < L.nG ? 0 : 3) : (q < gG + gR ? (q - gG < L.nR ? 1 : 3) : (q - gG - gR < L.nB ? 2 : 3));
+        atomicAdd((unsigned long long *)&a.dbg[8 * (size_t)gridDim.x + 2 * grp], (unsigned long long)dt);
+        atomicAdd((unsigned long long *)&a.dbg[8 * (size_t)gridDim.x + 2 * grp + 1], 1ull);
+      }
+      (void)tn0;
       __syncthreads();
       if (RQ_TIMING && a.dbg && tid == 0) {
         long long tw3 = clock64();
         a.dbg[8 * blockIdx.x + 0] += tw1 - tw0;  // level record wait
         a.dbg[8 * blockIdx.x + 1] += tw2 - tw1;  // tid0 node work
+        a.dbg[8 * blockIdx.x + 5] += (long long)t_max_node;  // slowest warp finishes (from step start)
         (void)tw3;
         a.dbg[8 * blockIdx.x + 4] += 1;          // level steps
       }
@@ -487,7 +501,7 @@ __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
       }
     }
     __syncthreads();
-    if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 5] += clock64() - to0;
+    (void)to0;
   }
   if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 7] = clock64() - t_kernel0;
 #undef HEAD
@@ -782,8 +796,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
   DBuf dbg;
   if (timing) {
-    dbg.alloc((size_t)cfg.grid * 64);
-    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
+    dbg.alloc((size_t)cfg.grid * 64 + 64);
+    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64 + 64, s));
     a.dbg = dbg.as<long long>();
   }
   TopCtx t{};
@@ -837,15 +851,15 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
     }
     if (timing && do_chunks) {
-      std::vector<long long> h((size_t)cfg.grid * 8);
+      std::vector<long long> h((size_t)cfg.grid * 8 + 8);
       RQ_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
       RQ_CUDA(cudaStreamSynchronize(s));
       double acc[8] = {0};
       for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) acc[i] += (double)h[8 * g + i];
-      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f level-total %.0f | per chunk: head+vec wait %.0f, out %.0f, level steps %.1f, chunks/CTA %.1f, CTA total %.0f (max %.0f)\n",
+      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f level-total %.0f | per chunk: head+vec wait %.0f, slowest-warp/step %.0f, level steps %.1f, chunks/CTA %.1f, CTA total %.0f (max %.0f)\n",
               op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[4], acc[1] / acc[4], acc[2] / acc[4], acc[3] / acc[6],
-              acc[5] / acc[6], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
-      RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64, s));
+              acc[5] / acc[4], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
+      RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64 + 64, s));
     }
     if ((phases & 4u) && sm1 > sm0 && op <= 1)
       k_small<<<(unsigned)((3 * (sm1 - sm0) + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>() + sm0, sm1 - sm0,
