@@ -293,10 +293,11 @@ __device__ __forceinline__ int level_rec_doubles(const LevelDesc &L) {
 //   * chunk k  : swept level by level; the records of level h+1 are TMA-copied
 //                (from L2) into the second record stage while level h runs.
 template <bool UP, int NT>
-#ifndef RQ_MIN_BLOCKS
-#define RQ_MIN_BLOCKS 1
-#endif
+#ifdef RQ_MIN_BLOCKS
 __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
+#else
+__global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
+#endif
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[3 + NLS];  // 0-2 heads, 3.. level-record stages
   const int tid = threadIdx.x;
@@ -409,8 +410,9 @@ __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
       const int ls = (int)(lctr % NLS);
       const LevelDesc L = cv.LV[h];
       if (tid == 0) issue_levels(lctr, k + 1 < cnt ? k + 1 : k);
-      __shared__ unsigned long long t_max_node, t_step0;
-      if (RQ_TIMING && a.dbg && tid == 0) { t_max_node = 0; t_step0 = clock64(); }
+      __shared__ unsigned long long t_max_node, t_step0, t_grp[4];
+      if (RQ_TIMING && a.dbg && tid == 0) { t_max_node = 0; t_step0 = clock64(); t_grp[0] = t_grp[1] = t_grp[2] = t_grp[3] = 0; }
+      if (RQ_TIMING && a.dbg) __syncthreads();
       long long tw0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       mbar_wait(&bar[3 + ls], (phase >> (3 + ls)) & 1u);
       phase ^= 1u << (3 + ls);
@@ -460,8 +462,7 @@ __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
         // per-group slowest: 0 GEN, 1 RB, 2 BB, 3 idle
         const int q = tid;
         const int grp = q < gG ? (q < L.nG ? 0 : 3) : (q < gG + gR ? (q - gG < L.nR ? 1 : 3) : (q - gG - gR < L.nB ? 2 : 3));
-        atomicAdd((unsigned long long *)&a.dbg[8 * (size_t)gridDim.x + 2 * grp], (unsigned long long)dt);
-        atomicAdd((unsigned long long *)&a.dbg[8 * (size_t)gridDim.x + 2 * grp + 1], 1ull);
+        atomicMax(&t_grp[grp], dt);
       }
       (void)tn0;
       __syncthreads();
@@ -472,6 +473,8 @@ __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
         a.dbg[8 * blockIdx.x + 5] += (long long)t_max_node;  // slowest warp finishes (from step start)
         (void)tw3;
         a.dbg[8 * blockIdx.x + 4] += 1;          // level steps
+        for (int g = 0; g < 4; g++)
+          if (t_grp[g]) { a.dbg[8 * (gridDim.x + blockIdx.x) + g] += (long long)t_grp[g]; a.dbg[8 * (gridDim.x + blockIdx.x) + 4 + g] += 1; }
       }
     }
     long long to0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
@@ -796,8 +799,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
   DBuf dbg;
   if (timing) {
-    dbg.alloc((size_t)cfg.grid * 64 + 64);
-    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64 + 64, s));
+    dbg.alloc((size_t)cfg.grid * 256 + 64);
+    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 256 + 64, s));
     a.dbg = dbg.as<long long>();
   }
   TopCtx t{};
@@ -851,7 +854,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
     }
     if (timing && do_chunks) {
-      std::vector<long long> h((size_t)cfg.grid * 8 + 8);
+      std::vector<long long> h((size_t)cfg.grid * 16 + 8);
       RQ_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
       RQ_CUDA(cudaStreamSynchronize(s));
       double acc[8] = {0};
@@ -859,7 +862,11 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f level-total %.0f | per chunk: head+vec wait %.0f, slowest-warp/step %.0f, level steps %.1f, chunks/CTA %.1f, CTA total %.0f (max %.0f)\n",
               op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[4], acc[1] / acc[4], acc[2] / acc[4], acc[3] / acc[6],
               acc[5] / acc[4], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
-      RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 64 + 64, s));
+      double gs[8] = {0};
+      for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) gs[i] += (double)h[8 * (cfg.grid + g) + i];
+      fprintf(stderr, "[rq timing] slowest warp finish after step start, per group (avg over steps where present): GEN %.0f (%.0f) RB %.0f (%.0f) BB %.0f (%.0f) idle %.0f (%.0f)\n",
+              gs[0] / std::max(1.0, gs[4]), gs[4], gs[1] / std::max(1.0, gs[5]), gs[5], gs[2] / std::max(1.0, gs[6]), gs[6], gs[3] / std::max(1.0, gs[7]), gs[7]);
+      RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 256 + 64, s));
     }
     if ((phases & 4u) && sm1 > sm0 && op <= 1)
       k_small<<<(unsigned)((3 * (sm1 - sm0) + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>() + sm0, sm1 - sm0,
