@@ -775,6 +775,15 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     p.scratch.alloc(std::max<int64_t>(p.n_slots, 1) * 48);
     p.scratch_k = 1;
   }
+  int64_t max_n = 0;
+  if (k >= p.mrhs_min)
+    for (int64_t j = 0; j < p.m; j++) max_n = std::max(max_n, p.bead_off[j + 1] - p.bead_off[j]);
+  const int64_t lim32 = int64_t(1) << 31;
+  if (k >= p.mrhs_min && 3 * max_n * k < lim32 && 6 * std::max<int64_t>(p.n_slots, 1) * k < lim32) {
+    // column-parallel stack-machine kernels (rq_mrhs.cu)
+    run_apply_mrhs(p, op, in, out, k, s, range);
+    return;
+  }
   const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);
   const bool all = range.j1 < 0;
   const int64_t j0 = all ? 0 : range.j0, j1 = all ? p.m : range.j1;

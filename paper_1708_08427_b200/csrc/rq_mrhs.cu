@@ -1,0 +1,665 @@
+// rq_mrhs.cu -- multi-right-hand-side application (k >= RQ_MRHS_MIN columns):
+// Q V, Q^T W, Q~ V, Q~^T G for (rows, k) row-major blocks (matfree.py:86-92:
+// a 2-D v applies the operator column by column; the reference does it as
+// one gemm per node, matfree.py:55-60).
+//
+// Design: every warp runs a "stack machine" over one unit (a tile = maximal
+// subtree of <= tile_leaves beads, or the top tree of a big body) for 32
+// columns at once: lane = column, so all lanes share one node, its record is
+// a broadcast load, and every vector access is one coalesced 256-byte row
+// segment of the (rows, k) block.  Nodes are visited in heavy-child-first
+// postorder, so the stack of pending information vectors never holds more than
+// floor(log2(leaves)) + 1 entries (the lighter child always has at most half
+// the leaves); it lives in shared memory, [depth][6][32] doubles per warp.
+// Bead inputs/outputs are read/written straight from/to the vector blocks;
+// tile roots exchange their 6-vectors with the top units through a scratch
+// block [slot][6][k].  Units are independent, warps never synchronise.
+//
+// Unit program: entries at a fixed 256-byte stride (forward for Q, backward
+// for Q^T), each = SEntry header (16 B) + the node's compact record.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "rq_nodeops.cuh"
+#include "rq_plan.hpp"
+
+namespace rq {
+
+namespace {
+
+constexpr int ENTRY_BYTES = 256;
+constexpr int MRHS_NT = 128;  // 4 independent warps per block
+
+
+// ---- program builder ------------------------------------------------------------------
+
+struct BuildCtx {
+  int S;
+  int64_t NN, m;
+  const int64_t *bead_off, *node_off, *rec_off;
+  const int32_t *start, *stop, *left, *right, *parent, *res_off, *perm;
+  const uint8_t *flags;
+  const double *rec;
+};
+
+__device__ __forceinline__ int64_t body_of_node(const BuildCtx &c, int64_t g) {
+  int64_t lo = 0, hi = c.m;  // node_off[lo] <= g < node_off[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) / 2;
+    if (c.node_off[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// unit roots: tile roots (2 <= L <= S, parent absent or > S) and big-body roots (L > S)
+__global__ void k_unit_flags(BuildCtx c, int32_t *is_tile_unit, int32_t *is_top_unit, int32_t *tile_nodes,
+                             int32_t *top_count) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= c.NN) return;
+  const int64_t j = body_of_node(c, g);
+  const int L = c.stop[g] - c.start[g];
+  const int nj = (int)(c.bead_off[j + 1] - c.bead_off[j]);
+  const bool root = (g - c.node_off[j]) == 2 * (int64_t)nj - 2;
+  const int Lp = root ? 0 : c.stop[c.node_off[j] + c.parent[g]] - c.start[c.node_off[j] + c.parent[g]];
+  const bool tile = L >= 2 && L <= c.S && (root || Lp > c.S);
+  is_tile_unit[g] = tile;
+  tile_nodes[g] = tile ? L - 1 : 0;
+  is_top_unit[g] = root && L > c.S;
+  if (L > c.S) atomicAdd(&top_count[j], 1);
+}
+
+struct UnitDesc {  // 32 bytes
+  int64_t entry0;  // first entry (index of ENTRY_BYTES blocks)
+  int32_t n;       // entries (internal nodes of the unit)
+  int32_t body;
+  int32_t out_slot;  // tile unit: its scratch slot, -1 if its root is the body root; top unit: -1
+  int32_t depth;     // stack entries needed
+  int64_t root;      // global node id of the unit root
+};
+
+struct SEntry {    // 16 bytes; the record (rec_size doubles) follows
+  int32_t x, y;    // formula-x / -y child: >= 0 body-local original bead; -1 stack; <= -2 scratch slot (-2 - v)
+  int32_t res;     // body-relative Q~ row of the residues (res_off - 6), -1 for BEAD_BEAD
+  uint8_t flags;   // case | swapped | signs
+  uint8_t x_first; // both children on the stack: 1 if x finished first (y on top)
+  uint16_t pad;
+};
+
+__global__ void k_unit_list(BuildCtx c, const int32_t *is_tile_unit, const int32_t *tile_scan,
+                            const int64_t *tile_entry_scan, const int32_t *is_top_unit, const int32_t *top_scan,
+                            const int64_t *top_entry_base, const int32_t *top_count, int64_t n_tile_units,
+                            UnitDesc *units, int32_t *tile_slot_of) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= c.NN) return;
+  const int64_t j = body_of_node(c, g);
+  if (is_tile_unit[g]) {
+    const int64_t u = tile_scan[g];
+    UnitDesc d;
+    d.entry0 = tile_entry_scan[g];
+    d.n = c.stop[g] - c.start[g] - 1;
+    d.body = (int32_t)j;
+    const int nj = (int)(c.bead_off[j + 1] - c.bead_off[j]);
+    const bool root = (g - c.node_off[j]) == 2 * (int64_t)nj - 2;
+    d.out_slot = root ? -1 : (int32_t)u;
+    d.depth = 0;
+    d.root = g;
+    units[u] = d;
+    tile_slot_of[g] = (int32_t)u;
+  }
+  if (is_top_unit[g]) {
+    const int64_t u = n_tile_units + top_scan[g];
+    UnitDesc d;
+    d.entry0 = top_entry_base[top_scan[g]];
+    d.n = top_count[j];
+    d.body = (int32_t)j;
+    d.out_slot = -1;
+    d.depth = 0;
+    d.root = g;
+    units[u] = d;
+  }
+}
+
+// one thread per unit: heavy-first postorder, entries written in visiting order
+__global__ void k_unit_program(BuildCtx c, UnitDesc *units, int64_t n_units, const int32_t *tile_slot_of,
+                               uint8_t *prog, int32_t *max_depth_tile, int32_t *max_depth_top,
+                               int64_t n_tile_units) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= n_units) return;
+  UnitDesc d = units[u];
+  const int64_t j = d.body, no = c.node_off[j], bo = c.bead_off[j];
+  const bool top = u >= n_tile_units;
+  auto Lof = [&](int64_t g) { return c.stop[g] - c.start[g]; };
+  auto in_unit = [&](int64_t g) { return Lof(g) >= 2 && (!top || Lof(g) > c.S); };
+  // explicit DFS stack: (node, state) with state 0 = enter, 1 = first child done, 2 = both done
+  constexpr int MAXS = 128;
+  int64_t st_node[MAXS];
+  int8_t st_state[MAXS];
+  int sp = 0;
+  st_node[sp] = d.root;
+  st_state[sp] = 0;
+  sp++;
+  int64_t e = 0;
+  int depth = 0, maxdepth = 1;
+  while (sp > 0) {
+    const int64_t g = st_node[sp - 1];
+    const int8_t s = st_state[sp - 1];
+    const int64_t lc = no + c.left[g], rc = no + c.right[g];
+    const bool heavy_left = Lof(lc) >= Lof(rc);
+    const int64_t first = heavy_left ? lc : rc, second = heavy_left ? rc : lc;
+    if (s == 0) {
+      st_state[sp - 1] = 1;
+      if (in_unit(first)) { st_node[sp] = first; st_state[sp] = 0; sp++; }
+      continue;
+    }
+    if (s == 1) {
+      st_state[sp - 1] = 2;
+      if (in_unit(second)) { st_node[sp] = second; st_state[sp] = 0; sp++; }
+      continue;
+    }
+    sp--;
+    // emit g
+    const unsigned f = c.flags[g];
+    const int cs = flag_case(f);
+    const int64_t xc = flag_swapped(f) ? rc : lc, yc = flag_swapped(f) ? lc : rc;
+    auto src = [&](int64_t ch) -> int32_t {
+      if (Lof(ch) == 1) return c.perm[bo + c.start[ch]];
+      if (in_unit(ch)) return -1;
+      return -2 - tile_slot_of[ch];
+    };
+    SEntry h;
+    h.x = src(xc);
+    h.y = src(yc);
+    h.res = cs == BEAD_BEAD ? -1 : c.res_off[g] - 6;
+    h.flags = (uint8_t)f;
+    h.x_first = (uint8_t)(xc == first);
+    h.pad = 0;
+    uint8_t *dst = prog + (d.entry0 + e) * ENTRY_BYTES;
+    *reinterpret_cast<SEntry *>(dst) = h;
+    const double *r = c.rec + c.rec_off[g];
+    double *rd = reinterpret_cast<double *>(dst + sizeof(SEntry));
+    for (int i = 0; i < rec_size(cs); i++) rd[i] = r[i];
+    e++;
+    // simulated information-vector stack: pop the stack children, push g
+    maxdepth = max(maxdepth, depth);  // stack children resident before the pops
+    depth += 1 - (h.x == -1) - (h.y == -1);
+    maxdepth = max(maxdepth, depth);
+  }
+  units[u].depth = maxdepth;
+  atomicMax(top ? max_depth_top : max_depth_tile, maxdepth);
+}
+
+// ---- kernels ----------------------------------------------------------------------------
+
+struct MrhsCtx {
+  const UnitDesc *units;
+  int64_t n_units;  // units of this launch
+  int64_t n_cg;     // column groups of 32
+  const uint8_t *prog;
+  const int64_t *bead_off;
+  const double *in;
+  double *out;
+  double *scratch;  // [slot][6][K]
+  int64_t K;
+  int op;
+  int depth;        // stack entries per warp
+  long long *dbg;   // per-warp phase timers, only with -DRQ_TIMING
+};
+#ifndef RQ_TIMING
+#define RQ_TIMING 0
+#endif
+
+// stack entry d, component r, this lane
+#define STK(d, r) stk[((d) * 6 + (r)) * 32 + lane]
+
+__device__ __forceinline__ uint32_t smem_u32m(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16m(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32m(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit_m() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_m() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void prefetch_l2m(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
+}
+
+constexpr int RING = 4;     // unit entries staged per warp (cp.async, RING-1 ahead)
+constexpr int L2_AHEAD = 8; // entries prefetched into L2 ahead of the ring
+
+template <int CS>
+__device__ __forceinline__ void lds_rec(const uint8_t *e, double (&R)[rec_size(GENERAL)]) {
+  const double2 *r2 = reinterpret_cast<const double2 *>(e + sizeof(SEntry));
+#pragma unroll
+  for (int i = 0; i < rec_size(CS) / 2; i++) {
+    const double2 v = r2[i];
+    R[2 * i] = v.x;
+    R[2 * i + 1] = v.y;
+  }
+}
+
+__device__ __forceinline__ int ld_case_rec(const uint8_t *e, double (&R)[rec_size(GENERAL)]) {
+  const int cs = flag_case(reinterpret_cast<const SEntry *>(e)->flags);
+  if (cs == GENERAL) lds_rec<GENERAL>(e, R);
+  else if (cs == RIGID_BEAD) lds_rec<RIGID_BEAD>(e, R);
+  else lds_rec<BEAD_BEAD>(e, R);
+  return cs;
+}
+
+// Per-lane views used by the node bodies: S = stack base + lane (entry d,
+// component r at S[(6d + r) * 32]); column-relative row pointers of the body.
+struct LaneIO {
+  double *S;
+  const double *inB, *inR;  // bead rows / residue rows of the body (input)
+  double *outB, *outR;      // bead rows / residue rows of the body (output)
+  double *scr;              // exchange rows of tile roots
+  int Ki;
+};
+
+template <bool ACT>
+__device__ __forceinline__ void st_rows(double *p, int Ki, const double *v, int n, bool act) {
+  if (ACT || act) {
+#pragma unroll
+    for (int r = 0; r < 6; r++)
+      if (r < n) p[r * Ki] = v[r];
+  }
+}
+
+// merge_infosets (matfree.py:41-62) for one node of a unit, 32 columns
+template <int CS, bool ACT>
+__device__ __forceinline__ void up_m(const int4 &hw, const double (&R)[rec_size(GENERAL)], const double (&gin)[6],
+                                     const LaneIO &io, int &sp, bool act) {
+  double mx[6], my[6];
+  if (CS == BEAD_BEAD) {
+#pragma unroll
+    for (int r = 0; r < 3; r++) { mx[r] = gin[r]; my[r] = gin[3 + r]; mx[3 + r] = 0.0; my[3 + r] = 0.0; }
+  } else {
+    const bool xs = hw.x == -1, ys = CS == GENERAL && hw.y == -1;
+    int dx = sp - 1, dy = sp - 1;
+    if (xs && ys) {
+      if (hw.w >> 8) dx = sp - 2; else dy = sp - 2;  // x finished first: y on top
+    }
+    const double *px = xs ? io.S + dx * 192 : io.scr + (-2 - hw.x) * 6 * io.Ki;
+    const int stx = xs ? 32 : io.Ki;
+#pragma unroll
+    for (int r = 0; r < 6; r++) mx[r] = px[r * stx];
+    if (CS == GENERAL) {
+      const double *py = ys ? io.S + dy * 192 : io.scr + (-2 - hw.y) * 6 * io.Ki;
+      const int sty = ys ? 32 : io.Ki;
+#pragma unroll
+      for (int r = 0; r < 6; r++) my[r] = py[r * sty];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 3; r++) { my[r] = gin[3 + r]; my[3 + r] = 0.0; }
+    }
+    sp -= (int)xs + (int)ys;
+  }
+  double aa, bb, mp[6], res[6];
+  rec_ratios(CS, R, 1, aa, bb);
+  merge(CS, R, 1, flag_signs(hw.w & 0xff), aa, bb, mx, my, mp, res);
+  if (CS != BEAD_BEAD) st_rows<ACT>(io.outR + hw.z * io.Ki, io.Ki, res, res_rows(CS), act);
+  __syncwarp();
+  double *pp = io.S + sp * 192;
+#pragma unroll
+  for (int r = 0; r < 6; r++) pp[r * 32] = mp[r];
+  sp++;
+}
+
+// split_rvset (matfree.py:65-83) for one node of a unit, 32 columns
+template <int CS, bool ACT>
+__device__ __forceinline__ void down_m(const int4 &hw, const double (&R)[rec_size(GENERAL)],
+                                       const double (&gin)[6], const LaneIO &io, int &sp, bool act) {
+  double lp[6], lx[6], ly[6];
+  sp--;
+  const double *pp = io.S + sp * 192;
+#pragma unroll
+  for (int r = 0; r < 6; r++) lp[r] = pp[r * 32];
+  double aa, bb;
+  rec_ratios(CS, R, 1, aa, bb);
+  split(CS, R, 1, flag_signs(hw.w & 0xff), aa, bb, lp, gin, lx, ly);
+  __syncwarp();
+  // child outputs: beads -> velocity rows; tile roots -> exchange rows; others -> stack,
+  // pushed so that the child finished LAST upward (visited next here) ends on top
+  auto emit = [&](int32_t src, const double (&l)[6], bool bead) {
+    if (bead) {
+      st_rows<ACT>(io.outB + 3 * src * io.Ki, io.Ki, l, 3, act);
+    } else if (src == -1) {
+      double *q = io.S + sp * 192;
+#pragma unroll
+      for (int r = 0; r < 6; r++) q[r * 32] = l[r];
+      sp++;
+    } else {
+      st_rows<ACT>(io.scr + (-2 - src) * 6 * io.Ki, io.Ki, l, 6, act);
+    }
+  };
+  if (CS == BEAD_BEAD) {
+    emit(hw.x, lx, true);
+    emit(hw.y, ly, true);
+  } else if (CS == RIGID_BEAD) {
+    emit(hw.x, lx, false);
+    emit(hw.y, ly, true);
+  } else if (hw.x == -1 && hw.y == -1 && !(hw.w >> 8)) {
+    emit(hw.y, ly, false);
+    emit(hw.x, lx, false);
+  } else {
+    emit(hw.x, lx, false);
+    emit(hw.y, ly, false);
+  }
+}
+
+template <bool UP, bool ACT>
+__device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, double *stk, uint8_t *ring, int lane,
+                                         int64_t col) {
+  const int64_t K = a.K;
+  const bool act = ACT || col < K;
+  const int64_t cc = act ? col : 0;  // clamped column: inactive lanes read valid memory, never store
+  const bool full = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV);
+  const int64_t bead0 = a.bead_off[U.body];
+  const int64_t sbase = full ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)U.body;
+  const uint8_t *E = a.prog + U.entry0 * ENTRY_BYTES;
+  const int n = U.n;
+  LaneIO io;
+  io.S = stk + lane;
+  io.Ki = (int)K;  // body-relative 32-bit row offsets (host guarantees rows * k < 2^31)
+  io.inB = a.in + 3 * bead0 * K + cc;
+  io.outB = a.out + 3 * bead0 * K + cc;
+  io.inR = a.in + sbase * K + cc;
+  io.outR = a.out + sbase * K + cc;
+  io.scr = a.scratch + cc;
+  // entry t (visiting order) lives at E + idx(t); the downward sweep visits backwards
+  auto idx = [&](int t) -> int64_t { return (int64_t)(UP ? t : n - 1 - t) * ENTRY_BYTES; };
+  auto issue = [&](int t) {
+    if (t < n && lane < ENTRY_BYTES / 16) cp_async16m(ring + (t % RING) * ENTRY_BYTES + 16 * lane, E + idx(t) + 16 * lane);
+    cp_commit_m();
+  };
+  auto slot = [&](int t) -> const uint8_t * { return ring + (t % RING) * ENTRY_BYTES; };
+  for (int t = 0; t < L2_AHEAD && t < n; t++)
+    if (lane < 2) prefetch_l2m(E + idx(t) + 128 * lane);
+  for (int t = 0; t < RING - 1; t++) issue(t);
+  cp_wait_m<RING - 2>();  // entry 0 resident
+  __syncwarp();
+  // gathered inputs of a node, prefetched one node ahead:
+  // UP: bead rows of x and y (BEAD_BEAD, RIGID_BEAD y); DOWN: residue rows
+  auto fetch = [&](const uint8_t *e, double (&g)[6]) {
+    const int4 hw = *reinterpret_cast<const int4 *>(e);
+    if (UP) {
+      const double *px = io.inB + 3 * (hw.x < 0 ? 0 : hw.x) * io.Ki, *py = io.inB + 3 * (hw.y < 0 ? 0 : hw.y) * io.Ki;
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+        g[r] = hw.x >= 0 ? __ldg(px + r * io.Ki) : 0.0;
+        g[3 + r] = hw.y >= 0 ? __ldg(py + r * io.Ki) : 0.0;
+      }
+    } else {
+      const int nres = res_rows(flag_case(hw.w & 0xff));
+      const double *pr = io.inR + (hw.z < 0 ? 0 : hw.z) * io.Ki;
+#pragma unroll
+      for (int r = 0; r < 6; r++) g[r] = r < nres ? __ldg(pr + r * io.Ki) : 0.0;
+    }
+  };
+  double gin[6], gnx[6];
+  if (n > 0) fetch(slot(0), gin);
+  int sp = 0;
+  if (!UP) {  // root RV-set of the unit
+    double v[6];
+#pragma unroll
+    for (int r = 0; r < 6; r++) {
+      v[r] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
+      if (U.out_slot >= 0) v[r] = io.scr[(U.out_slot * 6 + r) * io.Ki];
+      else if (a.op == RQ_OP_QTV) v[r] = io.inB[r * io.Ki];
+      io.S[r * 32] = v[r];
+    }
+    sp = 1;
+    __syncwarp();
+  }
+  for (int t = 0; t < n; t++) {
+    issue(t + RING - 1);
+    if (lane < 2 && t + L2_AHEAD < n) prefetch_l2m(E + idx(t + L2_AHEAD) + 128 * lane);
+    cp_wait_m<RING - 2>();  // entries <= t+1 resident
+    __syncwarp();
+    const uint8_t *e = slot(t);
+    const int4 hw = *reinterpret_cast<const int4 *>(e);
+    const int cs = flag_case(hw.w & 0xff);
+    if (t + 1 < n) fetch(slot(t + 1), gnx);
+    double R[rec_size(GENERAL)];
+    if (cs == GENERAL) {
+      lds_rec<GENERAL>(e, R);
+      if (UP) up_m<GENERAL, ACT>(hw, R, gin, io, sp, act); else down_m<GENERAL, ACT>(hw, R, gin, io, sp, act);
+    } else if (cs == RIGID_BEAD) {
+      lds_rec<RIGID_BEAD>(e, R);
+      if (UP) up_m<RIGID_BEAD, ACT>(hw, R, gin, io, sp, act); else down_m<RIGID_BEAD, ACT>(hw, R, gin, io, sp, act);
+    } else {
+      lds_rec<BEAD_BEAD>(e, R);
+      if (UP) up_m<BEAD_BEAD, ACT>(hw, R, gin, io, sp, act); else down_m<BEAD_BEAD, ACT>(hw, R, gin, io, sp, act);
+    }
+#pragma unroll
+    for (int r = 0; r < 6; r++) gin[r] = gnx[r];
+    __syncwarp();  // ring slot t is refilled by the next iteration's issue
+  }
+  cp_wait_m<0>();
+  if (UP && (ACT || act)) {  // unit root
+    const double *top = io.S + (sp - 1) * 192;
+    if (U.out_slot >= 0) {
+#pragma unroll
+      for (int r = 0; r < 6; r++) io.scr[(U.out_slot * 6 + r) * io.Ki] = top[r * 32];
+    } else if (a.op == RQ_OP_QV) {
+#pragma unroll
+      for (int r = 0; r < 6; r++) io.outB[r * io.Ki] = top[r * 32];
+    }
+  }
+  __syncwarp();
+}
+
+template <bool UP>
+__global__ void __launch_bounds__(MRHS_NT, 4) k_mrhs(MrhsCtx a) {
+  extern __shared__ __align__(16) double smem_m[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const size_t warp_doubles = (size_t)a.depth * 6 * 32 + RING * ENTRY_BYTES / 8;
+  double *stk = smem_m + (size_t)wib * warp_doubles;
+  uint8_t *ring = reinterpret_cast<uint8_t *>(stk + (size_t)a.depth * 6 * 32);
+  const int64_t GW = (int64_t)gridDim.x * (MRHS_NT / 32);
+  const bool all_full = (a.K % 32) == 0;
+  for (int64_t item = (int64_t)blockIdx.x * (MRHS_NT / 32) + wib; item < a.n_units * a.n_cg; item += GW) {
+    const UnitDesc U = a.units[item / a.n_cg];
+    const int64_t col = (item % a.n_cg) * 32 + lane;
+    if (all_full) run_unit<UP, true>(a, U, stk, ring, lane, col);
+    else run_unit<UP, false>(a, U, stk, ring, lane, col);
+  }
+}
+#undef STK
+
+__global__ void k_small_m(const int32_t *bodies, int64_t n, const int64_t *bead_off, const double *in,
+                          double *out, int64_t K) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= 3 * n * K) return;
+  const int64_t b = t / (3 * K), rc = t % (3 * K);
+  const int64_t i = 3 * bead_off[bodies[b]] * K + rc;
+  out[i] = in[i];
+}
+
+template <class T>
+T d2h1m(const void *src, cudaStream_t s) {
+  T v;
+  RQ_CUDA(cudaMemcpyAsync(&v, src, sizeof(T), cudaMemcpyDeviceToHost, s));
+  RQ_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+}  // namespace
+
+void build_mrhs(const Plan &p, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(p.mrhs_mu);
+  if (p.mrhs_built) return;
+  const int64_t NN = p.NN, m = p.m;
+  BuildCtx c;
+  c.S = p.tile_leaves;
+  c.NN = NN;
+  c.m = m;
+  c.bead_off = p.bead_off_d.as<int64_t>();
+  c.node_off = p.node_off_d.as<int64_t>();
+  c.rec_off = p.rec_off.as<int64_t>();
+  c.start = p.start.as<int32_t>();
+  c.stop = p.stop.as<int32_t>();
+  c.left = p.left.as<int32_t>();
+  c.right = p.right.as<int32_t>();
+  c.parent = p.parent.as<int32_t>();
+  c.res_off = p.res_off.as<int32_t>();
+  c.perm = p.perm.as<int32_t>();
+  c.flags = p.flags.as<uint8_t>();
+  c.rec = p.rec.as<double>();
+  auto nb = [](int64_t n) { return (unsigned)std::max<int64_t>(1, (n + 255) / 256); };
+  DBuf is_tile, is_top, tile_nodes, top_count, tile_scan, top_scan, tile_entry_scan, slot_of, dmax;
+  const int64_t NNa = std::max<int64_t>(NN, 1);
+  is_tile.alloc(NNa * 4);
+  is_top.alloc(NNa * 4);
+  tile_nodes.alloc(NNa * 4);
+  top_count.alloc(std::max<int64_t>(m, 1) * 4);
+  tile_scan.alloc(NNa * 4);
+  top_scan.alloc(NNa * 4);
+  tile_entry_scan.alloc(NNa * 8);
+  slot_of.alloc(NNa * 4);
+  dmax.alloc(8);
+  RQ_CUDA(cudaMemsetAsync(top_count.p, 0, std::max<int64_t>(m, 1) * 4, s));
+  RQ_CUDA(cudaMemsetAsync(slot_of.p, 0xff, NNa * 4, s));
+  RQ_CUDA(cudaMemsetAsync(dmax.p, 0, 8, s));
+  if (NN > 0) k_unit_flags<<<nb(NN), 256, 0, s>>>(c, is_tile.as<int32_t>(), is_top.as<int32_t>(),
+                                                  tile_nodes.as<int32_t>(), top_count.as<int32_t>());
+  // scans on the host side of the device (small, one-time): copy flags back
+  std::vector<int32_t> h_tile(NN), h_top(NN), h_tn(NN), h_tc(m);
+  if (NN) {
+    RQ_CUDA(cudaMemcpyAsync(h_tile.data(), is_tile.p, NN * 4, cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaMemcpyAsync(h_top.data(), is_top.p, NN * 4, cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaMemcpyAsync(h_tn.data(), tile_nodes.p, NN * 4, cudaMemcpyDeviceToHost, s));
+  }
+  if (m) RQ_CUDA(cudaMemcpyAsync(h_tc.data(), top_count.p, m * 4, cudaMemcpyDeviceToHost, s));
+  RQ_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> h_tscan(NN), h_pscan(NN);
+  std::vector<int64_t> h_escan(NN);
+  int64_t nt = 0, np = 0, ne = 0;
+  std::vector<int64_t> top_entry_base;
+  std::vector<int64_t> h_body_of_top;
+  for (int64_t g = 0; g < NN; g++) {
+    h_tscan[g] = (int32_t)nt;
+    h_escan[g] = ne;
+    h_pscan[g] = (int32_t)np;
+    if (h_tile[g]) { nt++; ne += h_tn[g]; }
+    if (h_top[g]) np++;
+  }
+  // top-unit entries follow all tile-unit entries, in body order
+  {
+    int64_t e = ne;
+    for (int64_t j = 0; j < m; j++) {
+      if (h_tc[j] > 0) { top_entry_base.push_back(e); e += h_tc[j]; }
+    }
+    p.mrhs_entries = e;
+  }
+  p.n_tile_units = nt;
+  p.n_top_units = np;
+  RQ_CUDA(cudaMemcpyAsync(tile_scan.p, h_tscan.data(), NN * 4, cudaMemcpyHostToDevice, s));
+  RQ_CUDA(cudaMemcpyAsync(top_scan.p, h_pscan.data(), NN * 4, cudaMemcpyHostToDevice, s));
+  RQ_CUDA(cudaMemcpyAsync(tile_entry_scan.p, h_escan.data(), NN * 8, cudaMemcpyHostToDevice, s));
+  DBuf teb;
+  teb.alloc(std::max<size_t>(top_entry_base.size(), 1) * 8);
+  if (!top_entry_base.empty())
+    RQ_CUDA(cudaMemcpyAsync(teb.p, top_entry_base.data(), top_entry_base.size() * 8, cudaMemcpyHostToDevice, s));
+  const int64_t nu = nt + np;
+  p.mrhs_units.alloc(std::max<int64_t>(nu, 1) * sizeof(UnitDesc));
+  p.mrhs_prog.alloc(std::max<int64_t>(p.mrhs_entries, 1) * ENTRY_BYTES);
+  RQ_CUDA(cudaMemsetAsync(p.mrhs_prog.p, 0, std::max<int64_t>(p.mrhs_entries, 1) * ENTRY_BYTES, s));
+  if (NN > 0)
+    k_unit_list<<<nb(NN), 256, 0, s>>>(c, is_tile.as<int32_t>(), tile_scan.as<int32_t>(),
+                                       tile_entry_scan.as<int64_t>(), is_top.as<int32_t>(), top_scan.as<int32_t>(),
+                                       teb.as<int64_t>(), top_count.as<int32_t>(), nt,
+                                       p.mrhs_units.as<UnitDesc>(), slot_of.as<int32_t>());
+  if (nu > 0)
+    k_unit_program<<<nb(nu), 256, 0, s>>>(c, p.mrhs_units.as<UnitDesc>(), nu, slot_of.as<int32_t>(),
+                                          p.mrhs_prog.as<uint8_t>(), dmax.as<int32_t>(), dmax.as<int32_t>() + 1, nt);
+  RQ_CUDA(cudaGetLastError());
+  int32_t hd[2] = {0, 0};
+  RQ_CUDA(cudaMemcpyAsync(hd, dmax.p, 8, cudaMemcpyDeviceToHost, s));
+  RQ_CUDA(cudaStreamSynchronize(s));
+  p.mrhs_depth_tile = std::max(1, hd[0]);
+  p.mrhs_depth_top = std::max(1, hd[1]);
+  // body -> unit ranges (host), for body-segmented applications
+  std::vector<UnitDesc> hu(nu);
+  if (nu) RQ_CUDA(cudaMemcpy(hu.data(), p.mrhs_units.p, nu * sizeof(UnitDesc), cudaMemcpyDeviceToHost));
+  p.h_tile_unit_first.assign(m + 1, nt);
+  p.h_top_unit_first.assign(m + 1, np);
+  for (int64_t u = nt - 1; u >= 0; u--) p.h_tile_unit_first[hu[u].body] = u;
+  for (int64_t u = np - 1; u >= 0; u--) p.h_top_unit_first[hu[nt + u].body] = u;
+  for (int64_t j = m - 1; j >= 0; j--) {
+    p.h_tile_unit_first[j] = std::min(p.h_tile_unit_first[j], p.h_tile_unit_first[j + 1]);
+    p.h_top_unit_first[j] = std::min(p.h_top_unit_first[j], p.h_top_unit_first[j + 1]);
+  }
+  p.mrhs_built = true;
+}
+
+void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
+                    BodyRange range) {
+  build_mrhs(p, s);
+  const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);
+  const bool all = range.j1 < 0;
+  const int64_t j0 = all ? 0 : range.j0, j1 = all ? p.m : range.j1;
+  const int64_t t0 = p.h_tile_unit_first[j0], t1 = p.h_tile_unit_first[j1];
+  const int64_t q0 = p.h_top_unit_first[j0], q1 = p.h_top_unit_first[j1];
+  const size_t scratch_bytes = (size_t)std::max<int64_t>(p.n_tile_units, 1) * 6 * k * 8;
+  if (p.mrhs_scratch.bytes < scratch_bytes) p.mrhs_scratch.alloc(scratch_bytes);
+  int sms = 0;
+  RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+  MrhsCtx a{};
+  a.prog = p.mrhs_prog.as<uint8_t>();
+  a.bead_off = p.bead_off_d.as<int64_t>();
+  a.in = in;
+  a.out = out;
+  a.scratch = p.mrhs_scratch.as<double>();
+  a.K = k;
+  a.op = op;
+  a.n_cg = (k + 31) / 32;
+  auto launch = [&](int64_t u0, int64_t u1, int depth) {
+    if (u1 <= u0) return;
+    a.units = p.mrhs_units.as<UnitDesc>() + u0;
+    a.n_units = u1 - u0;
+    a.depth = depth;
+    const size_t smem = (size_t)(MRHS_NT / 32) * ((size_t)depth * 6 * 32 * 8 + RING * ENTRY_BYTES);
+    const void *fn = up ? (const void *)k_mrhs<true> : (const void *)k_mrhs<false>;
+    RQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MRHS_NT, smem));
+    if (occ < 1) throw Error(RQ_ERR_CUDA, "multi-RHS kernel does not fit on an SM");
+    const int64_t items = a.n_units * a.n_cg;
+    const int64_t blocks = std::min<int64_t>((items + MRHS_NT / 32 - 1) / (MRHS_NT / 32), (int64_t)sms * occ);
+    if (up) k_mrhs<true><<<(unsigned)blocks, MRHS_NT, smem, s>>>(a);
+    else k_mrhs<false><<<(unsigned)blocks, MRHS_NT, smem, s>>>(a);
+  };
+  static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
+  DBuf dbg;
+  if (timing) {
+    const size_t bytes = (size_t)sms * 32 * 4 * 64;
+    dbg.alloc(bytes);
+    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, bytes, s));
+    a.dbg = dbg.as<long long>();
+  }
+  const int64_t nt = p.n_tile_units;
+  if (up) {
+    launch(t0, t1, p.mrhs_depth_tile);
+    launch(nt + q0, nt + q1, p.mrhs_depth_top);
+  } else {
+    launch(nt + q0, nt + q1, p.mrhs_depth_top);
+    launch(t0, t1, p.mrhs_depth_tile);
+  }
+  if (timing) {
+    std::vector<long long> h((size_t)sms * 32 * 4 * 8);
+    RQ_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    double acc[8] = {0};
+    for (size_t w = 0; w < h.size() / 8; w++) for (int i = 0; i < 8; i++) acc[i] += (double)h[8 * w + i];
+    fprintf(stderr, "[rq timing] mrhs op %d: per node: ring wait %.0f, node %.0f, input-wait+sync %.0f (nodes %.0f)\n", op,
+            acc[0] / acc[3], acc[1] / acc[3], acc[2] / acc[3], acc[3]);
+  }
+  const int64_t sm0 = all ? 0 : p.h_small_first[j0], sm1 = all ? p.n_small : p.h_small_first[j1];
+  if (sm1 > sm0 && op <= 1)
+    k_small_m<<<(unsigned)((3 * (sm1 - sm0) * k + 255) / 256), 256, 0, s>>>(
+        p.small_bodies.as<int32_t>() + sm0, sm1 - sm0, p.bead_off_d.as<int64_t>(), in, out, k);
+  RQ_CUDA(cudaGetLastError());
+}
+
+}  // namespace rq

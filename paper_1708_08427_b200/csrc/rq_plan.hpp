@@ -138,6 +138,14 @@ struct Plan {
   mutable cudaStream_t host_stream = nullptr, host_stream2 = nullptr, host_stream3 = nullptr;
 
   mutable std::mutex host_mu;
+  // multi-RHS unit programs (rq_mrhs.cu), built on the first k >= mrhs_min application
+  int mrhs_min = 8;
+  mutable std::mutex mrhs_mu;
+  mutable bool mrhs_built = false;
+  mutable int64_t mrhs_entries = 0, n_tile_units = 0, n_top_units = 0;
+  mutable int mrhs_depth_tile = 1, mrhs_depth_top = 1;
+  mutable DBuf mrhs_units, mrhs_prog, mrhs_scratch;
+  mutable std::vector<int64_t> h_tile_unit_first, h_top_unit_first;
   int64_t device_bytes() const;
   ~Plan() {
     for (cudaStream_t st : {host_stream, host_stream2, host_stream3})
@@ -153,6 +161,9 @@ struct BodyRange {
 };
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
                unsigned phases = 7u, BodyRange range = BodyRange());
+void build_mrhs(const Plan &p, cudaStream_t s);
+void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
+                    BodyRange range = BodyRange());
 // Host-buffer application pipelined over body segments: H2D of segment i+1,
 // kernels of segment i and D2H of segment i-1 overlap (three streams).
 void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k);

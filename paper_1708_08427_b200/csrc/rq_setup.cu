@@ -1056,6 +1056,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     throw Error(RQ_ERR_VALUE, "max_depth must be in [1, 128 - ceil(log2 m)]");
   if (const char *e = getenv("RQ_TILE_LEAVES")) p.tile_leaves = std::min(1024, std::max(2, atoi(e)));
   if (const char *e = getenv("RQ_CHUNK_THREADS")) p.chunk_threads = atoi(e);
+  if (const char *e = getenv("RQ_MRHS_MIN")) p.mrhs_min = std::max(2, atoi(e));
   p.m = m;
   p.N = N;
   p.NN = 2 * N - m;

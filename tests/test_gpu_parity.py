@@ -182,6 +182,48 @@ def test_oracle_config_sizes(rq, oracle_mod):
     assert rel(op3.apply("qtilde_tv", g3), ref3.apply("qtilde_tv", g3)) < TOL
 
 
+@pytest.mark.parametrize("k", [8, 32, 45])
+def test_multi_rhs(rq, oracle_mod, k):
+    """(rows, k) blocks (config-5 shape, reduced): the column-parallel stack-machine
+    kernels vs the oracle and vs column-by-column single-RHS results."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    counts = [4096] * 3 + [2, 3, 65, 64, 129, 20000, 1000, 1]
+    pos, off = ellipsoid_batch(counts, seed=21)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    ref = oracle_mod.OracleBatch(pos, off, threads=8)
+    rng = np.random.default_rng(k)
+    n = np.diff(off)
+    V = rng.normal(size=(3 * off[-1], k))
+    for opn in ("qv", "qtv"):
+        out = op.apply(opn, V)
+        exp = ref.apply(opn, V)
+        for c in range(k):
+            assert per_body_rel(out[:, c], exp[:, c], 3 * n) < TOL, (opn, c)
+        col = op.apply(opn, np.ascontiguousarray(V[:, 5]))
+        assert np.abs(out[:, 5] - col).max() <= 1e-13 * np.abs(col).max()
+    # complement operators need n >= 2 everywhere (and the reference's Q~^T
+    # raises for n == 2 blocks, matfree.py:161-170)
+    keep = [j for j in range(len(counts)) if counts[j] >= 3]
+    pos2 = np.concatenate([pos[off[j]:off[j + 1]] for j in keep])
+    off2 = np.concatenate([[0], np.cumsum([counts[j] for j in keep])])
+    op2 = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos2, off2))
+    ref2 = oracle_mod.OracleBatch(pos2, off2, threads=8)
+    n2 = np.diff(off2)
+    V2 = rng.normal(size=(3 * off2[-1], k))
+    G2 = rng.normal(size=(3 * off2[-1] - 6 * len(keep), k))
+    out = op2.apply("qtilde_v", V2)
+    exp = ref2.apply("qtilde_v", V2)
+    for c in range(k):
+        assert per_body_rel(out[:, c], exp[:, c], 3 * n2 - 6) < TOL, ("qtilde_v", c)
+    out = op2.apply("qtilde_tv", G2)
+    for c in (0, k // 2, k - 1):
+        exp = ref2.apply("qtilde_tv", np.ascontiguousarray(G2[:, c]))
+        assert per_body_rel(out[:, c], exp, 3 * n2) < TOL, ("qtilde_tv", c)
+    # round trip through the block path
+    assert np.abs(op2.apply("qtilde_v", out) - G2).max() < 1e-12 * np.abs(G2).max()
+
+
 def test_properties_large(rq):
     """Size-independent properties at config-2 body size: round trip, isometry,
     adjointness, complement property."""
