@@ -243,6 +243,7 @@ def main():
     outs = {"qtilde_v": torch.empty((3 * N - 6 * m, k), device=dev, dtype=torch.float64),
             "qtilde_tv": torch.empty((3 * N, k), device=dev, dtype=torch.float64)}
     kern = {}
+    mrhs = k >= info["mrhs_min_k"] and lib.rq_launches_per_apply(h, L.OP_QTILDE_V, k) < 2 * k
     for opn, code, x in (("qtilde_v", L.OP_QTILDE_V, v2), ("qtilde_tv", L.OP_QTILDE_TV, g2)):
         for phase, label in ((1, "chunks"), (2, "top")):
             reps = 50
@@ -254,16 +255,28 @@ def main():
                 L.check(lib.rq_apply_ex(h, code, x.data_ptr(), outs[opn].data_ptr(), k, stream, phase))
             b.record(s)
             torch.cuda.synchronize()
-            kern[(opn, label)] = a.elapsed_time(b) / reps / k  # ms per launch (per column)
+            # ms per launch (the single-RHS path launches once per column)
+            kern[(opn, label)] = a.elapsed_time(b) / reps / (1 if mrhs else k)
+    per_step = 1 if mrhs else k  # launches of each phase per application
     chunk_ms = 0.5 * (kern[("qtilde_v", "chunks")] + kern[("qtilde_tv", "chunks")])
-    # algorithmic bytes per chunk launch: the chunk blobs (records + meta + perm)
-    # plus one read and one write of every bead's 3 fp64 and residue coordinates
-    vec_bytes = 8 * (3 * N + (3 * N - 6 * m))
-    chunk_bytes = info["blob_bytes"] + vec_bytes
+    info = op.plan.info()  # multi-RHS programs are built by the first k >= mrhs_min_k apply
+    if mrhs:
+        # tile-unit launch: the unit programs (entry headers + records) once per group of
+        # 32 columns, every bead row and residue row of the k columns once, and the
+        # tile-root exchange rows (written upward / read downward)
+        ncg = (k + 31) // 32
+        chunk_bytes = (info["mrhs_bytes"]["tiles"] * ncg + 8 * k * (3 * N + (3 * N - 6 * m))
+                       + 8 * 6 * k * info["mrhs_units"]["tiles"])
+        kname = "k_mrhs (column-parallel stack machine over tile units, lane = RHS column)"
+    else:
+        # algorithmic bytes per chunk launch: the chunk blobs (records + meta + perm)
+        # plus one read and one write of every bead's 3 fp64 and residue coordinates
+        chunk_bytes = info["blob_bytes"] + 8 * (3 * N + (3 * N - 6 * m))
+        kname = "k_chunk (level-synchronous chunk sweep, TMA bulk-copied blobs)"
     achieved = chunk_bytes / (chunk_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
-    step_ms_kernels = sum(kern.values()) * k
-    share = (kern[("qtilde_v", "chunks")] + kern[("qtilde_tv", "chunks")]) * k / step_ms_kernels
+    step_ms_kernels = sum(kern.values()) * per_step
+    share = (kern[("qtilde_v", "chunks")] + kern[("qtilde_tv", "chunks")]) * per_step / step_ms_kernels
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "chunk_traffic.json")
     if os.path.exists(tpath):
@@ -323,7 +336,7 @@ def main():
             "config": config_dict(name, off, k, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_chunk (level-synchronous chunk sweep, TMA bulk-copied blobs)",
+                         "kernel": kname,
                          "bytes_per_launch": chunk_bytes, "launch_ms": chunk_ms, "peak_source": peak_src,
                          "share_of_step": share},
             "kernels_ms": {f"{a}:{b}": v_ for (a, b), v_ in kern.items()},

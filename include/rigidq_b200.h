@@ -72,6 +72,9 @@ typedef struct rq_plan_info {
   int64_t chunk_smem[6];   /* max head bytes, max level-record bytes, max beads, max nodes, max residues, max tiles */
   int64_t top_staged;      /* bodies whose top tree is staged in shared memory */
   int64_t top_global;      /* bodies whose top tree is swept from global memory */
+  int64_t mrhs_min_k;      /* k at and above which the column-parallel (multi-RHS) kernels run */
+  int64_t mrhs_units[2];   /* multi-RHS unit programs: tiles, top trees (0 until the first k >= mrhs_min_k apply) */
+  int64_t mrhs_bytes[2];   /* program bytes read per column group: tile units, top units */
 } rq_plan_info;
 
 /* Last error message of the calling thread ("" if none). */

@@ -43,7 +43,8 @@ class PlanInfo(C.Structure):
                 ("n_top", C.c_int64), ("tile_leaves", C.c_int64), ("blob_bytes", C.c_int64),
                 ("record_doubles", C.c_int64), ("full_len", C.c_int64), ("comp_len", C.c_int64),
                 ("max_chunk_bytes", C.c_int64), ("n_case", C.c_int64 * 4), ("device_bytes", C.c_int64),
-                ("chunk_smem", C.c_int64 * 6), ("top_staged", C.c_int64), ("top_global", C.c_int64)]
+                ("chunk_smem", C.c_int64 * 6), ("top_staged", C.c_int64), ("top_global", C.c_int64),
+                ("mrhs_min_k", C.c_int64), ("mrhs_units", C.c_int64 * 2), ("mrhs_bytes", C.c_int64 * 2)]
 
 
 SIGNATURES = [

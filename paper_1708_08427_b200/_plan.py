@@ -69,7 +69,10 @@ class Plan:
     def info(self) -> dict:
         inf = L.PlanInfo()
         L.check(L.lib().rq_plan_get_info(self._h, C.byref(inf)))
-        d = {k: getattr(inf, k) for k, _ in L.PlanInfo._fields_ if k not in ("n_case", "chunk_smem")}
+        d = {k: getattr(inf, k) for k, _ in L.PlanInfo._fields_
+             if k not in ("n_case", "chunk_smem", "mrhs_units", "mrhs_bytes")}
+        d["mrhs_units"] = {"tiles": inf.mrhs_units[0], "tops": inf.mrhs_units[1]}
+        d["mrhs_bytes"] = {"tiles": inf.mrhs_bytes[0], "tops": inf.mrhs_bytes[1]}
         d["n_case"] = list(inf.n_case)
         d["chunk_smem"] = dict(zip(("head", "level_rec", "beads", "nodes", "res", "tiles"), list(inf.chunk_smem)))
         return d

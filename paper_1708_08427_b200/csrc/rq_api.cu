@@ -48,19 +48,13 @@ void need_gpu() {
     throw rq::Error(RQ_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
   }
 }
-int64_t in_len(const rq::Plan &p, int op) {
-  return (op == RQ_OP_QTILDE_TV) ? 3 * p.N - 6 * p.m : 3 * p.N;
-}
-int64_t out_len(const rq::Plan &p, int op) {
-  return (op == RQ_OP_QTILDE_V) ? 3 * p.N - 6 * p.m : 3 * p.N;
-}
 }  // namespace
 
 extern "C" {
 
 const char *rq_last_error(void) { return rq::last_error(); }
 
-int rq_version(void) { return 100; }
+int rq_version(void) { return 101; }
 
 int rq_device_count(void) {
   int n = 0;
@@ -140,6 +134,11 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
     info->chunk_smem[5] = p.max_chunk_tiles;
     info->top_staged = p.n_topblob;
     info->top_global = p.n_topbig;
+    info->mrhs_min_k = p.mrhs_min;
+    info->mrhs_units[0] = p.n_tile_units;
+    info->mrhs_units[1] = p.n_top_units;
+    info->mrhs_bytes[0] = p.mrhs_tile_bytes;
+    info->mrhs_bytes[1] = p.mrhs_top_bytes;
   })
 }
 
@@ -163,6 +162,15 @@ int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int6
 int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
   if (!plan) return -1;
   const rq::Plan &p = plan->p;
+  if (rq::use_mrhs(p, k)) {  // column-parallel kernels: one launch per phase for all k columns
+    int tiles = 0, tops = 0;
+    for (int64_t j = 0; j < p.m; j++) {
+      const int64_t n = p.bead_off[j + 1] - p.bead_off[j];
+      tiles |= n >= 2;
+      tops |= n > p.tile_leaves;
+    }
+    return tiles + tops + ((p.n_small && op <= 1) ? 1 : 0);
+  }
   int per_col = (p.n_chunks ? 1 : 0) + (p.n_topblob ? 1 : 0) + (p.n_topbig ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
   return (int)(per_col * k);
 }

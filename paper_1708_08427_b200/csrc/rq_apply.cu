@@ -41,9 +41,6 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -397,7 +394,6 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     const ChunkDesc &d = *cv.hdr;
     const int64_t bead0 = d.body_bead0;
     const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? d.spec_full : d.spec_comp;
-    const double *grec = reinterpret_cast<const double *>(a.blob + d.blob_off + d.off_rec);
     double *M = reinterpret_cast<double *>(smem + SM.o_m);
     const int H = d.n_levels;
     const long long t_lv0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
@@ -775,13 +771,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     p.scratch.alloc(std::max<int64_t>(p.n_slots, 1) * 48);
     p.scratch_k = 1;
   }
-  int64_t max_n = 0;
-  if (k >= p.mrhs_min)
-    for (int64_t j = 0; j < p.m; j++) max_n = std::max(max_n, p.bead_off[j + 1] - p.bead_off[j]);
-  const int64_t lim32 = int64_t(1) << 31;
-  if (k >= p.mrhs_min && 3 * max_n * k < lim32 && 6 * std::max<int64_t>(p.n_slots, 1) * k < lim32) {
-    // column-parallel stack-machine kernels (rq_mrhs.cu)
-    run_apply_mrhs(p, op, in, out, k, s, range);
+  if (use_mrhs(p, k)) {  // column-parallel stack-machine kernels (rq_mrhs.cu)
+    run_apply_mrhs(p, op, in, out, k, s, phases, range);
     return;
   }
   const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);

@@ -124,7 +124,7 @@ __global__ void k_unit_list(BuildCtx c, const int32_t *is_tile_unit, const int32
 // one thread per unit: heavy-first postorder, entries written in visiting order
 __global__ void k_unit_program(BuildCtx c, UnitDesc *units, int64_t n_units, const int32_t *tile_slot_of,
                                uint8_t *prog, int32_t *max_depth_tile, int32_t *max_depth_top,
-                               int64_t n_tile_units) {
+                               int64_t n_tile_units, unsigned long long *bytes) {
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= n_units) return;
   UnitDesc d = units[u];
@@ -140,7 +140,7 @@ __global__ void k_unit_program(BuildCtx c, UnitDesc *units, int64_t n_units, con
   st_node[sp] = d.root;
   st_state[sp] = 0;
   sp++;
-  int64_t e = 0;
+  int64_t e = 0, used = 0;
   int depth = 0, maxdepth = 1;
   while (sp > 0) {
     const int64_t g = st_node[sp - 1];
@@ -180,6 +180,7 @@ __global__ void k_unit_program(BuildCtx c, UnitDesc *units, int64_t n_units, con
     const double *r = c.rec + c.rec_off[g];
     double *rd = reinterpret_cast<double *>(dst + sizeof(SEntry));
     for (int i = 0; i < rec_size(cs); i++) rd[i] = r[i];
+    used += sizeof(SEntry) + 8 * rec_size(cs);
     e++;
     // simulated information-vector stack: pop the stack children, push g
     maxdepth = max(maxdepth, depth);  // stack children resident before the pops
@@ -188,6 +189,7 @@ __global__ void k_unit_program(BuildCtx c, UnitDesc *units, int64_t n_units, con
   }
   units[u].depth = maxdepth;
   atomicMax(top ? max_depth_top : max_depth_tile, maxdepth);
+  atomicAdd(&bytes[top ? 1 : 0], (unsigned long long)used);
 }
 
 // ---- kernels ----------------------------------------------------------------------------
@@ -224,8 +226,9 @@ __device__ __forceinline__ void prefetch_l2m(const void *p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
 }
 
-constexpr int RING = 4;     // unit entries staged per warp (cp.async, RING-1 ahead)
-constexpr int L2_AHEAD = 8; // entries prefetched into L2 ahead of the ring
+constexpr int RING = 8;      // unit entries staged per warp (cp.async, RING-1 ahead)
+constexpr int PD = 4;        // gathered inputs of node t+PD are prefetched into L2 at node t
+constexpr int L2_AHEAD = 12; // entries prefetched into L2 ahead of the ring
 
 template <int CS>
 __device__ __forceinline__ void lds_rec(const uint8_t *e, double (&R)[rec_size(GENERAL)]) {
@@ -238,37 +241,34 @@ __device__ __forceinline__ void lds_rec(const uint8_t *e, double (&R)[rec_size(G
   }
 }
 
-__device__ __forceinline__ int ld_case_rec(const uint8_t *e, double (&R)[rec_size(GENERAL)]) {
-  const int cs = flag_case(reinterpret_cast<const SEntry *>(e)->flags);
-  if (cs == GENERAL) lds_rec<GENERAL>(e, R);
-  else if (cs == RIGID_BEAD) lds_rec<RIGID_BEAD>(e, R);
-  else lds_rec<BEAD_BEAD>(e, R);
-  return cs;
-}
 
 // Per-lane views used by the node bodies: S = stack base + lane (entry d,
-// component r at S[(6d + r) * 32]); column-relative row pointers of the body.
+// component r at S[(6d + r) * 32]; every lane touches only its own column, so
+// the stack needs no synchronisation); column-relative row pointers of the body.
+// KS = k when specialised at compile time (row strides become immediates), else 0.
+template <int KS>
 struct LaneIO {
   double *S;
   const double *inB, *inR;  // bead rows / residue rows of the body (input)
   double *outB, *outR;      // bead rows / residue rows of the body (output)
   double *scr;              // exchange rows of tile roots
-  int Ki;
+  int Kr;                   // runtime k (KS == 0)
+  __device__ __forceinline__ int ki() const { return KS ? KS : Kr; }
 };
 
-template <bool ACT>
-__device__ __forceinline__ void st_rows(double *p, int Ki, const double *v, int n, bool act) {
+template <bool ACT, int KS>
+__device__ __forceinline__ void st_rows(double *p, const LaneIO<KS> &io, const double *v, int n, bool act) {
   if (ACT || act) {
 #pragma unroll
     for (int r = 0; r < 6; r++)
-      if (r < n) p[r * Ki] = v[r];
+      if (r < n) p[r * io.ki()] = v[r];
   }
 }
 
 // merge_infosets (matfree.py:41-62) for one node of a unit, 32 columns
-template <int CS, bool ACT>
+template <int CS, bool ACT, int KS>
 __device__ __forceinline__ void up_m(const int4 &hw, const double (&R)[rec_size(GENERAL)], const double (&gin)[6],
-                                     const LaneIO &io, int &sp, bool act) {
+                                     const LaneIO<KS> &io, int &sp, bool act) {
   double mx[6], my[6];
   if (CS == BEAD_BEAD) {
 #pragma unroll
@@ -279,15 +279,23 @@ __device__ __forceinline__ void up_m(const int4 &hw, const double (&R)[rec_size(
     if (xs && ys) {
       if (hw.w >> 8) dx = sp - 2; else dy = sp - 2;  // x finished first: y on top
     }
-    const double *px = xs ? io.S + dx * 192 : io.scr + (-2 - hw.x) * 6 * io.Ki;
-    const int stx = xs ? 32 : io.Ki;
+    if (xs) {
 #pragma unroll
-    for (int r = 0; r < 6; r++) mx[r] = px[r * stx];
+      for (int r = 0; r < 6; r++) mx[r] = io.S[(dx * 6 + r) * 32];
+    } else {
+      const double *px = io.scr + (-2 - hw.x) * 6 * io.ki();
+#pragma unroll
+      for (int r = 0; r < 6; r++) mx[r] = px[r * io.ki()];
+    }
     if (CS == GENERAL) {
-      const double *py = ys ? io.S + dy * 192 : io.scr + (-2 - hw.y) * 6 * io.Ki;
-      const int sty = ys ? 32 : io.Ki;
+      if (ys) {
 #pragma unroll
-      for (int r = 0; r < 6; r++) my[r] = py[r * sty];
+        for (int r = 0; r < 6; r++) my[r] = io.S[(dy * 6 + r) * 32];
+      } else {
+        const double *py = io.scr + (-2 - hw.y) * 6 * io.ki();
+#pragma unroll
+        for (int r = 0; r < 6; r++) my[r] = py[r * io.ki()];
+      }
     } else {
 #pragma unroll
       for (int r = 0; r < 3; r++) { my[r] = gin[3 + r]; my[3 + r] = 0.0; }
@@ -297,39 +305,34 @@ __device__ __forceinline__ void up_m(const int4 &hw, const double (&R)[rec_size(
   double aa, bb, mp[6], res[6];
   rec_ratios(CS, R, 1, aa, bb);
   merge(CS, R, 1, flag_signs(hw.w & 0xff), aa, bb, mx, my, mp, res);
-  if (CS != BEAD_BEAD) st_rows<ACT>(io.outR + hw.z * io.Ki, io.Ki, res, res_rows(CS), act);
-  __syncwarp();
-  double *pp = io.S + sp * 192;
+  if (CS != BEAD_BEAD) st_rows<ACT>(io.outR + hw.z * io.ki(), io, res, res_rows(CS), act);
 #pragma unroll
-  for (int r = 0; r < 6; r++) pp[r * 32] = mp[r];
+  for (int r = 0; r < 6; r++) io.S[(sp * 6 + r) * 32] = mp[r];
   sp++;
 }
 
 // split_rvset (matfree.py:65-83) for one node of a unit, 32 columns
-template <int CS, bool ACT>
+template <int CS, bool ACT, int KS>
 __device__ __forceinline__ void down_m(const int4 &hw, const double (&R)[rec_size(GENERAL)],
-                                       const double (&gin)[6], const LaneIO &io, int &sp, bool act) {
+                                       const double (&gin)[6], const LaneIO<KS> &io, int &sp, bool act) {
   double lp[6], lx[6], ly[6];
   sp--;
-  const double *pp = io.S + sp * 192;
 #pragma unroll
-  for (int r = 0; r < 6; r++) lp[r] = pp[r * 32];
+  for (int r = 0; r < 6; r++) lp[r] = io.S[(sp * 6 + r) * 32];
   double aa, bb;
   rec_ratios(CS, R, 1, aa, bb);
   split(CS, R, 1, flag_signs(hw.w & 0xff), aa, bb, lp, gin, lx, ly);
-  __syncwarp();
   // child outputs: beads -> velocity rows; tile roots -> exchange rows; others -> stack,
   // pushed so that the child finished LAST upward (visited next here) ends on top
   auto emit = [&](int32_t src, const double (&l)[6], bool bead) {
     if (bead) {
-      st_rows<ACT>(io.outB + 3 * src * io.Ki, io.Ki, l, 3, act);
+      st_rows<ACT>(io.outB + 3 * src * io.ki(), io, l, 3, act);
     } else if (src == -1) {
-      double *q = io.S + sp * 192;
 #pragma unroll
-      for (int r = 0; r < 6; r++) q[r * 32] = l[r];
+      for (int r = 0; r < 6; r++) io.S[(sp * 6 + r) * 32] = l[r];
       sp++;
     } else {
-      st_rows<ACT>(io.scr + (-2 - src) * 6 * io.Ki, io.Ki, l, 6, act);
+      st_rows<ACT>(io.scr + (-2 - src) * 6 * io.ki(), io, l, 6, act);
     }
   };
   if (CS == BEAD_BEAD) {
@@ -347,7 +350,33 @@ __device__ __forceinline__ void down_m(const int4 &hw, const double (&R)[rec_siz
   }
 }
 
-template <bool UP, bool ACT>
+// gathered inputs of a node (issued one node ahead): UP: bead rows of the bead
+// children (BEAD_BEAD: x and y, RIGID_BEAD: y); DOWN: the node's residue rows
+template <bool UP, int KS>
+__device__ __forceinline__ void fetch_m(const int4 &hw, const LaneIO<KS> &io, double (&g)[6]) {
+  const int cs = flag_case(hw.w & 0xff);
+  const int k = io.ki();
+  if (UP) {
+    if (cs == BEAD_BEAD) {
+      const double *px = io.inB + 3 * hw.x * k, *py = io.inB + 3 * hw.y * k;
+      g[0] = __ldg(px); g[1] = __ldg(px + k); g[2] = __ldg(px + 2 * k);
+      g[3] = __ldg(py); g[4] = __ldg(py + k); g[5] = __ldg(py + 2 * k);
+    } else if (cs == RIGID_BEAD) {
+      const double *py = io.inB + 3 * hw.y * k;
+      g[3] = __ldg(py); g[4] = __ldg(py + k); g[5] = __ldg(py + 2 * k);
+    }
+  } else {
+    const double *pr = io.inR + hw.z * k;
+    if (cs == GENERAL) {
+#pragma unroll
+      for (int r = 0; r < 6; r++) g[r] = __ldg(pr + r * k);
+    } else if (cs == RIGID_BEAD) {
+      g[0] = __ldg(pr); g[1] = __ldg(pr + k); g[2] = __ldg(pr + 2 * k);
+    }
+  }
+}
+
+template <bool UP, bool ACT, int KS>
 __device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, double *stk, uint8_t *ring, int lane,
                                          int64_t col) {
   const int64_t K = a.K;
@@ -358,9 +387,9 @@ __device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, do
   const int64_t sbase = full ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)U.body;
   const uint8_t *E = a.prog + U.entry0 * ENTRY_BYTES;
   const int n = U.n;
-  LaneIO io;
+  LaneIO<KS> io;
   io.S = stk + lane;
-  io.Ki = (int)K;  // body-relative 32-bit row offsets (host guarantees rows * k < 2^31)
+  io.Kr = (int)K;  // body-relative 32-bit row offsets (host guarantees rows * k < 2^31)
   io.inB = a.in + 3 * bead0 * K + cc;
   io.outB = a.out + 3 * bead0 * K + cc;
   io.inR = a.in + sbase * K + cc;
@@ -376,50 +405,49 @@ __device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, do
   for (int t = 0; t < L2_AHEAD && t < n; t++)
     if (lane < 2) prefetch_l2m(E + idx(t) + 128 * lane);
   for (int t = 0; t < RING - 1; t++) issue(t);
-  cp_wait_m<RING - 2>();  // entry 0 resident
+  cp_wait_m<RING - 1 - PD>();  // entries <= PD-1 resident
   __syncwarp();
-  // gathered inputs of a node, prefetched one node ahead:
-  // UP: bead rows of x and y (BEAD_BEAD, RIGID_BEAD y); DOWN: residue rows
-  auto fetch = [&](const uint8_t *e, double (&g)[6]) {
-    const int4 hw = *reinterpret_cast<const int4 *>(e);
+  // L2 prefetch of the gathered rows of node t (bead rows / residue rows), one line per lane
+  const int64_t col0 = col - lane;
+  const double *pfB = a.in + 3 * bead0 * K + col0, *pfR = a.in + sbase * K + col0;
+  auto prefetch_inputs = [&](int t) {
+    if (t >= n || lane >= 12) return;
+    const int4 hw = *reinterpret_cast<const int4 *>(slot(t));
+    const int half = lane & 1;
     if (UP) {
-      const double *px = io.inB + 3 * (hw.x < 0 ? 0 : hw.x) * io.Ki, *py = io.inB + 3 * (hw.y < 0 ? 0 : hw.y) * io.Ki;
-#pragma unroll
-      for (int r = 0; r < 3; r++) {
-        g[r] = hw.x >= 0 ? __ldg(px + r * io.Ki) : 0.0;
-        g[3 + r] = hw.y >= 0 ? __ldg(py + r * io.Ki) : 0.0;
-      }
+      const int b = lane < 6 ? hw.x : hw.y, r = (lane % 6) >> 1;
+      if (b >= 0) prefetch_l2m(pfB + (3 * (int64_t)b + r) * K + 16 * half);
     } else {
-      const int nres = res_rows(flag_case(hw.w & 0xff));
-      const double *pr = io.inR + (hw.z < 0 ? 0 : hw.z) * io.Ki;
-#pragma unroll
-      for (int r = 0; r < 6; r++) g[r] = r < nres ? __ldg(pr + r * io.Ki) : 0.0;
+      const int r = lane >> 1;
+      if (hw.z >= 0 && r < res_rows(flag_case(hw.w & 0xff))) prefetch_l2m(pfR + (int64_t)(hw.z + r) * K + 16 * half);
     }
   };
-  double gin[6], gnx[6];
-  if (n > 0) fetch(slot(0), gin);
+  for (int t = 0; t < PD; t++) prefetch_inputs(t);
+  double gA[6], gB[6];
+  if (n > 0) fetch_m<UP>(*reinterpret_cast<const int4 *>(slot(0)), io, gA);
   int sp = 0;
   if (!UP) {  // root RV-set of the unit
-    double v[6];
 #pragma unroll
     for (int r = 0; r < 6; r++) {
-      v[r] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
-      if (U.out_slot >= 0) v[r] = io.scr[(U.out_slot * 6 + r) * io.Ki];
-      else if (a.op == RQ_OP_QTV) v[r] = io.inB[r * io.Ki];
-      io.S[r * 32] = v[r];
+      double v = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
+      if (U.out_slot >= 0) v = io.scr[(U.out_slot * 6 + r) * io.ki()];
+      else if (a.op == RQ_OP_QTV) v = io.inB[r * io.ki()];
+      io.S[r * 32] = v;
     }
     sp = 1;
-    __syncwarp();
   }
-  for (int t = 0; t < n; t++) {
+  // one node: entries <= t+PD resident after the wait; the refill of ring slot
+  // t-1 is issued after the __syncwarp that ends every lane's reads of it
+  auto step = [&](int t, const double (&gin)[6], double (&gnx)[6]) {
+    cp_wait_m<RING - 2 - PD>();
+    __syncwarp();
     issue(t + RING - 1);
     if (lane < 2 && t + L2_AHEAD < n) prefetch_l2m(E + idx(t + L2_AHEAD) + 128 * lane);
-    cp_wait_m<RING - 2>();  // entries <= t+1 resident
-    __syncwarp();
+    prefetch_inputs(t + PD);
     const uint8_t *e = slot(t);
     const int4 hw = *reinterpret_cast<const int4 *>(e);
     const int cs = flag_case(hw.w & 0xff);
-    if (t + 1 < n) fetch(slot(t + 1), gnx);
+    if (t + 1 < n) fetch_m<UP>(*reinterpret_cast<const int4 *>(slot(t + 1)), io, gnx);
     double R[rec_size(GENERAL)];
     if (cs == GENERAL) {
       lds_rec<GENERAL>(e, R);
@@ -431,19 +459,19 @@ __device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, do
       lds_rec<BEAD_BEAD>(e, R);
       if (UP) up_m<BEAD_BEAD, ACT>(hw, R, gin, io, sp, act); else down_m<BEAD_BEAD, ACT>(hw, R, gin, io, sp, act);
     }
-#pragma unroll
-    for (int r = 0; r < 6; r++) gin[r] = gnx[r];
-    __syncwarp();  // ring slot t is refilled by the next iteration's issue
+  };
+  for (int t = 0; t < n; t += 2) {  // ping-pong input registers (no copies)
+    step(t, gA, gB);
+    if (t + 1 < n) step(t + 1, gB, gA);
   }
   cp_wait_m<0>();
   if (UP && (ACT || act)) {  // unit root
-    const double *top = io.S + (sp - 1) * 192;
     if (U.out_slot >= 0) {
 #pragma unroll
-      for (int r = 0; r < 6; r++) io.scr[(U.out_slot * 6 + r) * io.Ki] = top[r * 32];
+      for (int r = 0; r < 6; r++) io.scr[(U.out_slot * 6 + r) * io.ki()] = io.S[((sp - 1) * 6 + r) * 32];
     } else if (a.op == RQ_OP_QV) {
 #pragma unroll
-      for (int r = 0; r < 6; r++) io.outB[r * io.Ki] = top[r * 32];
+      for (int r = 0; r < 6; r++) io.outB[r * io.ki()] = io.S[((sp - 1) * 6 + r) * 32];
     }
   }
   __syncwarp();
@@ -457,12 +485,13 @@ __global__ void __launch_bounds__(MRHS_NT, 4) k_mrhs(MrhsCtx a) {
   double *stk = smem_m + (size_t)wib * warp_doubles;
   uint8_t *ring = reinterpret_cast<uint8_t *>(stk + (size_t)a.depth * 6 * 32);
   const int64_t GW = (int64_t)gridDim.x * (MRHS_NT / 32);
-  const bool all_full = (a.K % 32) == 0;
+  const int mode = a.K == 32 ? 0 : ((a.K % 32) == 0 ? 1 : 2);
   for (int64_t item = (int64_t)blockIdx.x * (MRHS_NT / 32) + wib; item < a.n_units * a.n_cg; item += GW) {
     const UnitDesc U = a.units[item / a.n_cg];
     const int64_t col = (item % a.n_cg) * 32 + lane;
-    if (all_full) run_unit<UP, true>(a, U, stk, ring, lane, col);
-    else run_unit<UP, false>(a, U, stk, ring, lane, col);
+    if (mode == 0) run_unit<UP, true, 32>(a, U, stk, ring, lane, col);
+    else if (mode == 1) run_unit<UP, true, 0>(a, U, stk, ring, lane, col);
+    else run_unit<UP, false, 0>(a, U, stk, ring, lane, col);
   }
 }
 #undef STK
@@ -507,7 +536,7 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
   c.flags = p.flags.as<uint8_t>();
   c.rec = p.rec.as<double>();
   auto nb = [](int64_t n) { return (unsigned)std::max<int64_t>(1, (n + 255) / 256); };
-  DBuf is_tile, is_top, tile_nodes, top_count, tile_scan, top_scan, tile_entry_scan, slot_of, dmax;
+  DBuf is_tile, is_top, tile_nodes, top_count, tile_scan, top_scan, tile_entry_scan, slot_of, dmax, dbytes;
   const int64_t NNa = std::max<int64_t>(NN, 1);
   is_tile.alloc(NNa * 4);
   is_top.alloc(NNa * 4);
@@ -521,6 +550,8 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
   RQ_CUDA(cudaMemsetAsync(top_count.p, 0, std::max<int64_t>(m, 1) * 4, s));
   RQ_CUDA(cudaMemsetAsync(slot_of.p, 0xff, NNa * 4, s));
   RQ_CUDA(cudaMemsetAsync(dmax.p, 0, 8, s));
+  dbytes.alloc(16);
+  RQ_CUDA(cudaMemsetAsync(dbytes.p, 0, 16, s));
   if (NN > 0) k_unit_flags<<<nb(NN), 256, 0, s>>>(c, is_tile.as<int32_t>(), is_top.as<int32_t>(),
                                                   tile_nodes.as<int32_t>(), top_count.as<int32_t>());
   // scans on the host side of the device (small, one-time): copy flags back
@@ -572,11 +603,16 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
                                        p.mrhs_units.as<UnitDesc>(), slot_of.as<int32_t>());
   if (nu > 0)
     k_unit_program<<<nb(nu), 256, 0, s>>>(c, p.mrhs_units.as<UnitDesc>(), nu, slot_of.as<int32_t>(),
-                                          p.mrhs_prog.as<uint8_t>(), dmax.as<int32_t>(), dmax.as<int32_t>() + 1, nt);
+                                          p.mrhs_prog.as<uint8_t>(), dmax.as<int32_t>(), dmax.as<int32_t>() + 1, nt,
+                                          dbytes.as<unsigned long long>());
   RQ_CUDA(cudaGetLastError());
   int32_t hd[2] = {0, 0};
   RQ_CUDA(cudaMemcpyAsync(hd, dmax.p, 8, cudaMemcpyDeviceToHost, s));
   RQ_CUDA(cudaStreamSynchronize(s));
+  unsigned long long hb[2] = {0, 0};
+  RQ_CUDA(cudaMemcpy(hb, dbytes.p, 16, cudaMemcpyDeviceToHost));
+  p.mrhs_tile_bytes = (int64_t)hb[0];
+  p.mrhs_top_bytes = (int64_t)hb[1];
   p.mrhs_depth_tile = std::max(1, hd[0]);
   p.mrhs_depth_top = std::max(1, hd[1]);
   // body -> unit ranges (host), for body-segmented applications
@@ -593,8 +629,17 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
   p.mrhs_built = true;
 }
 
+bool use_mrhs(const Plan &p, int64_t k) {
+  if (k < p.mrhs_min) return false;
+  int64_t max_n = 0;
+  for (int64_t j = 0; j < p.m; j++) max_n = std::max(max_n, p.bead_off[j + 1] - p.bead_off[j]);
+  // the kernels use 32-bit body-relative row offsets
+  const int64_t lim32 = int64_t(1) << 31;
+  return 3 * max_n * k < lim32 && 6 * std::max<int64_t>(p.n_slots, 1) * k < lim32;
+}
+
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
-                    BodyRange range) {
+                    unsigned phases, BodyRange range) {
   build_mrhs(p, s);
   const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);
   const bool all = range.j1 < 0;
@@ -639,12 +684,13 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
     a.dbg = dbg.as<long long>();
   }
   const int64_t nt = p.n_tile_units;
+  const bool do_tiles = phases & 1u, do_top = phases & 2u;
   if (up) {
-    launch(t0, t1, p.mrhs_depth_tile);
-    launch(nt + q0, nt + q1, p.mrhs_depth_top);
+    if (do_tiles) launch(t0, t1, p.mrhs_depth_tile);
+    if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top);
   } else {
-    launch(nt + q0, nt + q1, p.mrhs_depth_top);
-    launch(t0, t1, p.mrhs_depth_tile);
+    if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top);
+    if (do_tiles) launch(t0, t1, p.mrhs_depth_tile);
   }
   if (timing) {
     std::vector<long long> h((size_t)sms * 32 * 4 * 8);
@@ -656,7 +702,7 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
             acc[0] / acc[3], acc[1] / acc[3], acc[2] / acc[3], acc[3]);
   }
   const int64_t sm0 = all ? 0 : p.h_small_first[j0], sm1 = all ? p.n_small : p.h_small_first[j1];
-  if (sm1 > sm0 && op <= 1)
+  if ((phases & 4u) && sm1 > sm0 && op <= 1)
     k_small_m<<<(unsigned)((3 * (sm1 - sm0) * k + 255) / 256), 256, 0, s>>>(
         p.small_bodies.as<int32_t>() + sm0, sm1 - sm0, p.bead_off_d.as<int64_t>(), in, out, k);
   RQ_CUDA(cudaGetLastError());

@@ -143,6 +143,7 @@ struct Plan {
   mutable std::mutex mrhs_mu;
   mutable bool mrhs_built = false;
   mutable int64_t mrhs_entries = 0, n_tile_units = 0, n_top_units = 0;
+  mutable int64_t mrhs_tile_bytes = 0, mrhs_top_bytes = 0;  // entry header + record bytes per column group
   mutable int mrhs_depth_tile = 1, mrhs_depth_top = 1;
   mutable DBuf mrhs_units, mrhs_prog, mrhs_scratch;
   mutable std::vector<int64_t> h_tile_unit_first, h_top_unit_first;
@@ -163,7 +164,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
                unsigned phases = 7u, BodyRange range = BodyRange());
 void build_mrhs(const Plan &p, cudaStream_t s);
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
-                    BodyRange range = BodyRange());
+                    unsigned phases = 7u, BodyRange range = BodyRange());
+bool use_mrhs(const Plan &p, int64_t k);
 // Host-buffer application pipelined over body segments: H2D of segment i+1,
 // kernels of segment i and D2H of segment i-1 overlap (three streams).
 void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k);
