@@ -511,91 +511,131 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
 
 // ---- top tree (nodes with more than tile_leaves beads) ---------------------------------
 
-struct TopCtx {
-  const int32_t *tb_list;  // top-body indices processed by this launch
+// Top trees too large for shared memory (e.g. config 3's single 2^20-bead body:
+// ~23k top nodes, height ~15) run as dataflow sweeps over global memory, one
+// thread per "start" node (both children below the top tree):
+//  * upward: a thread merges its node, publishes the info vector (scratch slot),
+//    then climbs to the parent only if it is the second child to arrive (per-node
+//    arrival counters, self-resetting) -- no level barriers, full parallelism;
+//  * downward: every thread recomputes the split chain along its root-to-node
+//    path (identical arithmetic, so every path sees identical values) and writes
+//    the outputs of the children that leave the top tree (tile roots, beads).
+struct TopDfCtx {
+  const int32_t *starts;
+  int64_t n;
   const TopNode *top;
-  const int32_t *topbody, *topbody_lvl, *toplvl, *perm;
+  const int32_t *parent, *need;
+  int32_t *cnt;
+  const int32_t *perm;
   const int64_t *bead_off;
   const double *rec;
   const double *in;
   double *out;
   int64_t k, col;
   double *scratch;
-  int op;
+  int op, S;
 };
 
-template <bool UP>
-__global__ void __launch_bounds__(NT_TOP) k_top(TopCtx a) {
-  const int bi = a.tb_list[blockIdx.x];
-  const int j = a.topbody[bi];
-  const int64_t bead0 = a.bead_off[j];
-  const int64_t sbase = spec_base(a.op, a.bead_off, j);
-  const int64_t K = a.k, col = a.col;
-  const int lv0 = a.topbody_lvl[bi], lv1 = a.topbody_lvl[bi + 1];
-  for (int s = 0; s < lv1 - lv0; s++) {
-    const int lv = UP ? lv0 + s : lv1 - 1 - s;
-    const int p0 = a.toplvl[lv], p1 = a.toplvl[lv + 1];
-    for (int p = p0 + threadIdx.x; p < p1; p += NT_TOP) {
-      const TopNode T = a.top[p];
-      const int cs = flag_case(T.flags);
-      const unsigned signs = flag_signs(T.flags);
-      const double *rec = a.rec + T.rec_off;
-      double aa, bb;
-      rec_ratios(cs, rec, 1, aa, bb);
-      const int rr = res_rows(cs);
-      if (UP) {
-        double mx[6], my[6], mp[6], res[6];
-        auto fetch = [&](int32_t ref, double (&m)[6]) {
-          if (ref >= 0) {
+__device__ __forceinline__ void top_fetch(const TopDfCtx &a, int64_t bead0, int32_t ref, double (&m)[6]) {
+  if (ref >= 0) {
 #pragma unroll
-            for (int r = 0; r < 6; r++) m[r] = __ldcg(&a.scratch[6 * (int64_t)ref + r]);
-          } else {
-            const int64_t gb = ~(int64_t)ref;
-            const int64_t row = (bead0 + a.perm[gb]) * 3;
-            m[0] = a.in[(row + 0) * K + col];
-            m[1] = a.in[(row + 1) * K + col];
-            m[2] = a.in[(row + 2) * K + col];
-            m[3] = m[4] = m[5] = 0.0;
-          }
-        };
-        fetch(T.x, mx);
-        fetch(T.y, my);
-        merge(cs, rec, 1, signs, aa, bb, mx, my, mp, res);
-        for (int r = 0; r < rr; r++) a.out[(sbase + T.res_q + r) * K + col] = res[r];
-        if (T.is_root) {
-          if (a.op == RQ_OP_QV)
-            for (int r = 0; r < 6; r++) a.out[(3 * bead0 + r) * K + col] = mp[r];
-        } else {
-          for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)T.self_slot + r] = mp[r];
-        }
-      } else {
-        double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
-        if (T.is_root) {
-          for (int r = 0; r < 6; r++) lp[r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * K + col] : 0.0;
-        } else {
-          for (int r = 0; r < 6; r++) lp[r] = __ldcg(&a.scratch[6 * (int64_t)T.self_slot + r]);
-        }
-        for (int r = 0; r < rr; r++) res[r] = a.in[(sbase + T.res_q + r) * K + col];
-        split(cs, rec, 1, signs, aa, bb, lp, res, lx, ly);
-        auto store = [&](int32_t ref, const double (&l)[6]) {
-          if (ref >= 0) {
-            for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)ref + r] = l[r];
-          } else {
-            const int64_t gb = ~(int64_t)ref;
-            const int64_t row = (bead0 + a.perm[gb]) * 3;
-            a.out[(row + 0) * K + col] = l[0];
-            a.out[(row + 1) * K + col] = l[1];
-            a.out[(row + 2) * K + col] = l[2];
-          }
-        };
-        store(T.x, lx);
-        store(T.y, ly);
-      }
-    }
-    __syncthreads();
+    for (int r = 0; r < 6; r++) m[r] = __ldcg(&a.scratch[6 * (int64_t)ref + r]);
+  } else {
+    const int64_t row = (bead0 + a.perm[~(int64_t)ref]) * 3;
+    m[0] = a.in[(row + 0) * a.k + a.col];
+    m[1] = a.in[(row + 1) * a.k + a.col];
+    m[2] = a.in[(row + 2) * a.k + a.col];
+    m[3] = m[4] = m[5] = 0.0;
   }
 }
 
+__device__ __forceinline__ void top_store(const TopDfCtx &a, int64_t bead0, int32_t ref, const double (&l)[6]) {
+  if (ref >= 0) {
+#pragma unroll
+    for (int r = 0; r < 6; r++) __stcg(&a.scratch[6 * (int64_t)ref + r], l[r]);
+  } else {
+    const int64_t row = (bead0 + a.perm[~(int64_t)ref]) * 3;
+    a.out[(row + 0) * a.k + a.col] = l[0];
+    a.out[(row + 1) * a.k + a.col] = l[1];
+    a.out[(row + 2) * a.k + a.col] = l[2];
+  }
+}
+
+__global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  int q = a.starts[i];
+  for (;;) {
+    const TopNode T = a.top[q];
+    const int j = T.body;
+    const int64_t bead0 = a.bead_off[j];
+    const int64_t sbase = spec_base(a.op, a.bead_off, j);
+    const int cs = flag_case(T.flags);
+    const double *rec = a.rec + T.rec_off;
+    double aa, bb, mx[6], my[6], mp[6], res[6];
+    rec_ratios(cs, rec, 1, aa, bb);
+    top_fetch(a, bead0, T.x, mx);
+    top_fetch(a, bead0, T.y, my);
+    merge(cs, rec, 1, flag_signs(T.flags), aa, bb, mx, my, mp, res);
+    for (int r = 0; r < res_rows(cs); r++) a.out[(sbase + T.res_q + r) * a.k + a.col] = res[r];
+    if (T.is_root) {
+      if (a.op == RQ_OP_QV)
+        for (int r = 0; r < 6; r++) a.out[(3 * bead0 + r) * a.k + a.col] = mp[r];
+      return;
+    }
+#pragma unroll
+    for (int r = 0; r < 6; r++) __stcg(&a.scratch[6 * (int64_t)T.self_slot + r], mp[r]);
+    __threadfence();
+    const int par = a.parent[q];
+    if (a.need[par] == 2) {
+      if (atomicAdd(&a.cnt[par], 1) == 0) return;  // first arrival: the sibling's thread continues
+      a.cnt[par] = 0;                                // second arrival: reset for the next application
+      __threadfence();
+    }
+    q = par;
+  }
+}
+
+__global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  constexpr int MAXP = 128;  // top-tree height <= max_depth + 1
+  int path[MAXP];
+  int d = 0;
+  path[0] = a.starts[i];
+  while (d + 1 < MAXP && a.parent[path[d]] >= 0) { path[d + 1] = a.parent[path[d]]; d++; }
+  const TopNode R0 = a.top[path[d]];
+  const int j = R0.body;
+  const int64_t bead0 = a.bead_off[j];
+  const int64_t sbase = spec_base(a.op, a.bead_off, j);
+  double lp[6];
+  for (int r = 0; r < 6; r++) lp[r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * a.k + a.col] : 0.0;
+  for (; d >= 0; d--) {
+    const TopNode T = a.top[path[d]];
+    const int cs = flag_case(T.flags);
+    const double *rec = a.rec + T.rec_off;
+    double aa, bb, res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
+    rec_ratios(cs, rec, 1, aa, bb);
+    for (int r = 0; r < res_rows(cs); r++) res[r] = a.in[(sbase + T.res_q + r) * a.k + a.col];
+    split(cs, rec, 1, flag_signs(T.flags), aa, bb, lp, res, lx, ly);
+    if (d == 0) {  // start node: both children leave the top tree
+      top_store(a, bead0, T.x, lx);
+      top_store(a, bead0, T.y, ly);
+      break;
+    }
+    const bool x_on_path = T.x >= 0 && T.x == a.top[path[d - 1]].self_slot;
+    // the off-path child: written here unless it is itself a top node (another path's)
+    if (x_on_path) {
+      if (T.ny <= a.S) top_store(a, bead0, T.y, ly);
+#pragma unroll
+      for (int r = 0; r < 6; r++) lp[r] = lx[r];
+    } else {
+      if (T.nx <= a.S) top_store(a, bead0, T.x, lx);
+#pragma unroll
+      for (int r = 0; r < 6; r++) lp[r] = ly[r];
+    }
+  }
+}
 
 // ---- staged top tree: one CTA per body, whole top tree in shared memory --------------
 
@@ -780,7 +820,6 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   const int64_t j0 = all ? 0 : range.j0, j1 = all ? p.m : range.j1;
   const int64_t c0 = all ? 0 : p.h_chunk_first[j0], c1 = all ? p.n_chunks : p.h_chunk_first[j1];
   const int64_t tb0 = all ? 0 : p.h_topblob_first[j0], tb1 = all ? p.n_topblob : p.h_topblob_first[j1];
-  const int64_t tg0 = all ? 0 : p.h_topbig_first[j0], tg1 = all ? p.n_topbig : p.h_topbig_first[j1];
   const int64_t sm0 = all ? 0 : p.h_small_first[j0], sm1 = all ? p.n_small : p.h_small_first[j1];
   ApplyCtx a{};
   a.chunks = p.chunks.as<ChunkDesc>() + c0;
@@ -803,12 +842,14 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 256 + 64, s));
     a.dbg = dbg.as<long long>();
   }
-  TopCtx t{};
-  t.tb_list = p.topbig.as<int32_t>() + tg0;
+  TopDfCtx t{};
+  const int64_t ts0 = all ? 0 : p.h_topstart_first[j0], ts1 = all ? p.n_top_start : p.h_topstart_first[j1];
+  t.starts = p.top_start.as<int32_t>() + ts0;
+  t.n = ts1 - ts0;
   t.top = p.top.as<TopNode>();
-  t.topbody = p.topbody.as<int32_t>();
-  t.topbody_lvl = p.topbody_lvl.as<int32_t>();
-  t.toplvl = p.toplvl.as<int32_t>();
+  t.parent = p.top_parent.as<int32_t>();
+  t.cnt = p.top_cnt.as<int32_t>();
+  t.need = p.top_need.as<int32_t>();
   t.perm = p.perm.as<int32_t>();
   t.bead_off = p.bead_off_d.as<int64_t>();
   t.rec = p.rec.as<double>();
@@ -817,6 +858,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.k = k;
   t.scratch = p.scratch.as<double>();
   t.op = op;
+  t.S = p.tile_leaves;
   Top2Ctx t2{};
   t2.blob = p.topblob.as<uint8_t>();
   t2.blob_off = p.topblob_off.as<int64_t>() + tb0;
@@ -835,15 +877,16 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     a.col = col;
     t.col = col;
     t2.col = col;
-    const bool do_chunks = (phases & 1u) && a.n_chunks > 0, do_top = (phases & 2u) && (tb1 > tb0 || tg1 > tg0);
+    const bool do_chunks = (phases & 1u) && a.n_chunks > 0, do_top = (phases & 2u) && (tb1 > tb0 || t.n > 0);
     auto top_pass = [&]() {
       if (tb1 > tb0) {
         if (up) k_top2<true><<<(unsigned)(tb1 - tb0), NT_TOP, top_smem, s>>>(t2);
         else k_top2<false><<<(unsigned)(tb1 - tb0), NT_TOP, top_smem, s>>>(t2);
       }
-      if (tg1 > tg0) {
-        if (up) k_top<true><<<(unsigned)(tg1 - tg0), NT_TOP, 0, s>>>(t);
-        else k_top<false><<<(unsigned)(tg1 - tg0), NT_TOP, 0, s>>>(t);
+      if (t.n > 0) {
+        const unsigned nb = (unsigned)((t.n + NT_TOP - 1) / NT_TOP);
+        if (up) k_top_df_up<<<nb, NT_TOP, 0, s>>>(t);
+        else k_top_df_down<<<nb, NT_TOP, 0, s>>>(t);
       }
     };
     if (up) {

@@ -122,6 +122,13 @@ struct Plan {
   DBuf topblob_body;               // int32 [n_topblob]: top-body index (into topbody)
   DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
   int64_t n_topbig = 0;
+  // dataflow sweep of those big top trees (k_top_df): parent links, arrival counters, start nodes
+  DBuf top_parent;                 // int32 [n_top]: parent top index, -1 for roots / staged bodies
+  mutable DBuf top_cnt;            // int32 [n_top]: upward arrival counters (self-resetting)
+  DBuf top_need;                   // int32 [n_top]: children inside the top tree (arrivals to wait for)
+  DBuf top_start;                  // int32 [n_top_start]: top nodes whose children are both below the top tree
+  int64_t n_top_start = 0;
+  std::vector<int64_t> h_topstart_first;  // [m+1]
   // host-side body -> work-list ranges (segmented / pipelined applications)
   std::vector<int64_t> h_chunk_first, h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each
   mutable DBuf scratch;            // double [6 * n_slots * kcap]

@@ -809,6 +809,23 @@ __global__ void k_top_levels(const uint64_t *keys_sorted, const int32_t *flag, c
 
 // ---- staged top-tree blobs ------------------------------------------------------------
 
+// top trees too large for shared memory (k_top_df): parent links and start nodes
+__global__ void k_top_slot2top(const TopNode *top, int64_t nt, int32_t *slot2top) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q < nt) slot2top[top[q].self_slot] = (int32_t)q;
+}
+__global__ void k_top_links(const TopNode *top, int64_t q0, int64_t q1, const int32_t *slot2top, int32_t *parent,
+                            int32_t *is_start, int32_t *need) {
+  int64_t q = q0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= q1) return;
+  const TopNode T = top[q];
+  const int32_t cx = T.x >= 0 ? slot2top[T.x] : -1, cy = T.y >= 0 ? slot2top[T.y] : -1;
+  if (cx >= 0) parent[cx] = (int32_t)q;
+  if (cy >= 0) parent[cy] = (int32_t)q;
+  is_start[q] = cx < 0 && cy < 0;
+  need[q] = (cx >= 0) + (cy >= 0);  // arrivals before the node can be merged
+}
+
 __global__ void k_top_slotmap(const TopNode *top, int64_t nt, const int32_t *topbody_idx, const int32_t *topbody_lvl,
                               const int32_t *toplvl, int32_t *slot_to_local, int32_t *nin, int64_t *recsz) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1033,7 +1050,7 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topbig};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topbig, &top_parent, &top_cnt, &top_need, &top_start, &mrhs_units, &mrhs_prog, &mrhs_scratch};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
@@ -1579,9 +1596,51 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           RQ_CUDA(cudaMemcpyAsync(p.topblob.p, all_blob.p, total, cudaMemcpyDeviceToDevice, s));
           RQ_CUDA(cudaStreamSynchronize(s));
         }
+        // dataflow top trees (bodies whose top tree does not fit shared memory)
+        p.top_parent.alloc(std::max<int64_t>(nt, 1) * 4);
+        p.top_cnt.alloc(std::max<int64_t>(nt, 1) * 4);
+        p.top_need.alloc(std::max<int64_t>(nt, 1) * 4);
+        RQ_CUDA(cudaMemsetAsync(p.top_need.p, 0, std::max<int64_t>(nt, 1) * 4, s));
+        RQ_CUDA(cudaMemsetAsync(p.top_parent.p, 0xff, std::max<int64_t>(nt, 1) * 4, s));
+        RQ_CUDA(cudaMemsetAsync(p.top_cnt.p, 0, std::max<int64_t>(nt, 1) * 4, s));
+        std::vector<int32_t> starts;
+        p.h_topstart_first.assign(m + 1, 0);
+        if (p.n_topbig) {
+          DBuf slot2top, is_start;
+          slot2top.alloc(std::max<int64_t>(p.n_slots, 1) * 4);
+          is_start.alloc(nt * 4);
+          RQ_CUDA(cudaMemsetAsync(slot2top.p, 0xff, std::max<int64_t>(p.n_slots, 1) * 4, s));
+          RQ_CUDA(cudaMemsetAsync(is_start.p, 0, nt * 4, s));
+          k_top_slot2top<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, slot2top.as<int32_t>());
+          for (auto bi : big_tb) {
+            const int64_t q0 = h_toplvl[h_lvl[bi]], q1 = h_toplvl[h_lvl[bi + 1]];
+            k_top_links<<<nblk(q1 - q0), NT, 0, s>>>(p.top.as<TopNode>(), q0, q1, slot2top.as<int32_t>(),
+                                                     p.top_parent.as<int32_t>(), is_start.as<int32_t>(),
+                                                     p.top_need.as<int32_t>());
+          }
+          std::vector<int32_t> hs(nt);
+          d2h(hs.data(), is_start.p, nt, s);
+          std::vector<int64_t> first_of_body(m + 1, -1);
+          for (auto bi : big_tb) {
+            const int64_t q0 = h_toplvl[h_lvl[bi]], q1 = h_toplvl[h_lvl[bi + 1]];
+            first_of_body[topbodies[bi]] = (int64_t)starts.size();
+            for (int64_t q = q0; q < q1; q++)
+              if (hs[q]) starts.push_back((int32_t)q);
+          }
+          first_of_body[m] = (int64_t)starts.size();
+          for (int64_t j = m - 1; j >= 0; j--)
+            if (first_of_body[j] < 0) first_of_body[j] = first_of_body[j + 1];
+          p.h_topstart_first.assign(first_of_body.begin(), first_of_body.end());
+        }
+        p.n_top_start = (int64_t)starts.size();
+        p.top_start.alloc(std::max<int64_t>(p.n_top_start, 1) * 4);
+        if (p.n_top_start)
+          RQ_CUDA(cudaMemcpyAsync(p.top_start.p, starts.data(), p.n_top_start * 4, cudaMemcpyHostToDevice, s));
+        RQ_CUDA(cudaStreamSynchronize(s));
       } else {
         p.h_topblob_first.assign(m + 1, 0);
         p.h_topbig_first.assign(m + 1, 0);
+        p.h_topstart_first.assign(m + 1, 0);
         p.toplvl.alloc(4);
         int32_t z = 0;
         RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.p, &z, 4, cudaMemcpyHostToDevice, s));
