@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -506,15 +508,18 @@ __host__ __device__ inline int64_t blob_bytes_of(int H, int nodes, int beads, in
   return head_bytes(tiles, H) + meta_bytes(nodes) + perm_bytes(beads) + rec * 8;  // rec is even: 16-byte multiple
 }
 
-// Greedy packing of a body's consecutive tiles into chunks (one thread per body).
-// pass 0: count chunks per body; pass 1: write descriptors.
-__global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, const int64_t *bead_off,
-                       int64_t m, ChunkLimits lim, int pass, const int64_t *chunk_base,
-                       const int32_t *big_scan, int64_t *n_chunks_body, ChunkDesc *chunks,
+// Greedy packing of consecutive tiles into chunks, one thread per packing segment
+// (a body's tile sequence cut every PACK_SEG tiles, so large bodies pack in parallel).
+// pass 0: count chunks per segment; pass 1: write descriptors.
+constexpr int PACK_SEG = 256;
+__global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, const int32_t *seg_body,
+                       const int64_t *bead_off, int64_t nseg, ChunkLimits lim, int pass, const int64_t *chunk_base,
+                       const int32_t *big_scan, int64_t *n_chunks_seg, ChunkDesc *chunks,
                        int64_t *chunk_of_tile, int32_t *res_local_of_tile) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  int64_t tb = body_tile_begin[j], te = body_tile_begin[j + 1];
+  const int64_t sg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (sg >= nseg) return;
+  const int64_t j = seg_body[sg];
+  int64_t tb = seg_tile_begin[sg], te = seg_tile_begin[sg + 1];
   int64_t nch = 0;
   bool open = false;
   int bead0 = 0, nodes = 0, H = 0, res = 0, ntiles = 0;
@@ -522,7 +527,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
   auto flush = [&]() {
     if (!open) return;
     if (pass == 1) {
-      ChunkDesc &d = chunks[chunk_base[j] + nch];
+      ChunkDesc &d = chunks[chunk_base[sg] + nch];
       d.blob_off = 0;
       d.n_nodes = nodes;
       d.n_levels = H;
@@ -554,7 +559,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
       if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res || ntiles + 1 > lim.max_tiles ||
           blob_bytes_of(H2, nodes2, beads2, rec2, ntiles + 1) > lim.max_bytes) {
         if (pass == 1) {
-          ChunkDesc &d = chunks[chunk_base[j] + nch];
+          ChunkDesc &d = chunks[chunk_base[sg] + nch];
           d.n_beads = last_stop - bead0;
           d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(d.n_beads));
           d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec, ntiles);
@@ -567,7 +572,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
       bead0 = T.start; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; tile0 = t;
     }
     if (pass == 1) {
-      chunk_of_tile[t] = chunk_base[j] + nch;
+      chunk_of_tile[t] = chunk_base[sg] + nch;
       res_local_of_tile[t] = res;
     }
     nodes += Tn;
@@ -578,13 +583,13 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *body_tile_begin, con
     last_stop = T.start + T.L;
   }
   if (open && pass == 1) {
-    ChunkDesc &d = chunks[chunk_base[j] + nch];
+    ChunkDesc &d = chunks[chunk_base[sg] + nch];
     d.n_beads = last_stop - bead0;
     d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(d.n_beads));
     d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec, ntiles);
   }
   flush();
-  if (pass == 0) n_chunks_body[j] = nch;
+  if (pass == 0) n_chunks_seg[sg] = nch;
 }
 
 __global__ void k_chunk_sizes(const ChunkDesc *chunks, int64_t nc, int64_t *bytes, int64_t *nodes,
@@ -1058,8 +1063,23 @@ int64_t Plan::device_bytes() const {
 
 void compute_body_centroids(Plan &p, cudaStream_t s);  // rq_z.cu
 
+struct SetupTimer {  // RQ_SETUP_TIMING=1: per-phase wall time of build_plan (synchronises the stream)
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit SetupTimer(cudaStream_t st) : on(getenv("RQ_SETUP_TIMING") != nullptr), s(st), t(std::chrono::steady_clock::now()) {}
+  void mark(const char *name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rq setup] %-12s %9.3f ms\n", name, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m, int max_depth,
                 bool host_input, cudaStream_t s) {
+  SetupTimer tm(s);
   if (m < 1) throw Error(RQ_ERR_VALUE, "need at least one body");
   if (offsets[0] != 0) throw Error(RQ_ERR_VALUE, "offsets[0] must be 0");
   for (int64_t j = 0; j < m; j++)
@@ -1122,6 +1142,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
   }
   compute_body_centroids(p, s);
 
+  tm.mark("bbox");
   // 2-3. keys + sort
   {
     DBuf keys, vals, keys2, vals2;
@@ -1157,6 +1178,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                                         ": split depth " + std::to_string(max_depth) +
                                         " exceeded without separating beads (near-coincident input)");
 
+    tm.mark("keys+sort");
     // 4. topology
     const int64_t n_internal = N - m;
     p.start.alloc(NN * 4);
@@ -1197,6 +1219,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     keys2.reset();
     vals2.reset();
 
+    tm.mark("topology");
     // sizes, residue and record offsets
     DBuf recsz, rr, rr_scan, node_body;
     recsz.alloc(NN * 8);
@@ -1221,6 +1244,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     rr.reset();
     rr_scan.reset();
 
+    tm.mark("offsets");
     // 5. factors
     p.t22.alloc(NN * 48);
     p.rec.alloc(std::max<int64_t>(p.rec_doubles, 1) * 8);
@@ -1254,6 +1278,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       RQ_CUDA(cudaStreamSynchronize(s));
     }
 
+    tm.mark("factors");
     // 6. apply layout
     const int S = p.tile_leaves;
     LayoutCtx lc{S,
@@ -1303,6 +1328,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       RQ_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, tb, marker.as<int32_t>(), tile_of.as<int32_t>(),
                                              MaxOp{}, NN, s));
     }
+    tm.mark("tiles");
     // per-body tile ranges (tiles are in global postorder = body order)
     std::vector<TileTmp> htiles(n_tiles_all);
     d2h(htiles.data(), tiles_tmp.p, n_tiles_all, s);
@@ -1318,10 +1344,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       for (int64_t i = 0; i < n_tiles_all; i++) big_scan[i + 1] = big_scan[i] + htiles[i].big;
     }
     p.n_tiles = big_scan[n_tiles_all];
-    DBuf d_body_tile_begin, d_big_scan;
-    d_body_tile_begin.alloc((m + 1) * 8);
+    DBuf d_big_scan;
     d_big_scan.alloc((n_tiles_all + 1) * 4);
-    RQ_CUDA(cudaMemcpyAsync(d_body_tile_begin.p, body_tile_begin.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
     RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
 
     ChunkLimits lim;
@@ -1333,23 +1357,41 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     lim.max_beads = 1024;
     lim.max_res = 3 * 1024;
     lim.max_tiles = 64;
-    DBuf nch_body, chunk_base;
-    nch_body.alloc(m * 8);
-    chunk_base.alloc((m + 1) * 8);
+    std::vector<int64_t> seg_tile_begin;
+    std::vector<int32_t> seg_body;
+    for (int64_t j = 0; j < m; j++)
+      for (int64_t t = body_tile_begin[j]; t < body_tile_begin[j + 1]; t += PACK_SEG) {
+        seg_tile_begin.push_back(t);
+        seg_body.push_back((int32_t)j);
+      }
+    const int64_t nseg = (int64_t)seg_body.size();
+    seg_tile_begin.push_back(n_tiles_all);
+    DBuf d_seg_tb, d_seg_body;
+    d_seg_tb.alloc((nseg + 1) * 8);
+    d_seg_body.alloc(std::max<int64_t>(nseg, 1) * 4);
+    RQ_CUDA(cudaMemcpyAsync(d_seg_tb.p, seg_tile_begin.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice, s));
+    if (nseg) RQ_CUDA(cudaMemcpyAsync(d_seg_body.p, seg_body.data(), nseg * 4, cudaMemcpyHostToDevice, s));
+    DBuf nch_seg, chunk_base;
+    nch_seg.alloc(std::max<int64_t>(nseg, 1) * 8);
+    chunk_base.alloc((nseg + 1) * 8);
     DBuf chunk_of_tile, res_local_of_tile;
     chunk_of_tile.alloc(n_tiles_all * 8);
     res_local_of_tile.alloc(n_tiles_all * 4);
-    k_pack<<<nblk(m, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_body_tile_begin.as<int64_t>(), boff, m,
-                                         lim, 0, nullptr, d_big_scan.as<int32_t>(), nch_body.as<int64_t>(),
-                                         nullptr, nullptr, nullptr);
-    exclusive_scan(nch_body.as<int64_t>(), chunk_base.as<int64_t>(), m, s);
-    p.n_chunks = d2h1<int64_t>(chunk_base.as<int64_t>() + m - 1, s) + d2h1<int64_t>(nch_body.as<int64_t>() + m - 1, s);
-    RQ_CUDA(cudaMemcpyAsync(chunk_base.as<int64_t>() + m, &p.n_chunks, 8, cudaMemcpyHostToDevice, s));
+    p.n_chunks = 0;
+    if (nseg) {
+      k_pack<<<nblk(nseg, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_seg_tb.as<int64_t>(), d_seg_body.as<int32_t>(),
+                                              boff, nseg, lim, 0, nullptr, d_big_scan.as<int32_t>(),
+                                              nch_seg.as<int64_t>(), nullptr, nullptr, nullptr);
+      exclusive_scan(nch_seg.as<int64_t>(), chunk_base.as<int64_t>(), nseg, s);
+      p.n_chunks = d2h1<int64_t>(chunk_base.as<int64_t>() + nseg - 1, s) + d2h1<int64_t>(nch_seg.as<int64_t>() + nseg - 1, s);
+    }
+    RQ_CUDA(cudaMemcpyAsync(chunk_base.as<int64_t>() + nseg, &p.n_chunks, 8, cudaMemcpyHostToDevice, s));
     p.chunks.alloc(std::max<int64_t>(p.n_chunks, 1) * sizeof(ChunkDesc));
-    k_pack<<<nblk(m, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_body_tile_begin.as<int64_t>(), boff, m,
-                                         lim, 1, chunk_base.as<int64_t>(), d_big_scan.as<int32_t>(),
-                                         nch_body.as<int64_t>(), p.chunks.as<ChunkDesc>(),
-                                         chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>());
+    if (nseg)
+      k_pack<<<nblk(nseg, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_seg_tb.as<int64_t>(), d_seg_body.as<int32_t>(),
+                                              boff, nseg, lim, 1, chunk_base.as<int64_t>(), d_big_scan.as<int32_t>(),
+                                              nch_seg.as<int64_t>(), p.chunks.as<ChunkDesc>(),
+                                              chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>());
     const int64_t nc = p.n_chunks;
     DBuf cbytes, cnodes, clevels, bytes_scan, node_scan, lvl_base;
     cbytes.alloc(nc * 8);
@@ -1449,6 +1491,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                                                     p.blob.as<uint8_t>());
     }
 
+    tm.mark("chunks+blob");
     // top tree
     {
       std::vector<int64_t> topbodies;
@@ -1647,6 +1690,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         RQ_CUDA(cudaStreamSynchronize(s));
       }
     }
+    tm.mark("top");
     // case counts
     {
       std::vector<uint8_t> hf(NN);
