@@ -171,7 +171,9 @@ int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
     }
     return tiles + tops + ((p.n_small && op <= 1) ? 1 : 0);
   }
-  int per_col = (p.n_chunks ? 1 : 0) + (p.n_topblob ? 1 : 0) + (p.n_topbig ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
+  int classes = 0;
+  for (int c = 0; c < 4; c++) classes += p.topclass_count[c] > 0;
+  int per_col = (p.n_chunks ? 1 : 0) + classes + (p.n_topbig ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
   return (int)(per_col * k);
 }
 

@@ -642,6 +642,8 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
 struct Top2Ctx {
   const uint8_t *blob;
   const int64_t *blob_off;
+  const uint8_t *cls;  // shared-memory class per staged body; a launch serves one class
+  int want;
   const int64_t *bead_off;
   const double *in;
   double *out;
@@ -655,6 +657,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
+  if (a.cls[blockIdx.x] != a.want) return;
   const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
   if (tid == 0) {
     const unsigned bytes = (unsigned)reinterpret_cast<const TopHdr *>(gB)->bytes;
@@ -862,16 +865,16 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   Top2Ctx t2{};
   t2.blob = p.topblob.as<uint8_t>();
   t2.blob_off = p.topblob_off.as<int64_t>() + tb0;
+  t2.cls = p.topblob_class.as<uint8_t>() + tb0;
   t2.bead_off = p.bead_off_d.as<int64_t>();
   t2.in = in;
   t2.out = out;
   t2.k = k;
   t2.scratch = p.scratch.as<double>();
   t2.op = op;
-  const size_t top_smem = (size_t)p.max_topblob_smem;
   if (p.n_topblob) {
     const void *f2 = up ? (const void *)k_top2<true> : (const void *)k_top2<false>;
-    RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)top_smem));
+    RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.max_topblob_smem));
   }
   for (int64_t col = 0; col < k; col++) {
     a.col = col;
@@ -879,9 +882,12 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     t2.col = col;
     const bool do_chunks = (phases & 1u) && a.n_chunks > 0, do_top = (phases & 2u) && (tb1 > tb0 || t.n > 0);
     auto top_pass = [&]() {
-      if (tb1 > tb0) {
-        if (up) k_top2<true><<<(unsigned)(tb1 - tb0), NT_TOP, top_smem, s>>>(t2);
-        else k_top2<false><<<(unsigned)(tb1 - tb0), NT_TOP, top_smem, s>>>(t2);
+      for (int c = 0; c < 4 && tb1 > tb0; c++) {
+        if (!p.topclass_count[c]) continue;
+        t2.want = c;
+        const size_t sm = (size_t)p.topclass_smem[c];
+        if (up) k_top2<true><<<(unsigned)(tb1 - tb0), NT_TOP, sm, s>>>(t2);
+        else k_top2<false><<<(unsigned)(tb1 - tb0), NT_TOP, sm, s>>>(t2);
       }
       if (t.n > 0) {
         const unsigned nb = (unsigned)((t.n + NT_TOP - 1) / NT_TOP);

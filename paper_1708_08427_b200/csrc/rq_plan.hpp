@@ -120,6 +120,8 @@ struct Plan {
   DBuf topblob;                    // bytes
   DBuf topblob_off;                // int64 [n_topblob]: blob byte offsets
   DBuf topblob_body;               // int32 [n_topblob]: top-body index (into topbody)
+  DBuf topblob_class;              // uint8 [n_topblob]: shared-memory class (one k_top2 launch per class)
+  int64_t topclass_smem[4] = {0, 0, 0, 0}, topclass_count[4] = {0, 0, 0, 0};
   DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
   int64_t n_topbig = 0;
   // dataflow sweep of those big top trees (k_top_df): parent links, arrival counters, start nodes

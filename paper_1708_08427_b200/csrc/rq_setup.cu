@@ -1055,7 +1055,7 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topbig, &top_parent, &top_cnt, &top_need, &top_start, &mrhs_units, &mrhs_prog, &mrhs_scratch};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_cnt, &top_need, &top_start, &mrhs_units, &mrhs_prog, &mrhs_scratch};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
@@ -1575,8 +1575,10 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         const int64_t smem_cap = 180 * 1024;
         std::vector<int64_t> blob_off(p.n_topbodies, -1), small_off;
         std::vector<int32_t> small_tb, big_tb;
+        std::vector<uint8_t> small_cls;
         int64_t total = 0;
         p.max_topblob_smem = 0;
+        for (int c = 0; c < 4; c++) p.topclass_smem[c] = p.topclass_count[c] = 0;
         for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
           const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
           const int nn = last - first, nl = h_lvl[bi + 1] - h_lvl[bi], ni = h_in[last] - h_in[first];
@@ -1588,6 +1590,11 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
             small_off.push_back(total);
             total += bytes;
             p.max_topblob_smem = std::max(p.max_topblob_smem, smem);
+            // shared-memory class: one launch per class, sized for the class maximum
+            const int c = smem <= 32 * 1024 ? 0 : (smem <= 64 * 1024 ? 1 : (smem <= 112 * 1024 ? 2 : 3));
+            small_cls.push_back((uint8_t)c);
+            p.topclass_smem[c] = std::max(p.topclass_smem[c], smem);
+            p.topclass_count[c]++;
           } else {
             blob_off[bi] = 0;  // unused
             big_tb.push_back((int32_t)bi);
@@ -1605,10 +1612,12 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.topblob.alloc(std::max<int64_t>(total, 16));
         p.topblob_off.alloc(std::max<int64_t>(p.n_topblob, 1) * 8);
         p.topblob_body.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
+        p.topblob_class.alloc(std::max<int64_t>(p.n_topblob, 1));
         p.topbig.alloc(std::max<int64_t>(p.n_topbig, 1) * 4);
         if (p.n_topblob) {
           RQ_CUDA(cudaMemcpyAsync(p.topblob_off.p, small_off.data(), p.n_topblob * 8, cudaMemcpyHostToDevice, s));
           RQ_CUDA(cudaMemcpyAsync(p.topblob_body.p, small_tb.data(), p.n_topblob * 4, cudaMemcpyHostToDevice, s));
+          RQ_CUDA(cudaMemcpyAsync(p.topblob_class.p, small_cls.data(), p.n_topblob, cudaMemcpyHostToDevice, s));
         }
         if (p.n_topbig) RQ_CUDA(cudaMemcpyAsync(p.topbig.p, big_tb.data(), p.n_topbig * 4, cudaMemcpyHostToDevice, s));
         DBuf d_blob_off;
