@@ -16,6 +16,7 @@
 // perm once per chunk.  No tensor cores: this is an HBM-bound sweep of tiny
 // orthogonal transforms (~0.3-0.6 flop/B).
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -246,32 +247,41 @@ __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
 // Stage the vector data a chunk needs, asynchronously (cp.async, one group):
 //   UP  : the chunk's bead forces, gathered through perm
 //   DOWN: the chunk's residue coefficients (contiguous per tile) + tile-root RV-sets
+__device__ __forceinline__ void cp_async8_u32(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+
 template <bool UP, int NT>
 __device__ __forceinline__ void prefetch_vectors(const ApplyCtx &a, const unsigned char *B, double *V, double *ROOT) {
   const ChunkView cv = view(B);
   const ChunkDesc &d = *cv.hdr;
   const int64_t bead0 = d.body_bead0;
   const int64_t K = a.k, col = a.col;
+  const uint32_t vb = smem_u32(V);
   if (UP) {
+    const double *inb = a.in + 3 * bead0 * K + col;
     for (int i = threadIdx.x; i < d.n_beads; i += NT) {
       const uint32_t pp = cv.PERM[i];
       if (!(pp & PERM_FOREIGN)) {
-        const int64_t row = (bead0 + pp) * 3;
-        cp_async8(V + 3 * i + 0, a.in + (row + 0) * K + col);
-        cp_async8(V + 3 * i + 1, a.in + (row + 1) * K + col);
-        cp_async8(V + 3 * i + 2, a.in + (row + 2) * K + col);
+        const double *src = inb + 3 * (int64_t)pp * K;
+        const uint32_t dst = vb + 24u * (uint32_t)i;
+        cp_async8_u32(dst, src);
+        cp_async8_u32(dst + 8, src + K);
+        cp_async8_u32(dst + 16, src + 2 * K);
       }
     }
   } else {
     const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? d.spec_full : d.spec_comp;
+    const uint32_t rb = smem_u32(ROOT);
     // one warp per tile (tiles are independent contiguous residue runs)
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int t = wid; t < d.n_tiles; t += NT / 32) {
       const TileDesc T = cv.tiles[t];
-      for (int r = lane; r < T.res_count; r += 32) cp_async8(V + T.res_local + r, a.in + (sbase + T.res_q + r) * K + col);
+      const double *src = a.in + (sbase + T.res_q + lane) * K + col;
+      for (int r = lane; r < T.res_count; r += 32, src += 32 * K) cp_async8_u32(vb + 8u * (uint32_t)(T.res_local + r), src);
       if (lane < 6) {
-        if (T.scratch >= 0) cp_async8(ROOT + 6 * t + lane, a.scratch + 6 * (int64_t)T.scratch + lane);
-        else if (a.op == RQ_OP_QTV) cp_async8(ROOT + 6 * t + lane, a.in + (3 * bead0 + lane) * K + col);
+        if (T.scratch >= 0) cp_async8_u32(rb + 8u * (6 * t + lane), a.scratch + 6 * (int64_t)T.scratch + lane);
+        else if (a.op == RQ_OP_QTV) cp_async8_u32(rb + 8u * (6 * t + lane), a.in + (3 * bead0 + lane) * K + col);
         else ROOT[6 * t + lane] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
       }
     }
@@ -298,6 +308,9 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[3 + NLS];  // 0-2 heads, 3.. level-record stages
   const int tid = threadIdx.x;
+  // TMA producer: lane 0 of the last warp, whose lanes carry the fewest nodes (case groups
+  // fill warps from warp 0), so the producer work stays off the slowest warp's path
+  constexpr int PROD = NT - 32;
   const long long t_kernel0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
   const SmemMap SM = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, UP);
 #define HEAD(i) (smem + (size_t)(i) * SM.head)
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     fence_mbar_init();
   }
   __syncthreads();
-  // thread 0 keeps the descriptors of chunks k+2 and k+3 in registers (loaded
+  // the producer keeps the descriptors of chunks k+2 and k+3 in registers (loaded
   // one iteration before use, so no global latency sits on the critical path)
   longlong2 dk2 = make_longlong2(0, 0), dk3 = make_longlong2(0, 0);  // {blob_off, off_rec | blob_bytes << 32}
   auto ldesc = [&](int64_t k) -> longlong2 {
@@ -321,7 +334,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     const ChunkDesc *d = &a.chunks[blockIdx.x + k * G];
     return make_longlong2(d->blob_off, (long long)(uint32_t)d->off_rec | ((long long)(uint32_t)d->blob_bytes << 32));
   };
-  if (tid == 0) {
+  if (tid == PROD) {
     for (int64_t k = 0; k < 3 && k < cnt; k++) {
       const longlong2 dd = ldesc(k);
       const unsigned hb = (unsigned)(dd.y & 0xffffffffll), rb = (unsigned)(dd.y >> 32) - hb;
@@ -360,10 +373,10 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       if (++pf_s == nH) { pf_s = 0; pf_k++; }
     }
   };
-  if (tid == 0) issue_levels(0, 0);
+  if (tid == PROD) issue_levels(0, 0);
   for (int64_t k = 0; k < cnt; k++) {
     const int st = (int)(k % 3), fb = (int)(k & 1);
-    if (tid == 0) {
+    if (tid == PROD) {
       if (k + 2 < cnt) {  // head of chunk k+2 (stage of chunk k-1, released at the end of k-1)
         const int s2 = (int)((k + 2) % 3);
         const unsigned hb = (unsigned)(dk2.y & 0xffffffffll);
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       const int h = UP ? s : H - 1 - s;
       const int ls = (int)(lctr % NLS);
       const LevelDesc L = cv.LV[h];
-      if (tid == 0) issue_levels(lctr, k + 1 < cnt ? k + 1 : k);
+      if (tid == PROD) issue_levels(lctr, k + 1 < cnt ? k + 1 : k);
       __shared__ unsigned long long t_max_node, t_step0, t_grp[4];
       if (RQ_TIMING && a.dbg && tid == 0) { t_max_node = 0; t_step0 = clock64(); t_grp[0] = t_grp[1] = t_grp[2] = t_grp[3] = 0; }
       if (RQ_TIMING && a.dbg) __syncthreads();
@@ -480,7 +493,9 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       const int wid = tid >> 5, lane = tid & 31;
       for (int t = wid; t < d.n_tiles; t += NT / 32) {  // residues (contiguous per tile) and tile-root info vectors
         const TileDesc T = cv.tiles[t];
-        for (int r = lane; r < T.res_count; r += 32) a.out[(sbase + T.res_q + r) * K + col] = RES[T.res_local + r];
+        double *o = a.out + (sbase + T.res_q + lane) * K + col;
+        const double *x = RES + T.res_local;
+        for (int r = lane; r < T.res_count; r += 32, o += 32 * K) *o = x[r];
         if (lane < 6) {
           const double v = M[6 * T.root_slot + lane];
           if (T.scratch >= 0) a.scratch[6 * (int64_t)T.scratch + lane] = v;
@@ -489,13 +504,14 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       }
     } else {
       const double *F = reinterpret_cast<const double *>(smem + SM.o_x);
+      double *ob = a.out + 3 * bead0 * K + col;
       for (int i = tid; i < d.n_beads; i += NT) {
         const uint32_t pp = cv.PERM[i];
         if (!(pp & PERM_FOREIGN)) {
-          const int64_t row = (bead0 + pp) * 3;
-          a.out[(row + 0) * K + col] = F[i * 3 + 0];
-          a.out[(row + 1) * K + col] = F[i * 3 + 1];
-          a.out[(row + 2) * K + col] = F[i * 3 + 2];
+          double *o = ob + 3 * (int64_t)pp * K;
+          o[0] = F[i * 3 + 0];
+          o[K] = F[i * 3 + 1];
+          o[2 * K] = F[i * 3 + 2];
         }
       }
     }
@@ -644,6 +660,7 @@ struct Top2Ctx {
   const int64_t *blob_off;
   const uint8_t *cls;  // shared-memory class per staged body; a launch serves one class
   int want;
+  long long *dbg;      // per-CTA phase timers, only with -DRQ_TIMING
   const int64_t *bead_off;
   const double *in;
   double *out;
@@ -658,6 +675,8 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   if (a.cls[blockIdx.x] != a.want) return;
+  const bool TM = RQ_TIMING && a.dbg && tid == 0;
+  const long long c0 = TM ? clock64() : 0;
   const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
   if (tid == 0) {
     const unsigned bytes = (unsigned)reinterpret_cast<const TopHdr *>(gB)->bytes;
@@ -668,6 +687,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
   }
   __syncthreads();
   mbar_wait(&bar, 0);
+  const long long c1 = TM ? clock64() : 0;
   const TopHdr h = *reinterpret_cast<const TopHdr *>(smem);
   const int32_t *LB = reinterpret_cast<const int32_t *>(smem + sizeof(TopHdr));
   const TopMeta *MD = reinterpret_cast<const TopMeta *>(smem + h.off_meta);
@@ -689,6 +709,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
       IN[i] = v;
     }
     __syncthreads();
+    const long long c2 = TM ? clock64() : 0;
     for (int lv = 0; lv < h.n_levels; lv++) {
       for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NT_TOP) {
         const TopMeta md = MD[q];
@@ -709,6 +730,12 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
         for (int r = 0; r < 6; r++) MT[6 * q + r] = mp[r];
       }
       __syncthreads();
+    }
+    if (TM) {
+      const long long c3 = clock64();
+      long long *d = a.dbg + 8 * blockIdx.x;
+      d[0] = c1 - c0; d[1] = c2 - c1; d[2] = c3 - c2; d[3] = h.n_levels; d[4] = h.n_nodes; d[5] = h.n_inputs;
+      d[6] = c0;
     }
   } else {
     for (int q = tid; q < h.n_nodes; q += NT_TOP) {
@@ -863,6 +890,13 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.op = op;
   t.S = p.tile_leaves;
   Top2Ctx t2{};
+  static const bool timing_top = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
+  DBuf dbg2;
+  if (timing_top && p.n_topblob) {
+    dbg2.alloc((size_t)p.n_topblob * 64);
+    RQ_CUDA(cudaMemsetAsync(dbg2.p, 0, (size_t)p.n_topblob * 64, s));
+    t2.dbg = dbg2.as<long long>() + 8 * tb0;
+  }
   t2.blob = p.topblob.as<uint8_t>();
   t2.blob_off = p.topblob_off.as<int64_t>() + tb0;
   t2.cls = p.topblob_class.as<uint8_t>() + tb0;
@@ -898,6 +932,21 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     if (up) {
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
       if (do_top) top_pass();
+      if (timing_top && do_top && p.n_topblob) {
+        std::vector<long long> h((size_t)p.n_topblob * 8);
+        RQ_CUDA(cudaMemcpyAsync(h.data(), dbg2.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        RQ_CUDA(cudaStreamSynchronize(s));
+        double acc[6] = {0};
+        long long t_min = LLONG_MAX, t_max = 0;
+        for (int64_t b = 0; b < p.n_topblob; b++) {
+          for (int i = 0; i < 6; i++) acc[i] += (double)h[8 * b + i];
+          t_min = std::min(t_min, h[8 * b + 6]);
+          t_max = std::max(t_max, h[8 * b + 6]);
+        }
+        const double nb = (double)p.n_topblob;
+        fprintf(stderr, "[rq timing] k_top2 UP per CTA: blob wait %.0f, inputs %.0f, levels %.0f (%.1f levels, %.0f nodes, %.0f inputs); CTA start spread %lld cycles\n",
+                acc[0] / nb, acc[1] / nb, acc[2] / nb, acc[3] / nb, acc[4] / nb, acc[5] / nb, t_max - t_min);
+      }
     } else {
       if (do_top) top_pass();
       if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
@@ -941,8 +990,11 @@ void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_
   const size_t bi = (size_t)rows(in_comp, p.m) * k * 8, bo = (size_t)rows(out_comp, p.m) * k * 8;
   if (p.stage_in.bytes < bi) p.stage_in.alloc(bi);
   if (p.stage_out.bytes < bo) p.stage_out.alloc(bo);
-  // segments of roughly equal bead count (at least ~2 MB of vector data each)
-  const int64_t seg_target = std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(bi / (2u << 20))));
+  // segments of roughly equal bead count (at least seg_mb MB of vector data each)
+  int64_t max_seg = 8, seg_mb = 2;
+  if (const char *e = getenv("RQ_HOST_SEGS")) max_seg = std::max(1, atoi(e));
+  if (const char *e = getenv("RQ_HOST_SEG_MB")) seg_mb = std::max(1, atoi(e));
+  const int64_t seg_target = std::max<int64_t>(1, std::min<int64_t>(max_seg, (int64_t)(bi / ((size_t)seg_mb << 20))));
   std::vector<int64_t> cuts{0};
   for (int64_t s = 1; s < seg_target; s++) {
     const int64_t target = p.bead_off[p.m] * s / seg_target;
