@@ -53,6 +53,27 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 32-bit shared-address forms (addresses computed once per kernel)
+__device__ __forceinline__ void mbar_expect_tx_u(uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_u(uint32_t dst, const void *src, unsigned bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u(uint32_t addr, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
   uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
@@ -313,6 +334,10 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   constexpr int PROD = NT - 32;
   const long long t_kernel0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
   const SmemMap SM = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, UP);
+  const uint32_t bar_u = smem_u32(bar), smem_u = smem_u32(smem);
+#define BAR(i) (bar_u + 8u * (uint32_t)(i))
+#define HEAD_U(i) (smem_u + (uint32_t)(i) * SM.head)
+#define LREC_U(i) (smem_u + SM.o_lrec + (uint32_t)(i) * SM.lrec)
 #define HEAD(i) (smem + (size_t)(i) * SM.head)
 #define LREC(i) reinterpret_cast<double *>(smem + SM.o_lrec + (size_t)(i) * SM.lrec)
 #define VBUF(i) reinterpret_cast<double *>(smem + SM.o_v + (size_t)(i) * SM.v)
@@ -340,24 +365,24 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       const unsigned hb = (unsigned)(dd.y & 0xffffffffll), rb = (unsigned)(dd.y >> 32) - hb;
       if (rb && k < a.pf_dist) prefetch_l2(a.blob + dd.x + hb, rb);
       if (k < 2) {
-        mbar_expect_tx(&bar[k], hb);
-        bulk_g2s(HEAD(k), a.blob + dd.x, hb, &bar[k]);
+        mbar_expect_tx_u(BAR(k), hb);
+        bulk_g2s_u(HEAD_U(k), a.blob + dd.x, hb, BAR(k));
       }
     }
     dk2 = ldesc(2);
     dk3 = ldesc(a.pf_dist);
   }
   unsigned phase = 0;  // parity bit per barrier
-  int64_t lctr = 0;    // level steps so far (selects the record stage)
-  mbar_wait(&bar[0], 0);
+  int lctr = 0;        // level steps so far (selects the record stage)
+  mbar_wait_u(BAR(0), 0);
   phase ^= 1u;
   prefetch_vectors<UP, NT>(a, HEAD(0), VBUF(0), ROOTBUF(0));
   // Level-record pipeline (thread 0): level steps are issued NLS-1 steps ahead of
   // the step being swept, across chunk boundaries as far as heads are resident.
   int64_t pf_k = 0;  // chunk iteration of the next level step to issue
   int pf_s = 0;      // its level step within that chunk
-  int64_t pf_n = 0;  // level steps issued so far
-  auto issue_levels = [&](int64_t g, int64_t k_avail) {
+  int pf_n = 0;      // level steps issued so far
+  auto issue_levels = [&](int g, int64_t k_avail) {
     // issue while fewer than NLS steps are in flight beyond the current one
     while (pf_n < g + NLS && pf_k < cnt && pf_k <= k_avail) {
       const ChunkView nv = view(HEAD(pf_k % 3));
@@ -366,9 +391,9 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       const LevelDesc L2 = nv.LV[UP ? pf_s : nH - 1 - pf_s];
       const double *g2 = reinterpret_cast<const double *>(a.blob + nd.blob_off + nd.off_rec) + L2.recG;
       const unsigned bytes = 8u * (unsigned)level_rec_doubles(L2);
-      const int st = (int)(pf_n % NLS);
-      mbar_expect_tx(&bar[3 + st], bytes);
-      bulk_g2s(LREC(st), g2, bytes, &bar[3 + st]);
+      const int st = pf_n & (NLS - 1);
+      mbar_expect_tx_u(BAR(3 + st), bytes);
+      bulk_g2s_u(LREC_U(st), g2, bytes, BAR(3 + st));
       pf_n++;
       if (++pf_s == nH) { pf_s = 0; pf_k++; }
     }
@@ -381,8 +406,8 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
         const int s2 = (int)((k + 2) % 3);
         const unsigned hb = (unsigned)(dk2.y & 0xffffffffll);
         // WAR on smem (generic reads -> TMA write) is ordered by the barrier; no proxy fence needed
-        mbar_expect_tx(&bar[s2], hb);
-        bulk_g2s(HEAD(s2), a.blob + dk2.x, hb, &bar[s2]);
+        mbar_expect_tx_u(BAR(s2), hb);
+        bulk_g2s_u(HEAD_U(s2), a.blob + dk2.x, hb, BAR(s2));
       }
       if (k + a.pf_dist < cnt) {  // records of chunk k+pf_dist into L2
         const unsigned hb = (unsigned)(dk3.y & 0xffffffffll), rb = (unsigned)(dk3.y >> 32) - hb;
@@ -394,7 +419,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     long long tc0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (k + 1 < cnt) {
       const int s1 = (int)((k + 1) % 3);
-      mbar_wait(&bar[s1], (phase >> s1) & 1u);
+      mbar_wait_u(BAR(s1), (phase >> s1) & 1u);
       phase ^= 1u << s1;
       prefetch_vectors<UP, NT>(a, HEAD(s1), VBUF(fb ^ 1), ROOTBUF(fb ^ 1));
       cp_async_wait<1>();
@@ -416,14 +441,14 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     }
     for (int s = 0; s < H; s++, lctr++) {
       const int h = UP ? s : H - 1 - s;
-      const int ls = (int)(lctr % NLS);
+      const int ls = lctr & (NLS - 1);
       const LevelDesc L = cv.LV[h];
       if (tid == PROD) issue_levels(lctr, k + 1 < cnt ? k + 1 : k);
       __shared__ unsigned long long t_max_node, t_step0, t_grp[4];
       if (RQ_TIMING && a.dbg && tid == 0) { t_max_node = 0; t_step0 = clock64(); t_grp[0] = t_grp[1] = t_grp[2] = t_grp[3] = 0; }
       if (RQ_TIMING && a.dbg) __syncthreads();
       long long tw0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
-      mbar_wait(&bar[3 + ls], (phase >> (3 + ls)) & 1u);
+      mbar_wait_u(BAR(3 + ls), (phase >> (3 + ls)) & 1u);
       phase ^= 1u << (3 + ls);
       long long tw1 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
       const long long tn0 = (RQ_TIMING && a.dbg) ? clock64() : 0;
@@ -519,6 +544,9 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     (void)to0;
   }
   if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 7] = clock64() - t_kernel0;
+#undef BAR
+#undef HEAD_U
+#undef LREC_U
 #undef HEAD
 #undef LREC
 #undef VBUF
