@@ -272,12 +272,12 @@ __device__ __forceinline__ void cp_async8_u32(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
 
-template <bool UP, int NT>
+template <bool UP, int NT, bool K1>
 __device__ __forceinline__ void prefetch_vectors(const ApplyCtx &a, const unsigned char *B, double *V, double *ROOT) {
   const ChunkView cv = view(B);
   const ChunkDesc &d = *cv.hdr;
   const int64_t bead0 = d.body_bead0;
-  const int64_t K = a.k, col = a.col;
+  const int64_t K = K1 ? 1 : a.k, col = K1 ? 0 : a.col;  // K1: single right-hand side
   const uint32_t vb = smem_u32(V);
   if (UP) {
     const double *inb = a.in + 3 * bead0 * K + col;
@@ -320,7 +320,7 @@ __device__ __forceinline__ int level_rec_doubles(const LevelDesc &L) {
 //   * chunk k+1: vectors staged with cp.async
 //   * chunk k  : swept level by level; the records of level h+1 are TMA-copied
 //                (from L2) into the second record stage while level h runs.
-template <bool UP, int NT>
+template <bool UP, int NT, bool K1>
 #ifdef RQ_MIN_BLOCKS
 __global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
 #else
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
 #define LREC(i) reinterpret_cast<double *>(smem + SM.o_lrec + (size_t)(i) * SM.lrec)
 #define VBUF(i) reinterpret_cast<double *>(smem + SM.o_v + (size_t)(i) * SM.v)
 #define ROOTBUF(i) reinterpret_cast<double *>(smem + SM.o_root + (size_t)(i) * SM.root)
-  const int64_t K = a.k, col = a.col;
+  const int64_t K = K1 ? 1 : a.k, col = K1 ? 0 : a.col;
   const int64_t G = gridDim.x;
   const int64_t cnt = a.n_chunks > blockIdx.x ? (a.n_chunks - blockIdx.x + G - 1) / G : 0;
   if (cnt == 0) return;
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   int lctr = 0;        // level steps so far (selects the record stage)
   mbar_wait_u(BAR(0), 0);
   phase ^= 1u;
-  prefetch_vectors<UP, NT>(a, HEAD(0), VBUF(0), ROOTBUF(0));
+  prefetch_vectors<UP, NT, K1>(a, HEAD(0), VBUF(0), ROOTBUF(0));
   // Level-record pipeline (thread 0): level steps are issued NLS-1 steps ahead of
   // the step being swept, across chunk boundaries as far as heads are resident.
   int64_t pf_k = 0;  // chunk iteration of the next level step to issue
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       const int s1 = (int)((k + 1) % 3);
       mbar_wait_u(BAR(s1), (phase >> s1) & 1u);
       phase ^= 1u << s1;
-      prefetch_vectors<UP, NT>(a, HEAD(s1), VBUF(fb ^ 1), ROOTBUF(fb ^ 1));
+      prefetch_vectors<UP, NT, K1>(a, HEAD(s1), VBUF(fb ^ 1), ROOTBUF(fb ^ 1));
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -824,12 +824,13 @@ struct KernelCfg {
 };
 
 template <bool UP>
-void (*chunk_fn(int nt))(ApplyCtx) {
+void (*chunk_fn(int nt, bool k1))(ApplyCtx) {
+  if (k1 && nt == 128) return k_chunk<UP, 128, true>;
   switch (nt) {
-    case 32: return k_chunk<UP, 32>;
-    case 64: return k_chunk<UP, 64>;
-    case 256: return k_chunk<UP, 256>;
-    default: return k_chunk<UP, 128>;
+    case 32: return k_chunk<UP, 32, false>;
+    case 64: return k_chunk<UP, 64, false>;
+    case 256: return k_chunk<UP, 256, false>;
+    default: return k_chunk<UP, 128, false>;
   }
 }
 
@@ -846,7 +847,7 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   KernelCfg cfg;
   cfg.threads = p.chunk_threads;
   cfg.smem = smem_total(smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, up));
-  cfg.fn = up ? chunk_fn<true>(cfg.threads) : chunk_fn<false>(cfg.threads);
+  cfg.fn = up ? chunk_fn<true>(cfg.threads, a.k == 1) : chunk_fn<false>(cfg.threads, a.k == 1);
   RQ_CUDA(cudaFuncSetAttribute((const void *)cfg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   int occ = 0;
   RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)cfg.fn, cfg.threads, cfg.smem));
