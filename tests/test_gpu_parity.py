@@ -248,6 +248,29 @@ def test_properties_large(rq):
     assert np.abs(op.apply("qtilde_v", op.ztu(u))).max() < 1e-12 * np.abs(op.ztu(u)).max() * 10
 
 
+def test_properties_full_config2(rq):
+    """BASELINE config 2 at full size (1000 x 4096 beads) through size-independent
+    properties on device tensors: Q~ Q~^T = I, Q Q^T = I (round trips), isometry and
+    Z Q~^T = 0 (the complement property), all at the 1e-12 level."""
+    import torch
+
+    from paper_1708_08427_b200.workloads import make_config
+
+    pos, off = make_config(2, seed=1000)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    N, m = int(off[-1]), len(off) - 1
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    g = torch.randn(3 * N - 6 * m, generator=gen, device="cuda", dtype=torch.float64)
+    v = torch.randn(3 * N, generator=gen, device="cuda", dtype=torch.float64)
+    w = op.apply("qtilde_tv", g)
+    assert float((op.apply("qtilde_v", w) - g).abs().max()) < 1e-12 * float(g.abs().max())
+    qv = op.apply("qv", v)
+    assert abs(float(qv.norm()) - float(v.norm())) < 1e-12 * float(v.norm())
+    assert float((op.apply("qtv", qv) - v).abs().max()) < 1e-12 * float(v.abs().max())
+    zf = op.zf(w)
+    assert float(zf.abs().max()) < 1e-11 * float(g.norm()) / np.sqrt(m)
+
+
 def test_batch_bitwise_equals_per_body(rq):
     """multi-body blocks equal independent per-body runs bit-exactly."""
     from paper_1708_08427_b200.workloads import ellipsoid_batch
