@@ -204,11 +204,18 @@ def main():
         wop.apply("qtilde_v", wv)
         wop.apply("qtilde_tv", np.zeros((3 * int(wo[-1]) - 6 * (len(wo) - 1), wk)))
     del wop
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    op = rq.MultiBodyOperator(model)
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
+    # setup timed twice (the plan is rebuilt; the first build also pays one-time driver costs
+    # on a fresh box, e.g. lazy kernel loading); the steady-state second build is reported
+    setup_times = []
+    for rep in range(2):
+        if rep:
+            del op
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op = rq.MultiBodyOperator(model)
+        torch.cuda.synchronize()
+        setup_times.append(time.perf_counter() - t0)
+    setup_s = setup_times[-1]
     info = op.plan.info()
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -351,7 +358,8 @@ def main():
                          "share_of_step": share},
             "kernels_ms": {f"{a}:{b}": v_ for (a, b), v_ in kern.items()},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": ck, "gpu_launches": int(launches),
-            "setup": {"seconds": setup_s, "beads_per_s": N / setup_s},
+            "setup": {"seconds": setup_s, "beads_per_s": N / setup_s, "first_build_seconds": setup_times[0],
+                      "from": "host positions (pageable numpy), tree + factors + apply layout, device-synchronised"},
             "plan": {kk: info[kk] for kk in ("n_chunks", "n_top", "blob_bytes", "max_chunk_bytes", "n_case",
                                              "device_bytes", "tile_leaves", "chunk_smem", "top_staged",
                                              "top_global")},
