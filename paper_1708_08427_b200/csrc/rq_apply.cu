@@ -28,7 +28,7 @@
 namespace rq {
 namespace {
 
-constexpr int NT_TOP = 128;
+constexpr int NT_TOP = 128;  // dataflow top kernels
 constexpr int NLS = 2;  // level-record stages in shared memory (records issued NLS-1 steps ahead)
 
 // ---- PTX helpers: mbarrier + bulk copy ------------------------------------------
@@ -697,8 +697,27 @@ struct Top2Ctx {
   int op;
 };
 
-template <bool UP>
-__global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
+// a node record (global memory, 16-byte aligned) into registers
+__device__ __forceinline__ void ldg_rec(int cs, const double *g, double (&R)[rec_size(GENERAL)]) {
+  const double2 *g2 = reinterpret_cast<const double2 *>(g);
+  const int n2 = rec_size(cs) / 2;
+#pragma unroll
+  for (int i = 0; i < rec_size(GENERAL) / 2; i++) {
+    if (i < n2) {
+      const double2 v = __ldg(g2 + i);
+      R[2 * i] = v.x;
+      R[2 * i + 1] = v.y;
+    } else {
+      R[2 * i] = 0.0;
+      R[2 * i + 1] = 0.0;
+    }
+  }
+}
+
+// NTT threads per top tree: one warp for the small shared-memory classes (top trees
+// of config-2 bodies: ~7 nodes per level), 128 for the large ones
+template <bool UP, int NTT>
+__global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
@@ -706,12 +725,17 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
   const bool TM = RQ_TIMING && a.dbg && tid == 0;
   const long long c0 = TM ? clock64() : 0;
   const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
+  // stage the header part (levels, meta, inputs) with one TMA copy; the records stay
+  // in global memory (prefetched into L2 here) and are read per node, so the CTA
+  // needs little shared memory and many top trees are swept concurrently per SM
   if (tid == 0) {
-    const unsigned bytes = (unsigned)reinterpret_cast<const TopHdr *>(gB)->bytes;
+    const TopHdr *gh = reinterpret_cast<const TopHdr *>(gB);
+    const unsigned hbytes = (unsigned)gh->off_rec, rbytes = (unsigned)gh->bytes - hbytes;
+    if (rbytes) prefetch_l2(gB + hbytes, rbytes);
     mbar_init(&bar, 1);
     fence_mbar_init();
-    mbar_expect_tx(&bar, bytes);
-    bulk_g2s(smem, gB, bytes, &bar);
+    mbar_expect_tx(&bar, hbytes);
+    bulk_g2s(smem, gB, hbytes, &bar);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
@@ -720,29 +744,43 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
   const int32_t *LB = reinterpret_cast<const int32_t *>(smem + sizeof(TopHdr));
   const TopMeta *MD = reinterpret_cast<const TopMeta *>(smem + h.off_meta);
   const int32_t *INREF = reinterpret_cast<const int32_t *>(smem + h.off_in);
-  const double *REC = reinterpret_cast<const double *>(smem + h.off_rec);
-  double *IN = reinterpret_cast<double *>(smem + (h.bytes + 127) / 128 * 128);
-  double *MT = IN + 6 * h.n_inputs;
-  double *RT = MT + 6 * h.n_nodes;
+  const double *REC = reinterpret_cast<const double *>(gB + h.off_rec);
+  // X | MT: X holds the input info vectors (UP) or the staged residues (DOWN)
+  double *IN = reinterpret_cast<double *>(smem + (h.off_rec + 127) / 128 * 128);
+  double *RT = IN;
+  double *MT = IN + 6 * max(h.n_inputs, h.n_nodes);
   const int64_t K = a.k, col = a.col;
   const int64_t bead0 = a.bead_off[h.body];
   const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)h.body;
   if (UP) {
-    for (int i = tid; i < 6 * h.n_inputs; i += NT_TOP) {
-      const int q = i / 6, r = i % 6;
-      const int32_t ref = INREF[q];
-      double v;
-      if (ref >= 0) v = __ldcg(&a.scratch[6 * (int64_t)ref + r]);
-      else v = r < 3 ? a.in[((bead0 + ~(int64_t)ref) * 3 + r) * K + col] : 0.0;
-      IN[i] = v;
+    // 4 independent loads in flight per thread (tile-root vectors from L2)
+    const int n_in = 6 * h.n_inputs;
+    for (int i0 = tid; i0 < n_in; i0 += 4 * NTT) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int i = i0 + u * NTT;
+        v[u] = 0.0;
+        if (i < n_in) {
+          const int q = i / 6, r = i % 6;
+          const int32_t ref = INREF[q];
+          if (ref >= 0) v[u] = __ldcg(&a.scratch[6 * (int64_t)ref + r]);
+          else if (r < 3) v[u] = a.in[((bead0 + ~(int64_t)ref) * 3 + r) * K + col];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (i0 + u * NTT < n_in) IN[i0 + u * NTT] = v[u];
     }
     __syncthreads();
     const long long c2 = TM ? clock64() : 0;
     for (int lv = 0; lv < h.n_levels; lv++) {
-      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NT_TOP) {
+      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NTT) {
         const TopMeta md = MD[q];
         const int cs = flag_case(md.flags);
-        const double *rec = REC + md.rec;
+        double recv[rec_size(GENERAL)];
+        ldg_rec(cs, REC + md.rec, recv);
+        const double *rec = recv;
         double mx[6], my[6], mp[6], res[6], aa, bb;
         const double *px = md.x >= 0 ? MT + 6 * md.x : IN + 6 * ~(int)md.x;
         const double *py = md.y >= 0 ? MT + 6 * md.y : IN + 6 * ~(int)md.y;
@@ -766,7 +804,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
       d[6] = c0;
     }
   } else {
-    for (int q = tid; q < h.n_nodes; q += NT_TOP) {
+    for (int q = tid; q < h.n_nodes; q += NTT) {
       const TopMeta md = MD[q];
       const int rr = res_rows(flag_case(md.flags));
       for (int r = 0; r < rr; r++) RT[6 * q + r] = a.in[(sbase + md.res_q + r) * K + col];
@@ -775,10 +813,12 @@ __global__ void __launch_bounds__(NT_TOP) k_top2(Top2Ctx a) {
     }
     __syncthreads();
     for (int lv = h.n_levels - 1; lv >= 0; lv--) {
-      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NT_TOP) {
+      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NTT) {
         const TopMeta md = MD[q];
         const int cs = flag_case(md.flags);
-        const double *rec = REC + md.rec;
+        double recv[rec_size(GENERAL)];
+        ldg_rec(cs, REC + md.rec, recv);
+        const double *rec = recv;
         double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6], aa, bb;
 #pragma unroll
         for (int r = 0; r < 6; r++) lp[r] = MT[6 * q + r];
@@ -936,8 +976,9 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t2.scratch = p.scratch.as<double>();
   t2.op = op;
   if (p.n_topblob) {
-    const void *f2 = up ? (const void *)k_top2<true> : (const void *)k_top2<false>;
-    RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.max_topblob_smem));
+    for (const void *f2 : {(const void *)k_top2<true, 32>, (const void *)k_top2<false, 32>,
+                           (const void *)k_top2<true, 128>, (const void *)k_top2<false, 128>})
+      RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.max_topblob_smem));
   }
   for (int64_t col = 0; col < k; col++) {
     a.col = col;
@@ -949,8 +990,13 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
         if (!p.topclass_count[c]) continue;
         t2.want = c;
         const size_t sm = (size_t)p.topclass_smem[c];
-        if (up) k_top2<true><<<(unsigned)(tb1 - tb0), NT_TOP, sm, s>>>(t2);
-        else k_top2<false><<<(unsigned)(tb1 - tb0), NT_TOP, sm, s>>>(t2);
+        if (c < 2) {
+          if (up) k_top2<true, 32><<<(unsigned)(tb1 - tb0), 32, sm, s>>>(t2);
+          else k_top2<false, 32><<<(unsigned)(tb1 - tb0), 32, sm, s>>>(t2);
+        } else {
+          if (up) k_top2<true, 128><<<(unsigned)(tb1 - tb0), 128, sm, s>>>(t2);
+          else k_top2<false, 128><<<(unsigned)(tb1 - tb0), 128, sm, s>>>(t2);
+        }
       }
       if (t.n > 0) {
         const unsigned nb = (unsigned)((t.n + NT_TOP - 1) / NT_TOP);

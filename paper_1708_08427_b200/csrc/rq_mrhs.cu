@@ -520,7 +520,7 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
   if (p.mrhs_built) return;
   const int64_t NN = p.NN, m = p.m;
   BuildCtx c;
-  c.S = p.tile_leaves;
+  c.S = p.mrhs_tile;  // unit size of the column-parallel programs (independent of the chunk tiles)
   c.NN = NN;
   c.m = m;
   c.bead_off = p.bead_off_d.as<int64_t>();

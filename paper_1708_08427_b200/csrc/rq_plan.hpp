@@ -72,7 +72,7 @@ struct Plan {
   int device = 0;
   int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
   int max_depth = 96;
-  int tile_leaves = 64;            // S
+  int tile_leaves = 48;            // S (measured best for config 2 with 36 KiB chunks)
   int chunk_threads = 128;         // threads per chunk CTA
   int64_t max_blob = 0;            // largest chunk blob (bytes)
   int64_t max_head_bytes = 0;      // largest chunk head (everything before the records)
@@ -149,6 +149,7 @@ struct Plan {
   mutable std::mutex host_mu;
   // multi-RHS unit programs (rq_mrhs.cu), built on the first k >= mrhs_min application
   int mrhs_min = 8;
+  int mrhs_tile = 64;              // leaves per multi-RHS tile unit
   mutable std::mutex mrhs_mu;
   mutable bool mrhs_built = false;
   mutable int64_t mrhs_entries = 0, n_tile_units = 0, n_top_units = 0;

@@ -1094,6 +1094,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
   if (const char *e = getenv("RQ_TILE_LEAVES")) p.tile_leaves = std::min(1024, std::max(2, atoi(e)));
   if (const char *e = getenv("RQ_CHUNK_THREADS")) p.chunk_threads = atoi(e);
   if (const char *e = getenv("RQ_MRHS_MIN")) p.mrhs_min = std::max(2, atoi(e));
+  if (const char *e = getenv("RQ_MRHS_TILE")) p.mrhs_tile = std::max(2, std::min(4096, atoi(e)));
   p.m = m;
   p.N = N;
   p.NN = 2 * N - m;
@@ -1349,7 +1350,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
 
     ChunkLimits lim;
-    lim.max_bytes = 32 * 1024;
+    lim.max_bytes = 36 * 1024;
     if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
     // a single worst-case tile (all GENERAL nodes) must fit a chunk
     lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
@@ -1583,7 +1584,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
           const int nn = last - first, nl = h_lvl[bi + 1] - h_lvl[bi], ni = h_in[last] - h_in[first];
           const int64_t bytes = topblob_bytes(nn, nl, ni, h_rec[last] - h_rec[first]);
-          const int64_t smem = (bytes + 127) / 128 * 128 + 48 * (int64_t)(ni + 2 * nn) + 128;
+          // staged: header, levels, meta and inputs (records are read from L2)
+          const int64_t hdr_bytes = bytes - 8 * (h_rec[last] - h_rec[first]);
+          const int64_t smem = (hdr_bytes + 127) / 128 * 128 + 48 * (int64_t)(std::max(ni, nn) + nn) + 128;
           if (smem <= smem_cap && nn < 32000 && ni < 32000) {
             blob_off[bi] = total;
             small_tb.push_back((int32_t)bi);
