@@ -361,7 +361,7 @@ def main():
             "setup": {"seconds": setup_s, "beads_per_s": N / setup_s, "first_build_seconds": setup_times[0],
                       "from": "host positions (pageable numpy), tree + factors + apply layout, device-synchronised"},
             "plan": {kk: info[kk] for kk in ("n_chunks", "n_top", "blob_bytes", "max_chunk_bytes", "n_case",
-                                             "device_bytes", "tile_leaves", "chunk_smem", "top_staged",
+                                             "device_bytes", "tile_leaves", "chunk_smem", "top_staged", "chunk_ctas_per_sm", "chunk_smem_bytes",
                                              "top_global")},
             "bytes_per_bead_per_op": chunk_bytes / N,
         }

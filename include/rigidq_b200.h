@@ -75,6 +75,8 @@ typedef struct rq_plan_info {
   int64_t mrhs_min_k;      /* k at and above which the column-parallel (multi-RHS) kernels run */
   int64_t mrhs_units[2];   /* multi-RHS unit programs: tiles, top trees (0 until the first k >= mrhs_min_k apply) */
   int64_t mrhs_bytes[2];   /* program bytes read per column group: tile units, top units */
+  int64_t chunk_ctas_per_sm[2]; /* resident single-RHS chunk CTAs per SM: downward, upward sweep */
+  int64_t chunk_smem_bytes[2];  /* their dynamic shared memory per CTA */
 } rq_plan_info;
 
 /* Last error message of the calling thread ("" if none). */

@@ -44,7 +44,8 @@ class PlanInfo(C.Structure):
                 ("record_doubles", C.c_int64), ("full_len", C.c_int64), ("comp_len", C.c_int64),
                 ("max_chunk_bytes", C.c_int64), ("n_case", C.c_int64 * 4), ("device_bytes", C.c_int64),
                 ("chunk_smem", C.c_int64 * 6), ("top_staged", C.c_int64), ("top_global", C.c_int64),
-                ("mrhs_min_k", C.c_int64), ("mrhs_units", C.c_int64 * 2), ("mrhs_bytes", C.c_int64 * 2)]
+                ("mrhs_min_k", C.c_int64), ("mrhs_units", C.c_int64 * 2), ("mrhs_bytes", C.c_int64 * 2),
+                ("chunk_ctas_per_sm", C.c_int64 * 2), ("chunk_smem_bytes", C.c_int64 * 2)]
 
 
 SIGNATURES = [

@@ -139,6 +139,13 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
     info->mrhs_units[1] = p.n_top_units;
     info->mrhs_bytes[0] = p.mrhs_tile_bytes;
     info->mrhs_bytes[1] = p.mrhs_top_bytes;
+    int ctas[2] = {0, 0};
+    int64_t sm[2] = {0, 0};
+    if (p.n_chunks) rq::chunk_occupancy(p, ctas, sm);
+    for (int u = 0; u < 2; u++) {
+      info->chunk_ctas_per_sm[u] = ctas[u];
+      info->chunk_smem_bytes[u] = sm[u];
+    }
   })
 }
 

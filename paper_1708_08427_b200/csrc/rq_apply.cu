@@ -232,7 +232,7 @@ __host__ __device__ __forceinline__ SmemMap smem_map(int head_bytes, int lrec_by
   m.lrec = (uint32_t)al128(lrec_bytes);
   m.v = (uint32_t)al128(8 * (size_t)(up ? 3 * max_beads : max_res));
   m.x = (uint32_t)al128(8 * (size_t)(up ? max_res : 3 * max_beads));
-  m.root = (uint32_t)al128(48 * (size_t)max_tiles);
+  m.root = up ? 0u : (uint32_t)al128(48 * (size_t)max_tiles);  // tile-root RV-sets (DOWN only)
   m.o_lrec = 3 * m.head;
   m.o_v = m.o_lrec + NLS * m.lrec;
   m.o_m = m.o_v + 2 * m.v;
@@ -898,6 +898,19 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
 }
 
 }  // namespace
+
+void chunk_occupancy(const Plan &p, int ctas[2], int64_t smem[2]) {
+  for (int u = 0; u < 2; u++) {
+    ApplyCtx a{};
+    a.k = 1;
+    a.n_chunks = p.n_chunks;
+    KernelCfg cfg = chunk_cfg(p, u == 1, a);
+    smem[u] = (int64_t)cfg.smem;
+    int sms = 0;
+    RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+    ctas[u] = sms ? (int)((cfg.grid + sms - 1) / sms) : 0;
+  }
+}
 
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases,
                BodyRange range) {

@@ -176,6 +176,8 @@ void build_mrhs(const Plan &p, cudaStream_t s);
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
                     unsigned phases = 7u, BodyRange range = BodyRange());
 bool use_mrhs(const Plan &p, int64_t k);
+// resident chunk CTAs per SM and dynamic shared memory of k_chunk (index 0: DOWN, 1: UP)
+void chunk_occupancy(const Plan &p, int ctas[2], int64_t smem[2]);
 // Host-buffer application pipelined over body segments: H2D of segment i+1,
 // kernels of segment i and D2H of segment i-1 overlap (three streams).
 void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k);
