@@ -142,9 +142,11 @@ __device__ __forceinline__ void store6(double *p, const double (&v)[6]) {
 }
 
 // one node of the upward sweep (merge_infosets, matfree.py:41-62)
-template <int CS>
+// Residues go straight to the output block: row = sbase + tile.res_q - tile.res_local + md.res,
+// the chunk-local tile index in md.flags bits 6-15 (OB = out + sbase * K + col).
+template <int CS, bool K1>
 __device__ __forceinline__ void up_node(int slot, const double *rec, const NodeMeta *ME, double *M, const double *F,
-                                        double *RES) {
+                                        const TileDesc *TD, double *OB, int64_t K) {
   double R[rec_size(CS)];
   load_rec<CS>(rec, R);
   const NodeMeta md = ME[slot];
@@ -164,19 +166,21 @@ __device__ __forceinline__ void up_node(int slot, const double *rec, const NodeM
   double aa, bb, mp[6], res[6];
   rec_ratios(CS, R, 1, aa, bb);
   merge(CS, R, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
-  if (CS == GENERAL) {
+  if (CS != BEAD_BEAD) {
+    const TileDesc &T = TD[md.flags >> 6];
+    const int64_t kk = K1 ? 1 : K;
+    double *o = OB + (int64_t)(T.res_q - T.res_local + md.res) * kk;
 #pragma unroll
-    for (int r = 0; r < 6; r++) RES[md.res + r] = res[r];  // residue offsets are 8-byte aligned only
-  } else if (CS == RIGID_BEAD) {
-    RES[md.res + 0] = res[0]; RES[md.res + 1] = res[1]; RES[md.res + 2] = res[2];
+    for (int r = 0; r < res_rows(CS); r++) o[r * kk] = res[r];
   }
   store6(M + 6 * slot, mp);
 }
 
 // one node of the downward sweep (split_rvset, matfree.py:65-83)
-template <int CS>
-__device__ __forceinline__ void down_node(int slot, const double *rec, const NodeMeta *ME, double *M, double *F,
-                                          const double *RES) {
+// Bead velocities go straight to the output block through perm (OB = out + 3 bead0 K + col).
+template <int CS, bool K1>
+__device__ __forceinline__ void down_node(int slot, const double *rec, const NodeMeta *ME, double *M,
+                                          const uint32_t *PERM, double *OB, int64_t K, const double *RES) {
   double R[rec_size(CS)];
   load_rec<CS>(rec, R);
   const NodeMeta md = ME[slot];
@@ -190,15 +194,16 @@ __device__ __forceinline__ void down_node(int slot, const double *rec, const Nod
   double aa, bb;
   rec_ratios(CS, R, 1, aa, bb);
   split(CS, R, 1, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
+  const int64_t kk = K1 ? 1 : K;
   if (CS == BEAD_BEAD) {
-    double *f = F + 3 * (md.x & 0x7fff);
-    f[0] = lx[0]; f[1] = lx[1]; f[2] = lx[2];
+    double *o = OB + 3 * (int64_t)PERM[md.x & 0x7fff] * kk;
+    o[0] = lx[0]; o[kk] = lx[1]; o[2 * kk] = lx[2];
   } else {
     store6(M + 6 * md.x, lx);
   }
   if (CS != GENERAL) {
-    double *f = F + 3 * (md.y & 0x7fff);
-    f[0] = ly[0]; f[1] = ly[1]; f[2] = ly[2];
+    double *o = OB + 3 * (int64_t)PERM[md.y & 0x7fff] * kk;
+    o[0] = ly[0]; o[kk] = ly[1]; o[2 * kk] = ly[2];
   } else {
     store6(M + 6 * md.y, ly);
   }
@@ -231,7 +236,7 @@ __host__ __device__ __forceinline__ SmemMap smem_map(int head_bytes, int lrec_by
   m.head = (uint32_t)al128(head_bytes);
   m.lrec = (uint32_t)al128(lrec_bytes);
   m.v = (uint32_t)al128(8 * (size_t)(up ? 3 * max_beads : max_res));
-  m.x = (uint32_t)al128(8 * (size_t)(up ? max_res : 3 * max_beads));
+  m.x = 0u;  // outputs go straight to global memory (residues upward, velocities downward)
   m.root = up ? 0u : (uint32_t)al128(48 * (size_t)max_tiles);  // tile-root RV-sets (DOWN only)
   m.o_lrec = 3 * m.head;
   m.o_v = m.o_lrec + NLS * m.lrec;
@@ -459,33 +464,38 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
       const int tot = gG + gR + L.nB;
       if (UP) {
         const double *F = VBUF(fb);
-        double *RES = reinterpret_cast<double *>(smem + SM.o_x);
+        double *OB = a.out + sbase * K + col;
         for (int q = tid; q < tot; q += NT) {
           if (q < gG) {
-            if (q < L.nG) up_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
+            if (q < L.nG)
+              up_node<GENERAL, K1>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, cv.tiles, OB, K);
           } else if (q < gG + gR) {
             const int qq = q - gG;
             if (qq < L.nR)
-              up_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
+              up_node<RIGID_BEAD, K1>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F,
+                                      cv.tiles, OB, K);
           } else {
             const int qq = q - gG - gR;
-            up_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F, RES);
+            up_node<BEAD_BEAD, K1>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F,
+                                   cv.tiles, OB, K);
           }
         }
       } else {
         const double *RES = VBUF(fb);
-        double *F = reinterpret_cast<double *>(smem + SM.o_x);
+        double *OB = a.out + 3 * bead0 * K + col;
         for (int q = tid; q < tot; q += NT) {
           if (q < gG) {
-            if (q < L.nG) down_node<GENERAL>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, F, RES);
+            if (q < L.nG)
+              down_node<GENERAL, K1>(L.slot_begin + q, R + q * rec_size(GENERAL), cv.ME, M, cv.PERM, OB, K, RES);
           } else if (q < gG + gR) {
             const int qq = q - gG;
             if (qq < L.nR)
-              down_node<RIGID_BEAD>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, F, RES);
+              down_node<RIGID_BEAD, K1>(L.slot_begin + L.nG + qq, R + oR + qq * rec_size(RIGID_BEAD), cv.ME, M, cv.PERM,
+                                        OB, K, RES);
           } else {
             const int qq = q - gG - gR;
-            down_node<BEAD_BEAD>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M, F,
-                                 RES);
+            down_node<BEAD_BEAD, K1>(L.slot_begin + L.nG + L.nR + qq, R + oB + qq * rec_size(BEAD_BEAD), cv.ME, M,
+                                     cv.PERM, OB, K, RES);
           }
         }
       }
@@ -514,29 +524,13 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     long long to0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
     if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 2] += to0 - t_lv0;  // whole level loop
     if (UP) {
-      const double *RES = reinterpret_cast<const double *>(smem + SM.o_x);
       const int wid = tid >> 5, lane = tid & 31;
-      for (int t = wid; t < d.n_tiles; t += NT / 32) {  // residues (contiguous per tile) and tile-root info vectors
+      for (int t = wid; t < d.n_tiles; t += NT / 32) {  // tile-root info vectors
         const TileDesc T = cv.tiles[t];
-        double *o = a.out + (sbase + T.res_q + lane) * K + col;
-        const double *x = RES + T.res_local;
-        for (int r = lane; r < T.res_count; r += 32, o += 32 * K) *o = x[r];
         if (lane < 6) {
           const double v = M[6 * T.root_slot + lane];
           if (T.scratch >= 0) a.scratch[6 * (int64_t)T.scratch + lane] = v;
           else if (a.op == RQ_OP_QV) a.out[(3 * bead0 + lane) * K + col] = v;
-        }
-      }
-    } else {
-      const double *F = reinterpret_cast<const double *>(smem + SM.o_x);
-      double *ob = a.out + 3 * bead0 * K + col;
-      for (int i = tid; i < d.n_beads; i += NT) {
-        const uint32_t pp = cv.PERM[i];
-        if (!(pp & PERM_FOREIGN)) {
-          double *o = ob + 3 * (int64_t)pp * K;
-          o[0] = F[i * 3 + 0];
-          o[K] = F[i * 3 + 1];
-          o[2 * K] = F[i * 3 + 2];
         }
       }
     }

@@ -671,6 +671,7 @@ struct WriteCtx {
   const LevelDesc *lvl;
   const double *rec;
   uint8_t *blob;
+  const int32_t *big_scan;  // tile -> global TileDesc index (chunk-local = big_scan - chunk.tile_begin)
 };
 
 __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
@@ -702,7 +703,8 @@ __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
   const TileTmp &T = w.tiles[w.tile_of[g]];
   int tile_idx = w.tile_of[g];
   md.res = (uint16_t)(w.res_local_of_tile[tile_idx] + (w.c.res_off[g] - 6 - T.res_q));
-  md.flags = (uint16_t)f;
+  // bits 0-5: case | swapped | signs; bits 6-15: chunk-local tile index (upward residue stores)
+  md.flags = (uint16_t)(f | ((w.big_scan[tile_idx] - d.tile_begin) << 6));
   uint8_t *base = w.blob + d.blob_off;
   reinterpret_cast<NodeMeta *>(base + d.off_meta)[slot] = md;
   double *R = reinterpret_cast<double *>(base + d.off_rec);
@@ -1350,7 +1352,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
 
     ChunkLimits lim;
-    lim.max_bytes = 36 * 1024;
+    lim.max_bytes = 40 * 1024;
     if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
     // a single worst-case tile (all GENERAL nodes) must fit a chunk
     lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
@@ -1477,7 +1479,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                   lvl_base.as<int64_t>(),
                   lvl.as<LevelDesc>(),
                   p.rec.as<double>(),
-                  p.blob.as<uint8_t>()};
+                  p.blob.as<uint8_t>(),
+                  d_big_scan.as<int32_t>()};
       if (n_part > 0) k_write_nodes<<<nblk(n_part), NT, 0, s>>>(wc, n_part);
       if (nc) k_write_perm<<<(unsigned)nc, 128, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, p.perm.as<int32_t>(),
                                                   leaf_id.as<int32_t>(), noff, p.parent.as<int32_t>(),
