@@ -148,7 +148,7 @@ struct Plan {
 
   mutable std::mutex host_mu;
   // multi-RHS unit programs (rq_mrhs.cu), built on the first k >= mrhs_min application
-  int mrhs_min = 8;
+  int mrhs_min = 5;                // k at which the column-parallel kernels beat the column loop (measured)
   int mrhs_tile = 64;              // leaves per multi-RHS tile unit
   mutable std::mutex mrhs_mu;
   mutable bool mrhs_built = false;
