@@ -200,8 +200,9 @@ def test_multi_rhs(rq, oracle_mod, k):
         exp = ref.apply(opn, V)
         for c in range(k):
             assert per_body_rel(out[:, c], exp[:, c], 3 * n) < TOL, (opn, c)
-        col = op.apply(opn, np.ascontiguousarray(V[:, 5]))
-        assert np.abs(out[:, 5] - col).max() <= 1e-13 * np.abs(col).max()
+        c0 = k // 2
+        col = op.apply(opn, np.ascontiguousarray(V[:, c0]))
+        assert np.abs(out[:, c0] - col).max() <= 1e-13 * np.abs(col).max()
     # complement operators need n >= 2 everywhere (and the reference's Q~^T
     # raises for n == 2 blocks, matfree.py:161-170)
     keep = [j for j in range(len(counts)) if counts[j] >= 3]
