@@ -718,13 +718,16 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   if (a.cls[blockIdx.x] != a.want) return;
   const bool TM = RQ_TIMING && a.dbg && tid == 0;
   const long long c0 = TM ? clock64() : 0;
+  unsigned long long g0 = 0;
+  if (TM) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
   // stage the header part (levels, meta, inputs) with one TMA copy; the records stay
   // in global memory (prefetched into L2 here) and are read per node, so the CTA
   // needs little shared memory and many top trees are swept concurrently per SM
   if (tid == 0) {
     const TopHdr *gh = reinterpret_cast<const TopHdr *>(gB);
-    const unsigned hbytes = (unsigned)gh->off_rec, rbytes = (unsigned)gh->bytes - hbytes;
+    const unsigned hbytes = (unsigned)gh->off_rec;
+    const unsigned rbytes = (unsigned)gh->bytes - hbytes;
     if (rbytes) prefetch_l2(gB + hbytes, rbytes);
     mbar_init(&bar, 1);
     fence_mbar_init();
@@ -747,12 +750,12 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   const int64_t bead0 = a.bead_off[h.body];
   const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)h.body;
   if (UP) {
-    // 4 independent loads in flight per thread (tile-root vectors from L2)
+    // 8 independent loads in flight per thread (tile-root vectors from L2)
     const int n_in = 6 * h.n_inputs;
-    for (int i0 = tid; i0 < n_in; i0 += 4 * NTT) {
-      double v[4];
+    for (int i0 = tid; i0 < n_in; i0 += 8 * NTT) {
+      double v[8];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < 8; u++) {
         const int i = i0 + u * NTT;
         v[u] = 0.0;
         if (i < n_in) {
@@ -763,7 +766,7 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++)
+      for (int u = 0; u < 8; u++)
         if (i0 + u * NTT < n_in) IN[i0 + u * NTT] = v[u];
     }
     __syncthreads();
@@ -794,8 +797,10 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
     if (TM) {
       const long long c3 = clock64();
       long long *d = a.dbg + 8 * blockIdx.x;
+      unsigned long long g1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
       d[0] = c1 - c0; d[1] = c2 - c1; d[2] = c3 - c2; d[3] = h.n_levels; d[4] = h.n_nodes; d[5] = h.n_inputs;
-      d[6] = c0;
+      d[6] = (long long)g0; d[7] = (long long)g1;
     }
   } else {
     for (int q = tid; q < h.n_nodes; q += NTT) {
@@ -1019,12 +1024,17 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
         RQ_CUDA(cudaMemcpyAsync(h.data(), dbg2.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
         RQ_CUDA(cudaStreamSynchronize(s));
         double acc[6] = {0};
-        long long t_min = LLONG_MAX, t_max = 0;
+        long long t_min = LLONG_MAX, t_max = 0, e_max = 0;
+        double dur = 0;
         for (int64_t b = 0; b < p.n_topblob; b++) {
           for (int i = 0; i < 6; i++) acc[i] += (double)h[8 * b + i];
           t_min = std::min(t_min, h[8 * b + 6]);
           t_max = std::max(t_max, h[8 * b + 6]);
+          e_max = std::max(e_max, h[8 * b + 7]);
+          dur += (double)(h[8 * b + 7] - h[8 * b + 6]);
         }
+        fprintf(stderr, "[rq timing] k_top2 UP timeline: CTA starts spread %.1f us, last end %.1f us after first start, mean CTA duration %.1f us\n",
+                (t_max - t_min) / 1e3, (e_max - t_min) / 1e3, dur / (double)p.n_topblob / 1e3);
         const double nb = (double)p.n_topblob;
         fprintf(stderr, "[rq timing] k_top2 UP per CTA: blob wait %.0f, inputs %.0f, levels %.0f (%.1f levels, %.0f nodes, %.0f inputs); CTA start spread %lld cycles\n",
                 acc[0] / nb, acc[1] / nb, acc[2] / nb, acc[3] / nb, acc[4] / nb, acc[5] / nb, t_max - t_min);

@@ -1587,7 +1587,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
           const int nn = last - first, nl = h_lvl[bi + 1] - h_lvl[bi], ni = h_in[last] - h_in[first];
           const int64_t bytes = topblob_bytes(nn, nl, ni, h_rec[last] - h_rec[first]);
-          // staged: header, levels, meta and inputs (records are read from L2)
+          // staged: header, levels, meta and inputs; the records are read from L2 (staging
+          // them too was measured slower: fewer top trees resident per SM)
           const int64_t hdr_bytes = bytes - 8 * (h_rec[last] - h_rec[first]);
           const int64_t smem = (hdr_bytes + 127) / 128 * 128 + 48 * (int64_t)(std::max(ni, nn) + nn) + 128;
           if (smem <= smem_cap && nn < 32000 && ni < 32000) {
@@ -1596,7 +1597,6 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
             small_off.push_back(total);
             total += bytes;
             p.max_topblob_smem = std::max(p.max_topblob_smem, smem);
-            // shared-memory class: one launch per class, sized for the class maximum
             const int c = smem <= 32 * 1024 ? 0 : (smem <= 64 * 1024 ? 1 : (smem <= 112 * 1024 ? 2 : 3));
             small_cls.push_back((uint8_t)c);
             p.topclass_smem[c] = std::max(p.topclass_smem[c], smem);
