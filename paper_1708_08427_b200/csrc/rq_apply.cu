@@ -53,6 +53,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Programmatic dependent launch: every apply kernel is launched with programmatic
+// stream serialisation, lets its successor launch early (launch_dependents) and waits
+// for its predecessor's results (griddepcontrol.wait) only before touching data another
+// kernel produces (input/output vectors, exchange slots); plan data is read before.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // 32-bit shared-address forms (addresses computed once per kernel)
 __device__ __forceinline__ void mbar_expect_tx_u(uint32_t bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -379,6 +386,8 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   }
   unsigned phase = 0;  // parity bit per barrier
   int lctr = 0;        // level steps so far (selects the record stage)
+
+  pdl_wait();  // vectors and exchange slots may come from the previous kernel
   mbar_wait_u(BAR(0), 0);
   phase ^= 1u;
   prefetch_vectors<UP, NT, K1>(a, HEAD(0), VBUF(0), ROOTBUF(0));
@@ -600,6 +609,8 @@ __device__ __forceinline__ void top_store(const TopDfCtx &a, int64_t bead0, int3
 }
 
 __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
+
+  pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   int q = a.starts[i];
@@ -635,6 +646,8 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
 }
 
 __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
+
+  pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   constexpr int MAXP = 128;  // top-tree height <= max_depth + 1
@@ -735,6 +748,8 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
     bulk_g2s(smem, gB, hbytes, &bar);
   }
   __syncthreads();
+
+  pdl_wait();
   mbar_wait(&bar, 0);
   const long long c1 = TM ? clock64() : 0;
   const TopHdr h = *reinterpret_cast<const TopHdr *>(smem);
@@ -850,10 +865,27 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
 // single-bead bodies: Qv and Q^T w are the identity (matfree.py:99-100, 127-128)
 __global__ void k_small(const int32_t *bodies, int64_t n, const int64_t *bead_off, const double *in,
                         double *out, int64_t K, int64_t col) {
+
+  pdl_wait();
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= 3 * n) return;
   int64_t row = 3 * bead_off[bodies[t / 3]] + t % 3;
   out[row * K + col] = in[row * K + col];
+}
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
 }
 
 struct KernelCfg {
@@ -1003,21 +1035,21 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
         t2.want = c;
         const size_t sm = (size_t)p.topclass_smem[c];
         if (c < 2) {
-          if (up) k_top2<true, 32><<<(unsigned)(tb1 - tb0), 32, sm, s>>>(t2);
-          else k_top2<false, 32><<<(unsigned)(tb1 - tb0), 32, sm, s>>>(t2);
+          if (up) launch_pdl(k_top2<true, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
+          else launch_pdl(k_top2<false, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
         } else {
-          if (up) k_top2<true, 128><<<(unsigned)(tb1 - tb0), 128, sm, s>>>(t2);
-          else k_top2<false, 128><<<(unsigned)(tb1 - tb0), 128, sm, s>>>(t2);
+          if (up) launch_pdl(k_top2<true, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
+          else launch_pdl(k_top2<false, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
         }
       }
       if (t.n > 0) {
         const unsigned nb = (unsigned)((t.n + NT_TOP - 1) / NT_TOP);
-        if (up) k_top_df_up<<<nb, NT_TOP, 0, s>>>(t);
-        else k_top_df_down<<<nb, NT_TOP, 0, s>>>(t);
+        if (up) launch_pdl(k_top_df_up, nb, NT_TOP, 0, s, t);
+        else launch_pdl(k_top_df_down, nb, NT_TOP, 0, s, t);
       }
     };
     if (up) {
-      if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
+      if (do_chunks) launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
       if (do_top) top_pass();
       if (timing_top && do_top && p.n_topblob) {
         std::vector<long long> h((size_t)p.n_topblob * 8);
@@ -1041,7 +1073,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       }
     } else {
       if (do_top) top_pass();
-      if (do_chunks) cfg.fn<<<cfg.grid, cfg.threads, cfg.smem, s>>>(a);
+      if (do_chunks) launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
     }
     if (timing && do_chunks) {
       std::vector<long long> h((size_t)cfg.grid * 16 + 8);
@@ -1059,8 +1091,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 256 + 64, s));
     }
     if ((phases & 4u) && sm1 > sm0 && op <= 1)
-      k_small<<<(unsigned)((3 * (sm1 - sm0) + 255) / 256), 256, 0, s>>>(p.small_bodies.as<int32_t>() + sm0, sm1 - sm0,
-                                                                        p.bead_off_d.as<int64_t>(), in, out, k, col);
+      launch_pdl(k_small, (unsigned)((3 * (sm1 - sm0) + 255) / 256), 256, 0, s, p.small_bodies.as<int32_t>() + sm0,
+                 (int64_t)(sm1 - sm0), (const int64_t *)p.bead_off_d.as<int64_t>(), in, out, (int64_t)k, (int64_t)col);
   }
   RQ_CUDA(cudaGetLastError());
 }
