@@ -51,19 +51,46 @@ struct DBuf {
     return *this;
   }
   ~DBuf() { reset(); }
+  // Stream-ordered allocations from the device's default memory pool, configured to
+  // retain freed memory: rebuilding plans (and setup temporaries) reuses mapped memory
+  // instead of paying cudaMalloc/cudaFree (which synchronise and remap) every time.
+  // An allocation is completed before it is returned, so any stream may use it; a free
+  // first waits for the device, so no kernel still using the buffer can see it reused.
   void alloc(size_t b) {
     reset();
     if (b == 0) b = 16;
-    cudaError_t e = cudaMalloc(&p, b);
+    cudaStream_t s = pool_stream();
+    cudaError_t e = cudaMallocAsync(&p, b, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
       p = nullptr;
-      throw Error(RQ_ERR_NOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+      cudaGetLastError();
+      throw Error(RQ_ERR_NOMEM, std::string("cudaMallocAsync(") + std::to_string(b) + "): " + cudaGetErrorString(e));
     }
     bytes = b;
   }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, pool_stream());
+    }
     p = nullptr; bytes = 0;
+  }
+  static cudaStream_t pool_stream() {
+    static thread_local int dev_cached = -1;
+    static thread_local cudaStream_t st = nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!st || dev != dev_cached) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      dev_cached = dev;
+    }
+    return st;
   }
   template <class T> T *as() const { return static_cast<T *>(p); }
 };
