@@ -17,6 +17,7 @@
 // orthogonal transforms (~0.3-0.6 flop/B).
 #include <algorithm>
 #include <climits>
+#include <cuda/atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -567,6 +568,23 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
 //  * downward: every thread recomputes the split chain along its root-to-node
 //    path (identical arithmetic, so every path sees identical values) and writes
 //    the outputs of the children that leave the top tree (tile roots, beads).
+// a node record (global memory, 16-byte aligned) into registers
+__device__ __forceinline__ void ldg_rec(int cs, const double *g, double (&R)[rec_size(GENERAL)]) {
+  const double2 *g2 = reinterpret_cast<const double2 *>(g);
+  const int n2 = rec_size(cs) / 2;
+#pragma unroll
+  for (int i = 0; i < rec_size(GENERAL) / 2; i++) {
+    if (i < n2) {
+      const double2 v = __ldg(g2 + i);
+      R[2 * i] = v.x;
+      R[2 * i + 1] = v.y;
+    } else {
+      R[2 * i] = 0.0;
+      R[2 * i + 1] = 0.0;
+    }
+  }
+}
+
 struct TopDfCtx {
   const int32_t *starts;
   int64_t n;
@@ -609,23 +627,25 @@ __device__ __forceinline__ void top_store(const TopDfCtx &a, int64_t bead0, int3
 }
 
 __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
-
   pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   int q = a.starts[i];
   for (;;) {
     const TopNode T = a.top[q];
+    const int par = T.is_root ? -1 : __ldg(&a.parent[q]);
+    const int need = par >= 0 ? __ldg(&a.need[par]) : 0;
     const int j = T.body;
     const int64_t bead0 = a.bead_off[j];
     const int64_t sbase = spec_base(a.op, a.bead_off, j);
     const int cs = flag_case(T.flags);
-    const double *rec = a.rec + T.rec_off;
+    double R[rec_size(GENERAL)];
+    ldg_rec(cs, a.rec + T.rec_off, R);
     double aa, bb, mx[6], my[6], mp[6], res[6];
-    rec_ratios(cs, rec, 1, aa, bb);
     top_fetch(a, bead0, T.x, mx);
     top_fetch(a, bead0, T.y, my);
-    merge(cs, rec, 1, flag_signs(T.flags), aa, bb, mx, my, mp, res);
+    rec_ratios(cs, R, 1, aa, bb);
+    merge(cs, R, 1, flag_signs(T.flags), aa, bb, mx, my, mp, res);
     for (int r = 0; r < res_rows(cs); r++) a.out[(sbase + T.res_q + r) * a.k + a.col] = res[r];
     if (T.is_root) {
       if (a.op == RQ_OP_QV)
@@ -634,12 +654,11 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
     }
 #pragma unroll
     for (int r = 0; r < 6; r++) __stcg(&a.scratch[6 * (int64_t)T.self_slot + r], mp[r]);
-    __threadfence();
-    const int par = a.parent[q];
-    if (a.need[par] == 2) {
-      if (atomicAdd(&a.cnt[par], 1) == 0) return;  // first arrival: the sibling's thread continues
-      a.cnt[par] = 0;                                // second arrival: reset for the next application
-      __threadfence();
+    if (need == 2) {
+      // acq_rel: the first arrival's slot writes are released, the second arrival acquires them
+      cuda::atomic_ref<int, cuda::thread_scope_device> c(a.cnt[par]);
+      if (c.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // the sibling's thread continues
+      c.store(0, cuda::memory_order_relaxed);                         // reset for the next application
     }
     q = par;
   }
@@ -703,23 +722,6 @@ struct Top2Ctx {
   double *scratch;
   int op;
 };
-
-// a node record (global memory, 16-byte aligned) into registers
-__device__ __forceinline__ void ldg_rec(int cs, const double *g, double (&R)[rec_size(GENERAL)]) {
-  const double2 *g2 = reinterpret_cast<const double2 *>(g);
-  const int n2 = rec_size(cs) / 2;
-#pragma unroll
-  for (int i = 0; i < rec_size(GENERAL) / 2; i++) {
-    if (i < n2) {
-      const double2 v = __ldg(g2 + i);
-      R[2 * i] = v.x;
-      R[2 * i + 1] = v.y;
-    } else {
-      R[2 * i] = 0.0;
-      R[2 * i + 1] = 0.0;
-    }
-  }
-}
 
 // NTT threads per top tree: one warp for the small shared-memory classes (top trees
 // of config-2 bodies: ~7 nodes per level), 128 for the large ones
