@@ -588,6 +588,8 @@ __device__ __forceinline__ void ldg_rec(int cs, const double *g, double (&R)[rec
 struct TopDfCtx {
   const int32_t *starts;
   int64_t n;
+  const int32_t *paths;     // root-to-start paths (downward sweep)
+  const int64_t *path_off;
   const TopNode *top;
   const int32_t *parent, *need;
   int32_t *cnt;
@@ -665,35 +667,44 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
 }
 
 __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
-
   pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= a.n) return;
-  constexpr int MAXP = 128;  // top-tree height <= max_depth + 1
-  int path[MAXP];
-  int d = 0;
-  path[0] = a.starts[i];
-  while (d + 1 < MAXP && a.parent[path[d]] >= 0) { path[d + 1] = a.parent[path[d]]; d++; }
-  const TopNode R0 = a.top[path[d]];
-  const int j = R0.body;
+  // precomputed root-to-start path; the next node's TopNode, record and residue rows are
+  // loaded while the current one is split (one node of software pipelining)
+  const int32_t *path = a.paths + a.path_off[i];
+  const int len = (int)(a.path_off[i + 1] - a.path_off[i]);
+  TopNode T = a.top[path[0]];
+  const int j = T.body;
   const int64_t bead0 = a.bead_off[j];
   const int64_t sbase = spec_base(a.op, a.bead_off, j);
+  auto load_node = [&](const TopNode &N, double (&R)[rec_size(GENERAL)], double (&res)[6]) {
+    const int cs = flag_case(N.flags);
+    ldg_rec(cs, a.rec + N.rec_off, R);
+#pragma unroll
+    for (int r = 0; r < 6; r++) res[r] = r < res_rows(cs) ? a.in[(sbase + N.res_q + r) * a.k + a.col] : 0.0;
+  };
   double lp[6];
   for (int r = 0; r < 6; r++) lp[r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * a.k + a.col] : 0.0;
-  for (; d >= 0; d--) {
-    const TopNode T = a.top[path[d]];
+  double R[rec_size(GENERAL)], res[6];
+  load_node(T, R, res);
+  for (int d = 0; d < len; d++) {
+    TopNode Tn = T;
+    double Rn[rec_size(GENERAL)], resn[6];
+    if (d + 1 < len) {
+      Tn = a.top[path[d + 1]];
+      load_node(Tn, Rn, resn);
+    }
     const int cs = flag_case(T.flags);
-    const double *rec = a.rec + T.rec_off;
-    double aa, bb, res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
-    rec_ratios(cs, rec, 1, aa, bb);
-    for (int r = 0; r < res_rows(cs); r++) res[r] = a.in[(sbase + T.res_q + r) * a.k + a.col];
-    split(cs, rec, 1, flag_signs(T.flags), aa, bb, lp, res, lx, ly);
-    if (d == 0) {  // start node: both children leave the top tree
+    double aa, bb, lx[6], ly[6];
+    rec_ratios(cs, R, 1, aa, bb);
+    split(cs, R, 1, flag_signs(T.flags), aa, bb, lp, res, lx, ly);
+    if (d + 1 == len) {  // start node: both children leave the top tree
       top_store(a, bead0, T.x, lx);
       top_store(a, bead0, T.y, ly);
       break;
     }
-    const bool x_on_path = T.x >= 0 && T.x == a.top[path[d - 1]].self_slot;
+    const bool x_on_path = T.x >= 0 && T.x == Tn.self_slot;
     // the off-path child: written here unless it is itself a top node (another path's)
     if (x_on_path) {
       if (T.ny <= a.S) top_store(a, bead0, T.y, ly);
@@ -704,6 +715,11 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
 #pragma unroll
       for (int r = 0; r < 6; r++) lp[r] = ly[r];
     }
+    T = Tn;
+#pragma unroll
+    for (int e = 0; e < rec_size(GENERAL); e++) R[e] = Rn[e];
+#pragma unroll
+    for (int r = 0; r < 6; r++) res[r] = resn[r];
   }
 }
 
@@ -990,6 +1006,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   TopDfCtx t{};
   const int64_t ts0 = all ? 0 : p.h_topstart_first[j0], ts1 = all ? p.n_top_start : p.h_topstart_first[j1];
   t.starts = p.top_start.as<int32_t>() + ts0;
+  t.paths = p.top_paths.as<int32_t>();
+  t.path_off = p.top_path_off.as<int64_t>() + ts0;
   t.n = ts1 - ts0;
   t.top = p.top.as<TopNode>();
   t.parent = p.top_parent.as<int32_t>();

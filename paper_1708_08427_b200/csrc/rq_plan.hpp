@@ -157,6 +157,7 @@ struct Plan {
   DBuf top_need;                   // int32 [n_top]: children inside the top tree (arrivals to wait for)
   DBuf top_start;                  // int32 [n_top_start]: top nodes whose children are both below the top tree
   int64_t n_top_start = 0;
+  DBuf top_paths, top_path_off;    // int32 root-to-start paths, int64 [n_top_start+1] CSR offsets
   std::vector<int64_t> h_topstart_first;  // [m+1]
   // host-side body -> work-list ranges (segmented / pipelined applications)
   std::vector<int64_t> h_chunk_first, h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each

@@ -833,6 +833,24 @@ __global__ void k_top_links(const TopNode *top, int64_t q0, int64_t q1, const in
   need[q] = (cx >= 0) + (cy >= 0);  // arrivals before the node can be merged
 }
 
+__global__ void k_top_path_len(const int32_t *parent, const int32_t *starts, int64_t n, int64_t *len) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t l = 1;
+  for (int q = starts[i]; parent[q] >= 0; q = parent[q]) l++;
+  len[i] = l;
+}
+__global__ void k_top_path_write(const int32_t *parent, const int32_t *starts, int64_t n, const int64_t *off,
+                                 int32_t *paths) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t w = off[i + 1] - 1;  // start node last, root first
+  for (int q = starts[i];; q = parent[q]) {
+    paths[w--] = q;
+    if (parent[q] < 0) break;
+  }
+}
+
 __global__ void k_top_slotmap(const TopNode *top, int64_t nt, const int32_t *topbody_idx, const int32_t *topbody_lvl,
                               const int32_t *toplvl, int32_t *slot_to_local, int32_t *nin, int64_t *recsz) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1057,7 +1075,7 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_cnt, &top_need, &top_start, &mrhs_units, &mrhs_prog, &mrhs_scratch};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_cnt, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog, &mrhs_scratch};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
@@ -1694,6 +1712,23 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.top_start.alloc(std::max<int64_t>(p.n_top_start, 1) * 4);
         if (p.n_top_start)
           RQ_CUDA(cudaMemcpyAsync(p.top_start.p, starts.data(), p.n_top_start * 4, cudaMemcpyHostToDevice, s));
+        // root-to-start paths (downward dataflow sweep), CSR over the start nodes
+        {
+          const int64_t ns = p.n_top_start;
+          DBuf plen;
+          plen.alloc(std::max<int64_t>(ns, 1) * 8);
+          p.top_path_off.alloc((ns + 1) * 8);
+          if (ns) k_top_path_len<<<nblk(ns), NT, 0, s>>>(p.top_parent.as<int32_t>(), p.top_start.as<int32_t>(), ns,
+                                                       plen.as<int64_t>());
+          if (ns) exclusive_scan(plen.as<int64_t>(), p.top_path_off.as<int64_t>(), ns, s);
+          const int64_t total = ns ? d2h1<int64_t>(p.top_path_off.as<int64_t>() + ns - 1, s) +
+                                         d2h1<int64_t>(plen.as<int64_t>() + ns - 1, s)
+                                   : 0;
+          RQ_CUDA(cudaMemcpyAsync(p.top_path_off.as<int64_t>() + ns, &total, 8, cudaMemcpyHostToDevice, s));
+          p.top_paths.alloc(std::max<int64_t>(total, 1) * 4);
+          if (ns) k_top_path_write<<<nblk(ns), NT, 0, s>>>(p.top_parent.as<int32_t>(), p.top_start.as<int32_t>(), ns,
+                                                         p.top_path_off.as<int64_t>(), p.top_paths.as<int32_t>());
+        }
         RQ_CUDA(cudaStreamSynchronize(s));
       } else {
         p.h_topblob_first.assign(m + 1, 0);
