@@ -1594,7 +1594,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         d2h(h_toplvl.data(), p.toplvl.p, p.n_toplevels + 1, s);
         d2h(h_in.data(), in_scan.p, nt + 1, s);
         d2h(h_rec.data(), rec_scan.p, nt + 1, s);
-        const int64_t smem_cap = 180 * 1024;
+        int64_t smem_cap = 112 * 1024;  // larger top trees go to the dataflow kernels (measured on config 4)
+        if (const char *e = getenv("RQ_TOP_SMEM_KB")) smem_cap = std::max(16, atoi(e)) * 1024;
         std::vector<int64_t> blob_off(p.n_topbodies, -1), small_off;
         std::vector<int32_t> small_tb, big_tb;
         std::vector<uint8_t> small_cls;
