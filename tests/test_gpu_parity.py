@@ -363,3 +363,35 @@ def test_node_primitives(rq, oracle_mod):
         if fac.case is rq.NodeCase.GENERAL:
             np.testing.assert_allclose(lx, mx, atol=1e-13)
             np.testing.assert_allclose(ly, my, atol=1e-13)
+
+
+def test_rigid_body_basis(rq):
+    """estimator.RigidBodyBasis (reference estimator.py:43-78) on the GPU operators:
+    rows are force vectors; a batch of rows is one multi-RHS block."""
+    from paper_1708_08427_b200.estimator import RigidBodyBasis
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+    from sklearn.exceptions import NotFittedError
+
+    pos, _ = ellipsoid_batch([700], seed=4)
+    n = pos.shape[0]
+    rng = np.random.default_rng(8)
+    V = rng.normal(size=(7, 3 * n))
+    op = rq.BodyOperator(rq.BeadModel(pos))
+    for comp, fwd in ((False, op.qv), (True, op.qtilde_v)):
+        est = RigidBodyBasis(complement=comp).fit(pos)
+        C = est.transform(V)
+        assert C.shape == (7, 3 * n - (6 if comp else 0))
+        ref = np.stack([fwd(V[i]) for i in range(7)])
+        assert np.abs(C - ref).max() <= 1e-13 * np.abs(ref).max()
+        assert np.allclose(est.transform(V[2]), C[2], rtol=0, atol=1e-13 * np.abs(ref).max())
+        back = est.inverse_transform(C)
+        if comp:  # Q~^T Q~ is the projector onto the complement; Q~ Q~^T = I
+            assert np.abs(est.transform(back) - C).max() < 1e-12 * np.abs(C).max()
+        else:
+            assert np.abs(back - V).max() < 1e-12 * np.abs(V).max()
+    with pytest.raises(NotFittedError):
+        RigidBodyBasis().transform(V)
+    with pytest.raises(ValueError):
+        RigidBodyBasis().fit(pos).transform(V[:, :-1])
+    with pytest.raises(ValueError):
+        RigidBodyBasis(complement=True).fit(pos[:1])

@@ -107,3 +107,13 @@ def test_workload_generators():
     assert pos.shape == (30, 3) and list(off) == [0, 10, 30]
     c = config4_counts(m=20000)
     assert c.min() >= 500 and c.max() < 50000 and 1.9e8 < c.sum() < 2.4e8
+
+
+def test_rigid_body_basis_validation():
+    """Shape / finiteness checks of the estimator run before any GPU work."""
+    from paper_1708_08427_b200.estimator import RigidBodyBasis
+
+    with pytest.raises(ValueError, match="shape"):
+        RigidBodyBasis().fit(np.zeros((4, 2)))
+    with pytest.raises(ValueError, match="finite"):
+        RigidBodyBasis().fit(np.array([[0.0, 0.0, np.nan], [1.0, 0.0, 0.0]]))
