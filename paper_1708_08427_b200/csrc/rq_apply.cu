@@ -948,6 +948,13 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
 
 }  // namespace
 
+Plan::StreamState &Plan::state_for(cudaStream_t s) const {
+  std::lock_guard<std::mutex> lock(state_mu);
+  auto &slot = stream_state[s];
+  if (!slot) slot.reset(new StreamState());
+  return *slot;
+}
+
 void chunk_occupancy(const Plan &p, int ctas[2], int64_t smem[2]) {
   for (int u = 0; u < 2; u++) {
     ApplyCtx a{};
@@ -968,9 +975,11 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     throw Error(RQ_ERR_BODY_TOO_SMALL, "complement operators need every body to have >= 2 beads");
   if (k < 1) throw Error(RQ_ERR_LENGTH, "k must be >= 1");
   RQ_CUDA(cudaSetDevice(p.device));
-  if (p.scratch_k < 1 || p.scratch.bytes < (size_t)std::max<int64_t>(p.n_slots, 1) * 48) {
-    p.scratch.alloc(std::max<int64_t>(p.n_slots, 1) * 48);
-    p.scratch_k = 1;
+  Plan::StreamState &ss = p.state_for(s);
+  if (ss.scratch.bytes < (size_t)std::max<int64_t>(p.n_slots, 1) * 48) ss.scratch.alloc(std::max<int64_t>(p.n_slots, 1) * 48);
+  if (!ss.top_cnt.p) {  // arrival counters start at zero and reset themselves
+    ss.top_cnt.alloc(std::max<int64_t>(p.n_top, 1) * 4);
+    RQ_CUDA(cudaMemsetAsync(ss.top_cnt.p, 0, std::max<int64_t>(p.n_top, 1) * 4, s));
   }
   if (use_mrhs(p, k)) {  // column-parallel stack-machine kernels (rq_mrhs.cu)
     run_apply_mrhs(p, op, in, out, k, s, phases, range);
@@ -991,7 +1000,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   a.in = in;
   a.out = out;
   a.k = k;
-  a.scratch = p.scratch.as<double>();
+  a.scratch = ss.scratch.as<double>();
   a.op = op;
   KernelCfg cfg = chunk_cfg(p, up, a);
   a.pf_dist = 1;
@@ -1011,7 +1020,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.n = ts1 - ts0;
   t.top = p.top.as<TopNode>();
   t.parent = p.top_parent.as<int32_t>();
-  t.cnt = p.top_cnt.as<int32_t>();
+  t.cnt = ss.top_cnt.as<int32_t>();
   t.need = p.top_need.as<int32_t>();
   t.perm = p.perm.as<int32_t>();
   t.bead_off = p.bead_off_d.as<int64_t>();
@@ -1019,7 +1028,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.in = in;
   t.out = out;
   t.k = k;
-  t.scratch = p.scratch.as<double>();
+  t.scratch = ss.scratch.as<double>();
   t.op = op;
   t.S = p.tile_leaves;
   Top2Ctx t2{};
@@ -1037,7 +1046,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t2.in = in;
   t2.out = out;
   t2.k = k;
-  t2.scratch = p.scratch.as<double>();
+  t2.scratch = ss.scratch.as<double>();
   t2.op = op;
   if (p.n_topblob) {
     for (const void *f2 : {(const void *)k_top2<true, 32>, (const void *)k_top2<false, 32>,

@@ -647,7 +647,8 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
   const int64_t t0 = p.h_tile_unit_first[j0], t1 = p.h_tile_unit_first[j1];
   const int64_t q0 = p.h_top_unit_first[j0], q1 = p.h_top_unit_first[j1];
   const size_t scratch_bytes = (size_t)std::max<int64_t>(p.n_tile_units, 1) * 6 * k * 8;
-  if (p.mrhs_scratch.bytes < scratch_bytes) p.mrhs_scratch.alloc(scratch_bytes);
+  Plan::StreamState &ss = p.state_for(s);
+  if (ss.mrhs_scratch.bytes < scratch_bytes) ss.mrhs_scratch.alloc(scratch_bytes);
   int sms = 0;
   RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
   MrhsCtx a{};
@@ -655,7 +656,7 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
   a.bead_off = p.bead_off_d.as<int64_t>();
   a.in = in;
   a.out = out;
-  a.scratch = p.mrhs_scratch.as<double>();
+  a.scratch = ss.mrhs_scratch.as<double>();
   a.K = k;
   a.op = op;
   a.n_cg = (k + 31) / 32;

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -153,7 +155,6 @@ struct Plan {
   int64_t n_topbig = 0;
   // dataflow sweep of those big top trees (k_top_df): parent links, arrival counters, start nodes
   DBuf top_parent;                 // int32 [n_top]: parent top index, -1 for roots / staged bodies
-  mutable DBuf top_cnt;            // int32 [n_top]: upward arrival counters (self-resetting)
   DBuf top_need;                   // int32 [n_top]: children inside the top tree (arrivals to wait for)
   DBuf top_start;                  // int32 [n_top_start]: top nodes whose children are both below the top tree
   int64_t n_top_start = 0;
@@ -161,8 +162,6 @@ struct Plan {
   std::vector<int64_t> h_topstart_first;  // [m+1]
   // host-side body -> work-list ranges (segmented / pipelined applications)
   std::vector<int64_t> h_chunk_first, h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each
-  mutable DBuf scratch;            // double [6 * n_slots * kcap]
-  mutable int64_t scratch_k = 0;
   DBuf err;                        // int64 [8] device error flags
   // deterministic per-body reductions (centroid, Zf): fixed segments
   int64_t n_seg = 0;
@@ -175,6 +174,16 @@ struct Plan {
   mutable cudaStream_t host_stream = nullptr, host_stream2 = nullptr, host_stream3 = nullptr;
 
   mutable std::mutex host_mu;
+  // Per-stream exchange state: applications of one plan on different streams may run
+  // concurrently (matfree.py:16-17: applies on one fitted tree are safe), so the tile-root
+  // exchange slots, the multi-RHS exchange block and the top-tree arrival counters are
+  // owned per stream.
+  struct StreamState {
+    DBuf scratch, mrhs_scratch, top_cnt;
+  };
+  mutable std::mutex state_mu;
+  mutable std::map<cudaStream_t, std::unique_ptr<StreamState>> stream_state;
+  StreamState &state_for(cudaStream_t s) const;
   // multi-RHS unit programs (rq_mrhs.cu), built on the first k >= mrhs_min application
   int mrhs_min = 5;                // k at which the column-parallel kernels beat the column loop (measured)
   int mrhs_tile = 64;              // leaves per multi-RHS tile unit
@@ -183,7 +192,7 @@ struct Plan {
   mutable int64_t mrhs_entries = 0, n_tile_units = 0, n_top_units = 0;
   mutable int64_t mrhs_tile_bytes = 0, mrhs_top_bytes = 0;  // entry header + record bytes per column group
   mutable int mrhs_depth_tile = 1, mrhs_depth_top = 1;
-  mutable DBuf mrhs_units, mrhs_prog, mrhs_scratch;
+  mutable DBuf mrhs_units, mrhs_prog;
   mutable std::vector<int64_t> h_tile_unit_first, h_top_unit_first;
   int64_t device_bytes() const;
   ~Plan() {

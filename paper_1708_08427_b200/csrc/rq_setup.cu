@@ -1075,7 +1075,7 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &scratch, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_cnt, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog, &mrhs_scratch};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
@@ -1675,11 +1675,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         }
         // dataflow top trees (bodies whose top tree does not fit shared memory)
         p.top_parent.alloc(std::max<int64_t>(nt, 1) * 4);
-        p.top_cnt.alloc(std::max<int64_t>(nt, 1) * 4);
         p.top_need.alloc(std::max<int64_t>(nt, 1) * 4);
         RQ_CUDA(cudaMemsetAsync(p.top_need.p, 0, std::max<int64_t>(nt, 1) * 4, s));
         RQ_CUDA(cudaMemsetAsync(p.top_parent.p, 0xff, std::max<int64_t>(nt, 1) * 4, s));
-        RQ_CUDA(cudaMemsetAsync(p.top_cnt.p, 0, std::max<int64_t>(nt, 1) * 4, s));
         std::vector<int32_t> starts;
         p.h_topstart_first.assign(m + 1, 0);
         if (p.n_topbig) {

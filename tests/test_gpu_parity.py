@@ -395,3 +395,30 @@ def test_rigid_body_basis(rq):
         RigidBodyBasis().fit(pos).transform(V[:, :-1])
     with pytest.raises(ValueError):
         RigidBodyBasis(complement=True).fit(pos[:1])
+
+
+def test_concurrent_streams(rq):
+    """Applications of one plan on different CUDA streams may overlap (matfree.py:16-17):
+    every stream has its own exchange slots and top-tree counters."""
+    import torch
+
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([4096] * 40 + [50000, 30000], seed=13)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    N, m = int(off[-1]), len(off) - 1
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    vs = [torch.randn(3 * N, generator=gen, device="cuda", dtype=torch.float64) for _ in range(4)]
+    gs = [torch.randn(3 * N - 6 * m, generator=gen, device="cuda", dtype=torch.float64) for _ in range(4)]
+    seq = [(op.apply("qtilde_v", v), op.apply("qtilde_tv", g)) for v, g in zip(vs, gs)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = [None] * 4
+    for rep in range(3):
+        for i, st in enumerate(streams):
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                outs[i] = (op.apply("qtilde_v", vs[i]), op.apply("qtilde_tv", gs[i]))
+        torch.cuda.synchronize()
+        for i in range(4):
+            assert torch.equal(outs[i][0], seq[i][0]) and torch.equal(outs[i][1], seq[i][1]), (rep, i)
