@@ -397,20 +397,26 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   int64_t pf_k = 0;  // chunk iteration of the next level step to issue
   int pf_s = 0;      // its level step within that chunk
   int pf_n = 0;      // level steps issued so far
+  int pf_hs = 0;     // head stage of chunk pf_k (= pf_k % 3, tracked incrementally)
   auto issue_levels = [&](int g, int64_t k_avail) {
     // issue while fewer than NLS steps are in flight beyond the current one
     while (pf_n < g + NLS && pf_k < cnt && pf_k <= k_avail) {
-      const ChunkView nv = view(HEAD(pf_k % 3));
-      const ChunkDesc &nd = *nv.hdr;
+      const unsigned char *HB = HEAD(pf_hs);
+      const ChunkDesc &nd = *reinterpret_cast<const ChunkDesc *>(HB);
       const int nH = nd.n_levels;
-      const LevelDesc L2 = nv.LV[UP ? pf_s : nH - 1 - pf_s];
+      const LevelDesc *LV = reinterpret_cast<const LevelDesc *>(HB + sizeof(ChunkDesc) + sizeof(TileDesc) * nd.n_tiles);
+      const LevelDesc &L2 = LV[UP ? pf_s : nH - 1 - pf_s];
       const double *g2 = reinterpret_cast<const double *>(a.blob + nd.blob_off + nd.off_rec) + L2.recG;
       const unsigned bytes = 8u * (unsigned)level_rec_doubles(L2);
       const int st = pf_n & (NLS - 1);
       mbar_expect_tx_u(BAR(3 + st), bytes);
       bulk_g2s_u(LREC_U(st), g2, bytes, BAR(3 + st));
       pf_n++;
-      if (++pf_s == nH) { pf_s = 0; pf_k++; }
+      if (++pf_s == nH) {
+        pf_s = 0;
+        pf_k++;
+        pf_hs = pf_hs == 2 ? 0 : pf_hs + 1;
+      }
     }
   };
   if (tid == PROD) issue_levels(0, 0);
