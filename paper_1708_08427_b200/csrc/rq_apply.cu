@@ -31,6 +31,7 @@ namespace {
 
 constexpr int NT_TOP = 128;  // dataflow top kernels
 constexpr int NLS = 2;  // level-record stages in shared memory (records issued NLS-1 steps ahead)
+static_assert((NLS & (NLS - 1)) == 0, "stage indices use & (NLS - 1)");
 
 // ---- PTX helpers: mbarrier + bulk copy ------------------------------------------
 
