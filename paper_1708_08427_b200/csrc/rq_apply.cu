@@ -714,11 +714,11 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
     const bool x_on_path = T.x >= 0 && T.x == Tn.self_slot;
     // the off-path child: written here unless it is itself a top node (another path's)
     if (x_on_path) {
-      if (T.ny <= a.S) top_store(a, bead0, T.y, ly);
+      if (!T.y_top) top_store(a, bead0, T.y, ly);
 #pragma unroll
       for (int r = 0; r < 6; r++) lp[r] = lx[r];
     } else {
-      if (T.nx <= a.S) top_store(a, bead0, T.x, lx);
+      if (!T.x_top) top_store(a, bead0, T.x, lx);
 #pragma unroll
       for (int r = 0; r < 6; r++) lp[r] = ly[r];
     }

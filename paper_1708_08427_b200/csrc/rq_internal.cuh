@@ -85,7 +85,7 @@ struct TopNode {         // node with more than tile_leaves beads
   int32_t x, y;          // >= 0: exchange slot; < 0: ~(global tree-order bead index)
   int32_t self_slot;     // exchange slot of this node
   int32_t res_q;         // body-relative Q~ offset of its residue rows (-1 if none)
-  int32_t nx, ny;
+  int32_t x_top, y_top;  // 1 if the formula-x / -y child is itself a top-tree node
   int32_t body;
   uint16_t flags;
   uint16_t is_root;

@@ -102,6 +102,7 @@ struct Plan {
   int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
   int max_depth = 96;
   int tile_leaves = 48;            // S (measured best for config 2 with 40 KiB chunks)
+  int tile_height = 0;             // tile height cut (0: none)
   int chunk_threads = 128;         // threads per chunk CTA
   int64_t max_blob = 0;            // largest chunk blob (bytes)
   int64_t max_head_bytes = 0;      // largest chunk head (everything before the records)

@@ -443,6 +443,7 @@ __global__ void k_factor(FactorCtx c, int64_t N) {
 
 struct LayoutCtx {
   int S;
+  int Hc;  // tile height cut (0: none): tiles are maximal subtrees with <= S leaves and height <= Hc
   const int64_t *bead_off, *node_off;
   const int32_t *node_body, *start, *stop, *parent, *height, *res_off;
   const int64_t *rec_off;
@@ -459,8 +460,9 @@ __global__ void k_classify(LayoutCtx c, int64_t NN, int32_t *is_tile, int32_t *i
   int64_t nb = c.node_off[j];
   int L = nodeL(c, g);
   int p = c.parent[g];
-  bool top = L > c.S;
-  bool tile = !top && (p < 0 || nodeL(c, nb + p) > c.S);
+  auto is_top_node = [&](int64_t q) { return nodeL(c, q) > c.S || (c.Hc > 0 && c.height[q] > c.Hc); };
+  bool top = is_top_node(g);
+  bool tile = !top && (p < 0 || is_top_node(nb + p));
   is_top[g] = top;
   is_tile[g] = tile;
   is_slot[g] = top || (tile && L >= 2);
@@ -722,9 +724,17 @@ __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
 }
 
 // perm section of each blob; beads of singleton tiles are marked foreign
+__global__ void k_root_is_top(const int32_t *is_top, const int64_t *bead_off, const int64_t *node_off, int64_t m,
+                              int32_t *out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int64_t n = bead_off[j + 1] - bead_off[j];
+  out[j] = is_top[node_off[j] + 2 * n - 2];
+}
+
 __global__ void k_write_perm(const ChunkDesc *chunks, int64_t nc, const int32_t *perm,
                              const int32_t *leaf_id, const int64_t *node_off, const int32_t *parent,
-                             const int32_t *start, const int32_t *stop, int S, uint8_t *blob) {
+                             const int32_t *is_top, uint8_t *blob) {
   int64_t c = blockIdx.x;
   if (c >= nc) return;
   const ChunkDesc &d = chunks[c];
@@ -734,7 +744,7 @@ __global__ void k_write_perm(const ChunkDesc *chunks, int64_t nc, const int32_t 
     int64_t gb = d.bead_begin + i;
     int lf = leaf_id[gb];
     int p = parent[nb + lf];
-    bool foreign = p >= 0 && (stop[nb + p] - start[nb + p]) > S;
+    bool foreign = p >= 0 && is_top[nb + p];  // singleton tile: the bead's parent is a top node
     P[i] = (uint32_t)perm[gb] | (foreign ? PERM_FOREIGN : 0u);
   }
 }
@@ -783,8 +793,8 @@ __global__ void k_top_fill(LayoutCtx c, int64_t NN, const int32_t *is_top, const
   T.self_slot = slot_scan[g];
   int cs = flag_case(f);
   T.res_q = res_rows(cs) ? c.res_off[g] - 6 : -1;
-  T.nx = c.stop[nb + xi] - c.start[nb + xi];
-  T.ny = c.stop[nb + yi] - c.start[nb + yi];
+  T.x_top = is_top[nb + xi];
+  T.y_top = is_top[nb + yi];
   T.body = j;
   T.flags = (uint16_t)f;
   T.is_root = c.parent[g] < 0;
@@ -1112,6 +1122,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
   if (max_depth < 1 || max_depth + body_bits > 128)
     throw Error(RQ_ERR_VALUE, "max_depth must be in [1, 128 - ceil(log2 m)]");
   if (const char *e = getenv("RQ_TILE_LEAVES")) p.tile_leaves = std::min(1024, std::max(2, atoi(e)));
+  if (const char *e = getenv("RQ_TILE_HEIGHT")) p.tile_height = std::max(0, atoi(e));
   if (const char *e = getenv("RQ_CHUNK_THREADS")) p.chunk_threads = atoi(e);
   if (const char *e = getenv("RQ_MRHS_MIN")) p.mrhs_min = std::max(2, atoi(e));
   if (const char *e = getenv("RQ_MRHS_TILE")) p.mrhs_tile = std::max(2, std::min(4096, atoi(e)));
@@ -1303,6 +1314,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     // 6. apply layout
     const int S = p.tile_leaves;
     LayoutCtx lc{S,
+                 p.tile_height,
                  boff,
                  noff,
                  node_body.as<int32_t>(),
@@ -1502,7 +1514,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       if (n_part > 0) k_write_nodes<<<nblk(n_part), NT, 0, s>>>(wc, n_part);
       if (nc) k_write_perm<<<(unsigned)nc, 128, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, p.perm.as<int32_t>(),
                                                   leaf_id.as<int32_t>(), noff, p.parent.as<int32_t>(),
-                                                  p.start.as<int32_t>(), p.stop.as<int32_t>(), S,
+                                                  is_top.as<int32_t>(),
                                                   p.blob.as<uint8_t>());
       p.tiles.alloc(std::max<int64_t>(p.n_tiles, 1) * sizeof(TileDesc));
       k_tile_desc<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
@@ -1519,9 +1531,18 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       std::vector<int64_t> topbodies;
       std::vector<int32_t> smalls;
       std::vector<int32_t> topbody_idx(m, -1);
+      // bodies with a top tree: their root is a top node (more than S beads, or taller
+      // than the tile height cut)
+      std::vector<int32_t> root_top(m, 0);
+      {
+        DBuf rt;
+        rt.alloc(m * 4);
+        k_root_is_top<<<nblk(m), NT, 0, s>>>(is_top.as<int32_t>(), boff, noff, m, rt.as<int32_t>());
+        d2h(root_top.data(), rt.p, m, s);
+      }
       for (int64_t j = 0; j < m; j++) {
         int64_t n = offsets[j + 1] - offsets[j];
-        if (n > S) { topbody_idx[j] = (int32_t)topbodies.size(); topbodies.push_back(j); }
+        if (root_top[j]) { topbody_idx[j] = (int32_t)topbodies.size(); topbodies.push_back(j); }
         if (n == 1) smalls.push_back((int32_t)j);
       }
       p.n_topbodies = (int64_t)topbodies.size();
