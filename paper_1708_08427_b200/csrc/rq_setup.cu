@@ -1648,6 +1648,21 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         }
         p.n_topblob = (int64_t)small_tb.size();
         p.n_topbig = (int64_t)big_tb.size();
+        if (getenv("RQ_VERBOSE")) {
+          int mx_nn = 0, mx_nl = 0;
+          double s_nn = 0, s_nl = 0;
+          for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
+            const int nn = h_toplvl[h_lvl[bi + 1]] - h_toplvl[h_lvl[bi]], nl = h_lvl[bi + 1] - h_lvl[bi];
+            mx_nn = std::max(mx_nn, nn), mx_nl = std::max(mx_nl, nl), s_nn += nn, s_nl += nl;
+          }
+          fprintf(stderr, "[rq] top trees: %lld bodies, nodes mean %.1f max %d, levels mean %.1f max %d; staged %lld "
+                  "(classes %lld/%lld/%lld/%lld, smem %lld/%lld/%lld/%lld), global %lld\n",
+                  (long long)p.n_topbodies, s_nn / std::max<int64_t>(1, p.n_topbodies), mx_nn,
+                  s_nl / std::max<int64_t>(1, p.n_topbodies), mx_nl, (long long)p.n_topblob,
+                  (long long)p.topclass_count[0], (long long)p.topclass_count[1], (long long)p.topclass_count[2],
+                  (long long)p.topclass_count[3], (long long)p.topclass_smem[0], (long long)p.topclass_smem[1],
+                  (long long)p.topclass_smem[2], (long long)p.topclass_smem[3], (long long)p.n_topbig);
+        }
         auto firsts = [&](const std::vector<int32_t> &list, std::vector<int64_t> &out) {
           out.assign(m + 1, (int64_t)list.size());
           for (int64_t i = (int64_t)list.size() - 1; i >= 0; i--) out[topbodies[list[i]]] = i;
