@@ -517,14 +517,14 @@ constexpr int PACK_SEG = 256;
 __global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, const int32_t *seg_body,
                        const int64_t *bead_off, int64_t nseg, ChunkLimits lim, int pass, const int64_t *chunk_base,
                        const int32_t *big_scan, int64_t *n_chunks_seg, ChunkDesc *chunks,
-                       int64_t *chunk_of_tile, int32_t *res_local_of_tile) {
+                       int64_t *chunk_of_tile, int32_t *res_local_of_tile, int32_t *bead_local_of_tile) {
   const int64_t sg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (sg >= nseg) return;
   const int64_t j = seg_body[sg];
   int64_t tb = seg_tile_begin[sg], te = seg_tile_begin[sg + 1];
   int64_t nch = 0;
   bool open = false;
-  int bead0 = 0, nodes = 0, H = 0, res = 0, ntiles = 0;
+  int beads = 0, nodes = 0, H = 0, res = 0, ntiles = 0;
   int64_t rec = 0, tile0 = 0;
   auto flush = [&]() {
     if (!open) return;
@@ -535,7 +535,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, cons
       d.n_levels = H;
       d.n_tiles = ntiles;
       d.body = (int32_t)j;
-      d.bead_begin = bead_off[j] + bead0;
+      d.bead_begin = bead_off[j];  // the chunk's beads are its tiles' beads, in tile order
       d.body_bead0 = bead_off[j];
       d.spec_full = 3 * bead_off[j] + 6;
       d.spec_comp = 3 * bead_off[j] - 6 * j;
@@ -544,51 +544,40 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, cons
       d.n_res = res;
       d.off_meta = (int32_t)head_bytes(ntiles, H);
       d.off_perm = (int32_t)(d.off_meta + meta_bytes(nodes));
-      // n_beads, off_rec and blob_bytes set by the caller below
+      d.n_beads = beads;
+      d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(beads));
+      d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, beads, rec, ntiles);
     }
     nch++;
     open = false;
   };
-  int last_stop = 0;
   for (int64_t t = tb; t < te; t++) {
     const TileTmp &T = tiles[t];
     if (!T.big) continue;
     int Tn = T.L - 1, Tres = 3 * T.L - 6;
     if (open) {
-      int beads2 = T.start + T.L - bead0;
+      int beads2 = beads + T.L;
       int nodes2 = nodes + Tn, H2 = max(H, T.height), res2 = res + Tres;
       int64_t rec2 = rec + T.rec_doubles;
       if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res || ntiles + 1 > lim.max_tiles ||
-          blob_bytes_of(H2, nodes2, beads2, rec2, ntiles + 1) > lim.max_bytes) {
-        if (pass == 1) {
-          ChunkDesc &d = chunks[chunk_base[sg] + nch];
-          d.n_beads = last_stop - bead0;
-          d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(d.n_beads));
-          d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec, ntiles);
-        }
+          blob_bytes_of(H2, nodes2, beads2, rec2, ntiles + 1) > lim.max_bytes)
         flush();
-      }
     }
     if (!open) {
       open = true;
-      bead0 = T.start; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; tile0 = t;
+      beads = 0; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; tile0 = t;
     }
     if (pass == 1) {
       chunk_of_tile[t] = chunk_base[sg] + nch;
       res_local_of_tile[t] = res;
+      bead_local_of_tile[t] = beads;
     }
     nodes += Tn;
     H = max(H, T.height);
     res += Tres;
     rec += T.rec_doubles;
     ntiles++;
-    last_stop = T.start + T.L;
-  }
-  if (open && pass == 1) {
-    ChunkDesc &d = chunks[chunk_base[sg] + nch];
-    d.n_beads = last_stop - bead0;
-    d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(d.n_beads));
-    d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, d.n_beads, rec, ntiles);
+    beads += T.L;
   }
   flush();
   if (pass == 0) n_chunks_seg[sg] = nch;
@@ -667,7 +656,7 @@ struct WriteCtx {
   const int32_t *vals;
   const int32_t *slot_of, *tile_of, *left, *right;
   const TileTmp *tiles;
-  const int32_t *res_local_of_tile;
+  const int32_t *res_local_of_tile, *bead_local_of_tile;
   const ChunkDesc *chunks;
   const int64_t *lvl_base;
   const LevelDesc *lvl;
@@ -690,7 +679,9 @@ __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
   int cs = flag_case(f);
   int j = d.body;
   int64_t nb = w.c.node_off[j];
-  int local0 = (int)(d.bead_begin - w.c.bead_off[j]);  // body-local bead index of chunk bead 0
+  const int tile_idx = w.tile_of[g];
+  const TileTmp &T = w.tiles[tile_idx];
+  const int local0 = T.start - w.bead_local_of_tile[tile_idx];  // chunk bead i <-> body bead local0 + i within the tile
   int l = w.left[g], r = w.right[g];
   int xi = l, yi = r;
   if (flag_swapped(f)) { xi = r; yi = l; }
@@ -702,8 +693,6 @@ __global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
   NodeMeta md;
   md.x = enc(xi);
   md.y = enc(yi);
-  const TileTmp &T = w.tiles[w.tile_of[g]];
-  int tile_idx = w.tile_of[g];
   md.res = (uint16_t)(w.res_local_of_tile[tile_idx] + (w.c.res_off[g] - 6 - T.res_q));
   // bits 0-5: case | swapped | signs; bits 6-15: chunk-local tile index (upward residue stores)
   md.flags = (uint16_t)(f | ((w.big_scan[tile_idx] - d.tile_begin) << 6));
@@ -732,21 +721,24 @@ __global__ void k_root_is_top(const int32_t *is_top, const int64_t *bead_off, co
   out[j] = is_top[node_off[j] + 2 * n - 2];
 }
 
-__global__ void k_write_perm(const ChunkDesc *chunks, int64_t nc, const int32_t *perm,
-                             const int32_t *leaf_id, const int64_t *node_off, const int32_t *parent,
-                             const int32_t *is_top, uint8_t *blob) {
-  int64_t c = blockIdx.x;
-  if (c >= nc) return;
-  const ChunkDesc &d = chunks[c];
-  int64_t nb = node_off[d.body];
-  uint32_t *P = reinterpret_cast<uint32_t *>(blob + d.blob_off + d.off_perm);
-  for (int i = threadIdx.x; i < d.n_beads; i += blockDim.x) {
-    int64_t gb = d.bead_begin + i;
-    int lf = leaf_id[gb];
-    int p = parent[nb + lf];
-    bool foreign = p >= 0 && is_top[nb + p];  // singleton tile: the bead's parent is a top node
-    P[i] = (uint32_t)perm[gb] | (foreign ? PERM_FOREIGN : 0u);
-  }
+// chunk perm: one thread per tile writes its beads' body-local original indices
+__global__ void k_write_perm(const TileTmp *tiles, int64_t n_tiles_all, const int64_t *chunk_of_tile,
+                             const int32_t *bead_local_of_tile, const ChunkDesc *chunks, const int32_t *perm,
+                             const int64_t *bead_off, uint8_t *blob) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_tiles_all) return;
+  const TileTmp &T = tiles[t];
+  if (!T.big) return;
+  const ChunkDesc &d = chunks[chunk_of_tile[t]];
+  uint32_t *P = reinterpret_cast<uint32_t *>(blob + d.blob_off + d.off_perm) + bead_local_of_tile[t];
+  const int64_t gb = bead_off[T.body] + T.start;
+  for (int i = 0; i < T.L; i++) P[i] = (uint32_t)perm[gb + i];
+}
+
+// tile renumbering after the per-body height sort
+__global__ void k_remap_tiles(int32_t *tile_of, int64_t NN, const int32_t *inv) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < NN && tile_of[g] >= 0) tile_of[g] = inv[tile_of[g]];
 }
 
 __global__ void k_tile_desc(const TileTmp *tiles, int64_t n_tiles_all, const int32_t *big_scan,
@@ -1374,6 +1366,37 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         while (t < n_tiles_all && htiles[t].body == j) t++;
       }
       body_tile_begin[m] = n_tiles_all;
+      // Chunks sweep their tiles level by level, so a chunk costs as many level steps as
+      // its tallest tile.  Ordering each body's tiles by height (stable counting sort)
+      // packs tiles of equal height together and cuts the nearly empty upper steps.
+      const char *es = getenv("RQ_TILE_SORT");
+      if (!(es && atoi(es) == 0) && n_tiles_all > 0) {
+        std::vector<int32_t> inv(n_tiles_all);
+        std::vector<TileTmp> sorted(n_tiles_all);
+        std::vector<int64_t> cnt;
+        for (int64_t j = 0; j < m; j++) {
+          const int64_t t0 = body_tile_begin[j], t1 = body_tile_begin[j + 1];
+          int hmax = 0;
+          for (int64_t i = t0; i < t1; i++) hmax = std::max(hmax, htiles[i].height);
+          const bool desc = es && atoi(es) == 2;
+          auto key = [&](int64_t i) { return desc ? hmax - htiles[i].height : htiles[i].height; };
+          cnt.assign(hmax + 2, 0);
+          for (int64_t i = t0; i < t1; i++) cnt[key(i) + 1]++;
+          for (int h = 0; h <= hmax; h++) cnt[h + 1] += cnt[h];
+          for (int64_t i = t0; i < t1; i++) {
+            const int64_t k = t0 + cnt[key(i)]++;
+            sorted[k] = htiles[i];
+            inv[i] = (int32_t)k;
+          }
+        }
+        htiles.swap(sorted);
+        RQ_CUDA(cudaMemcpyAsync(tiles_tmp.p, htiles.data(), n_tiles_all * sizeof(TileTmp), cudaMemcpyHostToDevice, s));
+        DBuf d_inv;
+        d_inv.alloc(n_tiles_all * 4);
+        RQ_CUDA(cudaMemcpyAsync(d_inv.p, inv.data(), n_tiles_all * 4, cudaMemcpyHostToDevice, s));
+        k_remap_tiles<<<nblk(NN), NT, 0, s>>>(tile_of.as<int32_t>(), NN, d_inv.as<int32_t>());
+        RQ_CUDA(cudaStreamSynchronize(s));
+      }
       for (int64_t i = 0; i < n_tiles_all; i++) big_scan[i + 1] = big_scan[i] + htiles[i].big;
     }
     p.n_tiles = big_scan[n_tiles_all];
@@ -1386,10 +1409,16 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
     // a single worst-case tile (all GENERAL nodes) must fit a chunk
     lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
+    // With height-sorted tiles a chunk can collect many small tiles; capping beads and
+    // tiles per chunk bounds the largest staging buffers (they size every CTA's shared
+    // memory), which keeps four downward chunk CTAs resident per SM (cfg2: 55.5 KB).
     lim.max_nodes = 1024;
-    lim.max_beads = 1024;
+    lim.max_beads = 5 * S;
     lim.max_res = 3 * 1024;
-    lim.max_tiles = 64;
+    lim.max_tiles = 14;
+    if (const char *e = getenv("RQ_CHUNK_MAX_TILES")) lim.max_tiles = std::max(1, std::min(64, atoi(e)));
+    if (const char *e = getenv("RQ_CHUNK_MAX_BEADS")) lim.max_beads = std::max(S, std::min(1024, atoi(e)));
+    if (const char *e = getenv("RQ_CHUNK_MAX_NODES")) lim.max_nodes = std::max(S, std::min(1024, atoi(e)));
     std::vector<int64_t> seg_tile_begin;
     std::vector<int32_t> seg_body;
     for (int64_t j = 0; j < m; j++)
@@ -1407,14 +1436,15 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     DBuf nch_seg, chunk_base;
     nch_seg.alloc(std::max<int64_t>(nseg, 1) * 8);
     chunk_base.alloc((nseg + 1) * 8);
-    DBuf chunk_of_tile, res_local_of_tile;
+    DBuf chunk_of_tile, res_local_of_tile, bead_local_of_tile;
     chunk_of_tile.alloc(n_tiles_all * 8);
     res_local_of_tile.alloc(n_tiles_all * 4);
+    bead_local_of_tile.alloc(n_tiles_all * 4);
     p.n_chunks = 0;
     if (nseg) {
       k_pack<<<nblk(nseg, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_seg_tb.as<int64_t>(), d_seg_body.as<int32_t>(),
                                               boff, nseg, lim, 0, nullptr, d_big_scan.as<int32_t>(),
-                                              nch_seg.as<int64_t>(), nullptr, nullptr, nullptr);
+                                              nch_seg.as<int64_t>(), nullptr, nullptr, nullptr, nullptr);
       exclusive_scan(nch_seg.as<int64_t>(), chunk_base.as<int64_t>(), nseg, s);
       p.n_chunks = d2h1<int64_t>(chunk_base.as<int64_t>() + nseg - 1, s) + d2h1<int64_t>(nch_seg.as<int64_t>() + nseg - 1, s);
     }
@@ -1424,7 +1454,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       k_pack<<<nblk(nseg, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_seg_tb.as<int64_t>(), d_seg_body.as<int32_t>(),
                                               boff, nseg, lim, 1, chunk_base.as<int64_t>(), d_big_scan.as<int32_t>(),
                                               nch_seg.as<int64_t>(), p.chunks.as<ChunkDesc>(),
-                                              chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>());
+                                              chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>(),
+                                              bead_local_of_tile.as<int32_t>());
     const int64_t nc = p.n_chunks;
     DBuf cbytes, cnodes, clevels, bytes_scan, node_scan, lvl_base;
     cbytes.alloc(nc * 8);
@@ -1457,6 +1488,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.max_chunk_tiles = std::max(p.max_chunk_tiles, d.n_tiles);
         p.max_head_bytes = std::max<int64_t>(p.max_head_bytes, d.off_rec);
       }
+      if (getenv("RQ_VERBOSE"))
+        fprintf(stderr, "[rq] chunks: %lld, level steps %lld (mean %.2f), tiles %lld, blob %.1f MB\n", (long long)nc,
+                (long long)n_lvl, nc ? (double)n_lvl / nc : 0.0, (long long)p.n_tiles, p.blob_bytes / 1e6);
       p.h_chunk_first.assign(m + 1, nc);
       for (int64_t c = nc - 1; c >= 0; c--) p.h_chunk_first[hc[c].body] = c;
       for (int64_t j = m - 1; j >= 0; j--) p.h_chunk_first[j] = std::min(p.h_chunk_first[j], p.h_chunk_first[j + 1]);
@@ -1505,6 +1539,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                   p.right.as<int32_t>(),
                   tiles_tmp.as<TileTmp>(),
                   res_local_of_tile.as<int32_t>(),
+                  bead_local_of_tile.as<int32_t>(),
                   p.chunks.as<ChunkDesc>(),
                   lvl_base.as<int64_t>(),
                   lvl.as<LevelDesc>(),
@@ -1512,10 +1547,10 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                   p.blob.as<uint8_t>(),
                   d_big_scan.as<int32_t>()};
       if (n_part > 0) k_write_nodes<<<nblk(n_part), NT, 0, s>>>(wc, n_part);
-      if (nc) k_write_perm<<<(unsigned)nc, 128, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, p.perm.as<int32_t>(),
-                                                  leaf_id.as<int32_t>(), noff, p.parent.as<int32_t>(),
-                                                  is_top.as<int32_t>(),
-                                                  p.blob.as<uint8_t>());
+      if (n_tiles_all)
+        k_write_perm<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all, chunk_of_tile.as<int64_t>(),
+                                                       bead_local_of_tile.as<int32_t>(), p.chunks.as<ChunkDesc>(),
+                                                       p.perm.as<int32_t>(), boff, p.blob.as<uint8_t>());
       p.tiles.alloc(std::max<int64_t>(p.n_tiles, 1) * sizeof(TileDesc));
       k_tile_desc<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
                                                     d_big_scan.as<int32_t>(), slot_of.as<int32_t>(),

@@ -7,4 +7,5 @@ from paper_1708_08427_b200.workloads import make_config  # noqa: E402
 
 pos, off = make_config(int(sys.argv[1]) if len(sys.argv) > 1 else 2, seed=1000)
 op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
-print("built")
+info = op.plan.info()
+print({k: info[k] for k in ("chunk_smem", "chunk_ctas_per_sm", "chunk_smem_bytes", "n_chunks")})
