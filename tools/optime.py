@@ -1,0 +1,31 @@
+"""Device time per application of each operator on config 2 (inputs resident)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_1708_08427_b200 as rq  # noqa: E402
+from paper_1708_08427_b200.workloads import make_config  # noqa: E402
+
+pos, off = make_config(2, seed=1000)
+N, m = int(off[-1]), len(off) - 1
+op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+v = torch.randn(3 * N, dtype=torch.float64, device="cuda")
+g = torch.randn(3 * N - 6 * m, dtype=torch.float64, device="cuda")
+for name, x in (("qtilde_v", v), ("qtilde_tv", g), ("both", None)):
+    def run():
+        if x is None:
+            op.apply("qtilde_v", v)
+            op.apply("qtilde_tv", g)
+        else:
+            op.apply(name, x)
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(50):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    print(f"{name}: {a.elapsed_time(b) / 50:.4f} ms")
