@@ -474,6 +474,8 @@ struct TileTmp {
   int64_t rec_doubles;
   int32_t res_q;     // body-relative Q~ offset of the first residue
   int32_t big;       // L >= 2
+  int32_t lvmax;     // record doubles of its widest height level
+  int32_t pad;
 };
 
 __global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const int32_t *tile_scan,
@@ -492,6 +494,15 @@ __global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const i
   T.rec_doubles = c.rec_off[g] + rec_size(flag_case(c.flags[g])) - c.rec_off[first];
   T.res_q = c.res_off[first] - 6;
   T.big = L >= 2;
+  // per-height record doubles of the tile (its nodes are contiguous in postorder)
+  int acc[64];
+  for (int h = 0; h < 64; h++) acc[h] = 0;
+  for (int64_t q = first; q <= g; q++)
+    if (nodeL(c, q) >= 2) acc[min(63, c.height[q])] += rec_size(flag_case(c.flags[q]));
+  int mx = 0;
+  for (int h = 0; h < 64; h++) mx = max(mx, acc[h]);
+  T.lvmax = mx;
+  T.pad = 0;
   tiles[t] = T;
   marker[first] = t;
 }
@@ -499,6 +510,7 @@ __global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const i
 struct ChunkLimits {
   int64_t max_bytes;
   int max_nodes, max_beads, max_res, max_tiles;
+  int max_lrec;  // bound on one level step's record doubles (sum of the tiles' widest levels)
 };
 
 __host__ __device__ inline int64_t meta_bytes(int nodes) { return ((int64_t)nodes * 8 + 15) / 16 * 16; }
@@ -524,7 +536,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, cons
   int64_t tb = seg_tile_begin[sg], te = seg_tile_begin[sg + 1];
   int64_t nch = 0;
   bool open = false;
-  int beads = 0, nodes = 0, H = 0, res = 0, ntiles = 0;
+  int beads = 0, nodes = 0, H = 0, res = 0, ntiles = 0, lrec = 0;
   int64_t rec = 0, tile0 = 0;
   auto flush = [&]() {
     if (!open) return;
@@ -556,16 +568,17 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, cons
     if (!T.big) continue;
     int Tn = T.L - 1, Tres = 3 * T.L - 6;
     if (open) {
-      int beads2 = beads + T.L;
+      int beads2 = beads + T.L, lrec2 = lrec + T.lvmax;
       int nodes2 = nodes + Tn, H2 = max(H, T.height), res2 = res + Tres;
       int64_t rec2 = rec + T.rec_doubles;
       if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res || ntiles + 1 > lim.max_tiles ||
+          lrec2 > lim.max_lrec ||
           blob_bytes_of(H2, nodes2, beads2, rec2, ntiles + 1) > lim.max_bytes)
         flush();
     }
     if (!open) {
       open = true;
-      beads = 0; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; tile0 = t;
+      beads = 0; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; lrec = 0; tile0 = t;
     }
     if (pass == 1) {
       chunk_of_tile[t] = chunk_base[sg] + nch;
@@ -578,6 +591,7 @@ __global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, cons
     rec += T.rec_doubles;
     ntiles++;
     beads += T.L;
+    lrec += T.lvmax;
   }
   flush();
   if (pass == 0) n_chunks_seg[sg] = nch;
@@ -1416,6 +1430,9 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     lim.max_beads = 5 * S;
     lim.max_res = 3 * 1024;
     lim.max_tiles = 14;
+    lim.max_lrec = 1280;  // 10 KB level-record stages
+    if (const char *e = getenv("RQ_CHUNK_MAX_LREC")) lim.max_lrec = std::max(64, atoi(e));
+    lim.max_lrec = std::max(lim.max_lrec, rec_size(GENERAL) * S / 2);  // any single tile fits
     if (const char *e = getenv("RQ_CHUNK_MAX_TILES")) lim.max_tiles = std::max(1, std::min(64, atoi(e)));
     if (const char *e = getenv("RQ_CHUNK_MAX_BEADS")) lim.max_beads = std::max(S, std::min(1024, atoi(e)));
     if (const char *e = getenv("RQ_CHUNK_MAX_NODES")) lim.max_nodes = std::max(S, std::min(1024, atoi(e)));
