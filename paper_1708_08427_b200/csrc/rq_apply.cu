@@ -110,6 +110,7 @@ struct ApplyCtx {
   int op;
   int head_bytes, lrec_bytes, max_nodes, max_beads, max_res, max_tiles;
   int pf_dist;     // L2 prefetch distance of chunk records (chunks ahead)
+  unsigned long long *ctr;  // {claim, done}: chunks are claimed dynamically (reset by the last CTA)
   long long *dbg;  // phase timers, only with -DRQ_TIMING (8 per CTA)
 };
 
@@ -334,12 +335,13 @@ __device__ __forceinline__ int level_rec_doubles(const LevelDesc &L) {
 //   * chunk k+1: vectors staged with cp.async
 //   * chunk k  : swept level by level; the records of level h+1 are TMA-copied
 //                (from L2) into the second record stage while level h runs.
-template <bool UP, int NT, bool K1>
-#ifdef RQ_MIN_BLOCKS
-__global__ void __launch_bounds__(NT, RQ_MIN_BLOCKS) k_chunk(ApplyCtx a) {
-#else
-__global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
+// 128-thread CTAs are bounded to 4 per SM (<= 128 registers): without the bound the
+// upward K = 1 specialisation takes 159 registers and drops to 3 CTAs/SM.
+#ifndef RQ_MIN_BLOCKS
+#define RQ_MIN_BLOCKS 4
 #endif
+template <bool UP, int NT, bool K1>
+__global__ void __launch_bounds__(NT, NT == 128 ? RQ_MIN_BLOCKS : 1) k_chunk(ApplyCtx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[3 + NLS];  // 0-2 heads, 3.. level-record stages
   const int tid = threadIdx.x;
@@ -357,23 +359,62 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
 #define VBUF(i) reinterpret_cast<double *>(smem + SM.o_v + (size_t)(i) * SM.v)
 #define ROOTBUF(i) reinterpret_cast<double *>(smem + SM.o_root + (size_t)(i) * SM.root)
   const int64_t K = K1 ? 1 : a.k, col = K1 ? 0 : a.col;
-  const int64_t G = gridDim.x;
-  const int64_t cnt = a.n_chunks > blockIdx.x ? (a.n_chunks - blockIdx.x + G - 1) / G : 0;
-  if (cnt == 0) return;
+  // Dynamic schedule: the producer claims chunk indices from a global counter a few
+  // iterations ahead (atomicAdd, off the critical path), so CTAs finish within about one
+  // chunk of each other (a static round robin left the slowest CTA ~12% behind the mean).
+  // s_cid[i & 15] = chunk of iteration i; s_cnt = first iteration without a chunk.
+  __shared__ long long s_cid[16];
+  __shared__ long long s_cnt;
+  int64_t n_claimed = 0, cnt_p = LLONG_MAX;  // producer's view
+  auto claim_upto = [&](int64_t i) {
+    while (n_claimed <= i && cnt_p == LLONG_MAX) {
+#ifdef RQ_STATIC_SCHED  // round robin (comparison builds)
+      const long long c = (long long)blockIdx.x + n_claimed * (long long)gridDim.x;
+#else
+      const long long c = (long long)atomicAdd(a.ctr, 1ull);
+#endif
+      if (c >= a.n_chunks) {
+        cnt_p = n_claimed;
+        s_cnt = n_claimed;
+      } else {
+        s_cid[n_claimed & 15] = c;
+        n_claimed++;
+      }
+    }
+  };
   if (tid == 0) {
     for (int i = 0; i < 3 + NLS; i++) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
+  if (tid == PROD) {
+    s_cnt = LLONG_MAX;
+    claim_upto(3 + a.pf_dist);
+  }
   __syncthreads();
+  auto finish = [&]() {  // the last CTA to finish resets the counters for a later launch
+    if (tid == PROD) {
+      __threadfence();
+      if (atomicAdd(a.ctr + 1, 1ull) == (unsigned long long)gridDim.x - 1) {
+        atomicExch(a.ctr, 0ull);
+        atomicExch(a.ctr + 1, 0ull);
+      }
+    }
+  };
+  if (*(volatile long long *)&s_cnt == 0) {
+    finish();
+    return;
+  }
   // the producer keeps the descriptors of chunks k+2 and k+3 in registers (loaded
   // one iteration before use, so no global latency sits on the critical path)
   longlong2 dk2 = make_longlong2(0, 0), dk3 = make_longlong2(0, 0);  // {blob_off, off_rec | blob_bytes << 32}
   auto ldesc = [&](int64_t k) -> longlong2 {
-    if (k >= cnt) return make_longlong2(0, 0);
-    const ChunkDesc *d = &a.chunks[blockIdx.x + k * G];
+    claim_upto(k);
+    if (k >= cnt_p) return make_longlong2(0, 0);
+    const ChunkDesc *d = &a.chunks[s_cid[k & 15]];
     return make_longlong2(d->blob_off, (long long)(uint32_t)d->off_rec | ((long long)(uint32_t)d->blob_bytes << 32));
   };
   if (tid == PROD) {
+    const int64_t cnt = cnt_p;
     for (int64_t k = 0; k < 3 && k < cnt; k++) {
       const longlong2 dd = ldesc(k);
       const unsigned hb = (unsigned)(dd.y & 0xffffffffll), rb = (unsigned)(dd.y >> 32) - hb;
@@ -401,7 +442,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
   int pf_hs = 0;     // head stage of chunk pf_k (= pf_k % 3, tracked incrementally)
   auto issue_levels = [&](int g, int64_t k_avail) {
     // issue while fewer than NLS steps are in flight beyond the current one
-    while (pf_n < g + NLS && pf_k < cnt && pf_k <= k_avail) {
+    while (pf_n < g + NLS && pf_k < cnt_p && pf_k <= k_avail) {
       const unsigned char *HB = HEAD(pf_hs);
       const ChunkDesc &nd = *reinterpret_cast<const ChunkDesc *>(HB);
       const int nH = nd.n_levels;
@@ -421,17 +462,20 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     }
   };
   if (tid == PROD) issue_levels(0, 0);
-  for (int64_t k = 0; k < cnt; k++) {
+  for (int64_t k = 0;; k++) {
+    // iteration k+1's chunk was claimed at least two CTA barriers ago
+    const int64_t cnt = *(volatile long long *)&s_cnt;
+    if (k >= cnt) break;
     const int st = (int)(k % 3), fb = (int)(k & 1);
     if (tid == PROD) {
-      if (k + 2 < cnt) {  // head of chunk k+2 (stage of chunk k-1, released at the end of k-1)
+      if (k + 2 < cnt_p) {  // head of chunk k+2 (stage of chunk k-1, released at the end of k-1)
         const int s2 = (int)((k + 2) % 3);
         const unsigned hb = (unsigned)(dk2.y & 0xffffffffll);
         // WAR on smem (generic reads -> TMA write) is ordered by the barrier; no proxy fence needed
         mbar_expect_tx_u(BAR(s2), hb);
         bulk_g2s_u(HEAD_U(s2), a.blob + dk2.x, hb, BAR(s2));
       }
-      if (k + a.pf_dist < cnt) {  // records of chunk k+pf_dist into L2
+      if (k + a.pf_dist < cnt_p) {  // records of chunk k+pf_dist into L2
         const unsigned hb = (unsigned)(dk3.y & 0xffffffffll), rb = (unsigned)(dk3.y >> 32) - hb;
         if (rb) prefetch_l2(a.blob + dk3.x + hb, rb);
       }
@@ -554,6 +598,7 @@ __global__ void __launch_bounds__(NT) k_chunk(ApplyCtx a) {
     __syncthreads();
     (void)to0;
   }
+  finish();
   if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 7] = clock64() - t_kernel0;
 #undef BAR
 #undef HEAD_U
@@ -1010,6 +1055,10 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   a.scratch = ss.scratch.as<double>();
   a.op = op;
   KernelCfg cfg = chunk_cfg(p, up, a);
+  if (!ss.chunk_ctr.p) {  // claim/done counters start at zero and reset themselves
+    ss.chunk_ctr.alloc(4 * sizeof(unsigned long long));
+    RQ_CUDA(cudaMemsetAsync(ss.chunk_ctr.p, 0, 4 * sizeof(unsigned long long), s));
+  }
   a.pf_dist = 1;
   if (const char *e = getenv("RQ_PF_DIST")) a.pf_dist = std::max(1, std::min(8, atoi(e)));
   static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
@@ -1085,7 +1134,10 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       }
     };
     if (up) {
-      if (do_chunks) launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
+      if (do_chunks) {
+        a.ctr = ss.chunk_ctr.as<unsigned long long>() + 2 * (ss.chunk_epoch++ & 1u);
+        launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
+      }
       if (do_top) top_pass();
       if (timing_top && do_top && p.n_topblob) {
         std::vector<long long> h((size_t)p.n_topblob * 8);
@@ -1109,7 +1161,10 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       }
     } else {
       if (do_top) top_pass();
-      if (do_chunks) launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
+      if (do_chunks) {
+        a.ctr = ss.chunk_ctr.as<unsigned long long>() + 2 * (ss.chunk_epoch++ & 1u);
+        launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
+      }
     }
     if (timing && do_chunks) {
       std::vector<long long> h((size_t)cfg.grid * 16 + 8);
@@ -1120,6 +1175,16 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f level-total %.0f | per chunk: head+vec wait %.0f, slowest-warp/step %.0f, level steps %.1f, chunks/CTA %.1f, CTA total %.0f (max %.0f)\n",
               op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[4], acc[1] / acc[4], acc[2] / acc[4], acc[3] / acc[6],
               acc[5] / acc[4], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
+      {  // load balance of the static round-robin chunk assignment
+        long long smax = 0, smin = LLONG_MAX, tmin = LLONG_MAX;
+        for (int g = 0; g < cfg.grid; g++) {
+          smax = std::max(smax, h[8 * g + 4]);
+          smin = std::min(smin, h[8 * g + 4]);
+          tmin = std::min(tmin, h[8 * g + 7]);
+        }
+        fprintf(stderr, "[rq timing] level steps per CTA: mean %.1f min %lld max %lld; CTA total cycles min %lld\n",
+                acc[4] / cfg.grid, smin, smax, tmin);
+      }
       double gs[8] = {0};
       for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) gs[i] += (double)h[8 * (cfg.grid + g) + i];
       fprintf(stderr, "[rq timing] slowest warp finish after step start, per group (avg over steps where present): GEN %.0f (%.0f) RB %.0f (%.0f) BB %.0f (%.0f) idle %.0f (%.0f)\n",

@@ -181,6 +181,8 @@ struct Plan {
   // owned per stream.
   struct StreamState {
     DBuf scratch, mrhs_scratch, top_cnt;
+    DBuf chunk_ctr;           // 2 x {claim, done} counters of the dynamic chunk schedule
+    uint32_t chunk_epoch = 0;  // chunk launches so far (consecutive launches alternate counters)
   };
   mutable std::mutex state_mu;
   mutable std::map<cudaStream_t, std::unique_ptr<StreamState>> stream_state;
