@@ -23,7 +23,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rq_lq.cuh"
@@ -362,81 +364,104 @@ __device__ inline void load_child(const FactorCtx &c, int64_t nb, int64_t base, 
   h = __ldcg(&c.height[g]);
 }
 
-__global__ void k_factor(FactorCtx c, int64_t N) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  int j = c.body_of[i];
-  int64_t base = c.bead_off[j], nb = c.node_off[j];
-  int x = c.parent[nb + c.leaf_id[i]];
-  while (x >= 0) {
-    int64_t g = nb + x;
-    __threadfence();
-    if (atomicAdd(&c.counter[g], 1) == 0) return;
-    __threadfence();
-    int l = c.left[g], r = c.right[g];
-    double cl[3], cr[3], tl[9], tr[9];
-    int nl, nr, hl, hr;
-    load_child(c, nb, base, l, cl, tl, nl, hl);
-    load_child(c, nb, base, r, cr, tr, nr, hr);
-    int n = nl + nr;
-    double cp[3];
-    for (int a = 0; a < 3; a++)  // tree.py:126
-      cp[a] = ((double)nl * cl[a] + (double)nr * cr[a]) / (double)n;
-    double t6[6];
-    unsigned signs = 0;
-    int cs = flag_case(c.flags[g]);
-    double *rec = c.rec + c.rec_off[g];
-    if (cs == BEAD_BEAD) {  // factor.py:224-225
-      double d[3];
-      for (int a = 0; a < 3; a++) d[a] = c.pos_tree[(base + c.start[nb + l]) * 3 + a] - cp[a];
-      double gm[9];
-      factor_bead_bead(d, t6, gm);
-      for (int a = 0; a < 9; a++) rec[a] = gm[a];
-    } else if (cs == RIGID_BEAD) {  // factor.py:226-236, 171-178
-      bool sw = nl == 1;
-      const double *cg = sw ? cr : cl;
-      const double *tg = sw ? tr : tl;
-      int nx = sw ? nr : nl;
-      double dr[3], R[9];
-      for (int a = 0; a < 3; a++) dr[a] = cg[a] - cp[a];
-      skew3(dr, R);
-      double sc = sqrt((double)((int64_t)nx * n));
-      double cpl[18];
-      for (int a = 0; a < 3; a++)
-        for (int b = 0; b < 3; b++) {
-          cpl[a * 6 + b] = tg[a * 3 + b];
-          cpl[a * 6 + 3 + b] = sc * R[a * 3 + b];
-        }
-      double wy[WY<6>::SIZE];
-      lq_factor<6>(cpl, t6, wy, signs);
-      for (int a = 0; a < WY<6>::RA; a++) rec[a] = wy[a];
-      rec[WY<6>::RA] = sqrt((double)nx / (double)n);  // NodeFactor.ratios (factor.py:85-87)
-      rec[WY<6>::RB] = sqrt(1.0 / (double)n);
-    } else {  // factor.py:237-243, 181-188
-      double dr[3], R[9];
-      for (int a = 0; a < 3; a++) dr[a] = cl[a] - cp[a];
-      skew3(dr, R);
-      double sc = sqrt((double)((int64_t)nl * n) / (double)nr);
-      double cpl[27];
-      for (int a = 0; a < 3; a++)
-        for (int b = 0; b < 3; b++) {
-          cpl[a * 9 + b] = tl[a * 3 + b];
-          cpl[a * 9 + 3 + b] = tr[a * 3 + b];
-          cpl[a * 9 + 6 + b] = sc * R[a * 3 + b];
-        }
-      double wy[WY<9>::SIZE];
-      lq_factor<9>(cpl, t6, wy, signs);
-      for (int a = 0; a < WY<9>::RA; a++) rec[a] = wy[a];
-      rec[WY<9>::RA] = sqrt((double)nl / (double)n);
-      rec[WY<9>::RB] = sqrt((double)nr / (double)n);
-    }
-    for (int a = 0; a < 3; a++) c.centroid[g * 3 + a] = cp[a];
-    for (int a = 0; a < 6; a++) c.t22[g * 6 + a] = t6[a];
-    c.height[g] = max(hl, hr) + 1;
-    c.flags[g] = (uint8_t)((c.flags[g] & 7u) | (signs << 3));
-    __threadfence();
-    x = c.parent[g];
+// One internal node (factor_all's per-node dispatch, factor.py:217-243); its children are done.
+__device__ __forceinline__ void factor_node(const FactorCtx &c, int64_t base, int64_t nb, int64_t g) {
+  int l = c.left[g], r = c.right[g];
+  double cl[3], cr[3], tl[9], tr[9];
+  int nl, nr, hl, hr;
+  load_child(c, nb, base, l, cl, tl, nl, hl);
+  load_child(c, nb, base, r, cr, tr, nr, hr);
+  int n = nl + nr;
+  double cp[3];
+  for (int a = 0; a < 3; a++)  // tree.py:126
+    cp[a] = ((double)nl * cl[a] + (double)nr * cr[a]) / (double)n;
+  double t6[6];
+  unsigned signs = 0;
+  int cs = flag_case(c.flags[g]);
+  double *rec = c.rec + c.rec_off[g];
+  if (cs == BEAD_BEAD) {  // factor.py:224-225
+    double d[3];
+    for (int a = 0; a < 3; a++) d[a] = c.pos_tree[(base + c.start[nb + l]) * 3 + a] - cp[a];
+    double gm[9];
+    factor_bead_bead(d, t6, gm);
+    for (int a = 0; a < 9; a++) rec[a] = gm[a];
+  } else if (cs == RIGID_BEAD) {  // factor.py:226-236, 171-178
+    bool sw = nl == 1;
+    const double *cg = sw ? cr : cl;
+    const double *tg = sw ? tr : tl;
+    int nx = sw ? nr : nl;
+    double dr[3], R[9];
+    for (int a = 0; a < 3; a++) dr[a] = cg[a] - cp[a];
+    skew3(dr, R);
+    double sc = sqrt((double)((int64_t)nx * n));
+    double cpl[18];
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 3; b++) {
+        cpl[a * 6 + b] = tg[a * 3 + b];
+        cpl[a * 6 + 3 + b] = sc * R[a * 3 + b];
+      }
+    double wy[WY<6>::SIZE];
+    lq_factor<6>(cpl, t6, wy, signs);
+    for (int a = 0; a < WY<6>::RA; a++) rec[a] = wy[a];
+    rec[WY<6>::RA] = sqrt((double)nx / (double)n);  // NodeFactor.ratios (factor.py:85-87)
+    rec[WY<6>::RB] = sqrt(1.0 / (double)n);
+  } else {  // factor.py:237-243, 181-188
+    double dr[3], R[9];
+    for (int a = 0; a < 3; a++) dr[a] = cl[a] - cp[a];
+    skew3(dr, R);
+    double sc = sqrt((double)((int64_t)nl * n) / (double)nr);
+    double cpl[27];
+    for (int a = 0; a < 3; a++)
+      for (int b = 0; b < 3; b++) {
+        cpl[a * 9 + b] = tl[a * 3 + b];
+        cpl[a * 9 + 3 + b] = tr[a * 3 + b];
+        cpl[a * 9 + 6 + b] = sc * R[a * 3 + b];
+      }
+    double wy[WY<9>::SIZE];
+    lq_factor<9>(cpl, t6, wy, signs);
+    for (int a = 0; a < WY<9>::RA; a++) rec[a] = wy[a];
+    rec[WY<9>::RA] = sqrt((double)nl / (double)n);
+    rec[WY<9>::RB] = sqrt((double)nr / (double)n);
   }
+  for (int a = 0; a < 3; a++) c.centroid[g * 3 + a] = cp[a];
+  for (int a = 0; a < 6; a++) c.t22[g * 6 + a] = t6[a];
+  c.height[g] = max(hl, hr) + 1;
+  c.flags[g] = (uint8_t)((c.flags[g] & 7u) | (signs << 3));
+}
+
+// Internal nodes are factored level by level, deepest ghost depth first (a child's depth
+// always exceeds its parent's, tree.py:116-123), each level's nodes ordered by case so the
+// warps run one LQ shape (GEN 3x9, RB 3x6, BB closed form) without divergence.
+// Sort key: (1023 - depth) << 2 | case rank; leaves get level 1024 (sorted last, skipped).
+__global__ void k_factor_keys(const uint8_t *flags, const int32_t *start, const int32_t *stop,
+                              const int16_t *depth, int64_t NN, uint32_t *key, int32_t *val) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN) return;
+  uint32_t k = 1024u << 2;
+  if (stop[g] - start[g] >= 2) {
+    const int cs = flag_case(flags[g]);
+    const uint32_t rank = cs == GENERAL ? 0u : (cs == RIGID_BEAD ? 1u : 2u);
+    k = ((uint32_t)(1023 - min(1023, (int)depth[g])) << 2) | rank;
+  }
+  key[g] = k;
+  val[g] = (int32_t)g;
+}
+
+// first sorted position of every depth-level key (bnd[L] for L = key >> 2; bnd sized 1025)
+__global__ void k_level_bounds(const uint32_t *key, int64_t n, int32_t *bnd) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t L = key[i] >> 2;
+  if (L > 1023u) return;
+  if (i == 0 || (key[i - 1] >> 2) != L) bnd[L] = (int32_t)i;
+}
+
+__global__ void k_factor_level(FactorCtx c, const int32_t *order, const int32_t *node_body, int64_t b, int64_t e) {
+  const int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= e) return;
+  const int64_t g = order[i];
+  const int j = node_body[g];
+  factor_node(c, c.bead_off[j], c.node_off[j], g);
 }
 
 // ---- 6. apply layout ------------------------------------------------------------
@@ -750,6 +775,30 @@ __global__ void k_write_perm(const TileTmp *tiles, int64_t n_tiles_all, const in
 }
 
 // tile renumbering after the per-body height sort
+__global__ void k_tile_keys(const TileTmp *tiles, int64_t n, bool desc, uint64_t *key, int32_t *val) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t h = (uint32_t)min(tiles[t].height, 0xffff);
+  key[t] = ((uint64_t)tiles[t].body << 16) | (desc ? 0xffffu - h : h);
+  val[t] = (int32_t)t;
+}
+
+__global__ void k_tile_permute(const TileTmp *tiles, const int32_t *order, int64_t n, TileTmp *sorted, int32_t *inv) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t t = order[k];
+  sorted[k] = tiles[t];
+  inv[t] = (int32_t)k;
+}
+
+// big flag per tile; first tile of each body (tiles are grouped by body)
+__global__ void k_tile_flags(const TileTmp *tiles, int64_t n, int32_t *big, int64_t *body_begin) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  big[t] = tiles[t].big ? 1 : 0;
+  if (t == 0 || tiles[t - 1].body != tiles[t].body) body_begin[tiles[t].body] = t;
+}
+
 __global__ void k_remap_tiles(int32_t *tile_of, int64_t NN, const int32_t *inv) {
   int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g < NN && tile_of[g] >= 0) tile_of[g] = inv[tile_of[g]];
@@ -952,6 +1001,68 @@ __global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *topbod
 
 // ---- helpers ------------------------------------------------------------------------
 
+// node count per case (flags & 3), grid-stride with a shared-memory histogram
+__global__ void k_case_count(const uint8_t *flags, int64_t NN, unsigned long long *cnt) {
+  __shared__ unsigned int h[4];
+  if (threadIdx.x < 4) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < NN; g += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[flags[g] & 3], 1u);
+  __syncthreads();
+  if (threadIdx.x < 4) atomicAdd(&cnt[threadIdx.x], (unsigned long long)h[threadIdx.x]);
+}
+
+// Host -> device copy of a (possibly pageable) host array.  Pageable cudaMemcpyAsync runs
+// at ~8 GB/s on the B200 hosts; here RQ_H2D_THREADS host threads memcpy 4 MiB pieces into
+// their own pair of pinned slots and queue the DMA of each piece on the stream, so host
+// copies and PCIe transfers overlap.  Pinned (page-locked / registered) sources and small
+// arrays take the plain path.  The slots are allocated once per process.
+void h2d_host(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  constexpr size_t C = size_t(4) << 20;
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // clear a possible error from the attribute query on plain malloc'd memory
+  int T = 4;
+  if (const char *e = getenv("RQ_H2D_THREADS")) T = std::max(0, std::min(16, atoi(e)));
+  if (pinned || bytes < 4 * C || T == 0) {
+    RQ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  static std::mutex mu;
+  static std::vector<void *> slot;
+  static std::vector<cudaEvent_t> ev;
+  std::lock_guard<std::mutex> lock(mu);
+  while ((int)slot.size() < 2 * T) {
+    void *h = nullptr;
+    cudaEvent_t e;
+    RQ_CUDA(cudaHostAlloc(&h, C, cudaHostAllocPortable));
+    RQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    RQ_CUDA(cudaEventRecord(e, s));
+    slot.push_back(h);
+    ev.push_back(e);
+  }
+  const size_t pieces = (bytes + C - 1) / C;
+  std::vector<std::thread> th;
+  std::vector<int> fail(T, 0);
+  for (int t = 0; t < T; t++) {
+    th.emplace_back([&, t]() {
+      int use = 0;  // thread t owns slots 2t and 2t+1
+      for (size_t i = (size_t)t; i < pieces; i += (size_t)T, use ^= 1) {
+        const int sl = 2 * t + use;
+        const size_t off = i * C, len = std::min(C, bytes - off);
+        if (cudaEventSynchronize(ev[sl]) != cudaSuccess) { fail[t] = 1; return; }
+        memcpy(slot[sl], (const char *)src + off, len);
+        if (cudaMemcpyAsync((char *)dst + off, slot[sl], len, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaEventRecord(ev[sl], s) != cudaSuccess) { fail[t] = 1; return; }
+      }
+    });
+  }
+  for (auto &x : th) x.join();
+  for (int t = 0; t < T; t++)
+    if (fail[t]) throw Error(RQ_ERR_CUDA, "staged host-to-device copy failed");
+  // the slots are reused by the next call only after their events complete
+}
+
 template <class T>
 void d2h(T *dst, const void *src, size_t count, cudaStream_t s) {
   RQ_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -1148,8 +1259,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
   RQ_CUDA(cudaMemcpyAsync(p.bead_off_d.p, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, s));
   RQ_CUDA(cudaMemcpyAsync(p.node_off_d.p, node_off.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
   p.pos_orig.alloc(N * 24);
-  RQ_CUDA(cudaMemcpyAsync(p.pos_orig.p, pos_in, N * 24,
-                          host_input ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  if (host_input) h2d_host(p.pos_orig.p, pos_in, N * 24, s);
+  else RQ_CUDA(cudaMemcpyAsync(p.pos_orig.p, pos_in, N * 24, cudaMemcpyDeviceToDevice, s));
   p.err.alloc(8 * 8);
   {
     long long init[8] = {0x7fffffffffffffffLL, 0, 0, 0, 0, 0, 0, 0};
@@ -1292,8 +1403,6 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     RQ_CUDA(cudaMemsetAsync(p.t22.p, 0, NN * 48, s));
     {
       DBuf counter;
-      counter.alloc(NN * 4);
-      RQ_CUDA(cudaMemsetAsync(counter.p, 0, NN * 4, s));
       FactorCtx fc{boff,
                    noff,
                    p.body_of.as<int32_t>(),
@@ -1311,7 +1420,33 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                    p.centroid.as<double>(),
                    p.t22.as<double>(),
                    p.rec.as<double>()};
-      k_factor<<<nblk(N, 128), 128, 0, s>>>(fc, N);
+      // level order: sort internal nodes by (deepest first, case), one launch per level
+      DBuf fkey, fval, fkey2, fval2, bnd;
+      fkey.alloc(NN * 4);
+      fval.alloc(NN * 4);
+      fkey2.alloc(NN * 4);
+      fval2.alloc(NN * 4);
+      bnd.alloc(1025 * 4);
+      k_factor_keys<<<nblk(NN), NT, 0, s>>>(p.flags.as<uint8_t>(), p.start.as<int32_t>(), p.stop.as<int32_t>(),
+                                             p.depth.as<int16_t>(), NN, fkey.as<uint32_t>(), fval.as<int32_t>());
+      size_t tb = 0;
+      RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, fkey.as<uint32_t>(), fkey2.as<uint32_t>(),
+                                              fval.as<int32_t>(), fval2.as<int32_t>(), (int)NN, 0, 13, s));
+      DBuf tmp;
+      tmp.alloc(tb);
+      RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, fkey.as<uint32_t>(), fkey2.as<uint32_t>(),
+                                              fval.as<int32_t>(), fval2.as<int32_t>(), (int)NN, 0, 13, s));
+      RQ_CUDA(cudaMemsetAsync(bnd.p, 0xff, 1025 * 4, s));
+      k_level_bounds<<<nblk(NN), NT, 0, s>>>(fkey2.as<uint32_t>(), NN, bnd.as<int32_t>());
+      std::vector<int32_t> hb(1024);
+      d2h(hb.data(), bnd.as<int32_t>(), 1024, s);
+      std::vector<int64_t> lv;
+      for (int L = 0; L < 1024; L++)
+        if (hb[L] >= 0) lv.push_back(hb[L]);
+      lv.push_back(n_internal);
+      for (size_t i = 0; i + 1 < lv.size(); i++)
+        k_factor_level<<<nblk(lv[i + 1] - lv[i], 128), 128, 0, s>>>(fc, fval2.as<int32_t>(), node_body.as<int32_t>(),
+                                                                    lv[i], lv[i + 1]);
       RQ_CUDA(cudaGetLastError());
       RQ_CUDA(cudaStreamSynchronize(s));
     }
@@ -1368,55 +1503,62 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                                              MaxOp{}, NN, s));
     }
     tm.mark("tiles");
-    // per-body tile ranges (tiles are in global postorder = body order)
-    std::vector<TileTmp> htiles(n_tiles_all);
-    d2h(htiles.data(), tiles_tmp.p, n_tiles_all, s);
+    // Chunks sweep their tiles level by level, so a chunk costs as many level steps as its
+    // tallest tile.  Ordering each body's tiles by height (stable radix sort on
+    // (body, height); tiles are in global postorder = body order) packs tiles of equal
+    // height together and cuts the nearly empty upper steps.  RQ_TILE_SORT=0 keeps
+    // postorder, =2 sorts by descending height.
     std::vector<int64_t> body_tile_begin(m + 1, 0);
-    std::vector<int32_t> big_scan(n_tiles_all + 1, 0);
-    {
-      int64_t t = 0;
-      for (int64_t j = 0; j < m; j++) {
-        body_tile_begin[j] = t;
-        while (t < n_tiles_all && htiles[t].body == j) t++;
-      }
-      body_tile_begin[m] = n_tiles_all;
-      // Chunks sweep their tiles level by level, so a chunk costs as many level steps as
-      // its tallest tile.  Ordering each body's tiles by height (stable counting sort)
-      // packs tiles of equal height together and cuts the nearly empty upper steps.
-      const char *es = getenv("RQ_TILE_SORT");
-      if (!(es && atoi(es) == 0) && n_tiles_all > 0) {
-        std::vector<int32_t> inv(n_tiles_all);
-        std::vector<TileTmp> sorted(n_tiles_all);
-        std::vector<int64_t> cnt;
-        for (int64_t j = 0; j < m; j++) {
-          const int64_t t0 = body_tile_begin[j], t1 = body_tile_begin[j + 1];
-          int hmax = 0;
-          for (int64_t i = t0; i < t1; i++) hmax = std::max(hmax, htiles[i].height);
-          const bool desc = es && atoi(es) == 2;
-          auto key = [&](int64_t i) { return desc ? hmax - htiles[i].height : htiles[i].height; };
-          cnt.assign(hmax + 2, 0);
-          for (int64_t i = t0; i < t1; i++) cnt[key(i) + 1]++;
-          for (int h = 0; h <= hmax; h++) cnt[h + 1] += cnt[h];
-          for (int64_t i = t0; i < t1; i++) {
-            const int64_t k = t0 + cnt[key(i)]++;
-            sorted[k] = htiles[i];
-            inv[i] = (int32_t)k;
-          }
-        }
-        htiles.swap(sorted);
-        RQ_CUDA(cudaMemcpyAsync(tiles_tmp.p, htiles.data(), n_tiles_all * sizeof(TileTmp), cudaMemcpyHostToDevice, s));
-        DBuf d_inv;
-        d_inv.alloc(n_tiles_all * 4);
-        RQ_CUDA(cudaMemcpyAsync(d_inv.p, inv.data(), n_tiles_all * 4, cudaMemcpyHostToDevice, s));
-        k_remap_tiles<<<nblk(NN), NT, 0, s>>>(tile_of.as<int32_t>(), NN, d_inv.as<int32_t>());
-        RQ_CUDA(cudaStreamSynchronize(s));
-      }
-      for (int64_t i = 0; i < n_tiles_all; i++) big_scan[i + 1] = big_scan[i] + htiles[i].big;
-    }
-    p.n_tiles = big_scan[n_tiles_all];
     DBuf d_big_scan;
     d_big_scan.alloc((n_tiles_all + 1) * 4);
-    RQ_CUDA(cudaMemcpyAsync(d_big_scan.p, big_scan.data(), (n_tiles_all + 1) * 4, cudaMemcpyHostToDevice, s));
+    {
+      const char *es = getenv("RQ_TILE_SORT");
+      const int mode = es ? atoi(es) : 1;
+      if (mode != 0 && n_tiles_all > 1) {
+        DBuf tkey, tval, tkey2, tval2, sorted, inv;
+        tkey.alloc(n_tiles_all * 8);
+        tval.alloc(n_tiles_all * 4);
+        tkey2.alloc(n_tiles_all * 8);
+        tval2.alloc(n_tiles_all * 4);
+        sorted.alloc(n_tiles_all * sizeof(TileTmp));
+        inv.alloc(n_tiles_all * 4);
+        k_tile_keys<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all, mode == 2,
+                                                     tkey.as<uint64_t>(), tval.as<int32_t>());
+        int end_bit = 16 + body_bits + 1;
+        size_t tb = 0;
+        RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(),
+                                                tval.as<int32_t>(), tval2.as<int32_t>(), (int)n_tiles_all, 0,
+                                                end_bit, s));
+        DBuf tmp;
+        tmp.alloc(tb);
+        RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(),
+                                                tval.as<int32_t>(), tval2.as<int32_t>(), (int)n_tiles_all, 0,
+                                                end_bit, s));
+        k_tile_permute<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), tval2.as<int32_t>(), n_tiles_all,
+                                                        sorted.as<TileTmp>(), inv.as<int32_t>());
+        RQ_CUDA(cudaMemcpyAsync(tiles_tmp.p, sorted.p, n_tiles_all * sizeof(TileTmp), cudaMemcpyDeviceToDevice, s));
+        k_remap_tiles<<<nblk(NN), NT, 0, s>>>(tile_of.as<int32_t>(), NN, inv.as<int32_t>());
+      }
+      // big-tile prefix (tile -> TileDesc index) and per-body tile ranges
+      DBuf bigf, btb;
+      bigf.alloc(std::max<int64_t>(n_tiles_all, 1) * 4);
+      btb.alloc((m + 1) * 8);
+      RQ_CUDA(cudaMemsetAsync(btb.p, 0xff, (m + 1) * 8, s));
+      k_tile_flags<<<nblk(std::max<int64_t>(n_tiles_all, 1)), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
+                                                                         bigf.as<int32_t>(), btb.as<int64_t>());
+      if (n_tiles_all) exclusive_scan(bigf.as<int32_t>(), d_big_scan.as<int32_t>(), n_tiles_all, s);
+      int32_t last[2] = {0, 0};
+      if (n_tiles_all) {
+        d2h(&last[0], d_big_scan.as<int32_t>() + n_tiles_all - 1, 1, s);
+        d2h(&last[1], bigf.as<int32_t>() + n_tiles_all - 1, 1, s);
+      }
+      p.n_tiles = (int64_t)last[0] + last[1];
+      RQ_CUDA(cudaMemcpyAsync(d_big_scan.as<int32_t>() + n_tiles_all, &p.n_tiles, 4, cudaMemcpyHostToDevice, s));
+      d2h(body_tile_begin.data(), btb.p, m + 1, s);
+      body_tile_begin[m] = n_tiles_all;
+      for (int64_t j = m - 1; j >= 0; j--)  // bodies without tiles start where the next one does
+        if (body_tile_begin[j] < 0) body_tile_begin[j] = body_tile_begin[j + 1];
+    }
 
     ChunkLimits lim;
     lim.max_bytes = 40 * 1024;
@@ -1474,6 +1616,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                                               chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>(),
                                               bead_local_of_tile.as<int32_t>());
     const int64_t nc = p.n_chunks;
+    tm.mark("pack");
     DBuf cbytes, cnodes, clevels, bytes_scan, node_scan, lvl_base;
     cbytes.alloc(nc * 8);
     cnodes.alloc(nc * 8);
@@ -1536,6 +1679,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, nkeys.as<uint64_t>(), nkeys2.as<uint64_t>(),
                                               nvals.as<int32_t>(), nvals2.as<int32_t>(), (int)NN, 0, 64, s));
       tmp.reset();
+      tm.mark("node sort");
       if (n_part > 0)
         k_slots<<<nblk(n_part), NT, 0, s>>>(nkeys2.as<uint64_t>(), nvals2.as<int32_t>(), n_part,
                                              node_scan.as<int64_t>(), slot_of.as<int32_t>(),
@@ -1830,9 +1974,14 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     tm.mark("top");
     // case counts
     {
-      std::vector<uint8_t> hf(NN);
-      d2h(hf.data(), p.flags.p, NN, s);
-      for (auto f : hf) p.n_case[f & 3]++;
+      DBuf cc;
+      cc.alloc(4 * 8);
+      RQ_CUDA(cudaMemsetAsync(cc.p, 0, 4 * 8, s));
+      k_case_count<<<(unsigned)std::min<int64_t>(nblk(NN), 4 * 148), NT, 0, s>>>(p.flags.as<uint8_t>(), NN,
+                                                                             cc.as<unsigned long long>());
+      unsigned long long hc[4];
+      d2h(hc, cc.p, 4, s);
+      for (int c = 0; c < 4; c++) p.n_case[c] = (int64_t)hc[c];
     }
     RQ_CUDA(cudaGetLastError());
     RQ_CUDA(cudaStreamSynchronize(s));
