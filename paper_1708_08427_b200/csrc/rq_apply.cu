@@ -366,12 +366,17 @@ __global__ void __launch_bounds__(NT, NT == 128 ? RQ_MIN_BLOCKS : 1) k_chunk(App
   __shared__ long long s_cid[16];
   __shared__ long long s_cnt;
   int64_t n_claimed = 0, cnt_p = LLONG_MAX;  // producer's view
+  const int64_t n_static = 4 + a.pf_dist;      // iterations claimed in the prologue
   auto claim_upto = [&](int64_t i) {
     while (n_claimed <= i && cnt_p == LLONG_MAX) {
-#ifdef RQ_STATIC_SCHED  // round robin (comparison builds)
-      const long long c = (long long)blockIdx.x + n_claimed * (long long)gridDim.x;
+      // the prologue's claims are static (round robin; 592 CTAs hitting one counter at
+      // launch would serialise ~3000 atomics), later claims come from the counter
+      const long long G0 = (long long)gridDim.x;
+#ifdef RQ_STATIC_SCHED  // round robin throughout (comparison builds)
+      const long long c = (long long)blockIdx.x + n_claimed * G0;
 #else
-      const long long c = (long long)atomicAdd(a.ctr, 1ull);
+      const long long c = n_claimed < n_static ? (long long)blockIdx.x + n_claimed * G0
+                                               : n_static * G0 + (long long)atomicAdd(a.ctr, 1ull);
 #endif
       if (c >= a.n_chunks) {
         cnt_p = n_claimed;
@@ -1236,11 +1241,15 @@ void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_
   }
   cudaStream_t s_in = p.host_stream, s_k = p.host_stream2, s_out = p.host_stream3;
   double *din = p.stage_in.as<double>(), *dout = p.stage_out.as<double>();
+  // every H2D is queued first, so the host-to-device engine never waits for the host to
+  // finish enqueueing a segment's kernels
   for (int i = 0; i < nseg; i++) {
-    const int64_t j0 = cuts[i], j1 = cuts[i + 1];
-    const int64_t r0 = rows(in_comp, j0), r1 = rows(in_comp, j1);
+    const int64_t r0 = rows(in_comp, cuts[i]), r1 = rows(in_comp, cuts[i + 1]);
     RQ_CUDA(cudaMemcpyAsync(din + r0 * k, in + r0 * k, (size_t)(r1 - r0) * k * 8, cudaMemcpyHostToDevice, s_in));
     RQ_CUDA(cudaEventRecord(ev_in[i], s_in));
+  }
+  for (int i = 0; i < nseg; i++) {
+    const int64_t j0 = cuts[i], j1 = cuts[i + 1];
     RQ_CUDA(cudaStreamWaitEvent(s_k, ev_in[i], 0));
     BodyRange br;
     br.j0 = j0;
