@@ -111,6 +111,8 @@ struct ApplyCtx {
   int head_bytes, lrec_bytes, max_nodes, max_beads, max_res, max_tiles;
   int pf_dist;     // L2 prefetch distance of chunk records (chunks ahead)
   unsigned long long *ctr;  // {claim, done}: chunks are claimed dynamically (reset by the last CTA)
+  const uint8_t *l2_next;   // upward: the staged top blobs the next kernel sweeps, prefetched into
+  int64_t l2_next_bytes;    // L2 by each CTA (a 1/grid slice) once it has no chunk left
   long long *dbg;  // phase timers, only with -DRQ_TIMING (8 per CTA)
 };
 
@@ -603,6 +605,15 @@ __global__ void __launch_bounds__(NT, NT == 128 ? RQ_MIN_BLOCKS : 1) k_chunk(App
     __syncthreads();
     (void)to0;
   }
+  if (UP && a.l2_next_bytes > 0 && tid == PROD) {
+    const int64_t per = (a.l2_next_bytes + gridDim.x - 1) / gridDim.x;
+    const int64_t b0 = (per * blockIdx.x) & ~(int64_t)15;
+    const int64_t b1 = std::min<int64_t>(a.l2_next_bytes, per * (blockIdx.x + 1));
+    for (int64_t b = b0; b < b1; b += 32768) {
+      const int64_t len = std::min<int64_t>(32768, b1 - b) & ~(int64_t)15;
+      if (len > 0) prefetch_l2(a.l2_next + b, (unsigned)len);
+    }
+  }
   finish();
   if (RQ_TIMING && a.dbg && tid == 0) a.dbg[8 * blockIdx.x + 7] = clock64() - t_kernel0;
 #undef BAR
@@ -1063,6 +1074,10 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   if (!ss.chunk_ctr.p) {  // claim/done counters start at zero and reset themselves
     ss.chunk_ctr.alloc(4 * sizeof(unsigned long long));
     RQ_CUDA(cudaMemsetAsync(ss.chunk_ctr.p, 0, 4 * sizeof(unsigned long long), s));
+  }
+  if (up && tb1 > tb0 && !getenv("RQ_NO_TOP_L2")) {  // the top pass that follows reads these blobs
+    a.l2_next = p.topblob.as<uint8_t>() + p.h_topblob_off[tb0];
+    a.l2_next_bytes = p.h_topblob_off[tb1] - p.h_topblob_off[tb0];
   }
   a.pf_dist = 1;
   if (const char *e = getenv("RQ_PF_DIST")) a.pf_dist = std::max(1, std::min(8, atoi(e)));

@@ -163,6 +163,7 @@ struct Plan {
   std::vector<int64_t> h_topstart_first;  // [m+1]
   // host-side body -> work-list ranges (segmented / pipelined applications)
   std::vector<int64_t> h_chunk_first, h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each
+  std::vector<int64_t> h_topblob_off;  // [n_topblob+1]: staged top blob byte offsets (host copy)
   DBuf err;                        // int64 [8] device error flags
   // deterministic per-body reductions (centroid, Zf): fixed segments
   int64_t n_seg = 0;

@@ -1844,6 +1844,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         }
         p.n_topblob = (int64_t)small_tb.size();
         p.n_topbig = (int64_t)big_tb.size();
+        p.h_topblob_off = small_off;
+        p.h_topblob_off.push_back(total);
         if (getenv("RQ_VERBOSE")) {
           int mx_nn = 0, mx_nl = 0;
           double s_nn = 0, s_nl = 0;
