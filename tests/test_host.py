@@ -91,7 +91,8 @@ def test_public_names_match_reference(built):
              "leaf_infoset", "merge_infosets", "split_rvset", "upward_apply", "downward_apply", "qtilde_apply",
              "qtilde_transpose_apply", "multibody_apply", "BodyOperator", "MultiBodyOperator", "RigidQError",
              "DuplicateBeadsError", "TooSmallError", "SizeGuardError", "LengthMismatchError",
-             "BodyTooSmallError", "ShapeMismatchError", "SingularHError"]
+             "BodyTooSmallError", "ShapeMismatchError", "SingularHError", "load_beads", "save_beads",
+             "load_vector", "save_vector", "RigidBodyBasis"]
     for n in names:
         assert hasattr(rq, n), n
 

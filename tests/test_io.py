@@ -1,0 +1,114 @@
+"""Text wire formats (reference io.py) against files the reference itself wrote
+(tests/golden/io, made by tests/golden/make_io_golden.py): writers byte-identical,
+readers value-identical, same ValueError messages."""
+
+import io
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+IO = os.path.join(GOLDEN, "io")
+
+
+def text(name):
+    with open(os.path.join(IO, name)) as f:
+        return f.read()
+
+
+@pytest.fixture(scope="module")
+def parsed():
+    with open(os.path.join(IO, "parsed.json")) as f:
+        return json.load(f)
+
+
+def _bodies():
+    # the same seeded bodies make_io_golden.py wrote
+    rng = np.random.default_rng(11)
+    b = [rng.normal(size=(5, 3)), rng.normal(size=(1, 3)) * 1e-300, rng.normal(size=(7, 3)) * 1e12]
+    b[0][0] = [-0.0, 1.0, 2.5]
+    b[2][3] = [1 / 3, -2 / 3, 1e-5]
+    return b
+
+
+def test_save_beads_bytes():
+    from paper_1708_08427_b200 import BeadModel, MultiBodyModel
+    from paper_1708_08427_b200 import io as rio
+
+    b = _bodies()
+    pos = np.concatenate(b)
+    off = np.cumsum([0] + [len(x) for x in b])
+    buf = io.StringIO()
+    rio.save_beads(MultiBodyModel.from_arrays(pos, off, check_duplicates=False), buf)
+    assert buf.getvalue() == text("beads_written.txt")
+    buf = io.StringIO()
+    rio.save_beads(MultiBodyModel([BeadModel(x, body_id=j, check_duplicates=False) for j, x in enumerate(b)]), buf)
+    assert buf.getvalue() == text("beads_written.txt")
+    buf = io.StringIO()
+    rio.save_beads(BeadModel(b[0], check_duplicates=False), buf)
+    assert buf.getvalue() == text("beads_single_written.txt")
+
+
+def test_save_vector_bytes():
+    from paper_1708_08427_b200 import io as rio
+
+    v, qv = np.load(os.path.join(IO, "vector_values.npy"))
+    buf = io.StringIO()
+    rio.save_vector(qv, buf, spectral_n=7)
+    assert buf.getvalue() == text("vector_spectral_written.txt")
+    buf = io.StringIO()
+    rio.save_vector(v, buf)
+    assert buf.getvalue() == text("vector_plain_written.txt")
+
+
+def test_vector_round_trip_exact():
+    from paper_1708_08427_b200 import io as rio
+
+    x = np.random.default_rng(3).normal(size=1000) * np.logspace(-300, 300, 1000)
+    buf = io.StringIO()
+    rio.save_vector(x, buf, spectral_n=12)
+    y, n = rio.load_vector(io.StringIO(buf.getvalue()))
+    assert n == 12 and np.array_equal(x, y)
+
+
+def test_readers_match_reference(parsed):
+    from paper_1708_08427_b200 import io as rio
+
+    pos, off, ids = rio.parse_beads(io.StringIO(text("beads_messy.txt")))
+    assert np.array_equal(pos, np.array(parsed["positions"]))
+    assert np.diff(off).tolist() == parsed["counts"]
+    assert ids.tolist() == parsed["body_ids"]
+    vals, sn = rio.load_vector(io.StringIO(parsed["vector_text"]))
+    assert vals.tolist() == parsed["vector"] and sn == parsed["spectral_n"]
+
+
+def test_reader_errors_match_reference(parsed):
+    from paper_1708_08427_b200 import io as rio
+
+    for name, (src, msg) in parsed["errors"].items():
+        fn = rio.load_vector if name == "bad_value" else rio.parse_beads
+        with pytest.raises(ValueError) as ei:
+            fn(io.StringIO(src))
+        assert str(ei.value) == msg, name
+
+
+@pytest.mark.gpu
+def test_load_beads_gpu(parsed):
+    import paper_1708_08427_b200 as rq
+    from paper_1708_08427_b200 import io as rio
+
+    m = rio.load_beads(io.StringIO(text("beads_messy.txt")))
+    assert [b.n for b in m.bodies] == parsed["counts"]
+    assert [b.body_id for b in m.bodies] == parsed["body_ids"]
+    assert np.array_equal(m.positions, np.array(parsed["positions"]))
+    with pytest.raises(rq.DuplicateBeadsError):
+        rio.load_beads(io.StringIO("0 0 0\n1 1 1\n---\n0 0 0\n0 0 0\n"))
+    # a written model reads back bit-exactly and gives the same operator
+    b = _bodies()
+    buf = io.StringIO()
+    rio.save_beads(rq.MultiBodyModel([rq.BeadModel(x) for x in b]), buf)
+    back = rio.load_beads(io.StringIO(buf.getvalue()))
+    assert np.array_equal(back.positions, np.concatenate(b))
