@@ -1249,12 +1249,21 @@ void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_
   }
   cuts.push_back(p.m);
   const int nseg = (int)cuts.size() - 1;
-  std::vector<cudaEvent_t> ev_in(nseg), ev_k(nseg);
+  static const bool trace = getenv("RQ_HOST_TRACE") != nullptr;  // diagnostics: per-stage timeline
+  std::vector<cudaEvent_t> ev_in(nseg), ev_k(nseg), ev_o(nseg);
+  cudaEvent_t ev0 = nullptr;
+  const unsigned evf = trace ? 0u : cudaEventDisableTiming;
   for (int i = 0; i < nseg; i++) {
-    RQ_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-    RQ_CUDA(cudaEventCreateWithFlags(&ev_k[i], cudaEventDisableTiming));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_in[i], evf));
+    RQ_CUDA(cudaEventCreateWithFlags(&ev_k[i], evf));
+    if (trace) RQ_CUDA(cudaEventCreate(&ev_o[i]));
+  }
+  if (trace) {
+    RQ_CUDA(cudaEventCreate(&ev0));
+    RQ_CUDA(cudaEventRecord(ev0, p.host_stream));
   }
   cudaStream_t s_in = p.host_stream, s_k = p.host_stream2, s_out = p.host_stream3;
+  static const unsigned host_phases = getenv("RQ_HOST_PHASES") ? (unsigned)atoi(getenv("RQ_HOST_PHASES")) : 7u;  // diagnostics
   double *din = p.stage_in.as<double>(), *dout = p.stage_out.as<double>();
   // every H2D is queued first, so the host-to-device engine never waits for the host to
   // finish enqueueing a segment's kernels
@@ -1269,13 +1278,25 @@ void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_
     BodyRange br;
     br.j0 = j0;
     br.j1 = j1;
-    run_apply(p, op, din, dout, k, s_k, 7u, br);
+    run_apply(p, op, din, dout, k, s_k, host_phases, br);
     RQ_CUDA(cudaEventRecord(ev_k[i], s_k));
     RQ_CUDA(cudaStreamWaitEvent(s_out, ev_k[i], 0));
     const int64_t o0 = rows(out_comp, j0), o1 = rows(out_comp, j1);
     RQ_CUDA(cudaMemcpyAsync(out + o0 * k, dout + o0 * k, (size_t)(o1 - o0) * k * 8, cudaMemcpyDeviceToHost, s_out));
+    if (trace) RQ_CUDA(cudaEventRecord(ev_o[i], s_out));
   }
   RQ_CUDA(cudaStreamSynchronize(s_out));
+  if (trace) {
+    for (int i = 0; i < nseg; i++) {
+      float a = 0, b = 0, c = 0;
+      cudaEventElapsedTime(&a, ev0, ev_in[i]);
+      cudaEventElapsedTime(&b, ev0, ev_k[i]);
+      cudaEventElapsedTime(&c, ev0, ev_o[i]);
+      fprintf(stderr, "[rq host] seg %d: h2d done %.3f  kernels done %.3f  d2h done %.3f ms\n", i, a, b, c);
+      cudaEventDestroy(ev_o[i]);
+    }
+    cudaEventDestroy(ev0);
+  }
   for (int i = 0; i < nseg; i++) {
     cudaEventDestroy(ev_in[i]);
     cudaEventDestroy(ev_k[i]);
