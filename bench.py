@@ -12,6 +12,8 @@ larger than the 126 MB L2, so no L2 flush is needed between steps.
 N > 1 runs under torchrun, one rank per GPU; bodies are independent so every
 rank owns its own 1000-body shard (weak scaling, no data-path collective);
 times are device-measured (CUDA events) and max-reduced over ranks.
+--sharding strong instead splits ONE config-sized model across the ranks by
+cumulative bead count (e.g. config 4's 20000 bodies over 8 GPUs).
 
 --impl reference times the reference algorithm on the host CPU: the C oracle
 (oracle/, a restatement of the pure-Python reference package that is 30-100x
@@ -48,24 +50,34 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharding", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank owns a full config-sized shard; strong: one config-sized "
+                         "model split across the ranks by cumulative bead count (parallel.shard_bounds)")
     return ap.parse_args()
 
 
-def workload(cfg: int, rank: int, scale: float):
+def workload(cfg: int, rank: int, scale: float, world: int = 1, strong: bool = False):
+    from paper_1708_08427_b200.parallel import shard_of
     from paper_1708_08427_b200.workloads import CONFIGS, make_config
 
-    pos, off = make_config(cfg, seed=1000 + rank, scale=scale)
+    if strong:  # one model for the whole job, this rank's contiguous shard of its bodies
+        pos, off = make_config(cfg, seed=1000, scale=scale)
+        pos, off, _ = shard_of(pos, off, rank, world)
+    else:
+        pos, off = make_config(cfg, seed=1000 + rank, scale=scale)
     name = CONFIGS[cfg]["workload"] if cfg in CONFIGS else "cfg4: 20000 ellipsoid bodies, n_j log-uniform [500, 50000]"
     k = CONFIGS.get(cfg, {}).get("k", 1)
     return pos, off, name, k
 
 
-def config_dict(name, off, k, n_gpus):
+def config_dict(name, off, k, n_gpus, strong=False):
     n = np.diff(off)
     return {"workload": name, "bodies": int(len(n)), "beads": int(off[-1]),
             "beads_per_body": int(n[0]) if np.all(n == n[0]) else "mixed", "rhs_k": k,
             "l2": "operator + vectors >> 126 MB L2 (no flush needed)",
-            "sharding": f"weak: one independent shard per rank x{n_gpus}"}
+            "sharding": (f"strong: one model split by cumulative bead count over {n_gpus} ranks "
+                         f"(bodies/beads above are rank 0's shard)") if strong else
+                        f"weak: one independent shard per rank x{n_gpus}"}
 
 
 def peaks():
@@ -191,8 +203,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    pos, off, name, k = workload(args.config, rank, args.scale)
+    strong = args.sharding == "strong"
+    pos, off, name, k = workload(args.config, rank, args.scale, world, strong)
     N, m = int(off[-1]), len(off) - 1
+    # beads processed per step by the whole job (strong: the sum of the shards)
+    n_job = world * N
+    if strong and dist:
+        t = torch.tensor([N], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        n_job = int(t.item())
     model = rq.MultiBodyModel.from_arrays(pos, off)
     # load the library's kernels (lazy module loading) before the setup is timed
     from paper_1708_08427_b200.workloads import make_config
@@ -249,7 +268,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    value = world * N / (ms * 1e-3)
+    value = n_job / (ms * 1e-3)
 
     # ---- kernel-level roofline: the chunk sweep (dominant kernel), timed alone
     lib = L.lib()
@@ -330,7 +349,7 @@ def main():
             e2e_ms = float(t.item())
         nbytes_in = (hv.numel() + hg.numel()) * 8
         nbytes_out = (ho1.numel() + ho2.numel()) * 8
-        e2e = {"value": world * N * k / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes_in,
+        e2e = {"value": n_job * k / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes_in,
                "d2h_bytes_per_step": nbytes_out, "ms_per_step": e2e_ms,
                "path": "rq_apply_host (C ABI, pinned host buffers, H2D+D2H inside the timed region)"}
 
@@ -349,8 +368,8 @@ def main():
         line = {
             "metric": METRIC, "value": value * k, "unit": UNIT if k == 1 else "bead-RHS/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(name, off, k, world),
+            "scaling": args.sharding, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(name, off, k, world, strong),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kname,
