@@ -110,6 +110,7 @@ struct ApplyCtx {
   int op;
   int head_bytes, lrec_bytes, max_nodes, max_beads, max_res, max_tiles;
   int pf_dist;     // L2 prefetch distance of chunk records (chunks ahead)
+  uint32_t sm_head, sm_lrec, sm_v, sm_root, sm_o_lrec, sm_o_v, sm_o_m, sm_o_root;  // smem_map(), host-computed
   unsigned long long *ctr;  // {claim, done}: chunks are claimed dynamically (reset by the last CTA)
   const uint8_t *l2_next;   // upward: the staged top blobs the next kernel sweeps, prefetched into
   int64_t l2_next_bytes;    // L2 by each CTA (a 1/grid slice) once it has no chunk left
@@ -351,7 +352,11 @@ __global__ void __launch_bounds__(NT, NT == 128 ? RQ_MIN_BLOCKS : 1) k_chunk(App
   // fill warps from warp 0), so the producer work stays off the slowest warp's path
   constexpr int PROD = NT - 32;
   const long long t_kernel0 = (RQ_TIMING && a.dbg && tid == 0) ? clock64() : 0;
-  const SmemMap SM = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, UP);
+  // section offsets come precomputed in the launch parameters (recomputing smem_map() from
+  // the sizes put ~a dozen dependent instructions in front of every node's first load)
+  SmemMap SM;
+  SM.head = a.sm_head; SM.lrec = a.sm_lrec; SM.v = a.sm_v; SM.root = a.sm_root; SM.x = 0u;
+  SM.o_lrec = a.sm_o_lrec; SM.o_v = a.sm_o_v; SM.o_m = a.sm_o_m; SM.o_x = a.sm_o_root; SM.o_root = a.sm_o_root;
   const uint32_t bar_u = smem_u32(bar), smem_u = smem_u32(smem);
 #define BAR(i) (bar_u + 8u * (uint32_t)(i))
 #define HEAD_U(i) (smem_u + (uint32_t)(i) * SM.head)
@@ -1003,7 +1008,10 @@ KernelCfg chunk_cfg(const Plan &p, bool up, ApplyCtx &a) {
   a.max_tiles = std::max(1, p.max_chunk_tiles);
   KernelCfg cfg;
   cfg.threads = p.chunk_threads;
-  cfg.smem = smem_total(smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, up));
+  const SmemMap sm = smem_map(a.head_bytes, a.lrec_bytes, a.max_beads, a.max_res, a.max_nodes, a.max_tiles, up);
+  a.sm_head = sm.head; a.sm_lrec = sm.lrec; a.sm_v = sm.v; a.sm_root = sm.root;
+  a.sm_o_lrec = sm.o_lrec; a.sm_o_v = sm.o_v; a.sm_o_m = sm.o_m; a.sm_o_root = sm.o_root;
+  cfg.smem = smem_total(sm);
   cfg.fn = up ? chunk_fn<true>(cfg.threads, a.k == 1) : chunk_fn<false>(cfg.threads, a.k == 1);
   RQ_CUDA(cudaFuncSetAttribute((const void *)cfg.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem));
   int occ = 0;
