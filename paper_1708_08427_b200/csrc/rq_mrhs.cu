@@ -477,20 +477,24 @@ __device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, do
   __syncwarp();
 }
 
-template <bool UP>
-__global__ void __launch_bounds__(MRHS_NT, 4) k_mrhs(MrhsCtx a) {
+// MODE (a template parameter, so each column layout gets its own register allocation):
+// 0: K == 32, 1: K a multiple of 32, 2: any K (inactive lanes in the last column group)
+// MINB: CTAs per SM the registers are bounded for.  Upward tile units run best at 3 (no
+// spills; 4 spilled ~90 bytes), the few top units and every downward launch at 4
+// (measured on config 5).
+template <bool UP, int MODE, int MINB>
+__global__ void __launch_bounds__(MRHS_NT, MINB) k_mrhs(MrhsCtx a) {
   extern __shared__ __align__(16) double smem_m[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const size_t warp_doubles = (size_t)a.depth * 6 * 32 + RING * ENTRY_BYTES / 8;
   double *stk = smem_m + (size_t)wib * warp_doubles;
   uint8_t *ring = reinterpret_cast<uint8_t *>(stk + (size_t)a.depth * 6 * 32);
   const int64_t GW = (int64_t)gridDim.x * (MRHS_NT / 32);
-  const int mode = a.K == 32 ? 0 : ((a.K % 32) == 0 ? 1 : 2);
   for (int64_t item = (int64_t)blockIdx.x * (MRHS_NT / 32) + wib; item < a.n_units * a.n_cg; item += GW) {
     const UnitDesc U = a.units[item / a.n_cg];
     const int64_t col = (item % a.n_cg) * 32 + lane;
-    if (mode == 0) run_unit<UP, true, 32>(a, U, stk, ring, lane, col);
-    else if (mode == 1) run_unit<UP, true, 0>(a, U, stk, ring, lane, col);
+    if (MODE == 0) run_unit<UP, true, 32>(a, U, stk, ring, lane, col);
+    else if (MODE == 1) run_unit<UP, true, 0>(a, U, stk, ring, lane, col);
     else run_unit<UP, false, 0>(a, U, stk, ring, lane, col);
   }
 }
@@ -660,21 +664,24 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
   a.K = k;
   a.op = op;
   a.n_cg = (k + 31) / 32;
-  auto launch = [&](int64_t u0, int64_t u1, int depth) {
+  auto launch = [&](int64_t u0, int64_t u1, int depth, bool tiles) {
     if (u1 <= u0) return;
     a.units = p.mrhs_units.as<UnitDesc>() + u0;
     a.n_units = u1 - u0;
     a.depth = depth;
     const size_t smem = (size_t)(MRHS_NT / 32) * ((size_t)depth * 6 * 32 * 8 + RING * ENTRY_BYTES);
-    const void *fn = up ? (const void *)k_mrhs<true> : (const void *)k_mrhs<false>;
-    RQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int mode = k == 32 ? 0 : ((k % 32) == 0 ? 1 : 2);
+    void (*fn)(MrhsCtx) = nullptr;
+    if (up && tiles) fn = mode == 0 ? k_mrhs<true, 0, 3> : (mode == 1 ? k_mrhs<true, 1, 3> : k_mrhs<true, 2, 3>);
+    else if (up) fn = mode == 0 ? k_mrhs<true, 0, 4> : (mode == 1 ? k_mrhs<true, 1, 4> : k_mrhs<true, 2, 4>);
+    else fn = mode == 0 ? k_mrhs<false, 0, 4> : (mode == 1 ? k_mrhs<false, 1, 4> : k_mrhs<false, 2, 4>);
+    RQ_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
-    RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, MRHS_NT, smem));
+    RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, MRHS_NT, smem));
     if (occ < 1) throw Error(RQ_ERR_CUDA, "multi-RHS kernel does not fit on an SM");
     const int64_t items = a.n_units * a.n_cg;
     const int64_t blocks = std::min<int64_t>((items + MRHS_NT / 32 - 1) / (MRHS_NT / 32), (int64_t)sms * occ);
-    if (up) k_mrhs<true><<<(unsigned)blocks, MRHS_NT, smem, s>>>(a);
-    else k_mrhs<false><<<(unsigned)blocks, MRHS_NT, smem, s>>>(a);
+    fn<<<(unsigned)blocks, MRHS_NT, smem, s>>>(a);
   };
   static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
   DBuf dbg;
@@ -687,11 +694,11 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
   const int64_t nt = p.n_tile_units;
   const bool do_tiles = phases & 1u, do_top = phases & 2u;
   if (up) {
-    if (do_tiles) launch(t0, t1, p.mrhs_depth_tile);
-    if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top);
+    if (do_tiles) launch(t0, t1, p.mrhs_depth_tile, true);
+    if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top, false);
   } else {
-    if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top);
-    if (do_tiles) launch(t0, t1, p.mrhs_depth_tile);
+    if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top, false);
+    if (do_tiles) launch(t0, t1, p.mrhs_depth_tile, true);
   }
   if (timing) {
     std::vector<long long> h((size_t)sms * 32 * 4 * 8);
