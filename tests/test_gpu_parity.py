@@ -182,7 +182,7 @@ def test_oracle_config_sizes(rq, oracle_mod):
     assert rel(op3.apply("qtilde_tv", g3), ref3.apply("qtilde_tv", g3)) < TOL
 
 
-@pytest.mark.parametrize("k", [5, 32, 45])
+@pytest.mark.parametrize("k", [5, 32, 45, 64])
 def test_multi_rhs(rq, oracle_mod, k):
     """(rows, k) blocks (config-5 shape, reduced): the column-parallel stack-machine
     kernels vs the oracle and vs column-by-column single-RHS results."""
