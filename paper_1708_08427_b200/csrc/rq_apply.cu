@@ -2,19 +2,20 @@
 //
 // Restates upward_apply (Algorithm 2, matfree.py:95-121, merge_infosets
 // matfree.py:41-62) and downward_apply (Algorithm 3, matfree.py:124-151,
-// split_rvset matfree.py:65-83) as two kernels each:
+// split_rvset matfree.py:65-83) as a chunk sweep plus a top-tree sweep:
 //
-//   UP   : k_chunk_up (all chunks, persistent CTAs) -> k_top_up (per body)
-//   DOWN : k_top_down (per body)                     -> k_chunk_down
+//   UP   : k_chunk<UP>   (all chunks, persistent CTAs) -> k_top2<UP> / k_top_df_up
+//   DOWN : k_top2<DOWN> / k_top_df_down                 -> k_chunk<DOWN>
 //
-// A chunk blob (level table | node meta | perm | SoA factor records) is moved
-// HBM -> shared memory with one cp.async.bulk (TMA bulk copy) per chunk,
-// double-buffered on an mbarrier so the next chunk streams in while the
-// current one is swept level by level (one thread per node, nodes of a level
-// are independent).  Children exchange their 6-long info/RV vectors through
-// shared memory; the beads' forces/velocities are gathered/scattered through
-// perm once per chunk.  No tensor cores: this is an HBM-bound sweep of tiny
-// orthogonal transforms (~0.3-0.6 flop/B).
+// A chunk is a set of tiles (maximal subtrees of <= tile_leaves beads) of one
+// body.  Per chunk, its head (descriptor | tiles | levels | node meta | perm) is
+// TMA bulk-copied into shared memory two chunks ahead, its records prefetched
+// into L2, its vector data gathered with cp.async one chunk ahead, and each
+// height level's records TMA-copied from L2 one level step ahead; the level
+// steps run case-uniform warps (GEN / RB / BB) separated by CTA barriers.
+// Tile-root 6-vectors pass to the top-tree kernels through exchange slots.
+// No tensor cores: this is an HBM-bound sweep of tiny fp64 orthogonal
+// transforms (~0.3 flop/B).  DESIGN.md §2.2 has the full description.
 #include <algorithm>
 #include <climits>
 #include <cuda/atomic>

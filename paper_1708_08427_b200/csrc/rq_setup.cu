@@ -10,11 +10,12 @@
 //   3. radix sort of (body, key) -> perm (tree.py:368)
 //   4. Karras radix-tree topology; reference postorder ids from
 //        id(X) = start + C(start) + 2L - 2,  C(s) = #internal nodes with stop <= s
-//   5. bottom-up factor pass (last-arriver): centroids (tree.py:126), the
-//      three node cases (factor.py:224-243), compact LQ records
-//   6. apply layout: tiles (maximal subtrees with <= S beads), chunks (greedy
-//      byte-budget packing of consecutive tiles), level-major SoA blobs, and
-//      the top tree above the tiles.
+//   5. bottom-up factor pass, one launch per ghost-depth level (deepest first,
+//      nodes case-sorted): centroids (tree.py:126), the three node cases
+//      (factor.py:224-243), compact LQ records
+//   6. apply layout: tiles (maximal subtrees with <= S beads, height-sorted per
+//      body), chunks (greedy byte-budget packing of a body's tiles), level-major
+//      AoS blobs, and the top tree above the tiles (staged blobs / dataflow).
 // Compiled with --fmad=false (see rq_lq.cuh).
 #include <cub/cub.cuh>
 
