@@ -269,6 +269,17 @@ def main():
         ms = float(t.item())
         dist.barrier()
     value = n_job / (ms * 1e-3)
+    # per-step spread (min / median over >= 10 individually timed steps, as the
+    # reference's own bench reports the min of 10); `value` stays the K-step average
+    reps = []
+    for _ in range(20):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s)
+        step()
+        a1.record(s)
+        a1.synchronize()
+        reps.append(a0.elapsed_time(a1))
+    step_stats = {"min_ms": float(np.min(reps)), "median_ms": float(np.median(reps)), "repeats": len(reps)}
 
     # ---- kernel-level roofline: the chunk sweep (dominant kernel), timed alone
     lib = L.lib()
@@ -376,6 +387,7 @@ def main():
                          "bytes_per_launch": chunk_bytes, "launch_ms": chunk_ms, "peak_source": peak_src,
                          "share_of_step": share},
             "kernels_ms": {f"{a}:{b}": v_ for (a, b), v_ in kern.items()},
+            "step_ms_single": step_stats,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": ck, "gpu_launches": int(launches),
             "setup": {"seconds": setup_s, "beads_per_s": N / setup_s, "first_build_seconds": setup_times[0],
                       "from": "host positions (pageable numpy), tree + factors + apply layout, device-synchronised"},
