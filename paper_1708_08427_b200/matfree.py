@@ -211,22 +211,26 @@ class MultiBodyOperator:
         self.plan = Plan(model.positions, model.offsets, max_depth=max_depth)
         self.bodies = _BodyViews(model)
         self._n = np.diff(model.offsets)
+        self._N = int(model.offsets[-1])
+        self._min_n = int(self._n.min())
 
     def _lengths(self, op: str):
-        full = [3 * int(n) for n in self._n]
+        """Total (input, output) lengths of the concatenated per-body blocks (matfree.py:223-233);
+        per-call host work is O(1) in the number of bodies (min body size cached)."""
+        full = 3 * self._N
         if op in ("qv", "qtv"):
             return full, full
-        if np.any(self._n < 2):
+        if self._min_n < 2:
             raise BodyTooSmallError("complement operators need every body to have >= 2 beads")
-        comp = [3 * int(n) - 6 for n in self._n]
+        comp = full - 6 * len(self._n)
         return (full, comp) if op == "qtilde_v" else (comp, full)
 
     def apply(self, op: str, v):
         if op not in _OP_NAMES:
             raise ValueError(f"op must be one of {_OP_NAMES}, got {op!r}")
-        in_lens, out_lens = self._lengths(op)
-        v2, single = _as_columns(v, sum(in_lens))
-        if op == "qtilde_tv" and min(in_lens) == 0:
+        in_len, out_len = self._lengths(op)
+        v2, single = _as_columns(v, in_len)
+        if op == "qtilde_tv" and self._min_n == 2:
             # the reference applies each body block separately and a length-0
             # block fails its reshape (matfree.py:92, 245): kept as-is
             raise ValueError("cannot reshape array of size 0 into shape (0,newaxis)")
