@@ -335,6 +335,14 @@ def test_errors(rq):
     np.testing.assert_allclose(mop.apply("qtv", mop.apply("qv", np.arange(9.0))), np.arange(9.0), atol=1e-14)
     with pytest.raises(rq.TooSmallError):
         rq.generate_explicit_q(one.tree)
+    # an n = 2 body: Q~ has a length-0 block; the reference's Q~^T rejects it (matfree.py:92, 245)
+    mm2 = rq.MultiBodyModel([rq.BeadModel([[0, 0, 0.0], [1, 0, 0]]), rq.BeadModel([[0, 0, 1.0], [1, 0, 0], [0, 2, 0]])])
+    mop2 = rq.MultiBodyOperator(mm2)
+    assert mop2.apply("qtilde_v", np.arange(15.0)).shape == (3,)
+    with pytest.raises(ValueError):
+        mop2.apply("qtilde_tv", np.zeros(3))
+    with pytest.raises(rq.LengthMismatchError):
+        mop2.apply("qtilde_v", np.zeros(14))
 
 
 def test_node_primitives(rq, oracle_mod):
