@@ -85,3 +85,19 @@ def test_gather_world2_gloo():
     got = np.array(q.get())
     want = np.arange(3 * 52 - 6 * 6, dtype=float) * 2.0
     np.testing.assert_array_equal(got, want)
+
+
+def test_bench_strong_sharding_covers_the_model():
+    """bench.py --sharding strong: the ranks' shards concatenate to the one config-4 model."""
+    import bench
+    from paper_1708_08427_b200.workloads import make_config
+
+    pos, off = make_config(4, seed=1000, scale=0.005)
+    for world in (2, 3, 8):
+        parts = [bench.workload(4, r, 0.005, world, True) for r in range(world)]
+        assert np.array_equal(np.concatenate([p[0] for p in parts]), pos)
+        sizes = np.concatenate([np.diff(p[1]) for p in parts])
+        assert np.array_equal(sizes, np.diff(off))
+        beads = [int(p[1][-1]) for p in parts]
+        # each cut lies within half a body of its ideal position: shard sizes differ by <= 2 bodies
+        assert max(beads) - min(beads) <= 2 * int(np.diff(off).max())
