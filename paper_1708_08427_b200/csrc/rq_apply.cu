@@ -57,11 +57,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       : "memory");
 }
 // Programmatic dependent launch: every apply kernel is launched with programmatic
-// stream serialisation, lets its successor launch early (launch_dependents) and waits
+// stream serialisation (no early trigger: the successor launches when it completes) and waits
 // for its predecessor's results (griddepcontrol.wait) only before touching data another
 // kernel produces (input/output vectors, exchange slots); plan data is read before.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // 32-bit shared-address forms (addresses computed once per kernel)
 __device__ __forceinline__ void mbar_expect_tx_u(uint32_t bar, unsigned bytes) {
@@ -223,9 +222,6 @@ __device__ __forceinline__ void down_node(int slot, const double *rec, const Nod
   }
 }
 
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
