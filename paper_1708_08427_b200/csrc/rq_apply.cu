@@ -283,6 +283,9 @@ __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
 // Stage the vector data a chunk needs, asynchronously (cp.async, one group):
 //   UP  : the chunk's bead forces, gathered through perm
 //   DOWN: the chunk's residue coefficients (contiguous per tile) + tile-root RV-sets
+__device__ __forceinline__ void cp_async16cg_u32(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async8_u32(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -853,25 +856,28 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   const int64_t bead0 = a.bead_off[h.body];
   const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)h.body;
   if (UP) {
-    // 8 independent loads in flight per thread (tile-root vectors from L2)
-    const int n_in = 6 * h.n_inputs;
-    for (int i0 = tid; i0 < n_in; i0 += 8 * NTT) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; u++) {
-        const int i = i0 + u * NTT;
-        v[u] = 0.0;
-        if (i < n_in) {
-          const int q = i / 6, r = i % 6;
-          const int32_t ref = INREF[q];
-          if (ref >= 0) v[u] = __ldcg(&a.scratch[6 * (int64_t)ref + r]);
-          else if (r < 3) v[u] = a.in[((bead0 + ~(int64_t)ref) * 3 + r) * K + col];
-        }
+    // inputs staged with cp.async, all in flight at once: tile-root vectors (3 x 16 B from
+    // L2, .cg) and bead forces (3 x 8 B; the upper half of a bead's info vector is 0)
+    for (int q = tid; q < h.n_inputs; q += NTT) {
+      const int32_t ref = INREF[q];
+      const uint32_t d = smem_u32(IN + 6 * q);
+      if (ref >= 0) {
+        const double *src = a.scratch + 6 * (int64_t)ref;
+        cp_async16cg_u32(d, src);
+        cp_async16cg_u32(d + 16, src + 2);
+        cp_async16cg_u32(d + 32, src + 4);
+      } else {
+        const double *src = a.in + ((bead0 + ~(int64_t)ref) * 3) * K + col;
+        cp_async8_u32(d, src);
+        cp_async8_u32(d + 8, src + K);
+        cp_async8_u32(d + 16, src + 2 * K);
+        IN[6 * q + 3] = 0.0;
+        IN[6 * q + 4] = 0.0;
+        IN[6 * q + 5] = 0.0;
       }
-#pragma unroll
-      for (int u = 0; u < 8; u++)
-        if (i0 + u * NTT < n_in) IN[i0 + u * NTT] = v[u];
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     const long long c2 = TM ? clock64() : 0;
     for (int lv = 0; lv < h.n_levels; lv++) {
@@ -906,13 +912,17 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
       d[6] = (long long)g0; d[7] = (long long)g1;
     }
   } else {
-    for (int q = tid; q < h.n_nodes; q += NTT) {
+    for (int q = tid; q < h.n_nodes; q += NTT) {  // residues staged with cp.async, all in flight
       const TopMeta md = MD[q];
       const int rr = res_rows(flag_case(md.flags));
-      for (int r = 0; r < rr; r++) RT[6 * q + r] = a.in[(sbase + md.res_q + r) * K + col];
+      const double *src = a.in + (sbase + md.res_q) * K + col;
+      const uint32_t d = smem_u32(RT + 6 * q);
+      for (int r = 0; r < rr; r++) cp_async8_u32(d + 8u * r, src + r * K);
       if (md.is_root)
         for (int r = 0; r < 6; r++) MT[6 * q + r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * K + col] : 0.0;
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     for (int lv = h.n_levels - 1; lv >= 0; lv--) {
       for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NTT) {
