@@ -333,6 +333,24 @@ def main():
         if tj.get("config") == args.config and tj.get("beads"):
             traffic = tj["dram_bytes_per_launch"] * N / tj["beads"]
 
+    # ---- Zf / Z^T u (config 4 names them): 48 algorithmic bytes per
+    # bead (positions in + forces in / velocities out), device-resident inputs
+    zops = {}
+    fz = torch.randn(3 * N, generator=gen, device=dev, dtype=torch.float64)
+    uz = torch.randn(6 * m, generator=gen, device=dev, dtype=torch.float64)
+    for zname, zfn in (("zf", lambda: op.zf(fz)), ("ztu", lambda: op.ztu(uz))):
+        for _ in range(3):
+            zfn()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s)
+        for _ in range(20):
+            zfn()
+        a1.record(s)
+        torch.cuda.synchronize()
+        zms = a0.elapsed_time(a1) / 20
+        zops[zname] = {"ms": zms, "beads_per_s": N / (zms * 1e-3), "achieved_gbs": 48 * N / (zms * 1e-3) / 1e9,
+                       "frac": 48 * N / (zms * 1e-3) / 1e9 / peaks()[0]}
+
     # ---- end to end through the C ABI with HOST buffers (pinned), copies inside
     e2e = None
     if not args.no_e2e:
@@ -388,6 +406,7 @@ def main():
                          "share_of_step": share},
             "kernels_ms": {f"{a}:{b}": v_ for (a, b), v_ in kern.items()},
             "step_ms_single": step_stats,
+            "z_ops": zops,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": ck, "gpu_launches": int(launches),
             "setup": {"seconds": setup_s, "beads_per_s": N / setup_s, "first_build_seconds": setup_times[0],
                       "from": "host positions (pageable numpy), tree + factors + apply layout, device-synchronised"},
