@@ -66,15 +66,44 @@ __global__ void __launch_bounds__(NTZ) k_seg_zf(const double *pos, const int64_t
   const int j = seg_body[s];
   const double cx = origin[j * 3], cy = origin[j * 3 + 1], cz = origin[j * 3 + 2];
   double v[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t i = b + threadIdx.x; i < e; i += NTZ) {
-    const double x = pos[i * 3] - cx, y = pos[i * 3 + 1] - cy, z = pos[i * 3 + 2] - cz;
-    const double fx = f[(i * 3) * K + col], fy = f[(i * 3 + 1) * K + col], fz = f[(i * 3 + 2) * K + col];
-    v[0] += fx;
-    v[1] += fy;
-    v[2] += fz;
-    v[3] += y * fz - z * fy;
-    v[4] += z * fx - x * fz;
-    v[5] += x * fy - y * fx;
+  // Fixed order, independent of where the body sits in the batch: thread t takes the bead
+  // pairs (2q, 2q+1), q = t, t + NTZ, ... of the segment (then thread 0 an odd last bead),
+  // followed by the fixed tree of block_sum.  Aligned K = 1 inputs load each pair as
+  // 3 x 16 B of positions and of forces; otherwise the same pairs load element-wise.
+  // explicit roundings (no FMA contraction), so both load paths compute bit-identically
+  auto acc = [&](double x, double y, double z, double fx, double fy, double fz) {
+    x = __dsub_rn(x, cx); y = __dsub_rn(y, cy); z = __dsub_rn(z, cz);
+    v[0] = __dadd_rn(v[0], fx);
+    v[1] = __dadd_rn(v[1], fy);
+    v[2] = __dadd_rn(v[2], fz);
+    v[3] = __dadd_rn(v[3], __dsub_rn(__dmul_rn(y, fz), __dmul_rn(z, fy)));
+    v[4] = __dadd_rn(v[4], __dsub_rn(__dmul_rn(z, fx), __dmul_rn(x, fz)));
+    v[5] = __dadd_rn(v[5], __dsub_rn(__dmul_rn(x, fy), __dmul_rn(y, fx)));
+  };
+  const int64_t npair = (e - b) / 2;
+  if (K == 1 && ((b & 1) == 0) && ((reinterpret_cast<uintptr_t>(f) & 15) == 0)) {
+    const double2 *P2 = reinterpret_cast<const double2 *>(pos + 3 * b);
+    const double2 *F2 = reinterpret_cast<const double2 *>(f + 3 * b);
+#pragma unroll 2
+    for (int64_t q = threadIdx.x; q < npair; q += NTZ) {
+      const double2 p0 = P2[3 * q], p1 = P2[3 * q + 1], p2 = P2[3 * q + 2];
+      const double2 f0 = F2[3 * q], f1 = F2[3 * q + 1], f2 = F2[3 * q + 2];
+      acc(p0.x, p0.y, p1.x, f0.x, f0.y, f1.x);
+      acc(p1.y, p2.x, p2.y, f1.y, f2.x, f2.y);
+    }
+  } else {
+    for (int64_t q = threadIdx.x; q < npair; q += NTZ) {
+      for (int h = 0; h < 2; h++) {
+        const int64_t i = b + 2 * q + h;
+        acc(pos[i * 3], pos[i * 3 + 1], pos[i * 3 + 2], f[(i * 3) * K + col], f[(i * 3 + 1) * K + col],
+            f[(i * 3 + 2) * K + col]);
+      }
+    }
+  }
+  if (((e - b) & 1) && threadIdx.x == 0) {
+    const int64_t i = e - 1;
+    acc(pos[i * 3], pos[i * 3 + 1], pos[i * 3 + 2], f[(i * 3) * K + col], f[(i * 3 + 1) * K + col],
+        f[(i * 3 + 2) * K + col]);
   }
   block_sum<6>(v, sh);
   if (threadIdx.x == 0)
@@ -89,6 +118,36 @@ __global__ void k_body_zf(const double *part, const int64_t *body_seg, int64_t m
   for (int64_t s = body_seg[j]; s < body_seg[j + 1]; s++)
     for (int a = 0; a < 6; a++) v[a] += part[s * 6 + a];
   for (int a = 0; a < 6; a++) out[(j * 6 + a) * K + col] = v[a];
+}
+
+// K = 1, 16-byte aligned output: a thread maps a bead pair (48 contiguous bytes in and out)
+__global__ void k_ztu2(const double *pos, const int32_t *body_of, const double *origin, const double *u, int64_t N,
+                       double *out) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (2 * q >= N) return;
+  const double2 *P2 = reinterpret_cast<const double2 *>(pos) + 3 * q;
+  double2 *O2 = reinterpret_cast<double2 *>(out) + 3 * q;
+  const double2 p0 = P2[0], p1 = P2[1], p2 = P2[2];
+  double o[6];
+  auto map = [&](int64_t i, double x, double y, double z, double *r) {
+    const int j = body_of[i];
+    x -= origin[j * 3]; y -= origin[j * 3 + 1]; z -= origin[j * 3 + 2];
+    const double *U = u + j * 6;
+    r[0] = U[0] + (z * U[4] - y * U[5]);
+    r[1] = U[1] + (x * U[5] - z * U[3]);
+    r[2] = U[2] + (y * U[3] - x * U[4]);
+  };
+  map(2 * q, p0.x, p0.y, p1.x, o);
+  if (2 * q + 1 < N) {
+    map(2 * q + 1, p1.y, p2.x, p2.y, o + 3);
+    O2[0] = make_double2(o[0], o[1]);
+    O2[1] = make_double2(o[2], o[3]);
+    O2[2] = make_double2(o[4], o[5]);
+  } else {  // odd N: the last bead alone
+    out[6 * q] = o[0];
+    out[6 * q + 1] = o[1];
+    out[6 * q + 2] = o[2];
+  }
 }
 
 __global__ void k_ztu(const double *pos, const int32_t *body_of, const double *origin, const double *u, int64_t N,
@@ -150,6 +209,10 @@ void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, cons
                                                  p.zpart.as<double>());
       k_body_zf<<<(unsigned)((p.m + 127) / 128), 128, 0, s>>>(p.zpart.as<double>(), p.body_seg.as<int64_t>(),
                                                               p.m, out, k, col);
+    } else if (k == 1 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+      const int64_t np = (p.N + 1) / 2;
+      k_ztu2<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(p.pos_orig.as<double>(), p.body_of.as<int32_t>(), origin,
+                                                          in, p.N, out);
     } else {
       k_ztu<<<(unsigned)((p.N + 255) / 256), 256, 0, s>>>(p.pos_orig.as<double>(), p.body_of.as<int32_t>(),
                                                           origin, in, p.N, k, col, out);

@@ -455,3 +455,22 @@ def test_setup_variants_bitwise(rq, monkeypatch, env):
     # and the layout really is exercised: Q~ round trip on the big body
     w = op.apply("qtv", op.apply("qv", v))
     assert rel(w, v) < 1e-12
+
+
+def test_zf_batch_independent(rq):
+    """Zf of a body is bit-identical whether the body sits at an even or an odd bead offset
+    of the batch (the aligned vector path and the element-wise path share one order)."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([5000, 9001], seed=4)
+    f = np.random.default_rng(1).normal(size=3 * off[-1])
+    both = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off)).zf(f)
+    # body 1 alone (even offset 0) vs inside the batch (offset 5000: even); shift by one bead
+    pos3 = np.concatenate([[[9.0, 9.0, 9.0]], pos])
+    off3 = np.concatenate([[0, 1], off[1:] + 1])
+    f3 = np.concatenate([[1.0, 2.0, 3.0], f])
+    shifted = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos3, off3)).zf(f3)
+    assert np.array_equal(shifted[6:], both)
+    import torch
+    dev = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off)).zf(torch.from_numpy(f).cuda())
+    assert np.array_equal(dev.cpu().numpy(), both)
