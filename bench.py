@@ -333,6 +333,28 @@ def main():
         if tj.get("config") == args.config and tj.get("beads"):
             traffic = tj["dram_bytes_per_launch"] * N / tj["beads"]
 
+    # ---- config 3 also as ONE batched application of its 100 fresh vectors (SURVEY 8(d):
+    # "report sequential and, separately, batched k=100"): the multi-RHS kernels
+    batched = None
+    if args.config == 3 and k == 1:
+        kb = 100
+        vb = torch.randn((3 * N, kb), generator=gen, device=dev, dtype=torch.float64)
+        gb = torch.randn((3 * N - 6 * m, kb), generator=gen, device=dev, dtype=torch.float64)
+        for _ in range(2):
+            op.apply("qtilde_v", vb)
+            op.apply("qtilde_tv", gb)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s)
+        for _ in range(5):
+            op.apply("qtilde_v", vb)
+            op.apply("qtilde_tv", gb)
+        a1.record(s)
+        torch.cuda.synchronize()
+        bms = a0.elapsed_time(a1) / 5
+        batched = {"k": kb, "ms_per_step": bms, "value": N * kb / (bms * 1e-3), "unit": "bead-RHS/s",
+                   "note": "Q~V + Q~^T G on (rows, 100) blocks: the 100 applications of config 3 batched"}
+        del vb, gb
+
     # ---- Zf / Z^T u (config 4 names them): 48 algorithmic bytes per
     # bead (positions in + forces in / velocities out), device-resident inputs
     zops = {}
@@ -407,6 +429,7 @@ def main():
             "kernels_ms": {f"{a}:{b}": v_ for (a, b), v_ in kern.items()},
             "step_ms_single": step_stats,
             "z_ops": zops,
+            "batched_k100": batched,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": ck, "gpu_launches": int(launches),
             "setup": {"seconds": setup_s, "beads_per_s": N / setup_s, "first_build_seconds": setup_times[0],
                       "from": "host positions (pageable numpy), tree + factors + apply layout, device-synchronised"},

@@ -1051,6 +1051,23 @@ void chunk_occupancy(const Plan &p, int ctas[2], int64_t smem[2]) {
   }
 }
 
+// dst (cols, rows) = src (rows, cols)^T, both row-major; 32 x 32 tiles through shared memory,
+// a 1-D grid over tiles (rows can exceed the 65535 limit of grid.y)
+__global__ void k_transpose(const double *src, int64_t R, int64_t Cn, double *dst) {
+  __shared__ double t[32][33];
+  const int64_t ntc = (Cn + 31) / 32;
+  const int64_t r0 = (int64_t)(blockIdx.x / ntc) * 32, c0 = (int64_t)(blockIdx.x % ntc) * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < R && c < Cn) t[i][threadIdx.x] = src[r * Cn + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < R && c < Cn) dst[c * R + r] = t[threadIdx.x][i];
+  }
+}
+
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases,
                BodyRange range) {
   if (op < 0 || op > 3) throw Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
@@ -1066,6 +1083,21 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   }
   if (use_mrhs(p, k)) {  // column-parallel stack-machine kernels (rq_mrhs.cu)
     run_apply_mrhs(p, op, in, out, k, s, phases, range);
+    return;
+  }
+  if (k > 1 && range.j1 < 0 && !getenv("RQ_COLLOOP_STRIDED")) {
+    // Column loop on contiguous columns: transpose the (rows, k) block once, run the K = 1
+    // kernels column by column, transpose back (a strided column costs 4x the sectors)
+    const bool in_comp = op == RQ_OP_QTILDE_TV, out_comp = op == RQ_OP_QTILDE_V;
+    const int64_t ri = 3 * p.N - (in_comp ? 6 * p.m : 0), ro = 3 * p.N - (out_comp ? 6 * p.m : 0);
+    if (ss.col_in.bytes < (size_t)(k * ri * 8)) ss.col_in.alloc(k * ri * 8);
+    if (ss.col_out.bytes < (size_t)(k * ro * 8)) ss.col_out.alloc(k * ro * 8);
+    double *ti = ss.col_in.as<double>(), *to = ss.col_out.as<double>();
+    auto tiles = [](int64_t R, int64_t Cn) { return (unsigned)(((R + 31) / 32) * ((Cn + 31) / 32)); };
+    if (ri > 0) k_transpose<<<tiles(ri, k), dim3(32, 8), 0, s>>>(in, ri, k, ti);
+    for (int64_t c = 0; c < k; c++) run_apply(p, op, ti + c * ri, to + c * ro, 1, s, phases, range);
+    if (ro > 0) k_transpose<<<tiles(k, ro), dim3(32, 8), 0, s>>>(to, k, ro, out);
+    RQ_CUDA(cudaGetLastError());
     return;
   }
   const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);

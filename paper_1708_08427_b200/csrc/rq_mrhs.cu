@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "rq_nodeops.cuh"
@@ -639,7 +640,16 @@ bool use_mrhs(const Plan &p, int64_t k) {
   for (int64_t j = 0; j < p.m; j++) max_n = std::max(max_n, p.bead_off[j + 1] - p.bead_off[j]);
   // the kernels use 32-bit body-relative row offsets
   const int64_t lim32 = int64_t(1) << 31;
-  return 3 * max_n * k < lim32 && 6 * std::max<int64_t>(p.n_slots, 1) * k < lim32;
+  if (!(3 * max_n * k < lim32 && 6 * std::max<int64_t>(p.n_slots, 1) * k < lim32)) return false;
+  const char *pol = getenv("RQ_MRHS");  // "always" / "never" override the cost model (tests, tuning)
+  if (pol && !strcmp(pol, "always")) return true;
+  if (pol && !strcmp(pol, "never")) return false;
+  // Cost model (measured on one B200): a body's top unit is one warp walking its top-tree
+  // nodes in sequence, ~35 ns per bead of the largest body (config 3, 2^20 beads: ~30 ms
+  // per operator, whatever k), while the column loop costs ~0.05 ns per bead-RHS more than
+  // the column-parallel tile kernels.  Config 5 (8192-bead bodies, k = 32) stays on the
+  // multi-RHS kernels; a single 2^20-bead body uses the column loop below k ~ 700.
+  return (double)max_n * 700.0 < (double)k * (double)p.N;
 }
 
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,

@@ -183,6 +183,7 @@ struct Plan {
   struct StreamState {
     DBuf scratch, mrhs_scratch, top_cnt;
     DBuf chunk_ctr;           // 2 x {claim, done} counters of the dynamic chunk schedule
+    DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
     uint32_t chunk_epoch = 0;  // chunk launches so far (consecutive launches alternate counters)
   };
   mutable std::mutex state_mu;

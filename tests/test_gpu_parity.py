@@ -183,11 +183,14 @@ def test_oracle_config_sizes(rq, oracle_mod):
 
 
 @pytest.mark.parametrize("k", [5, 32, 45, 64])
-def test_multi_rhs(rq, oracle_mod, k):
+def test_multi_rhs(rq, oracle_mod, k, monkeypatch):
     """(rows, k) blocks (config-5 shape, reduced): the column-parallel stack-machine
     kernels vs the oracle and vs column-by-column single-RHS results."""
     from paper_1708_08427_b200.workloads import ellipsoid_batch
 
+    # force the column-parallel kernels (the cost model would pick the column loop for a
+    # batch this small next to a 20000-bead body); test_multi_rhs_policy covers the choice
+    monkeypatch.setenv("RQ_MRHS", "always")
     counts = [4096] * 3 + [2, 3, 65, 64, 129, 20000, 1000, 1]
     pos, off = ellipsoid_batch(counts, seed=21)
     op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
@@ -474,3 +477,22 @@ def test_zf_batch_independent(rq):
     import torch
     dev = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off)).zf(torch.from_numpy(f).cuda())
     assert np.array_equal(dev.cpu().numpy(), both)
+
+
+def test_multi_rhs_policy(rq, monkeypatch):
+    """Blocks on one big body go column by column (its serial top unit would dominate);
+    both policies give the same block to rounding."""
+    from paper_1708_08427_b200 import _lib as L
+    from paper_1708_08427_b200.workloads import sphere_shell
+
+    p = sphere_shell(1 << 17, 2)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(p, np.array([0, 1 << 17])))
+    k = 12
+    V = np.random.default_rng(3).normal(size=(3 << 17, k))
+    lib = L.lib()
+    assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) >= 2 * k  # column loop
+    auto = op.apply("qtilde_v", V)
+    monkeypatch.setenv("RQ_MRHS", "always")
+    assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) < 2 * k
+    forced = op.apply("qtilde_v", V)
+    assert np.abs(auto - forced).max() <= 1e-12 * np.abs(auto).max()
