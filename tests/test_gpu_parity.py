@@ -496,3 +496,37 @@ def test_multi_rhs_policy(rq, monkeypatch):
     assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) < 2 * k
     forced = op.apply("qtilde_v", V)
     assert np.abs(auto - forced).max() <= 1e-12 * np.abs(auto).max()
+
+
+def test_cuda_graph_capture(rq):
+    """A Q~v + Q~^T g step captured in a CUDA graph replays bit-identically to eager calls
+    (stream-ordered scratch, self-resetting chunk / arrival counters)."""
+    import torch
+
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([4096] * 20 + [50000, 77], seed=13)
+    N, m = int(off[-1]), len(off) - 1
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    v = torch.randn(3 * N, dtype=torch.float64, device="cuda")
+    g = torch.randn(3 * N - 6 * m, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        op.apply("qtilde_v", v)  # lazy per-stream state outside the capture
+        op.apply("qtilde_tv", g)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        o1 = op.apply("qtilde_v", v)
+        o2 = op.apply("qtilde_tv", g)
+    for seed in range(3):
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        v.copy_(torch.randn(v.shape, generator=gen, dtype=torch.float64, device="cuda"))
+        g.copy_(torch.randn(g.shape, generator=gen, dtype=torch.float64, device="cuda"))
+        graph.replay()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s):
+            e1 = op.apply("qtilde_v", v)
+            e2 = op.apply("qtilde_tv", g)
+        s.synchronize()
+        assert torch.equal(o1, e1) and torch.equal(o2, e2)
