@@ -530,3 +530,16 @@ def test_cuda_graph_capture(rq):
             e2 = op.apply("qtilde_tv", g)
         s.synchronize()
         assert torch.equal(o1, e1) and torch.equal(o2, e2)
+
+
+def test_c_abi_host_program(rq):
+    """The C ABI from a plain C host (no Python in the loop): setup, Q~v, Q~^T g, Zf on host
+    buffers and an error code, checked against the oracle at 1e-12 (tests/c_abi)."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-s", "-C", os.path.join(root, "tests", "c_abi")], check=True)
+    r = subprocess.run([os.path.join(root, "tests", "c_abi", "c_abi_check")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr

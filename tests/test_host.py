@@ -118,3 +118,13 @@ def test_rigid_body_basis_validation():
         RigidBodyBasis().fit(np.zeros((4, 2)))
     with pytest.raises(ValueError, match="finite"):
         RigidBodyBasis().fit(np.array([[0.0, 0.0, np.nan], [1.0, 0.0, 0.0]]))
+
+
+def test_c_abi_host_program_builds(built):
+    """A plain C program compiles and links against include/rigidq_b200.h and
+    librigidq_b200.so (tests/c_abi; run on the GPU by test_gpu_parity.test_c_abi_host_program)."""
+    import subprocess
+
+    r = subprocess.run(["make", "-s", "-B", "-C", os.path.join(ROOT, "tests", "c_abi")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert os.path.exists(os.path.join(ROOT, "tests", "c_abi", "c_abi_check"))
