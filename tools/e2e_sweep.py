@@ -20,7 +20,7 @@ hv = torch.randn(3 * N, dtype=torch.float64).pin_memory()
 hg = torch.randn(3 * N - 6 * m, dtype=torch.float64).pin_memory()
 o1 = torch.empty(3 * N - 6 * m, dtype=torch.float64).pin_memory()
 o2 = torch.empty(3 * N, dtype=torch.float64).pin_memory()
-for segs, mb in [(8, 2), (12, 1), (16, 1), (24, 1), (32, 1)]:
+for segs, mb in [(4, 2), (6, 2), (8, 2), (10, 2), (12, 1)]:
     os.environ["RQ_HOST_SEGS"] = str(segs)
     os.environ["RQ_HOST_SEG_MB"] = str(mb)
     for _ in range(2):
