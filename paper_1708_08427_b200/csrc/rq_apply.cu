@@ -180,9 +180,8 @@ __device__ __forceinline__ void up_node(int slot, const double *rec, const NodeM
   rec_ratios(CS, R, 1, aa, bb);
   merge(CS, R, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
   if (CS != BEAD_BEAD) {
-    const TileDesc &T = TD[md.flags >> 6];
     const int64_t kk = K1 ? 1 : K;
-    double *o = OB + (int64_t)(T.res_q - T.res_local + md.res) * kk;
+    double *o = OB + (int64_t)(TD[md.flags >> 6].res_delta + md.res) * kk;
 #pragma unroll
     for (int r = 0; r < res_rows(CS); r++) o[r * kk] = res[r];
   }

@@ -78,7 +78,8 @@ struct TileDesc {        // 32 bytes; copies live in the chunk blob after the Ch
   int32_t res_q;         // body-relative complement (Q~) offset of the tile's first residue
   int32_t res_count;     // 3L - 6
   int32_t res_local;     // offset in the chunk staging buffer
-  int32_t pad[3];
+  int32_t res_delta;     // res_q - res_local (one load on the upward node path)
+  int32_t pad[2];
 };
 
 struct TopNode {         // node with more than tile_leaves beads

@@ -819,7 +819,8 @@ __global__ void k_tile_desc(const TileTmp *tiles, int64_t n_tiles_all, const int
   d.res_q = T.res_q;
   d.res_count = 3 * T.L - 6;
   d.res_local = res_local_of_tile[t];
-  d.pad[0] = d.pad[1] = d.pad[2] = 0;
+  d.pad[0] = d.pad[1] = 0;
+  d.res_delta = d.res_q - d.res_local;  // upward residue row = res_delta + node.res (body-relative)
   out[big_scan[t]] = d;
   const ChunkDesc &c = chunks[chunk_of_tile[t]];
   reinterpret_cast<TileDesc *>(blob + c.blob_off + sizeof(ChunkDesc))[big_scan[t] - c.tile_begin] = d;
