@@ -1569,11 +1569,12 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
     // With height-sorted tiles a chunk can collect many small tiles; capping beads and
     // tiles per chunk bounds the largest staging buffers (they size every CTA's shared
-    // memory), which keeps four downward chunk CTAs resident per SM (cfg2: 55.5 KB).
+    // memory) so four chunk CTAs stay resident per SM (cfg2: 56.7 KB; 18 tiles / 7S beads
+    // measured best on configs 2 and 4, 20 / 8S drops to 3 CTAs/SM).
     lim.max_nodes = 1024;
-    lim.max_beads = 5 * S;
+    lim.max_beads = 7 * S;
     lim.max_res = 3 * 1024;
-    lim.max_tiles = 14;
+    lim.max_tiles = 18;
     lim.max_lrec = 1280;  // 10 KB level-record stages
     if (const char *e = getenv("RQ_CHUNK_MAX_LREC")) lim.max_lrec = std::max(64, atoi(e));
     lim.max_lrec = std::max(lim.max_lrec, rec_size(GENERAL) * S / 2);  // any single tile fits
