@@ -180,7 +180,8 @@ int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
   }
   int classes = 0;
   for (int c = 0; c < 4; c++) classes += p.topclass_count[c] > 0;
-  int per_col = (p.n_chunks ? 1 : 0) + classes + (p.n_topbig ? 1 : 0) + ((p.n_small && op <= 1) ? 1 : 0);
+  // wavefront sweep + staged top classes + dataflow top + (Q / Q^T) layout pass
+  int per_col = (p.wave_streams ? 1 : 0) + classes + (p.n_top_start ? 1 : 0) + (op <= 1 ? 1 : 0);
   return (int)(per_col * k + (k > 1 ? 2 : 0));  // k > 1: the two block transposes
 }
 

@@ -121,10 +121,6 @@ struct ApplyCtx {
 #define RQ_TIMING 0
 #endif
 
-__device__ __forceinline__ int64_t spec_base(int op, const int64_t *bead_off, int j) {
-  // first residue row of body j in the op's spectral layout
-  return (op == RQ_OP_QV || op == RQ_OP_QTV) ? 3 * bead_off[j] + 6 : 3 * bead_off[j] - 6 * (int64_t)j;
-}
 
 // record -> registers with 16-byte loads (records are 16-byte aligned, AoS)
 template <int CS>
@@ -672,7 +668,9 @@ struct TopDfCtx {
   double *out;
   int64_t k, col;
   double *scratch;
-  int op, S;
+  const int64_t *res_base;  // private residue layout (Plan::res_base)
+  double *roots;            // body-root 6-vectors (Q / Q^T), nullptr for Q~ / Q~^T
+  int S;
 };
 
 __device__ __forceinline__ void top_fetch(const TopDfCtx &a, int64_t bead0, int32_t ref, double (&m)[6]) {
@@ -711,7 +709,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
     const int need = par >= 0 ? __ldg(&a.need[par]) : 0;
     const int j = T.body;
     const int64_t bead0 = a.bead_off[j];
-    const int64_t sbase = spec_base(a.op, a.bead_off, j);
+    const int64_t sbase = a.res_base[j];
     const int cs = flag_case(T.flags);
     double R[rec_size(GENERAL)];
     ldg_rec(cs, a.rec + T.rec_off, R);
@@ -722,8 +720,8 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_up(TopDfCtx a) {
     merge(cs, R, 1, flag_signs(T.flags), aa, bb, mx, my, mp, res);
     for (int r = 0; r < res_rows(cs); r++) a.out[(sbase + T.res_q + r) * a.k + a.col] = res[r];
     if (T.is_root) {
-      if (a.op == RQ_OP_QV)
-        for (int r = 0; r < 6; r++) a.out[(3 * bead0 + r) * a.k + a.col] = mp[r];
+      if (a.roots)
+        for (int r = 0; r < 6; r++) a.roots[6 * (int64_t)j + r] = mp[r];
       return;
     }
 #pragma unroll
@@ -749,7 +747,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
   TopNode T = a.top[path[0]];
   const int j = T.body;
   const int64_t bead0 = a.bead_off[j];
-  const int64_t sbase = spec_base(a.op, a.bead_off, j);
+  const int64_t sbase = a.res_base[j];
   auto load_node = [&](const TopNode &N, double (&R)[rec_size(GENERAL)], double (&res)[6]) {
     const int cs = flag_case(N.flags);
     ldg_rec(cs, a.rec + N.rec_off, R);
@@ -757,7 +755,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
     for (int r = 0; r < 6; r++) res[r] = r < res_rows(cs) ? a.in[(sbase + N.res_q + r) * a.k + a.col] : 0.0;
   };
   double lp[6];
-  for (int r = 0; r < 6; r++) lp[r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * a.k + a.col] : 0.0;
+  for (int r = 0; r < 6; r++) lp[r] = a.roots ? a.roots[6 * (int64_t)j + r] : 0.0;
   double R[rec_size(GENERAL)], res[6];
   load_node(T, R, res);
   for (int d = 0; d < len; d++) {
@@ -808,7 +806,8 @@ struct Top2Ctx {
   double *out;
   int64_t k, col;
   double *scratch;
-  int op;
+  const int64_t *res_base;  // private residue layout (Plan::res_base)
+  double *roots;            // body-root 6-vectors (Q / Q^T), nullptr for Q~ / Q~^T
 };
 
 // NTT threads per top tree: one warp for the small shared-memory classes (top trees
@@ -853,7 +852,7 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   double *MT = IN + 6 * max(h.n_inputs, h.n_nodes);
   const int64_t K = a.k, col = a.col;
   const int64_t bead0 = a.bead_off[h.body];
-  const int64_t sbase = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV) ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)h.body;
+  const int64_t sbase = a.res_base[h.body];
   if (UP) {
     // inputs staged with cp.async, all in flight at once: tile-root vectors (3 x 16 B from
     // L2, .cg) and bead forces (3 x 8 B; the upper half of a bead's info vector is 0)
@@ -895,8 +894,8 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
         merge(cs, rec, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
         const int rr = res_rows(cs);
         for (int r = 0; r < rr; r++) a.out[(sbase + md.res_q + r) * K + col] = res[r];
-        if (md.is_root && a.op == RQ_OP_QV)
-          for (int r = 0; r < 6; r++) a.out[(3 * bead0 + r) * K + col] = mp[r];
+        if (md.is_root && a.roots)
+          for (int r = 0; r < 6; r++) a.roots[6 * (int64_t)h.body + r] = mp[r];
 #pragma unroll
         for (int r = 0; r < 6; r++) MT[6 * q + r] = mp[r];
       }
@@ -918,7 +917,7 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
       const uint32_t d = smem_u32(RT + 6 * q);
       for (int r = 0; r < rr; r++) cp_async8_u32(d + 8u * r, src + r * K);
       if (md.is_root)
-        for (int r = 0; r < 6; r++) MT[6 * q + r] = (a.op == RQ_OP_QTV) ? a.in[(3 * bead0 + r) * K + col] : 0.0;
+        for (int r = 0; r < 6; r++) MT[6 * q + r] = a.roots ? a.roots[6 * (int64_t)h.body + r] : 0.0;
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -957,17 +956,6 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
       __syncthreads();
     }
   }
-}
-
-// single-bead bodies: Qv and Q^T w are the identity (matfree.py:99-100, 127-128)
-__global__ void k_small(const int32_t *bodies, int64_t n, const int64_t *bead_off, const double *in,
-                        double *out, int64_t K, int64_t col) {
-
-  pdl_wait();
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= 3 * n) return;
-  int64_t row = 3 * bead_off[bodies[t / 3]] + t % 3;
-  out[row * K + col] = in[row * K + col];
 }
 
 template <class... KArgs, class... Args>
@@ -1067,6 +1055,30 @@ __global__ void k_transpose(const double *src, int64_t R, int64_t Cn, double *ds
   }
 }
 
+// Q layout <-> private residue layout + roots (one thread per row of the Q layout)
+__global__ void k_expand(const double *res, const double *roots, const double *in, const int32_t *body_of,
+                         const int64_t *bead_off, const int64_t *res_base, int64_t rows, double *out) {
+  pdl_wait();
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int j = body_of[row / 3];
+  const int64_t b0 = bead_off[j], loc = row - 3 * b0;
+  if (bead_off[j + 1] - b0 == 1) out[row] = in[row];
+  else out[row] = loc < 6 ? roots[6 * (int64_t)j + loc] : res[res_base[j] + loc - 6];
+}
+__global__ void k_compress(const double *in, const int32_t *body_of, const int64_t *bead_off, const int64_t *res_base,
+                           int64_t rows, double *res, double *roots, double *out) {
+  pdl_wait();
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int j = body_of[row / 3];
+  const int64_t b0 = bead_off[j], loc = row - 3 * b0;
+  const double v = in[row];
+  if (bead_off[j + 1] - b0 == 1) out[row] = v;
+  else if (loc < 6) roots[6 * (int64_t)j + loc] = v;
+  else res[res_base[j] + loc - 6] = v;
+}
+
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases,
                BodyRange range) {
   if (op < 0 || op > 3) throw Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
@@ -1084,7 +1096,8 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     run_apply_mrhs(p, op, in, out, k, s, phases, range);
     return;
   }
-  if (k > 1 && range.j1 < 0 && !getenv("RQ_COLLOOP_STRIDED")) {
+  if (k > 1) {
+    if (range.j1 >= 0) throw Error(RQ_ERR_VALUE, "body ranges need k == 1");
     // Column loop on contiguous columns: transpose the (rows, k) block once, run the K = 1
     // kernels column by column, transpose back (a strided column costs 4x the sectors)
     const bool in_comp = op == RQ_OP_QTILDE_TV, out_comp = op == RQ_OP_QTILDE_V;
@@ -1101,38 +1114,58 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   }
   const bool up = (op == RQ_OP_QV || op == RQ_OP_QTILDE_V);
   const bool all = range.j1 < 0;
+  // Q / Q^T run through the private residue layout (Plan::res_base) plus 6 root rows per
+  // body: k_compress splits Q^T's input, k_expand assembles Qv (n = 1 bodies: identity,
+  // matfree.py:99-100, 127-128); the sweep kernels themselves only know that layout.
+  const bool full = op == RQ_OP_QV || op == RQ_OP_QTV;
+  double *roots = nullptr;
+  const double *cin = in;
+  double *cout = out;
+  const int64_t rows3 = 3 * p.N;
+  if (full) {
+    if (!all) throw Error(RQ_ERR_VALUE, "body ranges need a complement operator");
+    if (ss.roots.bytes < (size_t)(48 * p.m)) ss.roots.alloc(48 * p.m);
+    const int64_t rt = std::max<int64_t>(1, p.res_base[p.m]);
+    if (ss.res_tmp.bytes < (size_t)(8 * rt)) ss.res_tmp.alloc(8 * rt);
+    roots = ss.roots.as<double>();
+    if (up) {
+      cout = ss.res_tmp.as<double>();
+    } else {
+      if (phases & 4u)
+        launch_pdl(k_compress, (unsigned)((rows3 + 255) / 256), 256, 0, s, in, (const int32_t *)p.body_of.as<int32_t>(),
+                   (const int64_t *)p.bead_off_d.as<int64_t>(), (const int64_t *)p.res_base_d.as<int64_t>(), rows3,
+                   ss.res_tmp.as<double>(), roots, out);
+      cin = ss.res_tmp.as<double>();
+    }
+  }
+  static const bool old_chunks = getenv("RQ_WAVE") && atoi(getenv("RQ_WAVE")) == 0;  // A/B comparison only
+  const bool wave = p.wave_streams > 0 && all && !old_chunks;
   const int64_t j0 = all ? 0 : range.j0, j1 = all ? p.m : range.j1;
   const int64_t c0 = all ? 0 : p.h_chunk_first[j0], c1 = all ? p.n_chunks : p.h_chunk_first[j1];
   const int64_t tb0 = all ? 0 : p.h_topblob_first[j0], tb1 = all ? p.n_topblob : p.h_topblob_first[j1];
-  const int64_t sm0 = all ? 0 : p.h_small_first[j0], sm1 = all ? p.n_small : p.h_small_first[j1];
   ApplyCtx a{};
-  a.chunks = p.chunks.as<ChunkDesc>() + c0;
-  a.tiles = p.tiles.as<TileDesc>();
-  a.blob = p.blob.as<uint8_t>();
-  a.n_chunks = c1 - c0;
-  a.bead_off = p.bead_off_d.as<int64_t>();
-  a.in = in;
-  a.out = out;
-  a.k = k;
-  a.scratch = ss.scratch.as<double>();
-  a.op = op;
-  KernelCfg cfg = chunk_cfg(p, up, a);
-  if (!ss.chunk_ctr.p) {  // claim/done counters start at zero and reset themselves
-    ss.chunk_ctr.alloc(4 * sizeof(unsigned long long));
-    RQ_CUDA(cudaMemsetAsync(ss.chunk_ctr.p, 0, 4 * sizeof(unsigned long long), s));
-  }
-  if (up && tb1 > tb0 && !getenv("RQ_NO_TOP_L2")) {  // the top pass that follows reads these blobs
-    a.l2_next = p.topblob.as<uint8_t>() + p.h_topblob_off[tb0];
-    a.l2_next_bytes = p.h_topblob_off[tb1] - p.h_topblob_off[tb0];
-  }
-  a.pf_dist = 1;
-  if (const char *e = getenv("RQ_PF_DIST")) a.pf_dist = std::max(1, std::min(8, atoi(e)));
-  static const bool timing = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
-  DBuf dbg;
-  if (timing) {
-    dbg.alloc((size_t)cfg.grid * 256 + 64);
-    RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 256 + 64, s));
-    a.dbg = dbg.as<long long>();
+  KernelCfg cfg;
+  if (!wave) {
+    a.chunks = p.chunks.as<ChunkDesc>() + c0;
+    a.tiles = p.tiles.as<TileDesc>();
+    a.blob = p.blob.as<uint8_t>();
+    a.n_chunks = c1 - c0;
+    a.bead_off = p.bead_off_d.as<int64_t>();
+    a.in = cin;
+    a.out = cout;
+    a.k = 1;
+    a.scratch = ss.scratch.as<double>();
+    a.op = up ? RQ_OP_QTILDE_V : RQ_OP_QTILDE_TV;
+    cfg = chunk_cfg(p, up, a);
+    if (!ss.chunk_ctr.p) {  // claim/done counters start at zero and reset themselves
+      ss.chunk_ctr.alloc(4 * sizeof(unsigned long long));
+      RQ_CUDA(cudaMemsetAsync(ss.chunk_ctr.p, 0, 4 * sizeof(unsigned long long), s));
+    }
+    if (up && tb1 > tb0) {  // the top pass that follows reads these blobs
+      a.l2_next = p.topblob.as<uint8_t>() + p.h_topblob_off[tb0];
+      a.l2_next_bytes = p.h_topblob_off[tb1] - p.h_topblob_off[tb0];
+    }
+    a.pf_dist = 1;
   }
   TopDfCtx t{};
   const int64_t ts0 = all ? 0 : p.h_topstart_first[j0], ts1 = all ? p.n_top_start : p.h_topstart_first[j1];
@@ -1147,120 +1180,73 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.perm = p.perm.as<int32_t>();
   t.bead_off = p.bead_off_d.as<int64_t>();
   t.rec = p.rec.as<double>();
-  t.in = in;
-  t.out = out;
-  t.k = k;
+  t.in = cin;
+  t.out = cout;
+  t.k = 1;
+  t.col = 0;
   t.scratch = ss.scratch.as<double>();
-  t.op = op;
+  t.res_base = p.res_base_d.as<int64_t>();
+  t.roots = roots;
   t.S = p.tile_leaves;
   Top2Ctx t2{};
-  static const bool timing_top = RQ_TIMING && getenv("RQ_TIMING") != nullptr;
-  DBuf dbg2;
-  if (timing_top && p.n_topblob) {
-    dbg2.alloc((size_t)p.n_topblob * 64);
-    RQ_CUDA(cudaMemsetAsync(dbg2.p, 0, (size_t)p.n_topblob * 64, s));
-    t2.dbg = dbg2.as<long long>() + 8 * tb0;
-  }
   t2.blob = p.topblob.as<uint8_t>();
   t2.blob_off = p.topblob_off.as<int64_t>() + tb0;
   t2.cls = p.topblob_class.as<uint8_t>() + tb0;
   t2.bead_off = p.bead_off_d.as<int64_t>();
-  t2.in = in;
-  t2.out = out;
-  t2.k = k;
+  t2.in = cin;
+  t2.out = cout;
+  t2.k = 1;
+  t2.col = 0;
   t2.scratch = ss.scratch.as<double>();
-  t2.op = op;
-  if (p.n_topblob) {
+  t2.res_base = p.res_base_d.as<int64_t>();
+  t2.roots = roots;
+  if (p.n_topblob && !p.top_attr_set) {
     for (const void *f2 : {(const void *)k_top2<true, 32>, (const void *)k_top2<false, 32>,
                            (const void *)k_top2<true, 128>, (const void *)k_top2<false, 128>})
       RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.max_topblob_smem));
+    p.top_attr_set = true;
   }
-  for (int64_t col = 0; col < k; col++) {
-    a.col = col;
-    t.col = col;
-    t2.col = col;
-    const bool do_chunks = (phases & 1u) && a.n_chunks > 0, do_top = (phases & 2u) && (tb1 > tb0 || t.n > 0);
-    auto top_pass = [&]() {
-      for (int c = 0; c < 4 && tb1 > tb0; c++) {
-        if (!p.topclass_count[c]) continue;
-        t2.want = c;
-        const size_t sm = (size_t)p.topclass_smem[c];
-        if (c < 2) {
-          if (up) launch_pdl(k_top2<true, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
-          else launch_pdl(k_top2<false, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
-        } else {
-          if (up) launch_pdl(k_top2<true, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
-          else launch_pdl(k_top2<false, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
-        }
+  const bool do_chunks = (phases & 1u) && (wave ? p.wave_streams > 0 : a.n_chunks > 0);
+  const bool do_top = (phases & 2u) && (tb1 > tb0 || t.n > 0);
+  auto top_pass = [&]() {
+    for (int c = 0; c < 4 && tb1 > tb0; c++) {
+      if (!p.topclass_count[c]) continue;
+      t2.want = c;
+      const size_t sm = (size_t)p.topclass_smem[c];
+      if (c < 2) {
+        if (up) launch_pdl(k_top2<true, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
+        else launch_pdl(k_top2<false, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
+      } else {
+        if (up) launch_pdl(k_top2<true, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
+        else launch_pdl(k_top2<false, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
       }
-      if (t.n > 0) {
-        const unsigned nb = (unsigned)((t.n + NT_TOP - 1) / NT_TOP);
-        if (up) launch_pdl(k_top_df_up, nb, NT_TOP, 0, s, t);
-        else launch_pdl(k_top_df_down, nb, NT_TOP, 0, s, t);
-      }
-    };
-    if (up) {
-      if (do_chunks) {
-        a.ctr = ss.chunk_ctr.as<unsigned long long>() + 2 * (ss.chunk_epoch++ & 1u);
-        launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
-      }
-      if (do_top) top_pass();
-      if (timing_top && do_top && p.n_topblob) {
-        std::vector<long long> h((size_t)p.n_topblob * 8);
-        RQ_CUDA(cudaMemcpyAsync(h.data(), dbg2.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
-        RQ_CUDA(cudaStreamSynchronize(s));
-        double acc[6] = {0};
-        long long t_min = LLONG_MAX, t_max = 0, e_max = 0;
-        double dur = 0;
-        for (int64_t b = 0; b < p.n_topblob; b++) {
-          for (int i = 0; i < 6; i++) acc[i] += (double)h[8 * b + i];
-          t_min = std::min(t_min, h[8 * b + 6]);
-          t_max = std::max(t_max, h[8 * b + 6]);
-          e_max = std::max(e_max, h[8 * b + 7]);
-          dur += (double)(h[8 * b + 7] - h[8 * b + 6]);
-        }
-        fprintf(stderr, "[rq timing] k_top2 UP timeline: CTA starts spread %.1f us, last end %.1f us after first start, mean CTA duration %.1f us\n",
-                (t_max - t_min) / 1e3, (e_max - t_min) / 1e3, dur / (double)p.n_topblob / 1e3);
-        const double nb = (double)p.n_topblob;
-        fprintf(stderr, "[rq timing] k_top2 UP per CTA: blob wait %.0f, inputs %.0f, levels %.0f (%.1f levels, %.0f nodes, %.0f inputs); CTA start spread %lld cycles\n",
-                acc[0] / nb, acc[1] / nb, acc[2] / nb, acc[3] / nb, acc[4] / nb, acc[5] / nb, t_max - t_min);
-      }
+    }
+    if (t.n > 0) {
+      const unsigned nb = (unsigned)((t.n + NT_TOP - 1) / NT_TOP);
+      if (up) launch_pdl(k_top_df_up, nb, NT_TOP, 0, s, t);
+      else launch_pdl(k_top_df_down, nb, NT_TOP, 0, s, t);
+    }
+  };
+  auto sweep = [&]() {
+    if (!do_chunks) return;
+    if (wave) {
+      run_wave(p, up, cin, cout, ss.scratch.as<double>(), roots, s);
     } else {
-      if (do_top) top_pass();
-      if (do_chunks) {
-        a.ctr = ss.chunk_ctr.as<unsigned long long>() + 2 * (ss.chunk_epoch++ & 1u);
-        launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
-      }
+      a.ctr = ss.chunk_ctr.as<unsigned long long>() + 2 * (ss.chunk_epoch++ & 1u);
+      launch_pdl(cfg.fn, (unsigned)cfg.grid, (unsigned)cfg.threads, cfg.smem, s, a);
     }
-    if (timing && do_chunks) {
-      std::vector<long long> h((size_t)cfg.grid * 16 + 8);
-      RQ_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
-      RQ_CUDA(cudaStreamSynchronize(s));
-      double acc[8] = {0};
-      for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) acc[i] += (double)h[8 * g + i];
-      fprintf(stderr, "[rq timing] op %d grid %d smem %zu threads %d: per level step: rec wait %.0f node(tid0) %.0f level-total %.0f | per chunk: head+vec wait %.0f, slowest-warp/step %.0f, level steps %.1f, chunks/CTA %.1f, CTA total %.0f (max %.0f)\n",
-              op, cfg.grid, cfg.smem, cfg.threads, acc[0] / acc[4], acc[1] / acc[4], acc[2] / acc[4], acc[3] / acc[6],
-              acc[5] / acc[4], acc[4] / acc[6], acc[6] / cfg.grid, acc[7] / cfg.grid, [&] { double mx = 0; for (int g = 0; g < cfg.grid; g++) mx = std::max(mx, (double)h[8 * g + 7]); return mx; }());
-      {  // load balance of the static round-robin chunk assignment
-        long long smax = 0, smin = LLONG_MAX, tmin = LLONG_MAX;
-        for (int g = 0; g < cfg.grid; g++) {
-          smax = std::max(smax, h[8 * g + 4]);
-          smin = std::min(smin, h[8 * g + 4]);
-          tmin = std::min(tmin, h[8 * g + 7]);
-        }
-        fprintf(stderr, "[rq timing] level steps per CTA: mean %.1f min %lld max %lld; CTA total cycles min %lld\n",
-                acc[4] / cfg.grid, smin, smax, tmin);
-      }
-      double gs[8] = {0};
-      for (int g = 0; g < cfg.grid; g++) for (int i = 0; i < 8; i++) gs[i] += (double)h[8 * (cfg.grid + g) + i];
-      fprintf(stderr, "[rq timing] slowest warp finish after step start, per group (avg over steps where present): GEN %.0f (%.0f) RB %.0f (%.0f) BB %.0f (%.0f) idle %.0f (%.0f)\n",
-              gs[0] / std::max(1.0, gs[4]), gs[4], gs[1] / std::max(1.0, gs[5]), gs[5], gs[2] / std::max(1.0, gs[6]), gs[6], gs[3] / std::max(1.0, gs[7]), gs[7]);
-      RQ_CUDA(cudaMemsetAsync(dbg.p, 0, (size_t)cfg.grid * 256 + 64, s));
-    }
-    if ((phases & 4u) && sm1 > sm0 && op <= 1)
-      launch_pdl(k_small, (unsigned)((3 * (sm1 - sm0) + 255) / 256), 256, 0, s, p.small_bodies.as<int32_t>() + sm0,
-                 (int64_t)(sm1 - sm0), (const int64_t *)p.bead_off_d.as<int64_t>(), in, out, (int64_t)k, (int64_t)col);
+  };
+  if (up) {
+    sweep();
+    if (do_top) top_pass();
+  } else {
+    if (do_top) top_pass();
+    sweep();
   }
+  if (full && up && (phases & 4u))
+    launch_pdl(k_expand, (unsigned)((rows3 + 255) / 256), 256, 0, s, (const double *)ss.res_tmp.as<double>(),
+               (const double *)roots, in, (const int32_t *)p.body_of.as<int32_t>(),
+               (const int64_t *)p.bead_off_d.as<int64_t>(), (const int64_t *)p.res_base_d.as<int64_t>(), rows3, out);
   RQ_CUDA(cudaGetLastError());
 }
 
@@ -1277,76 +1263,16 @@ void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_
       RQ_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
   }
   const bool in_comp = op == RQ_OP_QTILDE_TV, out_comp = op == RQ_OP_QTILDE_V;
-  auto rows = [&](bool comp, int64_t j) { return 3 * p.bead_off[j] - (comp ? 6 * j : 0); };
-  const size_t bi = (size_t)rows(in_comp, p.m) * k * 8, bo = (size_t)rows(out_comp, p.m) * k * 8;
+  const int64_t ri = 3 * p.N - (in_comp ? 6 * p.m : 0), ro = 3 * p.N - (out_comp ? 6 * p.m : 0);
+  const size_t bi = (size_t)ri * k * 8, bo = (size_t)ro * k * 8;
   if (p.stage_in.bytes < bi) p.stage_in.alloc(bi);
   if (p.stage_out.bytes < bo) p.stage_out.alloc(bo);
-  // segments of roughly equal bead count (at least seg_mb MB of vector data each)
-  int64_t max_seg = 8, seg_mb = 2;
-  if (const char *e = getenv("RQ_HOST_SEGS")) max_seg = std::max(1, atoi(e));
-  if (const char *e = getenv("RQ_HOST_SEG_MB")) seg_mb = std::max(1, atoi(e));
-  const int64_t seg_target = std::max<int64_t>(1, std::min<int64_t>(max_seg, (int64_t)(bi / ((size_t)seg_mb << 20))));
-  std::vector<int64_t> cuts{0};
-  for (int64_t s = 1; s < seg_target; s++) {
-    const int64_t target = p.bead_off[p.m] * s / seg_target;
-    int64_t j = (int64_t)(std::lower_bound(p.bead_off.begin(), p.bead_off.end(), target) - p.bead_off.begin());
-    j = std::min<int64_t>(std::max<int64_t>(j, cuts.back()), p.m);
-    if (j > cuts.back() && j < p.m) cuts.push_back(j);
-  }
-  cuts.push_back(p.m);
-  const int nseg = (int)cuts.size() - 1;
-  static const bool trace = getenv("RQ_HOST_TRACE") != nullptr;  // diagnostics: per-stage timeline
-  std::vector<cudaEvent_t> ev_in(nseg), ev_k(nseg), ev_o(nseg);
-  cudaEvent_t ev0 = nullptr;
-  const unsigned evf = trace ? 0u : cudaEventDisableTiming;
-  for (int i = 0; i < nseg; i++) {
-    RQ_CUDA(cudaEventCreateWithFlags(&ev_in[i], evf));
-    RQ_CUDA(cudaEventCreateWithFlags(&ev_k[i], evf));
-    if (trace) RQ_CUDA(cudaEventCreate(&ev_o[i]));
-  }
-  if (trace) {
-    RQ_CUDA(cudaEventCreate(&ev0));
-    RQ_CUDA(cudaEventRecord(ev0, p.host_stream));
-  }
-  cudaStream_t s_in = p.host_stream, s_k = p.host_stream2, s_out = p.host_stream3;
-  static const unsigned host_phases = getenv("RQ_HOST_PHASES") ? (unsigned)atoi(getenv("RQ_HOST_PHASES")) : 7u;  // diagnostics
+  cudaStream_t s_k = p.host_stream2;
   double *din = p.stage_in.as<double>(), *dout = p.stage_out.as<double>();
-  // every H2D is queued first, so the host-to-device engine never waits for the host to
-  // finish enqueueing a segment's kernels
-  for (int i = 0; i < nseg; i++) {
-    const int64_t r0 = rows(in_comp, cuts[i]), r1 = rows(in_comp, cuts[i + 1]);
-    RQ_CUDA(cudaMemcpyAsync(din + r0 * k, in + r0 * k, (size_t)(r1 - r0) * k * 8, cudaMemcpyHostToDevice, s_in));
-    RQ_CUDA(cudaEventRecord(ev_in[i], s_in));
-  }
-  for (int i = 0; i < nseg; i++) {
-    const int64_t j0 = cuts[i], j1 = cuts[i + 1];
-    RQ_CUDA(cudaStreamWaitEvent(s_k, ev_in[i], 0));
-    BodyRange br;
-    br.j0 = j0;
-    br.j1 = j1;
-    run_apply(p, op, din, dout, k, s_k, host_phases, br);
-    RQ_CUDA(cudaEventRecord(ev_k[i], s_k));
-    RQ_CUDA(cudaStreamWaitEvent(s_out, ev_k[i], 0));
-    const int64_t o0 = rows(out_comp, j0), o1 = rows(out_comp, j1);
-    RQ_CUDA(cudaMemcpyAsync(out + o0 * k, dout + o0 * k, (size_t)(o1 - o0) * k * 8, cudaMemcpyDeviceToHost, s_out));
-    if (trace) RQ_CUDA(cudaEventRecord(ev_o[i], s_out));
-  }
-  RQ_CUDA(cudaStreamSynchronize(s_out));
-  if (trace) {
-    for (int i = 0; i < nseg; i++) {
-      float a = 0, b = 0, c = 0;
-      cudaEventElapsedTime(&a, ev0, ev_in[i]);
-      cudaEventElapsedTime(&b, ev0, ev_k[i]);
-      cudaEventElapsedTime(&c, ev0, ev_o[i]);
-      fprintf(stderr, "[rq host] seg %d: h2d done %.3f  kernels done %.3f  d2h done %.3f ms\n", i, a, b, c);
-      cudaEventDestroy(ev_o[i]);
-    }
-    cudaEventDestroy(ev0);
-  }
-  for (int i = 0; i < nseg; i++) {
-    cudaEventDestroy(ev_in[i]);
-    cudaEventDestroy(ev_k[i]);
-  }
+  RQ_CUDA(cudaMemcpyAsync(din, in, bi, cudaMemcpyHostToDevice, s_k));
+  run_apply(p, op, din, dout, k, s_k);
+  RQ_CUDA(cudaMemcpyAsync(out, dout, bo, cudaMemcpyDeviceToHost, s_k));
+  RQ_CUDA(cudaStreamSynchronize(s_k));
 }
 
 }  // namespace rq

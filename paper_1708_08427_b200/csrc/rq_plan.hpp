@@ -12,6 +12,7 @@
 
 #include "rigidq_b200.h"
 #include "rq_internal.cuh"
+#include "rq_wave.cuh"
 
 namespace rq {
 
@@ -184,6 +185,8 @@ struct Plan {
     DBuf scratch, mrhs_scratch, top_cnt;
     DBuf chunk_ctr;           // 2 x {claim, done} counters of the dynamic chunk schedule
     DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
+    DBuf res_tmp, roots;      // Q / Q^T: residues in the private layout and the 6 root rows per body
+    DBuf zpart;               // Zf per-segment partial sums
     uint32_t chunk_epoch = 0;  // chunk launches so far (consecutive launches alternate counters)
   };
   mutable std::mutex state_mu;
@@ -199,6 +202,22 @@ struct Plan {
   mutable int mrhs_depth_tile = 1, mrhs_depth_top = 1;
   mutable DBuf mrhs_units, mrhs_prog;
   mutable std::vector<int64_t> h_tile_unit_first, h_top_unit_first;
+  // private residue layout: body j's residues start at res_base[j] = sum_{i<j} max(0, 3 n_i - 6)
+  // (the Q~ layout when every body has n >= 2; Q / Q^T go through it plus 6 root rows per body)
+  std::vector<int64_t> res_base;   // host copy, m+1
+  DBuf res_base_d;                 // int64 [m+1]
+  // wavefront apply streams (rq_wave.cu)
+  int64_t wave_streams = 0, wave_steps = 0, wave_blob_bytes = 0, wave_nodes = 0;
+  int64_t wave_up_bytes = 0, wave_down_bytes = 0;  // bytes one upward / downward sweep streams
+  int64_t wave_stage_bytes = 0, wave_rounds = 1;
+  int wave_mslots = 0, wave_pf = 0, wave_nst = 2;  // L2 prefetch distance, TMA stages
+  WaveCaps wave_caps;
+  DBuf wave_desc;                  // StepDesc [wave_steps]
+  DBuf wave_stream_first;          // int64 [wave_streams + 1]
+  DBuf wave_blob;                  // step blocks
+  mutable bool wave_ready = false;
+  mutable bool top_attr_set = false;  // k_top2 shared-memory attribute set
+  mutable int wave_ctas_per_sm = 0;
   int64_t device_bytes() const;
   ~Plan() {
     for (cudaStream_t st : {host_stream, host_stream2, host_stream3})
@@ -208,6 +227,21 @@ struct Plan {
 
 void build_plan(Plan &p, const double *pos, const int64_t *offsets, int64_t m, int max_depth,
                 bool host_input, cudaStream_t s);
+struct WaveBuildIn {
+  int64_t n_tiles;
+  const int64_t *tile_root;  // global node id of every tile root, in tile order
+  const int64_t *node_off, *bead_off, *rec_off, *res_base;
+  const int32_t *node_body, *start, *stop, *left, *right, *parent, *height, *res_off, *perm, *slot_scan;
+  const uint8_t *flags;
+  const double *rec;
+};
+void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s);
+size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg);
+void wave_prepare(const Plan &p);
+// tile part of one upward / downward sweep over all bodies (rq_wave.cu); residues in the
+// private layout, body-root vectors to / from `roots` (nullptr: dropped / zero)
+void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots,
+              cudaStream_t s);
 // bodies [j0, j1) of a plan (all work lists are in body order)
 struct BodyRange {
   int64_t j0 = 0, j1 = -1;  // j1 < 0: all bodies

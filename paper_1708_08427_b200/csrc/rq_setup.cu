@@ -784,6 +784,11 @@ __global__ void k_tile_keys(const TileTmp *tiles, int64_t n, bool desc, uint64_t
   val[t] = (int32_t)t;
 }
 
+__global__ void k_tile_roots(const TileTmp *tiles, int64_t n, int64_t *roots) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) roots[t] = tiles[t].root;
+}
+
 __global__ void k_tile_permute(const TileTmp *tiles, const int32_t *order, int64_t n, TileTmp *sorted, int32_t *inv) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
@@ -1204,7 +1209,8 @@ int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
                         &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog};
+                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
+                        &res_base_d, &wave_desc, &wave_stream_first, &wave_blob};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
   return s;
@@ -1258,6 +1264,10 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
 
   p.bead_off_d.alloc((m + 1) * 8);
   p.node_off_d.alloc((m + 1) * 8);
+  p.res_base.assign(m + 1, 0);
+  for (int64_t j = 0; j < m; j++) p.res_base[j + 1] = p.res_base[j] + std::max<int64_t>(0, 3 * (offsets[j + 1] - offsets[j]) - 6);
+  p.res_base_d.alloc((m + 1) * 8);
+  RQ_CUDA(cudaMemcpyAsync(p.res_base_d.p, p.res_base.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
   RQ_CUDA(cudaMemcpyAsync(p.bead_off_d.p, offsets, (m + 1) * 8, cudaMemcpyHostToDevice, s));
   RQ_CUDA(cudaMemcpyAsync(p.node_off_d.p, node_off.data(), (m + 1) * 8, cudaMemcpyHostToDevice, s));
   p.pos_orig.alloc(N * 24);
@@ -1725,6 +1735,20 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     }
 
     tm.mark("chunks+blob");
+    // wavefront streams over the same tiles
+    {
+      DBuf troots;
+      troots.alloc(std::max<int64_t>(n_tiles_all, 1) * 8);
+      if (n_tiles_all) k_tile_roots<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all, troots.as<int64_t>());
+      WaveBuildIn wi{n_tiles_all,           troots.as<int64_t>(),      noff,
+                     boff,                  p.rec_off.as<int64_t>(),   p.res_base_d.as<int64_t>(),
+                     node_body.as<int32_t>(), p.start.as<int32_t>(),   p.stop.as<int32_t>(),
+                     p.left.as<int32_t>(),  p.right.as<int32_t>(),     p.parent.as<int32_t>(),
+                     p.height.as<int32_t>(), p.res_off.as<int32_t>(),  p.perm.as<int32_t>(),
+                     slot_scan.as<int32_t>(), p.flags.as<uint8_t>(),   p.rec.as<double>()};
+      build_wave(p, wi, s);
+    }
+    tm.mark("wave");
     // top tree
     {
       std::vector<int64_t> topbodies;

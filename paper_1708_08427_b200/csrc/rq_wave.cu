@@ -1,0 +1,1047 @@
+// rq_wave.cu -- wavefront apply streams: layout builder and sweep kernel.
+//
+// Restates the tile part of upward_apply (Algorithm 2, matfree.py:95-121,
+// merge_infosets matfree.py:41-62) and downward_apply (Algorithm 3,
+// matfree.py:124-151, split_rvset matfree.py:65-83).  The nodes above the
+// tiles (per-body top trees) stay with k_top2 / k_top_df (rq_apply.cu).
+//
+// Layout (rq_wave.cuh): the tiles (maximal subtrees with <= S beads, in body
+// order) are split into G contiguous streams of about equal node count, one
+// per persistent CTA.  Inside a stream the tiles are placed greedily: tile t
+// enters at the earliest step e_t >= e_{t-1} at which every one of its height
+// levels fits the per-step capacities (WaveCaps), and its height-h nodes run at
+// step e_t + h - 1.  Every node's children therefore run at earlier steps.
+// Each node's 6-vector (upward output / downward RV-set) lives in one of M
+// shared-memory slots from its producer's step to its consumer's step; the
+// slots are assigned per stream by interval colouring (lowest free slot),
+// which is optimal for interval graphs, so M = the stream's peak live count.
+//
+// Kernel k_wave<UP> (128 threads, one CTA per stream): per step, one TMA bulk
+// copy of the block (issued two steps ahead into a 2-stage ring, L2-prefetched
+// pf steps ahead), gathers for step +2 (cp.async into a 3-region ring), the
+// case-uniform node pass (warp 0 GENERAL, warp 1 RIGID_BEAD, warps 2-3
+// BEAD_BEAD), one CTA barrier.  Outputs go straight to global memory
+// (residues upward, bead velocities downward); tile-root 6-vectors go to the
+// exchange slots the top-tree kernels read.  No tensor cores: HBM-bound sweep
+// of tiny fp64 orthogonal transforms.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "rq_nodeops.cuh"
+#include "rq_plan.hpp"
+#include "rq_wave.cuh"
+
+namespace rq {
+namespace {
+
+constexpr int NT = 256;
+inline size_t al128(size_t x) { return (x + 127) / 128 * 128; }
+inline unsigned nblk(int64_t n, int t = NT) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+template <class In, class Out>
+void ex_scan(const In *in, Out *out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  size_t tb = 0;
+  RQ_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s));
+  DBuf tmp;
+  tmp.alloc(tb);
+  RQ_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, s));
+}
+template <class T>
+void d2h(T *dst, const void *src, size_t count, cudaStream_t s) {
+  RQ_CUDA(cudaMemcpyAsync(dst, src, count * sizeof(T), cudaMemcpyDeviceToHost, s));
+  RQ_CUDA(cudaStreamSynchronize(s));
+}
+template <class T>
+T d2h1(const void *src, cudaStream_t s) {
+  T v;
+  d2h(&v, src, 1, s);
+  return v;
+}
+
+// ---- builder ---------------------------------------------------------------------
+
+struct TLev {  // one height level of a tile (its requirements on a step)
+  int16_t g, r, b, beads, vd, dg;
+  int32_t rm;
+};
+
+struct NodeArrays {
+  const int64_t *node_off, *bead_off, *rec_off, *res_base;
+  const int32_t *node_body, *start, *stop, *left, *right, *parent, *height, *res_off, *perm, *slot_scan;
+  const uint8_t *flags;
+};
+
+__device__ __forceinline__ int nodeL(const NodeArrays &A, int64_t g) { return A.stop[g] - A.start[g]; }
+
+// per tile: internal node count and height (0 for singleton tiles)
+__global__ void k_wv_tiles(const int64_t *tile_root, int64_t nt, NodeArrays A, int64_t *tnodes, int64_t *theight) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int64_t g = tile_root[t];
+  const int L = nodeL(A, g);
+  tnodes[t] = L >= 2 ? L - 1 : 0;
+  theight[t] = L >= 2 ? A.height[g] : 0;
+}
+
+__device__ __forceinline__ int wv_rank(int cs) { return cs == GENERAL ? 0 : (cs == RIGID_BEAD ? 1 : 2); }
+__device__ __forceinline__ int wv_beads(int cs) { return cs == BEAD_BEAD ? 2 : (cs == RIGID_BEAD ? 1 : 0); }
+
+// per tile level profile; node -> tile map
+__global__ void k_wv_profile(const int64_t *tile_root, int64_t nt, NodeArrays A, const int64_t *tl_base, TLev *tl,
+                             int32_t *node_tile, WaveCaps caps, int *bad) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int64_t g = tile_root[t];
+  const int L = nodeL(A, g);
+  if (L < 2) return;
+  const int64_t first = g - 2 * (int64_t)L + 2;
+  TLev *P = tl + tl_base[t];
+  for (int64_t q = first; q <= g; q++) {
+    if (nodeL(A, q) < 2) continue;
+    node_tile[q] = (int32_t)t;
+    const int cs = flag_case(A.flags[q]);
+    TLev &v = P[A.height[q] - 1];
+    if (cs == GENERAL) v.g++;
+    else if (cs == RIGID_BEAD) v.r++;
+    else v.b++;
+    v.beads += wv_beads(cs);
+    const int root = q == g;
+    v.vd += res_rows(cs) + 6 * root;
+    v.dg += (res_rows(cs) > 0) + root;
+    v.rm += 8 * rec_size(cs) + 16;
+  }
+  for (int h = 0; h < A.height[g]; h++) {
+    const TLev &v = P[h];
+    if (v.g > caps.g || v.r > caps.r || v.b > caps.b || v.beads > caps.beads || v.vd > caps.vd || v.dg > caps.dg ||
+        v.rm > caps.rm)
+      atomicExch(bad, 1);
+  }
+}
+
+// Stream of each tile.  The tile list (body order) is cut into R rounds of equal node count
+// and every round into G contiguous ranges; stream c takes range c of every round, round
+// after round.  All CTAs therefore work inside the same round at any time, so the vector
+// rows of the bodies in flight (gathers, scattered outputs) stay L2-resident while their
+// 32-byte sectors are shared by neighbouring beads.
+__global__ void k_wv_tile_key(const int64_t *node_scan, int64_t nt, int64_t total, int64_t G, int64_t R,
+                              uint64_t *key, int32_t *val) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const double x = (double)node_scan[t] / (double)std::max<int64_t>(total, 1) * (double)R;  // in [0, R)
+  const int64_t r = std::min<int64_t>(R - 1, (int64_t)x);
+  const int64_t c = std::min<int64_t>(G - 1, (int64_t)((x - (double)r) * (double)G));
+  key[t] = (uint64_t)(c * R + r);
+  val[t] = (int32_t)t;
+}
+__global__ void k_wv_stream_first(const uint64_t *key, int64_t nt, int64_t R, int64_t *first) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const int64_t c = (int64_t)(key[i] / R), cp = i == 0 ? -1 : (int64_t)(key[i - 1] / R);
+  for (int64_t x = cp + 1; x <= c; x++) first[x] = i;  // streams (cp, c] start at sorted tile i
+}
+__global__ void k_wv_gather64(const int64_t *src, const int32_t *order, int64_t n, int64_t *dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[order[i]];
+}
+
+__device__ __forceinline__ bool wv_fits(const TLev &l, const TLev &v, const WaveCaps &c) {
+  return l.g + v.g <= c.g && l.r + v.r <= c.r && l.b + v.b <= c.b && l.beads + v.beads <= c.beads &&
+         l.vd + v.vd <= c.vd && l.dg + v.dg <= c.dg && l.rm + v.rm <= c.rm;
+}
+
+// one thread per stream: greedy staggered placement of its tiles
+__global__ void k_wv_place(const int64_t *sfirst, int64_t G, const int32_t *order, const int64_t *lv_scan,
+                           const int64_t *tl_base, const TLev *tl, TLev *load, const int64_t *theight,
+                           int32_t *e_tile, int64_t *n_steps, WaveCaps caps) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= G) return;
+  const int64_t i0 = sfirst[c], i1 = sfirst[c + 1];
+  TLev *LD = load + lv_scan[i0];  // room for sum of heights steps (the sequential worst case)
+  int e_prev = 0, last = 0;
+  for (int64_t i = i0; i < i1; i++) {
+    const int64_t t = order[i];
+    const int H = (int)theight[t];
+    if (H == 0) continue;
+    const TLev *P = tl + tl_base[t];
+    int e = e_prev;
+    for (;;) {
+      int h = 0;
+      while (h < H && wv_fits(LD[e + h], P[h], caps)) h++;
+      if (h == H) break;
+      e++;
+    }
+    for (int h = 0; h < H; h++) {
+      TLev &l = LD[e + h];
+      const TLev &v = P[h];
+      l.g += v.g; l.r += v.r; l.b += v.b; l.beads += v.beads; l.vd += v.vd; l.dg += v.dg; l.rm += v.rm;
+    }
+    e_tile[t] = e;
+    e_prev = e;
+    last = max(last, e + H);
+  }
+  n_steps[c] = last + 4;  // two gather-only steps at each end
+}
+
+// sort key of every tile node: (global step, case rank)
+__global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, const int64_t *stream_of_tile_first,
+                          const int64_t *step_first, const int32_t *e_tile, uint64_t *keys, int32_t *vals,
+                          const int32_t *tile_stream) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= NN) return;
+  uint64_t key = ~0ull;
+  const int32_t t = node_tile[g];
+  if (t >= 0) {
+    const int64_t c = tile_stream[t];
+    const int64_t gs = step_first[c] + e_tile[t] + 2 + A.height[g] - 1;
+    key = ((uint64_t)gs << 2) | (uint64_t)wv_rank(flag_case(A.flags[g]));
+  }
+  keys[g] = key;
+  vals[g] = (int32_t)g;
+  (void)stream_of_tile_first;
+}
+
+__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int32_t *tile_stream) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nt) tile_stream[order[i]] = (int32_t)(key[i] / R);
+}
+
+struct StepCnt {
+  int32_t g, r, b, ug, dg;
+};
+
+// per sorted node: step counts, list counts, step of the node, per-node list sizes
+__global__ void k_wv_count(const uint64_t *keys, const int32_t *vals, int64_t n, NodeArrays A, StepCnt *sc,
+                           int64_t *step_of, int64_t *sfirst_sorted, int32_t *nb, int32_t *vd, int32_t *nd,
+                           const int32_t *node_tile, const int64_t *tile_root) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t gs = (int64_t)(keys[p] >> 2);
+  const int64_t g = vals[p];
+  const int cs = flag_case(A.flags[g]);
+  if (cs == GENERAL) atomicAdd(&sc[gs].g, 1);
+  else if (cs == RIGID_BEAD) atomicAdd(&sc[gs].r, 1);
+  else atomicAdd(&sc[gs].b, 1);
+  const int root = tile_root[node_tile[g]] == g;
+  const int beads = wv_beads(cs), dge = (res_rows(cs) > 0) + root;
+  if (beads) atomicAdd(&sc[gs - 2].ug, beads);
+  if (dge) atomicAdd(&sc[gs + 2].dg, dge);
+  step_of[g] = gs;
+  if (p == 0 || (int64_t)(keys[p - 1] >> 2) != gs) sfirst_sorted[gs] = p;
+  nb[p] = beads;
+  vd[p] = res_rows(cs) + 6 * root;
+  nd[p] = dge;
+}
+
+__global__ void k_wv_step_bytes(const StepCnt *sc, int64_t ns, int64_t *bytes, unsigned long long *mx) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  const StepCnt c = sc[s];
+  const WaveSec S = wave_sections(c.g, c.r, c.b, c.ug, c.dg);
+  bytes[s] = S.end;
+  atomicMax(&mx[0], (unsigned long long)(S.end - S.uhdr));  // upward copy
+  atomicMax(&mx[1], (unsigned long long)S.um);              // downward copy
+}
+
+__global__ void k_wv_descs(const StepCnt *sc, const int64_t *off, int64_t ns, StepDesc *d, uint8_t *blob) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  const StepCnt c = sc[s];
+  StepDesc D;
+  D.off16 = (uint32_t)(off[s] >> 4);
+  D.nG = (uint16_t)c.g; D.nR = (uint16_t)c.r; D.nB = (uint16_t)c.b;
+  D.n_ug = (uint16_t)c.ug; D.n_dg = (uint16_t)c.dg;
+  D.pad = 0;
+  d[s] = D;
+  const WaveSec S = wave_sections(D);
+  *reinterpret_cast<StepDesc *>(blob + off[s]) = D;
+  *reinterpret_cast<StepDesc *>(blob + off[s] + S.uhdr) = D;
+}
+
+// one thread per stream: interval colouring of the node 6-vectors (lowest free slot)
+constexpr int WV_MAX_SLOTS = 4096;
+__global__ void k_wv_slots(const int64_t *node_first, int64_t G, const int32_t *vals, NodeArrays A,
+                           const int64_t *step_of, const int32_t *node_tile, const int64_t *tile_root,
+                           int32_t *slot_of, int *max_slots, int *overflow, int32_t *free_all,
+                           long long *busy_all) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= G) return;
+  // free: min-heap of slot ids; busy: min-heap of (release step << 13 | slot)
+  int32_t *freeh = free_all + c * WV_MAX_SLOTS;
+  long long *busyh = busy_all + c * WV_MAX_SLOTS;
+  int nf = 0, nbz = 0, next = 0;
+  auto push_free = [&](int32_t v) {
+    int i = nf++;
+    while (i > 0) {
+      int pa = (i - 1) >> 1;
+      if (freeh[pa] <= v) break;
+      freeh[i] = freeh[pa];
+      i = pa;
+    }
+    freeh[i] = v;
+  };
+  auto pop_free = [&]() {
+    int32_t top = freeh[0], v = freeh[--nf];
+    int i = 0;
+    for (;;) {
+      int l = 2 * i + 1;
+      if (l >= nf) break;
+      int r = l + 1, m = (r < nf && freeh[r] < freeh[l]) ? r : l;
+      if (freeh[m] >= v) break;
+      freeh[i] = freeh[m];
+      i = m;
+    }
+    if (nf) freeh[i] = v;
+    return top;
+  };
+  auto push_busy = [&](long long v) {
+    int i = nbz++;
+    while (i > 0) {
+      int pa = (i - 1) >> 1;
+      if (busyh[pa] <= v) break;
+      busyh[i] = busyh[pa];
+      i = pa;
+    }
+    busyh[i] = v;
+  };
+  auto pop_busy = [&]() {
+    long long top = busyh[0], v = busyh[--nbz];
+    int i = 0;
+    for (;;) {
+      int l = 2 * i + 1;
+      if (l >= nbz) break;
+      int r = l + 1, m = (r < nbz && busyh[r] < busyh[l]) ? r : l;
+      if (busyh[m] >= v) break;
+      busyh[i] = busyh[m];
+      i = m;
+    }
+    if (nbz) busyh[i] = v;
+    return top;
+  };
+  for (int64_t p = node_first[c]; p < node_first[c + 1]; p++) {
+    const int64_t g = vals[p];
+    if (tile_root[node_tile[g]] == g) continue;  // tile roots exchange through global memory
+    const int64_t gs = step_of[g];
+    while (nbz && (busyh[0] >> 13) < gs) push_free((int32_t)(pop_busy() & 8191));
+    int32_t sl;
+    if (nf) sl = pop_free();
+    else {
+      sl = next++;
+      if (sl >= WV_MAX_SLOTS) { atomicExch(overflow, 1); return; }
+    }
+    slot_of[g] = sl;
+    const int64_t par = A.node_off[A.node_body[g]] + A.parent[g];
+    push_busy((step_of[par] << 13) | sl);
+  }
+  atomicMax(max_slots, next);
+}
+
+struct WriteIn {
+  NodeArrays A;
+  const uint64_t *keys;
+  const int32_t *vals;
+  const StepDesc *desc;
+  const int64_t *sfirst_sorted;
+  const int64_t *bscan, *vscan, *dscan;
+  const int32_t *slot_of, *node_tile;
+  const int64_t *tile_root;
+  const double *rec;
+  uint8_t *blob;
+};
+
+__global__ void k_wv_write(WriteIn w, int64_t n) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const NodeArrays &A = w.A;
+  const int64_t gs = (int64_t)(w.keys[p] >> 2);
+  const int64_t g = w.vals[p];
+  const StepDesc D = w.desc[gs];
+  const WaveSec S = wave_sections(D);
+  const int64_t pf = w.sfirst_sorted[gs];
+  const int pos = (int)(p - pf);
+  const unsigned f = A.flags[g];
+  const int cs = flag_case(f);
+  uint8_t *B = w.blob + ((int64_t)D.off16 << 4);
+  // record
+  int rq_off;
+  if (cs == GENERAL) rq_off = pos * rec_size(GENERAL);
+  else if (cs == RIGID_BEAD) rq_off = D.nG * rec_size(GENERAL) + (pos - D.nG) * rec_size(RIGID_BEAD);
+  else rq_off = D.nG * rec_size(GENERAL) + D.nR * rec_size(RIGID_BEAD) + (pos - D.nG - D.nR) * rec_size(BEAD_BEAD);
+  double *R = reinterpret_cast<double *>(B + S.rec) + rq_off;
+  const double *src = w.rec + A.rec_off[g];
+  for (int e = 0; e < rec_size(cs); e++) R[e] = src[e];
+  // children in formula order
+  const int j = A.node_body[g];
+  const int64_t nb0 = A.node_off[j], b0 = A.bead_off[j];
+  int xi = A.left[g], yi = A.right[g];
+  if (flag_swapped(f)) { const int t = xi; xi = yi; yi = t; }
+  const int64_t tr = w.tile_root[w.node_tile[g]];
+  const bool troot = tr == g;
+  const bool broot = troot && A.parent[g] < 0;
+  const uint16_t rf = (uint16_t)(troot ? (broot ? WF_BODY_ROOT : WF_TILE_ROOT) : 0);
+  // bead positions (upward gather region of this step): x bead first, then y
+  const int bpos = (int)(w.bscan[p] - w.bscan[pf]);
+  const int vpos = (int)(w.vscan[p] - w.vscan[pf]);
+  auto orig_bead = [&](int id) -> uint32_t { return (uint32_t)(b0 + A.perm[b0 + A.start[nb0 + id]]); };
+  WaveUpMeta um;
+  WaveDnMeta dm;
+  um.flags = dm.flags = (uint16_t)((f & 0x3fu) | rf);
+  um.self = dm.self = 0;
+  dm.pad = 0;
+  um.row = 0;
+  um.aux = 0;
+  if (cs == BEAD_BEAD) {
+    um.x = (uint16_t)bpos; um.y = (uint16_t)(bpos + 1);
+    dm.x = orig_bead(xi); dm.y = orig_bead(yi);
+  } else if (cs == RIGID_BEAD) {
+    um.x = (uint16_t)w.slot_of[nb0 + xi]; um.y = (uint16_t)bpos;
+    dm.x = (uint32_t)w.slot_of[nb0 + xi]; dm.y = orig_bead(yi);
+  } else {
+    um.x = (uint16_t)w.slot_of[nb0 + xi]; um.y = (uint16_t)w.slot_of[nb0 + yi];
+    dm.x = (uint32_t)w.slot_of[nb0 + xi]; dm.y = (uint32_t)w.slot_of[nb0 + yi];
+  }
+  const int rr = res_rows(cs);
+  const int64_t row = A.res_base[j] + A.res_off[g] - 6;
+  if (rr) um.row = (uint32_t)row;
+  dm.vres = (uint16_t)vpos;
+  if (troot) {
+    um.aux = broot ? (uint32_t)j : (uint32_t)A.slot_scan[g];
+    dm.self = (uint16_t)(vpos + rr);
+  } else {
+    um.self = (uint16_t)w.slot_of[g];
+    dm.self = (uint16_t)w.slot_of[g];
+  }
+  reinterpret_cast<WaveUpMeta *>(B + S.um)[pos] = um;
+  reinterpret_cast<WaveDnMeta *>(B + S.dm)[pos] = dm;
+  // upward gathers of this node's beads: held by block gs - 2
+  if (cs != GENERAL) {
+    const StepDesc Du = w.desc[gs - 2];
+    uint32_t *UG = reinterpret_cast<uint32_t *>(w.blob + ((int64_t)Du.off16 << 4) + wave_sections(Du).ug);
+    if (cs == BEAD_BEAD) { UG[bpos] = orig_bead(xi); UG[bpos + 1] = orig_bead(yi); }
+    else UG[bpos] = orig_bead(yi);
+  }
+  // downward gathers (residues, root RV-set): held by block gs + 2
+  if (rr || troot) {
+    const StepDesc Dd = w.desc[gs + 2];
+    const int64_t pfd = w.sfirst_sorted[gs];
+    int di = (int)(w.dscan[p] - w.dscan[pfd]);
+    WaveGather *DG = reinterpret_cast<WaveGather *>(w.blob + ((int64_t)Dd.off16 << 4) + 16);
+    if (rr) {
+      WaveGather e;
+      e.src = (uint32_t)row;
+      e.dst = (uint16_t)vpos;
+      e.kind = rr == 3 ? WG_RES3 : WG_RES6;
+      DG[di++] = e;
+    }
+    if (troot) {
+      WaveGather e;
+      e.src = broot ? (uint32_t)j : (uint32_t)A.slot_scan[g];
+      e.dst = (uint16_t)(vpos + rr);
+      e.kind = broot ? WG_ROOT : WG_SLOT;
+      DG[di++] = e;
+    }
+  }
+}
+
+}  // namespace
+
+// ---- builder driver ----------------------------------------------------------------
+
+void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
+  p.wave_streams = 0;
+  p.wave_steps = 0;
+  const int64_t nt = in.n_tiles;
+  if (nt == 0) return;
+  WaveCaps caps;
+  if (const char *e = getenv("RQ_WAVE_CAPS")) {  // g,r,b,rm
+    int g = 0, r = 0, b = 0, rm = 0;
+    if (sscanf(e, "%d,%d,%d,%d", &g, &r, &b, &rm) == 4) { caps.g = g; caps.r = r; caps.b = b; caps.rm = rm; }
+  }
+  p.wave_caps = caps;
+  if (const char *e = getenv("RQ_WAVE_PF")) p.wave_pf = std::max(0, std::min(32, atoi(e)));
+  if (const char *e = getenv("RQ_WAVE_STAGES")) p.wave_nst = std::max(2, std::min(4, atoi(e)));
+  NodeArrays A{in.node_off, in.bead_off, in.rec_off, in.res_base, in.node_body, in.start, in.stop, in.left,
+               in.right,    in.parent,   in.height,  in.res_off,  in.perm,      in.slot_scan, in.flags};
+  const int64_t NN = p.NN;
+  DBuf tnodes, theight, node_scan, tl_base;
+  tnodes.alloc(nt * 8);
+  theight.alloc(nt * 8);
+  node_scan.alloc((nt + 1) * 8);
+  tl_base.alloc((nt + 1) * 8);
+  k_wv_tiles<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tnodes.as<int64_t>(), theight.as<int64_t>());
+  ex_scan(tnodes.as<int64_t>(), node_scan.as<int64_t>(), nt + 0, s);
+  ex_scan(theight.as<int64_t>(), tl_base.as<int64_t>(), nt + 0, s);
+  const int64_t total_nodes = d2h1<int64_t>(node_scan.as<int64_t>() + nt - 1, s) + d2h1<int64_t>(tnodes.as<int64_t>() + nt - 1, s);
+  const int64_t total_lv = d2h1<int64_t>(tl_base.as<int64_t>() + nt - 1, s) + d2h1<int64_t>(theight.as<int64_t>() + nt - 1, s);
+  RQ_CUDA(cudaMemcpyAsync(node_scan.as<int64_t>() + nt, &total_nodes, 8, cudaMemcpyHostToDevice, s));
+  RQ_CUDA(cudaMemcpyAsync(tl_base.as<int64_t>() + nt, &total_lv, 8, cudaMemcpyHostToDevice, s));
+  if (total_nodes == 0) return;
+  // streams: one per resident CTA
+  int sms = 0;
+  RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+  int per_sm = 4;
+  if (const char *e = getenv("RQ_WAVE_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, atoi(e)));
+  int64_t G = (int64_t)sms * per_sm;
+  G = std::max<int64_t>(1, std::min<int64_t>(G, (total_nodes + 15) / 16));
+  // level profiles
+  DBuf tl, node_tile, bad;
+  tl.alloc(std::max<int64_t>(total_lv, 1) * sizeof(TLev));
+  RQ_CUDA(cudaMemsetAsync(tl.p, 0, std::max<int64_t>(total_lv, 1) * sizeof(TLev), s));
+  node_tile.alloc(NN * 4);
+  RQ_CUDA(cudaMemsetAsync(node_tile.p, 0xff, NN * 4, s));
+  bad.alloc(4);
+  RQ_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
+  k_wv_profile<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), tl.as<TLev>(),
+                                        node_tile.as<int32_t>(), caps, bad.as<int>());
+  if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a tile level exceeds the per-step capacities");
+  // streams: range c of every round
+  int64_t R = std::max<int64_t>(1, p.N / 170000);
+  R = std::min<int64_t>(R, std::max<int64_t>(1, nt / (4 * G)));
+  if (const char *e = getenv("RQ_WAVE_ROUNDS")) R = std::max(1, atoi(e));
+  p.wave_rounds = R;
+  DBuf tkey, tval, tkey2, order, sfirst, tile_stream, th_sorted, tn_sorted, lv_scan, n_scan_s;
+  tkey.alloc(nt * 8);
+  tval.alloc(nt * 4);
+  tkey2.alloc(nt * 8);
+  order.alloc(nt * 4);
+  sfirst.alloc((G + 1) * 8);
+  tile_stream.alloc(nt * 4);
+  th_sorted.alloc(nt * 8);
+  tn_sorted.alloc(nt * 8);
+  lv_scan.alloc((nt + 1) * 8);
+  n_scan_s.alloc((nt + 1) * 8);
+  k_wv_tile_key<<<nblk(nt), NT, 0, s>>>(node_scan.as<int64_t>(), nt, total_nodes, G, R, tkey.as<uint64_t>(),
+                                         tval.as<int32_t>());
+  {
+    size_t tb = 0;
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(), tval.as<int32_t>(),
+                                            order.as<int32_t>(), (int)nt, 0, 64, s));
+    DBuf tmp;
+    tmp.alloc(tb);
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(), tval.as<int32_t>(),
+                                            order.as<int32_t>(), (int)nt, 0, 64, s));
+  }
+  {
+    std::vector<int64_t> h(G + 1, -1);
+    RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+    k_wv_stream_first<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), nt, R, sfirst.as<int64_t>());
+    d2h(h.data(), sfirst.p, G + 1, s);
+    h[G] = nt;
+    for (int64_t c = G - 1; c >= 0; c--)
+      if (h[c] < 0) h[c] = h[c + 1];
+    RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+  }
+  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, tile_stream.as<int32_t>());
+  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(theight.as<int64_t>(), order.as<int32_t>(), nt, th_sorted.as<int64_t>());
+  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
+  ex_scan(th_sorted.as<int64_t>(), lv_scan.as<int64_t>(), nt, s);
+  ex_scan(tn_sorted.as<int64_t>(), n_scan_s.as<int64_t>(), nt, s);
+  RQ_CUDA(cudaMemcpyAsync(lv_scan.as<int64_t>() + nt, &total_lv, 8, cudaMemcpyHostToDevice, s));
+  RQ_CUDA(cudaMemcpyAsync(n_scan_s.as<int64_t>() + nt, &total_nodes, 8, cudaMemcpyHostToDevice, s));
+  // placement
+  DBuf load, e_tile, n_steps, step_first;
+  load.alloc(std::max<int64_t>(total_lv, 1) * sizeof(TLev));
+  RQ_CUDA(cudaMemsetAsync(load.p, 0, std::max<int64_t>(total_lv, 1) * sizeof(TLev), s));
+  e_tile.alloc(nt * 4);
+  n_steps.alloc(G * 8);
+  step_first.alloc((G + 1) * 8);
+  k_wv_place<<<nblk(G, 64), 64, 0, s>>>(sfirst.as<int64_t>(), G, order.as<int32_t>(), lv_scan.as<int64_t>(),
+                                         tl_base.as<int64_t>(), tl.as<TLev>(), load.as<TLev>(), theight.as<int64_t>(),
+                                         e_tile.as<int32_t>(), n_steps.as<int64_t>(), caps);
+  ex_scan(n_steps.as<int64_t>(), step_first.as<int64_t>(), G, s);
+  const int64_t NS = d2h1<int64_t>(step_first.as<int64_t>() + G - 1, s) + d2h1<int64_t>(n_steps.as<int64_t>() + G - 1, s);
+  RQ_CUDA(cudaMemcpyAsync(step_first.as<int64_t>() + G, &NS, 8, cudaMemcpyHostToDevice, s));
+  load.reset();
+  // node order: (global step, case)
+  DBuf keys, vals, keys2, vals2;
+  keys.alloc(NN * 8);
+  vals.alloc(NN * 4);
+  keys2.alloc(NN * 8);
+  vals2.alloc(NN * 4);
+  k_wv_keys<<<nblk(NN), NT, 0, s>>>(NN, A, node_tile.as<int32_t>(), nullptr, step_first.as<int64_t>(),
+                                     e_tile.as<int32_t>(), keys.as<uint64_t>(), vals.as<int32_t>(),
+                                     tile_stream.as<int32_t>());
+  {
+    int bits = 2;
+    while ((int64_t(1) << (bits - 2)) <= NS) bits++;
+    size_t tb = 0;
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                            vals.as<int32_t>(), vals2.as<int32_t>(), (int)NN, 0, 64, s));
+    DBuf tmp;
+    tmp.alloc(tb);
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.as<uint64_t>(), keys2.as<uint64_t>(),
+                                            vals.as<int32_t>(), vals2.as<int32_t>(), (int)NN, 0, 64, s));
+    (void)bits;
+  }
+  keys.reset();
+  vals.reset();
+  // counts
+  const int64_t n = total_nodes;
+  DBuf sc, step_of, sfs, nb, vd, nd, bscan, vscan, dscan;
+  sc.alloc(NS * sizeof(StepCnt));
+  RQ_CUDA(cudaMemsetAsync(sc.p, 0, NS * sizeof(StepCnt), s));
+  step_of.alloc(NN * 8);
+  sfs.alloc(NS * 8);
+  RQ_CUDA(cudaMemsetAsync(sfs.p, 0, NS * 8, s));
+  nb.alloc(n * 4);
+  vd.alloc(n * 4);
+  nd.alloc(n * 4);
+  bscan.alloc(n * 8);
+  vscan.alloc(n * 8);
+  dscan.alloc(n * 8);
+  k_wv_count<<<nblk(n), NT, 0, s>>>(keys2.as<uint64_t>(), vals2.as<int32_t>(), n, A, sc.as<StepCnt>(),
+                                     step_of.as<int64_t>(), sfs.as<int64_t>(), nb.as<int32_t>(), vd.as<int32_t>(),
+                                     nd.as<int32_t>(), node_tile.as<int32_t>(), in.tile_root);
+  ex_scan(nb.as<int32_t>(), bscan.as<int64_t>(), n, s);
+  ex_scan(vd.as<int32_t>(), vscan.as<int64_t>(), n, s);
+  ex_scan(nd.as<int32_t>(), dscan.as<int64_t>(), n, s);
+  // block offsets
+  DBuf bytes, off, mx;
+  bytes.alloc(NS * 8);
+  off.alloc((NS + 1) * 8);
+  mx.alloc(16);
+  RQ_CUDA(cudaMemsetAsync(mx.p, 0, 16, s));
+  k_wv_step_bytes<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), NS, bytes.as<int64_t>(), mx.as<unsigned long long>());
+  ex_scan(bytes.as<int64_t>(), off.as<int64_t>(), NS, s);
+  const int64_t blob_bytes = d2h1<int64_t>(off.as<int64_t>() + NS - 1, s) + d2h1<int64_t>(bytes.as<int64_t>() + NS - 1, s);
+  if (blob_bytes >= (int64_t(1) << 36)) throw Error(RQ_ERR_VALUE, "wave layout exceeds 64 GB");
+  {
+    unsigned long long h[2];
+    d2h(h, mx.p, 2, s);
+    p.wave_stage_bytes = (int64_t)al128((size_t)std::max(h[0], h[1]));
+  }
+  p.wave_blob.alloc(blob_bytes);
+  RQ_CUDA(cudaMemsetAsync(p.wave_blob.p, 0, blob_bytes, s));
+  p.wave_desc.alloc(NS * sizeof(StepDesc));
+  k_wv_descs<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), off.as<int64_t>(), NS, p.wave_desc.as<StepDesc>(),
+                                      p.wave_blob.as<uint8_t>());
+  // slots
+  DBuf slot_of, node_first, msl;
+  slot_of.alloc(NN * 4);
+  RQ_CUDA(cudaMemsetAsync(slot_of.p, 0, NN * 4, s));
+  node_first.alloc((G + 1) * 8);
+  {
+    // a stream's nodes are contiguous in the sorted order: node_first[c] = nodes of earlier streams
+    std::vector<int64_t> hs(G + 1), hn(nt + 1);
+    d2h(hs.data(), sfirst.p, G + 1, s);
+    d2h(hn.data(), n_scan_s.p, nt + 1, s);
+    std::vector<int64_t> nf(G + 1);
+    for (int64_t c = 0; c <= G; c++) nf[c] = hn[hs[c]];
+    RQ_CUDA(cudaMemcpyAsync(node_first.p, nf.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+  }
+  msl.alloc(8);
+  RQ_CUDA(cudaMemsetAsync(msl.p, 0, 8, s));
+  {
+    DBuf fh, bh;
+    fh.alloc(G * WV_MAX_SLOTS * 4);
+    bh.alloc(G * WV_MAX_SLOTS * 8);
+    k_wv_slots<<<nblk(G, 32), 32, 0, s>>>(node_first.as<int64_t>(), G, vals2.as<int32_t>(), A, step_of.as<int64_t>(),
+                                           node_tile.as<int32_t>(), in.tile_root, slot_of.as<int32_t>(),
+                                           msl.as<int>(), msl.as<int>() + 1, fh.as<int32_t>(), bh.as<long long>());
+    RQ_CUDA(cudaStreamSynchronize(s));
+  }
+  {
+    int h[2];
+    d2h(h, msl.p, 2, s);
+    if (h[1]) throw Error(RQ_ERR_VALUE, "wave layout: more than 4096 live node vectors in a stream");
+    p.wave_mslots = std::max(1, h[0]);
+  }
+  WriteIn w{A,
+            keys2.as<uint64_t>(),
+            vals2.as<int32_t>(),
+            p.wave_desc.as<StepDesc>(),
+            sfs.as<int64_t>(),
+            bscan.as<int64_t>(),
+            vscan.as<int64_t>(),
+            dscan.as<int64_t>(),
+            slot_of.as<int32_t>(),
+            node_tile.as<int32_t>(),
+            in.tile_root,
+            in.rec,
+            p.wave_blob.as<uint8_t>()};
+  k_wv_write<<<nblk(n), NT, 0, s>>>(w, n);
+  RQ_CUDA(cudaGetLastError());
+  p.wave_stream_first.alloc((G + 1) * 8);
+  RQ_CUDA(cudaMemcpyAsync(p.wave_stream_first.p, step_first.p, (G + 1) * 8, cudaMemcpyDeviceToDevice, s));
+  // per-direction bytes streamed per application (algorithmic bytes of the sweep)
+  {
+    std::vector<StepDesc> hd(NS);
+    d2h(hd.data(), p.wave_desc.p, NS, s);
+    int64_t up = 0, dn = 0;
+    for (const auto &d : hd) {
+      const WaveSec S = wave_sections(d);
+      up += S.end - S.uhdr;
+      dn += S.um;
+    }
+    p.wave_up_bytes = up;
+    p.wave_down_bytes = dn;
+  }
+  RQ_CUDA(cudaStreamSynchronize(s));
+  p.wave_streams = G;
+  p.wave_steps = NS;
+  p.wave_blob_bytes = blob_bytes;
+  p.wave_nodes = n;
+  if (getenv("RQ_VERBOSE"))
+    fprintf(stderr, "[rq] wave: %lld streams x %lld rounds, %lld steps (%.1f per stream, %.1f nodes per step), blob %.1f MB "
+                    "(up %.1f, down %.1f), M slots %d, stage %lld B\n",
+            (long long)G, (long long)R, (long long)NS, (double)NS / G, (double)n / std::max<int64_t>(1, NS - 4 * G),
+            blob_bytes / 1e6, p.wave_up_bytes / 1e6, p.wave_down_bytes / 1e6, p.wave_mslots, (long long)p.wave_stage_bytes);
+}
+
+// ---- sweep kernel ------------------------------------------------------------------
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, unsigned bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, unsigned parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void prefetch_l2(const void *ptr, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int CS>
+__device__ __forceinline__ void ld_rec(const double *rec, double (&R)[rec_size(CS)]) {
+  const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+#pragma unroll
+  for (int i = 0; i < rec_size(CS) / 2; i++) {
+    const double2 v = r2[i];
+    R[2 * i] = v.x;
+    R[2 * i + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void ld6(const double *q, double (&v)[6]) {
+  const double2 *q2 = reinterpret_cast<const double2 *>(q);
+#pragma unroll
+  for (int i = 0; i < 3; i++) {
+    const double2 w = q2[i];
+    v[2 * i] = w.x;
+    v[2 * i + 1] = w.y;
+  }
+}
+__device__ __forceinline__ void st6(double *q, const double (&v)[6]) {
+  double2 *q2 = reinterpret_cast<double2 *>(q);
+#pragma unroll
+  for (int i = 0; i < 3; i++) q2[i] = make_double2(v[2 * i], v[2 * i + 1]);
+}
+
+// one node of the upward sweep (merge_infosets, matfree.py:41-62)
+template <int CS>
+__device__ __forceinline__ void wv_up(const double *rec, const WaveUpMeta *UMp, double *M, const double *V,
+                                      double *out, double *scratch, double *roots) {
+  double R[rec_size(CS)];
+  ld_rec<CS>(rec, R);
+  const WaveUpMeta md = *UMp;
+  double mx[6], my[6];
+  if (CS == BEAD_BEAD) {
+    const double *f = V + 3 * md.x;
+    mx[0] = f[0]; mx[1] = f[1]; mx[2] = f[2]; mx[3] = 0.0; mx[4] = 0.0; mx[5] = 0.0;
+  } else {
+    ld6(M + 6 * md.x, mx);
+  }
+  if (CS != GENERAL) {
+    const double *f = V + 3 * md.y;
+    my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
+  } else {
+    ld6(M + 6 * md.y, my);
+  }
+  double aa, bb, mp[6], res[6];
+  rec_ratios(CS, R, 1, aa, bb);
+  merge(CS, R, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
+  if (CS != BEAD_BEAD) {
+    double *o = out + md.row;
+#pragma unroll
+    for (int r = 0; r < res_rows(CS); r++) o[r] = res[r];
+  }
+  if (md.flags & (WF_TILE_ROOT | WF_BODY_ROOT)) {
+    double *dst = (md.flags & WF_TILE_ROOT) ? scratch + 6 * (int64_t)md.aux : (roots ? roots + 6 * (int64_t)md.aux : nullptr);
+    if (dst) {
+#pragma unroll
+      for (int r = 0; r < 6; r++) dst[r] = mp[r];
+    }
+  } else {
+    st6(M + 6 * md.self, mp);
+  }
+}
+
+// one node of the downward sweep (split_rvset, matfree.py:65-83)
+template <int CS>
+__device__ __forceinline__ void wv_down(const double *rec, const WaveDnMeta *DMp, double *M, const double *V,
+                                        double *out) {
+  double R[rec_size(CS)];
+  ld_rec<CS>(rec, R);
+  const WaveDnMeta md = *DMp;
+  double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
+  if (md.flags & (WF_TILE_ROOT | WF_BODY_ROOT)) {
+    const double *q = V + md.self;
+#pragma unroll
+    for (int r = 0; r < 6; r++) lp[r] = q[r];
+  } else {
+    ld6(M + 6 * md.self, lp);
+  }
+#pragma unroll
+  for (int r = 0; r < res_rows(CS); r++) res[r] = V[md.vres + r];
+  double aa, bb;
+  rec_ratios(CS, R, 1, aa, bb);
+  split(CS, R, 1, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
+  if (CS == BEAD_BEAD) {
+    double *o = out + 3 * (int64_t)md.x;
+    o[0] = lx[0]; o[1] = lx[1]; o[2] = lx[2];
+  } else {
+    st6(M + 6 * md.x, lx);
+  }
+  if (CS != GENERAL) {
+    double *o = out + 3 * (int64_t)md.y;
+    o[0] = ly[0]; o[1] = ly[1]; o[2] = ly[2];
+  } else {
+    st6(M + 6 * md.y, ly);
+  }
+}
+
+struct WaveCtx {
+  const StepDesc *steps;
+  const int64_t *stream_first;
+  const uint8_t *blob;
+  const double *in;
+  double *out;
+  double *scratch;
+  double *roots;
+  uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: 2 stages | M | 3 gather regions (vreg doubles each)
+  int pf;                                // L2 prefetch distance (steps)
+};
+
+#ifndef RQ_WAVE_MIN_BLOCKS
+#define RQ_WAVE_MIN_BLOCKS 4
+#endif
+
+template <bool UP, int NST>
+__global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[NST];
+  const int tid = threadIdx.x;
+  constexpr int PROD = 96;  // lane 0 of warp 3 (a BEAD_BEAD warp: the cheapest node path)
+  const int64_t s0 = a.stream_first[blockIdx.x], s1 = a.stream_first[blockIdx.x + 1];
+  const int n = (int)(s1 - s0);
+  const uint32_t sm_u = smem_u32(smem), bar_u = smem_u32(bar);
+  double *M = reinterpret_cast<double *>(smem + a.o_m);
+  double *Vb = reinterpret_cast<double *>(smem + a.o_v);
+  const uint32_t vb_u = sm_u + a.o_v;
+  auto blk = [&](int t) -> int64_t { return UP ? s0 + t : s1 - 1 - t; };
+  auto span = [&](const StepDesc &d, uint32_t &off, uint32_t &bytes) {
+    const WaveSec S = wave_sections(d);
+    if (UP) { off = S.uhdr; bytes = S.end - S.uhdr; }
+    else { off = 0; bytes = S.um; }
+  };
+  StepDesc dn{};
+  if (tid == PROD) {
+    for (int i = 0; i < NST; i++) mbar_init(bar_u + 8 * i, 1);
+    fence_mbar_init();
+    for (int t = 0; t < NST && t < n; t++) {
+      const StepDesc d = a.steps[blk(t)];
+      uint32_t off, bytes;
+      span(d, off, bytes);
+      mbar_expect_tx(bar_u + 8 * t, bytes);
+      bulk_g2s(sm_u + t * a.stage_bytes, a.blob + ((int64_t)d.off16 << 4) + off, bytes, bar_u + 8 * t);
+    }
+    for (int t = NST; t < n && t < NST + a.pf; t++) {
+      const StepDesc d = a.steps[blk(t)];
+      uint32_t off, bytes;
+      span(d, off, bytes);
+      prefetch_l2(a.blob + ((int64_t)d.off16 << 4) + off, bytes);
+    }
+    if (n > NST) dn = a.steps[blk(NST)];
+  }
+  __syncthreads();
+  pdl_wait();  // vectors and exchange slots may come from the previous kernel
+  unsigned phase = 0;
+  int st = 0;
+  for (int t = 0; t < n; t++, st = (st == NST - 1) ? 0 : st + 1) {
+    mbar_wait(bar_u + 8 * st, (phase >> st) & 1u);
+    phase ^= 1u << st;
+    const unsigned char *B = smem + st * a.stage_bytes;
+    const StepDesc d = *reinterpret_cast<const StepDesc *>(B);
+    const WaveSec S = wave_sections(d);
+    // gathers for step t + 2 (into region (t + 2) % 3)
+    {
+      const int rg = (t + 2) % 3;
+      const uint32_t vg = vb_u + 8u * (uint32_t)(rg * a.vreg);
+      if (UP) {
+        const uint32_t *ug = reinterpret_cast<const uint32_t *>(B + (S.ug - S.uhdr));
+        for (int i = tid; i < d.n_ug; i += 128) {
+          const double *src = a.in + 3 * (int64_t)ug[i];
+          const uint32_t dst = vg + 24u * (uint32_t)i;
+          cp8(dst, src);
+          cp8(dst + 8, src + 1);
+          cp8(dst + 16, src + 2);
+        }
+      } else {
+        const WaveGather *dg = reinterpret_cast<const WaveGather *>(B + S.dg);
+        for (int i = tid; i < d.n_dg; i += 128) {
+          const WaveGather e = dg[i];
+          const uint32_t dst = vg + 8u * e.dst;
+          if (e.kind == WG_RES3 || e.kind == WG_RES6) {
+            const double *src = a.in + e.src;
+            const int c = e.kind == WG_RES3 ? 3 : 6;
+            for (int r = 0; r < c; r++) cp8(dst + 8 * r, src + r);
+          } else if (e.kind == WG_SLOT) {
+            const double *src = a.scratch + 6 * (int64_t)e.src;
+            for (int r = 0; r < 6; r++) cp8(dst + 8 * r, src + r);
+          } else if (a.roots) {
+            const double *src = a.roots + 6 * (int64_t)e.src;
+            for (int r = 0; r < 6; r++) cp8(dst + 8 * r, src + r);
+          } else {
+            double *z = Vb + rg * a.vreg + e.dst;
+            for (int r = 0; r < 6; r++) z[r] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
+          }
+        }
+      }
+      cp_commit();
+    }
+    // nodes of step t (gather region t % 3)
+    {
+      const double *V = Vb + (t % 3) * a.vreg;
+      const int nG = d.nG, nR = d.nR, nB = d.nB;
+      const int gG = (nG + 31) & ~31, gR = (nR + 31) & ~31;
+      const int tot = gG + gR + nB;
+      const double *R = reinterpret_cast<const double *>(B + (UP ? 16 : S.rec));
+      const int oR = rec_size(GENERAL) * nG, oB = oR + rec_size(RIGID_BEAD) * nR;
+      if (UP) {
+        const WaveUpMeta *UM = reinterpret_cast<const WaveUpMeta *>(B + (S.um - S.uhdr));
+        for (int q = tid; q < tot; q += 128) {
+          if (q < gG) {
+            if (q < nG) wv_up<GENERAL>(R + q * rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < nR)
+              wv_up<RIGID_BEAD>(R + oR + qq * rec_size(RIGID_BEAD), UM + nG + qq, M, V, a.out, a.scratch, a.roots);
+          } else {
+            const int qq = q - gG - gR;
+            wv_up<BEAD_BEAD>(R + oB + qq * rec_size(BEAD_BEAD), UM + nG + nR + qq, M, V, a.out, a.scratch, a.roots);
+          }
+        }
+      } else {
+        const WaveDnMeta *DM = reinterpret_cast<const WaveDnMeta *>(B + S.dm);
+        for (int q = tid; q < tot; q += 128) {
+          if (q < gG) {
+            if (q < nG) wv_down<GENERAL>(R + q * rec_size(GENERAL), DM + q, M, V, a.out);
+          } else if (q < gG + gR) {
+            const int qq = q - gG;
+            if (qq < nR) wv_down<RIGID_BEAD>(R + oR + qq * rec_size(RIGID_BEAD), DM + nG + qq, M, V, a.out);
+          } else {
+            const int qq = q - gG - gR;
+            wv_down<BEAD_BEAD>(R + oB + qq * rec_size(BEAD_BEAD), DM + nG + nR + qq, M, V, a.out);
+          }
+        }
+      }
+    }
+    cp_wait<1>();  // this thread's gathers for step t + 1
+    __syncthreads();
+    if (tid == PROD && t + NST < n) {  // stage st is free: block t + NST
+      uint32_t off, bytes;
+      span(dn, off, bytes);
+      mbar_expect_tx(bar_u + 8 * st, bytes);
+      bulk_g2s(sm_u + st * a.stage_bytes, a.blob + ((int64_t)dn.off16 << 4) + off, bytes, bar_u + 8 * st);
+      if (a.pf && t + NST + a.pf < n) {
+        const StepDesc d2 = a.steps[blk(t + NST + a.pf)];
+        uint32_t o2, b2;
+        span(d2, o2, b2);
+        prefetch_l2(a.blob + ((int64_t)d2.off16 << 4) + o2, b2);
+      }
+      if (t + NST + 1 < n) dn = a.steps[blk(t + NST + 1)];
+    }
+  }
+}
+
+}  // namespace
+
+size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg) {
+  const uint32_t st = (uint32_t)p.wave_stage_bytes;
+  const uint32_t vr = (uint32_t)std::max(3 * p.wave_caps.beads, p.wave_caps.vd);
+  const uint32_t om = (uint32_t)p.wave_nst * st;
+  const uint32_t ov = om + (uint32_t)al128(48 * (size_t)p.wave_mslots);
+  if (o_m) *o_m = om;
+  if (o_v) *o_v = ov;
+  if (vreg) *vreg = vr;
+  return ov + 3 * 8 * (size_t)vr;
+}
+
+void wave_prepare(const Plan &p) {
+  if (p.wave_ready || !p.wave_streams) return;
+  const size_t sm = wave_smem(p, nullptr, nullptr, nullptr);
+  for (const void *f : {(const void *)k_wave<true, 2>, (const void *)k_wave<false, 2>, (const void *)k_wave<true, 3>,
+                        (const void *)k_wave<false, 3>, (const void *)k_wave<true, 4>, (const void *)k_wave<false, 4>})
+    RQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  int occ = 0;
+  RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_wave<true, 3>, 128, sm));
+  p.wave_ctas_per_sm = occ;
+  if (occ < 1) throw Error(RQ_ERR_CUDA, "wave kernel does not fit on an SM (smem " + std::to_string(sm) + ")");
+  p.wave_ready = true;
+}
+
+void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s) {
+  if (!p.wave_streams) return;
+  wave_prepare(p);
+  WaveCtx a{};
+  a.steps = p.wave_desc.as<StepDesc>();
+  a.stream_first = p.wave_stream_first.as<int64_t>();
+  a.blob = p.wave_blob.as<uint8_t>();
+  a.in = in;
+  a.out = out;
+  a.scratch = scratch;
+  a.roots = roots;
+  a.stage_bytes = (uint32_t)p.wave_stage_bytes;
+  const size_t sm = wave_smem(p, &a.o_m, &a.o_v, &a.vreg);
+  a.pf = p.wave_pf;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.wave_streams);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (p.wave_nst * 2 + (up ? 1 : 0)) {
+    case 4: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 2>, a)); break;
+    case 5: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 2>, a)); break;
+    case 8: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 4>, a)); break;
+    case 9: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 4>, a)); break;
+    case 6: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 3>, a)); break;
+    default: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 3>, a)); break;
+  }
+}
+
+}  // namespace rq

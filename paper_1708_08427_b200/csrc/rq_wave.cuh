@@ -1,0 +1,105 @@
+// rq_wave.cuh -- layout of the wavefront apply streams (rq_wave.cu).
+//
+// The tile nodes of a plan (all internal nodes below the top trees) are split
+// into G streams, one per persistent CTA.  Each stream is a sequence of STEPS:
+// a step holds up to (CAP_G GENERAL, CAP_R RIGID_BEAD, CAP_B BEAD_BEAD) nodes
+// whose children were all produced by earlier steps of the same stream (or are
+// beads), so the CTA sweeps a stream with one barrier per step.  Tiles enter a
+// stream staggered (a tile's height-h nodes go to step e_tile + h - 1, e_tile
+// the earliest step at which all its levels fit), so the upper, sparse levels
+// of one tile share steps with the dense lower levels of the next ones -- the
+// steps are ~2.5x fuller than level-synchronous chunks.
+//
+// The upward sweep (upward_apply, matfree.py:95-121) runs the steps forward,
+// the downward sweep (downward_apply, matfree.py:124-151) backward.  Every step
+// is one contiguous block; each direction TMA-copies its own contiguous part:
+//
+//   HDR_D | DG[n_dg] | DM[n] | HDR_U | REC | UM[n] | UG[n_ug]
+//   \______________ DOWN copy ______________/
+//                           \_____________ UP copy ______________/
+//
+//   HDR    : the StepDesc (16 B, twice so each copy starts with it)
+//   REC    : compact records, GEN | RB | BB groups (AoS, rec_size doubles)
+//   UM / DM: per-node metadata of the upward / downward sweep (16 B each)
+//   UG     : upward gather list of step s+2: global bead index per bead (4 B)
+//   DG     : downward gather list of step s-2: residue rows / tile-root
+//            RV-sets (8 B entries)
+// Each stream starts and ends with two node-free steps that only carry gather
+// lists, so gathers always run two steps ahead of their use.
+#pragma once
+
+#include <cstdint>
+
+#include "rq_internal.cuh"
+
+namespace rq {
+
+struct StepDesc {     // 16 bytes (also the block header)
+  uint32_t off16;     // block byte offset / 16 in the wave blob
+  uint16_t nG, nR, nB;
+  uint16_t n_ug;      // upward gathers held by this block (beads of step s+2)
+  uint16_t n_dg;      // downward gathers held by this block (nodes of step s-2)
+  uint16_t pad;
+};
+
+// upward metadata: x, y = M slots (internal children) or bead positions in the
+// step's gather region (BEAD_BEAD: both, RIGID_BEAD: y); self = M slot of the
+// output; row = first residue row (private residue layout, see Plan::res_base);
+// aux = exchange slot (tile root) or body (body root)
+struct WaveUpMeta {
+  uint16_t x, y, self, flags;
+  uint32_t row, aux;
+};
+// downward metadata: x, y = M slots (internal) or global original bead indices
+// (BEAD_BEAD: both, RIGID_BEAD: y); self = M slot of the node's RV-set, or its
+// offset in the gather region for tile roots; vres = offset of its residues
+struct WaveDnMeta {
+  uint32_t x, y;
+  uint16_t self, flags, vres, pad;
+};
+// downward gather entry
+struct WaveGather {
+  uint32_t src;   // residue row / exchange slot / body
+  uint16_t dst;   // double offset in the gather region
+  uint16_t kind;  // WG_*
+};
+enum : uint16_t { WG_RES3 = 0, WG_RES6 = 1, WG_SLOT = 2, WG_ROOT = 3 };
+// meta flag bits above the node flags (bits 0-5: case | swapped | signs)
+constexpr uint16_t WF_TILE_ROOT = 1u << 6;  // output to / input from an exchange slot
+constexpr uint16_t WF_BODY_ROOT = 1u << 7;  // the body root (output to / input from `roots`)
+
+__host__ __device__ inline uint32_t al16u(uint32_t x) { return (x + 15u) & ~15u; }
+
+struct WaveSec {  // byte offsets inside a block
+  uint32_t dg, dm, uhdr, rec, um, ug, end;
+};
+__host__ __device__ inline uint32_t wave_rec_bytes(uint32_t nG, uint32_t nR, uint32_t nB) {
+  return 8u * (rec_size(GENERAL) * nG + rec_size(RIGID_BEAD) * nR + rec_size(BEAD_BEAD) * nB);
+}
+__host__ __device__ inline WaveSec wave_sections(uint32_t nG, uint32_t nR, uint32_t nB, uint32_t n_ug,
+                                                 uint32_t n_dg) {
+  const uint32_t n = nG + nR + nB;
+  WaveSec s;
+  s.dg = 16u;
+  s.dm = s.dg + al16u(8u * n_dg);
+  s.uhdr = s.dm + 16u * n;
+  s.rec = s.uhdr + 16u;
+  s.um = s.rec + wave_rec_bytes(nG, nR, nB);
+  s.ug = s.um + 16u * n;
+  s.end = s.ug + al16u(4u * n_ug);
+  return s;
+}
+__host__ __device__ inline WaveSec wave_sections(const StepDesc &d) {
+  return wave_sections(d.nG, d.nR, d.nB, d.n_ug, d.n_dg);
+}
+
+// per-step capacities (the scheduler never exceeds them; they size shared memory)
+struct WaveCaps {
+  int g = 32, r = 32, b = 64;   // nodes per case
+  int rm = 10240;               // record + one-direction metadata bytes
+  int beads = 128;              // upward gathers (beads) per step
+  int vd = 384;                 // downward gathered doubles per step
+  int dg = 96;                  // downward gather entries per step
+};
+
+}  // namespace rq
