@@ -4,16 +4,19 @@
 One step = one Q~v over every bead of the batch plus one Q~^T g over every
 complement coordinate (BASELINE.json metric), on BASELINE config 2 by default
 (1000 triaxial-ellipsoid-shell bodies x 4096 beads, fp64, synthetic seeded
-input).  Operator (~0.6 GB of chunk blobs) and vectors (~0.2 GB) are far
+input).  Operator (~0.8 GB of step blocks) and vectors (~0.2 GB) are far
 larger than the 126 MB L2, so no L2 flush is needed between steps.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 runs under torchrun, one rank per GPU; bodies are independent so every
-rank owns its own 1000-body shard (weak scaling, no data-path collective);
-times are device-measured (CUDA events) and max-reduced over ranks.
---sharding strong instead splits ONE config-sized model across the ranks by
-cumulative bead count (e.g. config 4's 20000 bodies over 8 GPUs).
+N > 1 runs under torchrun, one rank per GPU.  Bodies are independent, so the
+config's model is split across the ranks by cumulative bead count
+(parallel.shard_bounds; strong scaling, the default) and every rank applies
+its shard with no data-path collective; times are device-measured (CUDA
+events) and max-reduced over ranks; the one-time NCCL gather of the shard
+outputs is timed separately (gather_ms).  --sharding weak instead gives every
+rank its own full config-sized model.  --emulate-shard R/N times shard R of N
+alone on one GPU (per-shard device time for a strong-scaling estimate).
 
 --impl reference times the reference algorithm on the host CPU: the C oracle
 (oracle/, a restatement of the pure-Python reference package that is 30-100x
@@ -50,9 +53,11 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--sharding", default="weak", choices=["weak", "strong"],
-                    help="weak: every rank owns a full config-sized shard; strong: one config-sized "
-                         "model split across the ranks by cumulative bead count (parallel.shard_bounds)")
+    ap.add_argument("--sharding", default=None, choices=["weak", "strong"],
+                    help="strong (default for --gpus > 1): one config-sized model split across the ranks "
+                         "by cumulative bead count (parallel.shard_bounds); weak: every rank owns a full "
+                         "config-sized shard")
+    ap.add_argument("--emulate-shard", default=None, help="R/N: time shard R of an N-way strong split alone")
     return ap.parse_args()
 
 
@@ -60,7 +65,7 @@ def workload(cfg: int, rank: int, scale: float, world: int = 1, strong: bool = F
     from paper_1708_08427_b200.parallel import shard_of
     from paper_1708_08427_b200.workloads import CONFIGS, make_config
 
-    if strong:  # one model for the whole job, this rank's contiguous shard of its bodies
+    if strong and world > 1:  # one model for the whole job, this rank's contiguous shard of its bodies
         pos, off = make_config(cfg, seed=1000, scale=scale)
         pos, off, _ = shard_of(pos, off, rank, world)
     else:
@@ -203,8 +208,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    strong = args.sharding == "strong"
-    pos, off, name, k = workload(args.config, rank, args.scale, world, strong)
+    sharding = args.sharding or ("strong" if world > 1 else "weak")
+    strong = sharding == "strong"
+    emu = None
+    if args.emulate_shard:  # one shard of an N-way strong split, alone on this GPU
+        er, en = (int(x) for x in args.emulate_shard.split("/"))
+        emu = (er, en)
+        pos, off, name, k = workload(args.config, er, args.scale, en, True)
+    else:
+        pos, off, name, k = workload(args.config, rank, args.scale, world, strong)
     N, m = int(off[-1]), len(off) - 1
     # beads processed per step by the whole job (strong: the sum of the shards)
     n_job = world * N
@@ -281,7 +293,7 @@ def main():
         reps.append(a0.elapsed_time(a1))
     step_stats = {"min_ms": float(np.min(reps)), "median_ms": float(np.median(reps)), "repeats": len(reps)}
 
-    # ---- kernel-level roofline: the chunk sweep (dominant kernel), timed alone
+    # ---- kernel-level roofline: the tile sweep (dominant kernel), timed alone
     lib = L.lib()
     h = op.plan.handle
     stream = C.c_void_p(s.cuda_stream)
@@ -292,46 +304,75 @@ def main():
     kern = {}
     mrhs = k >= info["mrhs_min_k"] and lib.rq_launches_per_apply(h, L.OP_QTILDE_V, k) < 2 * k
     for opn, code, x in (("qtilde_v", L.OP_QTILDE_V, v2), ("qtilde_tv", L.OP_QTILDE_TV, g2)):
-        for phase, label in ((1, "chunks"), (2, "top")):
-            reps = 50
+        for phase, label in ((1, "sweep"), (2, "top")):
+            nrep = 50
             for _ in range(3):
                 L.check(lib.rq_apply_ex(h, code, x.data_ptr(), outs[opn].data_ptr(), k, stream, phase))
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(s)
-            for _ in range(reps):
+            for _ in range(nrep):
                 L.check(lib.rq_apply_ex(h, code, x.data_ptr(), outs[opn].data_ptr(), k, stream, phase))
             b.record(s)
             torch.cuda.synchronize()
             # ms per launch (the single-RHS path launches once per column)
-            kern[(opn, label)] = a.elapsed_time(b) / reps / (1 if mrhs else k)
+            kern[(opn, label)] = a.elapsed_time(b) / nrep / (1 if mrhs else k)
     per_step = 1 if mrhs else k  # launches of each phase per application
-    chunk_ms = 0.5 * (kern[("qtilde_v", "chunks")] + kern[("qtilde_tv", "chunks")])
+    sweep_ms = 0.5 * (kern[("qtilde_v", "sweep")] + kern[("qtilde_tv", "sweep")])
     info = op.plan.info()  # multi-RHS programs are built by the first k >= mrhs_min_k apply
     if mrhs:
         # tile-unit launch: the unit programs (entry headers + records) once per group of
         # 32 columns, every bead row and residue row of the k columns once, and the
         # tile-root exchange rows (written upward / read downward)
         ncg = (k + 31) // 32
-        chunk_bytes = (info["mrhs_bytes"]["tiles"] * ncg + 8 * k * (3 * N + (3 * N - 6 * m))
+        sweep_bytes = (info["mrhs_bytes"]["tiles"] * ncg + 8 * k * (3 * N + (3 * N - 6 * m))
                        + 8 * 6 * k * info["mrhs_units"]["tiles"])
         kname = "k_mrhs (column-parallel stack machine over tile units, lane = RHS column)"
     else:
-        # algorithmic bytes per chunk launch: the chunk blobs (records + meta + perm)
-        # plus one read and one write of every bead's 3 fp64 and residue coordinates
-        chunk_bytes = info["blob_bytes"] + 8 * (3 * N + (3 * N - 6 * m))
-        kname = "k_chunk (level-synchronous chunk sweep, TMA bulk-copied blobs)"
-    achieved = chunk_bytes / (chunk_ms * 1e-3) / 1e9
+        # algorithmic bytes per sweep launch (mean of the two directions): the step blocks the
+        # direction streams (records + its metadata + gather lists), one read and one write of
+        # every bead's 3 fp64 and residue coordinates, the tile-root exchange 6-vectors
+        sweep_bytes = (0.5 * (info["sweep_bytes"]["up"] + info["sweep_bytes"]["down"])
+                       + 8 * (3 * N + (3 * N - 6 * m)) + 48 * info["n_tiles"])
+        kname = "k_wave (wavefront step sweep, TMA bulk-copied step blocks)"
+    achieved = sweep_bytes / (sweep_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     step_ms_kernels = sum(kern.values()) * per_step
-    share = (kern[("qtilde_v", "chunks")] + kern[("qtilde_tv", "chunks")]) * per_step / step_ms_kernels
+    share = (kern[("qtilde_v", "sweep")] + kern[("qtilde_tv", "sweep")]) * per_step / step_ms_kernels
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "chunk_traffic.json")
-    if os.path.exists(tpath):
+    tpath = os.path.join(ROOT, "profiles", "wave_traffic.json")
+    if os.path.exists(tpath) and not mrhs:
         with open(tpath) as f:
             tj = json.load(f)
-        # dram bytes per launch measured by ncu on the same config, scaled per bead
+        # dram bytes per sweep launch measured by ncu on the same config, scaled per bead
         if tj.get("config") == args.config and tj.get("beads"):
             traffic = tj["dram_bytes_per_launch"] * N / tj["beads"]
+
+    # ---- parity of this run's own outputs against the CPU oracle on a sample of bodies
+    parity = None
+    if rank == 0:
+        from oracle.oracle import OracleBatch
+
+        nb = min(m, 64 if args.config != 3 else 1)
+        if k == 1 and (args.config != 3 or N <= (1 << 20)):
+            ob = OracleBatch(pos[:off[nb]], off[:nb + 1], threads=len(os.sched_getaffinity(0)))
+            outv = op.apply("qtilde_v", v).cpu().numpy()
+            outg = op.apply("qtilde_tv", g).cpu().numpy()
+            vh, gh = v.cpu().numpy(), g.cpu().numpy()
+            worst = 0.0
+            for opn, x, y, li, lo in (("qtilde_v", vh, outv, 3, 3), ("qtilde_tv", gh, outg, 3, 3)):
+                xi = x[:3 * int(off[nb])] if opn == "qtilde_v" else x[:3 * int(off[nb]) - 6 * nb]
+                ref = ob.apply(opn, xi)
+                yo = y[:len(ref)]
+                o = 0
+                for j in range(nb):
+                    nj = int(off[j + 1] - off[j])
+                    ln = 3 * nj - 6 if opn == "qtilde_v" else 3 * nj
+                    r = ref[o:o + ln]
+                    worst = max(worst, float(np.linalg.norm(yo[o:o + ln] - r) / max(np.linalg.norm(r), 1e-300)))
+                    o += ln
+            parity = {"max_rel": worst, "bodies": nb, "ops": ["qtilde_v", "qtilde_tv"],
+                      "against": "C oracle (oracle/rq_oracle.c, pinned to the reference by tests/golden)",
+                      "tolerance": 1e-12}
 
     # ---- config 3 also as ONE batched application of its 100 fresh vectors (SURVEY 8(d):
     # "report sequential and, separately, batched k=100"): the multi-RHS kernels
@@ -373,7 +414,9 @@ def main():
         zops[zname] = {"ms": zms, "beads_per_s": N / (zms * 1e-3), "achieved_gbs": 48 * N / (zms * 1e-3) / 1e9,
                        "frac": 48 * N / (zms * 1e-3) / 1e9 / peaks()[0]}
 
-    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside
+    # ---- end to end with HOST buffers, copies inside the timed region: the C ABI on pinned
+    # buffers (what a binding that owns pinned memory calls) and the drop-in Python API on
+    # numpy arrays (MultiBodyOperator.apply, the reference's own calling convention)
     e2e = None
     if not args.no_e2e:
         hv = torch.empty(v2.shape, dtype=torch.float64, pin_memory=True)
@@ -394,15 +437,50 @@ def main():
             L.check(lib.rq_apply_host(h, L.OP_QTILDE_V, hv.data_ptr(), ho1.data_ptr(), k))
             L.check(lib.rq_apply_host(h, L.OP_QTILDE_TV, hg.data_ptr(), ho2.data_ptr(), k))
         e2e_ms = (time.perf_counter() - t0) / e_steps * 1e3
+        # numpy (pageable) through the Python API
+        nv, ng = hv.numpy().reshape(v.shape).copy(), hg.numpy().reshape(g.shape).copy()
+        for _ in range(2):
+            op.apply("qtilde_v", nv)
+            op.apply("qtilde_tv", ng)
+        n_steps = max(3, min(10, args.steps))
+        t0 = time.perf_counter()
+        for _ in range(n_steps):
+            op.apply("qtilde_v", nv)
+            op.apply("qtilde_tv", ng)
+        np_ms = (time.perf_counter() - t0) / n_steps * 1e3
         if dist:
-            t = torch.tensor([e2e_ms], device=dev)
+            t = torch.tensor([e2e_ms, np_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms, np_ms = (float(x) for x in t.tolist())
         nbytes_in = (hv.numel() + hg.numel()) * 8
         nbytes_out = (ho1.numel() + ho2.numel()) * 8
         e2e = {"value": n_job * k / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes_in,
                "d2h_bytes_per_step": nbytes_out, "ms_per_step": e2e_ms,
-               "path": "rq_apply_host (C ABI, pinned host buffers, H2D+D2H inside the timed region)"}
+               "path": "rq_apply_host (C ABI, pinned host buffers, H2D+D2H inside the timed region)",
+               "numpy": {"value": n_job * k / (np_ms * 1e-3), "ms_per_step": np_ms,
+                         "path": "MultiBodyOperator.apply on numpy arrays (pageable host memory)"}}
+
+    # ---- one-time gather of the shard outputs (strong sharding): NCCL all_gather of the
+    # max-padded shards, timed on the device, max over ranks
+    gather = None
+    if dist and strong:
+        from paper_1708_08427_b200.parallel import gather_shards
+
+        yv = op.apply("qtilde_v", v).reshape(-1)
+        rt = torch.tensor([yv.shape[0]], device=dev, dtype=torch.int64)
+        rows = [torch.zeros_like(rt) for _ in range(world)]
+        dist.all_gather(rows, rt)
+        rows = [int(r.item()) for r in rows]
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(s)
+        full = gather_shards(yv, rows)
+        a1.record(s)
+        torch.cuda.synchronize()
+        gms = torch.tensor([a0.elapsed_time(a1)], device=dev)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        gather = {"ms": float(gms.item()), "bytes": int(full.numel()) * 8, "what": "Q~v of the whole job to every rank"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -416,27 +494,33 @@ def main():
     launches = args.steps * (lib.rq_launches_per_apply(h, L.OP_QTILDE_V, k) +
                              lib.rq_launches_per_apply(h, L.OP_QTILDE_TV, k))
     if rank == 0:
+        cfgd = config_dict(name, off, k, world, strong and world > 1)
+        if emu:
+            cfgd["sharding"] = f"emulated: shard {emu[0]} of a {emu[1]}-way strong split, alone on one GPU"
         line = {
             "metric": METRIC, "value": value * k, "unit": UNIT if k == 1 else "bead-RHS/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": args.sharding, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(name, off, k, world, strong),
+            "scaling": "strong" if (strong and world > 1) else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": cfgd,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kname,
-                         "bytes_per_launch": chunk_bytes, "launch_ms": chunk_ms, "peak_source": peak_src,
+                         "bytes_per_launch": sweep_bytes, "launch_ms": sweep_ms, "peak_source": peak_src,
                          "share_of_step": share},
             "kernels_ms": {f"{a}:{b}": v_ for (a, b), v_ in kern.items()},
             "step_ms_single": step_stats,
+            "parity": parity,
             "z_ops": zops,
             "batched_k100": batched,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": ck, "gpu_launches": int(launches),
+            "cpu_baseline": cpu, "e2e": e2e, "gather": gather, "clocks": ck, "gpu_launches": int(launches),
             "setup": {"seconds": setup_s, "beads_per_s": N / setup_s, "first_build_seconds": setup_times[0],
                       "from": "host positions (pageable numpy), tree + factors + apply layout, device-synchronised"},
-            "plan": {kk: info[kk] for kk in ("n_chunks", "n_top", "blob_bytes", "max_chunk_bytes", "n_case",
-                                             "device_bytes", "tile_leaves", "chunk_smem", "top_staged", "chunk_ctas_per_sm", "chunk_smem_bytes",
-                                             "top_global")},
-            "bytes_per_bead_per_op": chunk_bytes / N,
+            "plan": {kk: info[kk] for kk in ("n_streams", "n_steps", "n_top", "n_tiles", "blob_bytes", "sweep_bytes",
+                                             "n_case", "device_bytes", "tile_leaves", "rounds", "host_segments",
+                                             "node_slots", "stage_bytes", "sweep_smem", "sweep_ctas_per_sm",
+                                             "top_staged", "top_global")},
+            "bytes_per_bead_per_op": sweep_bytes / N,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -59,24 +59,29 @@ typedef struct rq_plan_info {
   int64_t m;               /* bodies */
   int64_t n_beads;         /* total beads */
   int64_t n_nodes;         /* total nodes (sum 2n_j - 1) */
-  int64_t n_chunks;        /* apply work units */
+  int64_t n_streams;       /* wavefront streams = persistent sweep CTAs */
+  int64_t n_steps;         /* barrier steps over all streams */
   int64_t n_top;           /* nodes above the tiles */
-  int64_t tile_leaves;     /* tile size limit */
-  int64_t blob_bytes;      /* chunk blobs streamed per apply */
+  int64_t tile_leaves;     /* tile size limit S */
+  int64_t n_tiles;         /* tiles with >= 2 beads */
+  int64_t blob_bytes;      /* wave blob (records + both sweeps' metadata and gather lists) */
+  int64_t sweep_bytes[2];  /* blob bytes one upward / downward sweep streams */
   int64_t record_doubles;  /* compact factor records */
   int64_t full_len;        /* 3N            */
   int64_t comp_len;        /* 3N - 6m       */
-  int64_t max_chunk_bytes; /* largest blob */
   int64_t n_case[4];       /* node counts per case (leaf, BB, RB, GEN) */
   int64_t device_bytes;    /* device memory held by the plan */
-  int64_t chunk_smem[6];   /* max head bytes, max level-record bytes, max beads, max nodes, max residues, max tiles */
+  int64_t rounds;          /* tile rounds (all streams work inside one round at a time) */
+  int64_t host_segments;   /* host-buffer pipeline segments (groups of rounds) */
+  int64_t node_slots;      /* node 6-vector slots per sweep CTA (shared memory) */
+  int64_t stage_bytes;     /* shared-memory stage of one step block */
+  int64_t sweep_smem;      /* dynamic shared memory per sweep CTA */
+  int64_t sweep_ctas_per_sm; /* resident sweep CTAs per SM */
   int64_t top_staged;      /* bodies whose top tree is staged in shared memory */
   int64_t top_global;      /* bodies whose top tree is swept from global memory */
   int64_t mrhs_min_k;      /* k at and above which the column-parallel (multi-RHS) kernels run */
   int64_t mrhs_units[2];   /* multi-RHS unit programs: tiles, top trees (0 until the first k >= mrhs_min_k apply) */
   int64_t mrhs_bytes[2];   /* program bytes read per column group: tile units, top units */
-  int64_t chunk_ctas_per_sm[2]; /* resident single-RHS chunk CTAs per SM: downward, upward sweep */
-  int64_t chunk_smem_bytes[2];  /* their dynamic shared memory per CTA */
 } rq_plan_info;
 
 /* Last error message of the calling thread ("" if none). */
@@ -118,11 +123,11 @@ int rq_plan_device(const rq_plan *plan);
  */
 int rq_apply(const rq_plan *plan, int op, const double *in, double *out, int64_t k,
              void *stream);
-/* Phase-selective variant for profiling (bench.py times the chunk sweep
+/* Phase-selective variant for profiling (bench.py times the tile sweep
  * alone): phases is a mask of RQ_PHASE_*; rq_apply == all phases. */
-#define RQ_PHASE_CHUNKS 1u
-#define RQ_PHASE_TOP 2u
-#define RQ_PHASE_SMALL 4u
+#define RQ_PHASE_SWEEP 1u   /* k_wave: the tiles */
+#define RQ_PHASE_TOP 2u     /* k_top2 / k_top_df: the top trees */
+#define RQ_PHASE_LAYOUT 4u  /* Q / Q^T: root rows <-> private residue layout */
 int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int64_t k,
                 void *stream, uint32_t phases);
 /* Number of kernel launches one rq_apply issues. */

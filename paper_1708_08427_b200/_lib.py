@@ -39,13 +39,14 @@ _dp, _ip, _i32p, _u8p, _vp = (C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POI
 
 
 class PlanInfo(C.Structure):
-    _fields_ = [("m", C.c_int64), ("n_beads", C.c_int64), ("n_nodes", C.c_int64), ("n_chunks", C.c_int64),
-                ("n_top", C.c_int64), ("tile_leaves", C.c_int64), ("blob_bytes", C.c_int64),
-                ("record_doubles", C.c_int64), ("full_len", C.c_int64), ("comp_len", C.c_int64),
-                ("max_chunk_bytes", C.c_int64), ("n_case", C.c_int64 * 4), ("device_bytes", C.c_int64),
-                ("chunk_smem", C.c_int64 * 6), ("top_staged", C.c_int64), ("top_global", C.c_int64),
-                ("mrhs_min_k", C.c_int64), ("mrhs_units", C.c_int64 * 2), ("mrhs_bytes", C.c_int64 * 2),
-                ("chunk_ctas_per_sm", C.c_int64 * 2), ("chunk_smem_bytes", C.c_int64 * 2)]
+    _fields_ = [("m", C.c_int64), ("n_beads", C.c_int64), ("n_nodes", C.c_int64), ("n_streams", C.c_int64),
+                ("n_steps", C.c_int64), ("n_top", C.c_int64), ("tile_leaves", C.c_int64), ("n_tiles", C.c_int64),
+                ("blob_bytes", C.c_int64), ("sweep_bytes", C.c_int64 * 2), ("record_doubles", C.c_int64),
+                ("full_len", C.c_int64), ("comp_len", C.c_int64), ("n_case", C.c_int64 * 4),
+                ("device_bytes", C.c_int64), ("rounds", C.c_int64), ("host_segments", C.c_int64),
+                ("node_slots", C.c_int64), ("stage_bytes", C.c_int64), ("sweep_smem", C.c_int64),
+                ("sweep_ctas_per_sm", C.c_int64), ("top_staged", C.c_int64), ("top_global", C.c_int64),
+                ("mrhs_min_k", C.c_int64), ("mrhs_units", C.c_int64 * 2), ("mrhs_bytes", C.c_int64 * 2)]
 
 
 SIGNATURES = [

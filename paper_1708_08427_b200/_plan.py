@@ -70,13 +70,11 @@ class Plan:
         inf = L.PlanInfo()
         L.check(L.lib().rq_plan_get_info(self._h, C.byref(inf)))
         d = {k: getattr(inf, k) for k, _ in L.PlanInfo._fields_
-             if k not in ("n_case", "chunk_smem", "mrhs_units", "mrhs_bytes", "chunk_ctas_per_sm", "chunk_smem_bytes")}
-        d["chunk_ctas_per_sm"] = {"down": inf.chunk_ctas_per_sm[0], "up": inf.chunk_ctas_per_sm[1]}
-        d["chunk_smem_bytes"] = {"down": inf.chunk_smem_bytes[0], "up": inf.chunk_smem_bytes[1]}
+             if k not in ("n_case", "sweep_bytes", "mrhs_units", "mrhs_bytes")}
+        d["sweep_bytes"] = {"up": inf.sweep_bytes[0], "down": inf.sweep_bytes[1]}
         d["mrhs_units"] = {"tiles": inf.mrhs_units[0], "tops": inf.mrhs_units[1]}
         d["mrhs_bytes"] = {"tiles": inf.mrhs_bytes[0], "tops": inf.mrhs_bytes[1]}
         d["n_case"] = list(inf.n_case)
-        d["chunk_smem"] = dict(zip(("head", "level_rec", "beads", "nodes", "res", "tiles"), list(inf.chunk_smem)))
         return d
 
     # ---- lengths -------------------------------------------------------------

@@ -54,7 +54,7 @@ extern "C" {
 
 const char *rq_last_error(void) { return rq::last_error(); }
 
-int rq_version(void) { return 101; }
+int rq_version(void) { return 200; }
 
 int rq_device_count(void) {
   int n = 0;
@@ -116,22 +116,29 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
     info->m = p.m;
     info->n_beads = p.N;
     info->n_nodes = p.NN;
-    info->n_chunks = p.n_chunks;
+    info->n_streams = p.wave_streams;
+    info->n_steps = p.wave_steps;
     info->n_top = p.n_top;
     info->tile_leaves = p.tile_leaves;
-    info->blob_bytes = p.blob_bytes;
+    info->n_tiles = p.n_tiles;
+    info->blob_bytes = p.wave_blob_bytes;
+    info->sweep_bytes[0] = p.wave_up_bytes;
+    info->sweep_bytes[1] = p.wave_down_bytes;
     info->record_doubles = p.rec_doubles;
     info->full_len = 3 * p.N;
     info->comp_len = 3 * p.N - 6 * p.m;
-    info->max_chunk_bytes = p.max_blob;
     for (int c = 0; c < 4; c++) info->n_case[c] = p.n_case[c];
     info->device_bytes = p.device_bytes();
-    info->chunk_smem[0] = p.max_head_bytes;
-    info->chunk_smem[1] = p.max_level_rec_bytes;
-    info->chunk_smem[2] = p.max_chunk_beads;
-    info->chunk_smem[3] = p.max_chunk_nodes;
-    info->chunk_smem[4] = p.max_chunk_res;
-    info->chunk_smem[5] = p.max_chunk_tiles;
+    info->rounds = p.wave_rounds;
+    info->host_segments = p.wave_nseg;
+    info->node_slots = p.wave_mslots;
+    info->stage_bytes = p.wave_stage_bytes;
+    if (p.wave_streams) {
+      info->sweep_smem = (int64_t)rq::wave_smem(p, nullptr, nullptr, nullptr);
+      RQ_CUDA(cudaSetDevice(p.device));
+      rq::wave_prepare(p);
+      info->sweep_ctas_per_sm = p.wave_ctas_per_sm;
+    }
     info->top_staged = p.n_topblob;
     info->top_global = p.n_topbig;
     info->mrhs_min_k = p.mrhs_min;
@@ -139,13 +146,6 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
     info->mrhs_units[1] = p.n_top_units;
     info->mrhs_bytes[0] = p.mrhs_tile_bytes;
     info->mrhs_bytes[1] = p.mrhs_top_bytes;
-    int ctas[2] = {0, 0};
-    int64_t sm[2] = {0, 0};
-    if (p.n_chunks) rq::chunk_occupancy(p, ctas, sm);
-    for (int u = 0; u < 2; u++) {
-      info->chunk_ctas_per_sm[u] = ctas[u];
-      info->chunk_smem_bytes[u] = sm[u];
-    }
   })
 }
 

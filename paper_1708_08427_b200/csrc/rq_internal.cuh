@@ -6,10 +6,9 @@
 //    node ids inside a body are the reference's postorder ids (tree.py:127-129).
 //  * every internal node has a compact factor record (Householder vectors of
 //    the LQ of factor.py:90-109 + taus; explicit 3x3 mixer for BEAD_BEAD).
-//  * the apply path streams "chunks": forests of maximal subtrees ("tiles")
-//    of <= tile_leaves beads, whose records are re-packed level-major and
-//    struct-of-arrays into one contiguous, 16-byte aligned blob per chunk.
-//    Nodes above the tiles form a small per-body "top tree".
+//  * the apply path sweeps "tiles" (maximal subtrees of <= tile_leaves beads)
+//    through wavefront streams of step blocks (rq_wave.cuh); the nodes above
+//    the tiles form a small per-body "top tree" (TopNode / staged top blobs).
 #pragma once
 
 #include <cstdint>
@@ -35,52 +34,7 @@ __host__ __device__ constexpr int res_rows(int c) {
   return c == RIGID_BEAD ? 3 : (c == GENERAL ? 6 : 0);
 }
 
-// ---- apply layout -------------------------------------------------------
-
-struct LevelDesc {       // one height level of a chunk, 32 bytes
-  int32_t slot_begin;    // first chunk-local slot of the level
-  int32_t nG, nR, nB;    // nodes per case (slots ordered GEN, RB, BB)
-  int32_t recG, recR, recB;  // double offsets of the per-case record groups (AoS, rec_size stride)
-  int32_t pad;
-};
-
-struct NodeMeta {        // 8 bytes, one per in-chunk internal node (slot order)
-  uint16_t x, y;         // formula-x/-y child: bit 15 set -> bead (local index), else slot
-  uint16_t res;          // residue offset in the chunk staging buffer
-  uint16_t flags;        // case | swapped | signs
-};
-
-// Chunk blob layout (16-byte aligned sections):
-//   ChunkDesc (64 B) | TileDesc[n_tiles] | LevelDesc[n_levels] | NodeMeta[n_nodes] | perm[n_beads] | records
-struct ChunkDesc {
-  int64_t blob_off;      // byte offset of the blob (16-byte aligned)
-  int32_t blob_bytes;    // multiple of 16
-  int32_t n_nodes;
-  int32_t n_beads;       // local bead window [bead_begin, bead_begin+n_beads) in tree order
-  int32_t n_levels;
-  int32_t n_tiles;
-  int32_t body;
-  int64_t bead_begin;    // global tree-order bead index of local bead 0
-  int64_t tile_begin;    // first TileDesc
-  int32_t off_meta;      // byte offsets inside the blob
-  int32_t off_perm;
-  int32_t off_rec;
-  int32_t n_res;         // residue doubles staged
-  int64_t body_bead0;    // first (global) bead of the body
-  int64_t spec_full;     // first residue row of the body in the Q layout (3 bead0 + 6)
-  int64_t spec_comp;     // first residue row of the body in the Q~ layout (3 bead0 - 6 body)
-  int64_t pad;
-};  // 96 bytes
-
-struct TileDesc {        // 32 bytes; copies live in the chunk blob after the ChunkDesc header
-  int32_t root_slot;     // chunk-local slot of the tile root
-  int32_t scratch;       // exchange slot with the top tree, -1 if the tile root is the body root
-  int32_t res_q;         // body-relative complement (Q~) offset of the tile's first residue
-  int32_t res_count;     // 3L - 6
-  int32_t res_local;     // offset in the chunk staging buffer
-  int32_t res_delta;     // res_q - res_local (one load on the upward node path)
-  int32_t pad[2];
-};
+// ---- top trees (nodes with more than S beads) ----------------------------
 
 struct TopNode {         // node with more than tile_leaves beads
   int32_t x, y;          // >= 0: exchange slot; < 0: ~(global tree-order bead index)
@@ -107,11 +61,6 @@ struct TopMeta {         // 16 bytes, nodes sorted by height
   int32_t rec;           // double offset of its record in the record area
 };
 // top-blob inputs: >= 0 exchange slot (a tile root), < 0 ~(body-local original bead index)
-
-// perm entries in a chunk blob: body-local original bead index, or
-// (PERM_FOREIGN | idx) for beads handled by the top tree (singleton tiles).
-constexpr uint32_t PERM_FOREIGN = 0x80000000u;
-constexpr uint16_t SRC_BEAD = 0x8000u;
 
 // Householder work layout for K in {3, 6, 9}: v0 (K-1), v1 (K-2), v2 (K-3), tau0, tau1, tau2.
 template <int K>

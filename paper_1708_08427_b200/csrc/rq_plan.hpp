@@ -102,18 +102,12 @@ struct Plan {
   int device = 0;
   int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
   int max_depth = 96;
-  int tile_leaves = 48;            // S (measured best for config 2 with 40 KiB chunks)
+  int tile_leaves = 48;            // S: tiles are maximal subtrees with <= S beads
   int tile_height = 0;             // tile height cut (0: none)
-  int chunk_threads = 128;         // threads per chunk CTA
-  int64_t max_blob = 0;            // largest chunk blob (bytes)
-  int64_t max_head_bytes = 0;      // largest chunk head (everything before the records)
-  int64_t max_level_rec_bytes = 0; // largest record block of one level of one chunk
-  int max_chunk_nodes = 0, max_chunk_beads = 0, max_chunk_levels = 0, max_chunk_res = 0, max_chunk_tiles = 0;
   std::vector<int64_t> bead_off;   // host copy, m+1
   int64_t n_case[4] = {0, 0, 0, 0};
   int64_t rec_doubles = 0;
-  int64_t blob_bytes = 0;
-  int64_t n_chunks = 0, n_tiles = 0, n_top = 0, n_slots = 0, n_topbodies = 0, n_toplevels = 0;
+  int64_t n_tiles = 0, n_top = 0, n_slots = 0, n_topbodies = 0, n_toplevels = 0;
   int64_t n_small = 0;             // bodies with n == 1
   int64_t min_n = 0;
 
@@ -137,10 +131,7 @@ struct Plan {
   DBuf rec_off;                    // int64 [NN]
   DBuf res_off;                    // int32 [NN] body-relative spectral offsets
   DBuf rec;                        // double [rec_doubles] compact records (postorder)
-  // apply layout
-  DBuf chunks;                     // ChunkDesc [n_chunks]
-  DBuf tiles;                      // TileDesc [n_tiles]
-  DBuf blob;                       // bytes
+  // top trees
   DBuf top;                        // TopNode [n_top], sorted by (body, height)
   DBuf topbody;                    // int32 [n_topbodies]: body ids needing the top kernels
   DBuf topbody_lvl;                // int32 [n_topbodies+1]: level CSR into toplvl
@@ -163,7 +154,7 @@ struct Plan {
   DBuf top_paths, top_path_off;    // int32 root-to-start paths, int64 [n_top_start+1] CSR offsets
   std::vector<int64_t> h_topstart_first;  // [m+1]
   // host-side body -> work-list ranges (segmented / pipelined applications)
-  std::vector<int64_t> h_chunk_first, h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each
+  std::vector<int64_t> h_topblob_first, h_topbig_first, h_small_first;  // [m+1] each
   std::vector<int64_t> h_topblob_off;  // [n_topblob+1]: staged top blob byte offsets (host copy)
   DBuf err;                        // int64 [8] device error flags
   // deterministic per-body reductions (centroid, Zf): fixed segments
@@ -175,6 +166,16 @@ struct Plan {
   // host-buffer entry points: persistent device staging (grown on demand)
   mutable DBuf stage_in, stage_out;
   mutable cudaStream_t host_stream = nullptr, host_stream2 = nullptr, host_stream3 = nullptr;
+  // host-buffer pipelining (rq_host.cu): per-segment flags / counters, and the top-tree residue
+  // rows (built on the first host application): row in the private layout, count, compact offset
+  mutable DBuf top_rows_d, top_coff_d, top_compact;
+  mutable void *host_sync = nullptr;  // uint32 flags [nseg] | counters [nseg]
+  mutable uint32_t host_epoch = 0;
+  mutable int64_t n_top_rows = -1, top_compact_doubles = 0;
+  mutable std::vector<int64_t> h_top_rows, h_top_coff;
+  mutable std::vector<int32_t> h_top_rr;
+  mutable double *top_pinned = nullptr;
+  mutable cudaEvent_t host_ev = nullptr;
 
   mutable std::mutex host_mu;
   // Per-stream exchange state: applications of one plan on different streams may run
@@ -186,6 +187,7 @@ struct Plan {
     DBuf chunk_ctr;           // 2 x {claim, done} counters of the dynamic chunk schedule
     DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
     DBuf res_tmp, roots;      // Q / Q^T: residues in the private layout and the 6 root rows per body
+    DBuf in_al;               // 16-byte aligned copy of a misaligned input
     DBuf zpart;               // Zf per-segment partial sums
     uint32_t chunk_epoch = 0;  // chunk launches so far (consecutive launches alternate counters)
   };
@@ -210,7 +212,9 @@ struct Plan {
   int64_t wave_streams = 0, wave_steps = 0, wave_blob_bytes = 0, wave_nodes = 0;
   int64_t wave_up_bytes = 0, wave_down_bytes = 0;  // bytes one upward / downward sweep streams
   int64_t wave_stage_bytes = 0, wave_rounds = 1;
-  int wave_mslots = 0, wave_pf = 0, wave_nst = 2;  // L2 prefetch distance, TMA stages
+  int wave_nseg = 1;                         // host segments (groups of rounds)
+  std::vector<int> wave_seg_minb, wave_seg_maxb;  // body range of each segment's tiles
+  int wave_mslots = 0, wave_pf = 0, wave_nst = 2;  // L2 prefetch distance (steps), TMA stages (fixed 2)
   WaveCaps wave_caps;
   DBuf wave_desc;                  // StepDesc [wave_steps]
   DBuf wave_stream_first;          // int64 [wave_streams + 1]
@@ -222,6 +226,9 @@ struct Plan {
   ~Plan() {
     for (cudaStream_t st : {host_stream, host_stream2, host_stream3})
       if (st) cudaStreamDestroy(st);
+    if (top_pinned) cudaFreeHost(top_pinned);
+    if (host_ev) cudaEventDestroy(host_ev);
+    if (host_sync) cudaFree(host_sync);
   }
 };
 
@@ -240,20 +247,25 @@ size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg);
 void wave_prepare(const Plan &p);
 // tile part of one upward / downward sweep over all bodies (rq_wave.cu); residues in the
 // private layout, body-root vectors to / from `roots` (nullptr: dropped / zero)
+struct WaveSync {             // host-buffer pipelining (rq_wave.cuh)
+  const uint32_t *flags;     // [nseg] written by the copy engine after each input segment
+  uint32_t *counters;        // [nseg] bumped by every CTA once a segment's outputs are written
+  uint32_t epoch;            // flags / counters targets of this application
+  cudaEvent_t before_top;    // upward: the top pass waits for it (all input copies done)
+};
 void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots,
-              cudaStream_t s);
+              cudaStream_t s, const WaveSync *sync = nullptr);
 // bodies [j0, j1) of a plan (all work lists are in body order)
 struct BodyRange {
   int64_t j0 = 0, j1 = -1;  // j1 < 0: all bodies
 };
+struct WaveSync;
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
-               unsigned phases = 7u, BodyRange range = BodyRange());
+               unsigned phases = 7u, const WaveSync *sync = nullptr);
 void build_mrhs(const Plan &p, cudaStream_t s);
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
                     unsigned phases = 7u, BodyRange range = BodyRange());
 bool use_mrhs(const Plan &p, int64_t k);
-// resident chunk CTAs per SM and dynamic shared memory of k_chunk (index 0: DOWN, 1: UP)
-void chunk_occupancy(const Plan &p, int ctas[2], int64_t smem[2]);
 // Host-buffer application pipelined over body segments: H2D of segment i+1,
 // kernels of segment i and D2H of segment i-1 overlap (three streams).
 void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k);

@@ -497,11 +497,6 @@ __global__ void k_classify(LayoutCtx c, int64_t NN, int32_t *is_tile, int32_t *i
 struct TileTmp {
   int64_t root;      // global node id
   int32_t body, L, start, height;
-  int64_t rec_doubles;
-  int32_t res_q;     // body-relative Q~ offset of the first residue
-  int32_t big;       // L >= 2
-  int32_t lvmax;     // record doubles of its widest height level
-  int32_t pad;
 };
 
 __global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const int32_t *tile_scan,
@@ -517,262 +512,16 @@ __global__ void k_tiles(LayoutCtx c, int64_t NN, const int32_t *is_tile, const i
   T.L = L;
   T.start = c.start[g];
   T.height = c.height[g];
-  T.rec_doubles = c.rec_off[g] + rec_size(flag_case(c.flags[g])) - c.rec_off[first];
-  T.res_q = c.res_off[first] - 6;
-  T.big = L >= 2;
-  // per-height record doubles of the tile (its nodes are contiguous in postorder)
-  int acc[64];
-  for (int h = 0; h < 64; h++) acc[h] = 0;
-  for (int64_t q = first; q <= g; q++)
-    if (nodeL(c, q) >= 2) acc[min(63, c.height[q])] += rec_size(flag_case(c.flags[q]));
-  int mx = 0;
-  for (int h = 0; h < 64; h++) mx = max(mx, acc[h]);
-  T.lvmax = mx;
-  T.pad = 0;
   tiles[t] = T;
   marker[first] = t;
 }
 
-struct ChunkLimits {
-  int64_t max_bytes;
-  int max_nodes, max_beads, max_res, max_tiles;
-  int max_lrec;  // bound on one level step's record doubles (sum of the tiles' widest levels)
-};
-
-__host__ __device__ inline int64_t meta_bytes(int nodes) { return ((int64_t)nodes * 8 + 15) / 16 * 16; }
-__host__ __device__ inline int64_t perm_bytes(int beads) { return ((int64_t)beads * 4 + 15) / 16 * 16; }
-__host__ __device__ inline int64_t head_bytes(int tiles, int H) {
-  return (int64_t)sizeof(ChunkDesc) + (int64_t)sizeof(TileDesc) * tiles + (int64_t)sizeof(LevelDesc) * H;
-}
-__host__ __device__ inline int64_t blob_bytes_of(int H, int nodes, int beads, int64_t rec, int tiles) {
-  return head_bytes(tiles, H) + meta_bytes(nodes) + perm_bytes(beads) + rec * 8;  // rec is even: 16-byte multiple
-}
-
-// Greedy packing of consecutive tiles into chunks, one thread per packing segment
-// (a body's tile sequence cut every PACK_SEG tiles, so large bodies pack in parallel).
-// pass 0: count chunks per segment; pass 1: write descriptors.
-constexpr int PACK_SEG = 256;
-__global__ void k_pack(const TileTmp *tiles, const int64_t *seg_tile_begin, const int32_t *seg_body,
-                       const int64_t *bead_off, int64_t nseg, ChunkLimits lim, int pass, const int64_t *chunk_base,
-                       const int32_t *big_scan, int64_t *n_chunks_seg, ChunkDesc *chunks,
-                       int64_t *chunk_of_tile, int32_t *res_local_of_tile, int32_t *bead_local_of_tile) {
-  const int64_t sg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (sg >= nseg) return;
-  const int64_t j = seg_body[sg];
-  int64_t tb = seg_tile_begin[sg], te = seg_tile_begin[sg + 1];
-  int64_t nch = 0;
-  bool open = false;
-  int beads = 0, nodes = 0, H = 0, res = 0, ntiles = 0, lrec = 0;
-  int64_t rec = 0, tile0 = 0;
-  auto flush = [&]() {
-    if (!open) return;
-    if (pass == 1) {
-      ChunkDesc &d = chunks[chunk_base[sg] + nch];
-      d.blob_off = 0;
-      d.n_nodes = nodes;
-      d.n_levels = H;
-      d.n_tiles = ntiles;
-      d.body = (int32_t)j;
-      d.bead_begin = bead_off[j];  // the chunk's beads are its tiles' beads, in tile order
-      d.body_bead0 = bead_off[j];
-      d.spec_full = 3 * bead_off[j] + 6;
-      d.spec_comp = 3 * bead_off[j] - 6 * j;
-      d.pad = 0;
-      d.tile_begin = big_scan[tile0];
-      d.n_res = res;
-      d.off_meta = (int32_t)head_bytes(ntiles, H);
-      d.off_perm = (int32_t)(d.off_meta + meta_bytes(nodes));
-      d.n_beads = beads;
-      d.off_rec = (int32_t)(head_bytes(ntiles, H) + meta_bytes(nodes) + perm_bytes(beads));
-      d.blob_bytes = (int32_t)blob_bytes_of(H, nodes, beads, rec, ntiles);
-    }
-    nch++;
-    open = false;
-  };
-  for (int64_t t = tb; t < te; t++) {
-    const TileTmp &T = tiles[t];
-    if (!T.big) continue;
-    int Tn = T.L - 1, Tres = 3 * T.L - 6;
-    if (open) {
-      int beads2 = beads + T.L, lrec2 = lrec + T.lvmax;
-      int nodes2 = nodes + Tn, H2 = max(H, T.height), res2 = res + Tres;
-      int64_t rec2 = rec + T.rec_doubles;
-      if (beads2 > lim.max_beads || nodes2 > lim.max_nodes || res2 > lim.max_res || ntiles + 1 > lim.max_tiles ||
-          lrec2 > lim.max_lrec ||
-          blob_bytes_of(H2, nodes2, beads2, rec2, ntiles + 1) > lim.max_bytes)
-        flush();
-    }
-    if (!open) {
-      open = true;
-      beads = 0; nodes = 0; H = 0; res = 0; rec = 0; ntiles = 0; lrec = 0; tile0 = t;
-    }
-    if (pass == 1) {
-      chunk_of_tile[t] = chunk_base[sg] + nch;
-      res_local_of_tile[t] = res;
-      bead_local_of_tile[t] = beads;
-    }
-    nodes += Tn;
-    H = max(H, T.height);
-    res += Tres;
-    rec += T.rec_doubles;
-    ntiles++;
-    beads += T.L;
-    lrec += T.lvmax;
-  }
-  flush();
-  if (pass == 0) n_chunks_seg[sg] = nch;
-}
-
-__global__ void k_chunk_sizes(const ChunkDesc *chunks, int64_t nc, int64_t *bytes, int64_t *nodes,
-                              int64_t *levels) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= nc) return;
-  bytes[c] = chunks[c].blob_bytes;
-  nodes[c] = chunks[c].n_nodes;
-  levels[c] = chunks[c].n_levels;
-}
-
-__global__ void k_chunk_offsets(ChunkDesc *chunks, int64_t nc, const int64_t *bytes_scan) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c < nc) chunks[c].blob_off = bytes_scan[c];
-}
-
-// key for the level-major node order inside chunks
-__global__ void k_node_keys(LayoutCtx c, int64_t NN, const int32_t *is_top, const int32_t *tile_of,
-                            const int64_t *chunk_of_tile, uint64_t *keys, int32_t *vals) {
-  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (g >= NN) return;
-  int cs = flag_case(c.flags[g]);
-  uint64_t key = ~0ull;
-  if (cs != LEAF && !is_top[g]) {
-    int64_t ch = chunk_of_tile[tile_of[g]];
-    int rank = cs == GENERAL ? 0 : (cs == RIGID_BEAD ? 1 : 2);
-    key = ((uint64_t)ch << 24) | ((uint64_t)c.height[g] << 2) | (uint64_t)rank;
-  }
-  keys[g] = key;
-  vals[g] = (int32_t)g;
-}
-
-__global__ void k_slots(const uint64_t *keys, const int32_t *vals, int64_t n_part,
-                        const int64_t *chunk_node_scan, int32_t *slot_of, const int64_t *lvl_base,
-                        LevelDesc *lvl, const uint8_t *flags) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n_part) return;
-  uint64_t key = keys[p];
-  int64_t ch = (int64_t)(key >> 24);
-  int h = (int)((key >> 2) & 0x3fffff);
-  int g = vals[p];
-  slot_of[g] = (int32_t)(p - chunk_node_scan[ch]);
-  int cs = flag_case(flags[g]);
-  LevelDesc *L = &lvl[lvl_base[ch] + h - 1];
-  atomicAdd(cs == GENERAL ? &L->nG : (cs == RIGID_BEAD ? &L->nR : &L->nB), 1);
-}
-
-__global__ void k_levels_finalize(const ChunkDesc *chunks, int64_t nc, const int64_t *lvl_base,
-                                  LevelDesc *lvl, uint8_t *blob, unsigned long long *max_lrec) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= nc) return;
-  const ChunkDesc &d = chunks[c];
-  int slot = 0, recd = 0;
-  LevelDesc *dst = reinterpret_cast<LevelDesc *>(blob + d.blob_off + sizeof(ChunkDesc) + sizeof(TileDesc) * d.n_tiles);
-  *reinterpret_cast<ChunkDesc *>(blob + d.blob_off) = d;  // header copy for the kernels
-  for (int h = 0; h < d.n_levels; h++) {
-    LevelDesc &L = lvl[lvl_base[c] + h];
-    L.slot_begin = slot;
-    L.recG = recd; recd += rec_size(GENERAL) * L.nG;
-    L.recR = recd; recd += rec_size(RIGID_BEAD) * L.nR;
-    L.recB = recd; recd += rec_size(BEAD_BEAD) * L.nB;
-    L.pad = 0;
-    slot += L.nG + L.nR + L.nB;
-    dst[h] = L;
-    atomicMax(max_lrec, (unsigned long long)8 * (rec_size(GENERAL) * L.nG + rec_size(RIGID_BEAD) * L.nR +
-                                                 rec_size(BEAD_BEAD) * L.nB));
-  }
-}
-
-struct WriteCtx {
-  LayoutCtx c;
-  const uint64_t *keys;
-  const int32_t *vals;
-  const int32_t *slot_of, *tile_of, *left, *right;
-  const TileTmp *tiles;
-  const int32_t *res_local_of_tile, *bead_local_of_tile;
-  const ChunkDesc *chunks;
-  const int64_t *lvl_base;
-  const LevelDesc *lvl;
-  const double *rec;
-  uint8_t *blob;
-  const int32_t *big_scan;  // tile -> global TileDesc index (chunk-local = big_scan - chunk.tile_begin)
-};
-
-__global__ void k_write_nodes(WriteCtx w, int64_t n_part) {
-  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= n_part) return;
-  uint64_t key = w.keys[p];
-  int64_t ch = (int64_t)(key >> 24);
-  int h = (int)((key >> 2) & 0x3fffff);
-  int64_t g = w.vals[p];
-  const ChunkDesc &d = w.chunks[ch];
-  const LevelDesc &L = w.lvl[w.lvl_base[ch] + h - 1];
-  int slot = w.slot_of[g];
-  unsigned f = w.c.flags[g];
-  int cs = flag_case(f);
-  int j = d.body;
-  int64_t nb = w.c.node_off[j];
-  const int tile_idx = w.tile_of[g];
-  const TileTmp &T = w.tiles[tile_idx];
-  const int local0 = T.start - w.bead_local_of_tile[tile_idx];  // chunk bead i <-> body bead local0 + i within the tile
-  int l = w.left[g], r = w.right[g];
-  int xi = l, yi = r;
-  if (flag_swapped(f)) { xi = r; yi = l; }
-  auto enc = [&](int id) -> uint16_t {
-    int64_t cg = nb + id;
-    if (w.c.stop[cg] - w.c.start[cg] == 1) return (uint16_t)(SRC_BEAD | (w.c.start[cg] - local0));
-    return (uint16_t)w.slot_of[cg];
-  };
-  NodeMeta md;
-  md.x = enc(xi);
-  md.y = enc(yi);
-  md.res = (uint16_t)(w.res_local_of_tile[tile_idx] + (w.c.res_off[g] - 6 - T.res_q));
-  // bits 0-5: case | swapped | signs; bits 6-15: chunk-local tile index (upward residue stores)
-  md.flags = (uint16_t)(f | ((w.big_scan[tile_idx] - d.tile_begin) << 6));
-  uint8_t *base = w.blob + d.blob_off;
-  reinterpret_cast<NodeMeta *>(base + d.off_meta)[slot] = md;
-  double *R = reinterpret_cast<double *>(base + d.off_rec);
-  int q = slot - L.slot_begin;
-  const double *src = w.rec + w.c.rec_off[g];
-  if (cs == GENERAL) {
-    for (int e = 0; e < rec_size(GENERAL); e++) R[L.recG + q * rec_size(GENERAL) + e] = src[e];
-  } else if (cs == RIGID_BEAD) {
-    q -= L.nG;
-    for (int e = 0; e < rec_size(RIGID_BEAD); e++) R[L.recR + q * rec_size(RIGID_BEAD) + e] = src[e];
-  } else {
-    q -= L.nG + L.nR;
-    for (int e = 0; e < rec_size(BEAD_BEAD); e++) R[L.recB + q * rec_size(BEAD_BEAD) + e] = src[e];
-  }
-}
-
-// perm section of each blob; beads of singleton tiles are marked foreign
 __global__ void k_root_is_top(const int32_t *is_top, const int64_t *bead_off, const int64_t *node_off, int64_t m,
                               int32_t *out) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= m) return;
   const int64_t n = bead_off[j + 1] - bead_off[j];
   out[j] = is_top[node_off[j] + 2 * n - 2];
-}
-
-// chunk perm: one thread per tile writes its beads' body-local original indices
-__global__ void k_write_perm(const TileTmp *tiles, int64_t n_tiles_all, const int64_t *chunk_of_tile,
-                             const int32_t *bead_local_of_tile, const ChunkDesc *chunks, const int32_t *perm,
-                             const int64_t *bead_off, uint8_t *blob) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n_tiles_all) return;
-  const TileTmp &T = tiles[t];
-  if (!T.big) return;
-  const ChunkDesc &d = chunks[chunk_of_tile[t]];
-  uint32_t *P = reinterpret_cast<uint32_t *>(blob + d.blob_off + d.off_perm) + bead_local_of_tile[t];
-  const int64_t gb = bead_off[T.body] + T.start;
-  for (int i = 0; i < T.L; i++) P[i] = (uint32_t)perm[gb + i];
 }
 
 // tile renumbering after the per-body height sort
@@ -797,38 +546,14 @@ __global__ void k_tile_permute(const TileTmp *tiles, const int32_t *order, int64
   inv[t] = (int32_t)k;
 }
 
-// big flag per tile; first tile of each body (tiles are grouped by body)
-__global__ void k_tile_flags(const TileTmp *tiles, int64_t n, int32_t *big, int64_t *body_begin) {
+__global__ void k_count_big(const TileTmp *tiles, int64_t n, unsigned long long *cnt) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  big[t] = tiles[t].big ? 1 : 0;
-  if (t == 0 || tiles[t - 1].body != tiles[t].body) body_begin[tiles[t].body] = t;
+  if (t < n && tiles[t].L >= 2) atomicAdd(cnt, 1ull);
 }
 
 __global__ void k_remap_tiles(int32_t *tile_of, int64_t NN, const int32_t *inv) {
   int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g < NN && tile_of[g] >= 0) tile_of[g] = inv[tile_of[g]];
-}
-
-__global__ void k_tile_desc(const TileTmp *tiles, int64_t n_tiles_all, const int32_t *big_scan,
-                            const int32_t *slot_of, const int32_t *slot_scan,
-                            const int32_t *res_local_of_tile, const int32_t *parent, TileDesc *out,
-                            const int64_t *chunk_of_tile, const ChunkDesc *chunks, uint8_t *blob) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= n_tiles_all) return;
-  const TileTmp &T = tiles[t];
-  if (!T.big) return;
-  TileDesc d;
-  d.root_slot = slot_of[T.root];
-  d.scratch = parent[T.root] < 0 ? -1 : slot_scan[T.root];
-  d.res_q = T.res_q;
-  d.res_count = 3 * T.L - 6;
-  d.res_local = res_local_of_tile[t];
-  d.pad[0] = d.pad[1] = 0;
-  d.res_delta = d.res_q - d.res_local;  // upward residue row = res_delta + node.res (body-relative)
-  out[big_scan[t]] = d;
-  const ChunkDesc &c = chunks[chunk_of_tile[t]];
-  reinterpret_cast<TileDesc *>(blob + c.blob_off + sizeof(ChunkDesc))[big_scan[t] - c.tile_begin] = d;
 }
 
 __global__ void k_top_fill(LayoutCtx c, int64_t NN, const int32_t *is_top, const int32_t *top_scan,
@@ -1208,8 +933,7 @@ __global__ void k_dup_query(DupCtx c, int64_t N) {
 int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
-                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &chunks, &tiles,
-                        &blob, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
+                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
                         &res_base_d, &wave_desc, &wave_stream_first, &wave_blob};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
@@ -1248,7 +972,6 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     throw Error(RQ_ERR_VALUE, "max_depth must be in [1, 128 - ceil(log2 m)]");
   if (const char *e = getenv("RQ_TILE_LEAVES")) p.tile_leaves = std::min(1024, std::max(2, atoi(e)));
   if (const char *e = getenv("RQ_TILE_HEIGHT")) p.tile_height = std::max(0, atoi(e));
-  if (const char *e = getenv("RQ_CHUNK_THREADS")) p.chunk_threads = atoi(e);
   if (const char *e = getenv("RQ_MRHS_MIN")) p.mrhs_min = std::max(2, atoi(e));
   if (const char *e = getenv("RQ_MRHS_TILE")) p.mrhs_tile = std::max(2, std::min(4096, atoi(e)));
   p.m = m;
@@ -1515,17 +1238,12 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                                              MaxOp{}, NN, s));
     }
     tm.mark("tiles");
-    // Chunks sweep their tiles level by level, so a chunk costs as many level steps as its
-    // tallest tile.  Ordering each body's tiles by height (stable radix sort on
-    // (body, height); tiles are in global postorder = body order) packs tiles of equal
-    // height together and cuts the nearly empty upper steps.  RQ_TILE_SORT=0 keeps
-    // postorder, =2 sorts by descending height.
-    std::vector<int64_t> body_tile_begin(m + 1, 0);
-    DBuf d_big_scan;
-    d_big_scan.alloc((n_tiles_all + 1) * 4);
+    // Tiles in body order; inside a body optionally ordered by height (stable radix sort on
+    // (body, height), RQ_TILE_SORT=1; =2 descending).  The wave placement fills the steps
+    // either way; the default keeps postorder.
     {
       const char *es = getenv("RQ_TILE_SORT");
-      const int mode = es ? atoi(es) : 1;
+      const int mode = es ? atoi(es) : 0;
       if (mode != 0 && n_tiles_all > 1) {
         DBuf tkey, tval, tkey2, tval2, sorted, inv;
         tkey.alloc(n_tiles_all * 8);
@@ -1551,190 +1269,13 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         RQ_CUDA(cudaMemcpyAsync(tiles_tmp.p, sorted.p, n_tiles_all * sizeof(TileTmp), cudaMemcpyDeviceToDevice, s));
         k_remap_tiles<<<nblk(NN), NT, 0, s>>>(tile_of.as<int32_t>(), NN, inv.as<int32_t>());
       }
-      // big-tile prefix (tile -> TileDesc index) and per-body tile ranges
-      DBuf bigf, btb;
-      bigf.alloc(std::max<int64_t>(n_tiles_all, 1) * 4);
-      btb.alloc((m + 1) * 8);
-      RQ_CUDA(cudaMemsetAsync(btb.p, 0xff, (m + 1) * 8, s));
-      k_tile_flags<<<nblk(std::max<int64_t>(n_tiles_all, 1)), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
-                                                                         bigf.as<int32_t>(), btb.as<int64_t>());
-      if (n_tiles_all) exclusive_scan(bigf.as<int32_t>(), d_big_scan.as<int32_t>(), n_tiles_all, s);
-      int32_t last[2] = {0, 0};
-      if (n_tiles_all) {
-        d2h(&last[0], d_big_scan.as<int32_t>() + n_tiles_all - 1, 1, s);
-        d2h(&last[1], bigf.as<int32_t>() + n_tiles_all - 1, 1, s);
-      }
-      p.n_tiles = (int64_t)last[0] + last[1];
-      RQ_CUDA(cudaMemcpyAsync(d_big_scan.as<int32_t>() + n_tiles_all, &p.n_tiles, 4, cudaMemcpyHostToDevice, s));
-      d2h(body_tile_begin.data(), btb.p, m + 1, s);
-      body_tile_begin[m] = n_tiles_all;
-      for (int64_t j = m - 1; j >= 0; j--)  // bodies without tiles start where the next one does
-        if (body_tile_begin[j] < 0) body_tile_begin[j] = body_tile_begin[j + 1];
+      DBuf cb;
+      cb.alloc(8);
+      RQ_CUDA(cudaMemsetAsync(cb.p, 0, 8, s));
+      if (n_tiles_all) k_count_big<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all, cb.as<unsigned long long>());
+      p.n_tiles = (int64_t)d2h1<unsigned long long>(cb.p, s);
     }
 
-    ChunkLimits lim;
-    lim.max_bytes = 40 * 1024;
-    if (const char *e = getenv("RQ_CHUNK_BYTES")) lim.max_bytes = std::max(8 * 1024, atoi(e));
-    // a single worst-case tile (all GENERAL nodes) must fit a chunk
-    lim.max_bytes = std::max<int64_t>(lim.max_bytes, blob_bytes_of(S - 1, S - 1, S, rec_size(GENERAL) * (S - 1), 1));
-    // With height-sorted tiles a chunk can collect many small tiles; capping beads and
-    // tiles per chunk bounds the largest staging buffers (they size every CTA's shared
-    // memory) so four chunk CTAs stay resident per SM (cfg2: 56.7 KB; 18 tiles / 7S beads
-    // measured best on configs 2 and 4, 20 / 8S drops to 3 CTAs/SM).
-    lim.max_nodes = 1024;
-    lim.max_beads = 7 * S;
-    lim.max_res = 3 * 1024;
-    lim.max_tiles = 18;
-    lim.max_lrec = 1280;  // 10 KB level-record stages
-    if (const char *e = getenv("RQ_CHUNK_MAX_LREC")) lim.max_lrec = std::max(64, atoi(e));
-    lim.max_lrec = std::max(lim.max_lrec, rec_size(GENERAL) * S / 2);  // any single tile fits
-    if (const char *e = getenv("RQ_CHUNK_MAX_TILES")) lim.max_tiles = std::max(1, std::min(64, atoi(e)));
-    if (const char *e = getenv("RQ_CHUNK_MAX_BEADS")) lim.max_beads = std::max(S, std::min(1024, atoi(e)));
-    if (const char *e = getenv("RQ_CHUNK_MAX_NODES")) lim.max_nodes = std::max(S, std::min(1024, atoi(e)));
-    std::vector<int64_t> seg_tile_begin;
-    std::vector<int32_t> seg_body;
-    for (int64_t j = 0; j < m; j++)
-      for (int64_t t = body_tile_begin[j]; t < body_tile_begin[j + 1]; t += PACK_SEG) {
-        seg_tile_begin.push_back(t);
-        seg_body.push_back((int32_t)j);
-      }
-    const int64_t nseg = (int64_t)seg_body.size();
-    seg_tile_begin.push_back(n_tiles_all);
-    DBuf d_seg_tb, d_seg_body;
-    d_seg_tb.alloc((nseg + 1) * 8);
-    d_seg_body.alloc(std::max<int64_t>(nseg, 1) * 4);
-    RQ_CUDA(cudaMemcpyAsync(d_seg_tb.p, seg_tile_begin.data(), (nseg + 1) * 8, cudaMemcpyHostToDevice, s));
-    if (nseg) RQ_CUDA(cudaMemcpyAsync(d_seg_body.p, seg_body.data(), nseg * 4, cudaMemcpyHostToDevice, s));
-    DBuf nch_seg, chunk_base;
-    nch_seg.alloc(std::max<int64_t>(nseg, 1) * 8);
-    chunk_base.alloc((nseg + 1) * 8);
-    DBuf chunk_of_tile, res_local_of_tile, bead_local_of_tile;
-    chunk_of_tile.alloc(n_tiles_all * 8);
-    res_local_of_tile.alloc(n_tiles_all * 4);
-    bead_local_of_tile.alloc(n_tiles_all * 4);
-    p.n_chunks = 0;
-    if (nseg) {
-      k_pack<<<nblk(nseg, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_seg_tb.as<int64_t>(), d_seg_body.as<int32_t>(),
-                                              boff, nseg, lim, 0, nullptr, d_big_scan.as<int32_t>(),
-                                              nch_seg.as<int64_t>(), nullptr, nullptr, nullptr, nullptr);
-      exclusive_scan(nch_seg.as<int64_t>(), chunk_base.as<int64_t>(), nseg, s);
-      p.n_chunks = d2h1<int64_t>(chunk_base.as<int64_t>() + nseg - 1, s) + d2h1<int64_t>(nch_seg.as<int64_t>() + nseg - 1, s);
-    }
-    RQ_CUDA(cudaMemcpyAsync(chunk_base.as<int64_t>() + nseg, &p.n_chunks, 8, cudaMemcpyHostToDevice, s));
-    p.chunks.alloc(std::max<int64_t>(p.n_chunks, 1) * sizeof(ChunkDesc));
-    if (nseg)
-      k_pack<<<nblk(nseg, 128), 128, 0, s>>>(tiles_tmp.as<TileTmp>(), d_seg_tb.as<int64_t>(), d_seg_body.as<int32_t>(),
-                                              boff, nseg, lim, 1, chunk_base.as<int64_t>(), d_big_scan.as<int32_t>(),
-                                              nch_seg.as<int64_t>(), p.chunks.as<ChunkDesc>(),
-                                              chunk_of_tile.as<int64_t>(), res_local_of_tile.as<int32_t>(),
-                                              bead_local_of_tile.as<int32_t>());
-    const int64_t nc = p.n_chunks;
-    tm.mark("pack");
-    DBuf cbytes, cnodes, clevels, bytes_scan, node_scan, lvl_base;
-    cbytes.alloc(nc * 8);
-    cnodes.alloc(nc * 8);
-    clevels.alloc(nc * 8);
-    bytes_scan.alloc((nc + 1) * 8);
-    node_scan.alloc((nc + 1) * 8);
-    lvl_base.alloc((nc + 1) * 8);
-    k_chunk_sizes<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, cbytes.as<int64_t>(),
-                                           cnodes.as<int64_t>(), clevels.as<int64_t>());
-    exclusive_scan(cbytes.as<int64_t>(), bytes_scan.as<int64_t>(), nc, s);
-    exclusive_scan(cnodes.as<int64_t>(), node_scan.as<int64_t>(), nc, s);
-    exclusive_scan(clevels.as<int64_t>(), lvl_base.as<int64_t>(), nc, s);
-    k_chunk_offsets<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, bytes_scan.as<int64_t>());
-    {
-      std::vector<ChunkDesc> hc(nc);
-      if (nc) d2h(hc.data(), p.chunks.p, nc, s);
-      p.blob_bytes = nc ? hc[nc - 1].blob_off + hc[nc - 1].blob_bytes : 0;
-      int64_t n_part = 0, n_lvl = 0;
-      p.max_blob = p.max_chunk_nodes = p.max_chunk_beads = p.max_chunk_levels = p.max_chunk_res = p.max_chunk_tiles = 0;
-      p.max_head_bytes = 0;
-      for (auto &d : hc) {
-        n_part += d.n_nodes;
-        n_lvl += d.n_levels;
-        p.max_blob = std::max<int64_t>(p.max_blob, d.blob_bytes);
-        p.max_chunk_nodes = std::max(p.max_chunk_nodes, d.n_nodes);
-        p.max_chunk_beads = std::max(p.max_chunk_beads, d.n_beads);
-        p.max_chunk_levels = std::max(p.max_chunk_levels, d.n_levels);
-        p.max_chunk_res = std::max(p.max_chunk_res, d.n_res);
-        p.max_chunk_tiles = std::max(p.max_chunk_tiles, d.n_tiles);
-        p.max_head_bytes = std::max<int64_t>(p.max_head_bytes, d.off_rec);
-      }
-      if (getenv("RQ_VERBOSE"))
-        fprintf(stderr, "[rq] chunks: %lld, level steps %lld (mean %.2f), tiles %lld, blob %.1f MB\n", (long long)nc,
-                (long long)n_lvl, nc ? (double)n_lvl / nc : 0.0, (long long)p.n_tiles, p.blob_bytes / 1e6);
-      p.h_chunk_first.assign(m + 1, nc);
-      for (int64_t c = nc - 1; c >= 0; c--) p.h_chunk_first[hc[c].body] = c;
-      for (int64_t j = m - 1; j >= 0; j--) p.h_chunk_first[j] = std::min(p.h_chunk_first[j], p.h_chunk_first[j + 1]);
-      p.blob.alloc(p.blob_bytes);
-      RQ_CUDA(cudaMemsetAsync(p.blob.p, 0, p.blob_bytes, s));
-      DBuf lvl;
-      lvl.alloc(std::max<int64_t>(n_lvl, 1) * sizeof(LevelDesc));
-      RQ_CUDA(cudaMemsetAsync(lvl.p, 0, std::max<int64_t>(n_lvl, 1) * sizeof(LevelDesc), s));
-
-      // level-major node order inside chunks
-      DBuf nkeys, nvals, nkeys2, nvals2, slot_of;
-      nkeys.alloc(NN * 8);
-      nvals.alloc(NN * 4);
-      nkeys2.alloc(NN * 8);
-      nvals2.alloc(NN * 4);
-      slot_of.alloc(NN * 4);
-      RQ_CUDA(cudaMemsetAsync(slot_of.p, 0xff, NN * 4, s));
-      k_node_keys<<<nblk(NN), NT, 0, s>>>(lc, NN, is_top.as<int32_t>(), tile_of.as<int32_t>(),
-                                           chunk_of_tile.as<int64_t>(), nkeys.as<uint64_t>(),
-                                           nvals.as<int32_t>());
-      size_t tb = 0;
-      RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, nkeys.as<uint64_t>(), nkeys2.as<uint64_t>(),
-                                              nvals.as<int32_t>(), nvals2.as<int32_t>(), (int)NN, 0, 64, s));
-      DBuf tmp;
-      tmp.alloc(tb);
-      RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, nkeys.as<uint64_t>(), nkeys2.as<uint64_t>(),
-                                              nvals.as<int32_t>(), nvals2.as<int32_t>(), (int)NN, 0, 64, s));
-      tmp.reset();
-      tm.mark("node sort");
-      if (n_part > 0)
-        k_slots<<<nblk(n_part), NT, 0, s>>>(nkeys2.as<uint64_t>(), nvals2.as<int32_t>(), n_part,
-                                             node_scan.as<int64_t>(), slot_of.as<int32_t>(),
-                                             lvl_base.as<int64_t>(), lvl.as<LevelDesc>(), p.flags.as<uint8_t>());
-      DBuf d_max_lrec;
-      d_max_lrec.alloc(8);
-      RQ_CUDA(cudaMemsetAsync(d_max_lrec.p, 0, 8, s));
-      k_levels_finalize<<<nblk(nc), NT, 0, s>>>(p.chunks.as<ChunkDesc>(), nc, lvl_base.as<int64_t>(),
-                                                 lvl.as<LevelDesc>(), p.blob.as<uint8_t>(),
-                                                 d_max_lrec.as<unsigned long long>());
-      p.max_level_rec_bytes = (int64_t)d2h1<unsigned long long>(d_max_lrec.p, s);
-      WriteCtx wc{lc,
-                  nkeys2.as<uint64_t>(),
-                  nvals2.as<int32_t>(),
-                  slot_of.as<int32_t>(),
-                  tile_of.as<int32_t>(),
-                  p.left.as<int32_t>(),
-                  p.right.as<int32_t>(),
-                  tiles_tmp.as<TileTmp>(),
-                  res_local_of_tile.as<int32_t>(),
-                  bead_local_of_tile.as<int32_t>(),
-                  p.chunks.as<ChunkDesc>(),
-                  lvl_base.as<int64_t>(),
-                  lvl.as<LevelDesc>(),
-                  p.rec.as<double>(),
-                  p.blob.as<uint8_t>(),
-                  d_big_scan.as<int32_t>()};
-      if (n_part > 0) k_write_nodes<<<nblk(n_part), NT, 0, s>>>(wc, n_part);
-      if (n_tiles_all)
-        k_write_perm<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all, chunk_of_tile.as<int64_t>(),
-                                                       bead_local_of_tile.as<int32_t>(), p.chunks.as<ChunkDesc>(),
-                                                       p.perm.as<int32_t>(), boff, p.blob.as<uint8_t>());
-      p.tiles.alloc(std::max<int64_t>(p.n_tiles, 1) * sizeof(TileDesc));
-      k_tile_desc<<<nblk(n_tiles_all), NT, 0, s>>>(tiles_tmp.as<TileTmp>(), n_tiles_all,
-                                                    d_big_scan.as<int32_t>(), slot_of.as<int32_t>(),
-                                                    slot_scan.as<int32_t>(), res_local_of_tile.as<int32_t>(),
-                                                    p.parent.as<int32_t>(), p.tiles.as<TileDesc>(),
-                                                    chunk_of_tile.as<int64_t>(), p.chunks.as<ChunkDesc>(),
-                                                    p.blob.as<uint8_t>());
-    }
-
-    tm.mark("chunks+blob");
     // wavefront streams over the same tiles
     {
       DBuf troots;

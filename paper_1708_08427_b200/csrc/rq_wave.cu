@@ -111,7 +111,8 @@ __global__ void k_wv_profile(const int64_t *tile_root, int64_t nt, NodeArrays A,
     else v.b++;
     v.beads += wv_beads(cs);
     const int root = q == g;
-    v.vd += res_rows(cs) + 6 * root;
+    const int rr = res_rows(cs);
+    v.vd += (rr ? 2 * wv_pieces(A.res_base[A.node_body[q]] + A.res_off[q] - 6, rr) : 0) + 6 * root;
     v.dg += (res_rows(cs) > 0) + root;
     v.rm += 8 * rec_size(cs) + 16;
   }
@@ -205,19 +206,34 @@ __global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, co
   (void)stream_of_tile_first;
 }
 
-__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int32_t *tile_stream) {
+__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int64_t nseg,
+                                 int32_t *tile_stream, int32_t *tile_seg, const int64_t *tile_root,
+                                 const int32_t *node_body, int *seg_minb, int *seg_maxb, const int64_t *tnodes) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < nt) tile_stream[order[i]] = (int32_t)(key[i] / R);
+  if (i >= nt) return;
+  const int64_t t = order[i];
+  const int64_t r = (int64_t)(key[i] % R);
+  const int e = (int)(r * nseg / R);
+  tile_stream[t] = (int32_t)(key[i] / R);
+  tile_seg[t] = e;
+  if (tnodes[t]) {  // body range of each segment (host-buffer pieces)
+    const int j = node_body[tile_root[t]];
+    atomicMin(&seg_minb[e], j);
+    atomicMax(&seg_maxb[e], j);
+  }
 }
 
 struct StepCnt {
   int32_t g, r, b, ug, dg;
+  int32_t ugseg, dgseg, updone, dndone;  // see StepDesc
 };
 
 // per sorted node: step counts, list counts, step of the node, per-node list sizes
 __global__ void k_wv_count(const uint64_t *keys, const int32_t *vals, int64_t n, NodeArrays A, StepCnt *sc,
                            int64_t *step_of, int64_t *sfirst_sorted, int32_t *nb, int32_t *vd, int32_t *nd,
-                           const int32_t *node_tile, const int64_t *tile_root) {
+                           const int32_t *node_tile, const int64_t *tile_root, const int32_t *tile_stream,
+                           const int32_t *tile_seg, int nseg, unsigned long long *seg_last,
+                           unsigned long long *seg_first) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int64_t gs = (int64_t)(keys[p] >> 2);
@@ -228,13 +244,45 @@ __global__ void k_wv_count(const uint64_t *keys, const int32_t *vals, int64_t n,
   else atomicAdd(&sc[gs].b, 1);
   const int root = tile_root[node_tile[g]] == g;
   const int beads = wv_beads(cs), dge = (res_rows(cs) > 0) + root;
-  if (beads) atomicAdd(&sc[gs - 2].ug, beads);
-  if (dge) atomicAdd(&sc[gs + 2].dg, dge);
+  const int32_t t = node_tile[g];
+  const int e = tile_seg[t];
+  if (beads) { atomicAdd(&sc[gs - 2].ug, beads); atomicMax(&sc[gs - 2].ugseg, e); }
+  if (dge) { atomicAdd(&sc[gs + 2].dg, dge); atomicMin(&sc[gs + 2].dgseg, e); }
+  const int64_t ce = (int64_t)tile_stream[t] * nseg + e;
+  atomicMax(&seg_last[ce], (unsigned long long)gs);
+  atomicMin(&seg_first[ce], (unsigned long long)gs);
   step_of[g] = gs;
   if (p == 0 || (int64_t)(keys[p - 1] >> 2) != gs) sfirst_sorted[gs] = p;
   nb[p] = beads;
-  vd[p] = res_rows(cs) + 6 * root;
+  const int rr = res_rows(cs);
+  vd[p] = (rr ? 2 * wv_pieces(A.res_base[A.node_body[g]] + A.res_off[g] - 6, rr) : 0) + 6 * root;
   nd[p] = dge;
+}
+
+// per stream: the step after which each host segment has no node left (upward order:
+// cumulative max of the segments' last steps; downward: cumulative min from the top)
+__global__ void k_wv_markers(const int64_t *step_first, int64_t G, int nseg, const unsigned long long *seg_last,
+                             const unsigned long long *seg_first, StepCnt *sc) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= G) return;
+  const int64_t s0 = step_first[c], s1 = step_first[c + 1];
+  int64_t cm = s0;
+  for (int e = 0; e < nseg; e++) {
+    const unsigned long long l = seg_last[c * nseg + e];
+    if (l != 0ull) cm = max(cm, (int64_t)l);
+    atomicMax(&sc[cm].updone, e + 1);
+  }
+  int64_t cn = s1 - 1;
+  for (int e = nseg - 1; e >= 0; e--) {
+    const unsigned long long f = seg_first[c * nseg + e];
+    if (f != ~0ull) cn = min(cn, (int64_t)f);
+    atomicMax(&sc[cn].dndone, nseg - e);
+  }
+}
+
+__global__ void k_wv_init_cnt(StepCnt *sc, int64_t ns) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < ns) sc[s].dgseg = 0x7fffffff;
 }
 
 __global__ void k_wv_step_bytes(const StepCnt *sc, int64_t ns, int64_t *bytes, unsigned long long *mx) {
@@ -253,8 +301,12 @@ __global__ void k_wv_descs(const StepCnt *sc, const int64_t *off, int64_t ns, St
   const StepCnt c = sc[s];
   StepDesc D;
   D.off16 = (uint32_t)(off[s] >> 4);
-  D.nG = (uint16_t)c.g; D.nR = (uint16_t)c.r; D.nB = (uint16_t)c.b;
+  D.nG = (uint8_t)c.g; D.nR = (uint8_t)c.r; D.nB = (uint8_t)c.b;
   D.n_ug = (uint16_t)c.ug; D.n_dg = (uint16_t)c.dg;
+  D.ug_seg = (uint8_t)c.ugseg;
+  D.dg_seg = (uint8_t)(c.dg ? c.dgseg : 0);
+  D.up_done = (uint8_t)c.updone;
+  D.dn_done = (uint8_t)c.dndone;
   D.pad = 0;
   d[s] = D;
   const WaveSec S = wave_sections(D);
@@ -394,11 +446,13 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
   dm.pad = 0;
   um.row = 0;
   um.aux = 0;
+  // a bead's 3 doubles: window of 4 at 4 * position, offset (bead & 1)
+  auto boff = [&](int id, int k) -> uint16_t { return (uint16_t)(4 * (bpos + k) + (orig_bead(id) & 1u)); };
   if (cs == BEAD_BEAD) {
-    um.x = (uint16_t)bpos; um.y = (uint16_t)(bpos + 1);
+    um.x = boff(xi, 0); um.y = boff(yi, 1);
     dm.x = orig_bead(xi); dm.y = orig_bead(yi);
   } else if (cs == RIGID_BEAD) {
-    um.x = (uint16_t)w.slot_of[nb0 + xi]; um.y = (uint16_t)bpos;
+    um.x = (uint16_t)w.slot_of[nb0 + xi]; um.y = boff(yi, 0);
     dm.x = (uint32_t)w.slot_of[nb0 + xi]; dm.y = orig_bead(yi);
   } else {
     um.x = (uint16_t)w.slot_of[nb0 + xi]; um.y = (uint16_t)w.slot_of[nb0 + yi];
@@ -406,11 +460,12 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
   }
   const int rr = res_rows(cs);
   const int64_t row = A.res_base[j] + A.res_off[g] - 6;
+  const int rwin = rr ? 2 * wv_pieces(row, rr) : 0;  // residue window (doubles, even)
   if (rr) um.row = (uint32_t)row;
-  dm.vres = (uint16_t)vpos;
+  dm.vres = (uint16_t)(vpos + (row & 1));
   if (troot) {
     um.aux = broot ? (uint32_t)j : (uint32_t)A.slot_scan[g];
-    dm.self = (uint16_t)(vpos + rr);
+    dm.self = (uint16_t)(vpos + rwin);
   } else {
     um.self = (uint16_t)w.slot_of[g];
     dm.self = (uint16_t)w.slot_of[g];
@@ -440,7 +495,7 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
     if (troot) {
       WaveGather e;
       e.src = broot ? (uint32_t)j : (uint32_t)A.slot_scan[g];
-      e.dst = (uint16_t)(vpos + rr);
+      e.dst = (uint16_t)(vpos + rwin);
       e.kind = broot ? WG_ROOT : WG_SLOT;
       DG[di++] = e;
     }
@@ -463,7 +518,6 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   }
   p.wave_caps = caps;
   if (const char *e = getenv("RQ_WAVE_PF")) p.wave_pf = std::max(0, std::min(32, atoi(e)));
-  if (const char *e = getenv("RQ_WAVE_STAGES")) p.wave_nst = std::max(2, std::min(4, atoi(e)));
   NodeArrays A{in.node_off, in.bead_off, in.rec_off, in.res_base, in.node_body, in.start, in.stop, in.left,
                in.right,    in.parent,   in.height,  in.res_off,  in.perm,      in.slot_scan, in.flags};
   const int64_t NN = p.NN;
@@ -535,7 +589,27 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
       if (h[c] < 0) h[c] = h[c + 1];
     RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
   }
-  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, tile_stream.as<int32_t>());
+  // host segments: groups of rounds
+  int64_t nseg = std::min<int64_t>(R, 32);
+  if (const char *e = getenv("RQ_WAVE_SEGS")) nseg = std::max<int64_t>(1, std::min<int64_t>(R, std::min(255, atoi(e))));
+  p.wave_nseg = (int)nseg;
+  DBuf tile_seg, segb;
+  tile_seg.alloc(nt * 4);
+  segb.alloc(nseg * 8);
+  {
+    std::vector<int> init(2 * nseg);
+    for (int64_t e = 0; e < nseg; e++) { init[e] = INT32_MAX; init[nseg + e] = -1; }
+    RQ_CUDA(cudaMemcpyAsync(segb.p, init.data(), nseg * 8, cudaMemcpyHostToDevice, s));
+  }
+  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, nseg,
+                                            tile_stream.as<int32_t>(), tile_seg.as<int32_t>(), in.tile_root,
+                                            in.node_body, segb.as<int>(), segb.as<int>() + nseg, tnodes.as<int64_t>());
+  {
+    std::vector<int> h(2 * nseg);
+    d2h(h.data(), segb.p, 2 * nseg, s);
+    p.wave_seg_minb.assign(h.begin(), h.begin() + nseg);
+    p.wave_seg_maxb.assign(h.begin() + nseg, h.end());
+  }
   k_wv_gather64<<<nblk(nt), NT, 0, s>>>(theight.as<int64_t>(), order.as<int32_t>(), nt, th_sorted.as<int64_t>());
   k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
   ex_scan(th_sorted.as<int64_t>(), lv_scan.as<int64_t>(), nt, s);
@@ -584,6 +658,12 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   DBuf sc, step_of, sfs, nb, vd, nd, bscan, vscan, dscan;
   sc.alloc(NS * sizeof(StepCnt));
   RQ_CUDA(cudaMemsetAsync(sc.p, 0, NS * sizeof(StepCnt), s));
+  k_wv_init_cnt<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), NS);
+  DBuf seg_last, seg_first;
+  seg_last.alloc(G * nseg * 8);
+  seg_first.alloc(G * nseg * 8);
+  RQ_CUDA(cudaMemsetAsync(seg_last.p, 0, G * nseg * 8, s));
+  RQ_CUDA(cudaMemsetAsync(seg_first.p, 0xff, G * nseg * 8, s));
   step_of.alloc(NN * 8);
   sfs.alloc(NS * 8);
   RQ_CUDA(cudaMemsetAsync(sfs.p, 0, NS * 8, s));
@@ -595,7 +675,11 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   dscan.alloc(n * 8);
   k_wv_count<<<nblk(n), NT, 0, s>>>(keys2.as<uint64_t>(), vals2.as<int32_t>(), n, A, sc.as<StepCnt>(),
                                      step_of.as<int64_t>(), sfs.as<int64_t>(), nb.as<int32_t>(), vd.as<int32_t>(),
-                                     nd.as<int32_t>(), node_tile.as<int32_t>(), in.tile_root);
+                                     nd.as<int32_t>(), node_tile.as<int32_t>(), in.tile_root, tile_stream.as<int32_t>(),
+                                     tile_seg.as<int32_t>(), (int)nseg, seg_last.as<unsigned long long>(),
+                                     seg_first.as<unsigned long long>());
+  k_wv_markers<<<nblk(G, 64), 64, 0, s>>>(step_first.as<int64_t>(), G, (int)nseg, seg_last.as<unsigned long long>(),
+                                           seg_first.as<unsigned long long>(), sc.as<StepCnt>());
   ex_scan(nb.as<int32_t>(), bscan.as<int64_t>(), n, s);
   ex_scan(vd.as<int32_t>(), vscan.as<int64_t>(), n, s);
   ex_scan(nd.as<int32_t>(), dscan.as<int64_t>(), n, s);
@@ -728,6 +812,14 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *q) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(q) : "memory");
+  return v;
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -766,13 +858,13 @@ __device__ __forceinline__ void wv_up(const double *rec, const WaveUpMeta *UMp, 
   const WaveUpMeta md = *UMp;
   double mx[6], my[6];
   if (CS == BEAD_BEAD) {
-    const double *f = V + 3 * md.x;
+    const double *f = V + md.x;
     mx[0] = f[0]; mx[1] = f[1]; mx[2] = f[2]; mx[3] = 0.0; mx[4] = 0.0; mx[5] = 0.0;
   } else {
     ld6(M + 6 * md.x, mx);
   }
   if (CS != GENERAL) {
-    const double *f = V + 3 * md.y;
+    const double *f = V + md.y;
     my[0] = f[0]; my[1] = f[1]; my[2] = f[2]; my[3] = 0.0; my[4] = 0.0; my[5] = 0.0;
   } else {
     ld6(M + 6 * md.y, my);
@@ -838,8 +930,16 @@ struct WaveCtx {
   double *out;
   double *scratch;
   double *roots;
-  uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: 2 stages | M | 3 gather regions (vreg doubles each)
+  uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: NST stages | M | 3 gather regions (vreg doubles each)
   int pf;                                // L2 prefetch distance (steps)
+  int64_t in_len;                        // doubles in `in` (16-byte windows never read past it)
+  // host-buffer pipelining (nullptr: inputs resident): a block's gathers wait until the copy
+  // engine has flagged their segment (flags[e] >= epoch); after the last step holding nodes
+  // of a segment every CTA bumps counters[e] (the D2H of that segment waits for G bumps)
+  const uint32_t *flags;
+  uint32_t *counters;
+  uint32_t epoch;
+  int nseg;
 };
 
 #ifndef RQ_WAVE_MIN_BLOCKS
@@ -886,6 +986,8 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
   __syncthreads();
   pdl_wait();  // vectors and exchange slots may come from the previous kernel
   unsigned phase = 0;
+  int seg_ok = UP ? -1 : 1 << 30;  // host segments known to have arrived
+  int done = 0;                    // host segments this CTA has counted as done
   int st = 0;
   for (int t = 0; t < n; t++, st = (st == NST - 1) ? 0 : st + 1) {
     mbar_wait(bar_u + 8 * st, (phase >> st) & 1u);
@@ -893,18 +995,35 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     const unsigned char *B = smem + st * a.stage_bytes;
     const StepDesc d = *reinterpret_cast<const StepDesc *>(B);
     const WaveSec S = wave_sections(d);
-    // gathers for step t + 2 (into region (t + 2) % 3)
+    // host-buffer path: the rows this block's gathers read must have arrived
+    if (a.flags) {
+      const int need = UP ? d.ug_seg : d.dg_seg;
+      if (UP ? need > seg_ok : need < seg_ok) {
+        if (tid == 0)
+          while ((int32_t)(ld_acquire(a.flags + need) - a.epoch) < 0) __nanosleep(256);
+        __syncthreads();
+        seg_ok = need;
+      }
+    }
+    // gathers for step t + 2 (into region (t + 2) % 3): 16-byte L2 copies (cp.async.cg)
     {
       const int rg = (t + 2) % 3;
       const uint32_t vg = vb_u + 8u * (uint32_t)(rg * a.vreg);
       if (UP) {
         const uint32_t *ug = reinterpret_cast<const uint32_t *>(B + (S.ug - S.uhdr));
         for (int i = tid; i < d.n_ug; i += 128) {
-          const double *src = a.in + 3 * (int64_t)ug[i];
-          const uint32_t dst = vg + 24u * (uint32_t)i;
-          cp8(dst, src);
-          cp8(dst + 8, src + 1);
-          cp8(dst + 16, src + 2);
+          const int64_t b = ug[i];
+          const int64_t w0 = 3 * b - (b & 1);  // even: 16-byte aligned window of 4 doubles
+          const uint32_t dst = vg + 32u * (uint32_t)i;
+          if (w0 + 4 <= a.in_len) {
+            cp16(dst, a.in + w0);
+            cp16(dst + 16, a.in + w0 + 2);
+          } else {  // the vector's last bead: no read past the end
+            const uint32_t d1 = dst + 8u * (uint32_t)(b & 1);
+            cp8(d1, a.in + 3 * b);
+            cp8(d1 + 8, a.in + 3 * b + 1);
+            cp8(d1 + 16, a.in + 3 * b + 2);
+          }
         }
       } else {
         const WaveGather *dg = reinterpret_cast<const WaveGather *>(B + S.dg);
@@ -912,15 +1031,22 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           const WaveGather e = dg[i];
           const uint32_t dst = vg + 8u * e.dst;
           if (e.kind == WG_RES3 || e.kind == WG_RES6) {
-            const double *src = a.in + e.src;
-            const int c = e.kind == WG_RES3 ? 3 : 6;
-            for (int r = 0; r < c; r++) cp8(dst + 8 * r, src + r);
+            const int64_t row = e.src;
+            const int rr = e.kind == WG_RES3 ? 3 : 6;
+            const int np = wv_pieces(row, rr);
+            const int64_t w0 = row & ~(int64_t)1;
+            if (w0 + 2 * np <= a.in_len) {
+              for (int k = 0; k < np; k++) cp16(dst + 16u * k, a.in + w0 + 2 * k);
+            } else {
+              const uint32_t d1 = dst + 8u * (uint32_t)(row & 1);
+              for (int r = 0; r < rr; r++) cp8(d1 + 8u * r, a.in + row + r);
+            }
           } else if (e.kind == WG_SLOT) {
             const double *src = a.scratch + 6 * (int64_t)e.src;
-            for (int r = 0; r < 6; r++) cp8(dst + 8 * r, src + r);
+            for (int k = 0; k < 3; k++) cp16(dst + 16u * k, src + 2 * k);
           } else if (a.roots) {
             const double *src = a.roots + 6 * (int64_t)e.src;
-            for (int r = 0; r < 6; r++) cp8(dst + 8 * r, src + r);
+            for (int k = 0; k < 3; k++) cp16(dst + 16u * k, src + 2 * k);
           } else {
             double *z = Vb + rg * a.vreg + e.dst;
             for (int r = 0; r < 6; r++) z[r] = 0.0;  // Q~^T: zero root RV-set (matfree.py:167-168)
@@ -967,7 +1093,14 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       }
     }
     cp_wait<1>();  // this thread's gathers for step t + 1
+    const int done_now = a.counters ? (UP ? d.up_done : d.dn_done) : 0;
+    if (done_now > done) __threadfence();  // this step's outputs before the segment counters
     __syncthreads();
+    if (done_now > done) {
+      if (tid == 0)
+        for (int e = done; e < done_now; e++) atomicAdd(a.counters + (UP ? e : a.nseg - 1 - e), 1u);
+      done = done_now;
+    }
     if (tid == PROD && t + NST < n) {  // stage st is free: block t + NST
       uint32_t off, bytes;
       span(dn, off, bytes);
@@ -982,13 +1115,17 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       if (t + NST + 1 < n) dn = a.steps[blk(t + NST + 1)];
     }
   }
+  if (a.counters && tid == 0 && done < a.nseg) {
+    __threadfence();
+    for (int e = done; e < a.nseg; e++) atomicAdd(a.counters + (UP ? e : a.nseg - 1 - e), 1u);
+  }
 }
 
 }  // namespace
 
 size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg) {
   const uint32_t st = (uint32_t)p.wave_stage_bytes;
-  const uint32_t vr = (uint32_t)std::max(3 * p.wave_caps.beads, p.wave_caps.vd);
+  const uint32_t vr = (uint32_t)std::max(4 * p.wave_caps.beads, p.wave_caps.vd);
   const uint32_t om = (uint32_t)p.wave_nst * st;
   const uint32_t ov = om + (uint32_t)al128(48 * (size_t)p.wave_mslots);
   if (o_m) *o_m = om;
@@ -1000,18 +1137,19 @@ size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg) {
 void wave_prepare(const Plan &p) {
   if (p.wave_ready || !p.wave_streams) return;
   const size_t sm = wave_smem(p, nullptr, nullptr, nullptr);
-  for (const void *f : {(const void *)k_wave<true, 2>, (const void *)k_wave<false, 2>, (const void *)k_wave<true, 3>,
-                        (const void *)k_wave<false, 3>, (const void *)k_wave<true, 4>, (const void *)k_wave<false, 4>})
+  for (const void *f : {(const void *)k_wave<true, 2>, (const void *)k_wave<false, 2>})
     RQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   int occ = 0;
-  RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_wave<true, 3>, 128, sm));
+  RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_wave<true, 2>, 128, sm));
   p.wave_ctas_per_sm = occ;
   if (occ < 1) throw Error(RQ_ERR_CUDA, "wave kernel does not fit on an SM (smem " + std::to_string(sm) + ")");
   p.wave_ready = true;
 }
 
-void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s) {
+void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s,
+              const WaveSync *sync) {
   if (!p.wave_streams) return;
+  if (reinterpret_cast<uintptr_t>(in) & 15) throw Error(RQ_ERR_VALUE, "wave sweep input must be 16-byte aligned");
   wave_prepare(p);
   WaveCtx a{};
   a.steps = p.wave_desc.as<StepDesc>();
@@ -1024,6 +1162,13 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
   a.stage_bytes = (uint32_t)p.wave_stage_bytes;
   const size_t sm = wave_smem(p, &a.o_m, &a.o_v, &a.vreg);
   a.pf = p.wave_pf;
+  a.in_len = up ? 3 * p.N : p.res_base[p.m];
+  a.nseg = p.wave_nseg;
+  if (sync) {
+    a.flags = sync->flags;
+    a.counters = sync->counters;
+    a.epoch = sync->epoch;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.wave_streams);
   cfg.blockDim = dim3(128);
@@ -1034,14 +1179,8 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  switch (p.wave_nst * 2 + (up ? 1 : 0)) {
-    case 4: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 2>, a)); break;
-    case 5: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 2>, a)); break;
-    case 8: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 4>, a)); break;
-    case 9: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 4>, a)); break;
-    case 6: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 3>, a)); break;
-    default: RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 3>, a)); break;
-  }
+  if (up) RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<true, 2>, a));
+  else RQ_CUDA(cudaLaunchKernelEx(&cfg, k_wave<false, 2>, a));
 }
 
 }  // namespace rq

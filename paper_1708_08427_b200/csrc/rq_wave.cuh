@@ -36,13 +36,20 @@ namespace rq {
 
 struct StepDesc {     // 16 bytes (also the block header)
   uint32_t off16;     // block byte offset / 16 in the wave blob
-  uint16_t nG, nR, nB;
+  uint8_t nG, nR, nB;
+  uint8_t ug_seg;     // host segment the upward gathers of this block read (the latest one)
   uint16_t n_ug;      // upward gathers held by this block (beads of step s+2)
   uint16_t n_dg;      // downward gathers held by this block (nodes of step s-2)
-  uint16_t pad;
+  uint8_t dg_seg;     // host segment the downward gathers read (the earliest one)
+  uint8_t up_done;    // upward: segments [0, up_done) have no node left in this stream after this step
+  uint8_t dn_done;    // downward: segments [nseg - dn_done, nseg) done after this step
+  uint8_t pad;
 };
+// Host segments: the rounds are grouped into nseg <= 255 segments; the host-buffer path
+// copies a segment's vector rows in (flag per segment, written by the copy engine) and out
+// (per-segment counters of the CTAs that are done with it) while the sweep runs.
 
-// upward metadata: x, y = M slots (internal children) or bead positions in the
+// upward metadata: x, y = M slots (internal children) or bead offsets (doubles) in the
 // step's gather region (BEAD_BEAD: both, RIGID_BEAD: y); self = M slot of the
 // output; row = first residue row (private residue layout, see Plan::res_base);
 // aux = exchange slot (tile root) or body (body root)
@@ -60,9 +67,14 @@ struct WaveDnMeta {
 // downward gather entry
 struct WaveGather {
   uint32_t src;   // residue row / exchange slot / body
-  uint16_t dst;   // double offset in the gather region
+  uint16_t dst;   // double offset in the gather region (even: 16-byte copies)
   uint16_t kind;  // WG_*
 };
+// Gathers are 16-byte cp.async.cg copies (L2 only: rows that arrive while the sweep runs
+// are never served stale from L1).  A bead's 3 doubles sit in a 4-double window starting
+// at the even row below 3b (offset b & 1); a residue run [row, row + rr) in the window
+// [row & ~1, ...) of wv_pieces(row, rr) 16-byte pieces (offset row & 1).
+__host__ __device__ inline int wv_pieces(int64_t row, int rr) { return (int)(((row & 1) + rr + 1) >> 1); }
 enum : uint16_t { WG_RES3 = 0, WG_RES6 = 1, WG_SLOT = 2, WG_ROOT = 3 };
 // meta flag bits above the node flags (bits 0-5: case | swapped | signs)
 constexpr uint16_t WF_TILE_ROOT = 1u << 6;  // output to / input from an exchange slot
@@ -98,7 +110,7 @@ struct WaveCaps {
   int g = 32, r = 32, b = 64;   // nodes per case
   int rm = 10240;               // record + one-direction metadata bytes
   int beads = 128;              // upward gathers (beads) per step
-  int vd = 384;                 // downward gathered doubles per step
+  int vd = 512;                 // downward gather-region doubles per step
   int dg = 96;                  // downward gather entries per step
 };
 

@@ -102,7 +102,10 @@ class ShardedMultiBodyOperator:
         self.rank, self.world = rank, world
         self.bounds = shard_bounds(self.offsets, world)
         pos, off, (self.j0, self.j1) = shard_of(positions, self.offsets, rank, world)
-        self.local = MultiBodyOperator(MultiBodyModel.from_arrays(pos, off), max_depth=max_depth)
+        # more ranks than bodies (or one body dominating) leaves a shard empty: it applies
+        # nothing and contributes zero rows to the gather
+        self.local = (MultiBodyOperator(MultiBodyModel.from_arrays(pos, off), max_depth=max_depth)
+                      if self.j1 > self.j0 else None)
 
     def _kinds(self, op):
         return {"qv": ("full", "full"), "qtv": ("full", "full"), "qtilde_v": ("full", "comp"),
@@ -113,6 +116,10 @@ class ShardedMultiBodyOperator:
         return a, b
 
     def apply(self, op: str, v_local):
+        if self.local is None:
+            if op not in ("qv", "qtv", "qtilde_v", "qtilde_tv"):
+                raise ValueError("op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')")
+            return v_local[:0]
         return self.local.apply(op, v_local)
 
     def apply_global(self, op: str, v):

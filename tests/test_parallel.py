@@ -101,3 +101,64 @@ def test_bench_strong_sharding_covers_the_model():
         beads = [int(p[1][-1]) for p in parts]
         # each cut lies within half a body of its ideal position: shard sizes differ by <= 2 bodies
         assert max(beads) - min(beads) <= 2 * int(np.diff(off).max())
+
+
+def _oracle_worker(rank, world, port, pos, off, v, result):
+    """Each rank applies Q~ to its shard with the CPU oracle (the checker standing in for the
+    CUDA operator, which needs a GPU) and the shards are gathered: the sharding + gather path
+    with real operator outputs."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import OracleBatch
+
+        b = shard_bounds(off, world)
+        p_loc, o_loc, (j0, j1) = shard_of(pos, off, rank, world)
+        a, e = vector_slice(off, b, rank, "full")
+        if j1 > j0:
+            y = OracleBatch(p_loc, o_loc, threads=1).apply("qtilde_v", v[a:e])
+        else:
+            y = np.zeros(0)
+        rows = [vector_slice(off, b, r, "comp") for r in range(world)]
+        out = gather_shards(torch.from_numpy(np.ascontiguousarray(y)), [q - p for p, q in rows])
+        if rank == 0:
+            result.put(out.numpy().tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_operator_outputs_world_gloo(world):
+    from oracle.oracle import OracleBatch
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([300, 1200, 64] if world == 2 else [500, 700], seed=9)  # world 3: one empty shard
+    v = np.random.default_rng(3).normal(size=3 * int(off[-1]))
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_oracle_worker, args=(r, world, port, pos, off, v, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+        assert p.exitcode == 0
+    got = np.array(q.get())
+    want = OracleBatch(pos, off, threads=1).apply("qtilde_v", v)
+    np.testing.assert_array_equal(got, want)  # per-body arithmetic does not depend on the split
+
+
+def test_empty_shard_operator():
+    """world > m: the empty rank builds nothing and returns zero-row outputs (no GPU needed)."""
+    from paper_1708_08427_b200.parallel import ShardedMultiBodyOperator
+
+    pos = np.random.default_rng(0).normal(size=(10, 3))
+    off = np.array([0, 10])
+    b = shard_bounds(off, 2)
+    empty = 0 if b[1] == b[0] else 1
+    sh = ShardedMultiBodyOperator(pos, off, rank=empty, world=2)
+    assert sh.local is None and sh.j0 == sh.j1
+    assert sh.apply("qtilde_v", np.zeros(0)).shape == (0,)
+    assert sh.apply_global("qtilde_tv", np.zeros(30 - 6)).shape == (0,)
+    with pytest.raises(ValueError):
+        sh.apply("bad", np.zeros(0))
