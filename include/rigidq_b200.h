@@ -72,7 +72,6 @@ typedef struct rq_plan_info {
   int64_t n_case[4];       /* node counts per case (leaf, BB, RB, GEN) */
   int64_t device_bytes;    /* device memory held by the plan */
   int64_t rounds;          /* tile rounds (all streams work inside one round at a time) */
-  int64_t host_segments;   /* host-buffer pipeline segments (groups of rounds) */
   int64_t node_slots;      /* node 6-vector slots per sweep CTA (shared memory) */
   int64_t stage_bytes;     /* shared-memory stage of one step block */
   int64_t sweep_smem;      /* dynamic shared memory per sweep CTA */
@@ -132,8 +131,15 @@ int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int6
                 void *stream, uint32_t phases);
 /* Number of kernel launches one rq_apply issues. */
 int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k);
-/* Same on HOST buffers: H2D copy, apply, D2H copy (synchronous). */
+/* Same on HOST buffers (pinned or pageable): H2D copy, apply, D2H copy; returns when
+ * `out` holds the result (the numpy path of the reference API, matfree.py:86-92). */
 int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, int64_t k);
+/* Asynchronous form: returns once the copies and kernels are queued on the plan's own
+ * streams (two staging slots), so the H2D of the next application overlaps the D2H of
+ * this one.  `in` and `out` must stay valid until rq_host_wait (pageable results are
+ * delivered by it; a third application implicitly completes the first). */
+int rq_apply_host_async(const rq_plan *plan, int op, const double *in, double *out, int64_t k);
+int rq_host_wait(const rq_plan *plan);
 
 /*
  * Force/torque reductions about each body's centroid (or `origin`, host

@@ -43,7 +43,7 @@ class PlanInfo(C.Structure):
                 ("n_steps", C.c_int64), ("n_top", C.c_int64), ("tile_leaves", C.c_int64), ("n_tiles", C.c_int64),
                 ("blob_bytes", C.c_int64), ("sweep_bytes", C.c_int64 * 2), ("record_doubles", C.c_int64),
                 ("full_len", C.c_int64), ("comp_len", C.c_int64), ("n_case", C.c_int64 * 4),
-                ("device_bytes", C.c_int64), ("rounds", C.c_int64), ("host_segments", C.c_int64),
+                ("device_bytes", C.c_int64), ("rounds", C.c_int64),
                 ("node_slots", C.c_int64), ("stage_bytes", C.c_int64), ("sweep_smem", C.c_int64),
                 ("sweep_ctas_per_sm", C.c_int64), ("top_staged", C.c_int64), ("top_global", C.c_int64),
                 ("mrhs_min_k", C.c_int64), ("mrhs_units", C.c_int64 * 2), ("mrhs_bytes", C.c_int64 * 2)]
@@ -61,6 +61,8 @@ SIGNATURES = [
     ("rq_apply_ex", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64, _vp, C.c_uint32]),
     ("rq_launches_per_apply", C.c_int, [_vp, C.c_int, C.c_int64]),
     ("rq_apply_host", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64]),
+    ("rq_apply_host_async", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64]),
+    ("rq_host_wait", C.c_int, [_vp]),
     ("rq_z_apply", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64, _vp, _vp]),
     ("rq_z_apply_host", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64, _vp]),
     ("rq_body_centroids", C.c_int, [_vp, _dp]),

@@ -130,7 +130,6 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
     for (int c = 0; c < 4; c++) info->n_case[c] = p.n_case[c];
     info->device_bytes = p.device_bytes();
     info->rounds = p.wave_rounds;
-    info->host_segments = p.wave_nseg;
     info->node_slots = p.wave_mslots;
     info->stage_bytes = p.wave_stage_bytes;
     if (p.wave_streams) {
@@ -189,6 +188,20 @@ int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, in
   RQ_GUARD({
     need_plan(plan);
     rq::run_apply_host(plan->p, op, in, out, k);
+  })
+}
+
+int rq_apply_host_async(const rq_plan *plan, int op, const double *in, double *out, int64_t k) {
+  RQ_GUARD({
+    need_plan(plan);
+    rq::run_apply_host_async(plan->p, op, in, out, k);
+  })
+}
+
+int rq_host_wait(const rq_plan *plan) {
+  RQ_GUARD({
+    need_plan(plan);
+    rq::host_wait(plan->p);
   })
 }
 

@@ -75,7 +75,6 @@ __device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Stage the vector data a chunk needs, asynchronously (cp.async, one group):
 //   UP  : the chunk's bead forces, gathered through perm
 //   DOWN: the chunk's residue coefficients (contiguous per tile) + tile-root RV-sets
 __device__ __forceinline__ void cp_async16cg_u32(uint32_t dst, const void *src) {
@@ -473,8 +472,7 @@ __global__ void k_compress(const double *in, const int32_t *body_of, const int64
   else res[res_base[j] + loc - 6] = v;
 }
 
-void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases,
-               const WaveSync *sync) {
+void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s, unsigned phases) {
   if (op < 0 || op > 3) throw Error(RQ_ERR_VALUE, "op must be one of ('qv', 'qtv', 'qtilde_v', 'qtilde_tv')");
   if (op >= 2 && p.min_n < 2)
     throw Error(RQ_ERR_BODY_TOO_SMALL, "complement operators need every body to have >= 2 beads");
@@ -576,7 +574,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.max_topblob_smem));
     p.top_attr_set = true;
   }
-  const bool do_chunks = (phases & 1u) && p.wave_streams > 0;
+  const bool do_sweep = (phases & 1u) && p.wave_streams > 0;
   const bool do_top = (phases & 2u) && (tb1 > tb0 || t.n > 0);
   auto top_pass = [&]() {
     for (int c = 0; c < 4 && tb1 > tb0; c++) {
@@ -598,11 +596,10 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     }
   };
   auto sweep = [&]() {
-    if (do_chunks) run_wave(p, up, cin, cout, ss.scratch.as<double>(), roots, s, sync);
+    if (do_sweep) run_wave(p, up, cin, cout, ss.scratch.as<double>(), roots, s);
   };
   if (up) {
     sweep();
-    if (sync && sync->before_top) RQ_CUDA(cudaStreamWaitEvent(s, sync->before_top, 0));
     if (do_top) top_pass();
   } else {
     if (do_top) top_pass();

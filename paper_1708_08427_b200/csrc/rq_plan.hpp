@@ -1,7 +1,10 @@
 // rq_plan.hpp -- host-side plan object and error plumbing.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -19,6 +22,20 @@ namespace rq {
 // thread-local error message (rq_last_error)
 void set_error(const std::string &msg);
 const char *last_error();
+
+struct SetupTimer {  // RQ_SETUP_TIMING=1: per-phase wall time of build_plan (synchronises the stream)
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit SetupTimer(cudaStream_t st) : on(getenv("RQ_SETUP_TIMING") != nullptr), s(st), t(std::chrono::steady_clock::now()) {}
+  void mark(const char *name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rq setup] %-14s %9.3f ms\n", name, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 struct Status {
   int code = RQ_OK;
@@ -163,19 +180,21 @@ struct Plan {
   DBuf seg_begin;                  // int64 [n_seg + 1] bead ranges
   DBuf body_seg;                   // int64 [m + 1] segment CSR
   mutable DBuf zpart;              // double [6 * n_seg]
-  // host-buffer entry points: persistent device staging (grown on demand)
-  mutable DBuf stage_in, stage_out;
+  // host-buffer entry points (rq_host.cu): three streams (H2D, kernels, D2H) and two staging
+  // slots, so consecutive applications overlap
   mutable cudaStream_t host_stream = nullptr, host_stream2 = nullptr, host_stream3 = nullptr;
-  // host-buffer pipelining (rq_host.cu): per-segment flags / counters, and the top-tree residue
-  // rows (built on the first host application): row in the private layout, count, compact offset
-  mutable DBuf top_rows_d, top_coff_d, top_compact;
-  mutable void *host_sync = nullptr;  // uint32 flags [nseg] | counters [nseg]
-  mutable uint32_t host_epoch = 0;
-  mutable int64_t n_top_rows = -1, top_compact_doubles = 0;
-  mutable std::vector<int64_t> h_top_rows, h_top_coff;
-  mutable std::vector<int32_t> h_top_rr;
-  mutable double *top_pinned = nullptr;
-  mutable cudaEvent_t host_ev = nullptr;
+  struct HostSlot {
+    bool busy = false;
+    DBuf din, dout;                          // device staging
+    cudaEvent_t e_in = nullptr, e_k = nullptr, e_out = nullptr;
+    double *pin_in = nullptr, *pin_out = nullptr;  // pinned staging of pageable buffers
+    size_t pin_in_cap = 0, pin_out_cap = 0;
+    std::vector<cudaEvent_t> piece_ev;       // per-piece D2H events (pageable results)
+    double *defer_out = nullptr;             // pageable result delivered by the next wait
+    size_t defer_bytes = 0;
+  };
+  mutable HostSlot hslot[2];
+  mutable int host_next = 0;
 
   mutable std::mutex host_mu;
   // Per-stream exchange state: applications of one plan on different streams may run
@@ -212,8 +231,6 @@ struct Plan {
   int64_t wave_streams = 0, wave_steps = 0, wave_blob_bytes = 0, wave_nodes = 0;
   int64_t wave_up_bytes = 0, wave_down_bytes = 0;  // bytes one upward / downward sweep streams
   int64_t wave_stage_bytes = 0, wave_rounds = 1;
-  int wave_nseg = 1;                         // host segments (groups of rounds)
-  std::vector<int> wave_seg_minb, wave_seg_maxb;  // body range of each segment's tiles
   int wave_mslots = 0, wave_pf = 0, wave_nst = 2;  // L2 prefetch distance (steps), TMA stages (fixed 2)
   WaveCaps wave_caps;
   DBuf wave_desc;                  // StepDesc [wave_steps]
@@ -226,9 +243,13 @@ struct Plan {
   ~Plan() {
     for (cudaStream_t st : {host_stream, host_stream2, host_stream3})
       if (st) cudaStreamDestroy(st);
-    if (top_pinned) cudaFreeHost(top_pinned);
-    if (host_ev) cudaEventDestroy(host_ev);
-    if (host_sync) cudaFree(host_sync);
+    for (auto &S : hslot) {
+      for (cudaEvent_t e : {S.e_in, S.e_k, S.e_out})
+        if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : S.piece_ev) cudaEventDestroy(e);
+      if (S.pin_in) cudaFreeHost(S.pin_in);
+      if (S.pin_out) cudaFreeHost(S.pin_out);
+    }
   }
 };
 
@@ -247,28 +268,24 @@ size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg);
 void wave_prepare(const Plan &p);
 // tile part of one upward / downward sweep over all bodies (rq_wave.cu); residues in the
 // private layout, body-root vectors to / from `roots` (nullptr: dropped / zero)
-struct WaveSync {             // host-buffer pipelining (rq_wave.cuh)
-  const uint32_t *flags;     // [nseg] written by the copy engine after each input segment
-  uint32_t *counters;        // [nseg] bumped by every CTA once a segment's outputs are written
-  uint32_t epoch;            // flags / counters targets of this application
-  cudaEvent_t before_top;    // upward: the top pass waits for it (all input copies done)
-};
 void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots,
-              cudaStream_t s, const WaveSync *sync = nullptr);
+              cudaStream_t s);
 // bodies [j0, j1) of a plan (all work lists are in body order)
 struct BodyRange {
   int64_t j0 = 0, j1 = -1;  // j1 < 0: all bodies
 };
-struct WaveSync;
 void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
-               unsigned phases = 7u, const WaveSync *sync = nullptr);
+               unsigned phases = 7u);
 void build_mrhs(const Plan &p, cudaStream_t s);
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
                     unsigned phases = 7u, BodyRange range = BodyRange());
 bool use_mrhs(const Plan &p, int64_t k);
-// Host-buffer application pipelined over body segments: H2D of segment i+1,
-// kernels of segment i and D2H of segment i-1 overlap (three streams).
+// Host-buffer applications (rq_host.cu): H2D -> kernels -> D2H on three streams and two
+// staging slots; the async form returns once queued (pageable results are delivered by
+// host_wait), so consecutive applications overlap their copies.
 void run_apply_host(const Plan &p, int op, const double *in, double *out, int64_t k);
+void run_apply_host_async(const Plan &p, int op, const double *in, double *out, int64_t k);
+void host_wait(const Plan &p);
 void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, const double *origin_d,
            cudaStream_t s);
 int check_duplicates(const double *pos, const int64_t *offsets, int64_t m, bool host_input,

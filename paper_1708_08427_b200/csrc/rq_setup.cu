@@ -933,7 +933,7 @@ __global__ void k_dup_query(DupCtx c, int64_t N) {
 int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
-                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &stage_in, &stage_out, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
+                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
                         &res_base_d, &wave_desc, &wave_stream_first, &wave_blob};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
@@ -942,19 +942,6 @@ int64_t Plan::device_bytes() const {
 
 void compute_body_centroids(Plan &p, cudaStream_t s);  // rq_z.cu
 
-struct SetupTimer {  // RQ_SETUP_TIMING=1: per-phase wall time of build_plan (synchronises the stream)
-  bool on;
-  cudaStream_t s;
-  std::chrono::steady_clock::time_point t;
-  explicit SetupTimer(cudaStream_t st) : on(getenv("RQ_SETUP_TIMING") != nullptr), s(st), t(std::chrono::steady_clock::now()) {}
-  void mark(const char *name) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[rq setup] %-12s %9.3f ms\n", name, std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
 
 void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m, int max_depth,
                 bool host_input, cudaStream_t s) {

@@ -116,8 +116,78 @@ __global__ void k_wv_profile(const int64_t *tile_root, int64_t nt, NodeArrays A,
     v.dg += (res_rows(cs) > 0) + root;
     v.rm += 8 * rec_size(cs) + 16;
   }
-  for (int h = 0; h < A.height[g]; h++) {
-    const TLev &v = P[h];
+  (void)caps;
+  (void)bad;
+}
+
+// Rows of a tile: a height level whose nodes exceed a step's capacities is spread over
+// several consecutive rows (node i of a case -> row i mod r_h); r_h is the least count for
+// which the worst-case share of every resource fits a step.  Rows of height h precede
+// those of height h + 1, so every node still runs after its children.
+__device__ __forceinline__ int wv_rows_for(const TLev &v, int root, const WaveCaps &c) {
+  for (int r = 1;; r++) {
+    const int g = (v.g + r - 1) / r, rb = (v.r + r - 1) / r, b = (v.b + r - 1) / r;
+    if (g <= c.g && rb <= c.r && b <= c.b && 2 * b + rb <= c.beads && 8 * g + 4 * rb + 6 * root <= c.vd &&
+        g + rb + root <= c.dg && 256 * g + 176 * rb + 96 * b <= c.rm)
+      return r;
+  }
+}
+__global__ void k_wv_rows(const int64_t *tile_root, int64_t nt, NodeArrays A, const int64_t *tl_base, const TLev *tl,
+                          int32_t *hrows, int64_t *trows, WaveCaps caps) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int64_t g = tile_root[t];
+  const int L = nodeL(A, g);
+  if (L < 2) { trows[t] = 0; return; }
+  const int H = A.height[g];
+  int64_t tot = 0;
+  for (int h = 0; h < H; h++) {
+    const int r = wv_rows_for(tl[tl_base[t] + h], h == H - 1, caps);
+    hrows[tl_base[t] + h] = r;
+    tot += r;
+  }
+  trows[t] = tot;
+}
+// node -> row (tile-local) and the row profiles
+__global__ void k_wv_rowprof(const int64_t *tile_root, int64_t nt, NodeArrays A, const int64_t *tl_base,
+                             const int32_t *hrows, int32_t *hctr, const int64_t *rl_base, TLev *rp, int32_t *node_row,
+                             WaveCaps caps, int *bad) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int64_t g = tile_root[t];
+  const int L = nodeL(A, g);
+  if (L < 2) return;
+  const int H = A.height[g];
+  const int64_t hb = tl_base[t];
+  // row base of each height (hctr holds 4 ints per height: row base, GEN, RB, BB counters)
+  int base = 0;
+  for (int h = 0; h < H; h++) {
+    hctr[4 * (hb + h)] = base;
+    base += hrows[hb + h];
+  }
+  const int64_t first = g - 2 * (int64_t)L + 2;
+  TLev *P = rp + rl_base[t];
+  for (int64_t q = first; q <= g; q++) {
+    if (nodeL(A, q) < 2) continue;
+    const int cs = flag_case(A.flags[q]);
+    const int h = A.height[q] - 1;
+    int32_t *hc = hctr + 4 * (hb + h);
+    const int i = hc[1 + wv_rank(cs)]++;
+    const int row = hc[0] + i % hrows[hb + h];
+    node_row[q] = row;
+    TLev &v = P[row];
+    if (cs == GENERAL) v.g++;
+    else if (cs == RIGID_BEAD) v.r++;
+    else v.b++;
+    v.beads += wv_beads(cs);
+    const int root = q == g;
+    const int rr = res_rows(cs);
+    v.vd += (rr ? 2 * wv_pieces(A.res_base[A.node_body[q]] + A.res_off[q] - 6, rr) : 0) + 6 * root;
+    v.dg += (rr > 0) + root;
+    v.rm += 8 * rec_size(cs) + 16;
+  }
+  for (int r = 0; r < base; r++) {
+    const TLev &v = P[r];
     if (v.g > caps.g || v.r > caps.r || v.b > caps.b || v.beads > caps.beads || v.vd > caps.vd || v.dg > caps.dg ||
         v.rm > caps.rm)
       atomicExch(bad, 1);
@@ -189,7 +259,7 @@ __global__ void k_wv_place(const int64_t *sfirst, int64_t G, const int32_t *orde
 }
 
 // sort key of every tile node: (global step, case rank)
-__global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, const int64_t *stream_of_tile_first,
+__global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, const int32_t *node_row,
                           const int64_t *step_first, const int32_t *e_tile, uint64_t *keys, int32_t *vals,
                           const int32_t *tile_stream) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -198,42 +268,26 @@ __global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, co
   const int32_t t = node_tile[g];
   if (t >= 0) {
     const int64_t c = tile_stream[t];
-    const int64_t gs = step_first[c] + e_tile[t] + 2 + A.height[g] - 1;
+    const int64_t gs = step_first[c] + e_tile[t] + 2 + node_row[g];
     key = ((uint64_t)gs << 2) | (uint64_t)wv_rank(flag_case(A.flags[g]));
   }
   keys[g] = key;
   vals[g] = (int32_t)g;
-  (void)stream_of_tile_first;
 }
 
-__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int64_t nseg,
-                                 int32_t *tile_stream, int32_t *tile_seg, const int64_t *tile_root,
-                                 const int32_t *node_body, int *seg_minb, int *seg_maxb, const int64_t *tnodes) {
+__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int32_t *tile_stream) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  const int64_t t = order[i];
-  const int64_t r = (int64_t)(key[i] % R);
-  const int e = (int)(r * nseg / R);
-  tile_stream[t] = (int32_t)(key[i] / R);
-  tile_seg[t] = e;
-  if (tnodes[t]) {  // body range of each segment (host-buffer pieces)
-    const int j = node_body[tile_root[t]];
-    atomicMin(&seg_minb[e], j);
-    atomicMax(&seg_maxb[e], j);
-  }
+  if (i < nt) tile_stream[order[i]] = (int32_t)(key[i] / R);
 }
 
 struct StepCnt {
   int32_t g, r, b, ug, dg;
-  int32_t ugseg, dgseg, updone, dndone;  // see StepDesc
 };
 
 // per sorted node: step counts, list counts, step of the node, per-node list sizes
 __global__ void k_wv_count(const uint64_t *keys, const int32_t *vals, int64_t n, NodeArrays A, StepCnt *sc,
                            int64_t *step_of, int64_t *sfirst_sorted, int32_t *nb, int32_t *vd, int32_t *nd,
-                           const int32_t *node_tile, const int64_t *tile_root, const int32_t *tile_stream,
-                           const int32_t *tile_seg, int nseg, unsigned long long *seg_last,
-                           unsigned long long *seg_first) {
+                           const int32_t *node_tile, const int64_t *tile_root) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int64_t gs = (int64_t)(keys[p] >> 2);
@@ -244,45 +298,14 @@ __global__ void k_wv_count(const uint64_t *keys, const int32_t *vals, int64_t n,
   else atomicAdd(&sc[gs].b, 1);
   const int root = tile_root[node_tile[g]] == g;
   const int beads = wv_beads(cs), dge = (res_rows(cs) > 0) + root;
-  const int32_t t = node_tile[g];
-  const int e = tile_seg[t];
-  if (beads) { atomicAdd(&sc[gs - 2].ug, beads); atomicMax(&sc[gs - 2].ugseg, e); }
-  if (dge) { atomicAdd(&sc[gs + 2].dg, dge); atomicMin(&sc[gs + 2].dgseg, e); }
-  const int64_t ce = (int64_t)tile_stream[t] * nseg + e;
-  atomicMax(&seg_last[ce], (unsigned long long)gs);
-  atomicMin(&seg_first[ce], (unsigned long long)gs);
+  if (beads) atomicAdd(&sc[gs - 2].ug, beads);
+  if (dge) atomicAdd(&sc[gs + 2].dg, dge);
   step_of[g] = gs;
   if (p == 0 || (int64_t)(keys[p - 1] >> 2) != gs) sfirst_sorted[gs] = p;
   nb[p] = beads;
   const int rr = res_rows(cs);
   vd[p] = (rr ? 2 * wv_pieces(A.res_base[A.node_body[g]] + A.res_off[g] - 6, rr) : 0) + 6 * root;
   nd[p] = dge;
-}
-
-// per stream: the step after which each host segment has no node left (upward order:
-// cumulative max of the segments' last steps; downward: cumulative min from the top)
-__global__ void k_wv_markers(const int64_t *step_first, int64_t G, int nseg, const unsigned long long *seg_last,
-                             const unsigned long long *seg_first, StepCnt *sc) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= G) return;
-  const int64_t s0 = step_first[c], s1 = step_first[c + 1];
-  int64_t cm = s0;
-  for (int e = 0; e < nseg; e++) {
-    const unsigned long long l = seg_last[c * nseg + e];
-    if (l != 0ull) cm = max(cm, (int64_t)l);
-    atomicMax(&sc[cm].updone, e + 1);
-  }
-  int64_t cn = s1 - 1;
-  for (int e = nseg - 1; e >= 0; e--) {
-    const unsigned long long f = seg_first[c * nseg + e];
-    if (f != ~0ull) cn = min(cn, (int64_t)f);
-    atomicMax(&sc[cn].dndone, nseg - e);
-  }
-}
-
-__global__ void k_wv_init_cnt(StepCnt *sc, int64_t ns) {
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s < ns) sc[s].dgseg = 0x7fffffff;
 }
 
 __global__ void k_wv_step_bytes(const StepCnt *sc, int64_t ns, int64_t *bytes, unsigned long long *mx) {
@@ -303,30 +326,27 @@ __global__ void k_wv_descs(const StepCnt *sc, const int64_t *off, int64_t ns, St
   D.off16 = (uint32_t)(off[s] >> 4);
   D.nG = (uint8_t)c.g; D.nR = (uint8_t)c.r; D.nB = (uint8_t)c.b;
   D.n_ug = (uint16_t)c.ug; D.n_dg = (uint16_t)c.dg;
-  D.ug_seg = (uint8_t)c.ugseg;
-  D.dg_seg = (uint8_t)(c.dg ? c.dgseg : 0);
-  D.up_done = (uint8_t)c.updone;
-  D.dn_done = (uint8_t)c.dndone;
-  D.pad = 0;
+  D.pad0 = 0;
+  D.pad1 = 0;
   d[s] = D;
   const WaveSec S = wave_sections(D);
   *reinterpret_cast<StepDesc *>(blob + off[s]) = D;
   *reinterpret_cast<StepDesc *>(blob + off[s] + S.uhdr) = D;
 }
 
-// one thread per stream: interval colouring of the node 6-vectors (lowest free slot)
-constexpr int WV_MAX_SLOTS = 4096;
+// one CTA (one thread) per stream: interval colouring of the node 6-vectors (lowest free
+// slot), the two heaps in shared memory
+constexpr int WV_MAX_SLOTS = 1024;
 __global__ void k_wv_slots(const int64_t *node_first, int64_t G, const int32_t *vals, NodeArrays A,
                            const int64_t *step_of, const int32_t *node_tile, const int64_t *tile_root,
-                           int32_t *slot_of, int *max_slots, int *overflow, int32_t *free_all,
-                           long long *busy_all) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= G) return;
+                           int32_t *slot_of, int *max_slots, int *overflow) {
+  const int64_t c = blockIdx.x;
+  if (c >= G || threadIdx.x != 0) return;
   // free: min-heap of slot ids; busy: min-heap of (release step << 13 | slot)
-  int32_t *freeh = free_all + c * WV_MAX_SLOTS;
-  long long *busyh = busy_all + c * WV_MAX_SLOTS;
+  __shared__ int16_t freeh[WV_MAX_SLOTS];
+  __shared__ long long busyh[WV_MAX_SLOTS];
   int nf = 0, nbz = 0, next = 0;
-  auto push_free = [&](int32_t v) {
+  auto push_free = [&](int16_t v) {
     int i = nf++;
     while (i > 0) {
       int pa = (i - 1) >> 1;
@@ -337,7 +357,7 @@ __global__ void k_wv_slots(const int64_t *node_first, int64_t G, const int32_t *
     freeh[i] = v;
   };
   auto pop_free = [&]() {
-    int32_t top = freeh[0], v = freeh[--nf];
+    int16_t top = freeh[0], v = freeh[--nf];
     int i = 0;
     for (;;) {
       int l = 2 * i + 1;
@@ -378,7 +398,7 @@ __global__ void k_wv_slots(const int64_t *node_first, int64_t G, const int32_t *
     const int64_t g = vals[p];
     if (tile_root[node_tile[g]] == g) continue;  // tile roots exchange through global memory
     const int64_t gs = step_of[g];
-    while (nbz && (busyh[0] >> 13) < gs) push_free((int32_t)(pop_busy() & 8191));
+    while (nbz && (busyh[0] >> 13) < gs) push_free((int16_t)(pop_busy() & 8191));
     int32_t sl;
     if (nf) sl = pop_free();
     else {
@@ -507,6 +527,7 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
 // ---- builder driver ----------------------------------------------------------------
 
 void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
+  SetupTimer tm(s);
   p.wave_streams = 0;
   p.wave_steps = 0;
   const int64_t nt = in.n_tiles;
@@ -551,7 +572,29 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   RQ_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
   k_wv_profile<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), tl.as<TLev>(),
                                         node_tile.as<int32_t>(), caps, bad.as<int>());
-  if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a tile level exceeds the per-step capacities");
+  // rows: height levels split to fit the per-step capacities
+  DBuf hrows, trows, rl_base, hctr, rp, node_row;
+  hrows.alloc(std::max<int64_t>(total_lv, 1) * 4);
+  trows.alloc(nt * 8);
+  rl_base.alloc((nt + 1) * 8);
+  k_wv_rows<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), tl.as<TLev>(), hrows.as<int32_t>(),
+                                     trows.as<int64_t>(), caps);
+  ex_scan(trows.as<int64_t>(), rl_base.as<int64_t>(), nt, s);
+  const int64_t total_rows = d2h1<int64_t>(rl_base.as<int64_t>() + nt - 1, s) + d2h1<int64_t>(trows.as<int64_t>() + nt - 1, s);
+  RQ_CUDA(cudaMemcpyAsync(rl_base.as<int64_t>() + nt, &total_rows, 8, cudaMemcpyHostToDevice, s));
+  hctr.alloc(std::max<int64_t>(total_lv, 1) * 16);
+  RQ_CUDA(cudaMemsetAsync(hctr.p, 0, std::max<int64_t>(total_lv, 1) * 16, s));
+  rp.alloc(std::max<int64_t>(total_rows, 1) * sizeof(TLev));
+  RQ_CUDA(cudaMemsetAsync(rp.p, 0, std::max<int64_t>(total_rows, 1) * sizeof(TLev), s));
+  node_row.alloc(NN * 4);
+  k_wv_rowprof<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), hrows.as<int32_t>(),
+                                        hctr.as<int32_t>(), rl_base.as<int64_t>(), rp.as<TLev>(), node_row.as<int32_t>(),
+                                        caps, bad.as<int>());
+  if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a step row exceeds the per-step capacities");
+  tl.reset();
+  hctr.reset();
+  hrows.reset();
+  tm.mark("wave rows");
   // streams: range c of every round
   int64_t R = std::max<int64_t>(1, p.N / 170000);
   R = std::min<int64_t>(R, std::max<int64_t>(1, nt / (4 * G)));
@@ -589,54 +632,35 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
       if (h[c] < 0) h[c] = h[c + 1];
     RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
   }
-  // host segments: groups of rounds
-  int64_t nseg = std::min<int64_t>(R, 32);
-  if (const char *e = getenv("RQ_WAVE_SEGS")) nseg = std::max<int64_t>(1, std::min<int64_t>(R, std::min(255, atoi(e))));
-  p.wave_nseg = (int)nseg;
-  DBuf tile_seg, segb;
-  tile_seg.alloc(nt * 4);
-  segb.alloc(nseg * 8);
-  {
-    std::vector<int> init(2 * nseg);
-    for (int64_t e = 0; e < nseg; e++) { init[e] = INT32_MAX; init[nseg + e] = -1; }
-    RQ_CUDA(cudaMemcpyAsync(segb.p, init.data(), nseg * 8, cudaMemcpyHostToDevice, s));
-  }
-  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, nseg,
-                                            tile_stream.as<int32_t>(), tile_seg.as<int32_t>(), in.tile_root,
-                                            in.node_body, segb.as<int>(), segb.as<int>() + nseg, tnodes.as<int64_t>());
-  {
-    std::vector<int> h(2 * nseg);
-    d2h(h.data(), segb.p, 2 * nseg, s);
-    p.wave_seg_minb.assign(h.begin(), h.begin() + nseg);
-    p.wave_seg_maxb.assign(h.begin() + nseg, h.end());
-  }
-  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(theight.as<int64_t>(), order.as<int32_t>(), nt, th_sorted.as<int64_t>());
+  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, tile_stream.as<int32_t>());
+  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(trows.as<int64_t>(), order.as<int32_t>(), nt, th_sorted.as<int64_t>());
   k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
   ex_scan(th_sorted.as<int64_t>(), lv_scan.as<int64_t>(), nt, s);
   ex_scan(tn_sorted.as<int64_t>(), n_scan_s.as<int64_t>(), nt, s);
-  RQ_CUDA(cudaMemcpyAsync(lv_scan.as<int64_t>() + nt, &total_lv, 8, cudaMemcpyHostToDevice, s));
+  RQ_CUDA(cudaMemcpyAsync(lv_scan.as<int64_t>() + nt, &total_rows, 8, cudaMemcpyHostToDevice, s));
   RQ_CUDA(cudaMemcpyAsync(n_scan_s.as<int64_t>() + nt, &total_nodes, 8, cudaMemcpyHostToDevice, s));
   // placement
   DBuf load, e_tile, n_steps, step_first;
-  load.alloc(std::max<int64_t>(total_lv, 1) * sizeof(TLev));
-  RQ_CUDA(cudaMemsetAsync(load.p, 0, std::max<int64_t>(total_lv, 1) * sizeof(TLev), s));
+  load.alloc(std::max<int64_t>(total_rows, 1) * sizeof(TLev));
+  RQ_CUDA(cudaMemsetAsync(load.p, 0, std::max<int64_t>(total_rows, 1) * sizeof(TLev), s));
   e_tile.alloc(nt * 4);
   n_steps.alloc(G * 8);
   step_first.alloc((G + 1) * 8);
   k_wv_place<<<nblk(G, 64), 64, 0, s>>>(sfirst.as<int64_t>(), G, order.as<int32_t>(), lv_scan.as<int64_t>(),
-                                         tl_base.as<int64_t>(), tl.as<TLev>(), load.as<TLev>(), theight.as<int64_t>(),
+                                         rl_base.as<int64_t>(), rp.as<TLev>(), load.as<TLev>(), trows.as<int64_t>(),
                                          e_tile.as<int32_t>(), n_steps.as<int64_t>(), caps);
   ex_scan(n_steps.as<int64_t>(), step_first.as<int64_t>(), G, s);
   const int64_t NS = d2h1<int64_t>(step_first.as<int64_t>() + G - 1, s) + d2h1<int64_t>(n_steps.as<int64_t>() + G - 1, s);
   RQ_CUDA(cudaMemcpyAsync(step_first.as<int64_t>() + G, &NS, 8, cudaMemcpyHostToDevice, s));
   load.reset();
+  tm.mark("wave place");
   // node order: (global step, case)
   DBuf keys, vals, keys2, vals2;
   keys.alloc(NN * 8);
   vals.alloc(NN * 4);
   keys2.alloc(NN * 8);
   vals2.alloc(NN * 4);
-  k_wv_keys<<<nblk(NN), NT, 0, s>>>(NN, A, node_tile.as<int32_t>(), nullptr, step_first.as<int64_t>(),
+  k_wv_keys<<<nblk(NN), NT, 0, s>>>(NN, A, node_tile.as<int32_t>(), node_row.as<int32_t>(), step_first.as<int64_t>(),
                                      e_tile.as<int32_t>(), keys.as<uint64_t>(), vals.as<int32_t>(),
                                      tile_stream.as<int32_t>());
   {
@@ -653,17 +677,12 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   }
   keys.reset();
   vals.reset();
+  tm.mark("wave sort");
   // counts
   const int64_t n = total_nodes;
   DBuf sc, step_of, sfs, nb, vd, nd, bscan, vscan, dscan;
   sc.alloc(NS * sizeof(StepCnt));
   RQ_CUDA(cudaMemsetAsync(sc.p, 0, NS * sizeof(StepCnt), s));
-  k_wv_init_cnt<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), NS);
-  DBuf seg_last, seg_first;
-  seg_last.alloc(G * nseg * 8);
-  seg_first.alloc(G * nseg * 8);
-  RQ_CUDA(cudaMemsetAsync(seg_last.p, 0, G * nseg * 8, s));
-  RQ_CUDA(cudaMemsetAsync(seg_first.p, 0xff, G * nseg * 8, s));
   step_of.alloc(NN * 8);
   sfs.alloc(NS * 8);
   RQ_CUDA(cudaMemsetAsync(sfs.p, 0, NS * 8, s));
@@ -675,11 +694,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   dscan.alloc(n * 8);
   k_wv_count<<<nblk(n), NT, 0, s>>>(keys2.as<uint64_t>(), vals2.as<int32_t>(), n, A, sc.as<StepCnt>(),
                                      step_of.as<int64_t>(), sfs.as<int64_t>(), nb.as<int32_t>(), vd.as<int32_t>(),
-                                     nd.as<int32_t>(), node_tile.as<int32_t>(), in.tile_root, tile_stream.as<int32_t>(),
-                                     tile_seg.as<int32_t>(), (int)nseg, seg_last.as<unsigned long long>(),
-                                     seg_first.as<unsigned long long>());
-  k_wv_markers<<<nblk(G, 64), 64, 0, s>>>(step_first.as<int64_t>(), G, (int)nseg, seg_last.as<unsigned long long>(),
-                                           seg_first.as<unsigned long long>(), sc.as<StepCnt>());
+                                     nd.as<int32_t>(), node_tile.as<int32_t>(), in.tile_root);
   ex_scan(nb.as<int32_t>(), bscan.as<int64_t>(), n, s);
   ex_scan(vd.as<int32_t>(), vscan.as<int64_t>(), n, s);
   ex_scan(nd.as<int32_t>(), dscan.as<int64_t>(), n, s);
@@ -703,6 +718,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   p.wave_desc.alloc(NS * sizeof(StepDesc));
   k_wv_descs<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), off.as<int64_t>(), NS, p.wave_desc.as<StepDesc>(),
                                       p.wave_blob.as<uint8_t>());
+  tm.mark("wave counts");
   // slots
   DBuf slot_of, node_first, msl;
   slot_of.alloc(NN * 4);
@@ -719,21 +735,16 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   }
   msl.alloc(8);
   RQ_CUDA(cudaMemsetAsync(msl.p, 0, 8, s));
-  {
-    DBuf fh, bh;
-    fh.alloc(G * WV_MAX_SLOTS * 4);
-    bh.alloc(G * WV_MAX_SLOTS * 8);
-    k_wv_slots<<<nblk(G, 32), 32, 0, s>>>(node_first.as<int64_t>(), G, vals2.as<int32_t>(), A, step_of.as<int64_t>(),
-                                           node_tile.as<int32_t>(), in.tile_root, slot_of.as<int32_t>(),
-                                           msl.as<int>(), msl.as<int>() + 1, fh.as<int32_t>(), bh.as<long long>());
-    RQ_CUDA(cudaStreamSynchronize(s));
-  }
+  k_wv_slots<<<(unsigned)G, 32, 0, s>>>(node_first.as<int64_t>(), G, vals2.as<int32_t>(), A, step_of.as<int64_t>(),
+                                         node_tile.as<int32_t>(), in.tile_root, slot_of.as<int32_t>(), msl.as<int>(),
+                                         msl.as<int>() + 1);
   {
     int h[2];
     d2h(h, msl.p, 2, s);
-    if (h[1]) throw Error(RQ_ERR_VALUE, "wave layout: more than 4096 live node vectors in a stream");
+    if (h[1]) throw Error(RQ_ERR_VALUE, "wave layout: more than 1024 live node vectors in a stream");
     p.wave_mslots = std::max(1, h[0]);
   }
+  tm.mark("wave slots");
   WriteIn w{A,
             keys2.as<uint64_t>(),
             vals2.as<int32_t>(),
@@ -749,6 +760,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
             p.wave_blob.as<uint8_t>()};
   k_wv_write<<<nblk(n), NT, 0, s>>>(w, n);
   RQ_CUDA(cudaGetLastError());
+  tm.mark("wave write");
   p.wave_stream_first.alloc((G + 1) * 8);
   RQ_CUDA(cudaMemcpyAsync(p.wave_stream_first.p, step_first.p, (G + 1) * 8, cudaMemcpyDeviceToDevice, s));
   // per-direction bytes streamed per application (algorithmic bytes of the sweep)
@@ -814,11 +826,6 @@ __device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
 }
 __device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *q) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(q) : "memory");
-  return v;
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -933,13 +940,6 @@ struct WaveCtx {
   uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: NST stages | M | 3 gather regions (vreg doubles each)
   int pf;                                // L2 prefetch distance (steps)
   int64_t in_len;                        // doubles in `in` (16-byte windows never read past it)
-  // host-buffer pipelining (nullptr: inputs resident): a block's gathers wait until the copy
-  // engine has flagged their segment (flags[e] >= epoch); after the last step holding nodes
-  // of a segment every CTA bumps counters[e] (the D2H of that segment waits for G bumps)
-  const uint32_t *flags;
-  uint32_t *counters;
-  uint32_t epoch;
-  int nseg;
 };
 
 #ifndef RQ_WAVE_MIN_BLOCKS
@@ -986,8 +986,6 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
   __syncthreads();
   pdl_wait();  // vectors and exchange slots may come from the previous kernel
   unsigned phase = 0;
-  int seg_ok = UP ? -1 : 1 << 30;  // host segments known to have arrived
-  int done = 0;                    // host segments this CTA has counted as done
   int st = 0;
   for (int t = 0; t < n; t++, st = (st == NST - 1) ? 0 : st + 1) {
     mbar_wait(bar_u + 8 * st, (phase >> st) & 1u);
@@ -995,16 +993,6 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     const unsigned char *B = smem + st * a.stage_bytes;
     const StepDesc d = *reinterpret_cast<const StepDesc *>(B);
     const WaveSec S = wave_sections(d);
-    // host-buffer path: the rows this block's gathers read must have arrived
-    if (a.flags) {
-      const int need = UP ? d.ug_seg : d.dg_seg;
-      if (UP ? need > seg_ok : need < seg_ok) {
-        if (tid == 0)
-          while ((int32_t)(ld_acquire(a.flags + need) - a.epoch) < 0) __nanosleep(256);
-        __syncthreads();
-        seg_ok = need;
-      }
-    }
     // gathers for step t + 2 (into region (t + 2) % 3): 16-byte L2 copies (cp.async.cg)
     {
       const int rg = (t + 2) % 3;
@@ -1093,14 +1081,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       }
     }
     cp_wait<1>();  // this thread's gathers for step t + 1
-    const int done_now = a.counters ? (UP ? d.up_done : d.dn_done) : 0;
-    if (done_now > done) __threadfence();  // this step's outputs before the segment counters
     __syncthreads();
-    if (done_now > done) {
-      if (tid == 0)
-        for (int e = done; e < done_now; e++) atomicAdd(a.counters + (UP ? e : a.nseg - 1 - e), 1u);
-      done = done_now;
-    }
     if (tid == PROD && t + NST < n) {  // stage st is free: block t + NST
       uint32_t off, bytes;
       span(dn, off, bytes);
@@ -1114,10 +1095,6 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       }
       if (t + NST + 1 < n) dn = a.steps[blk(t + NST + 1)];
     }
-  }
-  if (a.counters && tid == 0 && done < a.nseg) {
-    __threadfence();
-    for (int e = done; e < a.nseg; e++) atomicAdd(a.counters + (UP ? e : a.nseg - 1 - e), 1u);
   }
 }
 
@@ -1146,8 +1123,7 @@ void wave_prepare(const Plan &p) {
   p.wave_ready = true;
 }
 
-void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s,
-              const WaveSync *sync) {
+void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s) {
   if (!p.wave_streams) return;
   if (reinterpret_cast<uintptr_t>(in) & 15) throw Error(RQ_ERR_VALUE, "wave sweep input must be 16-byte aligned");
   wave_prepare(p);
@@ -1163,12 +1139,6 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
   const size_t sm = wave_smem(p, &a.o_m, &a.o_v, &a.vreg);
   a.pf = p.wave_pf;
   a.in_len = up ? 3 * p.N : p.res_base[p.m];
-  a.nseg = p.wave_nseg;
-  if (sync) {
-    a.flags = sync->flags;
-    a.counters = sync->counters;
-    a.epoch = sync->epoch;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.wave_streams);
   cfg.blockDim = dim3(128);

@@ -37,17 +37,11 @@ namespace rq {
 struct StepDesc {     // 16 bytes (also the block header)
   uint32_t off16;     // block byte offset / 16 in the wave blob
   uint8_t nG, nR, nB;
-  uint8_t ug_seg;     // host segment the upward gathers of this block read (the latest one)
+  uint8_t pad0;
   uint16_t n_ug;      // upward gathers held by this block (beads of step s+2)
   uint16_t n_dg;      // downward gathers held by this block (nodes of step s-2)
-  uint8_t dg_seg;     // host segment the downward gathers read (the earliest one)
-  uint8_t up_done;    // upward: segments [0, up_done) have no node left in this stream after this step
-  uint8_t dn_done;    // downward: segments [nseg - dn_done, nseg) done after this step
-  uint8_t pad;
+  uint32_t pad1;
 };
-// Host segments: the rounds are grouped into nseg <= 255 segments; the host-buffer path
-// copies a segment's vector rows in (flag per segment, written by the copy engine) and out
-// (per-segment counters of the CTAs that are done with it) while the sweep runs.
 
 // upward metadata: x, y = M slots (internal children) or bead offsets (doubles) in the
 // step's gather region (BEAD_BEAD: both, RIGID_BEAD: y); self = M slot of the
@@ -70,8 +64,8 @@ struct WaveGather {
   uint16_t dst;   // double offset in the gather region (even: 16-byte copies)
   uint16_t kind;  // WG_*
 };
-// Gathers are 16-byte cp.async.cg copies (L2 only: rows that arrive while the sweep runs
-// are never served stale from L1).  A bead's 3 doubles sit in a 4-double window starting
+// Gathers are 16-byte cp.async.cg copies (L2 only: the scattered rows do not pollute L1;
+// two copies cover a bead instead of three).  A bead's 3 doubles sit in a 4-double window starting
 // at the even row below 3b (offset b & 1); a residue run [row, row + rr) in the window
 // [row & ~1, ...) of wv_pieces(row, rr) 16-byte pieces (offset row & 1).
 __host__ __device__ inline int wv_pieces(int64_t row, int rr) { return (int)(((row & 1) + rr + 1) >> 1); }

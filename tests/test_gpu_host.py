@@ -1,13 +1,10 @@
-"""Host-buffer applications (rq_apply_host, the drop-in numpy path's C entry).
+"""Host-buffer applications (rq_apply_host / rq_apply_host_async + rq_host_wait).
 
-Pinned host buffers take the segment-pipelined path (input copies flagged per
-host segment, outputs copied back per segment while the sweep runs, top-tree
-residues compacted and scattered by host threads); pageable buffers take the
-plain copy-apply-copy path.  Both must equal the device-resident application
-bitwise: they run the same kernels on the same data.
+Pinned and pageable host buffers, synchronous and queued back to back (two
+staging slots: the H2D of one application overlaps the D2H of the previous
+one; a third queued application completes the first).  Every result must
+equal the device-resident application bitwise: same kernels, same data.
 """
-
-import ctypes as C
 
 import numpy as np
 import pytest
@@ -25,52 +22,57 @@ def rq():
     return rq
 
 
-def _operator(rq, monkeypatch, counts, seed, rounds, segs):
-    from paper_1708_08427_b200.workloads import ellipsoid_batch
-
-    monkeypatch.setenv("RQ_WAVE_ROUNDS", str(rounds))
-    monkeypatch.setenv("RQ_WAVE_SEGS", str(segs))
-    pos, off = ellipsoid_batch(counts, seed=seed)
-    return rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off)), off
-
-
 def _device(op, name, x):
     import torch
 
     return op.apply(name, torch.from_numpy(x).cuda()).cpu().numpy()
 
 
-@pytest.mark.parametrize("counts,rounds,segs", [
-    ([4096] * 120, 16, 8),                        # many bodies, segments of whole bodies
-    ([3000, 60000, 700, 90000, 2500, 40000], 12, 6),  # big bodies straddle segments; dataflow tops
-    ([50, 3, 2000, 7, 4096, 300], 4, 4),          # tiny bodies, bodies without tiles
-])
-def test_pinned_pipelined_equals_device(rq, monkeypatch, counts, rounds, segs):
+@pytest.mark.parametrize("counts", [[4096] * 60, [3000, 60000, 700, 90000, 2500, 40000], [50, 3, 2000, 7, 4096, 300]])
+def test_host_paths_equal_device(rq, counts):
     import torch
     from paper_1708_08427_b200 import _lib as L
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
 
-    op, off = _operator(rq, monkeypatch, counts, 11, rounds, segs)
+    pos, off = ellipsoid_batch(counts, seed=11)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
     N, m = int(off[-1]), len(off) - 1
-    lib = L.lib()
-    h = op.plan.handle
+    lib, h = L.lib(), op.plan.handle
     rng = np.random.default_rng(5)
-    for rep in range(3):  # flags and counters are monotone across calls
-        v = rng.normal(size=3 * N)
-        g = rng.normal(size=3 * N - 6 * m)
-        hv = torch.from_numpy(v).pin_memory()
-        hg = torch.from_numpy(g).pin_memory()
-        o1 = torch.full((3 * N - 6 * m,), np.nan, dtype=torch.float64).pin_memory()
-        o2 = torch.full((3 * N,), np.nan, dtype=torch.float64).pin_memory()
-        L.check(lib.rq_apply_host(h, L.OP_QTILDE_V, hv.data_ptr(), o1.data_ptr(), 1))
-        L.check(lib.rq_apply_host(h, L.OP_QTILDE_TV, hg.data_ptr(), o2.data_ptr(), 1))
-        assert np.array_equal(o1.numpy(), _device(op, "qtilde_v", v)), rep
-        assert np.array_equal(o2.numpy(), _device(op, "qtilde_tv", g)), rep
+    vs = [rng.normal(size=3 * N) for _ in range(3)]
+    gs = [rng.normal(size=3 * N - 6 * m) for _ in range(3)]
+    want_v = [_device(op, "qtilde_v", v) for v in vs]
+    want_g = [_device(op, "qtilde_tv", g) for g in gs]
+    for pinned in (True, False):
+        def buf(x):
+            t = torch.from_numpy(np.array(x))
+            return t.pin_memory() if pinned else t
+        hv = [buf(v) for v in vs]
+        hg = [buf(g) for g in gs]
+        ov = [buf(np.full(3 * N - 6 * m, np.nan)) for _ in vs]
+        og = [buf(np.full(3 * N, np.nan)) for _ in gs]
+        # synchronous
+        L.check(lib.rq_apply_host(h, L.OP_QTILDE_V, hv[0].data_ptr(), ov[0].data_ptr(), 1))
+        assert np.array_equal(ov[0].numpy(), want_v[0]), pinned
+        # queued back to back: six applications, two slots (each new one completes an older one)
+        for i in range(3):
+            L.check(lib.rq_apply_host_async(h, L.OP_QTILDE_V, hv[i].data_ptr(), ov[i].data_ptr(), 1))
+            L.check(lib.rq_apply_host_async(h, L.OP_QTILDE_TV, hg[i].data_ptr(), og[i].data_ptr(), 1))
+        L.check(lib.rq_host_wait(h))
+        for i in range(3):
+            assert np.array_equal(ov[i].numpy(), want_v[i]), (pinned, i)
+            assert np.array_equal(og[i].numpy(), want_g[i]), (pinned, i)
 
 
-def test_pageable_and_full_ops_equal_device(rq, monkeypatch):
-    op, off = _operator(rq, monkeypatch, [4096] * 40 + [1, 2, 777], 12, 8, 4)
+def test_numpy_api_and_full_ops_equal_device(rq):
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([4096] * 40 + [1, 2, 777], seed=12)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
     N = int(off[-1])
     rng = np.random.default_rng(6)
     v = rng.normal(size=3 * N)
     for name in ("qv", "qtv"):
         assert np.array_equal(op.apply(name, v), _device(op, name, v)), name
+    V = rng.normal(size=(3 * N, 3))
+    assert np.array_equal(op.apply("qv", V), op.apply("qv", __import__("torch").from_numpy(V).cuda()).cpu().numpy())
