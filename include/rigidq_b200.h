@@ -19,6 +19,11 @@
  *    one-to-one onto the reference exception classes (errors.py:4-33).
  *  - a plan (tree + factors + apply layout) is immutable after rq_setup;
  *    concurrent rq_apply calls on distinct streams are safe (matfree.py:16-17).
+ *    Each stream a plan is used on gets its own exchange state on first use, kept
+ *    until rq_plan_free: 48 B per tile root + 4 B per top node, plus (k > 1 column
+ *    loop) two k-column staging blocks and (Zf) 48 B per segment and column.
+ *  - every entry point runs on the plan's device and restores the caller's
+ *    current device before returning.
  */
 #ifndef RIGIDQ_B200_H
 #define RIGIDQ_B200_H

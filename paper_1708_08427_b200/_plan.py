@@ -19,10 +19,10 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
-def _torch_stream():
+def _torch_stream(device=None):
     import torch
 
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 class Plan:
@@ -77,6 +77,11 @@ class Plan:
         d["n_case"] = list(inf.n_case)
         return d
 
+    def _check_device(self, t):
+        dev = L.lib().rq_plan_device(self._h)
+        if t.device.index != dev:
+            raise ValueError(f"tensor on cuda:{t.device.index}, operator on cuda:{dev}")
+
     # ---- lengths -------------------------------------------------------------
     def lengths(self, op: str):
         full = 3 * self.N
@@ -95,7 +100,8 @@ class Plan:
             import torch
 
             out = torch.empty((lo, k), dtype=torch.float64, device=v2.device)
-            L.check(lib.rq_apply(self._h, code, v2.data_ptr(), out.data_ptr(), k, _torch_stream()))
+            self._check_device(v2)
+            L.check(lib.rq_apply(self._h, code, v2.data_ptr(), out.data_ptr(), k, _torch_stream(v2.device)))
             return out
         out = np.empty((lo, k))
         L.check(lib.rq_apply_host(self._h, code, v2.ctypes.data, out.ctypes.data, k))
@@ -113,7 +119,8 @@ class Plan:
             import torch
 
             out = torch.empty((lo, k), dtype=torch.float64, device=v2.device)
-            L.check(lib.rq_z_apply(self._h, op, v2.data_ptr(), out.data_ptr(), k, optr, _torch_stream()))
+            self._check_device(v2)
+            L.check(lib.rq_z_apply(self._h, op, v2.data_ptr(), out.data_ptr(), k, optr, _torch_stream(v2.device)))
             return out
         out = np.empty((lo, k))
         L.check(lib.rq_z_apply_host(self._h, op, v2.ctypes.data, out.ctypes.data, k, optr))

@@ -41,6 +41,7 @@ namespace {
 void need_plan(const rq_plan *p) {
   if (!p) throw rq::Error(RQ_ERR_VALUE, "null plan");
 }
+#define PLAN_DEVICE(plan) rq::DeviceGuard _dev_guard((plan)->p.device)
 void need_gpu() {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -111,6 +112,7 @@ int rq_plan_device(const rq_plan *plan) { return plan ? plan->p.device : -1; }
 int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     const rq::Plan &p = plan->p;
     memset(info, 0, sizeof(*info));
     info->m = p.m;
@@ -151,6 +153,7 @@ int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
 int rq_apply(const rq_plan *plan, int op, const double *in, double *out, int64_t k, void *stream) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     if (!in || !out) throw rq::Error(RQ_ERR_VALUE, "null vector");
     rq::run_apply(plan->p, op, in, out, k, static_cast<cudaStream_t>(stream));
   })
@@ -160,6 +163,7 @@ int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int6
                 uint32_t phases) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     if (!in || !out) throw rq::Error(RQ_ERR_VALUE, "null vector");
     rq::run_apply(plan->p, op, in, out, k, static_cast<cudaStream_t>(stream), phases);
   })
@@ -187,6 +191,7 @@ int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
 int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, int64_t k) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::run_apply_host(plan->p, op, in, out, k);
   })
 }
@@ -194,6 +199,7 @@ int rq_apply_host(const rq_plan *plan, int op, const double *in, double *out, in
 int rq_apply_host_async(const rq_plan *plan, int op, const double *in, double *out, int64_t k) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::run_apply_host_async(plan->p, op, in, out, k);
   })
 }
@@ -201,6 +207,7 @@ int rq_apply_host_async(const rq_plan *plan, int op, const double *in, double *o
 int rq_host_wait(const rq_plan *plan) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::host_wait(plan->p);
   })
 }
@@ -209,6 +216,7 @@ int rq_z_apply(const rq_plan *plan, int op, const double *in, double *out, int64
                void *stream) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     const rq::Plan &p = plan->p;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     rq::DBuf dorg;
@@ -224,6 +232,7 @@ int rq_z_apply(const rq_plan *plan, int op, const double *in, double *out, int64
 int rq_z_apply_host(const rq_plan *plan, int op, const double *in, double *out, int64_t k, const double *origin) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     const rq::Plan &p = plan->p;
     RQ_CUDA(cudaSetDevice(p.device));
     const int64_t li = (op == RQ_Z_F) ? 3 * p.N : 6 * p.m, lo = (op == RQ_Z_F) ? 6 * p.m : 3 * p.N;
@@ -243,6 +252,7 @@ int rq_z_apply_host(const rq_plan *plan, int op, const double *in, double *out, 
 int rq_body_centroids(const rq_plan *plan, double *out) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     RQ_CUDA(cudaSetDevice(plan->p.device));
     RQ_CUDA(cudaMemcpy(out, plan->p.body_centroid.p, plan->p.m * 24, cudaMemcpyDeviceToHost));
   })
@@ -281,6 +291,7 @@ int rq_export_tree(const rq_plan *plan, int64_t body, int64_t *perm, int64_t *st
                    int64_t *right, int32_t *split_axis, int32_t *depth, double *centroid, double *box) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::export_tree(plan->p, body, perm, start, stop, left, right, split_axis, depth, centroid, box);
   })
 }
@@ -289,6 +300,7 @@ int rq_export_factors(const rq_plan *plan, int64_t body, int32_t *ncase, int64_t
                       uint8_t *swapped, double *t22, double *omega, int64_t *res_offsets, int64_t *total_rows) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::export_factors(plan->p, body, ncase, n, nx, ny, swapped, t22, omega, res_offsets, total_rows);
   })
 }
@@ -296,6 +308,7 @@ int rq_export_factors(const rq_plan *plan, int64_t body, int32_t *ncase, int64_t
 int64_t rq_omega_size(const rq_plan *plan, int64_t body) {
   try {
     need_plan(plan);
+    PLAN_DEVICE(plan);
     return rq::omega_size(plan->p, body);
   } catch (const rq::Error &e) {
     rq::set_error(e.msg);
@@ -309,6 +322,7 @@ int64_t rq_omega_size(const rq_plan *plan, int64_t body) {
 int rq_explicit_q_size(const rq_plan *plan, int64_t body, int64_t *n_blocks, int64_t *n_doubles) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::explicit_q_size(plan->p, body, n_blocks, n_doubles);
   })
 }
@@ -317,6 +331,7 @@ int rq_explicit_q(const rq_plan *plan, int64_t body, double *root_rows, int64_t 
                   int64_t *block_rows, double *block_data) {
   RQ_GUARD({
     need_plan(plan);
+    PLAN_DEVICE(plan);
     rq::explicit_q(plan->p, body, root_rows, block_node, block_col, block_rows, block_data);
   })
 }

@@ -279,7 +279,12 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
-  if (a.cls[blockIdx.x] != a.want) return;
+  // every CTA waits for the predecessor grid before exiting, so this grid's completion
+  // always implies the predecessor's (the next kernel's griddepcontrol.wait relies on it)
+  if (a.cls[blockIdx.x] != a.want) {
+    pdl_wait();
+    return;
+  }
   const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
   // stage the header part (levels, meta, inputs) with one TMA copy; the records stay
   // in global memory (prefetched into L2 here) and are read per node, so the CTA
@@ -423,6 +428,9 @@ void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t 
 
 }  // namespace
 
+// Per-stream state is created on a stream's first use and kept for the plan's lifetime
+// (the header documents the footprint: applications on many distinct streams each hold
+// their own exchange slots and staging).
 Plan::StreamState &Plan::state_for(cudaStream_t s) const {
   std::lock_guard<std::mutex> lock(state_mu);
   auto &slot = stream_state[s];

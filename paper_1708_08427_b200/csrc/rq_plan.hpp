@@ -57,6 +57,20 @@ struct Error {
   Error(int c, std::string m) : code(c), msg(std::move(m)) {}
 };
 
+// Sets the plan's device for the duration of a C-ABI call and restores the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard &) = delete;
+  DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
 // owning device buffer
 struct DBuf {
   void *p = nullptr;
@@ -179,7 +193,6 @@ struct Plan {
   DBuf seg_body;                   // int32 [n_seg]
   DBuf seg_begin;                  // int64 [n_seg + 1] bead ranges
   DBuf body_seg;                   // int64 [m + 1] segment CSR
-  mutable DBuf zpart;              // double [6 * n_seg]
   // host-buffer entry points (rq_host.cu): three streams (H2D, kernels, D2H) and two staging
   // slots, so consecutive applications overlap
   mutable cudaStream_t host_stream = nullptr, host_stream2 = nullptr, host_stream3 = nullptr;
@@ -203,12 +216,10 @@ struct Plan {
   // owned per stream.
   struct StreamState {
     DBuf scratch, mrhs_scratch, top_cnt;
-    DBuf chunk_ctr;           // 2 x {claim, done} counters of the dynamic chunk schedule
     DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
     DBuf res_tmp, roots;      // Q / Q^T: residues in the private layout and the 6 root rows per body
     DBuf in_al;               // 16-byte aligned copy of a misaligned input
     DBuf zpart;               // Zf per-segment partial sums
-    uint32_t chunk_epoch = 0;  // chunk launches so far (consecutive launches alternate counters)
   };
   mutable std::mutex state_mu;
   mutable std::map<cudaStream_t, std::unique_ptr<StreamState>> stream_state;

@@ -933,7 +933,7 @@ __global__ void k_dup_query(DupCtx c, int64_t N) {
 int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
-                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &zpart, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
+                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
                         &res_base_d, &wave_desc, &wave_stream_first, &wave_blob};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;

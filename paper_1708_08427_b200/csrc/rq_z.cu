@@ -2,10 +2,11 @@
 // the model centroid (BeadModel.centroid = positions.mean(0), model.py:56-61).
 //
 // Z is never assembled: Zf = [sum f_k ; sum (r_k - c) x f_k] is a segmented
-// reduction with a FIXED order (segments of SEG beads, tree-reduced inside a
-// CTA, then summed in segment order per body), so results do not depend on
-// batch composition or GPU count.  Z^T u = V + w x (r_k - c) is a streaming
-// per-bead map (48 B/bead).
+// reduction with a FIXED order (segments of seg_len(n_j) beads -- a function of
+// the body's own size only -- tree-reduced inside a CTA, then reduced per body by
+// one warp in a fixed lane order), so results do not depend on batch composition
+// or GPU count.  All k columns go in one launch (grid.y = column).  Z^T u =
+// V + w x (r_k - c) is a streaming per-bead map (48 B/bead).
 #include <algorithm>
 #include <vector>
 
@@ -14,8 +15,9 @@
 namespace rq {
 namespace {
 
-constexpr int SEG = 4096;
 constexpr int NTZ = 256;
+// segment length: 4096 beads, 1024 for bodies of >= 2^18 beads (enough CTAs for one body)
+inline int64_t seg_len(int64_t n) { return n >= (int64_t(1) << 18) ? 1024 : 4096; }
 
 template <int W>
 __device__ __forceinline__ void block_sum(double (&v)[W], double *sh) {
@@ -58,10 +60,11 @@ __global__ void k_body_mean(const double *part, const int64_t *body_seg, const i
 }
 
 __global__ void __launch_bounds__(NTZ) k_seg_zf(const double *pos, const int64_t *seg_begin, const int32_t *seg_body,
-                                                const double *origin, const double *f, int64_t K, int64_t col,
+                                                const double *origin, const double *f, int64_t K, int64_t n_seg,
                                                 double *part) {
   __shared__ double sh[6 * NTZ];
   const int64_t s = blockIdx.x;
+  const int64_t col = blockIdx.y;
   const int64_t b = seg_begin[s], e = seg_begin[s + 1];
   const int j = seg_body[s];
   const double cx = origin[j * 3], cy = origin[j * 3 + 1], cz = origin[j * 3 + 2];
@@ -107,17 +110,26 @@ __global__ void __launch_bounds__(NTZ) k_seg_zf(const double *pos, const int64_t
   }
   block_sum<6>(v, sh);
   if (threadIdx.x == 0)
-    for (int a = 0; a < 6; a++) part[s * 6 + a] = v[a];
+    for (int a = 0; a < 6; a++) part[(col * n_seg + s) * 6 + a] = v[a];
 }
 
+// one warp per (body, column): lane l sums the body's segments l, l + 32, ... in order, then a
+// fixed shuffle tree (bodies with few segments: lane 0 alone, in segment order)
 __global__ void k_body_zf(const double *part, const int64_t *body_seg, int64_t m, double *out, int64_t K,
-                          int64_t col) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= m) return;
+                          int64_t n_seg) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t col = blockIdx.y;
+  if (w >= m) return;
+  const int64_t j = w;
+  const double *P = part + col * n_seg * 6;
   double v[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t s = body_seg[j]; s < body_seg[j + 1]; s++)
-    for (int a = 0; a < 6; a++) v[a] += part[s * 6 + a];
-  for (int a = 0; a < 6; a++) out[(j * 6 + a) * K + col] = v[a];
+  for (int64_t s = body_seg[j] + lane; s < body_seg[j + 1]; s += 32)
+    for (int a = 0; a < 6; a++) v[a] += P[s * 6 + a];
+  for (int o = 16; o > 0; o >>= 1)
+    for (int a = 0; a < 6; a++) v[a] += __shfl_down_sync(0xffffffffu, v[a], o);
+  if (lane == 0)
+    for (int a = 0; a < 6; a++) out[(j * 6 + a) * K + col] = v[a];
 }
 
 // K = 1, 16-byte aligned output: a thread maps a bead pair (48 contiguous bytes in and out)
@@ -151,7 +163,8 @@ __global__ void k_ztu2(const double *pos, const int32_t *body_of, const double *
 }
 
 __global__ void k_ztu(const double *pos, const int32_t *body_of, const double *origin, const double *u, int64_t N,
-                      int64_t K, int64_t col, double *out) {
+                      int64_t K, double *out) {
+  const int64_t col = blockIdx.y;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int j = body_of[i];
@@ -172,7 +185,8 @@ void compute_body_centroids(Plan &p, cudaStream_t s) {
   std::vector<int32_t> seg_body;
   for (int64_t j = 0; j < p.m; j++) {
     body_seg[j] = (int64_t)seg_body.size();
-    for (int64_t b = p.bead_off[j]; b < p.bead_off[j + 1]; b += SEG) {
+    const int64_t sl = seg_len(p.bead_off[j + 1] - p.bead_off[j]);
+    for (int64_t b = p.bead_off[j]; b < p.bead_off[j + 1]; b += sl) {
       seg_begin.push_back(b);
       seg_body.push_back((int32_t)j);
     }
@@ -183,14 +197,15 @@ void compute_body_centroids(Plan &p, cudaStream_t s) {
   p.seg_body.alloc(p.n_seg * 4);
   p.seg_begin.alloc((p.n_seg + 1) * 8);
   p.body_seg.alloc((p.m + 1) * 8);
-  p.zpart.alloc(p.n_seg * 48);
   RQ_CUDA(cudaMemcpyAsync(p.seg_body.p, seg_body.data(), p.n_seg * 4, cudaMemcpyHostToDevice, s));
   RQ_CUDA(cudaMemcpyAsync(p.seg_begin.p, seg_begin.data(), (p.n_seg + 1) * 8, cudaMemcpyHostToDevice, s));
   RQ_CUDA(cudaMemcpyAsync(p.body_seg.p, body_seg.data(), (p.m + 1) * 8, cudaMemcpyHostToDevice, s));
   p.body_centroid.alloc(p.m * 24);
+  DBuf part;
+  part.alloc(p.n_seg * 48);
   k_seg_possum<<<(unsigned)p.n_seg, NTZ, 0, s>>>(p.pos_orig.as<double>(), p.seg_begin.as<int64_t>(),
-                                                 p.zpart.as<double>());
-  k_body_mean<<<(unsigned)((p.m + 127) / 128), 128, 0, s>>>(p.zpart.as<double>(), p.body_seg.as<int64_t>(),
+                                                 part.as<double>());
+  k_body_mean<<<(unsigned)((p.m + 127) / 128), 128, 0, s>>>(part.as<double>(), p.body_seg.as<int64_t>(),
                                                             p.bead_off_d.as<int64_t>(), p.m,
                                                             p.body_centroid.as<double>());
   RQ_CUDA(cudaGetLastError());
@@ -199,24 +214,27 @@ void compute_body_centroids(Plan &p, cudaStream_t s) {
 void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, const double *origin_d,
            cudaStream_t s) {
   if (op != RQ_Z_F && op != RQ_Z_TU) throw Error(RQ_ERR_VALUE, "z op must be RQ_Z_F or RQ_Z_TU");
-  if (k < 1) throw Error(RQ_ERR_LENGTH, "k must be >= 1");
+  if (k < 1 || k > 65535) throw Error(RQ_ERR_LENGTH, "k must be in [1, 65535]");
   RQ_CUDA(cudaSetDevice(p.device));
   const double *origin = origin_d ? origin_d : p.body_centroid.as<double>();
-  for (int64_t col = 0; col < k; col++) {
-    if (op == RQ_Z_F) {
-      k_seg_zf<<<(unsigned)p.n_seg, NTZ, 0, s>>>(p.pos_orig.as<double>(), p.seg_begin.as<int64_t>(),
-                                                 p.seg_body.as<int32_t>(), origin, in, k, col,
-                                                 p.zpart.as<double>());
-      k_body_zf<<<(unsigned)((p.m + 127) / 128), 128, 0, s>>>(p.zpart.as<double>(), p.body_seg.as<int64_t>(),
-                                                              p.m, out, k, col);
-    } else if (k == 1 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-      const int64_t np = (p.N + 1) / 2;
-      k_ztu2<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(p.pos_orig.as<double>(), p.body_of.as<int32_t>(), origin,
-                                                          in, p.N, out);
-    } else {
-      k_ztu<<<(unsigned)((p.N + 255) / 256), 256, 0, s>>>(p.pos_orig.as<double>(), p.body_of.as<int32_t>(),
-                                                          origin, in, p.N, k, col, out);
-    }
+  if (op == RQ_Z_F) {
+    // per-segment partial sums are per-stream state: Zf calls on different streams never share them
+    Plan::StreamState &ss = p.state_for(s);
+    const size_t need = (size_t)p.n_seg * 48 * k;
+    if (ss.zpart.bytes < need) ss.zpart.alloc(need);
+    k_seg_zf<<<dim3((unsigned)p.n_seg, (unsigned)k), NTZ, 0, s>>>(p.pos_orig.as<double>(), p.seg_begin.as<int64_t>(),
+                                                                 p.seg_body.as<int32_t>(), origin, in, k, p.n_seg,
+                                                                 ss.zpart.as<double>());
+    k_body_zf<<<dim3((unsigned)((p.m * 32 + 255) / 256), (unsigned)k), 256, 0, s>>>(
+        ss.zpart.as<double>(), p.body_seg.as<int64_t>(), p.m, out, k, p.n_seg);
+  } else if (k == 1 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    const int64_t np = (p.N + 1) / 2;
+    k_ztu2<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(p.pos_orig.as<double>(), p.body_of.as<int32_t>(), origin,
+                                                        in, p.N, out);
+  } else {
+    k_ztu<<<dim3((unsigned)((p.N + 255) / 256), (unsigned)k), 256, 0, s>>>(p.pos_orig.as<double>(),
+                                                                         p.body_of.as<int32_t>(), origin, in, p.N, k,
+                                                                         out);
   }
   RQ_CUDA(cudaGetLastError());
 }

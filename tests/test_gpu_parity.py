@@ -140,20 +140,33 @@ def test_kat_pm(rq):
     np.testing.assert_allclose(f.t22, [[np.sqrt(2), 0, 0], [0, np.sqrt(2), 0], [0, 0, 0]], atol=1e-15)
 
 
-def test_degenerate_line_by_span(rq):
-    """Collinear input: compare spans (projector distance), never vectors."""
+def test_degenerate_line_by_span(rq, oracle_mod):
+    """Collinear input (Z has rank 5): compare spans, never vectors (the
+    reference's own oracle.py:38-58 dense_complement + projector_distance).  Q~ has
+    orthonormal rows inside the dense complement of Z's row space and spans all of it
+    but one direction."""
     g = load("line64")
     pos = g["positions"]
     n = pos.shape[0]
     op = rq.BodyOperator(rq.BeadModel(pos))
     qt = op.qtilde_v(np.eye(3 * n))  # Q~ itself, (3n-6) x 3n
-    assert np.abs(qt @ qt.T - np.eye(3 * n - 6)).max() < 1e-10
+    assert np.abs(qt @ qt.T - np.eye(3 * n - 6)).max() < 1e-12
     z = rq.assemble_z(rq.BeadModel(pos)).entries
     _, s, vt = np.linalg.svd(z, full_matrices=True)
     rank = int((s > max(z.shape) * np.finfo(float).eps * s[0]).sum())
     assert rank == 5
-    # Q~ is orthogonal to the row space of Z
-    assert np.abs(qt @ z.T).max() < 1e-10 * np.abs(z).max()
+    # dense complement (oracle.py:38-47): the trailing 3n - 5 right singular vectors
+    comp = vt[rank:]
+    assert np.abs(qt - (qt @ comp.T) @ comp).max() < 1e-12  # rows of Q~ lie in it
+    # Q~ spans all of that (3n - 5)-dim complement but one direction: P_comp - P_Q~ is a rank-1
+    # projector (projectors as in oracle.py:50-58)
+    d = comp.T @ comp - qt.T @ qt
+    assert np.abs(d @ d - d).max() < 1e-12 and abs(np.trace(d) - 1.0) < 1e-12
+    # the oracle's Q~ is an equally valid choice of that subspace (its noise-level pivots pick a
+    # different missing direction, so the two projectors are NOT compared to each other)
+    ref = oracle_mod.OracleBody(pos).qtilde_v(np.eye(3 * n))
+    dr = comp.T @ comp - ref.T @ ref
+    assert np.abs(dr @ dr - dr).max() < 1e-12 and abs(np.trace(dr) - 1.0) < 1e-12
 
 
 def test_oracle_config_sizes(rq, oracle_mod):
@@ -376,9 +389,10 @@ def test_node_primitives(rq, oracle_mod):
             np.testing.assert_allclose(ly, my, atol=1e-13)
 
 
-def test_rigid_body_basis(rq):
+def test_rigid_body_basis(rq, oracle_mod):
     """estimator.RigidBodyBasis (reference estimator.py:43-78) on the GPU operators:
-    rows are force vectors; a batch of rows is one multi-RHS block."""
+    rows are force vectors; a batch of rows is one multi-RHS block.  Checked against the
+    oracle (not only the package's own single-vector path)."""
     from paper_1708_08427_b200.estimator import RigidBodyBasis
     from paper_1708_08427_b200.workloads import ellipsoid_batch
     from sklearn.exceptions import NotFittedError
@@ -388,12 +402,15 @@ def test_rigid_body_basis(rq):
     rng = np.random.default_rng(8)
     V = rng.normal(size=(7, 3 * n))
     op = rq.BodyOperator(rq.BeadModel(pos))
-    for comp, fwd in ((False, op.qv), (True, op.qtilde_v)):
+    ob = oracle_mod.OracleBody(pos)
+    for comp, fwd, ofwd in ((False, op.qv, ob.qv), (True, op.qtilde_v, ob.qtilde_v)):
         est = RigidBodyBasis(complement=comp).fit(pos)
         C = est.transform(V)
         assert C.shape == (7, 3 * n - (6 if comp else 0))
         ref = np.stack([fwd(V[i]) for i in range(7)])
         assert np.abs(C - ref).max() <= 1e-13 * np.abs(ref).max()
+        oref = ofwd(np.ascontiguousarray(V.T)).T
+        assert np.linalg.norm(C - oref) / np.linalg.norm(oref) < 1e-12
         assert np.allclose(est.transform(V[2]), C[2], rtol=0, atol=1e-13 * np.abs(ref).max())
         back = est.inverse_transform(C)
         if comp:  # Q~^T Q~ is the projector onto the complement; Q~ Q~^T = I
@@ -406,6 +423,29 @@ def test_rigid_body_basis(rq):
         RigidBodyBasis().fit(pos).transform(V[:, :-1])
     with pytest.raises(ValueError):
         RigidBodyBasis(complement=True).fit(pos[:1])
+
+
+def test_scipy_operator(rq, oracle_mod):
+    """BodyOperator.scipy_operator (matfree.py:198-206): LinearOperator matvec / rmatvec /
+    matmat on the GPU operators vs the oracle."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, _ = ellipsoid_batch([900], seed=14)
+    n = pos.shape[0]
+    op = rq.BodyOperator(rq.BeadModel(pos))
+    ob = oracle_mod.OracleBody(pos)
+    rng = np.random.default_rng(15)
+    for comp, fwd, back in ((False, ob.qv, ob.qtv), (True, ob.qtilde_v, ob.qtilde_tv)):
+        L = op.scipy_operator(complement=comp)
+        rows = 3 * n - (6 if comp else 0)
+        assert L.shape == (rows, 3 * n)
+        v = rng.normal(size=3 * n)
+        w = rng.normal(size=rows)
+        assert np.linalg.norm(L.matvec(v) - fwd(v)) / np.linalg.norm(fwd(v)) < 1e-12
+        assert np.linalg.norm(L.rmatvec(w) - back(w)) / np.linalg.norm(back(w)) < 1e-12
+        M = rng.normal(size=(3 * n, 4))
+        assert np.linalg.norm(L.matmat(M) - fwd(M)) / np.linalg.norm(fwd(M)) < 1e-12
+        assert abs(L.matvec(v) @ w - v @ L.rmatvec(w)) < 1e-12 * np.linalg.norm(v) * np.linalg.norm(w)
 
 
 def test_concurrent_streams(rq):
