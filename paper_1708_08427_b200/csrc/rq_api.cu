@@ -172,14 +172,16 @@ int rq_apply_ex(const rq_plan *plan, int op, const double *in, double *out, int6
 int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
   if (!plan) return -1;
   const rq::Plan &p = plan->p;
-  if (rq::use_mrhs(p, k)) {  // column-parallel kernels: one launch per phase for all k columns
-    int tiles = 0, tops = 0;
-    for (int64_t j = 0; j < p.m; j++) {
-      const int64_t n = p.bead_off[j + 1] - p.bead_off[j];
-      tiles |= n >= 2;
-      tops |= n > p.tile_leaves;
+  if (rq::use_mrhs(p, k)) {  // column-parallel kernels: one launch for the tiles, one per top level
+    try {
+      rq::DeviceGuard g(p.device);
+      rq::build_mrhs(p, nullptr);
+    } catch (...) {
+      return -1;
     }
-    return tiles + tops + ((p.n_small && op <= 1) ? 1 : 0);
+    const int tiles = p.n_tile_units > 0 ? 1 : 0, tops = p.n_top_units > 0 ? 1 : 0;
+    const int levels = p.n_mtop ? (int)p.h_mtop_level.size() - 1 : 0;
+    return tiles + tops + levels + ((p.n_small && op <= 1) ? 1 : 0);
   }
   int classes = 0;
   for (int c = 0; c < 4; c++) classes += p.topclass_count[c] > 0;

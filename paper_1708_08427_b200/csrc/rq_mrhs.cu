@@ -3,8 +3,8 @@
 // a 2-D v applies the operator column by column; the reference does it as
 // one gemm per node, matfree.py:55-60).
 //
-// Design: every warp runs a "stack machine" over one unit (a tile = maximal
-// subtree of <= tile_leaves beads, or the top tree of a big body) for 32
+// Design (tiles): every warp runs a "stack machine" over one unit (a tile =
+// maximal subtree of <= mrhs_tile beads) for 32
 // columns at once: lane = column, so all lanes share one node, its record is
 // a broadcast load, and every vector access is one coalesced 256-byte row
 // segment of the (rows, k) block.  Nodes are visited in heavy-child-first
@@ -17,11 +17,19 @@
 //
 // Unit program: entries at a fixed 256-byte stride (forward for Q, backward
 // for Q^T), each = SEntry header (16 B) + the node's compact record.
+//
+// Design (top trees, the nodes above the tiles): level-parallel.  The top nodes
+// of all bodies are sorted by height; one launch per height level runs a warp
+// per (node, group of 32 columns), lane = column: children from the tile
+// exchange rows, the top exchange rows [top node][6][k] or the bead rows, so a
+// single large body (config 3) is swept with the whole GPU instead of one warp.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+
+#include <cub/cub.cuh>
 
 #include "rq_nodeops.cuh"
 #include "rq_plan.hpp"
@@ -38,6 +46,7 @@ constexpr int MRHS_NT = 128;  // 4 independent warps per block
 
 struct BuildCtx {
   int S;
+  int64_t big;  // bodies with more beads sweep their top tree level-parallel (k_mrhs_top)
   int64_t NN, m;
   const int64_t *bead_off, *node_off, *rec_off;
   const int32_t *start, *stop, *left, *right, *parent, *res_off, *perm;
@@ -67,8 +76,11 @@ __global__ void k_unit_flags(BuildCtx c, int32_t *is_tile_unit, int32_t *is_top_
   const bool tile = L >= 2 && L <= c.S && (root || Lp > c.S);
   is_tile_unit[g] = tile;
   tile_nodes[g] = tile ? L - 1 : 0;
-  is_top_unit[g] = root && L > c.S;
-  if (L > c.S) atomicAdd(&top_count[j], 1);
+  // top trees of bodies up to c.big beads: one stack-machine unit per body (the warp keeps
+  // the top vectors in shared memory); larger ones run level-parallel (k_mrhs_top)
+  const bool small_body = nj <= c.big;
+  is_top_unit[g] = root && L > c.S && small_body;
+  if (L > c.S && small_body) atomicAdd(&top_count[j], 1);
 }
 
 struct UnitDesc {  // 32 bytes
@@ -191,6 +203,58 @@ __global__ void k_unit_program(BuildCtx c, UnitDesc *units, int64_t n_units, con
   units[u].depth = maxdepth;
   atomicMax(top ? max_depth_top : max_depth_tile, maxdepth);
   atomicAdd(&bytes[top ? 1 : 0], (unsigned long long)used);
+}
+
+// level-parallel top trees: one entry per top node (L > S), sorted by height
+struct MTop {       // 32 bytes
+  int32_t x, y;     // formula-x / -y child: >= 0 top index; <= -2 tile exchange slot (-2 - v); bead: BEAD_REF | orig
+  int32_t res;      // body-relative Q~ row of the residues (res_off - 6), -1 for BEAD_BEAD
+  int32_t body;
+  int32_t flags;    // node flags | (is_root << 8)
+  int32_t pad;
+  int64_t rec_off;  // record in the plan's compact record table
+};
+constexpr int32_t BEAD_REF = 0x40000000;
+
+__global__ void k_mtop_keys(BuildCtx c, const int32_t *height, uint64_t *key, int32_t *val, int32_t *is_top) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= c.NN) return;
+  const int64_t j = body_of_node(c, g);
+  const bool top = c.stop[g] - c.start[g] > c.S && c.bead_off[j + 1] - c.bead_off[j] > c.big;
+  is_top[g] = top;
+  key[g] = top ? ((uint64_t)height[g] << 40) | (uint64_t)g : ~0ull;
+  val[g] = (int32_t)g;
+}
+__global__ void k_mtop_index(const int32_t *order, int64_t n, int32_t *tidx) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q < n) tidx[order[q]] = (int32_t)q;
+}
+__global__ void k_mtop_fill(BuildCtx c, const int32_t *order, int64_t n, const int32_t *tidx, const int32_t *tile_slot_of,
+                            MTop *out) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int64_t g = order[q];
+  const int64_t j = body_of_node(c, g), no = c.node_off[j], bo = c.bead_off[j];
+  const unsigned f = c.flags[g];
+  const int64_t lc = no + c.left[g], rc = no + c.right[g];
+  const int64_t xc = flag_swapped(f) ? rc : lc, yc = flag_swapped(f) ? lc : rc;
+  auto ref = [&](int64_t ch) -> int32_t {
+    const int L = c.stop[ch] - c.start[ch];
+    if (L == 1) return BEAD_REF | c.perm[bo + c.start[ch]];
+    if (L > c.S) return tidx[ch];
+    return -2 - tile_slot_of[ch];
+  };
+  MTop t;
+  t.x = ref(xc);
+  t.y = ref(yc);
+  const int cs = flag_case(f);
+  t.res = cs == BEAD_BEAD ? -1 : c.res_off[g] - 6;
+  t.body = (int32_t)j;
+  const int nj = (int)(c.bead_off[j + 1] - c.bead_off[j]);
+  t.flags = (int32_t)f | (((g - no) == 2 * (int64_t)nj - 2) ? 256 : 0);
+  t.pad = 0;
+  t.rec_off = c.rec_off[g];
+  out[q] = t;
 }
 
 // ---- kernels ----------------------------------------------------------------------------
@@ -510,6 +574,104 @@ __global__ void k_small_m(const int32_t *bodies, int64_t n, const int64_t *bead_
   out[i] = in[i];
 }
 
+struct MTopCtx {
+  const MTop *top;
+  int64_t q0, n;      // this level's top nodes [q0, q0 + n)
+  int64_t n_cg;       // column groups of 32
+  const double *rec;
+  const int64_t *bead_off;
+  const double *in;
+  double *out;
+  double *tx;         // top exchange [top][6][K]
+  double *scr;        // tile exchange [slot][6][K]
+  int64_t K;
+  int op;
+};
+
+// one warp per (top node, column group): merge (UP) / split (DOWN), lane = column
+template <bool UP>
+__global__ void __launch_bounds__(128) k_mrhs_top(MTopCtx a) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= a.n * a.n_cg) return;
+  const int64_t q = a.q0 + w / a.n_cg;
+  const int64_t col = (w % a.n_cg) * 32 + lane;
+  const bool act = col < a.K;
+  const int64_t K = a.K, c = act ? col : 0;
+  const MTop T = a.top[q];
+  const int cs = flag_case(T.flags & 0xff);
+  double R[rec_size(GENERAL)];
+  {
+    const double2 *r2 = reinterpret_cast<const double2 *>(a.rec + T.rec_off);
+#pragma unroll
+    for (int i = 0; i < rec_size(GENERAL) / 2; i++) {
+      double2 v = make_double2(0.0, 0.0);
+      if (2 * i < rec_size(cs)) v = __ldg(r2 + i);
+      R[2 * i] = v.x;
+      R[2 * i + 1] = v.y;
+    }
+  }
+  const bool full = (a.op == RQ_OP_QV || a.op == RQ_OP_QTV);
+  const int64_t bead0 = a.bead_off[T.body];
+  const int64_t sbase = full ? 3 * bead0 + 6 : 3 * bead0 - 6 * (int64_t)T.body;
+  auto vec = [&](int32_t ref) -> double * {  // 6-vector rows of a top node / tile root (column c)
+    return ref >= 0 ? a.tx + (int64_t)ref * 6 * K + c : a.scr + (int64_t)(-2 - ref) * 6 * K + c;
+  };
+  double aa, bb;
+  rec_ratios(cs, R, 1, aa, bb);
+  if (UP) {
+    double mx[6], my[6], mp[6], res[6];
+    auto load = [&](int32_t ref, double (&m)[6]) {
+      if (ref & BEAD_REF && ref > 0) {
+        const double *p = a.in + (3 * (bead0 + (ref & ~BEAD_REF))) * K + c;
+        m[0] = __ldg(p); m[1] = __ldg(p + K); m[2] = __ldg(p + 2 * K); m[3] = m[4] = m[5] = 0.0;
+      } else {
+        const double *p = vec(ref);
+#pragma unroll
+        for (int r = 0; r < 6; r++) m[r] = __ldcg(p + r * K);
+      }
+    };
+    load(T.x, mx);
+    load(T.y, my);
+    merge(cs, R, 1, flag_signs(T.flags & 0xff), aa, bb, mx, my, mp, res);
+    if (!act) return;
+    for (int r = 0; r < res_rows(cs); r++) a.out[(sbase + T.res + r) * K + c] = res[r];
+    if (T.flags & 256) {
+      if (a.op == RQ_OP_QV)
+        for (int r = 0; r < 6; r++) a.out[(3 * bead0 + r) * K + c] = mp[r];
+    } else {
+      double *p = a.tx + q * 6 * K + c;
+#pragma unroll
+      for (int r = 0; r < 6; r++) __stcg(p + r * K, mp[r]);
+    }
+  } else {
+    double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
+    if (T.flags & 256) {
+#pragma unroll
+      for (int r = 0; r < 6; r++) lp[r] = a.op == RQ_OP_QTV ? a.in[(3 * bead0 + r) * K + c] : 0.0;
+    } else {
+      const double *p = a.tx + q * 6 * K + c;
+#pragma unroll
+      for (int r = 0; r < 6; r++) lp[r] = __ldcg(p + r * K);
+    }
+    for (int r = 0; r < res_rows(cs); r++) res[r] = a.in[(sbase + T.res + r) * K + c];
+    split(cs, R, 1, flag_signs(T.flags & 0xff), aa, bb, lp, res, lx, ly);
+    if (!act) return;
+    auto store = [&](int32_t ref, const double (&l)[6]) {
+      if (ref & BEAD_REF && ref > 0) {
+        double *p = a.out + (3 * (bead0 + (ref & ~BEAD_REF))) * K + c;
+        p[0] = l[0]; p[K] = l[1]; p[2 * K] = l[2];
+      } else {
+        double *p = vec(ref);
+#pragma unroll
+        for (int r = 0; r < 6; r++) __stcg(p + r * K, l[r]);
+      }
+    };
+    store(T.x, lx);
+    store(T.y, ly);
+  }
+}
+
 template <class T>
 T d2h1m(const void *src, cudaStream_t s) {
   T v;
@@ -525,7 +687,9 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
   if (p.mrhs_built) return;
   const int64_t NN = p.NN, m = p.m;
   BuildCtx c;
-  c.S = p.mrhs_tile;  // unit size of the column-parallel programs (independent of the chunk tiles)
+  c.S = p.mrhs_tile;  // unit size of the column-parallel programs (independent of the wave tiles)
+  c.big = 65536;
+  if (const char *e = getenv("RQ_MRHS_TOP_LEVELS")) c.big = std::max<int64_t>(0, atoll(e));
   c.NN = NN;
   c.m = m;
   c.bead_off = p.bead_off_d.as<int64_t>();
@@ -620,6 +784,42 @@ void build_mrhs(const Plan &p, cudaStream_t s) {
   p.mrhs_top_bytes = (int64_t)hb[1];
   p.mrhs_depth_tile = std::max(1, hd[0]);
   p.mrhs_depth_top = std::max(1, hd[1]);
+  // level-parallel top trees: top nodes sorted by (height, id)
+  {
+    DBuf key, val, key2, val2, istop, tidx;
+    key.alloc(NNa * 8);
+    val.alloc(NNa * 4);
+    key2.alloc(NNa * 8);
+    val2.alloc(NNa * 4);
+    istop.alloc(NNa * 4);
+    tidx.alloc(NNa * 4);
+    if (NN > 0) k_mtop_keys<<<nb(NN), 256, 0, s>>>(c, p.height.as<int32_t>(), key.as<uint64_t>(), val.as<int32_t>(),
+                                                   istop.as<int32_t>());
+    size_t tb = 0;
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.as<uint64_t>(), key2.as<uint64_t>(), val.as<int32_t>(),
+                                            val2.as<int32_t>(), (int)NN, 0, 64, s));
+    DBuf tmp;
+    tmp.alloc(tb);
+    RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.as<uint64_t>(), key2.as<uint64_t>(), val.as<int32_t>(),
+                                            val2.as<int32_t>(), (int)NN, 0, 64, s));
+    std::vector<uint64_t> hk(NN);
+    if (NN) RQ_CUDA(cudaMemcpyAsync(hk.data(), key2.p, NN * 8, cudaMemcpyDeviceToHost, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    int64_t ntop = 0;
+    while (ntop < NN && hk[ntop] != ~0ull) ntop++;
+    p.n_mtop = ntop;
+    p.h_mtop_level.clear();
+    for (int64_t q = 0; q < ntop; q++)
+      if (q == 0 || (hk[q] >> 40) != (hk[q - 1] >> 40)) p.h_mtop_level.push_back(q);
+    p.h_mtop_level.push_back(ntop);
+    p.mtop.alloc(std::max<int64_t>(ntop, 1) * sizeof(MTop));
+    if (ntop) {
+      k_mtop_index<<<nb(ntop), 256, 0, s>>>(val2.as<int32_t>(), ntop, tidx.as<int32_t>());
+      k_mtop_fill<<<nb(ntop), 256, 0, s>>>(c, val2.as<int32_t>(), ntop, tidx.as<int32_t>(), slot_of.as<int32_t>(),
+                                           p.mtop.as<MTop>());
+    }
+    RQ_CUDA(cudaStreamSynchronize(s));
+  }
   // body -> unit ranges (host), for body-segmented applications
   std::vector<UnitDesc> hu(nu);
   if (nu) RQ_CUDA(cudaMemcpy(hu.data(), p.mrhs_units.p, nu * sizeof(UnitDesc), cudaMemcpyDeviceToHost));
@@ -644,12 +844,9 @@ bool use_mrhs(const Plan &p, int64_t k) {
   const char *pol = getenv("RQ_MRHS");  // "always" / "never" override the cost model (tests, tuning)
   if (pol && !strcmp(pol, "always")) return true;
   if (pol && !strcmp(pol, "never")) return false;
-  // Cost model (measured on one B200): a body's top unit is one warp walking its top-tree
-  // nodes in sequence, ~35 ns per bead of the largest body (config 3, 2^20 beads: ~30 ms
-  // per operator, whatever k), while the column loop costs ~0.05 ns per bead-RHS more than
-  // the column-parallel tile kernels.  Config 5 (8192-bead bodies, k = 32) stays on the
-  // multi-RHS kernels; a single 2^20-bead body uses the column loop below k ~ 700.
-  return (double)max_n * 700.0 < (double)k * (double)p.N;
+  // The column-parallel kernels beat the column loop from mrhs_min columns on (measured):
+  // their top trees run level-parallel, so single large bodies no longer need the loop.
+  return true;
 }
 
 void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_t k, cudaStream_t s,
@@ -661,8 +858,10 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
   const int64_t t0 = p.h_tile_unit_first[j0], t1 = p.h_tile_unit_first[j1];
   const int64_t q0 = p.h_top_unit_first[j0], q1 = p.h_top_unit_first[j1];
   const size_t scratch_bytes = (size_t)std::max<int64_t>(p.n_tile_units, 1) * 6 * k * 8;
+  const size_t tx_bytes = (size_t)std::max<int64_t>(p.n_mtop, 1) * 6 * k * 8;
   Plan::StreamState &ss = p.state_for(s);
   if (ss.mrhs_scratch.bytes < scratch_bytes) ss.mrhs_scratch.alloc(scratch_bytes);
+  if (ss.mrhs_tx.bytes < tx_bytes) ss.mrhs_tx.alloc(tx_bytes);
   int sms = 0;
   RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
   MrhsCtx a{};
@@ -701,12 +900,38 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
     RQ_CUDA(cudaMemsetAsync(dbg.p, 0, bytes, s));
     a.dbg = dbg.as<long long>();
   }
-  const int64_t nt = p.n_tile_units;
   const bool do_tiles = phases & 1u, do_top = phases & 2u;
+  // top trees: one launch per height level (upward: leaves first; downward: root level first)
+  auto top_levels = [&]() {
+    if (!all) throw Error(RQ_ERR_VALUE, "body ranges are not supported by the multi-RHS top sweep");
+    MTopCtx tc{};
+    tc.top = p.mtop.as<MTop>();
+    tc.n_cg = (k + 31) / 32;
+    tc.rec = p.rec.as<double>();
+    tc.bead_off = p.bead_off_d.as<int64_t>();
+    tc.in = in;
+    tc.out = out;
+    tc.tx = ss.mrhs_tx.as<double>();
+    tc.scr = ss.mrhs_scratch.as<double>();
+    tc.K = k;
+    tc.op = op;
+    const int64_t nl = (int64_t)p.h_mtop_level.size() - 1;
+    for (int64_t i = 0; i < nl; i++) {
+      const int64_t l = up ? i : nl - 1 - i;
+      tc.q0 = p.h_mtop_level[l];
+      tc.n = p.h_mtop_level[l + 1] - tc.q0;
+      const int64_t threads = tc.n * tc.n_cg * 32;
+      if (up) k_mrhs_top<true><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(tc);
+      else k_mrhs_top<false><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(tc);
+    }
+  };
+  const int64_t nt = p.n_tile_units;
   if (up) {
     if (do_tiles) launch(t0, t1, p.mrhs_depth_tile, true);
     if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top, false);
+    if (do_top && p.n_mtop) top_levels();
   } else {
+    if (do_top && p.n_mtop) top_levels();
     if (do_top) launch(nt + q0, nt + q1, p.mrhs_depth_top, false);
     if (do_tiles) launch(t0, t1, p.mrhs_depth_tile, true);
   }

@@ -215,7 +215,7 @@ struct Plan {
   // exchange slots, the multi-RHS exchange block and the top-tree arrival counters are
   // owned per stream.
   struct StreamState {
-    DBuf scratch, mrhs_scratch, top_cnt;
+    DBuf scratch, mrhs_scratch, mrhs_tx, top_cnt;  // mrhs_tx: multi-RHS top exchange [top][6][k]
     DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
     DBuf res_tmp, roots;      // Q / Q^T: residues in the private layout and the 6 root rows per body
     DBuf in_al;               // 16-byte aligned copy of a misaligned input
@@ -232,7 +232,9 @@ struct Plan {
   mutable int64_t mrhs_entries = 0, n_tile_units = 0, n_top_units = 0;
   mutable int64_t mrhs_tile_bytes = 0, mrhs_top_bytes = 0;  // entry header + record bytes per column group
   mutable int mrhs_depth_tile = 1, mrhs_depth_top = 1;
-  mutable DBuf mrhs_units, mrhs_prog;
+  mutable DBuf mrhs_units, mrhs_prog, mtop;  // mtop: multi-RHS top nodes by height
+  mutable int64_t n_mtop = 0;
+  mutable std::vector<int64_t> h_mtop_level;
   mutable std::vector<int64_t> h_tile_unit_first, h_top_unit_first;
   // private residue layout: body j's residues start at res_base[j] = sum_{i<j} max(0, 3 n_i - 6)
   // (the Q~ layout when every body has n >= 2; Q / Q^T go through it plus 6 root rows per body)

@@ -520,8 +520,9 @@ def test_zf_batch_independent(rq):
 
 
 def test_multi_rhs_policy(rq, monkeypatch):
-    """Blocks on one big body go column by column (its serial top unit would dominate);
-    both policies give the same block to rounding."""
+    """Blocks on one big body run the column-parallel kernels too (its top tree sweeps
+    level-parallel, a warp per top node and column group); the column loop gives the same
+    block to rounding."""
     from paper_1708_08427_b200 import _lib as L
     from paper_1708_08427_b200.workloads import sphere_shell
 
@@ -530,12 +531,16 @@ def test_multi_rhs_policy(rq, monkeypatch):
     k = 12
     V = np.random.default_rng(3).normal(size=(3 << 17, k))
     lib = L.lib()
-    assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) >= 2 * k  # column loop
+    assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) < 2 * k  # multi-RHS kernels
     auto = op.apply("qtilde_v", V)
+    monkeypatch.setenv("RQ_MRHS", "never")
+    assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) >= 2 * k  # column loop
+    loop = op.apply("qtilde_v", V)
+    assert np.abs(auto - loop).max() <= 1e-12 * np.abs(auto).max()
+    G = np.random.default_rng(4).normal(size=((3 << 17) - 6, k))
+    a2 = op.apply("qtilde_tv", G)
     monkeypatch.setenv("RQ_MRHS", "always")
-    assert lib.rq_launches_per_apply(op.plan.handle, L.OP_QTILDE_V, k) < 2 * k
-    forced = op.apply("qtilde_v", V)
-    assert np.abs(auto - forced).max() <= 1e-12 * np.abs(auto).max()
+    assert np.abs(op.apply("qtilde_tv", G) - a2).max() <= 1e-12 * np.abs(a2).max()
 
 
 def test_cuda_graph_capture(rq):
