@@ -244,7 +244,7 @@ struct Plan {
   int64_t wave_streams = 0, wave_steps = 0, wave_blob_bytes = 0, wave_nodes = 0;
   int64_t wave_up_bytes = 0, wave_down_bytes = 0;  // bytes one upward / downward sweep streams
   int64_t wave_stage_bytes = 0, wave_rounds = 1;
-  int wave_mslots = 0, wave_pf = 0, wave_nst = 2;  // L2 prefetch distance (steps), TMA stages (fixed 2)
+  int wave_mslots = 0, wave_nst = 2;  // TMA stages (fixed 2: the headers locate the block two steps ahead)
   WaveCaps wave_caps;
   DBuf wave_desc;                  // StepDesc [wave_steps]
   DBuf wave_stream_first;          // int64 [wave_streams + 1]

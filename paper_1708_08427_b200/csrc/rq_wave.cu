@@ -17,10 +17,11 @@
 // which is optimal for interval graphs, so M = the stream's peak live count.
 //
 // Kernel k_wave<UP> (128 threads, one CTA per stream): per step, one TMA bulk
-// copy of the block (issued two steps ahead into a 2-stage ring, L2-prefetched
-// pf steps ahead), gathers for step +2 (cp.async into a 3-region ring), the
-// case-uniform node pass (warp 0 GENERAL, warp 1 RIGID_BEAD, warps 2-3
-// BEAD_BEAD), one CTA barrier.  Outputs go straight to global memory
+// copy of the block (issued two steps ahead into a 2-stage ring; each block's
+// header locates the block two steps further, so the producer never waits on a
+// global load), gathers for step +2 (cp.async into a 3-region ring), the
+// case-uniform node pass (GENERAL, RIGID_BEAD and BEAD_BEAD nodes each padded
+// to whole warps), one CTA barrier.  Outputs go straight to global memory
 // (residues upward, bead velocities downward); tile-root 6-vectors go to the
 // exchange slots the top-tree kernels read.  No tensor cores: HBM-bound sweep
 // of tiny fp64 orthogonal transforms.
@@ -329,9 +330,43 @@ __global__ void k_wv_descs(const StepCnt *sc, const int64_t *off, int64_t ns, St
   D.pad0 = 0;
   D.pad1 = 0;
   d[s] = D;
+}
+
+// the two direction headers of every block (after all descriptors exist)
+__global__ void k_wv_headers(const StepDesc *d, int64_t ns, uint8_t *blob) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  const StepDesc D = d[s];
   const WaveSec S = wave_sections(D);
-  *reinterpret_cast<StepDesc *>(blob + off[s]) = D;
-  *reinterpret_cast<StepDesc *>(blob + off[s] + S.uhdr) = D;
+  uint8_t *B = blob + ((int64_t)D.off16 << 4);
+  DirHdr u{}, w{};
+  u.nG = w.nG = D.nG;
+  u.nR = w.nR = D.nR;
+  u.nB = w.nB = D.nB;
+  // upward copy [uhdr, end): header | records | metadata | bead list
+  u.n_list = D.n_ug;
+  u.o_rec = (uint16_t)(S.rec - S.uhdr);
+  u.o_meta = (uint16_t)(S.um - S.uhdr);
+  u.o_list = (uint16_t)(S.ug - S.uhdr);
+  u.next_off16 = 0xffffffffu;
+  if (s + 2 < ns) {
+    const WaveSec N = wave_sections(d[s + 2]);
+    u.next_off16 = (uint32_t)(((((int64_t)d[s + 2].off16) << 4) + N.uhdr) >> 4);
+    u.next_bytes = (uint16_t)(N.end - N.uhdr);
+  }
+  // downward copy [0, um): header | gather list | metadata | (upward header) | records
+  w.n_list = D.n_dg;
+  w.o_list = (uint16_t)S.dg;
+  w.o_meta = (uint16_t)S.dm;
+  w.o_rec = (uint16_t)S.rec;
+  w.next_off16 = 0xffffffffu;
+  if (s >= 2) {
+    const WaveSec N = wave_sections(d[s - 2]);
+    w.next_off16 = d[s - 2].off16;
+    w.next_bytes = (uint16_t)N.um;
+  }
+  *reinterpret_cast<DirHdr *>(B) = w;
+  *reinterpret_cast<DirHdr *>(B + S.uhdr) = u;
 }
 
 // one CTA (one thread) per stream: interval colouring of the node 6-vectors (lowest free
@@ -504,7 +539,7 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
     const StepDesc Dd = w.desc[gs + 2];
     const int64_t pfd = w.sfirst_sorted[gs];
     int di = (int)(w.dscan[p] - w.dscan[pfd]);
-    WaveGather *DG = reinterpret_cast<WaveGather *>(w.blob + ((int64_t)Dd.off16 << 4) + 16);
+    WaveGather *DG = reinterpret_cast<WaveGather *>(w.blob + ((int64_t)Dd.off16 << 4) + wave_sections(Dd).dg);
     if (rr) {
       WaveGather e;
       e.src = (uint32_t)row;
@@ -538,7 +573,6 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
     if (sscanf(e, "%d,%d,%d,%d", &g, &r, &b, &rm) == 4) { caps.g = g; caps.r = r; caps.b = b; caps.rm = rm; }
   }
   p.wave_caps = caps;
-  if (const char *e = getenv("RQ_WAVE_PF")) p.wave_pf = std::max(0, std::min(32, atoi(e)));
   NodeArrays A{in.node_off, in.bead_off, in.rec_off, in.res_base, in.node_body, in.start, in.stop, in.left,
                in.right,    in.parent,   in.height,  in.res_off,  in.perm,      in.slot_scan, in.flags};
   const int64_t NN = p.NN;
@@ -718,6 +752,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   p.wave_desc.alloc(NS * sizeof(StepDesc));
   k_wv_descs<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), off.as<int64_t>(), NS, p.wave_desc.as<StepDesc>(),
                                       p.wave_blob.as<uint8_t>());
+  k_wv_headers<<<nblk(NS), NT, 0, s>>>(p.wave_desc.as<StepDesc>(), NS, p.wave_blob.as<uint8_t>());
   tm.mark("wave counts");
   // slots
   DBuf slot_of, node_first, msl;
@@ -816,9 +851,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, unsigned parity) {
         : "r"(addr), "r"(parity)
         : "memory");
   }
-}
-__device__ __forceinline__ void prefetch_l2(const void *ptr, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void cp8(uint32_t dst, const void *src) {
@@ -938,7 +970,6 @@ struct WaveCtx {
   double *scratch;
   double *roots;
   uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: NST stages | M | 3 gather regions (vreg doubles each)
-  int pf;                                // L2 prefetch distance (steps)
   int64_t in_len;                        // doubles in `in` (16-byte windows never read past it)
 };
 
@@ -964,24 +995,16 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     if (UP) { off = S.uhdr; bytes = S.end - S.uhdr; }
     else { off = 0; bytes = S.um; }
   };
-  StepDesc dn{};
   if (tid == PROD) {
     for (int i = 0; i < NST; i++) mbar_init(bar_u + 8 * i, 1);
     fence_mbar_init();
-    for (int t = 0; t < NST && t < n; t++) {
+    for (int t = 0; t < NST && t < n; t++) {  // the first blocks; later ones come from the headers
       const StepDesc d = a.steps[blk(t)];
       uint32_t off, bytes;
       span(d, off, bytes);
       mbar_expect_tx(bar_u + 8 * t, bytes);
       bulk_g2s(sm_u + t * a.stage_bytes, a.blob + ((int64_t)d.off16 << 4) + off, bytes, bar_u + 8 * t);
     }
-    for (int t = NST; t < n && t < NST + a.pf; t++) {
-      const StepDesc d = a.steps[blk(t)];
-      uint32_t off, bytes;
-      span(d, off, bytes);
-      prefetch_l2(a.blob + ((int64_t)d.off16 << 4) + off, bytes);
-    }
-    if (n > NST) dn = a.steps[blk(NST)];
   }
   __syncthreads();
   pdl_wait();  // vectors and exchange slots may come from the previous kernel
@@ -991,15 +1014,14 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     mbar_wait(bar_u + 8 * st, (phase >> st) & 1u);
     phase ^= 1u << st;
     const unsigned char *B = smem + st * a.stage_bytes;
-    const StepDesc d = *reinterpret_cast<const StepDesc *>(B);
-    const WaveSec S = wave_sections(d);
+    const DirHdr h = *reinterpret_cast<const DirHdr *>(B);
     // gathers for step t + 2 (into region (t + 2) % 3): 16-byte L2 copies (cp.async.cg)
     {
       const int rg = (t + 2) % 3;
       const uint32_t vg = vb_u + 8u * (uint32_t)(rg * a.vreg);
       if (UP) {
-        const uint32_t *ug = reinterpret_cast<const uint32_t *>(B + (S.ug - S.uhdr));
-        for (int i = tid; i < d.n_ug; i += 128) {
+        const uint32_t *ug = reinterpret_cast<const uint32_t *>(B + h.o_list);
+        for (int i = tid; i < h.n_list; i += 128) {
           const int64_t b = ug[i];
           const int64_t w0 = 3 * b - (b & 1);  // even: 16-byte aligned window of 4 doubles
           const uint32_t dst = vg + 32u * (uint32_t)i;
@@ -1014,8 +1036,8 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           }
         }
       } else {
-        const WaveGather *dg = reinterpret_cast<const WaveGather *>(B + S.dg);
-        for (int i = tid; i < d.n_dg; i += 128) {
+        const WaveGather *dg = reinterpret_cast<const WaveGather *>(B + h.o_list);
+        for (int i = tid; i < h.n_list; i += 128) {
           const WaveGather e = dg[i];
           const uint32_t dst = vg + 8u * e.dst;
           if (e.kind == WG_RES3 || e.kind == WG_RES6) {
@@ -1046,13 +1068,13 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     // nodes of step t (gather region t % 3)
     {
       const double *V = Vb + (t % 3) * a.vreg;
-      const int nG = d.nG, nR = d.nR, nB = d.nB;
+      const int nG = h.nG, nR = h.nR, nB = h.nB;
       const int gG = (nG + 31) & ~31, gR = (nR + 31) & ~31;
       const int tot = gG + gR + nB;
-      const double *R = reinterpret_cast<const double *>(B + (UP ? 16 : S.rec));
+      const double *R = reinterpret_cast<const double *>(B + h.o_rec);
       const int oR = rec_size(GENERAL) * nG, oB = oR + rec_size(RIGID_BEAD) * nR;
       if (UP) {
-        const WaveUpMeta *UM = reinterpret_cast<const WaveUpMeta *>(B + (S.um - S.uhdr));
+        const WaveUpMeta *UM = reinterpret_cast<const WaveUpMeta *>(B + h.o_meta);
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
             if (q < nG) wv_up<GENERAL>(R + q * rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
@@ -1066,7 +1088,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           }
         }
       } else {
-        const WaveDnMeta *DM = reinterpret_cast<const WaveDnMeta *>(B + S.dm);
+        const WaveDnMeta *DM = reinterpret_cast<const WaveDnMeta *>(B + h.o_meta);
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
             if (q < nG) wv_down<GENERAL>(R + q * rec_size(GENERAL), DM + q, M, V, a.out);
@@ -1082,18 +1104,9 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     }
     cp_wait<1>();  // this thread's gathers for step t + 1
     __syncthreads();
-    if (tid == PROD && t + NST < n) {  // stage st is free: block t + NST
-      uint32_t off, bytes;
-      span(dn, off, bytes);
-      mbar_expect_tx(bar_u + 8 * st, bytes);
-      bulk_g2s(sm_u + st * a.stage_bytes, a.blob + ((int64_t)dn.off16 << 4) + off, bytes, bar_u + 8 * st);
-      if (a.pf && t + NST + a.pf < n) {
-        const StepDesc d2 = a.steps[blk(t + NST + a.pf)];
-        uint32_t o2, b2;
-        span(d2, o2, b2);
-        prefetch_l2(a.blob + ((int64_t)d2.off16 << 4) + o2, b2);
-      }
-      if (t + NST + 1 < n) dn = a.steps[blk(t + NST + 1)];
+    if (tid == PROD && t + NST < n) {  // stage st is free: block t + NST (located by this block's header)
+      mbar_expect_tx(bar_u + 8 * st, h.next_bytes);
+      bulk_g2s(sm_u + st * a.stage_bytes, a.blob + ((int64_t)h.next_off16 << 4), h.next_bytes, bar_u + 8 * st);
     }
   }
 }
@@ -1137,7 +1150,6 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
   a.roots = roots;
   a.stage_bytes = (uint32_t)p.wave_stage_bytes;
   const size_t sm = wave_smem(p, &a.o_m, &a.o_v, &a.vreg);
-  a.pf = p.wave_pf;
   a.in_len = up ? 3 * p.N : p.res_base[p.m];
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.wave_streams);

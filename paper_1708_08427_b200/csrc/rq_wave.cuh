@@ -18,7 +18,9 @@
 //   \______________ DOWN copy ______________/
 //                           \_____________ UP copy ______________/
 //
-//   HDR    : the StepDesc (16 B, twice so each copy starts with it)
+//   HDR    : a DirHdr (32 B) per direction: counts, section offsets within that
+//            direction's copy, and where the block two steps further in that
+//            direction lies (the producer issues its TMA from it: no global loads)
 //   REC    : compact records, GEN | RB | BB groups (AoS, rec_size doubles)
 //   UM / DM: per-node metadata of the upward / downward sweep (16 B each)
 //   UG     : upward gather list of step s+2: global bead index per bead (4 B)
@@ -76,8 +78,25 @@ constexpr uint16_t WF_BODY_ROOT = 1u << 7;  // the body root (output to / input 
 
 __host__ __device__ inline uint32_t al16u(uint32_t x) { return (x + 15u) & ~15u; }
 
+// per-direction block header (the first 32 bytes of each direction's copy)
+struct DirHdr {
+  uint8_t nG, nR, nB, pad0;
+  uint16_t n_list;      // gather entries (UP: beads of step s+2; DOWN: nodes of step s-2)
+  uint16_t o_list;      // byte offsets inside this direction's copy
+  uint16_t o_meta;
+  uint16_t o_rec;
+  uint16_t next_bytes;  // copy size of the block two steps further in this direction
+  uint16_t pad1;
+  uint32_t next_off16;  // its byte offset / 16 in the blob
+  uint32_t pad2[3];
+};
+static_assert(sizeof(DirHdr) == 32, "DirHdr is 32 bytes");
+
 struct WaveSec {  // byte offsets inside a block
   uint32_t dg, dm, uhdr, rec, um, ug, end;
+  // each direction's copy: [up0, end) upward, [0, dn_end) downward
+  __host__ __device__ uint32_t up0() const { return uhdr; }
+  __host__ __device__ uint32_t dn_end() const { return um; }
 };
 __host__ __device__ inline uint32_t wave_rec_bytes(uint32_t nG, uint32_t nR, uint32_t nB) {
   return 8u * (rec_size(GENERAL) * nG + rec_size(RIGID_BEAD) * nR + rec_size(BEAD_BEAD) * nB);
@@ -86,10 +105,10 @@ __host__ __device__ inline WaveSec wave_sections(uint32_t nG, uint32_t nR, uint3
                                                  uint32_t n_dg) {
   const uint32_t n = nG + nR + nB;
   WaveSec s;
-  s.dg = 16u;
+  s.dg = 32u;
   s.dm = s.dg + al16u(8u * n_dg);
   s.uhdr = s.dm + 16u * n;
-  s.rec = s.uhdr + 16u;
+  s.rec = s.uhdr + 32u;
   s.um = s.rec + wave_rec_bytes(nG, nR, nB);
   s.ug = s.um + 16u * n;
   s.end = s.ug + al16u(4u * n_ug);
@@ -101,8 +120,8 @@ __host__ __device__ inline WaveSec wave_sections(const StepDesc &d) {
 
 // per-step capacities (the scheduler never exceeds them; they size shared memory)
 struct WaveCaps {
-  int g = 32, r = 32, b = 64;   // nodes per case
-  int rm = 10240;               // record + one-direction metadata bytes
+  int g = 48, r = 48, b = 64;   // nodes per case (swept on config 2)
+  int rm = 12288;               // record + one-direction metadata bytes
   int beads = 128;              // upward gathers (beads) per step
   int vd = 512;                 // downward gather-region doubles per step
   int dg = 96;                  // downward gather entries per step
