@@ -12,7 +12,23 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Debug builds (make check -> librigidq_b200_check.so, -DRQ_DEBUG_CHECKS=1): device-side
+// bounds / staging-phase asserts in the hot kernels (compute-sanitizer is unavailable on the
+// GPU pool); a failed check prints its site and traps.
+#ifndef RQ_DEBUG_CHECKS
+#define RQ_DEBUG_CHECKS 0
+#endif
+#define RQ_CHECK(cond, what)                                                                        \
+  do {                                                                                              \
+    if (RQ_DEBUG_CHECKS && !(cond)) {                                                               \
+      printf("rq check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,          \
+             (int)blockIdx.x, (int)threadIdx.x);                                                    \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
 
 namespace rq {
 

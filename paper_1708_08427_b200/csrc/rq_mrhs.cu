@@ -527,7 +527,9 @@ __device__ __forceinline__ void run_unit(const MrhsCtx &a, const UnitDesc &U, do
   };
   for (int t = 0; t < n; t += 2) {  // ping-pong input registers (no copies)
     step(t, gA, gB);
+    RQ_CHECK(sp >= 0 && sp <= a.depth, "multi-RHS stack depth");
     if (t + 1 < n) step(t + 1, gB, gA);
+    RQ_CHECK(sp >= 0 && sp <= a.depth, "multi-RHS stack depth");
   }
   cp_wait_m<0>();
   if (UP && (ACT || act)) {  // unit root

@@ -340,6 +340,7 @@ __global__ void k_wv_headers(const StepDesc *d, int64_t ns, uint8_t *blob) {
   const WaveSec S = wave_sections(D);
   uint8_t *B = blob + ((int64_t)D.off16 << 4);
   DirHdr u{}, w{};
+  u.step = w.step = (uint32_t)s;
   u.nG = w.nG = D.nG;
   u.nR = w.nR = D.nR;
   u.nB = w.nB = D.nB;
@@ -971,6 +972,7 @@ struct WaveCtx {
   double *roots;
   uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: NST stages | M | 3 gather regions (vreg doubles each)
   int64_t in_len;                        // doubles in `in` (16-byte windows never read past it)
+  int mslots;                            // node-vector slots (debug checks)
 };
 
 #ifndef RQ_WAVE_MIN_BLOCKS
@@ -1015,6 +1017,8 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     phase ^= 1u << st;
     const unsigned char *B = smem + st * a.stage_bytes;
     const DirHdr h = *reinterpret_cast<const DirHdr *>(B);
+    RQ_CHECK(h.step == (uint32_t)blk(t), "staged block is the expected step (TMA landed, phase right)");
+    RQ_CHECK(h.o_list <= a.stage_bytes && h.o_meta <= a.stage_bytes && h.o_rec <= a.stage_bytes, "sections");
     // gathers for step t + 2 (into region (t + 2) % 3): 16-byte L2 copies (cp.async.cg)
     {
       const int rg = (t + 2) % 3;
@@ -1024,6 +1028,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
         for (int i = tid; i < h.n_list; i += 128) {
           const int64_t b = ug[i];
           const int64_t w0 = 3 * b - (b & 1);  // even: 16-byte aligned window of 4 doubles
+          RQ_CHECK(4 * i + 4 <= (int)a.vreg && 3 * b + 3 <= a.in_len, "upward gather bounds");
           const uint32_t dst = vg + 32u * (uint32_t)i;
           if (w0 + 4 <= a.in_len) {
             cp16(dst, a.in + w0);
@@ -1040,6 +1045,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
         for (int i = tid; i < h.n_list; i += 128) {
           const WaveGather e = dg[i];
           const uint32_t dst = vg + 8u * e.dst;
+          RQ_CHECK((e.dst & 1) == 0 && e.dst + 8 <= a.vreg, "downward gather bounds");
           if (e.kind == WG_RES3 || e.kind == WG_RES6) {
             const int64_t row = e.src;
             const int rr = e.kind == WG_RES3 ? 3 : 6;
@@ -1075,6 +1081,15 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       const int oR = rec_size(GENERAL) * nG, oB = oR + rec_size(RIGID_BEAD) * nR;
       if (UP) {
         const WaveUpMeta *UM = reinterpret_cast<const WaveUpMeta *>(B + h.o_meta);
+        if (RQ_DEBUG_CHECKS)
+          for (int q = tid; q < nG + nR + nB; q += 128) {
+            const WaveUpMeta md = UM[q];
+            const int cs = q < nG ? GENERAL : (q < nG + nR ? RIGID_BEAD : BEAD_BEAD);
+            RQ_CHECK(flag_case(md.flags) == cs, "upward meta case");
+            RQ_CHECK(cs == BEAD_BEAD ? md.x + 3 <= (int)a.vreg : md.x < a.mslots, "upward x source");
+            RQ_CHECK(cs != GENERAL ? md.y + 3 <= (int)a.vreg : md.y < a.mslots, "upward y source");
+            RQ_CHECK((md.flags & (WF_TILE_ROOT | WF_BODY_ROOT)) || md.self < a.mslots, "upward output slot");
+          }
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
             if (q < nG) wv_up<GENERAL>(R + q * rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
@@ -1089,6 +1104,17 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
         }
       } else {
         const WaveDnMeta *DM = reinterpret_cast<const WaveDnMeta *>(B + h.o_meta);
+        if (RQ_DEBUG_CHECKS)
+          for (int q = tid; q < nG + nR + nB; q += 128) {
+            const WaveDnMeta md = DM[q];
+            const int cs = q < nG ? GENERAL : (q < nG + nR ? RIGID_BEAD : BEAD_BEAD);
+            RQ_CHECK(flag_case(md.flags) == cs, "downward meta case");
+            RQ_CHECK(cs == BEAD_BEAD || md.x < (uint32_t)a.mslots, "downward x slot");
+            RQ_CHECK(cs != GENERAL || md.y < (uint32_t)a.mslots, "downward y slot");
+            RQ_CHECK((md.flags & (WF_TILE_ROOT | WF_BODY_ROOT)) ? md.self + 6 <= a.vreg : md.self < a.mslots,
+                     "downward input");
+            RQ_CHECK(md.vres + 6 <= a.vreg, "downward residues");
+          }
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
             if (q < nG) wv_down<GENERAL>(R + q * rec_size(GENERAL), DM + q, M, V, a.out);
@@ -1105,6 +1131,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
     cp_wait<1>();  // this thread's gathers for step t + 1
     __syncthreads();
     if (tid == PROD && t + NST < n) {  // stage st is free: block t + NST (located by this block's header)
+      RQ_CHECK(h.next_off16 != 0xffffffffu && h.next_bytes <= a.stage_bytes, "next block location");
       mbar_expect_tx(bar_u + 8 * st, h.next_bytes);
       bulk_g2s(sm_u + st * a.stage_bytes, a.blob + ((int64_t)h.next_off16 << 4), h.next_bytes, bar_u + 8 * st);
     }
@@ -1151,6 +1178,7 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
   a.stage_bytes = (uint32_t)p.wave_stage_bytes;
   const size_t sm = wave_smem(p, &a.o_m, &a.o_v, &a.vreg);
   a.in_len = up ? 3 * p.N : p.res_base[p.m];
+  a.mslots = p.wave_mslots;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.wave_streams);
   cfg.blockDim = dim3(128);

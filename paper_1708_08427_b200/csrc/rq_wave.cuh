@@ -88,7 +88,8 @@ struct DirHdr {
   uint16_t next_bytes;  // copy size of the block two steps further in this direction
   uint16_t pad1;
   uint32_t next_off16;  // its byte offset / 16 in the blob
-  uint32_t pad2[3];
+  uint32_t step;        // global step index of this block (staging-phase checks)
+  uint32_t pad2[2];
 };
 static_assert(sizeof(DirHdr) == 32, "DirHdr is 32 bytes");
 
