@@ -219,6 +219,8 @@ struct Plan {
     DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
     DBuf res_tmp, roots;      // Q / Q^T: residues in the private layout and the 6 root rows per body
     DBuf in_al;               // 16-byte aligned copy of a misaligned input
+    DBuf round_ctr;           // wave round-window arrival counters [2][rounds] (up, down)
+    uint32_t wave_epoch[2] = {0, 0};
     DBuf zpart;               // Zf per-segment partial sums
   };
   mutable std::mutex state_mu;
@@ -244,6 +246,7 @@ struct Plan {
   int64_t wave_streams = 0, wave_steps = 0, wave_blob_bytes = 0, wave_nodes = 0;
   int64_t wave_up_bytes = 0, wave_down_bytes = 0;  // bytes one upward / downward sweep streams
   int64_t wave_stage_bytes = 0, wave_rounds = 1;
+  int wave_window = 0, sms = 0;         // run-time round window (rounds); SM count
   int wave_mslots = 0, wave_nst = 2;  // TMA stages (fixed 2: the headers locate the block two steps ahead)
   WaveCaps wave_caps;
   DBuf wave_desc;                  // StepDesc [wave_steps]
@@ -282,7 +285,7 @@ void wave_prepare(const Plan &p);
 // tile part of one upward / downward sweep over all bodies (rq_wave.cu); residues in the
 // private layout, body-root vectors to / from `roots` (nullptr: dropped / zero)
 void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots,
-              cudaStream_t s);
+              cudaStream_t s, uint32_t *round_ctr = nullptr, uint32_t epoch = 0);
 // bodies [j0, j1) of a plan (all work lists are in body order)
 struct BodyRange {
   int64_t j0 = 0, j1 = -1;  // j1 < 0: all bodies

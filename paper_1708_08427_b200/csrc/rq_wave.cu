@@ -276,9 +276,23 @@ __global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, co
   vals[g] = (int32_t)g;
 }
 
-__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int32_t *tile_stream) {
+__global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int64_t nt, int64_t R, int32_t *tile_stream,
+                                 int32_t *tile_round) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < nt) tile_stream[order[i]] = (int32_t)(key[i] / R);
+  if (i >= nt) return;
+  tile_stream[order[i]] = (int32_t)(key[i] / R);
+  tile_round[order[i]] = (int32_t)(key[i] % R);
+}
+
+// per step and direction: the round of the tiles that start there (upward: entry row;
+// downward: last row), for the run-time round window (k_wave throttles CTAs that run ahead)
+__global__ void k_wv_round_marks(int64_t nt, const int64_t *trows, const int32_t *tile_stream, const int32_t *tile_round,
+                                 const int32_t *e_tile, const int64_t *step_first, int *up_mark, int *dn_mark) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt || trows[t] == 0) return;
+  const int64_t base = step_first[tile_stream[t]] + 2 + e_tile[t];
+  atomicMax(&up_mark[base], tile_round[t]);
+  atomicMin(&dn_mark[base + trows[t] - 1], tile_round[t]);
 }
 
 struct StepCnt {
@@ -333,7 +347,7 @@ __global__ void k_wv_descs(const StepCnt *sc, const int64_t *off, int64_t ns, St
 }
 
 // the two direction headers of every block (after all descriptors exist)
-__global__ void k_wv_headers(const StepDesc *d, int64_t ns, uint8_t *blob) {
+__global__ void k_wv_headers(const StepDesc *d, int64_t ns, uint8_t *blob, const int *up_mark, const int *dn_mark) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= ns) return;
   const StepDesc D = d[s];
@@ -341,6 +355,8 @@ __global__ void k_wv_headers(const StepDesc *d, int64_t ns, uint8_t *blob) {
   uint8_t *B = blob + ((int64_t)D.off16 << 4);
   DirHdr u{}, w{};
   u.step = w.step = (uint32_t)s;
+  u.round = up_mark[s] >= 0 ? (uint32_t)up_mark[s] : ~0u;
+  w.round = dn_mark[s] != INT32_MAX ? (uint32_t)dn_mark[s] : ~0u;
   u.nG = w.nG = D.nG;
   u.nR = w.nR = D.nR;
   u.nB = w.nB = D.nB;
@@ -593,6 +609,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   // streams: one per resident CTA
   int sms = 0;
   RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+  p.sms = sms;
   int per_sm = 4;
   if (const char *e = getenv("RQ_WAVE_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, atoi(e)));
   int64_t G = (int64_t)sms * per_sm;
@@ -667,7 +684,10 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
       if (h[c] < 0) h[c] = h[c + 1];
     RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
   }
-  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, tile_stream.as<int32_t>());
+  DBuf tile_round;
+  tile_round.alloc(nt * 4);
+  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, tile_stream.as<int32_t>(),
+                                            tile_round.as<int32_t>());
   k_wv_gather64<<<nblk(nt), NT, 0, s>>>(trows.as<int64_t>(), order.as<int32_t>(), nt, th_sorted.as<int64_t>());
   k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
   ex_scan(th_sorted.as<int64_t>(), lv_scan.as<int64_t>(), nt, s);
@@ -753,7 +773,28 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   p.wave_desc.alloc(NS * sizeof(StepDesc));
   k_wv_descs<<<nblk(NS), NT, 0, s>>>(sc.as<StepCnt>(), off.as<int64_t>(), NS, p.wave_desc.as<StepDesc>(),
                                       p.wave_blob.as<uint8_t>());
-  k_wv_headers<<<nblk(NS), NT, 0, s>>>(p.wave_desc.as<StepDesc>(), NS, p.wave_blob.as<uint8_t>());
+  {
+    DBuf marks;
+    marks.alloc(NS * 8);
+    std::vector<int> init(2 * NS);
+    for (int64_t i = 0; i < NS; i++) { init[i] = -1; init[NS + i] = INT32_MAX; }
+    RQ_CUDA(cudaMemcpyAsync(marks.p, init.data(), NS * 8, cudaMemcpyHostToDevice, s));
+    k_wv_round_marks<<<nblk(nt), NT, 0, s>>>(nt, trows.as<int64_t>(), tile_stream.as<int32_t>(), tile_round.as<int32_t>(),
+                                              e_tile.as<int32_t>(), step_first.as<int64_t>(), marks.as<int>(),
+                                              marks.as<int>() + NS);
+    k_wv_headers<<<nblk(NS), NT, 0, s>>>(p.wave_desc.as<StepDesc>(), NS, p.wave_blob.as<uint8_t>(), marks.as<int>(),
+                                          marks.as<int>() + NS);
+    RQ_CUDA(cudaStreamSynchronize(s));
+  }
+  // run-time round window: CTAs more than `window` rounds ahead of the slowest wait (a
+  // performance hint only: bounded waits, never a data dependency)
+  {
+    // (long runs only: over a few dozen rounds the streams do not drift apart; config 2 with 24
+    // rounds runs 1% faster without it, config 4's 1261 rounds 26% faster with it)
+    const double round_bytes = 48.0 * (double)p.N / (double)R;
+    p.wave_window = R < 64 ? 0 : (int)std::max<int64_t>(8, std::min<int64_t>(R, (int64_t)(40e6 / std::max(round_bytes, 1.0))));
+    if (const char *e = getenv("RQ_WAVE_WINDOW")) p.wave_window = std::max(0, atoi(e));
+  }
   tm.mark("wave counts");
   // slots
   DBuf slot_of, node_first, msl;
@@ -973,6 +1014,10 @@ struct WaveCtx {
   uint32_t stage_bytes, o_m, o_v, vreg;  // shared memory: NST stages | M | 3 gather regions (vreg doubles each)
   int64_t in_len;                        // doubles in `in` (16-byte windows never read past it)
   int mslots;                            // node-vector slots (debug checks)
+  // run-time round window (nullptr: off): per-round arrival counters of this direction
+  uint32_t *round_ctr;
+  uint32_t round_target;                 // arrivals per round when every CTA has passed it
+  int rounds, window;
 };
 
 #ifndef RQ_WAVE_MIN_BLOCKS
@@ -1012,11 +1057,29 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
   pdl_wait();  // vectors and exchange slots may come from the previous kernel
   unsigned phase = 0;
   int st = 0;
+  int cur_round = UP ? -1 : a.rounds;  // rounds this CTA has entered (arrivals counted)
   for (int t = 0; t < n; t++, st = (st == NST - 1) ? 0 : st + 1) {
     mbar_wait(bar_u + 8 * st, (phase >> st) & 1u);
     phase ^= 1u << st;
     const unsigned char *B = smem + st * a.stage_bytes;
     const DirHdr h = *reinterpret_cast<const DirHdr *>(B);
+    // round window: entering round r, wait (bounded) until every CTA has entered round r -/+ window,
+    // so the vector rows in flight stay within a few L2-resident rounds; the other threads run on
+    // and the step's closing barrier holds the CTA
+    if (a.round_ctr && h.round != ~0u && (UP ? (int)h.round > cur_round : (int)h.round < cur_round)) {
+      const int r = (int)h.round;
+      if (tid == 0) {
+        if (UP) for (int q = cur_round + 1; q <= r; q++) atomicAdd(a.round_ctr + q, 1u);
+        else for (int q = cur_round - 1; q >= r; q--) atomicAdd(a.round_ctr + q, 1u);
+        const int lag = UP ? r - a.window : r + a.window;
+        if (lag >= 0 && lag < a.rounds) {
+          const long long t0 = clock64();
+          while ((int32_t)(*(volatile uint32_t *)(a.round_ctr + lag) - a.round_target) < 0 && clock64() - t0 < 400000)
+            __nanosleep(128);
+        }
+      }
+      cur_round = r;
+    }
     RQ_CHECK(h.step == (uint32_t)blk(t), "staged block is the expected step (TMA landed, phase right)");
     RQ_CHECK(h.o_list <= a.stage_bytes && h.o_meta <= a.stage_bytes && h.o_rec <= a.stage_bytes, "sections");
     // gathers for step t + 2 (into region (t + 2) % 3): 16-byte L2 copies (cp.async.cg)
@@ -1136,6 +1199,10 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       bulk_g2s(sm_u + st * a.stage_bytes, a.blob + ((int64_t)h.next_off16 << 4), h.next_bytes, bar_u + 8 * st);
     }
   }
+  if (a.round_ctr && tid == 0) {  // arrivals for the rounds this stream has no tile in
+    if (UP) for (int q = cur_round + 1; q < a.rounds; q++) atomicAdd(a.round_ctr + q, 1u);
+    else for (int q = cur_round - 1; q >= 0; q--) atomicAdd(a.round_ctr + q, 1u);
+  }
 }
 
 }  // namespace
@@ -1163,7 +1230,8 @@ void wave_prepare(const Plan &p) {
   p.wave_ready = true;
 }
 
-void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s) {
+void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s,
+              uint32_t *round_ctr, uint32_t epoch) {
   if (!p.wave_streams) return;
   if (reinterpret_cast<uintptr_t>(in) & 15) throw Error(RQ_ERR_VALUE, "wave sweep input must be 16-byte aligned");
   wave_prepare(p);
@@ -1179,6 +1247,14 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
   const size_t sm = wave_smem(p, &a.o_m, &a.o_v, &a.vreg);
   a.in_len = up ? 3 * p.N : p.res_base[p.m];
   a.mslots = p.wave_mslots;
+  a.rounds = (int)p.wave_rounds;
+  a.window = p.wave_window;
+  // the window waits assume every CTA of the grid is resident (bounded anyway)
+  if (round_ctr && p.wave_window > 0 && p.wave_window < p.wave_rounds &&
+      (int64_t)p.wave_ctas_per_sm * p.sms >= p.wave_streams) {
+    a.round_ctr = round_ctr;
+    a.round_target = (uint32_t)((int64_t)epoch * p.wave_streams);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.wave_streams);
   cfg.blockDim = dim3(128);

@@ -89,7 +89,8 @@ struct DirHdr {
   uint16_t pad1;
   uint32_t next_off16;  // its byte offset / 16 in the blob
   uint32_t step;        // global step index of this block (staging-phase checks)
-  uint32_t pad2[2];
+  uint32_t round;       // round whose first tile starts at this step in this direction, ~0u if none
+  uint32_t pad2;
 };
 static_assert(sizeof(DirHdr) == 32, "DirHdr is 32 bytes");
 
