@@ -76,6 +76,20 @@ def main():
     parsed["errors"] = errors
     json.dump(parsed, open(os.path.join(OUT, "parsed.json"), "w"), indent=1)
 
+    # text dumps of a tree (tree.py:167-172) and of the explicit Q (factor.py:351-359)
+    from rigidq.factor import generate_explicit_q
+    from rigidq.tree import build_tree, dump_tree
+
+    pos = np.random.default_rng(12).normal(size=(40, 3))
+    np.save(os.path.join(OUT, "dump_positions.npy"), pos)
+    tree = build_tree(R.BeadModel(pos))
+    buf = io.StringIO()
+    dump_tree(tree, buf)
+    open(os.path.join(OUT, "tree_dump.txt"), "w").write(buf.getvalue())
+    buf = io.StringIO()
+    generate_explicit_q(tree).dump(buf)
+    open(os.path.join(OUT, "hierq_dump.txt"), "w").write(buf.getvalue())
+
 
 if __name__ == "__main__":
     main()

@@ -112,3 +112,31 @@ def test_load_beads_gpu(parsed):
     rio.save_beads(rq.MultiBodyModel([rq.BeadModel(x) for x in b]), buf)
     back = rio.load_beads(io.StringIO(buf.getvalue()))
     assert np.array_equal(back.positions, np.concatenate(b))
+
+
+@pytest.mark.gpu
+def test_dump_tree_bytes_and_hierq_dump():
+    """dump_tree (tree.py:167-172) is byte-identical to the reference's (centroids are bit-exact);
+    HierQ.dump (factor.py:351-359) has the reference's structure line for line and its values
+    within 1e-12 (the explicit rows are generated on the GPU)."""
+    import io as _io
+
+    import paper_1708_08427_b200 as rq
+
+    pos = np.load(os.path.join(IO, "dump_positions.npy"))
+    tree = rq.build_tree(rq.BeadModel(pos))
+    buf = _io.StringIO()
+    rq.dump_tree(tree, buf)
+    assert buf.getvalue() == open(os.path.join(IO, "tree_dump.txt")).read()
+    buf = _io.StringIO()
+    rq.generate_explicit_q(tree).dump(buf)
+    ours = buf.getvalue().splitlines()
+    ref = open(os.path.join(IO, "hierq_dump.txt")).read().splitlines()
+    assert len(ours) == len(ref)
+    for a, b in zip(ours, ref):
+        xa, xb = a.split(), b.split()
+        assert len(xa) == len(xb)
+        if len(xb) == 3 or len(xb) == 2:  # header / block header lines: identical
+            assert a == b
+        else:
+            assert np.abs(np.array(xa, float) - np.array(xb, float)).max() < 1e-12
