@@ -579,7 +579,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   if (p.n_topblob && !p.top_attr_set) {
     for (const void *f2 : {(const void *)k_top2<true, 32>, (const void *)k_top2<false, 32>,
                            (const void *)k_top2<true, 128>, (const void *)k_top2<false, 128>})
-      RQ_CUDA(cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.max_topblob_smem));
+      ensure_smem_attr(f2, (size_t)p.max_topblob_smem);
     p.top_attr_set = true;
   }
   const bool do_sweep = (phases & 1u) && p.wave_streams > 0;

@@ -886,7 +886,7 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
     if (up && tiles) fn = mode == 0 ? k_mrhs<true, 0, 3> : (mode == 1 ? k_mrhs<true, 1, 3> : k_mrhs<true, 2, 3>);
     else if (up) fn = mode == 0 ? k_mrhs<true, 0, 4> : (mode == 1 ? k_mrhs<true, 1, 4> : k_mrhs<true, 2, 4>);
     else fn = mode == 0 ? k_mrhs<false, 0, 4> : (mode == 1 ? k_mrhs<false, 1, 4> : k_mrhs<false, 2, 4>);
-    RQ_CUDA(cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem_attr((const void *)fn, smem);
     int occ = 0;
     RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, MRHS_NT, smem));
     if (occ < 1) throw Error(RQ_ERR_CUDA, "multi-RHS kernel does not fit on an SM");

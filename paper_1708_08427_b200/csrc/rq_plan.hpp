@@ -133,7 +133,7 @@ struct Plan {
   int device = 0;
   int64_t m = 0, N = 0, NN = 0;    // bodies, beads, nodes
   int max_depth = 96;
-  int tile_leaves = 48;            // S: tiles are maximal subtrees with <= S beads
+  int tile_leaves = 128;           // S: tiles are maximal subtrees with <= S beads
   int tile_height = 0;             // tile height cut (0: none)
   std::vector<int64_t> bead_off;   // host copy, m+1
   int64_t n_case[4] = {0, 0, 0, 0};
@@ -279,6 +279,10 @@ struct WaveBuildIn {
   const uint8_t *flags;
   const double *rec;
 };
+// Raise kernel f's dynamic shared-memory limit on the current device to at least `bytes`.
+// The attribute is process-wide, so it only ever grows: a plan with a smaller footprint never
+// lowers it under a bigger plan's launches (other threads included).
+void ensure_smem_attr(const void *f, size_t bytes);
 void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s);
 size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg);
 void wave_prepare(const Plan &p);

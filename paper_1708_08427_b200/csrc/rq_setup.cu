@@ -1617,4 +1617,21 @@ int check_duplicates(const double *pos_in, const int64_t *offsets, int64_t m, bo
   return RQ_OK;
 }
 
+void ensure_smem_attr(const void *f, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void *>, size_t>> set;  // (device, kernel) -> limit
+  int dev = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : set)
+    if (e.first.first == dev && e.first.second == f) {
+      if (e.second >= bytes) return;
+      RQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      e.second = bytes;
+      return;
+    }
+  RQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  set.push_back({{dev, f}, bytes});
+}
+
 }  // namespace rq

@@ -92,107 +92,15 @@ __global__ void k_wv_tiles(const int64_t *tile_root, int64_t nt, NodeArrays A, i
 __device__ __forceinline__ int wv_rank(int cs) { return cs == GENERAL ? 0 : (cs == RIGID_BEAD ? 1 : 2); }
 __device__ __forceinline__ int wv_beads(int cs) { return cs == BEAD_BEAD ? 2 : (cs == RIGID_BEAD ? 1 : 0); }
 
-// per tile level profile; node -> tile map
-__global__ void k_wv_profile(const int64_t *tile_root, int64_t nt, NodeArrays A, const int64_t *tl_base, TLev *tl,
-                             int32_t *node_tile, WaveCaps caps, int *bad) {
+// node -> tile map (tile-internal nodes only)
+__global__ void k_wv_node_tile(const int64_t *tile_root, int64_t nt, NodeArrays A, int32_t *node_tile) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= nt) return;
   const int64_t g = tile_root[t];
   const int L = nodeL(A, g);
   if (L < 2) return;
-  const int64_t first = g - 2 * (int64_t)L + 2;
-  TLev *P = tl + tl_base[t];
-  for (int64_t q = first; q <= g; q++) {
-    if (nodeL(A, q) < 2) continue;
-    node_tile[q] = (int32_t)t;
-    const int cs = flag_case(A.flags[q]);
-    TLev &v = P[A.height[q] - 1];
-    if (cs == GENERAL) v.g++;
-    else if (cs == RIGID_BEAD) v.r++;
-    else v.b++;
-    v.beads += wv_beads(cs);
-    const int root = q == g;
-    const int rr = res_rows(cs);
-    v.vd += (rr ? 2 * wv_pieces(A.res_base[A.node_body[q]] + A.res_off[q] - 6, rr) : 0) + 6 * root;
-    v.dg += (res_rows(cs) > 0) + root;
-    v.rm += 8 * rec_size(cs) + 16;
-  }
-  (void)caps;
-  (void)bad;
-}
-
-// Rows of a tile: a height level whose nodes exceed a step's capacities is spread over
-// several consecutive rows (node i of a case -> row i mod r_h); r_h is the least count for
-// which the worst-case share of every resource fits a step.  Rows of height h precede
-// those of height h + 1, so every node still runs after its children.
-__device__ __forceinline__ int wv_rows_for(const TLev &v, int root, const WaveCaps &c) {
-  for (int r = 1;; r++) {
-    const int g = (v.g + r - 1) / r, rb = (v.r + r - 1) / r, b = (v.b + r - 1) / r;
-    if (g <= c.g && rb <= c.r && b <= c.b && 2 * b + rb <= c.beads && 8 * g + 4 * rb + 6 * root <= c.vd &&
-        g + rb + root <= c.dg && 256 * g + 176 * rb + 96 * b <= c.rm)
-      return r;
-  }
-}
-__global__ void k_wv_rows(const int64_t *tile_root, int64_t nt, NodeArrays A, const int64_t *tl_base, const TLev *tl,
-                          int32_t *hrows, int64_t *trows, WaveCaps caps) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= nt) return;
-  const int64_t g = tile_root[t];
-  const int L = nodeL(A, g);
-  if (L < 2) { trows[t] = 0; return; }
-  const int H = A.height[g];
-  int64_t tot = 0;
-  for (int h = 0; h < H; h++) {
-    const int r = wv_rows_for(tl[tl_base[t] + h], h == H - 1, caps);
-    hrows[tl_base[t] + h] = r;
-    tot += r;
-  }
-  trows[t] = tot;
-}
-// node -> row (tile-local) and the row profiles
-__global__ void k_wv_rowprof(const int64_t *tile_root, int64_t nt, NodeArrays A, const int64_t *tl_base,
-                             const int32_t *hrows, int32_t *hctr, const int64_t *rl_base, TLev *rp, int32_t *node_row,
-                             WaveCaps caps, int *bad) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= nt) return;
-  const int64_t g = tile_root[t];
-  const int L = nodeL(A, g);
-  if (L < 2) return;
-  const int H = A.height[g];
-  const int64_t hb = tl_base[t];
-  // row base of each height (hctr holds 4 ints per height: row base, GEN, RB, BB counters)
-  int base = 0;
-  for (int h = 0; h < H; h++) {
-    hctr[4 * (hb + h)] = base;
-    base += hrows[hb + h];
-  }
-  const int64_t first = g - 2 * (int64_t)L + 2;
-  TLev *P = rp + rl_base[t];
-  for (int64_t q = first; q <= g; q++) {
-    if (nodeL(A, q) < 2) continue;
-    const int cs = flag_case(A.flags[q]);
-    const int h = A.height[q] - 1;
-    int32_t *hc = hctr + 4 * (hb + h);
-    const int i = hc[1 + wv_rank(cs)]++;
-    const int row = hc[0] + i % hrows[hb + h];
-    node_row[q] = row;
-    TLev &v = P[row];
-    if (cs == GENERAL) v.g++;
-    else if (cs == RIGID_BEAD) v.r++;
-    else v.b++;
-    v.beads += wv_beads(cs);
-    const int root = q == g;
-    const int rr = res_rows(cs);
-    v.vd += (rr ? 2 * wv_pieces(A.res_base[A.node_body[q]] + A.res_off[q] - 6, rr) : 0) + 6 * root;
-    v.dg += (rr > 0) + root;
-    v.rm += 8 * rec_size(cs) + 16;
-  }
-  for (int r = 0; r < base; r++) {
-    const TLev &v = P[r];
-    if (v.g > caps.g || v.r > caps.r || v.b > caps.b || v.beads > caps.beads || v.vd > caps.vd || v.dg > caps.dg ||
-        v.rm > caps.rm)
-      atomicExch(bad, 1);
-  }
+  for (int64_t q = g - 2 * (int64_t)L + 2; q <= g; q++)
+    if (nodeL(A, q) >= 2) node_tile[q] = (int32_t)t;
 }
 
 // Stream of each tile.  The tile list (body order) is cut into R rounds of equal node count
@@ -200,13 +108,28 @@ __global__ void k_wv_rowprof(const int64_t *tile_root, int64_t nt, NodeArrays A,
 // after round.  All CTAs therefore work inside the same round at any time, so the vector
 // rows of the bodies in flight (gathers, scattered outputs) stay L2-resident while their
 // 32-byte sectors are shared by neighbouring beads.
+// tile -> (stream, round): rounds split the node scan evenly; within a round stream c takes
+// range c -- evenly, or for rounds >= R0 by the cumulative weights W (G + 1 entries, W[0] = 0,
+// W[G] = 1) of the second placement pass (build_wave's tail rebalancing)
 __global__ void k_wv_tile_key(const int64_t *node_scan, int64_t nt, int64_t total, int64_t G, int64_t R,
-                              uint64_t *key, int32_t *val) {
+                              const double *W, int64_t R0, uint64_t *key, int32_t *val) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= nt) return;
   const double x = (double)node_scan[t] / (double)std::max<int64_t>(total, 1) * (double)R;  // in [0, R)
   const int64_t r = std::min<int64_t>(R - 1, (int64_t)x);
-  const int64_t c = std::min<int64_t>(G - 1, (int64_t)((x - (double)r) * (double)G));
+  int64_t c;
+  if (W != nullptr && r >= R0) {
+    const double f = x - (double)r;
+    int64_t lo = 0, hi = G;  // last c with W[c] <= f
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (W[mid] <= f) lo = mid;
+      else hi = mid;
+    }
+    c = lo;
+  } else {
+    c = std::min<int64_t>(G - 1, (int64_t)((x - (double)r) * (double)G));
+  }
   key[t] = (uint64_t)(c * R + r);
   val[t] = (int32_t)t;
 }
@@ -226,50 +149,83 @@ __device__ __forceinline__ bool wv_fits(const TLev &l, const TLev &v, const Wave
          l.vd + v.vd <= c.vd && l.dg + v.dg <= c.dg && l.rm + v.rm <= c.rm;
 }
 
-// one thread per stream: greedy staggered placement of its tiles
-__global__ void k_wv_place(const int64_t *sfirst, int64_t G, const int32_t *order, const int64_t *lv_scan,
-                           const int64_t *tl_base, const TLev *tl, TLev *load, const int64_t *theight,
-                           int32_t *e_tile, int64_t *n_steps, WaveCaps caps) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= G) return;
-  const int64_t i0 = sfirst[c], i1 = sfirst[c + 1];
-  TLev *LD = load + lv_scan[i0];  // room for sum of heights steps (the sequential worst case)
-  int e_prev = 0, last = 0;
-  for (int64_t i = i0; i < i1; i++) {
+// Node-level list scheduling, one CTA (one thread) per stream: the stream's tiles in order,
+// each tile's nodes in postorder; a node goes to the earliest step after its children's
+// (and not before the floor = the first step of the previous tile) with room for it.  Any
+// node shape fits (no rigid tile rows), so tiles can be large and the top trees small.
+// The step loads live in a shared-memory ring of WRING steps ahead of the floor.
+constexpr int WRING = 1024;
+__global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, int64_t G, const int32_t *order,
+                                                      const int64_t *tile_root, NodeArrays A, WaveCaps caps,
+                                                      int32_t *node_step, int64_t *n_steps, int32_t *tile_first,
+                                                      int32_t *tile_last, const int32_t *tile_round, int R0,
+                                                      int64_t *round_floor, int *bad) {
+  __shared__ TLev ring[WRING];
+  const int64_t c = blockIdx.x;
+  for (int i = threadIdx.x; i < WRING; i += 32) ring[i] = TLev{};
+  __syncwarp();
+  if (c >= G || threadIdx.x != 0) return;
+  int floor = 0, last = 0;
+  bool seen = false;
+  for (int64_t i = sfirst[c]; i < sfirst[c + 1]; i++) {
     const int64_t t = order[i];
-    const int H = (int)theight[t];
-    if (H == 0) continue;
-    const TLev *P = tl + tl_base[t];
-    int e = e_prev;
-    for (;;) {
-      int h = 0;
-      while (h < H && wv_fits(LD[e + h], P[h], caps)) h++;
-      if (h == H) break;
-      e++;
+    if (!seen && tile_round[t] >= R0) {  // where this stream enters the rebalanced tail rounds
+      round_floor[c] = floor;
+      seen = true;
     }
-    for (int h = 0; h < H; h++) {
-      TLev &l = LD[e + h];
-      const TLev &v = P[h];
+    const int64_t g = tile_root[t];
+    const int L = nodeL(A, g);
+    if (L < 2) continue;
+    const int j = A.node_body[g];
+    const int64_t nb = A.node_off[j];
+    const int64_t rb = A.res_base[j];
+    int tmin = INT32_MAX, tmax = 0;
+    for (int64_t q = g - 2 * (int64_t)L + 2; q <= g; q++) {
+      if (nodeL(A, q) < 2) continue;
+      int ready = floor;
+      const int64_t lc = nb + A.left[q], rc = nb + A.right[q];
+      if (nodeL(A, lc) >= 2) ready = max(ready, node_step[lc] + 1);
+      if (nodeL(A, rc) >= 2) ready = max(ready, node_step[rc] + 1);
+      const int cs = flag_case(A.flags[q]);
+      const int root = q == g, rr = res_rows(cs);
+      TLev v{};
+      if (cs == GENERAL) v.g = 1;
+      else if (cs == RIGID_BEAD) v.r = 1;
+      else v.b = 1;
+      v.beads = (int16_t)wv_beads(cs);
+      v.vd = (int16_t)((rr ? 2 * wv_pieces(rb + A.res_off[q] - 6, rr) : 0) + 6 * root);
+      v.dg = (int16_t)((rr > 0) + root);
+      v.rm = 8 * rec_size(cs) + 16;
+      int st = ready;
+      for (;; st++) {
+        if (st - floor >= WRING) { atomicExch(bad, 1); return; }
+        if (wv_fits(ring[st % WRING], v, caps)) break;
+      }
+      TLev &l = ring[st % WRING];
       l.g += v.g; l.r += v.r; l.b += v.b; l.beads += v.beads; l.vd += v.vd; l.dg += v.dg; l.rm += v.rm;
+      node_step[q] = st;
+      tmin = min(tmin, st);
+      tmax = max(tmax, st);
+      last = max(last, st + 1);
     }
-    e_tile[t] = e;
-    e_prev = e;
-    last = max(last, e + H);
+    tile_first[t] = tmin;
+    tile_last[t] = tmax;
+    for (; floor < tmin; floor++) ring[floor % WRING] = TLev{};  // steps no later tile can use
   }
+  if (!seen) round_floor[c] = last;
   n_steps[c] = last + 4;  // two gather-only steps at each end
 }
 
 // sort key of every tile node: (global step, case rank)
-__global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, const int32_t *node_row,
-                          const int64_t *step_first, const int32_t *e_tile, uint64_t *keys, int32_t *vals,
-                          const int32_t *tile_stream) {
+__global__ void k_wv_keys(int64_t NN, NodeArrays A, const int32_t *node_tile, const int32_t *node_step,
+                          const int64_t *step_first, uint64_t *keys, int32_t *vals, const int32_t *tile_stream) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= NN) return;
   uint64_t key = ~0ull;
   const int32_t t = node_tile[g];
   if (t >= 0) {
     const int64_t c = tile_stream[t];
-    const int64_t gs = step_first[c] + e_tile[t] + 2 + node_row[g];
+    const int64_t gs = step_first[c] + 2 + node_step[g];
     key = ((uint64_t)gs << 2) | (uint64_t)wv_rank(flag_case(A.flags[g]));
   }
   keys[g] = key;
@@ -286,13 +242,14 @@ __global__ void k_wv_tile_stream(const uint64_t *key, const int32_t *order, int6
 
 // per step and direction: the round of the tiles that start there (upward: entry row;
 // downward: last row), for the run-time round window (k_wave throttles CTAs that run ahead)
-__global__ void k_wv_round_marks(int64_t nt, const int64_t *trows, const int32_t *tile_stream, const int32_t *tile_round,
-                                 const int32_t *e_tile, const int64_t *step_first, int *up_mark, int *dn_mark) {
+__global__ void k_wv_round_marks(int64_t nt, const int64_t *tnodes, const int32_t *tile_stream, const int32_t *tile_round,
+                                 const int32_t *tile_first, const int32_t *tile_last, const int64_t *step_first,
+                                 int *up_mark, int *dn_mark) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= nt || trows[t] == 0) return;
-  const int64_t base = step_first[tile_stream[t]] + 2 + e_tile[t];
-  atomicMax(&up_mark[base], tile_round[t]);
-  atomicMin(&dn_mark[base + trows[t] - 1], tile_round[t]);
+  if (t >= nt || tnodes[t] == 0) return;
+  const int64_t base = step_first[tile_stream[t]] + 2;
+  atomicMax(&up_mark[base + tile_first[t]], tile_round[t]);
+  atomicMin(&dn_mark[base + tile_last[t]], tile_round[t]);
 }
 
 struct StepCnt {
@@ -593,18 +550,14 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   NodeArrays A{in.node_off, in.bead_off, in.rec_off, in.res_base, in.node_body, in.start, in.stop, in.left,
                in.right,    in.parent,   in.height,  in.res_off,  in.perm,      in.slot_scan, in.flags};
   const int64_t NN = p.NN;
-  DBuf tnodes, theight, node_scan, tl_base;
+  DBuf tnodes, theight, node_scan;
   tnodes.alloc(nt * 8);
   theight.alloc(nt * 8);
   node_scan.alloc((nt + 1) * 8);
-  tl_base.alloc((nt + 1) * 8);
   k_wv_tiles<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tnodes.as<int64_t>(), theight.as<int64_t>());
   ex_scan(tnodes.as<int64_t>(), node_scan.as<int64_t>(), nt + 0, s);
-  ex_scan(theight.as<int64_t>(), tl_base.as<int64_t>(), nt + 0, s);
   const int64_t total_nodes = d2h1<int64_t>(node_scan.as<int64_t>() + nt - 1, s) + d2h1<int64_t>(tnodes.as<int64_t>() + nt - 1, s);
-  const int64_t total_lv = d2h1<int64_t>(tl_base.as<int64_t>() + nt - 1, s) + d2h1<int64_t>(theight.as<int64_t>() + nt - 1, s);
   RQ_CUDA(cudaMemcpyAsync(node_scan.as<int64_t>() + nt, &total_nodes, 8, cudaMemcpyHostToDevice, s));
-  RQ_CUDA(cudaMemcpyAsync(tl_base.as<int64_t>() + nt, &total_lv, 8, cudaMemcpyHostToDevice, s));
   if (total_nodes == 0) return;
   // streams: one per resident CTA
   int sms = 0;
@@ -614,100 +567,110 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   if (const char *e = getenv("RQ_WAVE_CTAS_PER_SM")) per_sm = std::max(1, std::min(16, atoi(e)));
   int64_t G = (int64_t)sms * per_sm;
   G = std::max<int64_t>(1, std::min<int64_t>(G, (total_nodes + 15) / 16));
-  // level profiles
-  DBuf tl, node_tile, bad;
-  tl.alloc(std::max<int64_t>(total_lv, 1) * sizeof(TLev));
-  RQ_CUDA(cudaMemsetAsync(tl.p, 0, std::max<int64_t>(total_lv, 1) * sizeof(TLev), s));
+  DBuf node_tile, bad;
   node_tile.alloc(NN * 4);
   RQ_CUDA(cudaMemsetAsync(node_tile.p, 0xff, NN * 4, s));
   bad.alloc(4);
   RQ_CUDA(cudaMemsetAsync(bad.p, 0, 4, s));
-  k_wv_profile<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), tl.as<TLev>(),
-                                        node_tile.as<int32_t>(), caps, bad.as<int>());
-  // rows: height levels split to fit the per-step capacities
-  DBuf hrows, trows, rl_base, hctr, rp, node_row;
-  hrows.alloc(std::max<int64_t>(total_lv, 1) * 4);
-  trows.alloc(nt * 8);
-  rl_base.alloc((nt + 1) * 8);
-  k_wv_rows<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), tl.as<TLev>(), hrows.as<int32_t>(),
-                                     trows.as<int64_t>(), caps);
-  ex_scan(trows.as<int64_t>(), rl_base.as<int64_t>(), nt, s);
-  const int64_t total_rows = d2h1<int64_t>(rl_base.as<int64_t>() + nt - 1, s) + d2h1<int64_t>(trows.as<int64_t>() + nt - 1, s);
-  RQ_CUDA(cudaMemcpyAsync(rl_base.as<int64_t>() + nt, &total_rows, 8, cudaMemcpyHostToDevice, s));
-  hctr.alloc(std::max<int64_t>(total_lv, 1) * 16);
-  RQ_CUDA(cudaMemsetAsync(hctr.p, 0, std::max<int64_t>(total_lv, 1) * 16, s));
-  rp.alloc(std::max<int64_t>(total_rows, 1) * sizeof(TLev));
-  RQ_CUDA(cudaMemsetAsync(rp.p, 0, std::max<int64_t>(total_rows, 1) * sizeof(TLev), s));
-  node_row.alloc(NN * 4);
-  k_wv_rowprof<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, tl_base.as<int64_t>(), hrows.as<int32_t>(),
-                                        hctr.as<int32_t>(), rl_base.as<int64_t>(), rp.as<TLev>(), node_row.as<int32_t>(),
-                                        caps, bad.as<int>());
-  if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a step row exceeds the per-step capacities");
-  tl.reset();
-  hctr.reset();
-  hrows.reset();
-  tm.mark("wave rows");
+  k_wv_node_tile<<<nblk(nt), NT, 0, s>>>(in.tile_root, nt, A, node_tile.as<int32_t>());
   // streams: range c of every round
   int64_t R = std::max<int64_t>(1, p.N / 170000);
-  R = std::min<int64_t>(R, std::max<int64_t>(1, nt / (4 * G)));
+  R = std::min<int64_t>(R, std::max<int64_t>(1, nt / G));  // at least a tile per stream and round
   if (const char *e = getenv("RQ_WAVE_ROUNDS")) R = std::max(1, atoi(e));
   p.wave_rounds = R;
-  DBuf tkey, tval, tkey2, order, sfirst, tile_stream, th_sorted, tn_sorted, lv_scan, n_scan_s;
+  DBuf tkey, tval, tkey2, order, sfirst, tile_stream, tn_sorted, n_scan_s, tile_round;
   tkey.alloc(nt * 8);
   tval.alloc(nt * 4);
   tkey2.alloc(nt * 8);
   order.alloc(nt * 4);
   sfirst.alloc((G + 1) * 8);
   tile_stream.alloc(nt * 4);
-  th_sorted.alloc(nt * 8);
   tn_sorted.alloc(nt * 8);
-  lv_scan.alloc((nt + 1) * 8);
   n_scan_s.alloc((nt + 1) * 8);
-  k_wv_tile_key<<<nblk(nt), NT, 0, s>>>(node_scan.as<int64_t>(), nt, total_nodes, G, R, tkey.as<uint64_t>(),
-                                         tval.as<int32_t>());
-  {
-    size_t tb = 0;
-    RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(), tval.as<int32_t>(),
-                                            order.as<int32_t>(), (int)nt, 0, 64, s));
-    DBuf tmp;
-    tmp.alloc(tb);
-    RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(), tval.as<int32_t>(),
-                                            order.as<int32_t>(), (int)nt, 0, 64, s));
-  }
-  {
-    std::vector<int64_t> h(G + 1, -1);
-    RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
-    k_wv_stream_first<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), nt, R, sfirst.as<int64_t>());
-    d2h(h.data(), sfirst.p, G + 1, s);
-    h[G] = nt;
-    for (int64_t c = G - 1; c >= 0; c--)
-      if (h[c] < 0) h[c] = h[c + 1];
-    RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
-  }
-  DBuf tile_round;
   tile_round.alloc(nt * 4);
-  k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R, tile_stream.as<int32_t>(),
-                                            tile_round.as<int32_t>());
-  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(trows.as<int64_t>(), order.as<int32_t>(), nt, th_sorted.as<int64_t>());
-  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
-  ex_scan(th_sorted.as<int64_t>(), lv_scan.as<int64_t>(), nt, s);
-  ex_scan(tn_sorted.as<int64_t>(), n_scan_s.as<int64_t>(), nt, s);
-  RQ_CUDA(cudaMemcpyAsync(lv_scan.as<int64_t>() + nt, &total_rows, 8, cudaMemcpyHostToDevice, s));
-  RQ_CUDA(cudaMemcpyAsync(n_scan_s.as<int64_t>() + nt, &total_nodes, 8, cudaMemcpyHostToDevice, s));
-  // placement
-  DBuf load, e_tile, n_steps, step_first;
-  load.alloc(std::max<int64_t>(total_rows, 1) * sizeof(TLev));
-  RQ_CUDA(cudaMemsetAsync(load.p, 0, std::max<int64_t>(total_rows, 1) * sizeof(TLev), s));
-  e_tile.alloc(nt * 4);
+  DBuf node_step, n_steps, step_first, tile_first, tile_last, round_floor, Wd;
+  node_step.alloc(NN * 4);
   n_steps.alloc(G * 8);
   step_first.alloc((G + 1) * 8);
-  k_wv_place<<<nblk(G, 64), 64, 0, s>>>(sfirst.as<int64_t>(), G, order.as<int32_t>(), lv_scan.as<int64_t>(),
-                                         rl_base.as<int64_t>(), rp.as<TLev>(), load.as<TLev>(), trows.as<int64_t>(),
-                                         e_tile.as<int32_t>(), n_steps.as<int64_t>(), caps);
+  tile_first.alloc(nt * 4);
+  tile_last.alloc(nt * 4);
+  round_floor.alloc(G * 8);
+  // Tail rebalancing: placement noise accumulates over the rounds (stream step counts spread
+  // ~10% around the mean at S = 128), and the sweep lasts as long as the longest stream.  A
+  // first pass places everything with even ranges; the second re-cuts the last quarter of the
+  // rounds (rounds >= R0) so that every stream, starting from where pass 1 found it at round
+  // R0, ends at the same step T (same node rate nu for all streams).
+  const int64_t R0 = R - (R + 3) / 4;
+  auto assign_place = [&](const double *W) {
+    k_wv_tile_key<<<nblk(nt), NT, 0, s>>>(node_scan.as<int64_t>(), nt, total_nodes, G, R, W, R0, tkey.as<uint64_t>(),
+                                           tval.as<int32_t>());
+    {
+      size_t tb = 0;
+      RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(), tval.as<int32_t>(),
+                                              order.as<int32_t>(), (int)nt, 0, 64, s));
+      DBuf tmp;
+      tmp.alloc(tb);
+      RQ_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, tkey.as<uint64_t>(), tkey2.as<uint64_t>(), tval.as<int32_t>(),
+                                              order.as<int32_t>(), (int)nt, 0, 64, s));
+    }
+    {
+      std::vector<int64_t> h(G + 1, -1);
+      RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+      k_wv_stream_first<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), nt, R, sfirst.as<int64_t>());
+      d2h(h.data(), sfirst.p, G + 1, s);
+      h[G] = nt;
+      for (int64_t c = G - 1; c >= 0; c--)
+        if (h[c] < 0) h[c] = h[c + 1];
+      RQ_CUDA(cudaMemcpyAsync(sfirst.p, h.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+    }
+    k_wv_tile_stream<<<nblk(nt), NT, 0, s>>>(tkey2.as<uint64_t>(), order.as<int32_t>(), nt, R,
+                                              tile_stream.as<int32_t>(), tile_round.as<int32_t>());
+    // node-level placement
+    k_wv_place_nodes<<<(unsigned)G, 32, 0, s>>>(sfirst.as<int64_t>(), G, order.as<int32_t>(), in.tile_root, A, caps,
+                                                 node_step.as<int32_t>(), n_steps.as<int64_t>(),
+                                                 tile_first.as<int32_t>(), tile_last.as<int32_t>(),
+                                                 tile_round.as<int32_t>(), (int)R0, round_floor.as<int64_t>(),
+                                                 bad.as<int>());
+    if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a node does not fit the step window");
+  };
+  assign_place(nullptr);
+  bool rebalance = G > 1 && R > 1;
+  if (const char *e = getenv("RQ_WAVE_REBALANCE")) rebalance = rebalance && atoi(e) != 0;
+  if (rebalance) {
+    std::vector<int64_t> ns(G), fl(G);
+    d2h(ns.data(), n_steps.p, G, s);
+    d2h(fl.data(), round_floor.p, G, s);
+    const int64_t max1 = *std::max_element(ns.begin(), ns.end());
+    double span = 0;  // steps the tail rounds took in pass 1
+    for (int64_t c = 0; c < G; c++) span += std::max<double>(1.0, (double)(ns[c] - 4 - fl[c]));
+    // ends at T: sum_c max(0, T - F_c) = span (same node rate, same total tail work)
+    double lo = (double)*std::min_element(fl.begin(), fl.end()), hi = lo + span + 1.0;
+    for (int it = 0; it < 100; it++) {
+      const double T = 0.5 * (lo + hi);
+      double tot = 0;
+      for (int64_t c = 0; c < G; c++) tot += std::max(0.0, T - (double)fl[c]);
+      (tot < span ? lo : hi) = T;
+    }
+    std::vector<double> W(G + 1, 0.0);
+    for (int64_t c = 0; c < G; c++) W[c + 1] = W[c] + std::max(0.0, hi - (double)fl[c]);
+    for (int64_t c = 1; c <= G; c++) W[c] /= W[G];
+    W[G] = 1.0 + 1e-12;
+    Wd.alloc((G + 1) * 8);
+    RQ_CUDA(cudaMemcpyAsync(Wd.p, W.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
+    RQ_CUDA(cudaStreamSynchronize(s));
+    assign_place(Wd.as<double>());
+    d2h(ns.data(), n_steps.p, G, s);
+    const int64_t max2 = *std::max_element(ns.begin(), ns.end());
+    if (getenv("RQ_VERBOSE")) fprintf(stderr, "[rq] wave rebalance R0=%lld: max steps %lld -> %lld\n", (long long)R0,
+                                      (long long)max1, (long long)max2);
+    if (max2 > max1) assign_place(nullptr);  // pass 1 was better
+  }
+  k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
+  ex_scan(tn_sorted.as<int64_t>(), n_scan_s.as<int64_t>(), nt, s);
+  RQ_CUDA(cudaMemcpyAsync(n_scan_s.as<int64_t>() + nt, &total_nodes, 8, cudaMemcpyHostToDevice, s));
   ex_scan(n_steps.as<int64_t>(), step_first.as<int64_t>(), G, s);
   const int64_t NS = d2h1<int64_t>(step_first.as<int64_t>() + G - 1, s) + d2h1<int64_t>(n_steps.as<int64_t>() + G - 1, s);
   RQ_CUDA(cudaMemcpyAsync(step_first.as<int64_t>() + G, &NS, 8, cudaMemcpyHostToDevice, s));
-  load.reset();
   tm.mark("wave place");
   // node order: (global step, case)
   DBuf keys, vals, keys2, vals2;
@@ -715,9 +678,8 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   vals.alloc(NN * 4);
   keys2.alloc(NN * 8);
   vals2.alloc(NN * 4);
-  k_wv_keys<<<nblk(NN), NT, 0, s>>>(NN, A, node_tile.as<int32_t>(), node_row.as<int32_t>(), step_first.as<int64_t>(),
-                                     e_tile.as<int32_t>(), keys.as<uint64_t>(), vals.as<int32_t>(),
-                                     tile_stream.as<int32_t>());
+  k_wv_keys<<<nblk(NN), NT, 0, s>>>(NN, A, node_tile.as<int32_t>(), node_step.as<int32_t>(), step_first.as<int64_t>(),
+                                     keys.as<uint64_t>(), vals.as<int32_t>(), tile_stream.as<int32_t>());
   {
     int bits = 2;
     while ((int64_t(1) << (bits - 2)) <= NS) bits++;
@@ -779,9 +741,9 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
     std::vector<int> init(2 * NS);
     for (int64_t i = 0; i < NS; i++) { init[i] = -1; init[NS + i] = INT32_MAX; }
     RQ_CUDA(cudaMemcpyAsync(marks.p, init.data(), NS * 8, cudaMemcpyHostToDevice, s));
-    k_wv_round_marks<<<nblk(nt), NT, 0, s>>>(nt, trows.as<int64_t>(), tile_stream.as<int32_t>(), tile_round.as<int32_t>(),
-                                              e_tile.as<int32_t>(), step_first.as<int64_t>(), marks.as<int>(),
-                                              marks.as<int>() + NS);
+    k_wv_round_marks<<<nblk(nt), NT, 0, s>>>(nt, tnodes.as<int64_t>(), tile_stream.as<int32_t>(),
+                                              tile_round.as<int32_t>(), tile_first.as<int32_t>(), tile_last.as<int32_t>(),
+                                              step_first.as<int64_t>(), marks.as<int>(), marks.as<int>() + NS);
     k_wv_headers<<<nblk(NS), NT, 0, s>>>(p.wave_desc.as<StepDesc>(), NS, p.wave_blob.as<uint8_t>(), marks.as<int>(),
                                           marks.as<int>() + NS);
     RQ_CUDA(cudaStreamSynchronize(s));
@@ -858,11 +820,17 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   p.wave_steps = NS;
   p.wave_blob_bytes = blob_bytes;
   p.wave_nodes = n;
-  if (getenv("RQ_VERBOSE"))
-    fprintf(stderr, "[rq] wave: %lld streams x %lld rounds, %lld steps (%.1f per stream, %.1f nodes per step), blob %.1f MB "
-                    "(up %.1f, down %.1f), M slots %d, stage %lld B\n",
-            (long long)G, (long long)R, (long long)NS, (double)NS / G, (double)n / std::max<int64_t>(1, NS - 4 * G),
-            blob_bytes / 1e6, p.wave_up_bytes / 1e6, p.wave_down_bytes / 1e6, p.wave_mslots, (long long)p.wave_stage_bytes);
+  if (getenv("RQ_VERBOSE")) {
+    std::vector<int64_t> sf(G + 1);
+    d2h(sf.data(), p.wave_stream_first.p, G + 1, s);
+    int64_t mx = 0;
+    for (int64_t c = 0; c < G; c++) mx = std::max(mx, sf[c + 1] - sf[c]);
+    fprintf(stderr, "[rq] wave: %lld streams x %lld rounds, %lld steps (%.1f per stream, max %lld, %.1f nodes per step), "
+                    "blob %.1f MB (up %.1f, down %.1f), M slots %d, stage %lld B, window %d\n",
+            (long long)G, (long long)R, (long long)NS, (double)NS / G, (long long)mx,
+            (double)n / std::max<int64_t>(1, NS - 4 * G), blob_bytes / 1e6, p.wave_up_bytes / 1e6,
+            p.wave_down_bytes / 1e6, p.wave_mslots, (long long)p.wave_stage_bytes, p.wave_window);
+  }
 }
 
 // ---- sweep kernel ------------------------------------------------------------------
@@ -1222,7 +1190,7 @@ void wave_prepare(const Plan &p) {
   if (p.wave_ready || !p.wave_streams) return;
   const size_t sm = wave_smem(p, nullptr, nullptr, nullptr);
   for (const void *f : {(const void *)k_wave<true, 2>, (const void *)k_wave<false, 2>})
-    RQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    ensure_smem_attr(f, sm);
   int occ = 0;
   RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_wave<true, 2>, 128, sm));
   p.wave_ctas_per_sm = occ;

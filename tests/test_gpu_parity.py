@@ -475,6 +475,27 @@ def test_concurrent_streams(rq):
             assert torch.equal(outs[i][0], seq[i][0]) and torch.equal(outs[i][1], seq[i][1]), (rep, i)
 
 
+def test_interleaved_plans(rq, oracle_mod):
+    """Plans with different sweep footprints used alternately: the kernels' shared-memory
+    limits are process-wide, so a small plan prepared after a big one must not lower the big
+    plan's limit (the big plan's next launch failed with 'invalid argument')."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pa, oa = ellipsoid_batch([4096] * 24 + [20000], seed=21)
+    pb, ob = ellipsoid_batch([40, 70, 9], seed=22)
+    rng = np.random.default_rng(9)
+    big = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pa, oa))
+    va = rng.normal(size=3 * oa[-1])
+    first = big.apply("qtilde_v", va)
+    small = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pb, ob))
+    vb = rng.normal(size=3 * ob[-1])
+    ref_b = oracle_mod.OracleBatch(pb, ob, threads=1).apply("qtilde_v", vb)
+    for _ in range(2):
+        assert per_body_rel(small.apply("qtilde_v", vb), ref_b, 3 * np.diff(ob) - 6) < TOL
+        assert np.array_equal(big.apply("qtilde_v", va), first)
+    assert big.plan.info()["sweep_smem"] > small.plan.info()["sweep_smem"]
+
+
 @pytest.mark.parametrize("env", [{"RQ_TILE_SORT": "0"}, {"RQ_TILE_SORT": "2"}, {"RQ_H2D_THREADS": "0"},
                                  {"RQ_H2D_THREADS": "3"}])
 def test_setup_variants_bitwise(rq, monkeypatch, env):
