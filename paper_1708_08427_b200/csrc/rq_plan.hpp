@@ -222,6 +222,7 @@ struct Plan {
     DBuf round_ctr;           // wave round-window arrival counters [2][rounds] (up, down)
     uint32_t wave_epoch[2] = {0, 0};
     DBuf zpart;               // Zf per-segment partial sums
+    DBuf zcnt;                // Zf per-(column, body) arrival counters (self-resetting)
   };
   mutable std::mutex state_mu;
   mutable std::map<cudaStream_t, std::unique_ptr<StreamState>> stream_state;

@@ -4,8 +4,8 @@
 // Z is never assembled: Zf = [sum f_k ; sum (r_k - c) x f_k] is a segmented
 // reduction with a FIXED order (segments of seg_len(n_j) beads -- a function of
 // the body's own size only -- tree-reduced inside a CTA, then reduced per body by
-// one warp in a fixed lane order), so results do not depend on batch composition
-// or GPU count.  All k columns go in one launch (grid.y = column).  Z^T u =
+// the body's last-arriving CTA in a fixed order), so results do not depend on batch
+// composition or GPU count.  All k columns go in one launch (grid.y = column).  Z^T u =
 // V + w x (r_k - c) is a streaming per-bead map (48 B/bead).
 #include <algorithm>
 #include <vector>
@@ -21,23 +21,29 @@ inline int64_t seg_len(int64_t n) { return n >= (int64_t(1) << 18) ? 1024 : 4096
 
 template <int W>
 __device__ __forceinline__ void block_sum(double (&v)[W], double *sh) {
-  // sh: NTZ * W doubles; fixed reduction tree
-  const int tid = threadIdx.x;
+  // sh: (NTZ / 32) * W doubles; fixed reduction tree (shuffle tree per warp, then warp 0 over
+  // the warp sums); the result is valid in thread 0
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 #pragma unroll
-  for (int w = 0; w < W; w++) sh[w * NTZ + tid] = v[w];
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int w = 0; w < W; w++) v[w] = __dadd_rn(v[w], __shfl_down_sync(0xffffffffu, v[w], o));
+  if (lane == 0)
+#pragma unroll
+    for (int w = 0; w < W; w++) sh[w * (NTZ / 32) + wid] = v[w];
   __syncthreads();
-  for (int o = NTZ / 2; o > 0; o >>= 1) {
-    if (tid < o)
+  if (wid == 0) {
 #pragma unroll
-      for (int w = 0; w < W; w++) sh[w * NTZ + tid] += sh[w * NTZ + tid + o];
-    __syncthreads();
+    for (int w = 0; w < W; w++) v[w] = lane < NTZ / 32 ? sh[w * (NTZ / 32) + lane] : 0.0;
+#pragma unroll
+    for (int o = NTZ / 64; o > 0; o >>= 1)
+#pragma unroll
+      for (int w = 0; w < W; w++) v[w] = __dadd_rn(v[w], __shfl_down_sync(0xffffffffu, v[w], o));
   }
-#pragma unroll
-  for (int w = 0; w < W; w++) v[w] = sh[w * NTZ];
 }
 
 __global__ void __launch_bounds__(NTZ) k_seg_possum(const double *pos, const int64_t *seg_begin, double *part) {
-  __shared__ double sh[3 * NTZ];
+  __shared__ double sh[3 * NTZ / 32];
   const int64_t s = blockIdx.x;
   const int64_t b = seg_begin[s], e = seg_begin[s + 1];
   double v[3] = {0, 0, 0};
@@ -59,10 +65,16 @@ __global__ void k_body_mean(const double *part, const int64_t *body_seg, const i
   for (int a = 0; a < 3; a++) cen[j * 3 + a] = v[a] / n;
 }
 
-__global__ void __launch_bounds__(NTZ) k_seg_zf(const double *pos, const int64_t *seg_begin, const int32_t *seg_body,
-                                                const double *origin, const double *f, int64_t K, int64_t n_seg,
-                                                double *part) {
-  __shared__ double sh[6 * NTZ];
+// One launch: a CTA per (segment, column) reduces its segment; the last CTA of a body (per
+// column; arrival counter, threadfence) then sums the body's segment partials in a fixed order
+// (thread t: segments t, t + NTZ, ...; then the block tree), so the result depends only on
+// the body's size.  Single-segment bodies write their sums directly.  The counters reset
+// themselves, so back-to-back calls on one stream reuse them.
+__global__ void __launch_bounds__(NTZ) k_zf(const double *pos, const int64_t *seg_begin, const int32_t *seg_body,
+                                            const int64_t *body_seg, int64_t m, const double *origin, const double *f,
+                                            int64_t K, int64_t n_seg, double *part, unsigned *cnt, double *out) {
+  __shared__ double sh[6 * NTZ / 32];
+  __shared__ int last;
   const int64_t s = blockIdx.x;
   const int64_t col = blockIdx.y;
   const int64_t b = seg_begin[s], e = seg_begin[s + 1];
@@ -109,27 +121,30 @@ __global__ void __launch_bounds__(NTZ) k_seg_zf(const double *pos, const int64_t
         f[(i * 3 + 2) * K + col]);
   }
   block_sum<6>(v, sh);
-  if (threadIdx.x == 0)
-    for (int a = 0; a < 6; a++) part[(col * n_seg + s) * 6 + a] = v[a];
-}
-
-// one warp per (body, column): lane l sums the body's segments l, l + 32, ... in order, then a
-// fixed shuffle tree (bodies with few segments: lane 0 alone, in segment order)
-__global__ void k_body_zf(const double *part, const int64_t *body_seg, int64_t m, double *out, int64_t K,
-                          int64_t n_seg) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t col = blockIdx.y;
-  if (w >= m) return;
-  const int64_t j = w;
-  const double *P = part + col * n_seg * 6;
-  double v[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t s = body_seg[j] + lane; s < body_seg[j + 1]; s += 32)
-    for (int a = 0; a < 6; a++) v[a] += P[s * 6 + a];
-  for (int o = 16; o > 0; o >>= 1)
-    for (int a = 0; a < 6; a++) v[a] += __shfl_down_sync(0xffffffffu, v[a], o);
-  if (lane == 0)
+  const int64_t s0 = body_seg[j], s1 = body_seg[j + 1];
+  if (s1 - s0 == 1) {
+    if (threadIdx.x == 0)
+      for (int a = 0; a < 6; a++) out[(j * 6 + a) * K + col] = v[a];
+    return;
+  }
+  double *P = part + col * n_seg * 6;
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < 6; a++) P[s * 6 + a] = v[a];
+    __threadfence();
+    last = atomicAdd(&cnt[col * m + j], 1u) == (unsigned)(s1 - s0 - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int a = 0; a < 6; a++) v[a] = 0.0;
+  for (int64_t q = s0 + threadIdx.x; q < s1; q += NTZ)
+    for (int a = 0; a < 6; a++) v[a] = __dadd_rn(v[a], __ldcg(&P[q * 6 + a]));
+  __syncthreads();  // sh reused
+  block_sum<6>(v, sh);
+  if (threadIdx.x == 0) {
     for (int a = 0; a < 6; a++) out[(j * 6 + a) * K + col] = v[a];
+    cnt[col * m + j] = 0;
+  }
 }
 
 // K = 1, 16-byte aligned output: a thread maps a bead pair (48 contiguous bytes in and out)
@@ -222,11 +237,13 @@ void run_z(const Plan &p, int op, const double *in, double *out, int64_t k, cons
     Plan::StreamState &ss = p.state_for(s);
     const size_t need = (size_t)p.n_seg * 48 * k;
     if (ss.zpart.bytes < need) ss.zpart.alloc(need);
-    k_seg_zf<<<dim3((unsigned)p.n_seg, (unsigned)k), NTZ, 0, s>>>(p.pos_orig.as<double>(), p.seg_begin.as<int64_t>(),
-                                                                 p.seg_body.as<int32_t>(), origin, in, k, p.n_seg,
-                                                                 ss.zpart.as<double>());
-    k_body_zf<<<dim3((unsigned)((p.m * 32 + 255) / 256), (unsigned)k), 256, 0, s>>>(
-        ss.zpart.as<double>(), p.body_seg.as<int64_t>(), p.m, out, k, p.n_seg);
+    if (ss.zcnt.bytes < (size_t)p.m * 4 * k) {
+      ss.zcnt.alloc((size_t)p.m * 4 * k);
+      RQ_CUDA(cudaMemsetAsync(ss.zcnt.p, 0, (size_t)p.m * 4 * k, s));
+    }
+    k_zf<<<dim3((unsigned)p.n_seg, (unsigned)k), NTZ, 0, s>>>(
+        p.pos_orig.as<double>(), p.seg_begin.as<int64_t>(), p.seg_body.as<int32_t>(), p.body_seg.as<int64_t>(), p.m,
+        origin, in, k, p.n_seg, ss.zpart.as<double>(), ss.zcnt.as<unsigned>(), out);
   } else if (k == 1 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
     const int64_t np = (p.N + 1) / 2;
     k_ztu2<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(p.pos_orig.as<double>(), p.body_of.as<int32_t>(), origin,

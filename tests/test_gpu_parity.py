@@ -540,6 +540,30 @@ def test_zf_batch_independent(rq):
     assert np.array_equal(dev.cpu().numpy(), both)
 
 
+def test_zf_repeat_and_columns(rq):
+    """Zf's per-body arrival counters reset themselves: repeated calls (and a big body with
+    many 1024-bead segments) give identical sums; k columns equal k single-column calls
+    bitwise; values match a float64 numpy evaluation of Z f (model.py:129-149)."""
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([300000, 5000, 9001, 2], seed=6)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    F = np.random.default_rng(2).normal(size=(3 * off[-1], 3))
+    one = [op.zf(np.ascontiguousarray(F[:, c])) for c in range(3)]
+    for _ in range(3):
+        assert np.array_equal(op.zf(np.ascontiguousarray(F[:, 0])), one[0])
+    blk = op.zf(F)
+    for c in range(3):
+        assert np.array_equal(blk[:, c], one[c])
+    cen = op.plan.centroids()
+    for j in range(len(off) - 1):
+        r = pos[off[j]:off[j + 1]] - cen[j]
+        f = F[3 * off[j]:3 * off[j + 1], 0].reshape(-1, 3)
+        ref = np.concatenate([f.sum(0), np.cross(r, f).sum(0)])
+        scale = np.abs(r).max() * np.abs(f).sum() + np.abs(f).sum()
+        assert np.abs(one[0][6 * j:6 * j + 6] - ref).max() < 1e-13 * scale
+
+
 def test_multi_rhs_policy(rq, monkeypatch):
     """Blocks on one big body run the column-parallel kernels too (its top tree sweeps
     level-parallel, a warp per top node and column group); the column loop gives the same
