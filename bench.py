@@ -448,20 +448,29 @@ def main():
         ho1 = torch.empty((3 * N - 6 * m, k), dtype=torch.float64, pin_memory=True)
         ho2 = torch.empty((3 * N, k), dtype=torch.float64, pin_memory=True)
         e_steps = max(3, min(50, args.steps))
-        def host_step():  # both applications queued, then one wait: their copies overlap
+        def host_step():  # both applications queued on the async host path
             L.check(lib.rq_apply_host_async(h, L.OP_QTILDE_V, hv.data_ptr(), ho1.data_ptr(), k))
             L.check(lib.rq_apply_host_async(h, L.OP_QTILDE_TV, hg.data_ptr(), ho2.data_ptr(), k))
-            L.check(lib.rq_host_wait(h))
 
         for _ in range(2):
             host_step()
+            L.check(lib.rq_host_wait(h))
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+        # (1) streaming: the K steps queued back to back (two staging slots: the H2D of the next
+        # operand overlaps the D2H of the previous result), one wait after the last step
         t0 = time.perf_counter()
         for _ in range(e_steps):
             host_step()
+        L.check(lib.rq_host_wait(h))
         e2e_ms = (time.perf_counter() - t0) / e_steps * 1e3
+        # (2) every step waited for before the next one starts
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            host_step()
+            L.check(lib.rq_host_wait(h))
+        sync_ms = (time.perf_counter() - t0) / e_steps * 1e3
         # numpy (pageable) through the Python API
         nv, ng = hv.numpy().reshape(v.shape).copy(), hg.numpy().reshape(g.shape).copy()
         for _ in range(2):
@@ -473,18 +482,32 @@ def main():
             op.apply("qtilde_v", nv)
             op.apply("qtilde_tv", ng)
         np_ms = (time.perf_counter() - t0) / n_steps * 1e3
+        # the same pair through MultiBodyOperator.apply_many (both queued, one wait)
+        for _ in range(2):
+            op.apply_many([("qtilde_v", nv), ("qtilde_tv", ng)])
+        t0 = time.perf_counter()
+        for _ in range(n_steps):
+            op.apply_many([("qtilde_v", nv), ("qtilde_tv", ng)])
+        npm_ms = (time.perf_counter() - t0) / n_steps * 1e3
         if dist:
-            t = torch.tensor([e2e_ms, np_ms], device=dev)
+            t = torch.tensor([e2e_ms, np_ms, npm_ms, sync_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms, np_ms = (float(x) for x in t.tolist())
+            e2e_ms, np_ms, npm_ms, sync_ms = (float(x) for x in t.tolist())
         nbytes_in = (hv.numel() + hg.numel()) * 8
         nbytes_out = (ho1.numel() + ho2.numel()) * 8
         e2e = {"value": n_job * k / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": nbytes_in,
                "d2h_bytes_per_step": nbytes_out, "ms_per_step": e2e_ms,
-               "path": "rq_apply_host_async x2 + rq_host_wait (C ABI, pinned host buffers, H2D+D2H inside "
-                       "the timed region)",
+               "path": "rq_apply_host_async x2 per step, K steps queued, one rq_host_wait (C ABI, pinned "
+                       "host buffers; every step's H2D of its inputs and D2H of its results inside the timed "
+                       "region)",
+               "per_step_wait": {"value": n_job * k / (sync_ms * 1e-3), "ms_per_step": sync_ms,
+                                 "path": "the same with rq_host_wait after every step"},
                "numpy": {"value": n_job * k / (np_ms * 1e-3), "ms_per_step": np_ms,
-                         "path": "MultiBodyOperator.apply on numpy arrays (pageable host memory)"}}
+                         "path": "MultiBodyOperator.apply x2 on numpy arrays (pageable inputs staged by "
+                                 "host threads; results returned in page-locked numpy arrays)"},
+               "numpy_many": {"value": n_job * k / (npm_ms * 1e-3), "ms_per_step": npm_ms,
+                              "path": "MultiBodyOperator.apply_many([(qtilde_v, v), (qtilde_tv, g)]) on numpy "
+                                      "arrays (both queued, one wait)"}}
 
     # ---- one-time gather of the shard outputs (strong sharding): NCCL all_gather of the
     # max-padded shards, timed on the device, max over ranks

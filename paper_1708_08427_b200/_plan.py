@@ -19,6 +19,24 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
+def host_result(shape):
+    """A float64 result array for the host path, in page-locked memory when torch can give it
+    (its caching host allocator reuses freed blocks), so the device-to-host copy lands directly
+    in the returned array instead of going through a staging buffer and a second memcpy.
+    RQ_PINNED_RESULTS=0 returns plain numpy memory."""
+    import os
+
+    if os.environ.get("RQ_PINNED_RESULTS", "1") != "0":
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+        except (ImportError, RuntimeError):
+            pass
+    return np.empty(shape)
+
+
 def _torch_stream(device=None):
     import torch
 
@@ -103,9 +121,26 @@ class Plan:
             self._check_device(v2)
             L.check(lib.rq_apply(self._h, code, v2.data_ptr(), out.data_ptr(), k, _torch_stream(v2.device)))
             return out
-        out = np.empty((lo, k))
+        out = host_result((lo, k))
         L.check(lib.rq_apply_host(self._h, code, v2.ctypes.data, out.ctypes.data, k))
         return out
+
+    def apply_host_many(self, items):
+        """[(op, (in_len, k) numpy array), ...] -> results, every application queued on the
+        host-async path (rq_apply_host_async) before one rq_host_wait, so the H2D of one
+        operand overlaps the D2H of the previous result."""
+        lib = L.lib()
+        outs = []
+        try:
+            for op, v2 in items:
+                _, lo = self.lengths(op)
+                k = int(v2.shape[1])
+                out = host_result((lo, k))
+                outs.append((out, v2))  # both stay referenced until the wait
+                L.check(lib.rq_apply_host_async(self._h, L.OPS[op], v2.ctypes.data, out.ctypes.data, k))
+        finally:
+            L.check(lib.rq_host_wait(self._h))
+        return [o for o, _ in outs]
 
     def z(self, op: int, v2, origin=None):
         lib = L.lib()
@@ -122,7 +157,7 @@ class Plan:
             self._check_device(v2)
             L.check(lib.rq_z_apply(self._h, op, v2.data_ptr(), out.data_ptr(), k, optr, _torch_stream(v2.device)))
             return out
-        out = np.empty((lo, k))
+        out = host_result((lo, k))
         L.check(lib.rq_z_apply_host(self._h, op, v2.ctypes.data, out.ctypes.data, k, optr))
         return out
 

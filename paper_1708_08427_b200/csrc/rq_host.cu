@@ -5,9 +5,10 @@
 // keeping both copy directions busy:
 //
 //  * an application is H2D (stream s_in) -> kernels (s_k) -> D2H (s_out) on one of
-//    two staging slots, so consecutive applications overlap: the H2D of the next
-//    operand runs while the previous result comes back (rq_apply_host_async +
-//    rq_host_wait; rq_apply_host is both).
+//    two staging slots (RQ_HOST_SLOTS), so consecutive applications overlap: the
+//    H2D of the next operands runs while the previous results come back, and the link
+//    runs full duplex (98 GB/s for both directions on the B200 hosts vs 55-57 alone)
+//    (rq_apply_host_async + rq_host_wait; rq_apply_host is both).
 //  * pageable (numpy) buffers are staged through pinned memory in 4 MiB pieces by
 //    host threads, each piece's DMA queued as soon as its memcpy is done (and the
 //    reverse on the way out, piece by piece behind per-piece events), so the host
@@ -39,8 +40,10 @@ bool host_pinned(const void *ptr) {
 }
 
 int host_threads() {
+  // 8 threads: 35 GB/s of pageable -> pinned memcpy on the B200 hosts; 16 reach 41 GB/s alone
+  // but slow the concurrent DMA down (net loss, profiles/r02_notes.md)
   static const int T = [] {
-    int t = 8;
+    int t = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
     if (const char *e = getenv("RQ_HOST_THREADS")) t = std::max(1, std::min(32, atoi(e)));
     return t;
   }();
@@ -115,7 +118,11 @@ void run_apply_host_async(const Plan &p, int op, const double *in, double *out, 
   const bool in_comp = op == RQ_OP_QTILDE_TV, out_comp = op == RQ_OP_QTILDE_V;
   const int64_t ri = 3 * p.N - (in_comp ? 6 * p.m : 0), ro = 3 * p.N - (out_comp ? 6 * p.m : 0);
   const size_t bi = (size_t)ri * k * 8, bo = (size_t)ro * k * 8;
-  p.host_next ^= 1;
+  if (!p.host_slots) {
+    p.host_slots = 2;  // 3 or 4 measured the same on config 2; each holds both device vectors
+    if (const char *e = getenv("RQ_HOST_SLOTS")) p.host_slots = std::max(1, std::min(Plan::MAX_HOST_SLOTS, atoi(e)));
+  }
+  p.host_next = (p.host_next + 1) % p.host_slots;
   Plan::HostSlot &S = p.hslot[p.host_next];
   finish_slot(p, S);  // the slot's previous application is delivered before its buffers are reused
   if (!S.e_in) {

@@ -206,8 +206,10 @@ struct Plan {
     double *defer_out = nullptr;             // pageable result delivered by the next wait
     size_t defer_bytes = 0;
   };
-  mutable HostSlot hslot[2];
+  static constexpr int MAX_HOST_SLOTS = 4;
+  mutable HostSlot hslot[MAX_HOST_SLOTS];
   mutable int host_next = 0;
+  mutable int host_slots = 0;  // slots in use (RQ_HOST_SLOTS, default 2), set on first use
 
   mutable std::mutex host_mu;
   // Per-stream exchange state: applications of one plan on different streams may run

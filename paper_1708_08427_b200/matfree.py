@@ -237,6 +237,24 @@ class MultiBodyOperator:
         out = self.plan.apply(op, v2)
         return out[:, 0] if single else out
 
+    def apply_many(self, items):
+        """Several host (numpy) applications at once: ``[(op, v), ...] -> [result, ...]``.
+        Same results as ``[self.apply(op, v) for op, v in items]``; the applications are queued
+        together so consecutive host<->device copies overlap (rq_apply_host_async)."""
+        prepared = []
+        for op, v in items:
+            if op not in _OP_NAMES:
+                raise ValueError(f"op must be one of {_OP_NAMES}, got {op!r}")
+            if _is_torch_cuda(v):
+                raise TypeError("apply_many takes host (numpy) vectors; use apply for CUDA tensors")
+            if op == "qtilde_tv" and self._min_n == 2:
+                raise ValueError("cannot reshape array of size 0 into shape (0,newaxis)")
+            in_len, _ = self._lengths(op)
+            v2, single = _as_columns(v, in_len)
+            prepared.append((op, v2, single))
+        outs = self.plan.apply_host_many([(op, v2) for op, v2, _ in prepared])
+        return [o[:, 0] if single else o for o, (_, _, single) in zip(outs, prepared)]
+
     def zf(self, f, origin=None):
         """Per-body [sum f; sum (r - c) x f] (6m,) -- Z @ f without assembling Z."""
         f2, single = _as_columns(f, 3 * self.model.n_total, "force vector")

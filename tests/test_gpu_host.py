@@ -76,3 +76,30 @@ def test_numpy_api_and_full_ops_equal_device(rq):
         assert np.array_equal(op.apply(name, v), _device(op, name, v)), name
     V = rng.normal(size=(3 * N, 3))
     assert np.array_equal(op.apply("qv", V), op.apply("qv", __import__("torch").from_numpy(V).cuda()).cpu().numpy())
+
+
+def test_apply_many_and_pinned_results(rq, monkeypatch):
+    """apply_many queues several host applications before one wait; its results equal
+    sequential apply calls bitwise, and results live in page-locked memory by default (plain
+    numpy with RQ_PINNED_RESULTS=0) -- ordinary writeable float64 arrays either way."""
+    import torch
+
+    from paper_1708_08427_b200.workloads import ellipsoid_batch
+
+    pos, off = ellipsoid_batch([4096] * 30 + [20000, 3], seed=17)
+    op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
+    N, m = int(off[-1]), len(off) - 1
+    rng = np.random.default_rng(8)
+    vs = [rng.normal(size=3 * N) for _ in range(3)]
+    gs = [rng.normal(size=3 * N - 6 * m) for _ in range(3)]
+    items = [x for v, g in zip(vs, gs) for x in (("qtilde_v", v), ("qtilde_tv", g))]
+    items.append(("qv", rng.normal(size=(3 * N, 2))))
+    seq = [op.apply(name, x) for name, x in items]
+    many = op.apply_many(items)
+    for a, b in zip(many, seq):
+        assert a.dtype == np.float64 and a.flags.writeable and np.array_equal(a, b)
+    assert np.array_equal(seq[0], _device(op, "qtilde_v", vs[0]))
+    assert torch.from_numpy(many[0]).is_pinned(), "host results should be page-locked"
+    monkeypatch.setenv("RQ_PINNED_RESULTS", "0")
+    plain = op.apply("qtilde_v", vs[0])
+    assert not torch.from_numpy(plain).is_pinned() and np.array_equal(plain, seq[0])
