@@ -19,6 +19,8 @@
 // residue rows it had to gather and scatter on the host cost more than the ~15%
 // that overlapping both directions inside one application gains; see
 // profiles/r02_notes.md.)
+#include <immintrin.h>
+
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -48,6 +50,35 @@ int host_threads() {
     return t;
   }();
   return T;
+}
+
+// pageable -> pinned staging copy with non-temporal stores: the staging buffer is read next by
+// the copy engine, not by this core, so the stores skip the read-for-ownership of their lines
+// (the host memory bus is what the staging competes for with the concurrent DMA).  Falls back
+// to memcpy without AVX-512 or for unaligned pieces.
+__attribute__((target("avx512f"))) void stream_copy_avx512(char *dst, const char *src, size_t n) {
+  size_t i = 0;
+  for (; i + 256 <= n; i += 256) {
+    const __m512i a = _mm512_loadu_si512(src + i), b = _mm512_loadu_si512(src + i + 64);
+    const __m512i c = _mm512_loadu_si512(src + i + 128), d = _mm512_loadu_si512(src + i + 192);
+    _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + i), a);
+    _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + i + 64), b);
+    _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + i + 128), c);
+    _mm512_stream_si512(reinterpret_cast<__m512i *>(dst + i + 192), d);
+  }
+  _mm_sfence();
+  if (i < n) memcpy(dst + i, src + i, n - i);
+}
+
+void stage_copy(void *dst, const void *src, size_t n) {
+  static const bool nt = [] {
+    const char *e = getenv("RQ_HOST_NT");
+    return __builtin_cpu_supports("avx512f") && !(e && atoi(e) == 0);
+  }();
+  if (nt && (reinterpret_cast<uintptr_t>(dst) & 63) == 0)
+    stream_copy_avx512(static_cast<char *>(dst), static_cast<const char *>(src), n);
+  else
+    memcpy(dst, src, n);
 }
 
 void ensure_pinned(double *&buf, size_t &cap, size_t bytes) {
@@ -145,7 +176,7 @@ void run_apply_host_async(const Plan &p, int op, const double *in, double *out, 
       th.emplace_back([&, t] {
         for (size_t i = (size_t)t; i < np; i += (size_t)T) {
           const size_t off = i * PIECE, len = std::min(PIECE, bi - off);
-          memcpy((char *)S.pin_in + off, (const char *)in + off, len);
+          stage_copy((char *)S.pin_in + off, (const char *)in + off, len);
           if (cudaMemcpyAsync((char *)din + off, (char *)S.pin_in + off, len, cudaMemcpyHostToDevice, s_in) !=
               cudaSuccess) { fail[t] = 1; return; }
         }
