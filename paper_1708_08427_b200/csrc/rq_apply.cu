@@ -261,8 +261,7 @@ __global__ void __launch_bounds__(NT_TOP) k_top_df_down(TopDfCtx a) {
 struct Top2Ctx {
   const uint8_t *blob;
   const int64_t *blob_off;
-  const uint8_t *cls;  // shared-memory class per staged body; a launch serves one class
-  int want;
+  const int32_t *order;  // this launch's blobs (one shared-memory class): block b runs blob order[b]
   const int64_t *bead_off;
   const double *in;
   double *out;
@@ -279,13 +278,7 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
-  // every CTA waits for the predecessor grid before exiting, so this grid's completion
-  // always implies the predecessor's (the next kernel's griddepcontrol.wait relies on it)
-  if (a.cls[blockIdx.x] != a.want) {
-    pdl_wait();
-    return;
-  }
-  const uint8_t *gB = a.blob + a.blob_off[blockIdx.x];
+  const uint8_t *gB = a.blob + a.blob_off[a.order[blockIdx.x]];
   // stage the header part (levels, meta, inputs) with one TMA copy; the records stay
   // in global memory (prefetched into L2 here) and are read per node, so the CTA
   // needs little shared memory and many top trees are swept concurrently per SM
@@ -543,7 +536,6 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     RQ_CUDA(cudaMemcpyAsync(ss.in_al.p, cin, 8 * len, cudaMemcpyDeviceToDevice, s));
     cin = ss.in_al.as<double>();
   }
-  const int64_t tb0 = 0, tb1 = p.n_topblob;
   TopDfCtx t{};
   t.starts = p.top_start.as<int32_t>();
   t.paths = p.top_paths.as<int32_t>();
@@ -566,8 +558,7 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t.S = p.tile_leaves;
   Top2Ctx t2{};
   t2.blob = p.topblob.as<uint8_t>();
-  t2.blob_off = p.topblob_off.as<int64_t>() + tb0;
-  t2.cls = p.topblob_class.as<uint8_t>() + tb0;
+  t2.blob_off = p.topblob_off.as<int64_t>();
   t2.bead_off = p.bead_off_d.as<int64_t>();
   t2.in = cin;
   t2.out = cout;
@@ -583,18 +574,19 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
     p.top_attr_set = true;
   }
   const bool do_sweep = (phases & 1u) && p.wave_streams > 0;
-  const bool do_top = (phases & 2u) && (tb1 > tb0 || t.n > 0);
+  const bool do_top = (phases & 2u) && (p.n_topblob > 0 || t.n > 0);
   auto top_pass = [&]() {
-    for (int c = 0; c < 4 && tb1 > tb0; c++) {
-      if (!p.topclass_count[c]) continue;
-      t2.want = c;
+    for (int c = 0; c < 4; c++) {
+      const unsigned nb = (unsigned)(p.topclass_first[c + 1] - p.topclass_first[c]);
+      if (!nb) continue;
+      t2.order = p.topblob_order.as<int32_t>() + p.topclass_first[c];
       const size_t sm = (size_t)p.topclass_smem[c];
       if (c < 2) {
-        if (up) launch_pdl(k_top2<true, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
-        else launch_pdl(k_top2<false, 32>, (unsigned)(tb1 - tb0), 32, sm, s, t2);
+        if (up) launch_pdl(k_top2<true, 32>, nb, 32, sm, s, t2);
+        else launch_pdl(k_top2<false, 32>, nb, 32, sm, s, t2);
       } else {
-        if (up) launch_pdl(k_top2<true, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
-        else launch_pdl(k_top2<false, 128>, (unsigned)(tb1 - tb0), 128, sm, s, t2);
+        if (up) launch_pdl(k_top2<true, 128>, nb, 128, sm, s, t2);
+        else launch_pdl(k_top2<false, 128>, nb, 128, sm, s, t2);
       }
     }
     if (t.n > 0) {

@@ -174,7 +174,9 @@ struct Plan {
   DBuf topblob_off;                // int64 [n_topblob]: blob byte offsets
   DBuf topblob_body;               // int32 [n_topblob]: top-body index (into topbody)
   DBuf topblob_class;              // uint8 [n_topblob]: shared-memory class (one k_top2 launch per class)
+  DBuf topblob_order;              // int32 [n_topblob]: blob indices grouped by class (k_top2 block -> blob)
   int64_t topclass_smem[4] = {0, 0, 0, 0}, topclass_count[4] = {0, 0, 0, 0};
+  int64_t topclass_first[5] = {0, 0, 0, 0, 0};  // class c's blobs: topblob_order[first[c], first[c+1])
   DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
   int64_t n_topbig = 0;
   // dataflow sweep of those big top trees (k_top_df): parent links, arrival counters, start nodes

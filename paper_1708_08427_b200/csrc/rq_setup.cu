@@ -933,7 +933,7 @@ __global__ void k_dup_query(DupCtx c, int64_t N) {
 int64_t Plan::device_bytes() const {
   const DBuf *bufs[] = {&bead_off_d, &node_off_d, &body_centroid, &root_box, &perm, &pos_tree,
                         &pos_orig, &body_of, &start, &stop, &left, &right, &parent, &depth, &axis,
-                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &topblob, &topblob_off, &topblob_body, &topblob_class, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
+                        &flags, &height, &centroid, &t22, &rec_off, &res_off, &rec, &top, &topbody, &topbody_lvl, &toplvl, &small_bodies, &err, &seg_body, &seg_begin, &body_seg, &topblob, &topblob_off, &topblob_body, &topblob_class, &topblob_order, &topbig, &top_parent, &top_need, &top_start, &top_paths, &top_path_off, &mrhs_units, &mrhs_prog,
                         &res_base_d, &wave_desc, &wave_stream_first, &wave_blob};
   int64_t s = 0;
   for (auto b : bufs) s += (int64_t)b->bytes;
@@ -1428,10 +1428,22 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.topblob_body.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
         p.topblob_class.alloc(std::max<int64_t>(p.n_topblob, 1));
         p.topbig.alloc(std::max<int64_t>(p.n_topbig, 1) * 4);
+        // blob indices grouped by class (stable: body order inside a class), so each class launch
+        // runs exactly its own blobs
+        std::vector<int32_t> cls_order;
+        cls_order.reserve(p.n_topblob);
+        for (int c = 0; c < 4; c++) {
+          p.topclass_first[c] = (int64_t)cls_order.size();
+          for (int64_t i = 0; i < p.n_topblob; i++)
+            if (small_cls[i] == c) cls_order.push_back((int32_t)i);
+        }
+        p.topclass_first[4] = (int64_t)cls_order.size();
+        p.topblob_order.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
         if (p.n_topblob) {
           RQ_CUDA(cudaMemcpyAsync(p.topblob_off.p, small_off.data(), p.n_topblob * 8, cudaMemcpyHostToDevice, s));
           RQ_CUDA(cudaMemcpyAsync(p.topblob_body.p, small_tb.data(), p.n_topblob * 4, cudaMemcpyHostToDevice, s));
           RQ_CUDA(cudaMemcpyAsync(p.topblob_class.p, small_cls.data(), p.n_topblob, cudaMemcpyHostToDevice, s));
+          RQ_CUDA(cudaMemcpyAsync(p.topblob_order.p, cls_order.data(), p.n_topblob * 4, cudaMemcpyHostToDevice, s));
         }
         if (p.n_topbig) RQ_CUDA(cudaMemcpyAsync(p.topbig.p, big_tb.data(), p.n_topbig * 4, cudaMemcpyHostToDevice, s));
         DBuf d_blob_off;

@@ -1,4 +1,5 @@
-"""Launch only the top-tree phase of Q~v / Q~^T v on config 2 (for ncu), then time it."""
+"""Launch only the top-tree phase of Q~v / Q~^T v (for ncu), then time it.
+argv: [reps] [bodies] [config]"""
 import ctypes as C
 import sys
 
@@ -9,7 +10,8 @@ import paper_1708_08427_b200 as rq  # noqa: E402
 from paper_1708_08427_b200 import _lib as L  # noqa: E402
 from paper_1708_08427_b200.workloads import make_config  # noqa: E402
 
-pos, off = make_config(2, seed=1000)
+cfg = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+pos, off = make_config(cfg, seed=1000)
 mb = int(sys.argv[2]) if len(sys.argv) > 2 else len(off) - 1
 off = off[: mb + 1]
 pos = pos[: int(off[-1])]
@@ -32,4 +34,4 @@ for name, code, x, o in (("up", L.OP_QTILDE_V, v, ov), ("down", L.OP_QTILDE_TV, 
         L.check(lib.rq_apply_ex(h, code, x.data_ptr(), o.data_ptr(), 1, st, 2))
     b.record(s)
     torch.cuda.synchronize()
-    print(f"m={mb} {name} top {a.elapsed_time(b) / reps * 1e3:.1f} us")
+    print(f"cfg{cfg} m={mb} {name} top {a.elapsed_time(b) / reps * 1e3:.1f} us")
