@@ -116,6 +116,23 @@ __device__ __forceinline__ void ldg_rec(int cs, const double *g, double (&R)[rec
   }
 }
 
+// a node record staged in shared memory (generic loads) into registers
+__device__ __forceinline__ void lds_rec_any(int cs, const double *g, double (&R)[rec_size(GENERAL)]) {
+  const double2 *g2 = reinterpret_cast<const double2 *>(g);
+  const int n2 = rec_size(cs) / 2;
+#pragma unroll
+  for (int i = 0; i < rec_size(GENERAL) / 2; i++) {
+    if (i < n2) {
+      const double2 v = g2[i];
+      R[2 * i] = v.x;
+      R[2 * i + 1] = v.y;
+    } else {
+      R[2 * i] = 0.0;
+      R[2 * i + 1] = 0.0;
+    }
+  }
+}
+
 struct TopDfCtx {
   const int32_t *starts;
   int64_t n;
@@ -272,8 +289,9 @@ struct Top2Ctx {
 };
 
 // NTT threads per top tree: one warp for the small shared-memory classes (top trees
-// of config-2 bodies: ~7 nodes per level), 128 for the large ones
-template <bool UP, int NTT>
+// of config-2 bodies: ~4 nodes per level), 128 for the large ones.  SREC: the records are
+// staged with the rest of the blob (small top trees: no L2 round trip per level).
+template <bool UP, int NTT, bool SREC>
 __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar;
@@ -284,7 +302,7 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   // needs little shared memory and many top trees are swept concurrently per SM
   if (tid == 0) {
     const TopHdr *gh = reinterpret_cast<const TopHdr *>(gB);
-    const unsigned hbytes = (unsigned)gh->off_rec;
+    const unsigned hbytes = SREC ? (unsigned)gh->bytes : (unsigned)gh->off_rec;
     const unsigned rbytes = (unsigned)gh->bytes - hbytes;
     if (rbytes) prefetch_l2(gB + hbytes, rbytes);
     mbar_init(&bar, 1);
@@ -300,9 +318,9 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
   const int32_t *LB = reinterpret_cast<const int32_t *>(smem + sizeof(TopHdr));
   const TopMeta *MD = reinterpret_cast<const TopMeta *>(smem + h.off_meta);
   const int32_t *INREF = reinterpret_cast<const int32_t *>(smem + h.off_in);
-  const double *REC = reinterpret_cast<const double *>(gB + h.off_rec);
+  const double *REC = reinterpret_cast<const double *>((SREC ? smem : gB) + h.off_rec);
   // X | MT: X holds the input info vectors (UP) or the staged residues (DOWN)
-  double *IN = reinterpret_cast<double *>(smem + (h.off_rec + 127) / 128 * 128);
+  double *IN = reinterpret_cast<double *>(smem + ((SREC ? h.bytes : h.off_rec) + 127) / 128 * 128);
   double *RT = IN;
   double *MT = IN + 6 * max(h.n_inputs, h.n_nodes);
   const int64_t K = a.k, col = a.col;
@@ -337,7 +355,8 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
         const TopMeta md = MD[q];
         const int cs = flag_case(md.flags);
         double recv[rec_size(GENERAL)];
-        ldg_rec(cs, REC + md.rec, recv);
+        if (SREC) lds_rec_any(cs, REC + md.rec, recv);
+        else ldg_rec(cs, REC + md.rec, recv);
         const double *rec = recv;
         double mx[6], my[6], mp[6], res[6], aa, bb;
         const double *px = md.x >= 0 ? MT + 6 * md.x : IN + 6 * ~(int)md.x;
@@ -373,7 +392,8 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
         const TopMeta md = MD[q];
         const int cs = flag_case(md.flags);
         double recv[rec_size(GENERAL)];
-        ldg_rec(cs, REC + md.rec, recv);
+        if (SREC) lds_rec_any(cs, REC + md.rec, recv);
+        else ldg_rec(cs, REC + md.rec, recv);
         const double *rec = recv;
         double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6], aa, bb;
 #pragma unroll
@@ -568,25 +588,29 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   t2.res_base = p.res_base_d.as<int64_t>();
   t2.roots = roots;
   if (p.n_topblob && !p.top_attr_set) {
-    for (const void *f2 : {(const void *)k_top2<true, 32>, (const void *)k_top2<false, 32>,
-                           (const void *)k_top2<true, 128>, (const void *)k_top2<false, 128>})
+    for (const void *f2 : {(const void *)k_top2<true, 32, true>, (const void *)k_top2<false, 32, true>,
+                           (const void *)k_top2<true, 32, false>, (const void *)k_top2<false, 32, false>,
+                           (const void *)k_top2<true, 128, false>, (const void *)k_top2<false, 128, false>})
       ensure_smem_attr(f2, (size_t)p.max_topblob_smem);
     p.top_attr_set = true;
   }
   const bool do_sweep = (phases & 1u) && p.wave_streams > 0;
   const bool do_top = (phases & 2u) && (p.n_topblob > 0 || t.n > 0);
   auto top_pass = [&]() {
-    for (int c = 0; c < 4; c++) {
+    for (int c = 0; c < Plan::N_TOPCLASS; c++) {
       const unsigned nb = (unsigned)(p.topclass_first[c + 1] - p.topclass_first[c]);
       if (!nb) continue;
       t2.order = p.topblob_order.as<int32_t>() + p.topclass_first[c];
       const size_t sm = (size_t)p.topclass_smem[c];
-      if (c < 2) {
-        if (up) launch_pdl(k_top2<true, 32>, nb, 32, sm, s, t2);
-        else launch_pdl(k_top2<false, 32>, nb, 32, sm, s, t2);
+      if (c == 0) {
+        if (up) launch_pdl(k_top2<true, 32, true>, nb, 32, sm, s, t2);
+        else launch_pdl(k_top2<false, 32, true>, nb, 32, sm, s, t2);
+      } else if (c < 5) {
+        if (up) launch_pdl(k_top2<true, 32, false>, nb, 32, sm, s, t2);
+        else launch_pdl(k_top2<false, 32, false>, nb, 32, sm, s, t2);
       } else {
-        if (up) launch_pdl(k_top2<true, 128>, nb, 128, sm, s, t2);
-        else launch_pdl(k_top2<false, 128>, nb, 128, sm, s, t2);
+        if (up) launch_pdl(k_top2<true, 128, false>, nb, 128, sm, s, t2);
+        else launch_pdl(k_top2<false, 128, false>, nb, 128, sm, s, t2);
       }
     }
     if (t.n > 0) {

@@ -175,8 +175,11 @@ struct Plan {
   DBuf topblob_body;               // int32 [n_topblob]: top-body index (into topbody)
   DBuf topblob_class;              // uint8 [n_topblob]: shared-memory class (one k_top2 launch per class)
   DBuf topblob_order;              // int32 [n_topblob]: blob indices grouped by class (k_top2 block -> blob)
-  int64_t topclass_smem[4] = {0, 0, 0, 0}, topclass_count[4] = {0, 0, 0, 0};
-  int64_t topclass_first[5] = {0, 0, 0, 0, 0};  // class c's blobs: topblob_order[first[c], first[c+1])
+  // classes: 0 = records staged too; 1..4 = header part staged, <= 8 / 16 / 32 / 64 KB (one warp);
+  // 5 = <= 112 KB (128 threads).  Each launch allocates its class's largest footprint.
+  static constexpr int N_TOPCLASS = 6;
+  int64_t topclass_smem[N_TOPCLASS] = {}, topclass_count[N_TOPCLASS] = {};
+  int64_t topclass_first[N_TOPCLASS + 1] = {};  // class c's blobs: topblob_order[first[c], first[c+1])
   DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
   int64_t n_topbig = 0;
   // dataflow sweep of those big top trees (k_top_df): parent links, arrival counters, start nodes

@@ -1373,24 +1373,43 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         std::vector<uint8_t> small_cls;
         int64_t total = 0;
         p.max_topblob_smem = 0;
-        for (int c = 0; c < 4; c++) p.topclass_smem[c] = p.topclass_count[c] = 0;
+        for (int c = 0; c < Plan::N_TOPCLASS; c++) p.topclass_smem[c] = p.topclass_count[c] = 0;
+        // shared-memory footprints: header part (levels, meta, inputs) + vectors, and with the records
+        std::vector<int64_t> fp(p.n_topbodies), fp_rec(p.n_topbodies);
+        int64_t rec_all = 0;  // largest whole-blob footprint up to 48 KB
+        for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
+          const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
+          const int nn = last - first, ni = h_in[last] - h_in[first];
+          const int64_t bytes = topblob_bytes(nn, h_lvl[bi + 1] - h_lvl[bi], ni, h_rec[last] - h_rec[first]);
+          const int64_t hdr_bytes = bytes - 8 * (h_rec[last] - h_rec[first]);
+          const int64_t vec_bytes = 48 * (int64_t)(std::max(ni, nn) + nn) + 128;
+          fp[bi] = (hdr_bytes + 127) / 128 * 128 + vec_bytes;
+          fp_rec[bi] = (bytes + 127) / 128 * 128 + vec_bytes;
+          if (fp_rec[bi] <= 48 * 1024) rec_all = std::max(rec_all, fp_rec[bi]);
+        }
+        // Records staged too (no L2 round trip per level) when that costs no residency: every top
+        // tree resident at once, else only tiny ones (config 4's 20000 trees run in waves, where
+        // the footprint decides the throughput; measured)
+        if (!p.sms) RQ_CUDA(cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, p.device));
+        const int64_t per_sm = rec_all ? std::min<int64_t>(32, (227 * 1024) / rec_all) : 0;
+        int64_t rec_cap = (rec_all && p.n_topbodies <= per_sm * std::max(p.sms, 1)) ? rec_all : 16 * 1024;
+        if (const char *e = getenv("RQ_TOP_REC_KB")) rec_cap = std::max(0, atoi(e)) * 1024;
         for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
           const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
           const int nn = last - first, nl = h_lvl[bi + 1] - h_lvl[bi], ni = h_in[last] - h_in[first];
           const int64_t bytes = topblob_bytes(nn, nl, ni, h_rec[last] - h_rec[first]);
-          // staged: header, levels, meta and inputs; the records are read from L2 (staging
-          // them too was measured slower: fewer top trees resident per SM)
-          const int64_t hdr_bytes = bytes - 8 * (h_rec[last] - h_rec[first]);
-          const int64_t smem = (hdr_bytes + 127) / 128 * 128 + 48 * (int64_t)(std::max(ni, nn) + nn) + 128;
+          const int64_t smem = fp[bi], smem_rec = fp_rec[bi];
           if (smem <= smem_cap && nn < 32000 && ni < 32000) {
             blob_off[bi] = total;
             small_tb.push_back((int32_t)bi);
             small_off.push_back(total);
             total += bytes;
-            p.max_topblob_smem = std::max(p.max_topblob_smem, smem);
-            const int c = smem <= 32 * 1024 ? 0 : (smem <= 64 * 1024 ? 1 : (smem <= 112 * 1024 ? 2 : 3));
+            const int c = smem_rec <= rec_cap ? 0
+                        : smem <= 8 * 1024 ? 1 : smem <= 16 * 1024 ? 2 : smem <= 32 * 1024 ? 3 : smem <= 64 * 1024 ? 4 : 5;
+            const int64_t sm_c = c == 0 ? smem_rec : smem;
+            p.max_topblob_smem = std::max(p.max_topblob_smem, sm_c);
             small_cls.push_back((uint8_t)c);
-            p.topclass_smem[c] = std::max(p.topclass_smem[c], smem);
+            p.topclass_smem[c] = std::max(p.topclass_smem[c], sm_c);
             p.topclass_count[c]++;
           } else {
             blob_off[bi] = 0;  // unused
@@ -1408,13 +1427,13 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
             const int nn = h_toplvl[h_lvl[bi + 1]] - h_toplvl[h_lvl[bi]], nl = h_lvl[bi + 1] - h_lvl[bi];
             mx_nn = std::max(mx_nn, nn), mx_nl = std::max(mx_nl, nl), s_nn += nn, s_nl += nl;
           }
-          fprintf(stderr, "[rq] top trees: %lld bodies, nodes mean %.1f max %d, levels mean %.1f max %d; staged %lld "
-                  "(classes %lld/%lld/%lld/%lld, smem %lld/%lld/%lld/%lld), global %lld\n",
-                  (long long)p.n_topbodies, s_nn / std::max<int64_t>(1, p.n_topbodies), mx_nn,
-                  s_nl / std::max<int64_t>(1, p.n_topbodies), mx_nl, (long long)p.n_topblob,
-                  (long long)p.topclass_count[0], (long long)p.topclass_count[1], (long long)p.topclass_count[2],
-                  (long long)p.topclass_count[3], (long long)p.topclass_smem[0], (long long)p.topclass_smem[1],
-                  (long long)p.topclass_smem[2], (long long)p.topclass_smem[3], (long long)p.n_topbig);
+          fprintf(stderr, "[rq] top trees: %lld bodies, nodes mean %.1f max %d, levels mean %.1f max %d; staged %lld, "
+                  "global %lld; classes (count/smem):", (long long)p.n_topbodies,
+                  s_nn / std::max<int64_t>(1, p.n_topbodies), mx_nn, s_nl / std::max<int64_t>(1, p.n_topbodies), mx_nl,
+                  (long long)p.n_topblob, (long long)p.n_topbig);
+          for (int c = 0; c < Plan::N_TOPCLASS; c++)
+            fprintf(stderr, " %lld/%lld", (long long)p.topclass_count[c], (long long)p.topclass_smem[c]);
+          fprintf(stderr, "\n");
         }
         auto firsts = [&](const std::vector<int32_t> &list, std::vector<int64_t> &out) {
           out.assign(m + 1, (int64_t)list.size());
@@ -1432,12 +1451,12 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         // runs exactly its own blobs
         std::vector<int32_t> cls_order;
         cls_order.reserve(p.n_topblob);
-        for (int c = 0; c < 4; c++) {
+        for (int c = 0; c < Plan::N_TOPCLASS; c++) {
           p.topclass_first[c] = (int64_t)cls_order.size();
           for (int64_t i = 0; i < p.n_topblob; i++)
             if (small_cls[i] == c) cls_order.push_back((int32_t)i);
         }
-        p.topclass_first[4] = (int64_t)cls_order.size();
+        p.topclass_first[Plan::N_TOPCLASS] = (int64_t)cls_order.size();
         p.topblob_order.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
         if (p.n_topblob) {
           RQ_CUDA(cudaMemcpyAsync(p.topblob_off.p, small_off.data(), p.n_topblob * 8, cudaMemcpyHostToDevice, s));
