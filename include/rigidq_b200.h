@@ -20,8 +20,9 @@
  *  - a plan (tree + factors + apply layout) is immutable after rq_setup;
  *    concurrent rq_apply calls on distinct streams are safe (matfree.py:16-17).
  *    Each stream a plan is used on gets its own exchange state on first use, kept
- *    until rq_plan_free: 48 B per tile root + 4 B per top node, plus (k > 1 column
- *    loop) two k-column staging blocks and (Zf) 48 B per segment and column.
+ *    until rq_plan_release_stream or rq_plan_free: 48 B per tile root + 4 B per top
+ *    node, plus (k > 1 column loop) two k-column staging blocks and (Zf) 48 B per
+ *    segment and column.
  *  - every entry point runs on the plan's device and restores the caller's
  *    current device before returning.
  */
@@ -114,6 +115,10 @@ int rq_plan_free(rq_plan *plan);
 int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info);
 /* Device ordinal the plan lives on. */
 int rq_plan_device(const rq_plan *plan);
+/* Drop the per-stream exchange state the plan holds for `stream` (after synchronising it),
+ * e.g. before a caller destroys a stream it applied the plan on; the next application on
+ * that stream allocates it again.  No reference counterpart (resource management). */
+int rq_plan_release_stream(const rq_plan *plan, void *stream);
 
 /*
  * Operator application on device buffers (replaces upward_apply /

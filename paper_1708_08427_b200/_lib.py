@@ -57,6 +57,7 @@ SIGNATURES = [
     ("rq_plan_free", C.c_int, [_vp]),
     ("rq_plan_get_info", C.c_int, [_vp, C.POINTER(PlanInfo)]),
     ("rq_plan_device", C.c_int, [_vp]),
+    ("rq_plan_release_stream", C.c_int, [_vp, _vp]),
     ("rq_apply", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64, _vp]),
     ("rq_apply_ex", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int64, _vp, C.c_uint32]),
     ("rq_launches_per_apply", C.c_int, [_vp, C.c_int, C.c_int64]),

@@ -95,6 +95,12 @@ class Plan:
         d["n_case"] = list(inf.n_case)
         return d
 
+    def release_stream(self, stream):
+        """Free the exchange state this plan keeps for a CUDA stream (torch.cuda.Stream or raw
+        handle) after synchronising it; rq_plan_release_stream."""
+        h = getattr(stream, "cuda_stream", stream)
+        L.check(L.lib().rq_plan_release_stream(self._h, C.c_void_p(h)))
+
     def _check_device(self, t):
         dev = L.lib().rq_plan_device(self._h)
         if t.device.index != dev:

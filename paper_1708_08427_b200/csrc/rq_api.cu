@@ -109,6 +109,25 @@ int rq_plan_free(rq_plan *plan) {
 
 int rq_plan_device(const rq_plan *plan) { return plan ? plan->p.device : -1; }
 
+int rq_plan_release_stream(const rq_plan *plan, void *stream) {
+  RQ_GUARD({
+    need_plan(plan);
+    PLAN_DEVICE(plan);
+    const rq::Plan &p = plan->p;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::unique_ptr<rq::Plan::StreamState> st;
+    {
+      std::lock_guard<std::mutex> lock(p.state_mu);
+      auto it = p.stream_state.find(s);
+      if (it != p.stream_state.end()) {
+        st = std::move(it->second);
+        p.stream_state.erase(it);
+      }
+    }
+    if (st) RQ_CUDA(cudaStreamSynchronize(s));  // its buffers may still be in use by queued work
+  })
+}
+
 int rq_plan_get_info(const rq_plan *plan, rq_plan_info *info) {
   RQ_GUARD({
     need_plan(plan);

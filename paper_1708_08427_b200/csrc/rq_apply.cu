@@ -602,15 +602,19 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
       if (!nb) continue;
       t2.order = p.topblob_order.as<int32_t>() + p.topclass_first[c];
       const size_t sm = (size_t)p.topclass_smem[c];
-      if (c == 0) {
-        if (up) launch_pdl(k_top2<true, 32, true>, nb, 32, sm, s, t2);
-        else launch_pdl(k_top2<false, 32, true>, nb, 32, sm, s, t2);
-      } else if (c < 5) {
-        if (up) launch_pdl(k_top2<true, 32, false>, nb, 32, sm, s, t2);
-        else launch_pdl(k_top2<false, 32, false>, nb, 32, sm, s, t2);
-      } else {
+      static const int wide_from = [] {  // classes from here on run 128 threads per top tree
+        const char *e = getenv("RQ_TOP_WIDE_CLASS");
+        return e ? atoi(e) : 4;  // config 4: the <= 64 KB class's wide levels (measured -5%)
+      }();
+      if (c >= wide_from) {
         if (up) launch_pdl(k_top2<true, 128, false>, nb, 128, sm, s, t2);
         else launch_pdl(k_top2<false, 128, false>, nb, 128, sm, s, t2);
+      } else if (c == 0) {
+        if (up) launch_pdl(k_top2<true, 32, true>, nb, 32, sm, s, t2);
+        else launch_pdl(k_top2<false, 32, true>, nb, 32, sm, s, t2);
+      } else {
+        if (up) launch_pdl(k_top2<true, 32, false>, nb, 32, sm, s, t2);
+        else launch_pdl(k_top2<false, 32, false>, nb, 32, sm, s, t2);
       }
     }
     if (t.n > 0) {

@@ -864,8 +864,8 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
   Plan::StreamState &ss = p.state_for(s);
   if (ss.mrhs_scratch.bytes < scratch_bytes) ss.mrhs_scratch.alloc(scratch_bytes);
   if (ss.mrhs_tx.bytes < tx_bytes) ss.mrhs_tx.alloc(tx_bytes);
-  int sms = 0;
-  RQ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+  if (!p.sms) RQ_CUDA(cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, p.device));
+  const int sms = p.sms;
   MrhsCtx a{};
   a.prog = p.mrhs_prog.as<uint8_t>();
   a.bead_off = p.bead_off_d.as<int64_t>();
@@ -887,8 +887,7 @@ void run_apply_mrhs(const Plan &p, int op, const double *in, double *out, int64_
     else if (up) fn = mode == 0 ? k_mrhs<true, 0, 4> : (mode == 1 ? k_mrhs<true, 1, 4> : k_mrhs<true, 2, 4>);
     else fn = mode == 0 ? k_mrhs<false, 0, 4> : (mode == 1 ? k_mrhs<false, 1, 4> : k_mrhs<false, 2, 4>);
     ensure_smem_attr((const void *)fn, smem);
-    int occ = 0;
-    RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)fn, MRHS_NT, smem));
+    const int occ = occupancy_cached((const void *)fn, MRHS_NT, smem);
     if (occ < 1) throw Error(RQ_ERR_CUDA, "multi-RHS kernel does not fit on an SM");
     const int64_t items = a.n_units * a.n_cg;
     const int64_t blocks = std::min<int64_t>((items + MRHS_NT / 32 - 1) / (MRHS_NT / 32), (int64_t)sms * occ);

@@ -254,7 +254,8 @@ struct Plan {
   int64_t wave_streams = 0, wave_steps = 0, wave_blob_bytes = 0, wave_nodes = 0;
   int64_t wave_up_bytes = 0, wave_down_bytes = 0;  // bytes one upward / downward sweep streams
   int64_t wave_stage_bytes = 0, wave_rounds = 1;
-  int wave_window = 0, sms = 0;         // run-time round window (rounds); SM count
+  int wave_window = 0;                  // run-time round window (rounds)
+  mutable int sms = 0;                  // SM count of the plan's device
   int wave_mslots = 0, wave_nst = 2;  // TMA stages (fixed 2: the headers locate the block two steps ahead)
   WaveCaps wave_caps;
   DBuf wave_desc;                  // StepDesc [wave_steps]
@@ -291,6 +292,9 @@ struct WaveBuildIn {
 // The attribute is process-wide, so it only ever grows: a plan with a smaller footprint never
 // lowers it under a bigger plan's launches (other threads included).
 void ensure_smem_attr(const void *f, size_t bytes);
+// CTAs per SM of kernel f at (threads, dynamic smem) on the current device, memoised (the
+// multi-RHS launches ask on every application)
+int occupancy_cached(const void *f, int threads, size_t smem);
 void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s);
 size_t wave_smem(const Plan &p, uint32_t *o_m, uint32_t *o_v, uint32_t *vreg);
 void wave_prepare(const Plan &p);

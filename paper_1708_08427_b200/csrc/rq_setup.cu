@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <thread>
 #include <vector>
@@ -1367,7 +1368,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         d2h(h_in.data(), in_scan.p, nt + 1, s);
         d2h(h_rec.data(), rec_scan.p, nt + 1, s);
         int64_t smem_cap = 112 * 1024;  // larger top trees go to the dataflow kernels (measured on config 4)
-        if (const char *e = getenv("RQ_TOP_SMEM_KB")) smem_cap = std::max(16, atoi(e)) * 1024;
+        if (const char *e = getenv("RQ_TOP_SMEM_KB")) smem_cap = std::max(0, atoi(e)) * 1024;
         std::vector<int64_t> blob_off(p.n_topbodies, -1), small_off;
         std::vector<int32_t> small_tb, big_tb;
         std::vector<uint8_t> small_cls;
@@ -1663,6 +1664,21 @@ void ensure_smem_attr(const void *f, size_t bytes) {
     }
   RQ_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   set.push_back({{dev, f}, bytes});
+}
+
+int occupancy_cached(const void *f, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::tuple<int, const void *, int, size_t>, int>> memo;  // -> CTAs per SM
+  int dev = 0;
+  RQ_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, f, threads, smem);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : memo)
+    if (e.first == key) return e.second;
+  int occ = 0;
+  RQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, threads, smem));
+  memo.push_back({key, occ});
+  return occ;
 }
 
 }  // namespace rq
