@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, in
       v.beads = (int16_t)wv_beads(cs);
       v.vd = (int16_t)((rr ? 2 * wv_pieces(rb + A.res_off[q] - 6, rr) : 0) + 6 * root);
       v.dg = (int16_t)((rr > 0) + root);
-      v.rm = 8 * rec_size(cs) + 16;
+      v.rm = 8 * wave_rec_size(cs) + 16;
       int st = ready;
       for (;; st++) {
         if (st - floor >= WRING) { atomicExch(bad, 1); return; }
@@ -449,12 +449,16 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
   uint8_t *B = w.blob + ((int64_t)D.off16 << 4);
   // record
   int rq_off;
-  if (cs == GENERAL) rq_off = pos * rec_size(GENERAL);
-  else if (cs == RIGID_BEAD) rq_off = D.nG * rec_size(GENERAL) + (pos - D.nG) * rec_size(RIGID_BEAD);
-  else rq_off = D.nG * rec_size(GENERAL) + D.nR * rec_size(RIGID_BEAD) + (pos - D.nG - D.nR) * rec_size(BEAD_BEAD);
+  if (cs == GENERAL) rq_off = pos * wave_rec_size(GENERAL);
+  else if (cs == RIGID_BEAD) rq_off = D.nG * wave_rec_size(GENERAL) + (pos - D.nG) * wave_rec_size(RIGID_BEAD);
+  else
+    rq_off = D.nG * wave_rec_size(GENERAL) + D.nR * wave_rec_size(RIGID_BEAD) +
+             (pos - D.nG - D.nR) * wave_rec_size(BEAD_BEAD);
   double *R = reinterpret_cast<double *>(B + S.rec) + rq_off;
   const double *src = w.rec + A.rec_off[g];
-  for (int e = 0; e < rec_size(cs); e++) R[e] = src[e];
+  if (cs == GENERAL) wave_pack_wy<9>(src, R);
+  else if (cs == RIGID_BEAD) wave_pack_wy<6>(src, R);
+  else for (int e = 0; e < rec_size(cs); e++) R[e] = src[e];
   // children in formula order
   const int j = A.node_body[g];
   const int64_t nb0 = A.node_off[j], b0 = A.bead_off[j];
@@ -873,14 +877,58 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// packed wave record -> compact-WY record in registers: T's off-diagonal entries rebuilt from
+// V and the taus exactly as lq_factor forms them (no FMA contraction: bit-identical)
+template <int K>
+__device__ __forceinline__ void unpack_wy(const double *P, double (&R)[rec_size(K == 9 ? GENERAL : RIGID_BEAD)]) {
+  using W = WY<K>;
+  const double2 *p2 = reinterpret_cast<const double2 *>(P);
+  double Q[wave_rec_size(K == 9 ? GENERAL : RIGID_BEAD)];
+#pragma unroll
+  for (int i = 0; i < wave_rec_size(K == 9 ? GENERAL : RIGID_BEAD) / 2; i++) {
+    const double2 v = p2[i];
+    Q[2 * i] = v.x;
+    Q[2 * i + 1] = v.y;
+  }
+#pragma unroll
+  for (int e = 0; e < W::T; e++) R[e] = Q[e];
+  // v_i^T v_j (i < j; v_i[i] = 1, v_j[j] = 1, v_j[r < j] = 0); A[i*K + r] = V_i[r - i - 1]
+  auto Vv = [&](int i, int r) -> double { return Q[(i == 0 ? W::V0 : (i == 1 ? W::V1 : W::V2)) + r - i - 1]; };
+  auto vdot = [&](int i, int j) {
+    double d = Vv(i, j);
+#pragma unroll
+    for (int r = j + 1; r < K; r++) d = __dadd_rn(d, __dmul_rn(Vv(i, r), Vv(j, r)));
+    return d;
+  };
+  const double T00 = Q[W::T + 0], T11 = Q[W::T + 1], T22 = Q[W::T + 2];
+  const double T01 = __dmul_rn(__dmul_rn(-T11, T00), vdot(0, 1));
+  const double t0 = vdot(0, 2), t1 = vdot(1, 2);
+  const double T02 = __dmul_rn(-T22, __dadd_rn(__dmul_rn(T00, t0), __dmul_rn(T01, t1)));
+  const double T12 = __dmul_rn(-T22, __dmul_rn(T11, t1));
+  R[W::T + 0] = T00;
+  R[W::T + 1] = T01;
+  R[W::T + 2] = T02;
+  R[W::T + 3] = T11;
+  R[W::T + 4] = T12;
+  R[W::T + 5] = T22;
+  R[W::RA] = Q[W::T + 3];
+  R[W::RB] = Q[W::T + 4];
+}
+
 template <int CS>
 __device__ __forceinline__ void ld_rec(const double *rec, double (&R)[rec_size(CS)]) {
-  const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+  if constexpr (CS == GENERAL) {
+    unpack_wy<9>(rec, R);
+  } else if constexpr (CS == RIGID_BEAD) {
+    unpack_wy<6>(rec, R);
+  } else {
+    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
 #pragma unroll
-  for (int i = 0; i < rec_size(CS) / 2; i++) {
-    const double2 v = r2[i];
-    R[2 * i] = v.x;
-    R[2 * i + 1] = v.y;
+    for (int i = 0; i < rec_size(CS) / 2; i++) {
+      const double2 v = r2[i];
+      R[2 * i] = v.x;
+      R[2 * i + 1] = v.y;
+    }
   }
 }
 __device__ __forceinline__ void ld6(const double *q, double (&v)[6]) {
@@ -1109,7 +1157,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       const int gG = (nG + 31) & ~31, gR = (nR + 31) & ~31;
       const int tot = gG + gR + nB;
       const double *R = reinterpret_cast<const double *>(B + h.o_rec);
-      const int oR = rec_size(GENERAL) * nG, oB = oR + rec_size(RIGID_BEAD) * nR;
+      const int oR = wave_rec_size(GENERAL) * nG, oB = oR + wave_rec_size(RIGID_BEAD) * nR;
       if (UP) {
         const WaveUpMeta *UM = reinterpret_cast<const WaveUpMeta *>(B + h.o_meta);
         if (RQ_DEBUG_CHECKS)
@@ -1123,14 +1171,14 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           }
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
-            if (q < nG) wv_up<GENERAL>(R + q * rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
+            if (q < nG) wv_up<GENERAL>(R + q * wave_rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
           } else if (q < gG + gR) {
             const int qq = q - gG;
             if (qq < nR)
-              wv_up<RIGID_BEAD>(R + oR + qq * rec_size(RIGID_BEAD), UM + nG + qq, M, V, a.out, a.scratch, a.roots);
+              wv_up<RIGID_BEAD>(R + oR + qq * wave_rec_size(RIGID_BEAD), UM + nG + qq, M, V, a.out, a.scratch, a.roots);
           } else {
             const int qq = q - gG - gR;
-            wv_up<BEAD_BEAD>(R + oB + qq * rec_size(BEAD_BEAD), UM + nG + nR + qq, M, V, a.out, a.scratch, a.roots);
+            wv_up<BEAD_BEAD>(R + oB + qq * wave_rec_size(BEAD_BEAD), UM + nG + nR + qq, M, V, a.out, a.scratch, a.roots);
           }
         }
       } else {
@@ -1148,13 +1196,13 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           }
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
-            if (q < nG) wv_down<GENERAL>(R + q * rec_size(GENERAL), DM + q, M, V, a.out);
+            if (q < nG) wv_down<GENERAL>(R + q * wave_rec_size(GENERAL), DM + q, M, V, a.out);
           } else if (q < gG + gR) {
             const int qq = q - gG;
-            if (qq < nR) wv_down<RIGID_BEAD>(R + oR + qq * rec_size(RIGID_BEAD), DM + nG + qq, M, V, a.out);
+            if (qq < nR) wv_down<RIGID_BEAD>(R + oR + qq * wave_rec_size(RIGID_BEAD), DM + nG + qq, M, V, a.out);
           } else {
             const int qq = q - gG - gR;
-            wv_down<BEAD_BEAD>(R + oB + qq * rec_size(BEAD_BEAD), DM + nG + nR + qq, M, V, a.out);
+            wv_down<BEAD_BEAD>(R + oB + qq * wave_rec_size(BEAD_BEAD), DM + nG + nR + qq, M, V, a.out);
           }
         }
       }

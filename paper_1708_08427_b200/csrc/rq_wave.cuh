@@ -100,8 +100,29 @@ struct WaveSec {  // byte offsets inside a block
   __host__ __device__ uint32_t up0() const { return uhdr; }
   __host__ __device__ uint32_t dn_end() const { return um; }
 };
+// Records in the step blocks are packed: a GENERAL / RIGID_BEAD compact-WY record keeps V,
+// the diagonal of T (tau0, tau1, tau2) and the ratios a, b; the sweep rebuilds T's three
+// off-diagonal entries from V and the taus with the setup's own operations (lq_factor,
+// rq_lq.cuh), so they are bit-identical.  GENERAL 26 (vs 30), RIGID_BEAD 18 (vs 20, padded to
+// 16-byte alignment), BEAD_BEAD 10 doubles: the blocks stream ~7% fewer bytes.
+//   V0 (K-1) | V1 (K-2) | V2 (K-3) | tau0 tau1 tau2 | a b [| pad]
+__host__ __device__ constexpr int wave_rec_size(int c) {
+  return c == BEAD_BEAD ? 10 : (c == RIGID_BEAD ? 18 : (c == GENERAL ? 26 : 0));
+}
 __host__ __device__ inline uint32_t wave_rec_bytes(uint32_t nG, uint32_t nR, uint32_t nB) {
-  return 8u * (rec_size(GENERAL) * nG + rec_size(RIGID_BEAD) * nR + rec_size(BEAD_BEAD) * nB);
+  return 8u * (wave_rec_size(GENERAL) * nG + wave_rec_size(RIGID_BEAD) * nR + wave_rec_size(BEAD_BEAD) * nB);
+}
+// compact-WY record (WY<K> layout, T upper part + ratios) -> packed wave record
+template <int K>
+__host__ __device__ inline void wave_pack_wy(const double *src, double *dst) {
+  using W = WY<K>;
+  for (int e = 0; e < W::T; e++) dst[e] = src[e];  // V
+  dst[W::T + 0] = src[W::T + 0];                   // tau0 = T00
+  dst[W::T + 1] = src[W::T + 3];                   // tau1 = T11
+  dst[W::T + 2] = src[W::T + 5];                   // tau2 = T22
+  dst[W::T + 3] = src[W::RA];
+  dst[W::T + 4] = src[W::RB];
+  if ((W::T + 5) & 1) dst[W::T + 5] = 0.0;         // pad to an even count
 }
 __host__ __device__ inline WaveSec wave_sections(uint32_t nG, uint32_t nR, uint32_t nB, uint32_t n_ug,
                                                  uint32_t n_dg) {
