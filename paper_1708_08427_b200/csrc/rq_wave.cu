@@ -456,9 +456,10 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
              (pos - D.nG - D.nR) * wave_rec_size(BEAD_BEAD);
   double *R = reinterpret_cast<double *>(B + S.rec) + rq_off;
   const double *src = w.rec + A.rec_off[g];
+  bool bb_neg = false;
   if (cs == GENERAL) wave_pack_wy<9>(src, R);
   else if (cs == RIGID_BEAD) wave_pack_wy<6>(src, R);
-  else for (int e = 0; e < rec_size(cs); e++) R[e] = src[e];
+  else bb_neg = wave_pack_bb(src, R);
   // children in formula order
   const int j = A.node_body[g];
   const int64_t nb0 = A.node_off[j], b0 = A.bead_off[j];
@@ -474,7 +475,7 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
   auto orig_bead = [&](int id) -> uint32_t { return (uint32_t)(b0 + A.perm[b0 + A.start[nb0 + id]]); };
   WaveUpMeta um;
   WaveDnMeta dm;
-  um.flags = dm.flags = (uint16_t)((f & 0x3fu) | rf);
+  um.flags = dm.flags = (uint16_t)((f & 0x3fu) | rf | (bb_neg ? WF_BB_NEG : 0));
   um.self = dm.self = 0;
   dm.pad = 0;
   um.row = 0;
@@ -921,13 +922,20 @@ __device__ __forceinline__ void ld_rec(const double *rec, double (&R)[rec_size(C
     unpack_wy<9>(rec, R);
   } else if constexpr (CS == RIGID_BEAD) {
     unpack_wy<6>(rec, R);
-  } else {
+  } else {  // BEAD_BEAD: the sign of g is applied by the caller (meta flag WF_BB_NEG)
     const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+    const double2 q01 = r2[0], q23 = r2[1];
+    const double q[4] = {q01.x, q01.y, q23.x, q23.y};
+    wave_unpack_bb(q, false, R);
+  }
+}
+// BEAD_BEAD with det g = -1: g = -R(q)
+template <int CS>
+__device__ __forceinline__ void bb_sign(unsigned flags, double (&R)[rec_size(CS)]) {
+  if constexpr (CS == BEAD_BEAD) {
+    if (flags & WF_BB_NEG) {
 #pragma unroll
-    for (int i = 0; i < rec_size(CS) / 2; i++) {
-      const double2 v = r2[i];
-      R[2 * i] = v.x;
-      R[2 * i + 1] = v.y;
+      for (int e = 0; e < 9; e++) R[e] = -R[e];
     }
   }
 }
@@ -953,6 +961,7 @@ __device__ __forceinline__ void wv_up(const double *rec, const WaveUpMeta *UMp, 
   double R[rec_size(CS)];
   ld_rec<CS>(rec, R);
   const WaveUpMeta md = *UMp;
+  bb_sign<CS>(md.flags, R);
   double mx[6], my[6];
   if (CS == BEAD_BEAD) {
     const double *f = V + md.x;
@@ -992,6 +1001,7 @@ __device__ __forceinline__ void wv_down(const double *rec, const WaveDnMeta *DMp
   double R[rec_size(CS)];
   ld_rec<CS>(rec, R);
   const WaveDnMeta md = *DMp;
+  bb_sign<CS>(md.flags, R);
   double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
   if (md.flags & (WF_TILE_ROOT | WF_BODY_ROOT)) {
     const double *q = V + md.self;

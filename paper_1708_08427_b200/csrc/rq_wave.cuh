@@ -75,6 +75,7 @@ enum : uint16_t { WG_RES3 = 0, WG_RES6 = 1, WG_SLOT = 2, WG_ROOT = 3 };
 // meta flag bits above the node flags (bits 0-5: case | swapped | signs)
 constexpr uint16_t WF_TILE_ROOT = 1u << 6;  // output to / input from an exchange slot
 constexpr uint16_t WF_BODY_ROOT = 1u << 7;  // the body root (output to / input from `roots`)
+constexpr uint16_t WF_BB_NEG = 1u << 8;     // BEAD_BEAD: g = -R(q) (det g = -1)
 
 __host__ __device__ inline uint32_t al16u(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -104,10 +105,47 @@ struct WaveSec {  // byte offsets inside a block
 // the diagonal of T (tau0, tau1, tau2) and the ratios a, b; the sweep rebuilds T's three
 // off-diagonal entries from V and the taus with the setup's own operations (lq_factor,
 // rq_lq.cuh), so they are bit-identical.  GENERAL 26 (vs 30), RIGID_BEAD 18 (vs 20, padded to
-// 16-byte alignment), BEAD_BEAD 10 doubles: the blocks stream ~7% fewer bytes.
-//   V0 (K-1) | V1 (K-2) | V2 (K-3) | tau0 tau1 tau2 | a b [| pad]
+// 16-byte alignment).  A BEAD_BEAD node's 3x3 g is orthogonal (the mixer of two beads is,
+// factor.py:130-170), so the blocks carry it as a unit quaternion q (4 doubles vs 10) and a
+// flag bit for det g = -1 (g = -R(q)); the sweep rebuilds g to ~1 ulp.
+//   V0 (K-1) | V1 (K-2) | V2 (K-3) | tau0 tau1 tau2 | a b [| pad]        q_w q_x q_y q_z
 __host__ __device__ constexpr int wave_rec_size(int c) {
-  return c == BEAD_BEAD ? 10 : (c == RIGID_BEAD ? 18 : (c == GENERAL ? 26 : 0));
+  return c == BEAD_BEAD ? 4 : (c == RIGID_BEAD ? 18 : (c == GENERAL ? 26 : 0));
+}
+// g (3x3 row-major, orthogonal) -> unit quaternion of s g with s = sign(det g) (Shepperd's
+// method: the largest of the four squared components is taken from the diagonal)
+__host__ __device__ inline bool wave_pack_bb(const double *g, double *q) {
+  const double det = g[0] * (g[4] * g[8] - g[5] * g[7]) - g[1] * (g[3] * g[8] - g[5] * g[6]) +
+                     g[2] * (g[3] * g[7] - g[4] * g[6]);
+  const double sg = det < 0.0 ? -1.0 : 1.0;
+  double M[9];
+  for (int e = 0; e < 9; e++) M[e] = sg * g[e];
+  const double tr = M[0] + M[4] + M[8];
+  double w, x, y, z;
+  if (tr > 0.0) {
+    const double s = 2.0 * sqrt(tr + 1.0);
+    w = 0.25 * s; x = (M[7] - M[5]) / s; y = (M[2] - M[6]) / s; z = (M[3] - M[1]) / s;
+  } else if (M[0] > M[4] && M[0] > M[8]) {
+    const double s = 2.0 * sqrt(1.0 + M[0] - M[4] - M[8]);
+    w = (M[7] - M[5]) / s; x = 0.25 * s; y = (M[1] + M[3]) / s; z = (M[2] + M[6]) / s;
+  } else if (M[4] > M[8]) {
+    const double s = 2.0 * sqrt(1.0 + M[4] - M[0] - M[8]);
+    w = (M[2] - M[6]) / s; x = (M[1] + M[3]) / s; y = 0.25 * s; z = (M[5] + M[7]) / s;
+  } else {
+    const double s = 2.0 * sqrt(1.0 + M[8] - M[0] - M[4]);
+    w = (M[3] - M[1]) / s; x = (M[2] + M[6]) / s; y = (M[5] + M[7]) / s; z = 0.25 * s;
+  }
+  const double nrm = sqrt(w * w + x * x + y * y + z * z);
+  q[0] = w / nrm; q[1] = x / nrm; q[2] = y / nrm; q[3] = z / nrm;
+  return det < 0.0;
+}
+// unit quaternion -> rotation (row-major), negated when neg
+__host__ __device__ inline void wave_unpack_bb(const double *q, bool neg, double *g) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  const double s = neg ? -2.0 : 2.0, one = neg ? -1.0 : 1.0;
+  g[0] = one - s * (y * y + z * z); g[1] = s * (x * y - w * z);       g[2] = s * (x * z + w * y);
+  g[3] = s * (x * y + w * z);       g[4] = one - s * (x * x + z * z); g[5] = s * (y * z - w * x);
+  g[6] = s * (x * z - w * y);       g[7] = s * (y * z + w * x);       g[8] = one - s * (x * x + y * y);
 }
 __host__ __device__ inline uint32_t wave_rec_bytes(uint32_t nG, uint32_t nR, uint32_t nB) {
   return 8u * (wave_rec_size(GENERAL) * nG + wave_rec_size(RIGID_BEAD) * nR + wave_rec_size(BEAD_BEAD) * nB);
