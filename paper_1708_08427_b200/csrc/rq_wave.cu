@@ -449,16 +449,17 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
   uint8_t *B = w.blob + ((int64_t)D.off16 << 4);
   // record
   int rq_off;
-  if (cs == GENERAL) rq_off = pos * wave_rec_size(GENERAL);
-  else if (cs == RIGID_BEAD) rq_off = D.nG * wave_rec_size(GENERAL) + (pos - D.nG) * wave_rec_size(RIGID_BEAD);
-  else
-    rq_off = D.nG * wave_rec_size(GENERAL) + D.nR * wave_rec_size(RIGID_BEAD) +
-             (pos - D.nG - D.nR) * wave_rec_size(BEAD_BEAD);
+  // record groups BEAD_BEAD | RIGID_BEAD | GENERAL (GENERAL's odd size last, so the others stay
+  // 16-byte aligned); meta / node positions keep the G | R | B order
+  if (cs == BEAD_BEAD) rq_off = (pos - D.nG - D.nR) * wave_rec_size(BEAD_BEAD);
+  else if (cs == RIGID_BEAD) rq_off = D.nB * wave_rec_size(BEAD_BEAD) + (pos - D.nG) * wave_rec_size(RIGID_BEAD);
+  else rq_off = D.nB * wave_rec_size(BEAD_BEAD) + D.nR * wave_rec_size(RIGID_BEAD) + pos * wave_rec_size(GENERAL);
   double *R = reinterpret_cast<double *>(B + S.rec) + rq_off;
   const double *src = w.rec + A.rec_off[g];
   bool bb_neg = false;
-  if (cs == GENERAL) wave_pack_wy<9>(src, R);
-  else if (cs == RIGID_BEAD) wave_pack_wy<6>(src, R);
+  unsigned tau_zero = 0;
+  if (cs == GENERAL) tau_zero = wave_pack_wy<9>(src, R);
+  else if (cs == RIGID_BEAD) tau_zero = wave_pack_wy<6>(src, R);
   else bb_neg = wave_pack_bb(src, R);
   // children in formula order
   const int j = A.node_body[g];
@@ -475,7 +476,7 @@ __global__ void k_wv_write(WriteIn w, int64_t n) {
   auto orig_bead = [&](int id) -> uint32_t { return (uint32_t)(b0 + A.perm[b0 + A.start[nb0 + id]]); };
   WaveUpMeta um;
   WaveDnMeta dm;
-  um.flags = dm.flags = (uint16_t)((f & 0x3fu) | rf | (bb_neg ? WF_BB_NEG : 0));
+  um.flags = dm.flags = (uint16_t)((f & 0x3fu) | rf | (bb_neg ? WF_BB_NEG : 0) | (tau_zero << WF_TAU_ZERO_SHIFT));
   um.self = dm.self = 0;
   dm.pad = 0;
   um.row = 0;
@@ -878,51 +879,70 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// packed wave record -> compact-WY record in registers: T's off-diagonal entries rebuilt from
-// V and the taus exactly as lq_factor forms them (no FMA contraction: bit-identical)
+// packed wave record -> compact-WY record in registers: tau_i = 2 / (v_i^T v_i) (0 when the
+// node's flag says so) and T's off-diagonal entries as lq_factor forms them (rq_lq.cuh)
 template <int K>
-__device__ __forceinline__ void unpack_wy(const double *P, double (&R)[rec_size(K == 9 ? GENERAL : RIGID_BEAD)]) {
+__device__ __forceinline__ void unpack_wy(const double *P, unsigned flags,
+                                          double (&R)[rec_size(K == 9 ? GENERAL : RIGID_BEAD)]) {
   using W = WY<K>;
-  const double2 *p2 = reinterpret_cast<const double2 *>(P);
-  double Q[wave_rec_size(K == 9 ? GENERAL : RIGID_BEAD)];
+  constexpr int NQ = wave_rec_size(K == 9 ? GENERAL : RIGID_BEAD);
+  double Q[NQ];
+  if constexpr (NQ % 2 == 0) {
+    const double2 *p2 = reinterpret_cast<const double2 *>(P);
 #pragma unroll
-  for (int i = 0; i < wave_rec_size(K == 9 ? GENERAL : RIGID_BEAD) / 2; i++) {
-    const double2 v = p2[i];
-    Q[2 * i] = v.x;
-    Q[2 * i + 1] = v.y;
+    for (int i = 0; i < NQ / 2; i++) {
+      const double2 v = p2[i];
+      Q[2 * i] = v.x;
+      Q[2 * i + 1] = v.y;
+    }
+  } else {  // odd size: 8-byte loads
+#pragma unroll
+    for (int i = 0; i < NQ; i++) Q[i] = P[i];
   }
 #pragma unroll
   for (int e = 0; e < W::T; e++) R[e] = Q[e];
-  // v_i^T v_j (i < j; v_i[i] = 1, v_j[j] = 1, v_j[r < j] = 0); A[i*K + r] = V_i[r - i - 1]
+  // v_i (v_i[i] = 1, v_i[r < i] = 0, v_i[r > i] = V_i[r - i - 1])
   auto Vv = [&](int i, int r) -> double { return Q[(i == 0 ? W::V0 : (i == 1 ? W::V1 : W::V2)) + r - i - 1]; };
-  auto vdot = [&](int i, int j) {
+  auto vdot = [&](int i, int j) {  // v_i^T v_j, i < j
     double d = Vv(i, j);
 #pragma unroll
-    for (int r = j + 1; r < K; r++) d = __dadd_rn(d, __dmul_rn(Vv(i, r), Vv(j, r)));
+    for (int r = j + 1; r < K; r++) d = fma(Vv(i, r), Vv(j, r), d);
     return d;
   };
-  const double T00 = Q[W::T + 0], T11 = Q[W::T + 1], T22 = Q[W::T + 2];
-  const double T01 = __dmul_rn(__dmul_rn(-T11, T00), vdot(0, 1));
+  auto vnorm2 = [&](int i) {
+    double d = 1.0;
+#pragma unroll
+    for (int r = i + 1; r < K; r++) d = fma(Vv(i, r), Vv(i, r), d);
+    return d;
+  };
+  // the three taus from one division: tau_i = 2 / s_i
+  const double s0 = vnorm2(0), s1 = vnorm2(1), s2 = vnorm2(2);
+  const double s01 = s0 * s1, r = 2.0 / (s01 * s2);
+  const unsigned tz = flags >> WF_TAU_ZERO_SHIFT;
+  const double T00 = (tz & 1u) ? 0.0 : r * (s1 * s2);
+  const double T11 = (tz & 2u) ? 0.0 : r * (s0 * s2);
+  const double T22 = (tz & 4u) ? 0.0 : r * s01;
+  const double T01 = -T11 * T00 * vdot(0, 1);
   const double t0 = vdot(0, 2), t1 = vdot(1, 2);
-  const double T02 = __dmul_rn(-T22, __dadd_rn(__dmul_rn(T00, t0), __dmul_rn(T01, t1)));
-  const double T12 = __dmul_rn(-T22, __dmul_rn(T11, t1));
+  const double T02 = -T22 * (T00 * t0 + T01 * t1);
+  const double T12 = -T22 * (T11 * t1);
   R[W::T + 0] = T00;
   R[W::T + 1] = T01;
   R[W::T + 2] = T02;
   R[W::T + 3] = T11;
   R[W::T + 4] = T12;
   R[W::T + 5] = T22;
-  R[W::RA] = Q[W::T + 3];
-  R[W::RB] = Q[W::T + 4];
+  R[W::RA] = Q[W::T + 0];
+  R[W::RB] = Q[W::T + 1];
 }
 
 template <int CS>
-__device__ __forceinline__ void ld_rec(const double *rec, double (&R)[rec_size(CS)]) {
+__device__ __forceinline__ void ld_rec(const double *rec, unsigned flags, double (&R)[rec_size(CS)]) {
   if constexpr (CS == GENERAL) {
-    unpack_wy<9>(rec, R);
+    unpack_wy<9>(rec, flags, R);
   } else if constexpr (CS == RIGID_BEAD) {
-    unpack_wy<6>(rec, R);
-  } else {  // BEAD_BEAD: the sign of g is applied by the caller (meta flag WF_BB_NEG)
+    unpack_wy<6>(rec, flags, R);
+  } else {  // BEAD_BEAD: the sign of g is applied by bb_sign (meta flag WF_BB_NEG)
     const double2 *r2 = reinterpret_cast<const double2 *>(rec);
     const double2 q01 = r2[0], q23 = r2[1];
     const double q[4] = {q01.x, q01.y, q23.x, q23.y};
@@ -959,8 +979,8 @@ template <int CS>
 __device__ __forceinline__ void wv_up(const double *rec, const WaveUpMeta *UMp, double *M, const double *V,
                                       double *out, double *scratch, double *roots) {
   double R[rec_size(CS)];
-  ld_rec<CS>(rec, R);
   const WaveUpMeta md = *UMp;
+  ld_rec<CS>(rec, md.flags, R);
   bb_sign<CS>(md.flags, R);
   double mx[6], my[6];
   if (CS == BEAD_BEAD) {
@@ -999,8 +1019,8 @@ template <int CS>
 __device__ __forceinline__ void wv_down(const double *rec, const WaveDnMeta *DMp, double *M, const double *V,
                                         double *out) {
   double R[rec_size(CS)];
-  ld_rec<CS>(rec, R);
   const WaveDnMeta md = *DMp;
+  ld_rec<CS>(rec, md.flags, R);
   bb_sign<CS>(md.flags, R);
   double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6];
   if (md.flags & (WF_TILE_ROOT | WF_BODY_ROOT)) {
@@ -1167,7 +1187,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
       const int gG = (nG + 31) & ~31, gR = (nR + 31) & ~31;
       const int tot = gG + gR + nB;
       const double *R = reinterpret_cast<const double *>(B + h.o_rec);
-      const int oR = wave_rec_size(GENERAL) * nG, oB = oR + wave_rec_size(RIGID_BEAD) * nR;
+      const int oB = 0, oR = wave_rec_size(BEAD_BEAD) * nB, oG = oR + wave_rec_size(RIGID_BEAD) * nR;
       if (UP) {
         const WaveUpMeta *UM = reinterpret_cast<const WaveUpMeta *>(B + h.o_meta);
         if (RQ_DEBUG_CHECKS)
@@ -1181,7 +1201,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           }
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
-            if (q < nG) wv_up<GENERAL>(R + q * wave_rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
+            if (q < nG) wv_up<GENERAL>(R + oG + q * wave_rec_size(GENERAL), UM + q, M, V, a.out, a.scratch, a.roots);
           } else if (q < gG + gR) {
             const int qq = q - gG;
             if (qq < nR)
@@ -1206,7 +1226,7 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
           }
         for (int q = tid; q < tot; q += 128) {
           if (q < gG) {
-            if (q < nG) wv_down<GENERAL>(R + q * wave_rec_size(GENERAL), DM + q, M, V, a.out);
+            if (q < nG) wv_down<GENERAL>(R + oG + q * wave_rec_size(GENERAL), DM + q, M, V, a.out);
           } else if (q < gG + gR) {
             const int qq = q - gG;
             if (qq < nR) wv_down<RIGID_BEAD>(R + oR + qq * wave_rec_size(RIGID_BEAD), DM + nG + qq, M, V, a.out);

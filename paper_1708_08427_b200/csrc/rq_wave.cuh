@@ -21,7 +21,7 @@
 //   HDR    : a DirHdr (32 B) per direction: counts, section offsets within that
 //            direction's copy, and where the block two steps further in that
 //            direction lies (the producer issues its TMA from it: no global loads)
-//   REC    : compact records, GEN | RB | BB groups (AoS, rec_size doubles)
+//   REC    : packed records, BB | RB | GEN groups (AoS, wave_rec_size doubles; GEN's odd size last)
 //   UM / DM: per-node metadata of the upward / downward sweep (16 B each)
 //   UG     : upward gather list of step s+2: global bead index per bead (4 B)
 //   DG     : downward gather list of step s-2: residue rows / tile-root
@@ -76,6 +76,7 @@ enum : uint16_t { WG_RES3 = 0, WG_RES6 = 1, WG_SLOT = 2, WG_ROOT = 3 };
 constexpr uint16_t WF_TILE_ROOT = 1u << 6;  // output to / input from an exchange slot
 constexpr uint16_t WF_BODY_ROOT = 1u << 7;  // the body root (output to / input from `roots`)
 constexpr uint16_t WF_BB_NEG = 1u << 8;     // BEAD_BEAD: g = -R(q) (det g = -1)
+constexpr int WF_TAU_ZERO_SHIFT = 9;        // bits 9..11: reflector i of a WY record is the identity (tau_i = 0)
 
 __host__ __device__ inline uint32_t al16u(uint32_t x) { return (x + 15u) & ~15u; }
 
@@ -101,16 +102,17 @@ struct WaveSec {  // byte offsets inside a block
   __host__ __device__ uint32_t up0() const { return uhdr; }
   __host__ __device__ uint32_t dn_end() const { return um; }
 };
-// Records in the step blocks are packed: a GENERAL / RIGID_BEAD compact-WY record keeps V,
-// the diagonal of T (tau0, tau1, tau2) and the ratios a, b; the sweep rebuilds T's three
-// off-diagonal entries from V and the taus with the setup's own operations (lq_factor,
-// rq_lq.cuh), so they are bit-identical.  GENERAL 26 (vs 30), RIGID_BEAD 18 (vs 20, padded to
-// 16-byte alignment).  A BEAD_BEAD node's 3x3 g is orthogonal (the mixer of two beads is,
-// factor.py:130-170), so the blocks carry it as a unit quaternion q (4 doubles vs 10) and a
-// flag bit for det g = -1 (g = -R(q)); the sweep rebuilds g to ~1 ulp.
-//   V0 (K-1) | V1 (K-2) | V2 (K-3) | tau0 tau1 tau2 | a b [| pad]        q_w q_x q_y q_z
+// Records in the step blocks are packed.  A GENERAL / RIGID_BEAD compact-WY record keeps V and
+// the ratios a, b only: each reflector's tau is 2 / (v^T v) (H = I - tau v v^T is a reflection;
+// dlarfg's tau = 0, H = I, is a flag bit in the node meta), and T's off-diagonal entries follow
+// from V and the taus as in lq_factor (rq_lq.cuh) -- the sweep rebuilds them (~1 ulp).
+// GENERAL 23 (vs 30; odd: stored after the other groups and read with 8-byte loads, whose
+// 184-byte stride keeps a warp's lanes on distinct banks), RIGID_BEAD 14 (vs 20) doubles.  A BEAD_BEAD node's 3x3 g is orthogonal
+// (the mixer of two beads is, factor.py:130-170), so the blocks carry it as a unit quaternion q
+// (4 doubles vs 10) and a flag bit for det g = -1 (g = -R(q)); the sweep rebuilds g to ~1 ulp.
+//   V0 (K-1) | V1 (K-2) | V2 (K-3) | a b [| pad]        q_w q_x q_y q_z
 __host__ __device__ constexpr int wave_rec_size(int c) {
-  return c == BEAD_BEAD ? 4 : (c == RIGID_BEAD ? 18 : (c == GENERAL ? 26 : 0));
+  return c == BEAD_BEAD ? 4 : (c == RIGID_BEAD ? 14 : (c == GENERAL ? 23 : 0));
 }
 // g (3x3 row-major, orthogonal) -> unit quaternion of s g with s = sign(det g) (Shepperd's
 // method: the largest of the four squared components is taken from the diagonal)
@@ -148,19 +150,18 @@ __host__ __device__ inline void wave_unpack_bb(const double *q, bool neg, double
   g[6] = s * (x * z - w * y);       g[7] = s * (y * z + w * x);       g[8] = one - s * (x * x + y * y);
 }
 __host__ __device__ inline uint32_t wave_rec_bytes(uint32_t nG, uint32_t nR, uint32_t nB) {
-  return 8u * (wave_rec_size(GENERAL) * nG + wave_rec_size(RIGID_BEAD) * nR + wave_rec_size(BEAD_BEAD) * nB);
+  // 16-byte multiple: the sections after it (and the TMA copy sizes) stay 16-byte aligned
+  return al16u(8u * (wave_rec_size(GENERAL) * nG + wave_rec_size(RIGID_BEAD) * nR + wave_rec_size(BEAD_BEAD) * nB));
 }
-// compact-WY record (WY<K> layout, T upper part + ratios) -> packed wave record
+// compact-WY record (WY<K> layout, T upper part + ratios) -> packed wave record; returns the
+// tau = 0 mask (bit i: reflector i is the identity)
 template <int K>
-__host__ __device__ inline void wave_pack_wy(const double *src, double *dst) {
+__host__ __device__ inline unsigned wave_pack_wy(const double *src, double *dst) {
   using W = WY<K>;
   for (int e = 0; e < W::T; e++) dst[e] = src[e];  // V
-  dst[W::T + 0] = src[W::T + 0];                   // tau0 = T00
-  dst[W::T + 1] = src[W::T + 3];                   // tau1 = T11
-  dst[W::T + 2] = src[W::T + 5];                   // tau2 = T22
-  dst[W::T + 3] = src[W::RA];
-  dst[W::T + 4] = src[W::RB];
-  if ((W::T + 5) & 1) dst[W::T + 5] = 0.0;         // pad to an even count
+  dst[W::T + 0] = src[W::RA];
+  dst[W::T + 1] = src[W::RB];
+  return (src[W::T + 0] == 0.0 ? 1u : 0u) | (src[W::T + 3] == 0.0 ? 2u : 0u) | (src[W::T + 5] == 0.0 ? 4u : 0u);
 }
 __host__ __device__ inline WaveSec wave_sections(uint32_t nG, uint32_t nR, uint32_t nB, uint32_t n_ug,
                                                  uint32_t n_dg) {
