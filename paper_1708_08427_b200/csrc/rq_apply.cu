@@ -625,13 +625,15 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   };
   auto sweep = [&]() {
     if (!do_sweep) return;
+    const int64_t R = std::max<int64_t>(p.wave_rounds, 1);
     if (!ss.round_ctr.p) {  // monotone counters: zeroed once, targets advance per launch
-      ss.round_ctr.alloc(std::max<int64_t>(p.wave_rounds, 1) * 8);
-      RQ_CUDA(cudaMemsetAsync(ss.round_ctr.p, 0, std::max<int64_t>(p.wave_rounds, 1) * 8, s));
+      ss.round_ctr.alloc((2 * R + 2) * 4);
+      RQ_CUDA(cudaMemsetAsync(ss.round_ctr.p, 0, (2 * R + 2) * 4, s));
     }
     const uint32_t epoch = ++ss.wave_epoch[up ? 0 : 1];
     run_wave(p, up, cin, cout, ss.scratch.as<double>(), roots, s,
-             ss.round_ctr.as<uint32_t>() + (up ? 0 : p.wave_rounds), epoch);
+             ss.round_ctr.as<uint32_t>() + (up ? 0 : p.wave_rounds), epoch,
+             ss.round_ctr.as<uint32_t>() + 2 * R + (up ? 0 : 1));
   };
   if (up) {
     sweep();

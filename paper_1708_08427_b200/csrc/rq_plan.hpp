@@ -226,7 +226,7 @@ struct Plan {
     DBuf col_in, col_out;     // column-major copies of a (rows, k) block for the column loop
     DBuf res_tmp, roots;      // Q / Q^T: residues in the private layout and the 6 root rows per body
     DBuf in_al;               // 16-byte aligned copy of a misaligned input
-    DBuf round_ctr;           // wave round-window arrival counters [2][rounds] (up, down)
+    DBuf round_ctr;           // wave round-window arrival counters [2][rounds] (up, down) + 2 abandon flags
     uint32_t wave_epoch[2] = {0, 0};
     DBuf zpart;               // Zf per-segment partial sums
     DBuf zcnt;                // Zf per-(column, body) arrival counters (self-resetting)
@@ -301,7 +301,7 @@ void wave_prepare(const Plan &p);
 // tile part of one upward / downward sweep over all bodies (rq_wave.cu); residues in the
 // private layout, body-root vectors to / from `roots` (nullptr: dropped / zero)
 void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots,
-              cudaStream_t s, uint32_t *round_ctr = nullptr, uint32_t epoch = 0);
+              cudaStream_t s, uint32_t *round_ctr = nullptr, uint32_t epoch = 0, uint32_t *abandon = nullptr);
 // bodies [j0, j1) of a plan (all work lists are in body order)
 struct BodyRange {
   int64_t j0 = 0, j1 = -1;  // j1 < 0: all bodies

@@ -1063,6 +1063,8 @@ struct WaveCtx {
   // run-time round window (nullptr: off): per-round arrival counters of this direction
   uint32_t *round_ctr;
   uint32_t round_target;                 // arrivals per round when every CTA has passed it
+  uint32_t *abandon;                     // == epoch: a window wait timed out in this launch
+  uint32_t epoch;
   int rounds, window;
 };
 
@@ -1120,8 +1122,16 @@ __global__ void __launch_bounds__(128, RQ_WAVE_MIN_BLOCKS) k_wave(WaveCtx a) {
         const int lag = UP ? r - a.window : r + a.window;
         if (lag >= 0 && lag < a.rounds) {
           const long long t0 = clock64();
-          while ((int32_t)(*(volatile uint32_t *)(a.round_ctr + lag) - a.round_target) < 0 && clock64() - t0 < 400000)
+          // a wait that times out means the grid is not all resident (e.g. another application's
+          // sweep shares the GPU): the window is then abandoned for the rest of this launch
+          while ((int32_t)(*(volatile uint32_t *)(a.round_ctr + lag) - a.round_target) < 0 &&
+                 *(volatile uint32_t *)a.abandon != a.epoch) {
+            if (clock64() - t0 > 200000) {
+              atomicExch(a.abandon, a.epoch);
+              break;
+            }
             __nanosleep(128);
+          }
         }
       }
       cur_round = r;
@@ -1277,7 +1287,7 @@ void wave_prepare(const Plan &p) {
 }
 
 void run_wave(const Plan &p, bool up, const double *in, double *out, double *scratch, double *roots, cudaStream_t s,
-              uint32_t *round_ctr, uint32_t epoch) {
+              uint32_t *round_ctr, uint32_t epoch, uint32_t *abandon) {
   if (!p.wave_streams) return;
   if (reinterpret_cast<uintptr_t>(in) & 15) throw Error(RQ_ERR_VALUE, "wave sweep input must be 16-byte aligned");
   wave_prepare(p);
@@ -1300,6 +1310,8 @@ void run_wave(const Plan &p, bool up, const double *in, double *out, double *scr
       (int64_t)p.wave_ctas_per_sm * p.sms >= p.wave_streams) {
     a.round_ctr = round_ctr;
     a.round_target = (uint32_t)((int64_t)epoch * p.wave_streams);
+    a.abandon = abandon;
+    a.epoch = epoch;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p.wave_streams);
