@@ -200,12 +200,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RQ_BENCH_SHARE_GPU=1 (functional check of the multi-rank path on a one-GPU box only: ranks
+    # share the visible GPUs round-robin over gloo; its timings mean nothing)
+    share = os.environ.get("RQ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     sharding = args.sharding or ("strong" if world > 1 else "weak")
