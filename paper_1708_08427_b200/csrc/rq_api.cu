@@ -203,7 +203,8 @@ int rq_launches_per_apply(const rq_plan *plan, int op, int64_t k) {
     return tiles + tops + levels + ((p.n_small && op <= 1) ? 1 : 0);
   }
   int classes = 0;
-  for (int c = 0; c < rq::Plan::N_TOPCLASS; c++) classes += p.topclass_count[c] > 0;
+  for (int f = 0; f < 2; f++)
+    for (int c = 0; c < rq::Plan::N_TOPCLASS; c++) classes += p.topclass_first[f][c + 1] > p.topclass_first[f][c];
   // wavefront sweep + staged top classes + dataflow top + (Q / Q^T) layout pass
   int per_col = (p.wave_streams ? 1 : 0) + classes + (p.n_top_start ? 1 : 0) + (op <= 1 ? 1 : 0);
   return (int)(per_col * k + (k > 1 ? 2 : 0));  // k > 1: the two block transposes

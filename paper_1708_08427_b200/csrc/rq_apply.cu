@@ -367,8 +367,10 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
         merge(cs, rec, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
         const int rr = res_rows(cs);
         for (int r = 0; r < rr; r++) a.out[(sbase + md.res_q + r) * K + col] = res[r];
-        if (md.is_root && a.roots)
+        if (md.is_root == 1 && a.roots)
           for (int r = 0; r < 6; r++) a.roots[6 * (int64_t)h.body + r] = mp[r];
+        if (md.is_root == 2)  // piece root: its vector goes to the apex through its exchange slot
+          for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)h.root_slot + r] = mp[r];
 #pragma unroll
         for (int r = 0; r < 6; r++) MT[6 * q + r] = mp[r];
       }
@@ -381,8 +383,10 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
       const double *src = a.in + (sbase + md.res_q) * K + col;
       const uint32_t d = smem_u32(RT + 6 * q);
       for (int r = 0; r < rr; r++) cp_async8_u32(d + 8u * r, src + r * K);
-      if (md.is_root)
+      if (md.is_root == 1)
         for (int r = 0; r < 6; r++) MT[6 * q + r] = a.roots ? a.roots[6 * (int64_t)h.body + r] : 0.0;
+      else if (md.is_root == 2)  // piece root: the RV-set the apex wrote to its exchange slot
+        for (int r = 0; r < 6; r++) MT[6 * q + r] = a.scratch[6 * (int64_t)h.root_slot + r];
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -597,10 +601,13 @@ void run_apply(const Plan &p, int op, const double *in, double *out, int64_t k, 
   const bool do_sweep = (phases & 1u) && p.wave_streams > 0;
   const bool do_top = (phases & 2u) && (p.n_topblob > 0 || t.n > 0);
   auto top_pass = [&]() {
-    for (int c = 0; c < Plan::N_TOPCLASS; c++) {
-      const unsigned nb = (unsigned)(p.topclass_first[c + 1] - p.topclass_first[c]);
+    // phase 0 (whole top trees, pieces) and phase 1 (apexes of split trees): pieces feed the
+    // apex upward, the apex feeds the pieces downward
+    for (int i = 0; i < 2 * Plan::N_TOPCLASS; i++) {
+      const int f = up ? i / Plan::N_TOPCLASS : 1 - i / Plan::N_TOPCLASS, c = i % Plan::N_TOPCLASS;
+      const unsigned nb = (unsigned)(p.topclass_first[f][c + 1] - p.topclass_first[f][c]);
       if (!nb) continue;
-      t2.order = p.topblob_order.as<int32_t>() + p.topclass_first[c];
+      t2.order = p.topblob_order.as<int32_t>() + p.topclass_first[f][c];
       const size_t sm = (size_t)p.topclass_smem[c];
       static const int wide_from = [] {  // classes from here on run 128 threads per top tree
         const char *e = getenv("RQ_TOP_WIDE_CLASS");

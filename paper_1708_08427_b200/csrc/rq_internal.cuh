@@ -65,14 +65,19 @@ struct TopNode {         // node with more than tile_leaves beads
 
 // Per-body top-tree blob (one TMA bulk copy per body, swept in shared memory):
 //   TopHdr | int32 level_begin[n_levels+1] | TopMeta[n_nodes] | int32 inputs[n_inputs] | records
-struct TopHdr {          // 32 bytes
+struct TopHdr {          // 48 bytes
   int32_t n_nodes, n_levels, n_inputs, body;
   int32_t off_meta, off_in, off_rec, bytes;
+  int32_t root_slot;     // piece blobs: exchange slot of the piece root (-1 otherwise)
+  int32_t pad[3];
 };
+// A top tree too large for one blob is cut into PIECES (maximal subtrees of top nodes with at
+// most X beads) and an APEX (its nodes with more than X beads); a piece root hands its vector
+// to the apex (upward) / receives its RV-set from it (downward) through its exchange slot.
 struct TopMeta {         // 16 bytes, nodes sorted by height
   int16_t x, y;          // >= 0: local top node; < 0: ~input index
   uint16_t flags;
-  uint16_t is_root;
+  uint16_t is_root;      // 1: body root; 2: piece root (vector to / from the exchange slot)
   int32_t res_q;         // body-relative Q~ offset of its residue rows (-1 if none)
   int32_t rec;           // double offset of its record in the record area
 };

@@ -139,6 +139,7 @@ struct Plan {
   int64_t n_case[4] = {0, 0, 0, 0};
   int64_t rec_doubles = 0;
   int64_t n_tiles = 0, n_top = 0, n_slots = 0, n_topbodies = 0, n_toplevels = 0;
+  int64_t n_topunits = 0;          // top-tree blob units: whole top trees, or pieces + apex of a split one
   int64_t n_small = 0;             // bodies with n == 1
   int64_t min_n = 0;
 
@@ -165,7 +166,7 @@ struct Plan {
   // top trees
   DBuf top;                        // TopNode [n_top], sorted by (body, height)
   DBuf topbody;                    // int32 [n_topbodies]: body ids needing the top kernels
-  DBuf topbody_lvl;                // int32 [n_topbodies+1]: level CSR into toplvl
+  DBuf topbody_lvl;                // int32 [n_topunits+1]: level CSR into toplvl (per blob unit)
   DBuf toplvl;                     // int32 [n_toplevels+1]: top index ranges per level
   DBuf small_bodies;               // int32 [n_small]
   // staged top tree (bodies whose top blob fits shared memory)
@@ -179,7 +180,9 @@ struct Plan {
   // 5 = <= 112 KB (128 threads).  Each launch allocates its class's largest footprint.
   static constexpr int N_TOPCLASS = 6;
   int64_t topclass_smem[N_TOPCLASS] = {}, topclass_count[N_TOPCLASS] = {};
-  int64_t topclass_first[N_TOPCLASS + 1] = {};  // class c's blobs: topblob_order[first[c], first[c+1])
+  // phase 0: whole top trees and pieces; phase 1: apexes (after the pieces upward, before downward).
+  // Phase f, class c: topblob_order[first[f][c], first[f][c+1])
+  int64_t topclass_first[2][N_TOPCLASS + 1] = {};
   DBuf topbig;                     // int32 [n_topbig]: top-body indices handled by the global k_top
   int64_t n_topbig = 0;
   // dataflow sweep of those big top trees (k_top_df): parent links, arrival counters, start nodes

@@ -557,9 +557,13 @@ __global__ void k_remap_tiles(int32_t *tile_of, int64_t NN, const int32_t *inv) 
   if (g < NN && tile_of[g] >= 0) tile_of[g] = inv[tile_of[g]];
 }
 
+// Sort key of a top node: (unit, height).  The unit is named by a node id: the body root for a
+// whole top tree and for the apex of a split one (split_x[j] > 0: nodes with more than
+// split_x[j] beads), else the root of the node's piece -- its highest ancestor with at most
+// split_x[j] beads.
 __global__ void k_top_fill(LayoutCtx c, int64_t NN, const int32_t *is_top, const int32_t *top_scan,
                            const int32_t *slot_scan, const int32_t *left, const int32_t *right,
-                           TopNode *top, uint64_t *keys, int32_t *vals) {
+                           const int64_t *split_x, TopNode *top, uint64_t *keys, int32_t *vals) {
   int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= NN || !is_top[g]) return;
   int t = top_scan[g];
@@ -588,7 +592,18 @@ __global__ void k_top_fill(LayoutCtx c, int64_t NN, const int32_t *is_top, const
   T.is_root = c.parent[g] < 0;
   T.rec_off = c.rec_off[g];
   top[t] = T;
-  keys[t] = ((uint64_t)j << 32) | (uint64_t)c.height[g];
+  const int64_t root = nb + 2 * (c.bead_off[j + 1] - c.bead_off[j]) - 2;
+  int64_t unit = root;
+  const int64_t X = split_x[j];
+  if (X > 0 && c.stop[g] - c.start[g] <= X) {
+    unit = g;
+    for (int64_t a = g; c.parent[a] >= 0;) {
+      const int64_t pa = nb + c.parent[a];
+      if (c.stop[pa] - c.start[pa] > X) break;
+      unit = a = pa;
+    }
+  }
+  keys[t] = ((uint64_t)unit << 32) | (uint64_t)c.height[g];
   vals[t] = t;
 }
 
@@ -600,15 +615,34 @@ __global__ void k_top_gather(const TopNode *src, const int32_t *order, const uin
   lvl_start_flag[p] = (p == 0 || keys_sorted[p] != keys_sorted[p - 1]) ? 1 : 0;
 }
 
+__global__ void k_top_unitflag(const uint64_t *keys_sorted, int64_t n, int32_t *uflag) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) uflag[p] = (p == 0 || (keys_sorted[p] >> 32) != (keys_sorted[p - 1] >> 32)) ? 1 : 0;
+}
+// exclusive scan of the unit-start flags -> unit index of every node (inclusive scan - 1)
+__global__ void k_top_unitfix(const int32_t *uflag, int64_t n, int32_t *tunit) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < n) tunit[p] += uflag[p] - 1;
+}
+
+// level starts; per unit (at its first node): first level, body and kind (0 whole top tree,
+// 1 piece, 2 apex)
 __global__ void k_top_levels(const uint64_t *keys_sorted, const int32_t *flag, const int32_t *lvl_scan,
-                             int64_t n, int32_t *toplvl, const int32_t *topbody_idx,
-                             int32_t *topbody_lvl) {
+                             const int32_t *uflag, const int32_t *tunit, const TopNode *top, const int64_t *split_x,
+                             const int64_t *bead_off, const int64_t *node_off, int64_t n, int32_t *toplvl,
+                             int32_t *unit_lvl, int32_t *unit_body, int32_t *unit_kind) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= n || !flag[p]) return;
   int lv = lvl_scan[p];
   toplvl[lv] = (int32_t)p;
-  int j = (int)(keys_sorted[p] >> 32);
-  if (p == 0 || (keys_sorted[p - 1] >> 32) != (uint64_t)j) topbody_lvl[topbody_idx[j]] = lv;
+  if (uflag[p]) {
+    const int u = tunit[p];
+    const int j = top[p].body;
+    unit_lvl[u] = lv;
+    unit_body[u] = j;
+    const int64_t root = node_off[j] + 2 * (bead_off[j + 1] - bead_off[j]) - 2;
+    unit_kind[u] = split_x[j] == 0 ? 0 : ((int64_t)(keys_sorted[p] >> 32) == root ? 2 : 1);
+  }
 }
 
 
@@ -649,25 +683,28 @@ __global__ void k_top_path_write(const int32_t *parent, const int32_t *starts, i
   }
 }
 
-__global__ void k_top_slotmap(const TopNode *top, int64_t nt, const int32_t *topbody_idx, const int32_t *topbody_lvl,
-                              const int32_t *toplvl, int32_t *slot_to_local, int32_t *nin, int64_t *recsz) {
+__global__ void k_top_slotmap(const TopNode *top, int64_t nt, const int32_t *tunit, const int32_t *unit_lvl,
+                              const int32_t *toplvl, int32_t *slot_to_local, int32_t *slot_unit, int64_t *recsz) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= nt) return;
   const TopNode T = top[p];
-  const int bi = topbody_idx[T.body];
-  const int first = toplvl[topbody_lvl[bi]];
+  const int u = tunit[p];
+  const int first = toplvl[unit_lvl[u]];
   slot_to_local[T.self_slot] = (int32_t)(p - first);
+  slot_unit[T.self_slot] = u;
   recsz[p] = rec_size(flag_case(T.flags));
-  (void)nin;
 }
 
-__global__ void k_top_inputs(const TopNode *top, int64_t nt, const int32_t *slot_to_local, int32_t *nin) {
+// children outside the node's unit (tile roots, beads, piece roots under an apex) are inputs
+__global__ void k_top_inputs(const TopNode *top, int64_t nt, const int32_t *slot_unit, const int32_t *tunit,
+                             int32_t *nin) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= nt) return;
   const TopNode T = top[p];
+  const int u = tunit[p];
   int c = 0;
-  if (T.x < 0 || slot_to_local[T.x] < 0) c++;
-  if (T.y < 0 || slot_to_local[T.y] < 0) c++;
+  if (T.x < 0 || slot_unit[T.x] != u) c++;
+  if (T.y < 0 || slot_unit[T.y] != u) c++;
   nin[p] = c;
 }
 
@@ -682,15 +719,16 @@ __host__ __device__ inline int64_t topblob_bytes(int n_nodes, int n_levels, int 
 
 // one thread per top node: writes its meta, inputs and record; the body's first
 // node also writes the header and level table
-__global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *topbody_idx, const int32_t *topbody_lvl,
-                           const int32_t *toplvl, const int32_t *slot_to_local, const int32_t *in_scan,
-                           const int64_t *rec_scan, const int64_t *blob_off_of_tb, const double *rec,
-                           const int32_t *perm, const int64_t *bead_off, uint8_t *blob) {
+__global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *tunit, const int32_t *unit_lvl,
+                           const int32_t *unit_kind, const int32_t *toplvl, const int32_t *slot_to_local,
+                           const int32_t *slot_unit, const int32_t *in_scan, const int64_t *rec_scan,
+                           const int64_t *blob_off_of_tb, const double *rec, const int32_t *perm,
+                           const int64_t *bead_off, uint8_t *blob) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= nt) return;
   const TopNode T = top[p];
-  const int bi = topbody_idx[T.body];
-  const int lv0 = topbody_lvl[bi], lv1 = topbody_lvl[bi + 1];
+  const int bi = tunit[p];
+  const int lv0 = unit_lvl[bi], lv1 = unit_lvl[bi + 1];
   const int first = toplvl[lv0], last = toplvl[lv1];
   const int n_nodes = last - first, n_levels = lv1 - lv0;
   const int n_inputs = in_scan[last] - in_scan[first];
@@ -705,6 +743,9 @@ __global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *topbod
   h.off_in = h.off_meta + n_nodes * (int32_t)sizeof(TopMeta);
   h.off_rec = h.off_in + (int32_t)(((int64_t)n_inputs * 4 + 15) / 16 * 16);
   h.bytes = (int32_t)topblob_bytes(n_nodes, n_levels, n_inputs, n_rec);
+  const bool piece = unit_kind[bi] == 1;
+  h.root_slot = piece ? top[last - 1].self_slot : -1;  // nodes by height: the unit root is last
+  h.pad[0] = h.pad[1] = h.pad[2] = 0;
   const int local = (int)(p - first);
   if (local == 0) {
     *reinterpret_cast<TopHdr *>(B) = h;
@@ -714,7 +755,7 @@ __global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *topbod
   int32_t *IN = reinterpret_cast<int32_t *>(B + h.off_in);
   int in_i = in_scan[p] - in_scan[first];
   auto ref = [&](int32_t c) -> int16_t {
-    if (c >= 0 && slot_to_local[c] >= 0) return (int16_t)slot_to_local[c];
+    if (c >= 0 && slot_unit[c] == bi) return (int16_t)slot_to_local[c];
     IN[in_i] = c >= 0 ? c : ~perm[~(int64_t)c];  // slot, or ~(body-local original bead index)
     return (int16_t)~in_i++;
   };
@@ -722,7 +763,7 @@ __global__ void k_top_blob(const TopNode *top, int64_t nt, const int32_t *topbod
   md.x = ref(T.x);
   md.y = ref(T.y);
   md.flags = T.flags;
-  md.is_root = T.is_root;
+  md.is_root = T.is_root ? 1 : ((piece && local == n_nodes - 1) ? 2 : 0);
   md.res_q = T.res_q;
   md.rec = (int32_t)(rec_scan[p] - rec_scan[first]);
   reinterpret_cast<TopMeta *>(B + h.off_meta)[local] = md;
@@ -1282,7 +1323,6 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
     {
       std::vector<int64_t> topbodies;
       std::vector<int32_t> smalls;
-      std::vector<int32_t> topbody_idx(m, -1);
       // bodies with a top tree: their root is a top node (more than S beads, or taller
       // than the tile height cut)
       std::vector<int32_t> root_top(m, 0);
@@ -1294,7 +1334,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       }
       for (int64_t j = 0; j < m; j++) {
         int64_t n = offsets[j + 1] - offsets[j];
-        if (root_top[j]) { topbody_idx[j] = (int32_t)topbodies.size(); topbodies.push_back(j); }
+        if (root_top[j]) topbodies.push_back(j);
         if (n == 1) smalls.push_back((int32_t)j);
       }
       p.n_topbodies = (int64_t)topbodies.size();
@@ -1309,11 +1349,27 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
       p.top.alloc(std::max<int64_t>(nt, 1) * sizeof(TopNode));
       std::vector<int32_t> hb(topbodies.begin(), topbodies.end());
       p.topbody.alloc(std::max<int64_t>(p.n_topbodies, 1) * 4);
-      p.topbody_lvl.alloc((p.n_topbodies + 1) * 4);
       if (p.n_topbodies)
         RQ_CUDA(cudaMemcpyAsync(p.topbody.p, hb.data(), p.n_topbodies * 4, cudaMemcpyHostToDevice, s));
+      // top trees of bodies above split_min beads are cut into pieces (<= X beads) + an apex, so
+      // every blob stays small (shared memory per CTA -> residency) and no tree needs the slow
+      // dataflow sweep; X keeps the apex at ~2 x 512 nodes
+      int64_t split_min = 16384;
+      if (const char *e = getenv("RQ_TOP_SPLIT")) split_min = std::max<int64_t>(0, atoll(e));
+      std::vector<int64_t> split_x(m, 0);
+      for (int64_t j = 0; j < m; j++) {
+        const int64_t n = offsets[j + 1] - offsets[j];
+        if (split_min > 0 && root_top[j] && n > split_min) {
+          int64_t X = 4096;
+          while (X < n / 512) X *= 2;
+          split_x[j] = X;
+        }
+      }
+      DBuf d_split;
+      d_split.alloc(std::max<int64_t>(m, 1) * 8);
+      RQ_CUDA(cudaMemcpyAsync(d_split.p, split_x.data(), m * 8, cudaMemcpyHostToDevice, s));
       if (nt > 0) {
-        DBuf tmp_top, tkeys, tvals, tkeys2, tvals2, lflag, lscan, d_tbi;
+        DBuf tmp_top, tkeys, tvals, tkeys2, tvals2, lflag, lscan;
         tmp_top.alloc(nt * sizeof(TopNode));
         tkeys.alloc(nt * 8);
         tvals.alloc(nt * 4);
@@ -1321,11 +1377,10 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         tvals2.alloc(nt * 4);
         lflag.alloc(nt * 4);
         lscan.alloc(nt * 4);
-        d_tbi.alloc(m * 4);
-        RQ_CUDA(cudaMemcpyAsync(d_tbi.p, topbody_idx.data(), m * 4, cudaMemcpyHostToDevice, s));
         k_top_fill<<<nblk(NN), NT, 0, s>>>(lc, NN, is_top.as<int32_t>(), top_scan.as<int32_t>(),
                                             slot_scan.as<int32_t>(), p.left.as<int32_t>(), p.right.as<int32_t>(),
-                                            tmp_top.as<TopNode>(), tkeys.as<uint64_t>(), tvals.as<int32_t>());
+                                            d_split.as<int64_t>(), tmp_top.as<TopNode>(), tkeys.as<uint64_t>(),
+                                            tvals.as<int32_t>());
         size_t tb = 0;
         RQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, tkeys.as<uint64_t>(), tkeys2.as<uint64_t>(),
                                                 tvals.as<int32_t>(), tvals2.as<int32_t>(), (int)nt, 0, 64, s));
@@ -1337,48 +1392,71 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
                                               nt, p.top.as<TopNode>(), lflag.as<int32_t>());
         exclusive_scan(lflag.as<int32_t>(), lscan.as<int32_t>(), nt, s);
         p.n_toplevels = d2h1<int32_t>(lscan.as<int32_t>() + nt - 1, s) + d2h1<int32_t>(lflag.as<int32_t>() + nt - 1, s);
+        // blob units (whole top trees, pieces, apexes): unit index of every top node
+        DBuf uflag, tunit;
+        uflag.alloc(nt * 4);
+        tunit.alloc(nt * 4);
+        k_top_unitflag<<<nblk(nt), NT, 0, s>>>(tkeys2.as<uint64_t>(), nt, uflag.as<int32_t>());
+        exclusive_scan(uflag.as<int32_t>(), tunit.as<int32_t>(), nt, s);
+        const int64_t U = d2h1<int32_t>(tunit.as<int32_t>() + nt - 1, s) + d2h1<int32_t>(uflag.as<int32_t>() + nt - 1, s);
+        k_top_unitfix<<<nblk(nt), NT, 0, s>>>(uflag.as<int32_t>(), nt, tunit.as<int32_t>());
+        p.n_topunits = U;
+        p.topbody_lvl.alloc((U + 1) * 4);
+        DBuf unit_body, unit_kind;
+        unit_body.alloc(U * 4);
+        unit_kind.alloc(U * 4);
         p.toplvl.alloc((p.n_toplevels + 1) * 4);
-        k_top_levels<<<nblk(nt), NT, 0, s>>>(tkeys2.as<uint64_t>(), lflag.as<int32_t>(), lscan.as<int32_t>(), nt,
-                                              p.toplvl.as<int32_t>(), d_tbi.as<int32_t>(),
-                                              p.topbody_lvl.as<int32_t>());
+        k_top_levels<<<nblk(nt), NT, 0, s>>>(tkeys2.as<uint64_t>(), lflag.as<int32_t>(), lscan.as<int32_t>(),
+                                              uflag.as<int32_t>(), tunit.as<int32_t>(), p.top.as<TopNode>(),
+                                              d_split.as<int64_t>(), boff, noff, nt, p.toplvl.as<int32_t>(),
+                                              p.topbody_lvl.as<int32_t>(), unit_body.as<int32_t>(),
+                                              unit_kind.as<int32_t>());
         int32_t endv[2] = {(int32_t)nt, (int32_t)p.n_toplevels};
         RQ_CUDA(cudaMemcpyAsync(p.toplvl.as<int32_t>() + p.n_toplevels, &endv[0], 4, cudaMemcpyHostToDevice, s));
-        RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.as<int32_t>() + p.n_topbodies, &endv[1], 4, cudaMemcpyHostToDevice, s));
-        RQ_CUDA(cudaStreamSynchronize(s));
+        RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.as<int32_t>() + U, &endv[1], 4, cudaMemcpyHostToDevice, s));
+        std::vector<int32_t> unit_body_h(U), unit_kind_h(U);
+        d2h(unit_body_h.data(), unit_body.p, U, s);
+        d2h(unit_kind_h.data(), unit_kind.p, U, s);
         // staged per-body top blobs
-        DBuf slot2loc, nin, in_scan, recsz, rec_scan;
+        DBuf slot2loc, slot2unit, nin, in_scan, recsz, rec_scan;
         slot2loc.alloc(std::max<int64_t>(p.n_slots, 1) * 4);
         RQ_CUDA(cudaMemsetAsync(slot2loc.p, 0xff, std::max<int64_t>(p.n_slots, 1) * 4, s));
+        slot2unit.alloc(std::max<int64_t>(p.n_slots, 1) * 4);
+        RQ_CUDA(cudaMemsetAsync(slot2unit.p, 0xff, std::max<int64_t>(p.n_slots, 1) * 4, s));
         nin.alloc((nt + 1) * 4);
         in_scan.alloc((nt + 1) * 4);
         recsz.alloc((nt + 1) * 8);
         rec_scan.alloc((nt + 1) * 8);
         RQ_CUDA(cudaMemsetAsync(nin.p, 0, (nt + 1) * 4, s));
         RQ_CUDA(cudaMemsetAsync(recsz.p, 0, (nt + 1) * 8, s));
-        k_top_slotmap<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, d_tbi.as<int32_t>(), p.topbody_lvl.as<int32_t>(),
-                                               p.toplvl.as<int32_t>(), slot2loc.as<int32_t>(), nin.as<int32_t>(),
+        k_top_slotmap<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, tunit.as<int32_t>(), p.topbody_lvl.as<int32_t>(),
+                                               p.toplvl.as<int32_t>(), slot2loc.as<int32_t>(), slot2unit.as<int32_t>(),
                                                recsz.as<int64_t>());
-        k_top_inputs<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, slot2loc.as<int32_t>(), nin.as<int32_t>());
+        k_top_inputs<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, slot2unit.as<int32_t>(), tunit.as<int32_t>(),
+                                              nin.as<int32_t>());
         exclusive_scan(nin.as<int32_t>(), in_scan.as<int32_t>(), nt + 1, s);
         exclusive_scan(recsz.as<int64_t>(), rec_scan.as<int64_t>(), nt + 1, s);
-        std::vector<int32_t> h_lvl(p.n_topbodies + 1), h_toplvl(p.n_toplevels + 1), h_in(nt + 1);
+        std::vector<int32_t> h_lvl(U + 1), h_toplvl(p.n_toplevels + 1), h_in(nt + 1);
         std::vector<int64_t> h_rec(nt + 1);
-        d2h(h_lvl.data(), p.topbody_lvl.p, p.n_topbodies + 1, s);
+        d2h(h_lvl.data(), p.topbody_lvl.p, U + 1, s);
         d2h(h_toplvl.data(), p.toplvl.p, p.n_toplevels + 1, s);
         d2h(h_in.data(), in_scan.p, nt + 1, s);
         d2h(h_rec.data(), rec_scan.p, nt + 1, s);
         int64_t smem_cap = 112 * 1024;  // larger top trees go to the dataflow kernels (measured on config 4)
         if (const char *e = getenv("RQ_TOP_SMEM_KB")) smem_cap = std::max(0, atoi(e)) * 1024;
-        std::vector<int64_t> blob_off(p.n_topbodies, -1), small_off;
+        std::vector<int64_t> blob_off(U, -1), small_off;
         std::vector<int32_t> small_tb, big_tb;
-        std::vector<uint8_t> small_cls;
+        std::vector<uint8_t> small_cls, small_phase;
         int64_t total = 0;
         p.max_topblob_smem = 0;
         for (int c = 0; c < Plan::N_TOPCLASS; c++) p.topclass_smem[c] = p.topclass_count[c] = 0;
-        // shared-memory footprints: header part (levels, meta, inputs) + vectors, and with the records
-        std::vector<int64_t> fp(p.n_topbodies), fp_rec(p.n_topbodies);
+        // shared-memory footprints per unit: header part (levels, meta, inputs) + vectors, and with
+        // the records
+        std::vector<int64_t> fp(U), fp_rec(U);
+        std::vector<uint8_t> fits(U);
+        std::vector<uint8_t> body_big(m, 0);  // a split tree with a unit that does not fit: all dataflow
         int64_t rec_all = 0;  // largest whole-blob footprint up to 48 KB
-        for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
+        for (int64_t bi = 0; bi < U; bi++) {
           const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
           const int nn = last - first, ni = h_in[last] - h_in[first];
           const int64_t bytes = topblob_bytes(nn, h_lvl[bi + 1] - h_lvl[bi], ni, h_rec[last] - h_rec[first]);
@@ -1387,20 +1465,22 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           fp[bi] = (hdr_bytes + 127) / 128 * 128 + vec_bytes;
           fp_rec[bi] = (bytes + 127) / 128 * 128 + vec_bytes;
           if (fp_rec[bi] <= 48 * 1024) rec_all = std::max(rec_all, fp_rec[bi]);
+          fits[bi] = fp[bi] <= smem_cap && nn < 32000 && ni < 32000;
+          if (!fits[bi] && unit_kind_h[bi] != 0) body_big[unit_body_h[bi]] = 1;
         }
         // Records staged too (no L2 round trip per level) when that costs no residency: every top
         // tree resident at once, else only tiny ones (config 4's 20000 trees run in waves, where
         // the footprint decides the throughput; measured)
         if (!p.sms) RQ_CUDA(cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, p.device));
         const int64_t per_sm = rec_all ? std::min<int64_t>(32, (227 * 1024) / rec_all) : 0;
-        int64_t rec_cap = (rec_all && p.n_topbodies <= per_sm * std::max(p.sms, 1)) ? rec_all : 16 * 1024;
+        int64_t rec_cap = (rec_all && U <= per_sm * std::max(p.sms, 1)) ? rec_all : 16 * 1024;
         if (const char *e = getenv("RQ_TOP_REC_KB")) rec_cap = std::max(0, atoi(e)) * 1024;
-        for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
+        for (int64_t bi = 0; bi < U; bi++) {
           const int first = h_toplvl[h_lvl[bi]], last = h_toplvl[h_lvl[bi + 1]];
           const int nn = last - first, nl = h_lvl[bi + 1] - h_lvl[bi], ni = h_in[last] - h_in[first];
           const int64_t bytes = topblob_bytes(nn, nl, ni, h_rec[last] - h_rec[first]);
           const int64_t smem = fp[bi], smem_rec = fp_rec[bi];
-          if (smem <= smem_cap && nn < 32000 && ni < 32000) {
+          if (fits[bi] && !body_big[unit_body_h[bi]]) {
             blob_off[bi] = total;
             small_tb.push_back((int32_t)bi);
             small_off.push_back(total);
@@ -1410,6 +1490,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
             const int64_t sm_c = c == 0 ? smem_rec : smem;
             p.max_topblob_smem = std::max(p.max_topblob_smem, sm_c);
             small_cls.push_back((uint8_t)c);
+            small_phase.push_back((uint8_t)(unit_kind_h[bi] == 2 ? 1 : 0));
             p.topclass_smem[c] = std::max(p.topclass_smem[c], sm_c);
             p.topclass_count[c]++;
           } else {
@@ -1424,21 +1505,23 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         if (getenv("RQ_VERBOSE")) {
           int mx_nn = 0, mx_nl = 0;
           double s_nn = 0, s_nl = 0;
-          for (int64_t bi = 0; bi < p.n_topbodies; bi++) {
+          int64_t n_split = 0;
+          for (int64_t bi = 0; bi < U; bi++) {
             const int nn = h_toplvl[h_lvl[bi + 1]] - h_toplvl[h_lvl[bi]], nl = h_lvl[bi + 1] - h_lvl[bi];
             mx_nn = std::max(mx_nn, nn), mx_nl = std::max(mx_nl, nl), s_nn += nn, s_nl += nl;
+            n_split += unit_kind_h[bi] == 2;
           }
-          fprintf(stderr, "[rq] top trees: %lld bodies, nodes mean %.1f max %d, levels mean %.1f max %d; staged %lld, "
-                  "global %lld; classes (count/smem):", (long long)p.n_topbodies,
-                  s_nn / std::max<int64_t>(1, p.n_topbodies), mx_nn, s_nl / std::max<int64_t>(1, p.n_topbodies), mx_nl,
-                  (long long)p.n_topblob, (long long)p.n_topbig);
+          fprintf(stderr, "[rq] top trees: %lld bodies (%lld split) in %lld units, nodes mean %.1f max %d, levels mean "
+                  "%.1f max %d; staged %lld, global %lld; classes (count/smem):", (long long)p.n_topbodies,
+                  (long long)n_split, (long long)U, s_nn / std::max<int64_t>(1, U), mx_nn,
+                  s_nl / std::max<int64_t>(1, U), mx_nl, (long long)p.n_topblob, (long long)p.n_topbig);
           for (int c = 0; c < Plan::N_TOPCLASS; c++)
             fprintf(stderr, " %lld/%lld", (long long)p.topclass_count[c], (long long)p.topclass_smem[c]);
           fprintf(stderr, "\n");
         }
         auto firsts = [&](const std::vector<int32_t> &list, std::vector<int64_t> &out) {
           out.assign(m + 1, (int64_t)list.size());
-          for (int64_t i = (int64_t)list.size() - 1; i >= 0; i--) out[topbodies[list[i]]] = i;
+          for (int64_t i = (int64_t)list.size() - 1; i >= 0; i--) out[unit_body_h[list[i]]] = i;
           for (int64_t j = m - 1; j >= 0; j--) out[j] = std::min(out[j], out[j + 1]);
         };
         firsts(small_tb, p.h_topblob_first);
@@ -1452,12 +1535,14 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         // runs exactly its own blobs
         std::vector<int32_t> cls_order;
         cls_order.reserve(p.n_topblob);
-        for (int c = 0; c < Plan::N_TOPCLASS; c++) {
-          p.topclass_first[c] = (int64_t)cls_order.size();
-          for (int64_t i = 0; i < p.n_topblob; i++)
-            if (small_cls[i] == c) cls_order.push_back((int32_t)i);
+        for (int f = 0; f < 2; f++) {
+          for (int c = 0; c < Plan::N_TOPCLASS; c++) {
+            p.topclass_first[f][c] = (int64_t)cls_order.size();
+            for (int64_t i = 0; i < p.n_topblob; i++)
+              if (small_cls[i] == c && small_phase[i] == f) cls_order.push_back((int32_t)i);
+          }
+          p.topclass_first[f][Plan::N_TOPCLASS] = (int64_t)cls_order.size();
         }
-        p.topclass_first[Plan::N_TOPCLASS] = (int64_t)cls_order.size();
         p.topblob_order.alloc(std::max<int64_t>(p.n_topblob, 1) * 4);
         if (p.n_topblob) {
           RQ_CUDA(cudaMemcpyAsync(p.topblob_off.p, small_off.data(), p.n_topblob * 8, cudaMemcpyHostToDevice, s));
@@ -1467,12 +1552,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         }
         if (p.n_topbig) RQ_CUDA(cudaMemcpyAsync(p.topbig.p, big_tb.data(), p.n_topbig * 4, cudaMemcpyHostToDevice, s));
         DBuf d_blob_off;
-        d_blob_off.alloc(p.n_topbodies * 8);
-        RQ_CUDA(cudaMemcpyAsync(d_blob_off.p, blob_off.data(), p.n_topbodies * 8, cudaMemcpyHostToDevice, s));
-        // only bodies with a staged blob are written
-        DBuf is_small;
-        std::vector<uint8_t> hs(p.n_topbodies, 0);
-        for (auto bi : small_tb) hs[bi] = 1;
+        d_blob_off.alloc(U * 8);
+        RQ_CUDA(cudaMemcpyAsync(d_blob_off.p, blob_off.data(), U * 8, cudaMemcpyHostToDevice, s));
         if (p.n_topblob) {
           // write every node; nodes of "big" bodies write into a scratch blob that is dropped
           DBuf dummy;
@@ -1486,11 +1567,12 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           }
           DBuf all_blob;
           all_blob.alloc(total + big_bytes + 16);
-          RQ_CUDA(cudaMemcpyAsync(d_blob_off.p, off2.data(), p.n_topbodies * 8, cudaMemcpyHostToDevice, s));
-          k_top_blob<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, d_tbi.as<int32_t>(), p.topbody_lvl.as<int32_t>(),
-                                              p.toplvl.as<int32_t>(), slot2loc.as<int32_t>(), in_scan.as<int32_t>(),
-                                              rec_scan.as<int64_t>(), d_blob_off.as<int64_t>(), p.rec.as<double>(),
-                                              p.perm.as<int32_t>(), boff, all_blob.as<uint8_t>());
+          RQ_CUDA(cudaMemcpyAsync(d_blob_off.p, off2.data(), U * 8, cudaMemcpyHostToDevice, s));
+          k_top_blob<<<nblk(nt), NT, 0, s>>>(p.top.as<TopNode>(), nt, tunit.as<int32_t>(), p.topbody_lvl.as<int32_t>(),
+                                              unit_kind.as<int32_t>(), p.toplvl.as<int32_t>(), slot2loc.as<int32_t>(),
+                                              slot2unit.as<int32_t>(), in_scan.as<int32_t>(), rec_scan.as<int64_t>(),
+                                              d_blob_off.as<int64_t>(), p.rec.as<double>(), p.perm.as<int32_t>(), boff,
+                                              all_blob.as<uint8_t>());
           RQ_CUDA(cudaMemcpyAsync(p.topblob.p, all_blob.p, total, cudaMemcpyDeviceToDevice, s));
           RQ_CUDA(cudaStreamSynchronize(s));
         }
@@ -1519,7 +1601,7 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
           std::vector<int64_t> first_of_body(m + 1, -1);
           for (auto bi : big_tb) {
             const int64_t q0 = h_toplvl[h_lvl[bi]], q1 = h_toplvl[h_lvl[bi + 1]];
-            first_of_body[topbodies[bi]] = (int64_t)starts.size();
+            if (first_of_body[unit_body_h[bi]] < 0) first_of_body[unit_body_h[bi]] = (int64_t)starts.size();
             for (int64_t q = q0; q < q1; q++)
               if (hs[q]) starts.push_back((int32_t)q);
           }
@@ -1555,6 +1637,8 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         p.h_topbig_first.assign(m + 1, 0);
         p.h_topstart_first.assign(m + 1, 0);
         p.toplvl.alloc(4);
+        p.topbody_lvl.alloc(4);
+        p.n_topunits = 0;
         int32_t z = 0;
         RQ_CUDA(cudaMemcpyAsync(p.topbody_lvl.p, &z, 4, cudaMemcpyHostToDevice, s));
         RQ_CUDA(cudaStreamSynchronize(s));
