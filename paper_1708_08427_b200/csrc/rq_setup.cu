@@ -1353,14 +1353,19 @@ void build_plan(Plan &p, const double *pos_in, const int64_t *offsets, int64_t m
         RQ_CUDA(cudaMemcpyAsync(p.topbody.p, hb.data(), p.n_topbodies * 4, cudaMemcpyHostToDevice, s));
       // top trees of bodies above split_min beads are cut into pieces (<= X beads) + an apex, so
       // every blob stays small (shared memory per CTA -> residency) and no tree needs the slow
-      // dataflow sweep; X keeps the apex at ~2 x 512 nodes
+      // dataflow sweep; X >= n/512 keeps the apex at ~2 x 512 nodes.  X = 8192: config 3 top pass
+      // 45.7 -> 20.2 us (up), config 4 552 -> 460 us (X = 2048 / 4096 / 16384 measured worse)
       int64_t split_min = 16384;
       if (const char *e = getenv("RQ_TOP_SPLIT")) split_min = std::max<int64_t>(0, atoll(e));
       std::vector<int64_t> split_x(m, 0);
       for (int64_t j = 0; j < m; j++) {
         const int64_t n = offsets[j + 1] - offsets[j];
         if (split_min > 0 && root_top[j] && n > split_min) {
-          int64_t X = 4096;
+          static const int64_t x0 = [] {
+            const char *e = getenv("RQ_TOP_SPLIT_X");
+            return e ? std::max<int64_t>(256, atoll(e)) : int64_t(8192);  // measured: configs 3 and 4
+          }();
+          int64_t X = x0;
           while (X < n / 512) X *= 2;
           split_x[j] = X;
         }
