@@ -149,27 +149,38 @@ __device__ __forceinline__ bool wv_fits(const TLev &l, const TLev &v, const Wave
          l.vd + v.vd <= c.vd && l.dg + v.dg <= c.dg && l.rm + v.rm <= c.rm;
 }
 
-// Node-level list scheduling, one CTA (one thread) per stream: the stream's tiles in order,
-// each tile's nodes in postorder; a node goes to the earliest step after its children's
-// (and not before the floor = the first step of the previous tile) with room for it.  Any
-// node shape fits (no rigid tile rows), so tiles can be large and the top trees small.
-// The step loads live in a shared-memory ring of WRING steps ahead of the floor.
+// Node-level list scheduling, one warp per stream: the stream's tiles in order, each tile's
+// nodes in postorder; a node goes to the earliest step after its children's (and not before
+// the floor = the first step of the previous tile) with room for it.  Any node shape fits (no
+// rigid tile rows), so tiles can be large and the top trees small.  The step loads live in a
+// shared-memory ring of WRING steps ahead of the floor.  The greedy choice is serial (lane
+// 0), but the warp first stages each chunk of WV_CH tile nodes -- their step requirements
+// and tile-local child indices -- in shared memory with coalesced loads, so the serial loop
+// never waits on a global load (one dependent L2 round trip per node otherwise: 12 -> ~1 ms
+// per pass on config 2).  A tile is a contiguous postorder range, so its children's steps
+// sit in a tile-local array.
 constexpr int WRING = 1024;
+constexpr int WV_CH = 256;
+constexpr int WV_MAXT = 2048;  // nodes of the largest tile (tile_leaves <= 1024)
 __global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, int64_t G, const int32_t *order,
                                                       const int64_t *tile_root, NodeArrays A, WaveCaps caps,
                                                       int32_t *node_step, int64_t *n_steps, int32_t *tile_first,
                                                       int32_t *tile_last, const int32_t *tile_round, int R0,
                                                       int64_t *round_floor, int *bad) {
   __shared__ TLev ring[WRING];
+  __shared__ TLev cv[WV_CH];
+  __shared__ int16_t clc[WV_CH], crc[WV_CH];  // tile-local children (-1: a bead; clc -2: node skipped)
+  __shared__ int32_t lstep[WV_MAXT];
   const int64_t c = blockIdx.x;
-  for (int i = threadIdx.x; i < WRING; i += 32) ring[i] = TLev{};
+  const int lane = threadIdx.x;
+  if (c >= G) return;
+  for (int i = lane; i < WRING; i += 32) ring[i] = TLev{};
   __syncwarp();
-  if (c >= G || threadIdx.x != 0) return;
-  int floor = 0, last = 0;
+  int floor = 0, last = 0;  // uniform across the warp
   bool seen = false;
   for (int64_t i = sfirst[c]; i < sfirst[c + 1]; i++) {
     const int64_t t = order[i];
-    if (!seen && tile_round[t] >= R0) {  // where this stream enters the rebalanced tail rounds
+    if (lane == 0 && !seen && tile_round[t] >= R0) {  // where this stream enters the rebalanced tail rounds
       round_floor[c] = floor;
       seen = true;
     }
@@ -179,41 +190,79 @@ __global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, in
     const int j = A.node_body[g];
     const int64_t nb = A.node_off[j];
     const int64_t rb = A.res_base[j];
-    int tmin = INT32_MAX, tmax = 0;
-    for (int64_t q = g - 2 * (int64_t)L + 2; q <= g; q++) {
-      if (nodeL(A, q) < 2) continue;
-      int ready = floor;
-      const int64_t lc = nb + A.left[q], rc = nb + A.right[q];
-      if (nodeL(A, lc) >= 2) ready = max(ready, node_step[lc] + 1);
-      if (nodeL(A, rc) >= 2) ready = max(ready, node_step[rc] + 1);
-      const int cs = flag_case(A.flags[q]);
-      const int root = q == g, rr = res_rows(cs);
-      TLev v{};
-      if (cs == GENERAL) v.g = 1;
-      else if (cs == RIGID_BEAD) v.r = 1;
-      else v.b = 1;
-      v.beads = (int16_t)wv_beads(cs);
-      v.vd = (int16_t)((rr ? 2 * wv_pieces(rb + A.res_off[q] - 6, rr) : 0) + 6 * root);
-      v.dg = (int16_t)((rr > 0) + root);
-      v.rm = 8 * wave_rec_size(cs) + 16;
-      int st = ready;
-      for (;; st++) {
-        if (st - floor >= WRING) { atomicExch(bad, 1); return; }
-        if (wv_fits(ring[st % WRING], v, caps)) break;
-      }
-      TLev &l = ring[st % WRING];
-      l.g += v.g; l.r += v.r; l.b += v.b; l.beads += v.beads; l.vd += v.vd; l.dg += v.dg; l.rm += v.rm;
-      node_step[q] = st;
-      tmin = min(tmin, st);
-      tmax = max(tmax, st);
-      last = max(last, st + 1);
+    const int64_t q0 = g - 2 * (int64_t)L + 2;
+    const int cnt = (int)(g - q0 + 1);
+    if (cnt > WV_MAXT) {
+      if (lane == 0) atomicExch(bad, 1);
+      return;
     }
-    tile_first[t] = tmin;
-    tile_last[t] = tmax;
-    for (; floor < tmin; floor++) ring[floor % WRING] = TLev{};  // steps no later tile can use
+    int tmin = INT32_MAX, tmax = 0;
+    for (int base = 0; base < cnt; base += WV_CH) {
+      const int nch = min(WV_CH, cnt - base);
+      for (int e = lane; e < nch; e += 32) {
+        const int64_t q = q0 + base + e;
+        if (nodeL(A, q) < 2) { clc[e] = -2; continue; }
+        const int64_t lc = nb + A.left[q], rc = nb + A.right[q];
+        clc[e] = nodeL(A, lc) >= 2 ? (int16_t)(lc - q0) : (int16_t)-1;
+        crc[e] = nodeL(A, rc) >= 2 ? (int16_t)(rc - q0) : (int16_t)-1;
+        const int cs = flag_case(A.flags[q]);
+        const int root = q == g, rr = res_rows(cs);
+        TLev v{};
+        if (cs == GENERAL) v.g = 1;
+        else if (cs == RIGID_BEAD) v.r = 1;
+        else v.b = 1;
+        v.beads = (int16_t)wv_beads(cs);
+        v.vd = (int16_t)((rr ? 2 * wv_pieces(rb + A.res_off[q] - 6, rr) : 0) + 6 * root);
+        v.dg = (int16_t)((rr > 0) + root);
+        v.rm = 8 * wave_rec_size(cs) + 16;
+        cv[e] = v;
+      }
+      __syncwarp();
+      // every lane runs the (uniform) greedy loop; the step search tests 32 steps at once
+      for (int e = 0; e < nch; e++) {
+        if (clc[e] == -2) continue;
+        int ready = floor;
+        if (clc[e] >= 0) ready = max(ready, lstep[clc[e]] + 1);
+        if (crc[e] >= 0) ready = max(ready, lstep[crc[e]] + 1);
+        const TLev v = cv[e];
+        int st = -1;
+        for (int sb = ready;; sb += 32) {
+          const int cand = sb + lane;
+          const bool ok = cand - floor < WRING && wv_fits(ring[cand % WRING], v, caps);
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (m) { st = sb + __ffs(m) - 1; break; }
+          if (sb + 32 - floor >= WRING) break;  // the earliest step with room is out of the window
+        }
+        if (st < 0) {
+          if (lane == 0) atomicExch(bad, 1);
+          return;
+        }
+        if (lane == 0) {
+          TLev &l = ring[st % WRING];
+          l.g += v.g; l.r += v.r; l.b += v.b; l.beads += v.beads; l.vd += v.vd; l.dg += v.dg; l.rm += v.rm;
+          lstep[base + e] = st;
+        }
+        tmin = min(tmin, st);
+        tmax = max(tmax, st);
+        last = max(last, st + 1);
+        __syncwarp();
+      }
+      for (int e = lane; e < nch; e += 32)
+        if (clc[e] != -2) node_step[q0 + base + e] = lstep[base + e];
+      __syncwarp();
+    }
+    if (lane == 0) {
+      tile_first[t] = tmin;
+      tile_last[t] = tmax;
+    }
+    for (int f = floor + lane; f < tmin; f += 32) ring[f % WRING] = TLev{};  // steps no later tile can use
+    floor = max(floor, tmin);
+    __syncwarp();
   }
-  if (!seen) round_floor[c] = last;
-  n_steps[c] = last + 4;  // two gather-only steps at each end
+  if (lane == 0) {
+    if (!seen) round_floor[c] = last;
+    n_steps[c] = last + 4;  // two gather-only steps at each end
+  }
 }
 
 // sort key of every tile node: (global step, case rank)
@@ -343,82 +392,73 @@ __global__ void k_wv_headers(const StepDesc *d, int64_t ns, uint8_t *blob, const
   *reinterpret_cast<DirHdr *>(B + S.uhdr) = u;
 }
 
-// one CTA (one thread) per stream: interval colouring of the node 6-vectors (lowest free
-// slot), the two heaps in shared memory
+// one warp per stream: interval colouring of the node 6-vectors (lowest free slot; optimal
+// for interval graphs, so the slot count is the stream's peak live count).  The free set is a
+// 1024-bit mask, one 32-bit word per lane, so the lowest free slot is a ballot + ffs; a slot
+// is released once the step of its consumer (the parent) has passed, checked by every lane
+// over its word when the step advances.  The warp stages each chunk of WV_CH nodes' (step,
+// release step) pairs first, so the loop never waits on the dependent global loads (node ->
+// tile -> root, node -> body -> parent -> step) of a node.
 constexpr int WV_MAX_SLOTS = 1024;
-__global__ void k_wv_slots(const int64_t *node_first, int64_t G, const int32_t *vals, NodeArrays A,
-                           const int64_t *step_of, const int32_t *node_tile, const int64_t *tile_root,
-                           int32_t *slot_of, int *max_slots, int *overflow) {
+__global__ void __launch_bounds__(32) k_wv_slots(const int64_t *node_first, int64_t G, const int32_t *vals,
+                                                NodeArrays A, const int64_t *step_of, const int32_t *node_tile,
+                                                const int64_t *tile_root, int32_t *slot_of, int *max_slots,
+                                                int *overflow) {
   const int64_t c = blockIdx.x;
-  if (c >= G || threadIdx.x != 0) return;
-  // free: min-heap of slot ids; busy: min-heap of (release step << 13 | slot)
-  __shared__ int16_t freeh[WV_MAX_SLOTS];
-  __shared__ long long busyh[WV_MAX_SLOTS];
-  int nf = 0, nbz = 0, next = 0;
-  auto push_free = [&](int16_t v) {
-    int i = nf++;
-    while (i > 0) {
-      int pa = (i - 1) >> 1;
-      if (freeh[pa] <= v) break;
-      freeh[i] = freeh[pa];
-      i = pa;
+  const int lane = threadIdx.x;
+  if (c >= G) return;
+  __shared__ int64_t rel[WV_MAX_SLOTS];            // release step of a busy slot
+  __shared__ int64_t cstep[WV_CH], crel[WV_CH];  // crel < 0: tile root (no slot)
+  __shared__ int32_t cslot[WV_CH];
+  uint32_t freew = 0xffffffffu;  // slots 32 lane .. 32 lane + 31
+  int64_t cur = -1;
+  int next = 0;  // 1 + the highest slot used
+  for (int64_t p0 = node_first[c]; p0 < node_first[c + 1]; p0 += WV_CH) {
+    const int64_t rem = node_first[c + 1] - p0;
+    const int nch = rem < WV_CH ? (int)rem : WV_CH;
+    for (int e = lane; e < nch; e += 32) {
+      const int64_t g = vals[p0 + e];
+      if (tile_root[node_tile[g]] == g) {  // tile roots exchange through global memory
+        crel[e] = -1;
+        continue;
+      }
+      cstep[e] = step_of[g];
+      crel[e] = step_of[A.node_off[A.node_body[g]] + A.parent[g]];
     }
-    freeh[i] = v;
-  };
-  auto pop_free = [&]() {
-    int16_t top = freeh[0], v = freeh[--nf];
-    int i = 0;
-    for (;;) {
-      int l = 2 * i + 1;
-      if (l >= nf) break;
-      int r = l + 1, m = (r < nf && freeh[r] < freeh[l]) ? r : l;
-      if (freeh[m] >= v) break;
-      freeh[i] = freeh[m];
-      i = m;
+    __syncwarp();
+    for (int e = 0; e < nch; e++) {
+      if (crel[e] < 0) continue;
+      const int64_t gs = cstep[e];
+      if (gs != cur) {  // release every busy slot whose consumer ran before step gs
+        uint32_t busy = ~freew;
+        while (busy) {
+          const int bit = __ffs(busy) - 1;
+          busy &= busy - 1;
+          if (rel[32 * lane + bit] < gs) freew |= 1u << bit;
+        }
+        cur = gs;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, freew != 0);
+      if (!m) {
+        if (lane == 0) atomicExch(overflow, 1);
+        return;
+      }
+      const int fl = __ffs(m) - 1;
+      const uint32_t w = __shfl_sync(0xffffffffu, freew, fl);
+      const int sl = 32 * fl + __ffs(w) - 1;
+      if (lane == fl) freew &= ~(1u << (sl & 31));
+      if (lane == 0) {
+        rel[sl] = crel[e];
+        cslot[e] = sl;
+      }
+      next = max(next, sl + 1);
+      __syncwarp();
     }
-    if (nf) freeh[i] = v;
-    return top;
-  };
-  auto push_busy = [&](long long v) {
-    int i = nbz++;
-    while (i > 0) {
-      int pa = (i - 1) >> 1;
-      if (busyh[pa] <= v) break;
-      busyh[i] = busyh[pa];
-      i = pa;
-    }
-    busyh[i] = v;
-  };
-  auto pop_busy = [&]() {
-    long long top = busyh[0], v = busyh[--nbz];
-    int i = 0;
-    for (;;) {
-      int l = 2 * i + 1;
-      if (l >= nbz) break;
-      int r = l + 1, m = (r < nbz && busyh[r] < busyh[l]) ? r : l;
-      if (busyh[m] >= v) break;
-      busyh[i] = busyh[m];
-      i = m;
-    }
-    if (nbz) busyh[i] = v;
-    return top;
-  };
-  for (int64_t p = node_first[c]; p < node_first[c + 1]; p++) {
-    const int64_t g = vals[p];
-    if (tile_root[node_tile[g]] == g) continue;  // tile roots exchange through global memory
-    const int64_t gs = step_of[g];
-    while (nbz && (busyh[0] >> 13) < gs) push_free((int16_t)(pop_busy() & 8191));
-    int32_t sl;
-    if (nf) sl = pop_free();
-    else {
-      sl = next++;
-      if (sl >= WV_MAX_SLOTS) { atomicExch(overflow, 1); return; }
-    }
-    slot_of[g] = sl;
-    const int64_t par = A.node_off[A.node_body[g]] + A.parent[g];
-    push_busy((step_of[par] << 13) | sl);
+    for (int e = lane; e < nch; e += 32)
+      if (crel[e] >= 0) slot_of[vals[p0 + e]] = cslot[e];
+    __syncwarp();
   }
-  atomicMax(max_slots, next);
+  if (lane == 0) atomicMax(max_slots, next);
 }
 
 struct WriteIn {
@@ -608,6 +648,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   // R0, ends at the same step T (same node rate nu for all streams).
   const int64_t R0 = R - (R + 3) / 4;
   auto assign_place = [&](const double *W) {
+    tm.mark("place (other)");
     k_wv_tile_key<<<nblk(nt), NT, 0, s>>>(node_scan.as<int64_t>(), nt, total_nodes, G, R, W, R0, tkey.as<uint64_t>(),
                                            tval.as<int32_t>());
     {
@@ -638,6 +679,7 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
                                                  tile_round.as<int32_t>(), (int)R0, round_floor.as<int64_t>(),
                                                  bad.as<int>());
     if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a node does not fit the step window");
+    tm.mark("place pass");
   };
   assign_place(nullptr);
   bool rebalance = G > 1 && R > 1;
@@ -806,6 +848,15 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   k_wv_write<<<nblk(n), NT, 0, s>>>(w, n);
   RQ_CUDA(cudaGetLastError());
   tm.mark("wave write");
+  if (getenv("RQ_LAYOUT_HASH")) {  // layout identity checks across builder versions (tools)
+    std::vector<uint8_t> hb((size_t)blob_bytes);
+    RQ_CUDA(cudaStreamSynchronize(s));
+    RQ_CUDA(cudaMemcpy(hb.data(), p.wave_blob.p, (size_t)blob_bytes, cudaMemcpyDeviceToHost));
+    uint64_t h = 1469598103934665603ull;
+    for (uint8_t x : hb) h = (h ^ x) * 1099511628211ull;
+    fprintf(stderr, "[rq] wave layout: %lld steps, %lld bytes, %d slots, fnv %016llx\n", (long long)NS,
+            (long long)blob_bytes, p.wave_mslots, (unsigned long long)h);
+  }
   p.wave_stream_first.alloc((G + 1) * 8);
   RQ_CUDA(cudaMemcpyAsync(p.wave_stream_first.p, step_first.p, (G + 1) * 8, cudaMemcpyDeviceToDevice, s));
   // per-direction bytes streamed per application (algorithmic bytes of the sweep)
