@@ -13,6 +13,8 @@ N, m = int(off[-1]), len(off) - 1
 op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
 v = torch.randn(3 * N, dtype=torch.float64, device="cuda")
 g = torch.randn(3 * N - 6 * m, dtype=torch.float64, device="cuda")
+_i = op.plan.info()
+print({k: _i[k] for k in ("n_streams", "n_steps", "node_slots", "stage_bytes", "sweep_smem", "sweep_ctas_per_sm", "sweep_bytes")})
 for name, x in (("qtilde_v", v), ("qtilde_tv", g), ("both", None)):
     def run():
         if x is None:
