@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, in
                                                       const int64_t *tile_root, NodeArrays A, WaveCaps caps,
                                                       int32_t *node_step, int64_t *n_steps, int32_t *tile_first,
                                                       int32_t *tile_last, const int32_t *tile_round, int R0,
-                                                      int64_t *round_floor, int *bad) {
+                                                      int64_t *round_floor, int *bad, int mode, TLev *save_ring,
+                                                      int32_t *save_state) {
   __shared__ TLev ring[WRING];
   __shared__ TLev cv[WV_CH];
   __shared__ int16_t clc[WV_CH], crc[WV_CH];  // tile-local children (-1: a bead; clc -2: node skipped)
@@ -178,10 +179,27 @@ __global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, in
   __syncwarp();
   int floor = 0, last = 0;  // uniform across the warp
   bool seen = false;
+  // mode 1 saves the stream's state (step loads, floor, last) where it enters the tail rounds
+  // (>= R0); mode 2 (the rebalancing pass: same tiles, same order and same steps before the
+  // tail) restores it and places the tail tiles only
+  auto save = [&]() {
+    for (int k = lane; k < WRING; k += 32) save_ring[c * WRING + k] = ring[k];
+    if (lane == 0) { save_state[2 * c] = floor; save_state[2 * c + 1] = last; }
+  };
+  if (mode == 2) {
+    for (int k = lane; k < WRING; k += 32) ring[k] = save_ring[c * WRING + k];
+    floor = save_state[2 * c];
+    last = save_state[2 * c + 1];
+    seen = true;
+    __syncwarp();
+  }
   for (int64_t i = sfirst[c]; i < sfirst[c + 1]; i++) {
     const int64_t t = order[i];
-    if (lane == 0 && !seen && tile_round[t] >= R0) {  // where this stream enters the rebalanced tail rounds
-      round_floor[c] = floor;
+    const bool tail = tile_round[t] >= R0;
+    if (mode == 2 && !tail) continue;
+    if (!seen && tail) {  // where this stream enters the rebalanced tail rounds
+      if (lane == 0) round_floor[c] = floor;
+      if (mode == 1) save();
       seen = true;
     }
     const int64_t g = tile_root[t];
@@ -259,6 +277,7 @@ __global__ void __launch_bounds__(32) k_wv_place_nodes(const int64_t *sfirst, in
     floor = max(floor, tmin);
     __syncwarp();
   }
+  if (!seen && mode == 1) save();
   if (lane == 0) {
     if (!seen) round_floor[c] = last;
     n_steps[c] = last + 4;  // two gather-only steps at each end
@@ -647,7 +666,10 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
   // rounds (rounds >= R0) so that every stream, starting from where pass 1 found it at round
   // R0, ends at the same step T (same node rate nu for all streams).
   const int64_t R0 = R - (R + 3) / 4;
-  auto assign_place = [&](const double *W) {
+  DBuf save_ring, save_state;
+  save_ring.alloc((size_t)G * WRING * sizeof(TLev));
+  save_state.alloc((size_t)G * 2 * 4);
+  auto assign_place = [&](const double *W, int mode) {
     tm.mark("place (other)");
     k_wv_tile_key<<<nblk(nt), NT, 0, s>>>(node_scan.as<int64_t>(), nt, total_nodes, G, R, W, R0, tkey.as<uint64_t>(),
                                            tval.as<int32_t>());
@@ -677,11 +699,11 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
                                                  node_step.as<int32_t>(), n_steps.as<int64_t>(),
                                                  tile_first.as<int32_t>(), tile_last.as<int32_t>(),
                                                  tile_round.as<int32_t>(), (int)R0, round_floor.as<int64_t>(),
-                                                 bad.as<int>());
+                                                 bad.as<int>(), mode, save_ring.as<TLev>(), save_state.as<int32_t>());
     if (d2h1<int>(bad.p, s)) throw Error(RQ_ERR_VALUE, "wave layout: a node does not fit the step window");
     tm.mark("place pass");
   };
-  assign_place(nullptr);
+  assign_place(nullptr, 1);
   bool rebalance = G > 1 && R > 1;
   if (const char *e = getenv("RQ_WAVE_REBALANCE")) rebalance = rebalance && atoi(e) != 0;
   if (rebalance) {
@@ -706,12 +728,12 @@ void build_wave(Plan &p, const WaveBuildIn &in, cudaStream_t s) {
     Wd.alloc((G + 1) * 8);
     RQ_CUDA(cudaMemcpyAsync(Wd.p, W.data(), (G + 1) * 8, cudaMemcpyHostToDevice, s));
     RQ_CUDA(cudaStreamSynchronize(s));
-    assign_place(Wd.as<double>());
+    assign_place(Wd.as<double>(), 2);
     d2h(ns.data(), n_steps.p, G, s);
     const int64_t max2 = *std::max_element(ns.begin(), ns.end());
     if (getenv("RQ_VERBOSE")) fprintf(stderr, "[rq] wave rebalance R0=%lld: max steps %lld -> %lld\n", (long long)R0,
                                       (long long)max1, (long long)max2);
-    if (max2 > max1) assign_place(nullptr);  // pass 1 was better
+    if (max2 > max1) assign_place(nullptr, 0);  // pass 1 was better
   }
   k_wv_gather64<<<nblk(nt), NT, 0, s>>>(tnodes.as<int64_t>(), order.as<int32_t>(), nt, tn_sorted.as<int64_t>());
   ex_scan(tn_sorted.as<int64_t>(), n_scan_s.as<int64_t>(), nt, s);
