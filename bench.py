@@ -547,6 +547,19 @@ def main():
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"first {nb} bodies ({int(off[nb])} beads) of the workload, {steps} steps "
                          f"of Q~v+Q~^T g in {el:.1f} s (C oracle, OpenMP over bodies)"}
+        # the reference as shipped is pure Python and cannot travel to the GPU box: its rate on
+        # config-2 bodies was measured in the build container (tools/ref_python_timing.py) and is
+        # quoted here as recorded, not re-measured
+        rp = os.path.join(ROOT, "profiles", "r02f_reference_python_timing.json")
+        if os.path.exists(rp):
+            with open(rp) as fh:
+                r = json.load(fh)
+            cpu["reference_python_recorded"] = {
+                "single_process_beads_per_s": r["reference_python_single_process"]["step_beads_per_s"],
+                "pool_beads_per_s": r["reference_python_pool"]["step_beads_per_s"],
+                "pool_workers": r["reference_python_pool"]["workers"],
+                "c_oracle_over_python_pool": r["oracle_over_python_pool"],
+                "where": r["where"] + "; " + r["config"] + " (recorded file, not this run)"}
 
     launches = args.steps * (lib.rq_launches_per_apply(h, L.OP_QTILDE_V, k) +
                              lib.rq_launches_per_apply(h, L.OP_QTILDE_TV, k))
