@@ -70,6 +70,8 @@ __attribute__((target("avx512f"))) void stream_copy_avx512(char *dst, const char
   if (i < n) memcpy(dst + i, src + i, n - i);
 }
 
+}  // namespace
+
 void stage_copy(void *dst, const void *src, size_t n) {
   static const bool nt = [] {
     const char *e = getenv("RQ_HOST_NT");
@@ -80,6 +82,8 @@ void stage_copy(void *dst, const void *src, size_t n) {
   else
     memcpy(dst, src, n);
 }
+
+namespace {
 
 void ensure_pinned(double *&buf, size_t &cap, size_t bytes) {
   if (cap >= bytes) return;

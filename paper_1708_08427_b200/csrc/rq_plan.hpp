@@ -343,4 +343,7 @@ void node_merge(int cs, const double *om, double a, double b, const double *mx, 
 void node_split(int cs, const double *om, double a, double b, const double *lp, const double *res, int64_t K,
                 double *lx, double *ly);
 
+// pageable -> pinned staging copy (non-temporal AVX-512 stores when available; rq_host.cu)
+void stage_copy(void *dst, const void *src, size_t n);
+
 }  // namespace rq

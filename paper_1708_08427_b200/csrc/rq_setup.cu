@@ -787,7 +787,7 @@ __global__ void k_case_count(const uint8_t *flags, int64_t NN, unsigned long lon
 }
 
 // Host -> device copy of a (possibly pageable) host array.  Pageable cudaMemcpyAsync runs
-// at ~8 GB/s on the B200 hosts; here RQ_H2D_THREADS host threads memcpy 4 MiB pieces into
+// at ~8 GB/s on the B200 hosts; here RQ_H2D_THREADS host threads (8) copy 4 MiB pieces into
 // their own pair of pinned slots and queue the DMA of each piece on the stream, so host
 // copies and PCIe transfers overlap.  Pinned (page-locked / registered) sources and small
 // arrays take the plain path.  The slots are allocated once per process.
@@ -796,7 +796,7 @@ void h2d_host(void *dst, const void *src, size_t bytes, cudaStream_t s) {
   cudaPointerAttributes at{};
   const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
   cudaGetLastError();  // clear a possible error from the attribute query on plain malloc'd memory
-  int T = 4;
+  int T = (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
   if (const char *e = getenv("RQ_H2D_THREADS")) T = std::max(0, std::min(16, atoi(e)));
   if (pinned || bytes < 4 * C || T == 0) {
     RQ_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
@@ -825,7 +825,7 @@ void h2d_host(void *dst, const void *src, size_t bytes, cudaStream_t s) {
         const int sl = 2 * t + use;
         const size_t off = i * C, len = std::min(C, bytes - off);
         if (cudaEventSynchronize(ev[sl]) != cudaSuccess) { fail[t] = 1; return; }
-        memcpy(slot[sl], (const char *)src + off, len);
+        stage_copy(slot[sl], (const char *)src + off, len);
         if (cudaMemcpyAsync((char *)dst + off, slot[sl], len, cudaMemcpyHostToDevice, s) != cudaSuccess ||
             cudaEventRecord(ev[sl], s) != cudaSuccess) { fail[t] = 1; return; }
       }
