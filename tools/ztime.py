@@ -1,4 +1,4 @@
-"""Time Zf / Z^T u (device-resident CUDA tensors) on config 2."""
+"""Time Zf / Z^T u (device-resident CUDA tensors); argv: [config=2] [scale=1]."""
 import sys
 import time
 
@@ -8,7 +8,8 @@ sys.path.insert(0, ".")
 import paper_1708_08427_b200 as rq  # noqa: E402
 from paper_1708_08427_b200.workloads import make_config  # noqa: E402
 
-pos, off = make_config(2, seed=1000)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+pos, off = make_config(cfg, seed=1000, scale=float(sys.argv[2]) if len(sys.argv) > 2 else 1.0)
 N, m = int(off[-1]), len(off) - 1
 op = rq.MultiBodyOperator(rq.MultiBodyModel.from_arrays(pos, off))
 f = torch.randn(3 * N, dtype=torch.float64, device="cuda")
