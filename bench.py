@@ -207,7 +207,9 @@ def main():
         local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # RQ_BENCH_FORCE_DIST=1: initialise the process group even at world size 1 (under torchrun),
+    # so the NCCL calls of the multi-rank path execute on a one-GPU box
+    if world > 1 or os.environ.get("RQ_BENCH_FORCE_DIST") == "1":
         import torch.distributed as dist
 
         if share:
@@ -216,7 +218,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    sharding = args.sharding or ("strong" if world > 1 else "weak")
+    sharding = args.sharding or ("strong" if dist else "weak")
     strong = sharding == "strong"
     emu = None
     if args.emulate_shard:  # one shard of an N-way strong split, alone on this GPU

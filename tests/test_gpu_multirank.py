@@ -97,3 +97,21 @@ def test_bench_two_ranks_functional(tmp_path):
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["gather"] is not None and d["gather"]["bytes"] > 0
     assert d["config"]["sharding"].startswith("strong")
+
+
+def test_bench_nccl_single_rank(tmp_path):
+    """The NCCL calls of the multi-rank bench path (process group bound to the device, all_reduce,
+    barrier, the max-padded all_gather of the shard outputs) on the one GPU the pool gives:
+    torchrun with one rank, process group forced (RQ_BENCH_FORCE_DIST=1)."""
+    env = dict(os.environ, RQ_BENCH_FORCE_DIST="1")
+    env.pop("RQ_BENCH_SHARE_GPU", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "1", "--steps", "5", "--warmup", "3", "--scale", "0.05", "--no-e2e", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 1 and d["value"] > 0
+    assert d["gather"] is not None and d["gather"]["bytes"] > 0 and d["gather"]["ms"] > 0
