@@ -15,6 +15,7 @@
 // kernels of rq_mrhs.cu.  No tensor cores: HBM-bound sweeps of tiny fp64 orthogonal
 // transforms (~0.3 flop/B).  DESIGN.md §2 has the full description.
 #include <algorithm>
+#include <type_traits>
 #include <climits>
 #include <cuda/atomic>
 #include <cstdio>
@@ -114,6 +115,19 @@ __device__ __forceinline__ void ldg_rec(int cs, const double *g, double (&R)[rec
       R[2 * i + 1] = 0.0;
     }
   }
+}
+
+// a 6-vector at a 16-byte aligned address (48-byte entries of aligned regions)
+__device__ __forceinline__ void ld6(const double *p, double (&v)[6]) {
+  const double2 *p2 = reinterpret_cast<const double2 *>(p);
+  const double2 a = p2[0], b = p2[1], c = p2[2];
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+}
+__device__ __forceinline__ void st6(double *p, const double (&v)[6]) {
+  double2 *p2 = reinterpret_cast<double2 *>(p);
+  p2[0] = make_double2(v[0], v[1]);
+  p2[1] = make_double2(v[2], v[3]);
+  p2[2] = make_double2(v[4], v[5]);
 }
 
 // a node record staged in shared memory (generic loads) into registers
@@ -350,29 +364,49 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    // one node; CSC = GENERAL: the case is a compile-time constant (nearly every top node: the
+    // record loads, the transform and the stores carry no case tests -- ~40% fewer instructions
+    // on the one-warp-per-tree critical path), CSC = -1: any case
+    auto up_node = [&](auto CSC, int q, const TopMeta &md) {
+      constexpr int C = decltype(CSC)::value;
+      const int cs = C >= 0 ? C : flag_case(md.flags);
+      double recv[rec_size(GENERAL)];
+      if (SREC) lds_rec_any(cs, REC + md.rec, recv);
+      else ldg_rec(cs, REC + md.rec, recv);
+      const double *rec = recv;
+      double mx[6], my[6], mp[6], res[6], aa, bb;
+      const double *px = md.x >= 0 ? MT + 6 * md.x : IN + 6 * ~(int)md.x;
+      const double *py = md.y >= 0 ? MT + 6 * md.y : IN + 6 * ~(int)md.y;
+      if (C >= 0) {  // 48-byte entries of a 128-byte aligned region: 16-byte loads
+        ld6(px, mx);
+        ld6(py, my);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 6; r++) { mx[r] = px[r]; my[r] = py[r]; }
+      }
+      rec_ratios(cs, rec, 1, aa, bb);
+      merge(cs, rec, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
+      const int rr = res_rows(cs);
+      double *o = a.out + (sbase + md.res_q) * K + col;
+#pragma unroll
+      for (int r = 0; r < 6; r++)
+        if (r < rr) o[r * K] = res[r];
+      if (md.is_root == 1 && a.roots)
+        for (int r = 0; r < 6; r++) a.roots[6 * (int64_t)h.body + r] = mp[r];
+      if (md.is_root == 2)  // piece root: its vector goes to the apex through its exchange slot
+        for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)h.root_slot + r] = mp[r];
+      if (C >= 0) {
+        st6(MT + 6 * q, mp);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 6; r++) MT[6 * q + r] = mp[r];
+      }
+    };
     for (int lv = 0; lv < h.n_levels; lv++) {
       for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NTT) {
         const TopMeta md = MD[q];
-        const int cs = flag_case(md.flags);
-        double recv[rec_size(GENERAL)];
-        if (SREC) lds_rec_any(cs, REC + md.rec, recv);
-        else ldg_rec(cs, REC + md.rec, recv);
-        const double *rec = recv;
-        double mx[6], my[6], mp[6], res[6], aa, bb;
-        const double *px = md.x >= 0 ? MT + 6 * md.x : IN + 6 * ~(int)md.x;
-        const double *py = md.y >= 0 ? MT + 6 * md.y : IN + 6 * ~(int)md.y;
-#pragma unroll
-        for (int r = 0; r < 6; r++) { mx[r] = px[r]; my[r] = py[r]; }
-        rec_ratios(cs, rec, 1, aa, bb);
-        merge(cs, rec, 1, flag_signs(md.flags), aa, bb, mx, my, mp, res);
-        const int rr = res_rows(cs);
-        for (int r = 0; r < rr; r++) a.out[(sbase + md.res_q + r) * K + col] = res[r];
-        if (md.is_root == 1 && a.roots)
-          for (int r = 0; r < 6; r++) a.roots[6 * (int64_t)h.body + r] = mp[r];
-        if (md.is_root == 2)  // piece root: its vector goes to the apex through its exchange slot
-          for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)h.root_slot + r] = mp[r];
-#pragma unroll
-        for (int r = 0; r < 6; r++) MT[6 * q + r] = mp[r];
+        if (flag_case(md.flags) == GENERAL) up_node(std::integral_constant<int, GENERAL>{}, q, md);
+        else up_node(std::integral_constant<int, -1>{}, q, md);
       }
       __syncthreads();
     }
@@ -391,37 +425,55 @@ __global__ void __launch_bounds__(NTT) k_top2(Top2Ctx a) {
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    for (int lv = h.n_levels - 1; lv >= 0; lv--) {
-      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NTT) {
-        const TopMeta md = MD[q];
-        const int cs = flag_case(md.flags);
-        double recv[rec_size(GENERAL)];
-        if (SREC) lds_rec_any(cs, REC + md.rec, recv);
-        else ldg_rec(cs, REC + md.rec, recv);
-        const double *rec = recv;
-        double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6], aa, bb;
+    auto dn_node = [&](auto CSC, int q, const TopMeta &md) {
+      constexpr int C = decltype(CSC)::value;
+      const int cs = C >= 0 ? C : flag_case(md.flags);
+      double recv[rec_size(GENERAL)];
+      if (SREC) lds_rec_any(cs, REC + md.rec, recv);
+      else ldg_rec(cs, REC + md.rec, recv);
+      const double *rec = recv;
+      double lp[6], res[6] = {0, 0, 0, 0, 0, 0}, lx[6], ly[6], aa, bb;
+      if (C >= 0) {
+        ld6(MT + 6 * q, lp);
+        ld6(RT + 6 * q, res);
+      } else {
 #pragma unroll
         for (int r = 0; r < 6; r++) lp[r] = MT[6 * q + r];
         const int rr = res_rows(cs);
         for (int r = 0; r < rr; r++) res[r] = RT[6 * q + r];
-        rec_ratios(cs, rec, 1, aa, bb);
-        split(cs, rec, 1, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
-        auto put = [&](int16_t ref, const double (&l)[6]) {
-          if (ref >= 0) {
+      }
+      rec_ratios(cs, rec, 1, aa, bb);
+      split(cs, rec, 1, flag_signs(md.flags), aa, bb, lp, res, lx, ly);
+      auto put = [&](int16_t ref, const double (&l)[6]) {
+        if (ref >= 0) {
+          if (C >= 0) {
+            st6(MT + 6 * ref, l);
+          } else {
 #pragma unroll
             for (int r = 0; r < 6; r++) MT[6 * ref + r] = l[r];
-          } else {
-            const int32_t in = INREF[~(int)ref];
-            if (in >= 0) {
-              for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)in + r] = l[r];
-            } else {
-              const int64_t row = (bead0 + ~(int64_t)in) * 3;
-              for (int r = 0; r < 3; r++) a.out[(row + r) * K + col] = l[r];
-            }
           }
-        };
-        put(md.x, lx);
-        put(md.y, ly);
+        } else {
+          const int32_t in = INREF[~(int)ref];
+          if (in >= 0) {
+            if (C >= 0) {
+              st6(a.scratch + 6 * (int64_t)in, l);
+            } else {
+              for (int r = 0; r < 6; r++) a.scratch[6 * (int64_t)in + r] = l[r];
+            }
+          } else {
+            const int64_t row = (bead0 + ~(int64_t)in) * 3;
+            for (int r = 0; r < 3; r++) a.out[(row + r) * K + col] = l[r];
+          }
+        }
+      };
+      put(md.x, lx);
+      put(md.y, ly);
+    };
+    for (int lv = h.n_levels - 1; lv >= 0; lv--) {
+      for (int q = LB[lv] + tid; q < LB[lv + 1]; q += NTT) {
+        const TopMeta md = MD[q];
+        if (flag_case(md.flags) == GENERAL) dn_node(std::integral_constant<int, GENERAL>{}, q, md);
+        else dn_node(std::integral_constant<int, -1>{}, q, md);
       }
       __syncthreads();
     }
